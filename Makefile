@@ -1,0 +1,32 @@
+# Builds the product library (sm_100a) and the CPU checkers.
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+PKG       := paper_1609_07228_b200
+SRCS      := $(wildcard $(PKG)/csrc/*.cu)
+OBJS      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
+LIB       := $(PKG)/libannkit_b200.so
+
+all: $(LIB) oracle
+
+build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/annkit_b200.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean
+
+# device-debug build for compute-sanitizer sessions (not used by tests/bench)
+debug: $(SRCS)
+	@mkdir -p build/dbg
+	for f in $(SRCS); do $(NVCC) -O2 -lineinfo -DANNK_DEBUG_CHECKS -std=c++17 $(ARCH) -Xcompiler -fPIC --expt-relaxed-constexpr -c $$f -o build/dbg/$$(basename $$f .cu).o || exit 1; done
+	$(NVCC) $(ARCH) -shared -cudart static -o build/libannkit_b200_dbg.so build/dbg/*.o

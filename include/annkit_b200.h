@@ -1,0 +1,187 @@
+/*
+ * annkit_b200.h — the drop-in C-ABI for EFANNA's data-parallel hot paths on
+ * NVIDIA B200 (sm_100a).
+ *
+ * The reference ("annkit", /root/reference/proj) exposes its hot path as a
+ * C++ library API (free functions over value types, proj/include/annkit/*.hpp);
+ * it has no plugin registry or FFI.  This header is the thin C layer that the
+ * reference-shaped host API (paper_1609_07228_b200/api.py, and any C++/ctypes
+ * caller) binds: plain pointers and sizes, no torch types, opaque handles for
+ * device-resident objects.  Each entry point names the reference interface it
+ * replaces.
+ *
+ * Conventions
+ *   - Every function returns an annk_status; annk_last_error() (thread-local)
+ *     carries the message.  ANNK_INVALID_ARGUMENT / ANNK_OUT_OF_RANGE map to
+ *     the reference's std::invalid_argument / std::out_of_range.
+ *   - Host buffers are borrowed for the duration of the call.  Calls are
+ *     synchronous: on return, outputs are in the caller's buffers.
+ *   - Results are bit-identical to the reference at workers = 1 (distances are
+ *     the reference's sequential fp32 l2_sq; ties ordered by id).
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with ANNK_CUDA_ERROR.
+ */
+#ifndef ANNKIT_B200_H
+#define ANNKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ANNK_OK = 0,
+    ANNK_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    ANNK_OUT_OF_RANGE = 2,     /* reference: std::out_of_range     */
+    ANNK_CUDA_ERROR = 3,
+    ANNK_OUT_OF_MEMORY = 4,
+    ANNK_INTERNAL = 5
+} annk_status;
+
+typedef struct annk_dataset annk_dataset;   /* VectorSet       dataset.hpp:28-37      */
+typedef struct annk_forest annk_forest;     /* KdForest        kd_forest.hpp:47-53    */
+typedef struct annk_state annk_state;       /* RefineState     graph_build.hpp:17-30  */
+typedef struct annk_searcher annk_searcher; /* GraphSearcher   search.hpp:43-76       */
+
+/* ---------------------------------------------------------------- runtime */
+const char* annk_last_error(void);
+const char* annk_version(void);
+/* Selects the CUDA device for subsequent calls from this process (default 0). */
+int annk_set_device(int device);
+/* The library's CUDA stream (cudaStream_t as an integer) — for event timing. */
+uint64_t annk_stream(void);
+/* Number of kernels this library has launched since load. */
+uint64_t annk_launch_count(void);
+int annk_synchronize(void);
+
+/* ---------------------------------------------------------------- dataset */
+/* Uploads an n x dim row-major fp32 matrix (VectorSet::data).  Values must be
+ * finite (load_fvecs dataset.cpp:123-126 rejects the rest). */
+int annk_dataset_create(const float* host, uint32_t n, uint32_t dim, annk_dataset** out);
+int annk_dataset_destroy(annk_dataset* ds);
+int annk_dataset_shape(const annk_dataset* ds, uint32_t* n, uint32_t* dim);
+
+/* dataset.cpp:201-214 gen_synthetic — host helper, same bytes as the reference. */
+int annk_gen_synthetic(uint32_t n, uint32_t dim, uint64_t seed, float* out);
+/* Seeded Gaussian-mixture generator for the BASELINE configs (no reference
+ * counterpart).  round_to_int != 0 rounds to
+ * integers (SIFT-like); values are clipped to [lo, hi].  stream 1 = base,
+ * 2 = queries; centers always come from stream 0. */
+int annk_gen_mixture(uint32_t n, uint32_t dim, uint32_t n_centers, float center_lo,
+                     float center_hi, float sd, float clip_lo, float clip_hi, int round_to_int,
+                     uint64_t seed, uint32_t stream_id, float* out);
+
+/* ------------------------------------------------------------ exact kNN */
+/* eval.cpp:33-61 brute_force_knn and eval.cpp:63-80 brute_force_graph.
+ * queries == NULL selects self mode (row i excludes i; k <= n-1), else query
+ * mode (k <= n).  out_ids: nq*k; out_dists nullable; dist_comps (nullable) is
+ * incremented like the reference's counter. */
+int annk_brute_force_knn(const annk_dataset* base, const annk_dataset* queries, uint32_t k,
+                         uint32_t* out_ids, float* out_dists, uint64_t* dist_comps);
+/* Same on a subset of rows (self mode): rows[0..n_rows) selects which base
+ * rows act as queries (used to score accuracy on a seeded sample). */
+int annk_brute_force_rows(const annk_dataset* base, const uint32_t* rows, uint32_t n_rows,
+                          uint32_t k, uint32_t* out_ids, float* out_dists);
+
+/* ---------------------------------------------------------------- forest */
+/* kd_forest.cpp:245-264 build_forest — bit-identical trees (same split_dim,
+ * split_val, point_index, node numbering) for the same seed. */
+int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_cap, uint64_t seed,
+                      annk_forest** out);
+int annk_forest_destroy(annk_forest* f);
+/* counts[0..3] = n_trees, n, dim, leaf_cap; *seed */
+int annk_forest_info(const annk_forest* f, uint32_t* counts, uint64_t* seed);
+/* per tree: [num_nodes, root, leaf_count, max_depth] */
+int annk_forest_tree_info(const annk_forest* f, uint32_t t, uint32_t* info);
+/* KdTree fields (kd_forest.hpp:18-42); node arrays sized num_nodes, point_index n. */
+int annk_forest_export(const annk_forest* f, uint32_t t, uint32_t* split_dim, float* split_val,
+                       uint32_t* left, uint32_t* right, uint32_t* depth, uint8_t* even_split,
+                       uint32_t* point_index);
+/* Inverse of export (e.g. a forest loaded from an AKF1 file, kd_forest.cpp:332-372). */
+int annk_forest_import(uint32_t n, uint32_t dim, uint32_t leaf_cap, uint64_t seed,
+                       uint32_t n_trees, const uint32_t* node_counts, const uint32_t* roots,
+                       const uint32_t* split_dim, const float* split_val, const uint32_t* left,
+                       const uint32_t* right, const uint32_t* depth, const uint8_t* even_split,
+                       const uint32_t* point_index, annk_forest** out);
+/* kd_forest.cpp:276-305 search_leaves for a batch of queries on tree t:
+ * out is nq * n_leaves (unused slots = 0xffffffff), out_counts nq. */
+int annk_search_leaves(const annk_forest* f, uint32_t t, const float* queries, uint32_t nq,
+                       uint32_t dim, uint32_t n_leaves, uint32_t* out, uint32_t* out_counts);
+/* kd_forest.cpp:266-274 descend_from, batched: start[i] -> out[i]. */
+int annk_descend_from(const annk_forest* f, uint32_t t, const float* queries, uint32_t nq,
+                      uint32_t dim, const uint32_t* start, uint32_t* out);
+
+/* ------------------------------------------------------- graph building */
+/* graph_build.cpp:230-292 init_graph. */
+int annk_init_graph(const annk_dataset* ds, const annk_forest* f, uint32_t k,
+                    uint32_t conquer_depth, uint32_t pool_cap, uint32_t sample_cap, uint64_t seed,
+                    annk_state** out);
+/* A RefineState from host pools (n rows of pool_cap slots, sizes[i] used). */
+int annk_state_import(uint32_t n, uint32_t k, uint32_t pool_cap, uint32_t sample_cap,
+                      uint64_t seed, uint32_t iteration, uint64_t dist_comps,
+                      const uint32_t* sizes, const uint32_t* ids, const float* dists,
+                      const uint8_t* flags, annk_state** out);
+int annk_state_destroy(annk_state* s);
+/* meta = [n, k, pool_cap, sample_cap, seed, iteration, dist_comps, last_changes] */
+int annk_state_meta(const annk_state* s, uint64_t* meta);
+/* Pools to host (ids/dists/flags are n*pool_cap; slots >= sizes[i] unspecified). */
+int annk_state_export(const annk_state* s, uint32_t* sizes, uint32_t* ids, float* dists,
+                      uint8_t* flags);
+/* Adjacency lists of the last sampling step (which: 0 g_new, 1 g_old, 2 g_rnew,
+ * 3 g_rold), CSR: offsets n+1 (always), data nullable. */
+int annk_state_lists(const annk_state* s, int which, uint32_t* offsets, uint32_t* data);
+/* graph_build.cpp:105-162 detail::nn_descent_iteration.  *changes receives
+ * this library's deterministic count (entries inserted this round that
+ * survive in the pools) — see DESIGN.md on why the reference's count is
+ * order-dependent. */
+int annk_nn_descent_iteration(annk_state* s, const annk_dataset* ds, uint64_t* changes);
+/* graph_build.cpp:59-86 and :88-103 (the two halves of the sampling step). */
+int annk_rebuild_sample_lists(annk_state* s);
+int annk_union_reverse_lists(annk_state* s);
+/* graph_build.cpp:328-335 refine_nn_descent; *iters_run may be NULL. */
+int annk_refine_nn_descent(annk_state* s, const annk_dataset* ds, uint32_t max_iters,
+                           double min_change_rate, uint32_t* iters_run);
+/* graph_build.cpp:346-373 finalize: ids/dists are n*k. */
+int annk_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* ids, float* dists);
+/* graph_build.cpp:209-226 detail::pool_topk_accuracy.  rows == NULL scores all
+ * n rows against gt (n x gt_k); otherwise gt row r belongs to point rows[r]. */
+int annk_pool_topk_accuracy(const annk_state* s, const uint32_t* gt_ids, uint32_t gt_rows,
+                            uint32_t gt_k, const uint32_t* rows, double* acc);
+/* Sum over points of |g_new|+|g_old| for the last sampling step (the join's
+ * row-gather count; used for the roofline). */
+int annk_state_join_rows(const annk_state* s, uint64_t* rows);
+
+/* --------------------------------------------------------------- search */
+/* search.cpp:23-35 GraphSearcher(base, forest, graph): validates the graph
+ * and uploads it (n x graph_k ids). forest may be NULL (random init only). */
+int annk_searcher_create(const annk_dataset* base, const annk_forest* f, const uint32_t* graph_ids,
+                         uint32_t graph_n, uint32_t graph_k, annk_searcher** out);
+int annk_searcher_destroy(annk_searcher* s);
+typedef struct {
+    uint32_t k_return;          /* SearchParams (search.hpp:13-21) */
+    uint32_t pool_size;
+    uint32_t expansion;
+    uint32_t iters;
+    uint32_t n_trees_used;
+    uint32_t random_seed_count;
+    uint64_t seed;
+    int32_t random_init;        /* 1 = search_random_init (search.cpp:156-180) */
+} annk_search_params;
+/* search.cpp:121-154 GraphSearcher::search for a batch of queries (host
+ * nq x dim).  Per-query seed = substream(params.seed, qi) as in recall_curve
+ * (search.cpp:208).  out_ids/out_dists nq*k_return; stats (nullable) nq*4 =
+ * [dist_comps, leaves_visited, graph_hops, seed_points] (SearchStats). */
+int annk_search(annk_searcher* s, const float* queries, uint32_t nq, uint32_t dim,
+                const annk_search_params* params, uint32_t* out_ids, float* out_dists,
+                uint64_t* stats);
+/* Same with the queries already on the device (a dataset handle). */
+int annk_search_dataset(annk_searcher* s, const annk_dataset* queries,
+                        const annk_search_params* params, uint32_t* out_ids, float* out_dists,
+                        uint64_t* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,25 @@
+"""EFANNA hot paths (kNN-graph construction, batched search, exact kNN) on
+NVIDIA B200 (sm_100a), behind the reference library's host API.
+
+The compute path is libannkit_b200.so (hand-written CUDA, C-ABI in
+include/annkit_b200.h); this package is the reference-shaped host mirror.
+"""
+from ._lib import AnnkError, InvalidArgument, OutOfRange, lib  # noqa: F401
+from .api import (  # noqa: F401
+    BatchResult, BuildParams, BuildResult, BuildStats, GraphSearcher, IterationLog, KdForest, KdTree, KnnGraph,
+    RefineState, SearchParams, SearchResult, SearchStats, SweepPoint, SweepRow, VectorSet, brute_force_graph,
+    brute_force_knn, brute_force_rows, build_forest, build_graph, descend_from, detail, finalize, gen_mixture,
+    gen_synthetic, graph_accuracy, init_graph, recall, recall_curve, refine_nn_descent, search_leaves,
+)
+
+__version__ = "0.1.0"
+
+
+def launch_count() -> int:
+    """Kernels launched by libannkit_b200.so since load."""
+    return int(lib.annk_launch_count())
+
+
+def stream_handle() -> int:
+    """The library's cudaStream_t (for CUDA-event timing on the launching stream)."""
+    return int(lib.annk_stream())

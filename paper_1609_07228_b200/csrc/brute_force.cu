@@ -1,0 +1,303 @@
+// brute_force.cu — exact kNN (reference: proj/src/eval.cpp:17-80).
+//
+// v1 path: register-tiled CUDA-core distance tiles with a fused per-query
+// top-k filter.  Each CTA owns QT queries x one slice of the base set; each
+// thread accumulates a 2 x 4 block of pair distances over shared-memory
+// staged dimension chunks, in index order with separate mul/add (bit-exact
+// with the reference's l2_sq).  Candidates below the query's running k-th key
+// are appended to a per-query shared buffer, which is compacted (bitonic sort,
+// keep k) whenever it cannot absorb another tile.  Slices are merged by a
+// second kernel.  Keys order by (dist, id), so ties break by id exactly like
+// NeighborPool (neighbor_pool.hpp:17-20).
+#include <algorithm>
+
+#include "../../include/annkit_b200.h"
+#include "internal.cuh"
+
+namespace annk {
+namespace {
+
+constexpr int QT = 32;   // queries per CTA
+constexpr int BT = 64;   // base rows per tile
+constexpr int DC = 64;   // dims per smem chunk
+constexpr int kThreads = 256;
+constexpr uint32_t kBigK = 512;
+
+__global__ void __launch_bounds__(kThreads)
+bf_tile_kernel(const float* __restrict__ base, uint32_t nb, uint32_t ld, const float* __restrict__ q,
+               uint32_t nq, const uint32_t* __restrict__ self_ids, uint32_t k, uint32_t cb,
+               uint32_t splits, uint32_t tiles_per_split, uint64_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* buf = reinterpret_cast<uint64_t*>(smem);                   // QT x cb
+    uint64_t* thr = buf + size_t(QT) * cb;                               // QT
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(thr + QT);              // QT
+    uint32_t* selfq = cnt + QT;                                          // QT
+    float* sq = reinterpret_cast<float*>(selfq + QT);                    // QT x (DC+1)
+    float* sb = sq + QT * (DC + 1);                                      // BT x (DC+1)
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t q0 = blockIdx.x * QT;
+    const uint32_t split = blockIdx.y;
+    const uint32_t n_tiles = (nb + BT - 1) / BT;
+    const uint32_t t_begin = split * tiles_per_split;
+    const uint32_t t_end = min(n_tiles, t_begin + tiles_per_split);
+    if (tid < QT) {
+        cnt[tid] = 0;
+        thr[tid] = kEmptyKey;
+        const uint32_t qi = q0 + tid;
+        selfq[tid] = (self_ids && qi < nq) ? self_ids[qi] : kInvalidId;
+    }
+    const uint32_t tq = tid >> 4, tb = tid & 15;  // queries tq, tq+16; rows tb+16m
+    __syncthreads();
+
+    for (uint32_t t = t_begin; t < t_end; ++t) {
+        const uint32_t b0 = t * BT;
+        float acc[2][4];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+        for (uint32_t c0 = 0; c0 < ld; c0 += DC) {
+            const uint32_t cw = min(uint32_t(DC), ld - c0);
+            // stage (float4, coalesced): cw is a multiple of 4
+            const uint32_t v4 = cw / 4;
+            for (uint32_t j = tid; j < QT * v4; j += kThreads) {
+                const uint32_t r = j / v4, c = (j % v4) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (q0 + r < nq) v = __ldg(reinterpret_cast<const float4*>(q + size_t(q0 + r) * ld + c0 + c));
+                float* d = sq + r * (DC + 1) + c;
+                d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+            }
+            for (uint32_t j = tid; j < BT * v4; j += kThreads) {
+                const uint32_t r = j / v4, c = (j % v4) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (b0 + r < nb) v = __ldg(reinterpret_cast<const float4*>(base + size_t(b0 + r) * ld + c0 + c));
+                float* d = sb + r * (DC + 1) + c;
+                d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+            }
+            __syncthreads();
+            const float* qa = sq + tq * (DC + 1);
+            const float* qb = sq + (tq + 16) * (DC + 1);
+            const float* ba = sb + tb * (DC + 1);
+#pragma unroll 4
+            for (uint32_t i = 0; i < cw; ++i) {
+                const float x0 = qa[i], x1 = qb[i];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const float y = ba[b * 16 * (DC + 1) + i];
+                    const float d0 = __fsub_rn(x0, y), d1 = __fsub_rn(x1, y);
+                    acc[0][b] = __fadd_rn(acc[0][b], __fmul_rn(d0, d0));
+                    acc[1][b] = __fadd_rn(acc[1][b], __fmul_rn(d1, d1));
+                }
+            }
+            __syncthreads();
+        }
+        // fused top-k filter
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            const uint32_t ql = tq + 16 * a;
+            if (q0 + ql >= nq) continue;
+            const uint64_t th = thr[ql];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t bj = b0 + tb + 16 * b;
+                if (bj >= nb || bj == selfq[ql]) continue;
+                const uint64_t key = make_key(acc[a][b], bj);
+                if (key < th) {
+                    const uint32_t slot = atomicAdd(&cnt[ql], 1u);
+                    buf[size_t(ql) * cb + slot] = key;
+                }
+            }
+        }
+        __syncthreads();
+        // compact buffers that could not absorb another tile
+        for (uint32_t ql = warp; ql < QT; ql += kThreads / 32) {
+            const uint32_t c = cnt[ql];
+            if (c + BT <= cb) continue;
+            uint64_t* bq = buf + size_t(ql) * cb;
+            for (uint32_t j = c + lane; j < cb; j += 32) bq[j] = kEmptyKey;
+            __syncwarp();
+            warp_bitonic_sort(bq, cb);
+            if (lane == 0) {
+                const uint32_t keep = min(c, k);
+                cnt[ql] = keep;
+                if (keep == k) thr[ql] = bq[k - 1];
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    // final: sorted first k of each buffer
+    for (uint32_t ql = warp; ql < QT; ql += kThreads / 32) {
+        const uint32_t qi = q0 + ql;
+        if (qi >= nq) continue;
+        const uint32_t c = cnt[ql];
+        uint64_t* bq = buf + size_t(ql) * cb;
+        for (uint32_t j = c + lane; j < cb; j += 32) bq[j] = kEmptyKey;
+        __syncwarp();
+        warp_bitonic_sort(bq, cb);
+        uint64_t* o = out + (size_t(qi) * splits + split) * k;
+        for (uint32_t j = lane; j < k; j += 32) o[j] = bq[j];
+        __syncwarp();
+    }
+}
+
+// Merge `splits` sorted k-lists per query into the final k.
+__global__ void bf_merge_kernel(const uint64_t* __restrict__ part, uint32_t nq, uint32_t splits,
+                                uint32_t k, uint32_t m, uint64_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t qi = blockIdx.x * (blockDim.x / 32) + warp;
+    uint64_t* s = reinterpret_cast<uint64_t*>(smem) + size_t(warp) * m;
+    if (qi >= nq) return;
+    for (uint32_t j = lane; j < m; j += 32) s[j] = j < splits * k ? part[size_t(qi) * splits * k + j] : kEmptyKey;
+    __syncwarp();
+    warp_bitonic_sort(s, m);
+    for (uint32_t j = lane; j < k; j += 32) out[size_t(qi) * k + j] = s[j];
+}
+
+// Large-k path (k > kBigK, small inputs only): all keys, then a block sort per query.
+__global__ void bf_allkeys_kernel(const float* __restrict__ base, uint32_t nb, uint32_t ld,
+                                  const float* __restrict__ q, uint32_t dim_pad,
+                                  const uint32_t* __restrict__ self_ids, uint32_t m,
+                                  uint64_t* __restrict__ keys) {
+    const uint32_t qi = blockIdx.x;
+    const float* qq = q + size_t(qi) * ld;
+    const uint32_t self = self_ids ? self_ids[qi] : kInvalidId;
+    uint64_t* kq = keys + size_t(qi) * m;
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+        uint64_t key = kEmptyKey;
+        if (j < nb && j != self) key = make_key(l2_exact_ldg(qq, base + size_t(j) * ld, dim_pad), j);
+        kq[j] = key;
+    }
+}
+__global__ void bf_block_sort_kernel(uint64_t* keys, uint32_t m, uint32_t k, uint64_t* out) {
+    uint64_t* kq = keys + size_t(blockIdx.x) * m;
+    block_bitonic_sort(kq, m);
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) out[size_t(blockIdx.x) * k + j] = kq[j];
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ src, uint32_t ld, const uint32_t* __restrict__ rows,
+                                   uint32_t nr, float* __restrict__ dst) {
+    const uint32_t r = blockIdx.x;
+    if (r >= nr) return;
+    const float* s = src + size_t(rows[r]) * ld;
+    float* d = dst + size_t(r) * ld;
+    for (uint32_t j = threadIdx.x; j < ld; j += blockDim.x) d[j] = s[j];
+}
+
+__global__ void keys_to_ids_kernel(const uint64_t* __restrict__ keys, size_t n, uint32_t* __restrict__ ids,
+                                   float* __restrict__ dists) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const uint64_t k = keys[i];
+        ids[i] = key_id(k);
+        if (dists) dists[i] = key_dist(k);
+    }
+}
+
+}  // namespace
+
+void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
+                        const uint32_t* self_ids, uint32_t k, uint64_t* out_keys) {
+    if (nq == 0) return;
+    const uint32_t nb = base->n, ld = base->ld;
+    if (q_ld != ld) throw_invalid("brute_force: query stride mismatch");
+    if (k > kBigK) {
+        const uint32_t m = next_pow2(nb);
+        if (double(nq) * m * 8 > 8e9) throw_invalid("brute_force: k too large for this input size");
+        DevBuf<uint64_t> keys(size_t(nq) * m);
+        LAUNCH(bf_allkeys_kernel, nq, 256, 0, base->data.p, nb, ld, qdata, ld, self_ids, m, keys.p);
+        LAUNCH(bf_block_sort_kernel, nq, 1024, 0, keys.p, m, k, out_keys);
+        ssync();
+        return;
+    }
+    const uint32_t cb = next_pow2(k + BT);
+    const size_t smem = size_t(QT) * cb * 8 + QT * 8 + QT * 4 * 2 + size_t(QT + BT) * (DC + 1) * 4;
+    CK(cudaFuncSetAttribute(bf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_tile_kernel, kThreads, smem));
+    const uint32_t qtiles = (nq + QT - 1) / QT;
+    const uint32_t n_tiles = (nb + BT - 1) / BT;
+    const uint32_t want = uint32_t(num_sms()) * std::max(per_sm, 1) * 2;
+    uint32_t splits = std::max(1u, std::min(n_tiles, (want + qtiles - 1) / qtiles));
+    splits = std::min(splits, std::max(1u, 4096u / k));  // merge list fits 32 KB per warp
+    const uint32_t tps = (n_tiles + splits - 1) / splits;
+    splits = (n_tiles + tps - 1) / tps;
+    if (splits == 1) {
+        LAUNCH(bf_tile_kernel, dim3(qtiles, 1), kThreads, smem, base->data.p, nb, ld, qdata, nq, self_ids, k,
+               cb, 1u, tps, out_keys);
+    } else {
+        DevBuf<uint64_t> part(size_t(nq) * splits * k);
+        LAUNCH(bf_tile_kernel, dim3(qtiles, splits), kThreads, smem, base->data.p, nb, ld, qdata, nq, self_ids,
+               k, cb, splits, tps, part.p);
+        const uint32_t m = next_pow2(splits * k);
+        const uint32_t wpb = std::max(1u, std::min(8u, uint32_t(64 * 1024 / (m * 8))));
+        CK(cudaFuncSetAttribute(bf_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wpb * m * 8)));
+        LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part.p, nq, splits, k, m, out_keys);
+    }
+}
+
+}  // namespace annk
+
+using namespace annk;
+
+namespace {
+void finish_keys(const DevBuf<uint64_t>& keys, size_t count, uint32_t* ids, float* dists) {
+    DevBuf<uint32_t> di(count);
+    DevBuf<float> dd(dists ? count : 0);
+    const uint32_t grid = uint32_t(std::min<size_t>((count + 255) / 256, 65535));
+    LAUNCH(keys_to_ids_kernel, std::max(grid, 1u), 256, 0, keys.p, count, di.p, dists ? dd.p : nullptr);
+    di.download(ids, count);
+    if (dists) dd.download(dists, count);
+    ssync();
+}
+}  // namespace
+
+extern "C" {
+
+int annk_brute_force_knn(const annk_dataset* base, const annk_dataset* queries, uint32_t k,
+                         uint32_t* out_ids, float* out_dists, uint64_t* dist_comps) {
+    return abi([&] {
+        if (!base) throw_invalid("brute_force_knn: null base");
+        const bool self = queries == nullptr;
+        if (base->n == 0) throw_invalid("brute_force_knn: empty base set");
+        if (!self && queries->dim != base->dim) throw_invalid("brute_force_knn: query dim mismatch");
+        const uint32_t limit = self ? base->n - 1 : base->n;
+        if (k < 1 || k > limit)
+            throw_invalid("brute_force_knn: k=" + std::to_string(k) + " out of range (max " +
+                          std::to_string(limit) + ")");
+        const uint32_t nq = self ? base->n : queries->n;
+        DevBuf<uint64_t> keys(size_t(nq) * k);
+        DevBuf<uint32_t> selfids;
+        if (self) {
+            std::vector<uint32_t> iota(nq);
+            for (uint32_t i = 0; i < nq; ++i) iota[i] = i;
+            selfids.alloc(nq);
+            selfids.upload(iota.data(), nq);
+        }
+        brute_force_device(base, self ? base->data.p : queries->data.p, base->ld, nq,
+                           self ? selfids.p : nullptr, k, keys.p);
+        finish_keys(keys, size_t(nq) * k, out_ids, out_dists);
+        if (dist_comps) *dist_comps += uint64_t(nq) * (self ? base->n - 1 : base->n);
+    });
+}
+
+int annk_brute_force_rows(const annk_dataset* base, const uint32_t* rows, uint32_t n_rows, uint32_t k,
+                          uint32_t* out_ids, float* out_dists) {
+    return abi([&] {
+        if (!base || (!rows && n_rows)) throw_invalid("brute_force_rows: null argument");
+        if (k < 1 || k > base->n - 1) throw_invalid("brute_force_rows: k out of range");
+        for (uint32_t i = 0; i < n_rows; ++i)
+            if (rows[i] >= base->n) throw_range("brute_force_rows: row id out of range");
+        if (n_rows == 0) return;
+        DevBuf<uint32_t> drows(n_rows);
+        drows.upload(rows, n_rows);
+        DevBuf<float> q(size_t(n_rows) * base->ld);
+        LAUNCH(gather_rows_kernel, n_rows, 128, 0, base->data.p, base->ld, drows.p, n_rows, q.p);
+        DevBuf<uint64_t> keys(size_t(n_rows) * k);
+        brute_force_device(base, q.p, base->ld, n_rows, drows.p, k, keys.p);
+        finish_keys(keys, size_t(n_rows) * k, out_ids, out_dists);
+    });
+}
+
+}  // extern "C"

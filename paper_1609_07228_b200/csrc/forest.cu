@@ -1,0 +1,803 @@
+// forest.cu — randomized truncated KD-forest on B200, bit-identical to the
+// reference TreeBuilder (proj/src/kd_forest.cpp:29-97, build_forest :245-264).
+//
+// Why DFS and not level-synchronous: the reference draws split dimensions
+// from a per-tree std::mt19937_64(substream(seed, t)) in DFS PRE-ORDER of the
+// internal nodes (kd_forest.cpp:53, recursion :87-88).  A right child's draw
+// index depends on the internal-node count of its left sibling's subtree, so
+// no level-synchronous schedule can reproduce the reference's trees.  Each
+// tree is therefore built by one CTA walking the tree in pre-order with an
+// explicit stack:
+//   * nodes larger than kWarpSubtree points: the whole CTA (512 threads)
+//     computes the mean (exact double sum, see below) and the stable
+//     partition with block-wide ballot scans;
+//   * subtrees of <= kWarpSubtree points: warp 0 finishes the entire subtree
+//     with warp-synchronous ops (no block barriers), after prefetching the
+//     subtree's rows into L2 so the per-node gathers hit L2, not HBM.
+//   * the MT19937-64 state lives in shared memory; warp 0 regenerates 312
+//     words at a time with a 3-phase parallel twist.
+// Trees run concurrently (one CTA per tree).
+//
+// Exact mean: the reference sums x[p][d] sequentially in double.  A parallel
+// double sum equals it bit-for-bit whenever every partial sum is exactly
+// representable, which holds when (top bit of the largest |x|) +
+// ceil(log2(size)) - (lowest set bit over all x) <= 53.  That is checked per
+// node (always true for integer-valued data and for gen_synthetic data); when
+// it fails the node's sum is done serially in point_index order.
+#include <climits>
+
+#include "../../include/annkit_b200.h"
+#include "internal.cuh"
+
+namespace annk {
+namespace {
+
+constexpr uint32_t kBlock = 512;
+constexpr uint32_t kWarps = kBlock / 32;
+constexpr uint32_t kWarpSubtree = 4096;
+constexpr uint32_t kSortSmem = 4096;
+constexpr uint32_t kStack = 160;
+constexpr size_t kPrefetchBytes = 4u << 20;
+
+struct StackEntry {
+    uint32_t start, end, depth, parent, side;  // side 0 = left child, 1 = right
+};
+
+struct BuildArgs {
+    const float* x;
+    uint32_t n, dim, ld, leaf_cap;
+    uint64_t seed;
+    KdNodeDev* nodes;
+    uint32_t* depth;
+    uint8_t* even;
+    uint32_t* pidx;
+    uint32_t* rtmp;
+    uint64_t* sortbuf;  // next_pow2(n) keys, for fallback sorts larger than kSortSmem
+    uint32_t* meta;     // [num_nodes, root, leaf_count, max_depth, error]
+};
+
+struct Smem {
+    uint64_t mt[312];
+    uint64_t sortk[kSortSmem];
+    StackEntry bstack[kStack];
+    StackEntry wstack[kStack];
+    double red_sum[kWarps];
+    int red_top[kWarps], red_lsb[kWarps];
+    uint32_t cnt_l[kWarps], cnt_r[kWarps];
+    uint32_t mt_idx, node_count, leaf_count, max_depth, error;
+    uint32_t bsp;
+    // broadcast slots for the block path
+    uint32_t b_d, b_nl, b_nr, b_mid, b_even;
+    float b_split;
+    double b_sum;
+    int b_exact;
+};
+
+__device__ __forceinline__ float ldx(const BuildArgs& a, uint32_t p, uint32_t d) {
+    return __ldg(a.x + size_t(p) * a.ld + d);
+}
+
+// Magnitude/granularity of one value for the exact-sum test.
+__device__ __forceinline__ void val_stats(float v, int& top, int& lsb) {
+    const uint32_t b = __float_as_uint(v) & 0x7fffffffu;
+    if (b == 0) return;
+    const uint32_t ex = b >> 23, m = b & 0x7fffffu;
+    uint32_t mm;
+    int e0;
+    if (ex == 0) {
+        mm = m;
+        e0 = -149;
+    } else {
+        mm = m | 0x800000u;
+        e0 = int(ex) - 150;
+    }
+    lsb = min(lsb, e0 + __ffs(mm) - 1);
+    top = max(top, e0 + 32 - __clz(mm));
+}
+__device__ __forceinline__ bool sum_is_exact(int top, int lsb, uint32_t size) {
+    if (top == INT_MIN) return true;  // all zeros
+    const int clog = size <= 1 ? 0 : 32 - __clz(size - 1);
+    return top + clog - lsb <= 53;
+}
+
+// Orderable (value, id) key; -0 and +0 compare equal like the reference.
+__device__ __forceinline__ uint64_t val_id_key(float v, uint32_t id) {
+    uint32_t b = __float_as_uint(v);
+    if ((b & 0x7fffffffu) == 0) b = 0;
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return (uint64_t(b) << 32) | id;
+}
+
+// libstdc++ std::midpoint<float> for finite inputs.
+__device__ __forceinline__ float midpoint_f(float a, float b) {
+    const float aa = fabsf(a), ab = fabsf(b), hi = 3.40282347e38f / 2;
+    if (aa <= hi && ab <= hi) return __fdiv_rn(__fadd_rn(a, b), 2.0f);
+    if (aa < 1.17549435e-38f * 2) return __fadd_rn(a, __fdiv_rn(b, 2.0f));
+    if (ab < 1.17549435e-38f * 2) return __fadd_rn(__fdiv_rn(a, 2.0f), b);
+    return __fadd_rn(__fdiv_rn(a, 2.0f), __fdiv_rn(b, 2.0f));
+}
+
+// In-place std::mt19937_64 regeneration of 312 words by one warp.
+__device__ void warp_twist(uint64_t* mt) {
+    const uint32_t lane = lane_id();
+    for (uint32_t b = 0; b < 156; b += 32) {  // phase 1: i in [0,156)
+        const uint32_t i = b + lane;
+        uint64_t v = 0;
+        if (i < 156) v = mt_twist(mt[i], mt[i + 1], mt[i + 156]);
+        __syncwarp();
+        if (i < 156) mt[i] = v;
+        __syncwarp();
+    }
+    for (uint32_t b = 156; b < 311; b += 32) {  // phase 2: i in [156,311)
+        const uint32_t i = b + lane;
+        uint64_t v = 0;
+        if (i < 311) v = mt_twist(mt[i], mt[i + 1], mt[i - 156]);
+        __syncwarp();
+        if (i < 311) mt[i] = v;
+        __syncwarp();
+    }
+    if (lane == 0) mt[311] = mt_twist(mt[311], mt[0], mt[155]);
+    __syncwarp();
+}
+
+// Next split dimension (kd_forest.cpp:53: rng_() % dim). Warp-collective.
+__device__ uint32_t warp_draw(Smem& s, uint32_t dim) {
+    __syncwarp();
+    if (s.mt_idx >= 312) {
+        warp_twist(s.mt);
+        if (lane_id() == 0) s.mt_idx = 0;
+        __syncwarp();
+    }
+    const uint64_t v = mt_temper(s.mt[s.mt_idx]);
+    __syncwarp();
+    if (lane_id() == 0) s.mt_idx++;
+    __syncwarp();
+    return uint32_t(v % uint64_t(dim));
+}
+
+// -------------------------------------------------------------- warp path
+
+__device__ void warp_sort_node(const BuildArgs& a, Smem& s, uint32_t start, uint32_t size,
+                               uint32_t d) {
+    const uint32_t lane = lane_id();
+    const uint32_t m = next_pow2(size);
+    uint64_t* k = m <= kSortSmem ? s.sortk : a.sortbuf;
+    for (uint32_t j = lane; j < m; j += 32) {
+        uint64_t key = kEmptyKey;
+        if (j < size) {
+            const uint32_t id = a.pidx[start + j];
+            key = val_id_key(ldx(a, id, d), id);
+        }
+        k[j] = key;
+    }
+    __syncwarp();
+    warp_bitonic_sort(k, m);
+    for (uint32_t j = lane; j < size; j += 32) a.pidx[start + j] = uint32_t(k[j]);
+    __syncwarp();
+}
+
+// Builds the subtree rooted at `root` (its pre-order id is assigned here) with
+// warp 0 only.
+__device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root) {
+    const uint32_t lane = lane_id();
+    uint32_t wsp = 0;
+    if (lane == 0) s.wstack[0] = root;
+    wsp = 1;
+    bool prefetched = false;
+    __syncwarp();
+    while (wsp > 0) {
+        --wsp;
+        const StackEntry e = s.wstack[wsp];
+        __syncwarp();
+        const uint32_t size = e.end - e.start;
+        const uint32_t id = s.node_count;
+        __syncwarp();
+        if (lane == 0) {
+            s.node_count = id + 1;
+            if (e.parent != kInvalidId) {
+                if (e.side == 0) a.nodes[e.parent].left = id;
+                else a.nodes[e.parent].right = id;
+            }
+            a.depth[id] = e.depth;
+            s.max_depth = max(s.max_depth, e.depth);
+        }
+        if (size <= a.leaf_cap) {
+            if (lane == 0) {
+                a.nodes[id] = KdNodeDev{kLeaf, 0.0f, e.start, e.end};
+                a.even[id] = 0;
+                s.leaf_count++;
+            }
+            __syncwarp();
+            continue;
+        }
+        if (!prefetched && size_t(size) * a.ld * 4 <= kPrefetchBytes) {
+            // Stage this subtree's rows in L2: every deeper node gathers from them.
+            prefetched = true;
+            const uint32_t lines = (a.ld * 4 + 127) / 128;
+            for (uint32_t j = lane; j < size * lines; j += 32) {
+                const uint32_t p = a.pidx[e.start + j / lines];
+                const char* ptr = reinterpret_cast<const char*>(a.x + size_t(p) * a.ld) + (j % lines) * 128;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+            }
+        }
+        const uint32_t d = warp_draw(s, a.dim);
+        // mean (kd_forest.cpp:55-59)
+        double sum = 0.0;
+        int top = INT_MIN, lsb = INT_MAX;
+        for (uint32_t p = e.start + lane; p < e.end; p += 32) {
+            const float v = ldx(a, a.pidx[p], d);
+            sum += double(v);
+            val_stats(v, top, lsb);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            top = max(top, __shfl_xor_sync(0xffffffffu, top, o));
+            lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+        }
+        if (!sum_is_exact(top, lsb, size)) {
+            if (lane == 0) {
+                sum = 0.0;
+                for (uint32_t p = e.start; p < e.end; ++p) sum += double(ldx(a, a.pidx[p], d));
+            }
+            sum = __shfl_sync(0xffffffffu, sum, 0);
+        }
+        float split = __double2float_rn(__ddiv_rn(sum, double(size)));
+        // stable partition by value <= split (kd_forest.cpp:61-65)
+        uint32_t nl = 0, nr = 0;
+        for (uint32_t base = e.start; base < e.end; base += 32) {
+            const uint32_t p = base + lane;
+            const bool valid = p < e.end;
+            const uint32_t pid = valid ? a.pidx[p] : 0;
+            const bool left = valid && ldx(a, pid, d) <= split;
+            const uint32_t bl = __ballot_sync(0xffffffffu, left);
+            const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
+            const uint32_t lt = (1u << lane) - 1u;
+            if (left) a.pidx[e.start + nl + __popc(bl & lt)] = pid;
+            else if (valid) a.rtmp[e.start + nr + __popc(br & lt)] = pid;
+            nl += __popc(bl);
+            nr += __popc(br);
+        }
+        __syncwarp();
+        for (uint32_t j = lane; j < nr; j += 32) a.pidx[e.start + nl + j] = a.rtmp[e.start + j];
+        __syncwarp();
+        uint32_t mid = e.start + nl;
+        uint8_t even = 0;
+        if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
+            // kd_forest.cpp:70-83 degenerate split: sort by (value, id), split at the median
+            warp_sort_node(a, s, e.start, size, d);
+            mid = e.start + size / 2;
+            split = midpoint_f(ldx(a, a.pidx[mid - 1], d), ldx(a, a.pidx[mid], d));
+            even = 1;
+        }
+        if (lane == 0) {
+            a.nodes[id] = KdNodeDev{d, split, 0u, 0u};
+            a.even[id] = even;
+            s.wstack[wsp] = StackEntry{mid, e.end, e.depth + 1, id, 1};
+            s.wstack[wsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, 0};
+        }
+        wsp += 2;
+        if (wsp > kStack - 2 && lane == 0) s.error = 1;
+        if (wsp > kStack - 2) break;
+        __syncwarp();
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------- block path
+
+__device__ void block_reduce_stats(Smem& s, double& sum, int& top, int& lsb) {
+    const uint32_t lane = lane_id(), warp = threadIdx.x / 32;
+    for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        top = max(top, __shfl_xor_sync(0xffffffffu, top, o));
+        lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+    }
+    if (lane == 0) {
+        s.red_sum[warp] = sum;
+        s.red_top[warp] = top;
+        s.red_lsb[warp] = lsb;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        sum = lane < kWarps ? s.red_sum[lane] : 0.0;
+        top = lane < kWarps ? s.red_top[lane] : INT_MIN;
+        lsb = lane < kWarps ? s.red_lsb[lane] : INT_MAX;
+        for (int o = 16; o > 0; o >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            top = max(top, __shfl_xor_sync(0xffffffffu, top, o));
+            lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+        }
+        if (lane == 0) {
+            s.red_sum[0] = sum;
+            s.red_top[0] = top;
+            s.red_lsb[0] = lsb;
+        }
+    }
+    __syncthreads();
+    sum = s.red_sum[0];
+    top = s.red_top[0];
+    lsb = s.red_lsb[0];
+    __syncthreads();
+}
+
+__device__ void block_sort_node(const BuildArgs& a, Smem& s, uint32_t start, uint32_t size,
+                                uint32_t d) {
+    const uint32_t m = next_pow2(size);
+    uint64_t* k = m <= kSortSmem ? s.sortk : a.sortbuf;
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+        uint64_t key = kEmptyKey;
+        if (j < size) {
+            const uint32_t id = a.pidx[start + j];
+            key = val_id_key(ldx(a, id, d), id);
+        }
+        k[j] = key;
+    }
+    __syncthreads();
+    block_bitonic_sort(k, m);
+    for (uint32_t j = threadIdx.x; j < size; j += blockDim.x) a.pidx[start + j] = uint32_t(k[j]);
+    __syncthreads();
+}
+
+__device__ void block_split_node(const BuildArgs& a, Smem& s, const StackEntry& e, uint32_t id) {
+    const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid / 32;
+    const uint32_t size = e.end - e.start;
+    if (warp == 0) {
+        const uint32_t d = warp_draw(s, a.dim);
+        if (lane == 0) s.b_d = d;
+    }
+    __syncthreads();
+    const uint32_t d = s.b_d;
+    double sum = 0.0;
+    int top = INT_MIN, lsb = INT_MAX;
+    for (uint32_t p = e.start + tid; p < e.end; p += 4 * kBlock) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t q = p + u * kBlock;
+            v[u] = q < e.end ? ldx(a, a.pidx[q], d) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            sum += double(v[u]);
+            val_stats(v[u], top, lsb);
+        }
+    }
+    block_reduce_stats(s, sum, top, lsb);
+    if (!sum_is_exact(top, lsb, size)) {
+        if (tid == 0) {
+            sum = 0.0;
+            for (uint32_t p = e.start; p < e.end; ++p) sum += double(ldx(a, a.pidx[p], d));
+            s.b_sum = sum;
+        }
+        __syncthreads();
+        sum = s.b_sum;
+    }
+    float split = __double2float_rn(__ddiv_rn(sum, double(size)));
+    // block-wide stable partition
+    uint32_t nl = 0, nr = 0;
+    for (uint32_t base = e.start; base < e.end; base += kBlock) {
+        const uint32_t p = base + tid;
+        const bool valid = p < e.end;
+        const uint32_t pid = valid ? a.pidx[p] : 0;
+        const bool left = valid && ldx(a, pid, d) <= split;
+        const uint32_t bl = __ballot_sync(0xffffffffu, left);
+        const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
+        if (lane == 0) {
+            s.cnt_l[warp] = __popc(bl);
+            s.cnt_r[warp] = __popc(br);
+        }
+        __syncthreads();
+        uint32_t pl = 0, pr = 0, tl = 0, tr = 0;
+        for (uint32_t w = 0; w < kWarps; ++w) {
+            const uint32_t cl = s.cnt_l[w], cr = s.cnt_r[w];
+            if (w < warp) { pl += cl; pr += cr; }
+            tl += cl;
+            tr += cr;
+        }
+        const uint32_t lt = (1u << lane) - 1u;
+        if (left) a.pidx[e.start + nl + pl + __popc(bl & lt)] = pid;
+        else if (valid) a.rtmp[e.start + nr + pr + __popc(br & lt)] = pid;
+        nl += tl;
+        nr += tr;
+        __syncthreads();
+    }
+    for (uint32_t j = tid; j < nr; j += kBlock) a.pidx[e.start + nl + j] = a.rtmp[e.start + j];
+    __syncthreads();
+    uint32_t mid = e.start + nl;
+    uint8_t even = 0;
+    if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
+        block_sort_node(a, s, e.start, size, d);
+        mid = e.start + size / 2;
+        split = midpoint_f(ldx(a, a.pidx[mid - 1], d), ldx(a, a.pidx[mid], d));
+        even = 1;
+    }
+    if (tid == 0) {
+        a.nodes[id] = KdNodeDev{d, split, 0u, 0u};
+        a.even[id] = even;
+        s.bstack[s.bsp] = StackEntry{mid, e.end, e.depth + 1, id, 1};
+        s.bstack[s.bsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, 0};
+        s.bsp += 2;
+        if (s.bsp > kStack - 2) s.error = 1;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs* __restrict__ args) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+    const BuildArgs a = args[blockIdx.x];
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t i = tid; i < a.n; i += kBlock) a.pidx[i] = i;
+    if (tid == 0) {
+        s.mt[0] = a.seed;
+        for (int i = 1; i < 312; ++i)
+            s.mt[i] = 6364136223846793005ULL * (s.mt[i - 1] ^ (s.mt[i - 1] >> 62)) + uint64_t(i);
+        s.mt_idx = 312;
+        s.node_count = 0;
+        s.leaf_count = 0;
+        s.max_depth = 0;
+        s.error = 0;
+        s.bstack[0] = StackEntry{0, a.n, 0, kInvalidId, 0};
+        s.bsp = 1;
+    }
+    __syncthreads();
+    while (s.bsp > 0 && !s.error) {
+        const StackEntry e = s.bstack[s.bsp - 1];
+        __syncthreads();
+        const uint32_t size = e.end - e.start;
+        if (size <= kWarpSubtree) {
+            if (tid == 0) s.bsp -= 1;
+            __syncthreads();
+            if (tid < 32) warp_build_subtree(a, s, e);
+            __syncthreads();
+            continue;
+        }
+        const uint32_t id = s.node_count;
+        __syncthreads();
+        if (tid == 0) {
+            s.bsp -= 1;
+            s.node_count = id + 1;
+            if (e.parent != kInvalidId) {
+                if (e.side == 0) a.nodes[e.parent].left = id;
+                else a.nodes[e.parent].right = id;
+            }
+            a.depth[id] = e.depth;
+            s.max_depth = max(s.max_depth, e.depth);
+        }
+        __syncthreads();
+        block_split_node(a, s, e, id);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a.meta[0] = s.node_count;
+        a.meta[1] = 0;
+        a.meta[2] = s.leaf_count;
+        a.meta[3] = s.max_depth;
+        a.meta[4] = s.error;
+    }
+}
+
+// parent links and leaf ownership (graph_build.cpp:238-257 tables).
+__global__ void forest_links_kernel(const KdNodeDev* __restrict__ nodes, uint32_t num_nodes,
+                                    const uint32_t* __restrict__ pidx, uint32_t* __restrict__ parent,
+                                    uint32_t* __restrict__ owner) {
+    for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id < num_nodes; id += gridDim.x * blockDim.x) {
+        const KdNodeDev nd = nodes[id];
+        if (nd.split_dim == kLeaf) {
+            for (uint32_t p = nd.left; p < nd.right; ++p) owner[pidx[p]] = id;
+        } else {
+            parent[nd.left] = id;
+            parent[nd.right] = id;
+        }
+    }
+}
+
+// Batched best-bin-first (kd_forest.cpp:276-305).  One thread per query with
+// a binary min-heap over (double cost, node) in global scratch.
+struct HeapEnt {
+    double cost;
+    uint32_t node;
+    uint32_t pad;
+};
+__device__ __forceinline__ bool heap_less(const HeapEnt& x, const HeapEnt& y) {
+    return x.cost != y.cost ? x.cost < y.cost : x.node < y.node;
+}
+__global__ void search_leaves_kernel(const KdNodeDev* __restrict__ nodes, uint32_t root,
+                                     uint32_t leaf_count, const float* __restrict__ q, uint32_t nq,
+                                     uint32_t ld, uint32_t n_leaves, HeapEnt* __restrict__ heaps,
+                                     uint32_t heap_cap, uint32_t* __restrict__ out,
+                                     uint32_t* __restrict__ counts) {
+    const uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= nq) return;
+    const float* qq = q + size_t(qi) * ld;
+    HeapEnt* h = heaps + size_t(qi) * heap_cap;
+    uint32_t hn = 0, cnt = 0;
+    const uint32_t want = min(n_leaves, leaf_count);
+    uint32_t* o = out + size_t(qi) * n_leaves;
+    for (uint32_t j = 0; j < n_leaves; ++j) o[j] = kInvalidId;
+    if (want > 0) {
+        uint32_t nd = root;
+        double cost = 0.0;
+        for (;;) {
+            for (KdNodeDev x = nodes[nd]; x.split_dim != kLeaf; x = nodes[nd]) {
+                const double diff = double(qq[x.split_dim]) - double(x.split_val);
+                const HeapEnt v{cost + fabs(diff), diff <= 0.0 ? x.right : x.left, 0};
+                uint32_t i = hn++;
+                while (i > 0) {
+                    const uint32_t p = (i - 1) / 2;
+                    if (!heap_less(v, h[p])) break;
+                    h[i] = h[p];
+                    i = p;
+                }
+                h[i] = v;
+                nd = diff <= 0.0 ? x.left : x.right;
+            }
+            o[cnt++] = nd;
+            if (cnt >= want || hn == 0) break;
+            const HeapEnt top = h[0];
+            const HeapEnt last = h[--hn];
+            uint32_t i = 0;
+            for (;;) {
+                uint32_t c = 2 * i + 1;
+                if (c >= hn) break;
+                if (c + 1 < hn && heap_less(h[c + 1], h[c])) ++c;
+                if (!heap_less(h[c], last)) break;
+                h[i] = h[c];
+                i = c;
+            }
+            if (hn) h[i] = last;
+            nd = top.node;
+            cost = top.cost;
+        }
+    }
+    counts[qi] = cnt;
+}
+
+__global__ void descend_kernel(const KdNodeDev* __restrict__ nodes, const float* __restrict__ q,
+                               uint32_t nq, uint32_t ld, const uint32_t* __restrict__ start,
+                               uint32_t* __restrict__ out) {
+    const uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= nq) return;
+    const float* qq = q + size_t(qi) * ld;
+    uint32_t nd = start[qi];
+    for (KdNodeDev x = nodes[nd]; x.split_dim != kLeaf; x = nodes[nd])
+        nd = qq[x.split_dim] <= x.split_val ? x.left : x.right;
+    out[qi] = nd;
+}
+
+}  // namespace
+
+void forest_ensure_links(annk_forest* f) {
+    if (f->links_ready) return;
+    for (auto& t : f->trees) {
+        t.parent.alloc(t.num_nodes);
+        t.parent.fill_bytes(0xff);
+        t.owner.alloc(f->n);
+        t.owner.fill_bytes(0xff);
+        const uint32_t grid = std::min<uint32_t>((t.num_nodes + 255) / 256, 4096);
+        LAUNCH(forest_links_kernel, std::max(grid, 1u), 256, 0, t.nodes.p, t.num_nodes, t.pidx.p,
+               t.parent.p, t.owner.p);
+    }
+    f->links_ready = true;
+    forest_upload_views(f);
+}
+
+void forest_upload_views(annk_forest* f) {
+    std::vector<TreeView> v(f->n_trees);
+    for (uint32_t i = 0; i < f->n_trees; ++i) {
+        const TreeDev& t = f->trees[i];
+        v[i] = TreeView{t.nodes.p, t.depth.p, t.pidx.p, t.parent.p, t.owner.p,
+                        t.root, t.num_nodes, t.leaf_count, t.max_depth};
+    }
+    f->views.alloc(f->n_trees);
+    f->views.upload(v.data(), v.size());
+    ssync();
+}
+
+}  // namespace annk
+
+using namespace annk;
+
+extern "C" {
+
+int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_cap, uint64_t seed,
+                      annk_forest** out) {
+    return abi([&] {
+        if (!ds || !out) throw_invalid("build_forest: null argument");
+        if (ds->n < 1) throw_invalid("build_forest: empty dataset");
+        if (n_trees < 1) throw_invalid("build_forest: n_trees must be >= 1");
+        if (leaf_cap < 1) throw_invalid("build_forest: leaf_cap must be >= 1");
+        auto f = std::make_unique<annk_forest>();
+        f->n_trees = n_trees;
+        f->n = ds->n;
+        f->dim = ds->dim;
+        f->leaf_cap = leaf_cap;
+        f->seed = seed;
+        f->trees.resize(n_trees);
+        const uint32_t n = ds->n;
+        const size_t cap_nodes = 2 * size_t(n);
+        DevBuf<uint32_t> rtmp(size_t(n) * n_trees);
+        DevBuf<uint64_t> sortbuf(size_t(next_pow2(n)) * n_trees);
+        DevBuf<uint32_t> meta(5 * n_trees);
+        std::vector<BuildArgs> args(n_trees);
+        for (uint32_t t = 0; t < n_trees; ++t) {
+            TreeDev& tr = f->trees[t];
+            tr.nodes.alloc(cap_nodes);
+            tr.depth.alloc(cap_nodes);
+            tr.even.alloc(cap_nodes);
+            tr.pidx.alloc(n);
+            args[t] = BuildArgs{ds->data.p, n, ds->dim, ds->ld, leaf_cap, substream(seed, t),
+                                tr.nodes.p, tr.depth.p, tr.even.p, tr.pidx.p,
+                                rtmp.p + size_t(t) * n, sortbuf.p + size_t(t) * next_pow2(n),
+                                meta.p + 5 * t};
+        }
+        DevBuf<BuildArgs> dargs(n_trees);
+        dargs.upload(args.data(), n_trees);
+        const size_t smem = sizeof(Smem);
+        CK(cudaFuncSetAttribute(forest_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        LAUNCH(forest_build_kernel, n_trees, kBlock, smem, dargs.p);
+        std::vector<uint32_t> hm(5 * n_trees);
+        meta.download(hm.data(), hm.size());
+        ssync();
+        for (uint32_t t = 0; t < n_trees; ++t) {
+            if (hm[5 * t + 4]) throw Error(kInternal, "build_forest: traversal stack overflow");
+            TreeDev& tr = f->trees[t];
+            tr.num_nodes = hm[5 * t + 0];
+            tr.root = hm[5 * t + 1];
+            tr.leaf_count = hm[5 * t + 2];
+            tr.max_depth = hm[5 * t + 3];
+        }
+        forest_upload_views(f.get());
+        *out = f.release();
+    });
+}
+
+int annk_forest_destroy(annk_forest* f) {
+    return abi([&] { delete f; });
+}
+
+int annk_forest_info(const annk_forest* f, uint32_t* counts, uint64_t* seed) {
+    return abi([&] {
+        counts[0] = f->n_trees;
+        counts[1] = f->n;
+        counts[2] = f->dim;
+        counts[3] = f->leaf_cap;
+        if (seed) *seed = f->seed;
+    });
+}
+
+int annk_forest_tree_info(const annk_forest* f, uint32_t t, uint32_t* info) {
+    return abi([&] {
+        if (t >= f->n_trees) throw_range("forest_tree_info: tree index out of range");
+        const TreeDev& tr = f->trees[t];
+        info[0] = tr.num_nodes;
+        info[1] = tr.root;
+        info[2] = tr.leaf_count;
+        info[3] = tr.max_depth;
+    });
+}
+
+int annk_forest_export(const annk_forest* f, uint32_t t, uint32_t* split_dim, float* split_val,
+                       uint32_t* left, uint32_t* right, uint32_t* depth, uint8_t* even_split,
+                       uint32_t* point_index) {
+    return abi([&] {
+        if (t >= f->n_trees) throw_range("forest_export: tree index out of range");
+        const TreeDev& tr = f->trees[t];
+        std::vector<KdNodeDev> nodes(tr.num_nodes);
+        tr.nodes.download(nodes.data(), tr.num_nodes);
+        if (depth) tr.depth.download(depth, tr.num_nodes);
+        if (even_split) tr.even.download(even_split, tr.num_nodes);
+        if (point_index) tr.pidx.download(point_index, f->n);
+        ssync();
+        for (uint32_t i = 0; i < tr.num_nodes; ++i) {
+            if (split_dim) split_dim[i] = nodes[i].split_dim;
+            if (split_val) split_val[i] = nodes[i].split_val;
+            if (left) left[i] = nodes[i].left;
+            if (right) right[i] = nodes[i].right;
+        }
+    });
+}
+
+int annk_forest_import(uint32_t n, uint32_t dim, uint32_t leaf_cap, uint64_t seed,
+                       uint32_t n_trees, const uint32_t* node_counts, const uint32_t* roots,
+                       const uint32_t* split_dim, const float* split_val, const uint32_t* left,
+                       const uint32_t* right, const uint32_t* depth, const uint8_t* even_split,
+                       const uint32_t* point_index, annk_forest** out) {
+    return abi([&] {
+        if (n < 1 || dim < 1 || n_trees < 1 || leaf_cap < 1) throw_invalid("forest_import: degenerate header");
+        auto f = std::make_unique<annk_forest>();
+        f->n_trees = n_trees;
+        f->n = n;
+        f->dim = dim;
+        f->leaf_cap = leaf_cap;
+        f->seed = seed;
+        f->trees.resize(n_trees);
+        size_t off = 0;
+        for (uint32_t t = 0; t < n_trees; ++t) {
+            TreeDev& tr = f->trees[t];
+            const uint32_t m = node_counts[t];
+            if (m == 0 || m > 2 * n) throw_invalid("forest_import: implausible node count");
+            std::vector<KdNodeDev> nodes(m);
+            uint32_t leaves = 0, maxd = 0;
+            for (uint32_t i = 0; i < m; ++i) {
+                nodes[i] = KdNodeDev{split_dim[off + i], split_val[off + i], left[off + i], right[off + i]};
+                const bool leaf = split_dim[off + i] == kLeaf;
+                leaves += leaf;
+                if (leaf) {
+                    if (left[off + i] >= right[off + i] || right[off + i] > n) throw_invalid("forest_import: bad leaf range");
+                } else {
+                    if (split_dim[off + i] >= dim) throw_invalid("forest_import: split dimension out of range");
+                    if (left[off + i] >= m || right[off + i] >= m) throw_invalid("forest_import: child id out of range");
+                }
+                maxd = std::max(maxd, depth[off + i]);
+            }
+            tr.num_nodes = m;
+            tr.root = roots[t];
+            if (tr.root >= m) throw_invalid("forest_import: bad root");
+            tr.leaf_count = leaves;
+            tr.max_depth = maxd;
+            tr.nodes.alloc(m);
+            tr.nodes.upload(nodes.data(), m);
+            tr.depth.alloc(m);
+            tr.depth.upload(depth + off, m);
+            tr.even.alloc(m);
+            tr.even.upload(even_split + off, m);
+            tr.pidx.alloc(n);
+            tr.pidx.upload(point_index + size_t(t) * n, n);
+            ssync();
+            off += m;
+        }
+        forest_upload_views(f.get());
+        *out = f.release();
+    });
+}
+
+int annk_search_leaves(const annk_forest* f, uint32_t t, const float* queries, uint32_t nq,
+                       uint32_t dim, uint32_t n_leaves, uint32_t* out, uint32_t* out_counts) {
+    return abi([&] {
+        if (t >= f->n_trees) throw_range("search_leaves: tree index out of range");
+        if (dim != f->dim) throw_invalid("search_leaves: query length mismatch");
+        if (nq == 0) return;
+        const TreeDev& tr = f->trees[t];
+        const uint32_t ld = (dim + 3) & ~3u;
+        std::vector<float> qh(size_t(nq) * ld, 0.0f);
+        for (uint32_t i = 0; i < nq; ++i)
+            for (uint32_t j = 0; j < dim; ++j) qh[size_t(i) * ld + j] = queries[size_t(i) * dim + j];
+        DevBuf<float> dq(qh.size());
+        dq.upload(qh.data(), qh.size());
+        const uint32_t nl = std::max(n_leaves, 1u);
+        const uint32_t heap_cap = (std::min(n_leaves, tr.leaf_count) + 1) * (tr.max_depth + 1) + 1;
+        DevBuf<HeapEnt> heaps(size_t(nq) * heap_cap);
+        DevBuf<uint32_t> dout(size_t(nq) * nl), dcnt(nq);
+        LAUNCH(search_leaves_kernel, (nq + 127) / 128, 128, 0, tr.nodes.p, tr.root, tr.leaf_count, dq.p,
+               nq, ld, n_leaves, heaps.p, heap_cap, dout.p, dcnt.p);
+        if (n_leaves) dout.download(out, size_t(nq) * n_leaves);
+        dcnt.download(out_counts, nq);
+        ssync();
+    });
+}
+
+int annk_descend_from(const annk_forest* f, uint32_t t, const float* queries, uint32_t nq,
+                      uint32_t dim, const uint32_t* start, uint32_t* out) {
+    return abi([&] {
+        if (t >= f->n_trees) throw_range("descend_from: tree index out of range");
+        if (dim != f->dim) throw_invalid("descend_from: query length mismatch");
+        const TreeDev& tr = f->trees[t];
+        for (uint32_t i = 0; i < nq; ++i)
+            if (start[i] >= tr.num_nodes) throw_range("descend_from: node id out of range");
+        if (nq == 0) return;
+        const uint32_t ld = (dim + 3) & ~3u;
+        std::vector<float> qh(size_t(nq) * ld, 0.0f);
+        for (uint32_t i = 0; i < nq; ++i)
+            for (uint32_t j = 0; j < dim; ++j) qh[size_t(i) * ld + j] = queries[size_t(i) * dim + j];
+        DevBuf<float> dq(qh.size());
+        dq.upload(qh.data(), qh.size());
+        DevBuf<uint32_t> ds(nq), dout(nq);
+        ds.upload(start, nq);
+        LAUNCH(descend_kernel, (nq + 127) / 128, 128, 0, tr.nodes.p, dq.p, nq, ld, ds.p, dout.p);
+        dout.download(out, nq);
+        ssync();
+    });
+}
+
+}  // extern "C"

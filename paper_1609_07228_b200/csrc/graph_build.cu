@@ -1,0 +1,1010 @@
+// graph_build.cu — divide-and-conquer init + NN-descent on B200.
+//
+// Reference: proj/src/graph_build.cpp (init_graph :230-292, rebuild_sample_lists
+// :59-86, union_reverse_lists + sample_down :38-53,88-103, nn_descent_iteration
+// :105-162, finalize :346-373, pool_topk_accuracy :209-226).
+//
+// Pools are rows of P 64-bit keys (dist_bits << 32 | id) kept sorted, plus a
+// flag_new byte per slot.  The reference's NeighborPool insert keeps the top P
+// of everything offered, rejecting duplicates (neighbor_pool.hpp:35-53), and
+// an entry evicted within a round can never come back (the tail only
+// shrinks).  So the pool after a join round is exactly
+//       top-P by key of (start pool  U  all offers),
+// independent of the order offers arrive.  The GPU join therefore never
+// touches the pools: it appends every offer that beats the target's
+// start-of-round tail to a per-target buffer, and a merge kernel forms the
+// new pools.  Flags follow the reference: an entry already present keeps its
+// flag, an entry that arrived this round is new.
+//
+// The one order-dependent reference quantity is `changes` (accepted inserts,
+// counting ones later evicted).  This library reports the order-independent
+// count of entries inserted this round that survive in the pools.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <numeric>
+
+#include "../../include/annkit_b200.h"
+#include "internal.cuh"
+
+namespace annk {
+namespace {
+
+constexpr uint32_t kInitWarps = 4;
+constexpr uint32_t kInitCap = 1024;  // fast-path candidate capacity per point
+
+// ---------------------------------------------------------------- helpers
+
+// First `count` (<= 64) outputs of std::mt19937_64(seed), without building the
+// whole 312-word state: output k needs init words k, k+1 and k+156.
+__device__ void mt_first_outputs(uint64_t seed, uint32_t count, uint64_t* out) {
+    uint64_t lo[65], hi[64];
+    uint64_t x = seed;
+    lo[0] = x;
+    const uint32_t last = 155 + count;
+    for (uint32_t i = 1; i <= last; ++i) {
+        x = 6364136223846793005ULL * (x ^ (x >> 62)) + uint64_t(i);
+        if (i <= count) lo[i] = x;
+        if (i >= 156) hi[i - 156] = x;
+    }
+    for (uint32_t k = 0; k < count; ++k) out[k] = mt_temper(mt_twist(lo[k], lo[k + 1], hi[k]));
+}
+
+// graph_build.cpp:38-48 sample_down on an already sorted, unique list `a` of
+// length m: partial Fisher-Yates over the first cap slots.  Writes the
+// sampled prefix to out (order matters only for the subsequent sort-dedup).
+__device__ uint32_t sample_down_sorted(const uint32_t* a, uint32_t m, uint32_t cap, uint64_t seed,
+                                       uint32_t* out) {
+    if (m <= cap) {
+        for (uint32_t i = 0; i < m; ++i) out[i] = a[i];
+        return m;
+    }
+    uint64_t r[64];
+    mt_first_outputs(seed, cap, r);
+    // sparse overlay of swapped positions
+    uint32_t pos[128], val[128];
+    uint32_t no = 0;
+    auto get = [&](uint32_t p) -> uint32_t {
+        for (uint32_t j = 0; j < no; ++j)
+            if (pos[j] == p) return val[j];
+        return a[p];
+    };
+    auto set = [&](uint32_t p, uint32_t v) {
+        for (uint32_t j = 0; j < no; ++j)
+            if (pos[j] == p) { val[j] = v; return; }
+        pos[no] = p;
+        val[no] = v;
+        ++no;
+    };
+    for (uint32_t i = 0; i < cap; ++i) {
+        const uint32_t j = i + uint32_t(r[i] % uint64_t(m - i));
+        const uint32_t vi = get(i), vj = get(j);
+        set(i, vj);
+        set(j, vi);
+    }
+    for (uint32_t i = 0; i < cap; ++i) out[i] = get(i);
+    return cap;
+}
+
+// Sort + unique n u32 values in smem s (capacity m = pow2 >= n) by one warp.
+// Returns the unique count (values compacted to the front).
+__device__ uint32_t warp_sort_unique_u32(uint32_t* s, uint32_t n, uint32_t m) {
+    const uint32_t lane = lane_id();
+    for (uint32_t j = n + lane; j < m; j += 32) s[j] = 0xffffffffu;
+    __syncwarp();
+    warp_bitonic_sort_u32(s, m);
+    uint32_t out = 0;
+    for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t j = base + lane;
+        const uint32_t v = j < n ? s[j] : 0;
+        const bool keep = j < n && (j == 0 || s[j - 1] != v);
+        const uint32_t b = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) s[out + __popc(b & ((1u << lane) - 1u))] = v;
+        out += __popc(b);
+        __syncwarp();
+    }
+    return out;
+}
+
+// ----------------------------------------------------------------- init
+
+struct InitArgs {
+    const float* x;
+    uint32_t n, ld, n_trees, conquer_depth, P;
+    const TreeView* trees;
+    uint64_t* keys;
+    uint8_t* flags;
+    uint32_t* sizes;
+    unsigned long long* comps;
+    uint32_t* overflow;  // [count, ids...]
+};
+
+// Collects point i's candidate set (graph_build.cpp:266-280) into cand;
+// returns the count (may exceed cap: caller retries with a bigger buffer).
+__device__ uint32_t init_collect(const InitArgs& a, uint32_t i, const float* q, uint32_t* cand,
+                                 uint32_t cap, uint32_t* sib, uint32_t sib_cap, uint32_t* s_cnt) {
+    const uint32_t lane = lane_id();
+    if (lane == 0) { s_cnt[0] = 0; s_cnt[1] = 0; }
+    __syncwarp();
+    // own leaves + ancestor walk, one lane per tree
+    for (uint32_t t = lane; t < a.n_trees; t += 32) {
+        const TreeView tv = a.trees[t];
+        const uint32_t leaf = tv.owner[i];
+        const KdNodeDev ln = tv.nodes[leaf];
+        const uint32_t len = ln.right - ln.left;
+        const uint32_t slot = atomicAdd(&s_cnt[0], len);
+        for (uint32_t j = 0; j < len; ++j)
+            if (slot + j < cap) cand[slot + j] = tv.pidx[ln.left + j];
+        uint32_t node = leaf;
+        for (;;) {
+            const uint32_t par = tv.parent[node];
+            if (par == kInvalidId || tv.depth[par] < a.conquer_depth) break;
+            const KdNodeDev pn = tv.nodes[par];
+            const uint32_t sb = pn.left == node ? pn.right : pn.left;
+            const uint32_t k = atomicAdd(&s_cnt[1], 1u);
+            if (k < sib_cap) {
+                sib[k] = sb;
+                sib[sib_cap + k] = t;
+            }
+            node = par;
+        }
+    }
+    __syncwarp();
+    const uint32_t nsib = min(s_cnt[1], sib_cap);
+    // descend every off-path sibling with the point itself (descend_from)
+    for (uint32_t k = lane; k < nsib; k += 32) {
+        const TreeView tv = a.trees[sib[sib_cap + k]];
+        uint32_t nd = sib[k];
+        for (KdNodeDev x = tv.nodes[nd]; x.split_dim != kLeaf; x = tv.nodes[nd])
+            nd = q[x.split_dim] <= x.split_val ? x.left : x.right;
+        const KdNodeDev ln = tv.nodes[nd];
+        const uint32_t len = ln.right - ln.left;
+        const uint32_t slot = atomicAdd(&s_cnt[0], len);
+        for (uint32_t j = 0; j < len; ++j)
+            if (slot + j < cap) cand[slot + j] = tv.pidx[ln.left + j];
+    }
+    __syncwarp();
+    const uint32_t c = s_cnt[0];
+    __syncwarp();
+    return s_cnt[1] > sib_cap ? UINT32_MAX : c;
+}
+
+__device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, uint32_t* cand, uint32_t c,
+                            uint32_t m, uint64_t* keys) {
+    const uint32_t lane = lane_id();
+    const uint32_t u = warp_sort_unique_u32(cand, c, m);
+    // drop self, compute exact distances
+    uint32_t nk = 0;
+    for (uint32_t base = 0; base < u; base += 32) {
+        const uint32_t j = base + lane;
+        const uint32_t id = j < u ? cand[j] : kInvalidId;
+        const bool keep = j < u && id != i;
+        const uint32_t b = __ballot_sync(0xffffffffu, keep);
+        if (keep) keys[nk + __popc(b & ((1u << lane) - 1u))] =
+            make_key(l2_exact_ldg(q, a.x + size_t(id) * a.ld, a.ld), id);
+        nk += __popc(b);
+    }
+    const uint32_t mk = next_pow2(max(nk, 1u));
+    for (uint32_t j = nk + lane; j < mk; j += 32) keys[j] = kEmptyKey;
+    __syncwarp();
+    warp_bitonic_sort(keys, mk);
+    const uint32_t take = min(nk, a.P);
+    uint64_t* pk = a.keys + size_t(i) * a.P;
+    uint8_t* pf = a.flags + size_t(i) * a.P;
+    for (uint32_t j = lane; j < a.P; j += 32) {
+        pk[j] = j < take ? keys[j] : kEmptyKey;
+        pf[j] = j < take ? 1 : 0;
+    }
+    if (lane == 0) {
+        a.sizes[i] = take;
+        atomicAdd(a.comps, (unsigned long long)nk);
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint32_t sib_cap) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
+    const size_t per_warp = (size_t(kInitCap) * 4 + size_t(kInitCap) * 8 + size_t(a.ld) * 4 +
+                             size_t(sib_cap) * 8 + 16 + 15) & ~size_t(15);  // float4 rows stay aligned
+    unsigned char* base = smem + warp * per_warp;
+    uint64_t* keys = reinterpret_cast<uint64_t*>(base);
+    uint32_t* cand = reinterpret_cast<uint32_t*>(base + size_t(kInitCap) * 8);
+    float* q = reinterpret_cast<float*>(base + size_t(kInitCap) * 12);
+    uint32_t* sib = reinterpret_cast<uint32_t*>(base + size_t(kInitCap) * 12 + size_t(a.ld) * 4);
+    uint32_t* s_cnt = sib + 2 * sib_cap;
+    for (uint32_t i = blockIdx.x * kInitWarps + warp; i < a.n; i += gridDim.x * kInitWarps) {
+        for (uint32_t j = lane; j < a.ld; j += 32) q[j] = a.x[size_t(i) * a.ld + j];
+        __syncwarp();
+        const uint32_t c = init_collect(a, i, q, cand, kInitCap, sib, sib_cap, s_cnt);
+        if (c > kInitCap) {
+            if (lane == 0) {
+                const uint32_t o = atomicAdd(&a.overflow[0], 1u);
+                a.overflow[1 + o] = i;
+            }
+            __syncwarp();
+            continue;
+        }
+        init_finish(a, i, q, cand, c, next_pow2(max(c, 1u)), keys);
+    }
+}
+
+// Overflow path: one warp per point with global scratch of capacity cap.
+__global__ void init_overflow_kernel(InitArgs a, const uint32_t* list, uint32_t count, uint32_t cap,
+                                     uint32_t sib_cap, uint32_t* gcand, uint64_t* gkeys, float* gq,
+                                     uint32_t* gsib) {
+    __shared__ uint32_t s_cnt[2];
+    const uint32_t lane = lane_id();
+    for (uint32_t r = blockIdx.x; r < count; r += gridDim.x) {
+        const uint32_t i = list[r];
+        uint32_t* cand = gcand + size_t(blockIdx.x) * cap;
+        uint64_t* keys = gkeys + size_t(blockIdx.x) * cap;
+        float* q = gq + size_t(blockIdx.x) * a.ld;
+        uint32_t* sib = gsib + size_t(blockIdx.x) * 2 * sib_cap;
+        for (uint32_t j = lane; j < a.ld; j += 32) q[j] = a.x[size_t(i) * a.ld + j];
+        __syncwarp();
+        const uint32_t c = init_collect(a, i, q, cand, cap, sib, sib_cap, s_cnt);
+        init_finish(a, i, q, cand, min(c, cap), next_pow2(max(min(c, cap), 1u)), keys);
+    }
+}
+
+// -------------------------------------------------------------- sampling
+
+struct SampleArgs {
+    uint32_t n, P, S;
+    const uint64_t* keys;
+    uint8_t* flags;
+    const uint32_t* sizes;
+    uint32_t* fnew;  // n x S
+    uint32_t* fold;  // n x P
+    uint32_t* cnew;
+    uint32_t* cold;
+    uint32_t* rn_cnt;
+    uint32_t* ro_cnt;
+    uint64_t* thr;
+};
+
+// graph_build.cpp:71-85: ascending scan until S new entries are taken.
+__global__ void sample_kernel(SampleArgs a) {
+    const uint32_t lane = lane_id();
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= a.n) return;
+    const uint32_t sz = a.sizes[i];
+    const uint64_t* pk = a.keys + size_t(i) * a.P;
+    uint8_t* pf = a.flags + size_t(i) * a.P;
+    uint32_t taken = 0, nold = 0;
+    for (uint32_t base = 0; base < sz && taken < a.S; base += 32) {
+        const uint32_t j = base + lane;
+        const bool valid = j < sz;
+        const bool isnew = valid && pf[j];
+        const uint32_t bn = __ballot_sync(0xffffffffu, isnew);
+        // entries are scanned while fewer than S news have been taken
+        const uint32_t lt = (1u << lane) - 1u;
+        const uint32_t rank_new = taken + __popc(bn & lt);  // news before me
+        const bool in_scan = valid && rank_new < a.S;
+        const uint32_t id = valid ? key_id(pk[j]) : 0;
+        const uint32_t bo = __ballot_sync(0xffffffffu, in_scan && !isnew);
+        if (in_scan && isnew) {
+            a.fnew[size_t(i) * a.S + rank_new] = id;
+            pf[j] = 0;
+            atomicAdd(&a.rn_cnt[id], 1u);
+        } else if (in_scan) {
+            a.fold[size_t(i) * a.P + nold + __popc(bo & lt)] = id;
+            atomicAdd(&a.ro_cnt[id], 1u);
+        }
+        taken = min(a.S, taken + __popc(bn));
+        nold += __popc(bo);
+    }
+    if (lane == 0) {
+        a.cnew[i] = taken;
+        a.cold[i] = nold;
+        a.thr[i] = sz == a.P ? pk[a.P - 1] : kEmptyKey;
+    }
+}
+
+__global__ void reverse_scatter_kernel(uint32_t n, uint32_t width, const uint32_t* __restrict__ fwd,
+                                       const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                                       uint32_t* __restrict__ cursor, uint32_t* __restrict__ data) {
+    const uint32_t lane = lane_id();
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= n) return;
+    const uint32_t c = cnt[i];
+    for (uint32_t j = lane; j < c; j += 32) {
+        const uint32_t id = fwd[size_t(i) * width + j];
+        const uint32_t pos = atomicAdd(&cursor[id], 1u);
+        data[off[id] + pos] = i;
+    }
+}
+
+struct UnionArgs {
+    uint32_t n, P, S;
+    uint64_t round_seed;
+    const uint32_t *fnew, *fold, *cnew, *cold;
+    const uint32_t *rn_off, *rn_data, *ro_off, *ro_data;
+    uint32_t* gnew;  // n x 2S
+    uint32_t* gold;  // n x (P+S)
+    uint32_t* gncnt;
+    uint32_t* gocnt;
+    unsigned long long* join_rows;
+};
+
+// graph_build.cpp:88-103 per point: sample reverse lists, union, sort-dedup.
+__global__ void union_kernel(UnionArgs a, uint32_t m_new, uint32_t m_old) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
+    const uint32_t wpb = blockDim.x / 32;
+    uint32_t* sn = reinterpret_cast<uint32_t*>(smem) + warp * (m_new + m_old);
+    uint32_t* so = sn + m_new;
+    const uint32_t i = blockIdx.x * wpb + warp;
+    if (i >= a.n) return;
+    const uint32_t cn = a.cnew[i], co = a.cold[i];
+    for (uint32_t j = lane; j < cn; j += 32) sn[j] = a.fnew[size_t(i) * a.S + j];
+    for (uint32_t j = lane; j < co; j += 32) so[j] = a.fold[size_t(i) * a.P + j];
+    const uint32_t rnb = a.rn_off[i], rnm = a.rn_off[i + 1] - rnb;
+    const uint32_t rob = a.ro_off[i], rom = a.ro_off[i + 1] - rob;
+    uint32_t addn = min(rnm, a.S), addo = min(rom, a.S);
+    if (rnm <= a.S) {
+        for (uint32_t j = lane; j < rnm; j += 32) sn[cn + j] = a.rn_data[rnb + j];
+    }
+    if (rom <= a.S) {
+        for (uint32_t j = lane; j < rom; j += 32) so[co + j] = a.ro_data[rob + j];
+    }
+    if (lane == 0 && rnm > a.S)
+        sample_down_sorted(a.rn_data + rnb, rnm, a.S, substream(a.round_seed, 2 * uint64_t(i)), sn + cn);
+    if (lane == 1 && rom > a.S)
+        sample_down_sorted(a.ro_data + rob, rom, a.S, substream(a.round_seed, 2 * uint64_t(i) + 1), so + co);
+    __syncwarp();
+    const uint32_t un = warp_sort_unique_u32(sn, cn + addn, m_new);
+    const uint32_t uo = warp_sort_unique_u32(so, co + addo, m_old);
+    for (uint32_t j = lane; j < un; j += 32) a.gnew[size_t(i) * 2 * a.S + j] = sn[j];
+    for (uint32_t j = lane; j < uo; j += 32) a.gold[size_t(i) * (a.P + a.S) + j] = so[j];
+    if (lane == 0) {
+        a.gncnt[i] = un;
+        a.gocnt[i] = uo;
+        atomicAdd(a.join_rows, (unsigned long long)(un + uo));
+    }
+}
+
+// ------------------------------------------------------------------ join
+
+struct JoinArgs {
+    const float* x;
+    uint32_t n, ld, P, S, cap;
+    const uint32_t *gnew, *gold, *gncnt, *gocnt;
+    const uint64_t* thr;
+    uint32_t* ocnt;
+    uint64_t* obuf;
+    unsigned long long* comps;
+};
+
+__device__ __forceinline__ void offer(const JoinArgs& a, uint32_t owner, uint32_t cand, float d) {
+    const uint64_t key = make_key(d, cand);
+    if (key < a.thr[owner]) {
+        const uint32_t slot = atomicAdd(&a.ocnt[owner], 1u);
+        if (slot < a.cap) a.obuf[size_t(owner) * a.cap + slot] = key;
+    }
+}
+
+// graph_build.cpp:129-156: every new x new pair (a<b) and new x old pair
+// (l != j), offered both ways.  One warp per point; the shared row of the
+// pair (new[x]) is staged in shared memory.
+__global__ void join_kernel(JoinArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
+    const uint32_t wpb = blockDim.x / 32;
+    float* row = reinterpret_cast<float*>(smem) + size_t(warp) * a.ld;
+    const uint32_t i = blockIdx.x * wpb + warp;
+    if (i >= a.n) return;
+    const uint32_t A = a.gncnt[i], B = a.gocnt[i];
+    const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
+    const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
+    unsigned long long comps = 0;
+    for (uint32_t xi = 0; xi < A; ++xi) {
+        const uint32_t j = nw[xi];
+        __syncwarp();
+        for (uint32_t c = lane; c < a.ld; c += 32) row[c] = a.x[size_t(j) * a.ld + c];
+        __syncwarp();
+        const uint32_t tri = A - 1 - xi;
+        const uint32_t total = tri + B;
+        for (uint32_t t = lane; t < total; t += 32) {
+            const uint32_t k2 = t < tri ? nw[xi + 1 + t] : od[t - tri];
+            if (t >= tri && k2 == j) continue;
+            const float d = l2_exact_ldg(row, a.x + size_t(k2) * a.ld, a.ld);
+            ++comps;
+            offer(a, j, k2, d);
+            offer(a, k2, j, d);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
+    if (lane == 0 && comps) atomicAdd(a.comps, comps);
+}
+
+// ----------------------------------------------------------------- merge
+
+struct MergeArgs {
+    uint32_t n, P, cap;
+    uint64_t* keys;
+    uint8_t* flags;
+    uint32_t* sizes;
+    const uint32_t* ocnt;
+    const uint64_t* obuf;
+    unsigned long long* changes;
+};
+
+__device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t n, uint64_t v) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// New pool = top-P of (pool U offers); duplicates keep the pool's entry.
+__global__ void merge_kernel(MergeArgs a, uint32_t m) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
+    const uint32_t wpb = blockDim.x / 32;
+    uint64_t* so = reinterpret_cast<uint64_t*>(smem) + size_t(warp) * (m + 2 * a.P);
+    uint64_t* sp = so + m;        // pool keys (P)
+    uint64_t* sout = sp + a.P;    // result (P)
+    uint8_t* sflag = reinterpret_cast<uint8_t*>(reinterpret_cast<uint64_t*>(smem) + size_t(wpb) * (m + 2 * a.P)) +
+                     size_t(warp) * 2 * a.P;
+    uint8_t* soutf = sflag + a.P;
+    const uint32_t i = blockIdx.x * wpb + warp;
+    if (i >= a.n) return;
+    const uint32_t c = min(a.ocnt[i], a.cap);
+    if (c == 0) return;
+    const uint32_t sz = a.sizes[i];
+    uint64_t* pk = a.keys + size_t(i) * a.P;
+    uint8_t* pf = a.flags + size_t(i) * a.P;
+    for (uint32_t j = lane; j < a.P; j += 32) {
+        sp[j] = j < sz ? pk[j] : kEmptyKey;
+        sflag[j] = j < sz ? pf[j] : 0;
+    }
+    const uint64_t* ob = a.obuf + size_t(i) * a.cap;
+    for (uint32_t j = lane; j < m; j += 32) so[j] = j < c ? ob[j] : kEmptyKey;
+    __syncwarp();
+    warp_bitonic_sort(so, m);
+    // unique offers not already in the pool
+    uint32_t nu = 0;
+    for (uint32_t base = 0; base < c; base += 32) {
+        const uint32_t j = base + lane;
+        const uint64_t v = j < c ? so[j] : kEmptyKey;
+        bool keep = j < c && (j == 0 || so[j - 1] != v);
+        if (keep) {
+            const uint32_t p = lower_bound_u64(sp, sz, v);
+            keep = !(p < sz && sp[p] == v);
+        }
+        const uint32_t b = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) so[nu + __popc(b & ((1u << lane) - 1u))] = v;
+        nu += __popc(b);
+        __syncwarp();
+    }
+    // merge by ranks (no equal keys remain between the two sorted runs)
+    uint32_t added = 0;
+    for (uint32_t j = lane; j < sz; j += 32) {
+        const uint32_t r = j + lower_bound_u64(so, nu, sp[j]);
+        if (r < a.P) { sout[r] = sp[j]; soutf[r] = sflag[j]; }
+    }
+    for (uint32_t j = lane; j < nu; j += 32) {
+        const uint32_t r = j + lower_bound_u64(sp, sz, so[j]);
+        if (r < a.P) { sout[r] = so[j]; soutf[r] = 1; ++added; }
+    }
+    __syncwarp();
+    const uint32_t nsz = min(a.P, sz + nu);
+    for (uint32_t j = lane; j < a.P; j += 32) {
+        pk[j] = j < nsz ? sout[j] : kEmptyKey;
+        pf[j] = j < nsz ? soutf[j] : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) added += __shfl_xor_sync(0xffffffffu, added, o);
+    if (lane == 0) {
+        a.sizes[i] = nsz;
+        if (added) atomicAdd(a.changes, (unsigned long long)added);
+    }
+}
+
+// --------------------------------------------------------------- finalize
+
+// graph_build.cpp:357-365: pools smaller than k are topped up by scanning ids
+// in ascending order (tiny inputs only).  One warp per deficient point.
+__global__ void fill_sparse_kernel(const float* __restrict__ x, uint32_t n, uint32_t ld, uint32_t P,
+                                   uint32_t k, uint64_t* keys, uint8_t* flags, uint32_t* sizes,
+                                   unsigned long long* comps) {
+    const uint32_t lane = lane_id();
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= n) return;
+    uint32_t sz = sizes[i];
+    if (sz >= k) return;
+    uint64_t* pk = keys + size_t(i) * P;
+    uint8_t* pf = flags + size_t(i) * P;
+    const float* xi = x + size_t(i) * ld;
+    uint32_t added = 0;
+    for (uint32_t base = 0; base < n && sz < k; base += 32) {
+        const uint32_t j = base + lane;
+        bool ok = j < n && j != i;
+        for (uint32_t e = 0; ok && e < sz; ++e) ok = key_id(pk[e]) != j;
+        const uint32_t b = __ballot_sync(0xffffffffu, ok);
+        const uint32_t rank = __popc(b & ((1u << lane) - 1u));
+        const uint32_t need = k - sz;
+        uint64_t key = kEmptyKey;
+        if (ok && rank < need) key = make_key(l2_exact_ldg(xi, x + size_t(j) * ld, ld), j);
+        // insertion (sequential, rare path)
+        for (uint32_t l = 0; l < 32; ++l) {
+            const uint64_t kv = __shfl_sync(0xffffffffu, key, l);
+            if (kv == kEmptyKey) continue;
+            if (lane == 0) {
+                uint32_t p = sz;
+                while (p > 0 && pk[p - 1] > kv) { pk[p] = pk[p - 1]; pf[p] = pf[p - 1]; --p; }
+                pk[p] = kv;
+                pf[p] = 0;
+            }
+            ++sz;
+            ++added;
+            __syncwarp();
+        }
+    }
+    if (lane == 0) {
+        sizes[i] = sz;
+        atomicAdd(comps, (unsigned long long)added);
+    }
+}
+
+__global__ void finalize_kernel(const uint64_t* __restrict__ keys, uint32_t n, uint32_t P, uint32_t k,
+                                uint32_t* __restrict__ ids, float* __restrict__ dists) {
+    const size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (t >= size_t(n) * k) return;
+    const uint32_t i = uint32_t(t / k), j = uint32_t(t % k);
+    const uint64_t key = keys[size_t(i) * P + j];
+    ids[t] = key_id(key);
+    dists[t] = key_dist(key);
+}
+
+// graph_build.cpp:209-226: per-row hit counts (host sums them in row order).
+__global__ void topk_hits_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ sizes,
+                                 uint32_t P, uint32_t k, const uint32_t* __restrict__ gt, uint32_t gt_rows,
+                                 uint32_t gt_k, const uint32_t* __restrict__ rows, uint32_t* __restrict__ hits) {
+    const uint32_t lane = lane_id();
+    const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (r >= gt_rows) return;
+    const uint32_t i = rows ? rows[r] : r;
+    const uint32_t m = min(k, sizes[i]);
+    uint32_t h = 0;
+    for (uint32_t j = lane; j < m; j += 32) {
+        const uint32_t id = key_id(keys[size_t(i) * P + j]);
+        for (uint32_t g = 0; g < gt_k; ++g)
+            if (gt[size_t(r) * gt_k + g] == id) { ++h; break; }
+    }
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0) hits[r] = h;
+}
+
+__global__ void split_keys_kernel(const uint64_t* __restrict__ keys, size_t cnt, uint32_t* ids, float* dists) {
+    for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < cnt; t += size_t(gridDim.x) * blockDim.x) {
+        const uint64_t k = keys[t];
+        ids[t] = key_id(k);
+        dists[t] = key_dist(k);
+    }
+}
+
+// --------------------------------------------------------- host helpers
+
+uint32_t grid_for(size_t items, uint32_t per_block) {
+    return uint32_t(std::max<size_t>(1, std::min<size_t>((items + per_block - 1) / per_block, 1u << 30)));
+}
+
+void exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t n) {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n + 1, stream()));
+    DevBuf<unsigned char> t(tmp);
+    CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n + 1, stream()));
+    note_launch();
+}
+
+void segmented_sort(uint32_t* data, uint32_t total, const uint32_t* off, uint32_t n) {
+    if (total == 0) return;
+    DevBuf<uint32_t> out(total);
+    size_t tmp = 0;
+    CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, data, out.p, total, n, off, off + 1, stream()));
+    DevBuf<unsigned char> t(tmp);
+    CK(cub::DeviceSegmentedSort::SortKeys(t.p, tmp, data, out.p, total, n, off, off + 1, stream()));
+    note_launch();
+    CK(cudaMemcpyAsync(data, out.p, size_t(total) * 4, cudaMemcpyDeviceToDevice, stream()));
+}
+
+// Host copy of CSR lists built from fixed-width rows + counts.
+void csr_from_rows(const DevBuf<uint32_t>& rows, uint32_t width, const DevBuf<uint32_t>& cnt, uint32_t n,
+                   uint32_t* offsets, uint32_t* data) {
+    std::vector<uint32_t> c(n);
+    cnt.download(c.data(), n);
+    std::vector<uint32_t> r;
+    if (data) {
+        r.resize(size_t(n) * width);
+        rows.download(r.data(), r.size());
+    }
+    ssync();
+    uint32_t o = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        offsets[i] = o;
+        if (data) std::copy(r.begin() + size_t(i) * width, r.begin() + size_t(i) * width + c[i], data + o);
+        o += c[i];
+    }
+    offsets[n] = o;
+}
+
+}  // namespace
+}  // namespace annk
+
+
+// ------------------------------------------------------------------ host
+
+using namespace annk;
+
+namespace {
+
+constexpr uint32_t kMaxSample = 64;  // device sample_down keeps 2*S swap slots in registers
+
+void ensure_scratch(annk_state* s) {
+    const size_t n = s->n;
+    if (s->fnew.n == n * s->S && s->fold.n == n * s->P) return;
+    s->fnew.alloc(n * s->S);
+    s->fold.alloc(n * s->P);
+    s->cnew.alloc(n);
+    s->cold.alloc(n);
+    s->rn_cnt.alloc(n + 1);
+    s->ro_cnt.alloc(n + 1);
+    s->rn_off.alloc(n + 1);
+    s->ro_off.alloc(n + 1);
+    s->rn_cur.alloc(n);
+    s->ro_cur.alloc(n);
+    s->rn_data.alloc(std::max<size_t>(n * s->S, 1));
+    s->ro_data.alloc(std::max<size_t>(n * s->P, 1));
+    s->gnew.alloc(n * 2 * s->S);
+    s->gold.alloc(n * (s->P + s->S));
+    s->gncnt.alloc(n);
+    s->gocnt.alloc(n);
+    s->thr.alloc(n);
+    s->ocnt.alloc(n);
+}
+
+void do_rebuild(annk_state* s) {
+    ensure_scratch(s);
+    const uint32_t n = s->n;
+    s->rn_cnt.zero();
+    s->ro_cnt.zero();
+    SampleArgs a{n, s->P, s->S, s->keys.p, s->flags.p, s->sizes.p, s->fnew.p, s->fold.p,
+                 s->cnew.p, s->cold.p, s->rn_cnt.p, s->ro_cnt.p, s->thr.p};
+    LAUNCH(sample_kernel, grid_for(size_t(n) * 32, 256), 256, 0, a);
+    exclusive_scan(s->rn_cnt.p, s->rn_off.p, n);
+    exclusive_scan(s->ro_cnt.p, s->ro_off.p, n);
+    s->rn_cur.zero();
+    s->ro_cur.zero();
+    LAUNCH(reverse_scatter_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->S, s->fnew.p, s->cnew.p,
+           s->rn_off.p, s->rn_cur.p, s->rn_data.p);
+    LAUNCH(reverse_scatter_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->P, s->fold.p, s->cold.p,
+           s->ro_off.p, s->ro_cur.p, s->ro_data.p);
+    uint32_t tot[2];
+    CK(cudaMemcpyAsync(&tot[0], s->rn_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
+    CK(cudaMemcpyAsync(&tot[1], s->ro_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
+    ssync();
+    // reverse lists as sets in ascending id order (the reference pushes them in
+    // ascending owner order, graph_build.cpp:71-85)
+    segmented_sort(s->rn_data.p, tot[0], s->rn_off.p, n);
+    segmented_sort(s->ro_data.p, tot[1], s->ro_off.p, n);
+    s->stage = 1;
+}
+
+void do_union(annk_state* s) {
+    if (s->stage != 1) throw_invalid("union_reverse_lists: call rebuild_sample_lists first");
+    const uint32_t n = s->n;
+    const uint32_t m_new = next_pow2(2 * s->S), m_old = next_pow2(s->P + s->S);
+    DevBuf<unsigned long long> rows(1);
+    rows.zero();
+    UnionArgs a{n, s->P, s->S, substream(s->seed, s->iteration), s->fnew.p, s->fold.p, s->cnew.p, s->cold.p,
+                s->rn_off.p, s->rn_data.p, s->ro_off.p, s->ro_data.p, s->gnew.p, s->gold.p,
+                s->gncnt.p, s->gocnt.p, rows.p};
+    const uint32_t wpb = 4;
+    LAUNCH(union_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * (m_new + m_old) * 4, a, m_new, m_old);
+    unsigned long long h = 0;
+    rows.download(&h, 1);
+    ssync();
+    s->join_rows = h;
+    s->stage = 2;
+}
+
+uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
+    const uint32_t n = s->n;
+    if (s->offer_cap == 0) s->offer_cap = next_pow2(std::max(2 * s->P, 64u));
+    DevBuf<unsigned long long> counters(2);
+    size_t red_tmp = 0;
+    DevBuf<uint32_t> dmax(1);
+    CK(cub::DeviceReduce::Max(nullptr, red_tmp, s->ocnt.p, dmax.p, n, stream()));
+    DevBuf<unsigned char> red(red_tmp);
+    for (;;) {
+        if (s->obuf.n != size_t(n) * s->offer_cap) s->obuf.alloc(size_t(n) * s->offer_cap);
+        s->ocnt.zero();
+        counters.zero();
+        JoinArgs ja{ds->data.p, n, ds->ld, s->P, s->S, s->offer_cap, s->gnew.p, s->gold.p, s->gncnt.p,
+                    s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p};
+        const uint32_t wpb = 8;
+        LAUNCH(join_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
+        CK(cub::DeviceReduce::Max(red.p, red_tmp, s->ocnt.p, dmax.p, n, stream()));
+        note_launch();
+        uint32_t mx = 0;
+        dmax.download(&mx, 1);
+        ssync();
+        if (mx <= s->offer_cap) break;
+        s->offer_cap = next_pow2(mx);  // buffers too small: grow and redo (pools untouched so far)
+    }
+    unsigned long long comps = 0;
+    counters.download(&comps, 1);
+    const uint32_t m = next_pow2(s->offer_cap);
+    const size_t per_warp = size_t(m + 2 * s->P) * 8 + 2 * s->P;
+    uint32_t wpb = uint32_t(std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per_warp)));
+    const size_t smem = wpb * per_warp;
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    MergeArgs ma{n, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p, counters.p + 1};
+    LAUNCH(merge_kernel, (n + wpb - 1) / wpb, wpb * 32, smem, ma, m);
+    unsigned long long changes = 0;
+    CK(cudaMemcpyAsync(&changes, counters.p + 1, 8, cudaMemcpyDeviceToHost, stream()));
+    ssync();
+    s->dist_comps += comps;
+    s->iteration += 1;
+    s->last_changes = changes;
+    return changes;
+}
+
+annk_state* new_state(uint32_t n, uint32_t k, uint32_t P, uint32_t S, uint64_t seed) {
+    // graph_build.cpp:18-35 make_state
+    if (n < 2) throw_invalid("graph build: need at least 2 points");
+    if (k < 1) throw_invalid("graph build: k must be >= 1");
+    if (P < k) throw_invalid("graph build: pool_cap must be >= k");
+    if (S < 1) throw_invalid("graph build: sample_cap must be >= 1");
+    if (S > kMaxSample) throw_invalid("graph build: sample_cap > 64 is not supported on the device path");
+    auto* s = new annk_state;
+    s->n = n;
+    s->k = k;
+    s->P = P;
+    s->S = S;
+    s->seed = seed;
+    s->keys.alloc(size_t(n) * P);
+    s->flags.alloc(size_t(n) * P);
+    s->sizes.alloc(n);
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int annk_init_graph(const annk_dataset* ds, const annk_forest* fc, uint32_t k, uint32_t conquer_depth,
+                    uint32_t pool_cap, uint32_t sample_cap, uint64_t seed, annk_state** out) {
+    return abi([&] {
+        if (!ds || !fc || !out) throw_invalid("init_graph: null argument");
+        if (fc->n != ds->n || fc->dim != ds->dim)
+            throw_invalid("init_graph: forest was built over different data");
+        annk_forest* f = const_cast<annk_forest*>(fc);
+        std::unique_ptr<annk_state> s(new_state(ds->n, k, pool_cap, sample_cap, seed));
+        forest_ensure_links(f);
+        uint32_t max_depth = 0;
+        for (const auto& t : f->trees) max_depth = std::max(max_depth, t.max_depth);
+        const uint32_t n = ds->n;
+        DevBuf<unsigned long long> comps(1);
+        comps.zero();
+        DevBuf<uint32_t> overflow(size_t(n) + 1);
+        CK(cudaMemsetAsync(overflow.p, 0, 4, stream()));
+        InitArgs a{ds->data.p, n, ds->ld, f->n_trees, conquer_depth, pool_cap, f->views.p,
+                   s->keys.p, s->flags.p, s->sizes.p, comps.p, overflow.p};
+        const uint32_t sib_full = f->n_trees * (max_depth + 1);
+        const uint32_t sib_cap = std::min<uint32_t>(sib_full, 512);
+        const size_t per_warp = (size_t(kInitCap) * 12 + size_t(ds->ld) * 4 + size_t(sib_cap) * 8 + 16 + 15) &
+                                ~size_t(15);
+        const size_t smem = per_warp * kInitWarps;
+        CK(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const uint32_t grid = std::min<uint32_t>((n + kInitWarps - 1) / kInitWarps, uint32_t(num_sms()) * 16);
+        LAUNCH(init_kernel, grid, kInitWarps * 32, smem, a, sib_cap);
+        uint32_t n_over = 0;
+        overflow.download(&n_over, 1);
+        ssync();
+        if (n_over) {
+            const uint32_t cap = next_pow2(f->n_trees * (max_depth + 1) * f->leaf_cap);
+            const uint32_t blocks = std::min<uint32_t>(n_over, 1024);
+            DevBuf<uint32_t> gcand(size_t(blocks) * cap), gsib(size_t(blocks) * 2 * sib_full);
+            DevBuf<uint64_t> gkeys(size_t(blocks) * cap);
+            DevBuf<float> gq(size_t(blocks) * ds->ld);
+            LAUNCH(init_overflow_kernel, blocks, 32, 0, a, overflow.p + 1, n_over, cap, sib_full, gcand.p,
+                   gkeys.p, gq.p, gsib.p);
+        }
+        unsigned long long c = 0;
+        comps.download(&c, 1);
+        ssync();
+        s->dist_comps = c;
+        *out = s.release();
+    });
+}
+
+int annk_state_import(uint32_t n, uint32_t k, uint32_t pool_cap, uint32_t sample_cap, uint64_t seed,
+                      uint32_t iteration, uint64_t dist_comps, const uint32_t* sizes, const uint32_t* ids,
+                      const float* dists, const uint8_t* flags, annk_state** out) {
+    return abi([&] {
+        std::unique_ptr<annk_state> s(new_state(n, k, pool_cap, sample_cap, seed));
+        s->iteration = iteration;
+        s->dist_comps = dist_comps;
+        std::vector<uint64_t> keys(size_t(n) * pool_cap, kEmptyKey);
+        std::vector<uint8_t> fl(size_t(n) * pool_cap, 0);
+        std::vector<uint32_t> sz(n);
+        for (uint32_t i = 0; i < n; ++i) {
+            // reference NeighborPool::insert semantics (sorted, dedup, capped)
+            std::vector<std::pair<uint64_t, uint8_t>> row;
+            for (uint32_t j = 0; j < std::min(sizes[i], pool_cap); ++j) {
+                const size_t o = size_t(i) * pool_cap + j;
+                if (ids[o] >= n) throw_range("state_import: id out of range");
+                row.emplace_back(make_key(dists[o], ids[o]), flags[o]);
+            }
+            std::stable_sort(row.begin(), row.end(), [](auto& x, auto& y) { return x.first < y.first; });
+            row.erase(std::unique(row.begin(), row.end(), [](auto& x, auto& y) { return x.first == y.first; }),
+                      row.end());
+            if (row.size() > pool_cap) row.resize(pool_cap);
+            sz[i] = uint32_t(row.size());
+            for (size_t j = 0; j < row.size(); ++j) {
+                keys[size_t(i) * pool_cap + j] = row[j].first;
+                fl[size_t(i) * pool_cap + j] = row[j].second;
+            }
+        }
+        s->keys.upload(keys.data(), keys.size());
+        s->flags.upload(fl.data(), fl.size());
+        s->sizes.upload(sz.data(), n);
+        ssync();
+        *out = s.release();
+    });
+}
+
+int annk_state_destroy(annk_state* s) {
+    return abi([&] { delete s; });
+}
+
+int annk_state_meta(const annk_state* s, uint64_t* meta) {
+    return abi([&] {
+        meta[0] = s->n;
+        meta[1] = s->k;
+        meta[2] = s->P;
+        meta[3] = s->S;
+        meta[4] = s->seed;
+        meta[5] = s->iteration;
+        meta[6] = s->dist_comps;
+        meta[7] = s->last_changes;
+    });
+}
+
+int annk_state_export(const annk_state* s, uint32_t* sizes, uint32_t* ids, float* dists, uint8_t* flags) {
+    return abi([&] {
+        const size_t cnt = size_t(s->n) * s->P;
+        if (sizes) s->sizes.download(sizes, s->n);
+        if (flags) s->flags.download(flags, cnt);
+        if (ids || dists) {
+            DevBuf<uint32_t> di(cnt);
+            DevBuf<float> dd(cnt);
+            LAUNCH(split_keys_kernel, grid_for(cnt, 256), 256, 0, s->keys.p, cnt, di.p, dd.p);
+            if (ids) di.download(ids, cnt);
+            if (dists) dd.download(dists, cnt);
+            ssync();
+        }
+        ssync();
+    });
+}
+
+int annk_state_lists(const annk_state* s, int which, uint32_t* offsets, uint32_t* data) {
+    return abi([&] {
+        if (which < 0 || which > 3) throw_invalid("state_lists: which must be 0..3");
+        const uint32_t n = s->n;
+        if (s->stage == 0) {
+            for (uint32_t i = 0; i <= n; ++i) offsets[i] = 0;
+            return;
+        }
+        if (which == 0) {
+            if (s->stage == 2) csr_from_rows(s->gnew, 2 * s->S, s->gncnt, n, offsets, data);
+            else csr_from_rows(s->fnew, s->S, s->cnew, n, offsets, data);
+        } else if (which == 1) {
+            if (s->stage == 2) csr_from_rows(s->gold, s->P + s->S, s->gocnt, n, offsets, data);
+            else csr_from_rows(s->fold, s->P, s->cold, n, offsets, data);
+        } else {
+            const DevBuf<uint32_t>& off = which == 2 ? s->rn_off : s->ro_off;
+            const DevBuf<uint32_t>& dat = which == 2 ? s->rn_data : s->ro_data;
+            off.download(offsets, n + 1);
+            ssync();
+            if (data && offsets[n]) dat.download(data, offsets[n]);
+            ssync();
+        }
+    });
+}
+
+int annk_rebuild_sample_lists(annk_state* s) {
+    return abi([&] { do_rebuild(s); });
+}
+
+int annk_union_reverse_lists(annk_state* s) {
+    return abi([&] { do_union(s); });
+}
+
+int annk_nn_descent_iteration(annk_state* s, const annk_dataset* ds, uint64_t* changes) {
+    return abi([&] {
+        if (!s || !ds || ds->n != s->n) throw_invalid("nn_descent_iteration: state/dataset mismatch");
+        do_rebuild(s);
+        do_union(s);
+        const uint64_t c = do_join_merge(s, ds);
+        if (changes) *changes = c;
+    });
+}
+
+int annk_refine_nn_descent(annk_state* s, const annk_dataset* ds, uint32_t max_iters, double min_change_rate,
+                           uint32_t* iters_run) {
+    return abi([&] {
+        if (!s || !ds || ds->n != s->n) throw_invalid("refine_nn_descent: state/dataset mismatch");
+        const double threshold = min_change_rate * double(s->n) * double(s->P);
+        uint32_t it = 0;
+        while (it < max_iters) {
+            do_rebuild(s);
+            do_union(s);
+            const uint64_t c = do_join_merge(s, ds);
+            ++it;
+            if (double(c) < threshold) break;
+        }
+        if (iters_run) *iters_run = it;
+    });
+}
+
+int annk_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* ids, float* dists) {
+    return abi([&] {
+        const uint32_t n = s->n;
+        if (n < 2 || n - 1 < k) throw_invalid("finalize: need n-1 >= k");
+        if (k > s->P) throw_invalid("finalize: k exceeds pool capacity");
+        if (!ds || ds->n != n) throw_invalid("finalize: dataset mismatch");
+        DevBuf<unsigned long long> comps(1);
+        comps.zero();
+        LAUNCH(fill_sparse_kernel, grid_for(size_t(n) * 32, 256), 256, 0, ds->data.p, n, ds->ld, s->P, k,
+               s->keys.p, s->flags.p, s->sizes.p, comps.p);
+        DevBuf<uint32_t> di(size_t(n) * k);
+        DevBuf<float> dd(size_t(n) * k);
+        LAUNCH(finalize_kernel, grid_for(size_t(n) * k, 256), 256, 0, s->keys.p, n, s->P, k, di.p, dd.p);
+        unsigned long long c = 0;
+        comps.download(&c, 1);
+        if (ids) di.download(ids, size_t(n) * k);
+        if (dists) dd.download(dists, size_t(n) * k);
+        ssync();
+        s->dist_comps += c;
+    });
+}
+
+int annk_pool_topk_accuracy(const annk_state* s, const uint32_t* gt_ids, uint32_t gt_rows, uint32_t gt_k,
+                            const uint32_t* rows, double* acc) {
+    return abi([&] {
+        if (!rows && gt_rows != s->n) throw_invalid("accuracy hook: ground truth shape");
+        if (gt_rows == 0 || gt_k == 0) throw_invalid("accuracy hook: empty ground truth");
+        DevBuf<uint32_t> dgt(size_t(gt_rows) * gt_k), drows(rows ? gt_rows : 0), hits(gt_rows);
+        dgt.upload(gt_ids, size_t(gt_rows) * gt_k);
+        if (rows) {
+            for (uint32_t r = 0; r < gt_rows; ++r)
+                if (rows[r] >= s->n) throw_range("accuracy hook: row out of range");
+            drows.upload(rows, gt_rows);
+        }
+        LAUNCH(topk_hits_kernel, grid_for(size_t(gt_rows) * 32, 256), 256, 0, s->keys.p, s->sizes.p, s->P, s->k,
+               dgt.p, gt_rows, gt_k, rows ? drows.p : nullptr, hits.p);
+        std::vector<uint32_t> h(gt_rows);
+        hits.download(h.data(), gt_rows);
+        ssync();
+        double sum = 0.0;  // graph_build.cpp:213-225 summation order
+        for (uint32_t r = 0; r < gt_rows; ++r) sum += double(h[r]) / double(gt_k);
+        *acc = sum / gt_rows;
+    });
+}
+
+int annk_state_join_rows(const annk_state* s, uint64_t* rows) {
+    return abi([&] { *rows = s->join_rows; });
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// internal.cuh — device-resident object layouts shared by the kernels.
+#pragma once
+
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+// Tree node as the kernels see it: 16 bytes, one sector per descent hop.
+// (Reference KdNode, kd_forest.hpp:18-27; depth and even_split live in
+// side arrays because descents never read them.)
+struct KdNodeDev {
+    uint32_t split_dim;  // annk::kLeaf => leaf
+    float split_val;
+    uint32_t left;   // internal: left child; leaf: range start in point_index
+    uint32_t right;  // internal: right child; leaf: range end
+};
+
+struct annk_dataset {
+    uint32_t n = 0, dim = 0, ld = 0;  // ld = padded row stride (floats), multiple of 4
+    annk::DevBuf<float> data;         // n x ld, zero padded
+};
+
+struct TreeDev {
+    annk::DevBuf<KdNodeDev> nodes;
+    annk::DevBuf<uint32_t> depth;
+    annk::DevBuf<uint8_t> even;
+    annk::DevBuf<uint32_t> pidx;    // point_index permutation (n)
+    annk::DevBuf<uint32_t> parent;  // lazily built (init_graph)
+    annk::DevBuf<uint32_t> owner;   // lazily built: leaf owning each point
+    uint32_t num_nodes = 0, root = 0, leaf_count = 0, max_depth = 0;
+};
+
+// Plain view passed to kernels that walk several trees.
+struct TreeView {
+    const KdNodeDev* nodes;
+    const uint32_t* depth;
+    const uint32_t* pidx;
+    const uint32_t* parent;
+    const uint32_t* owner;
+    uint32_t root, num_nodes, leaf_count, max_depth;
+};
+
+struct annk_forest {
+    uint32_t n_trees = 0, n = 0, dim = 0, leaf_cap = 0;
+    uint64_t seed = 0;
+    std::vector<TreeDev> trees;
+    annk::DevBuf<TreeView> views;  // device copy of per-tree views
+    bool links_ready = false;
+};
+
+struct annk_state {
+    uint32_t n = 0, k = 0, P = 0, S = 0;
+    uint64_t seed = 0;
+    uint32_t iteration = 0;
+    uint64_t dist_comps = 0, last_changes = 0;
+    annk::DevBuf<uint64_t> keys;   // n x P ascending; kEmptyKey beyond size
+    annk::DevBuf<uint8_t> flags;   // n x P flag_new
+    annk::DevBuf<uint32_t> sizes;  // n
+    // sampling-step scratch, reused across iterations
+    annk::DevBuf<uint32_t> fnew, fold, cnew, cold;  // forward lists, pool order (n x S, n x P)
+    annk::DevBuf<uint32_t> rn_cnt, ro_cnt, rn_off, ro_off, rn_cur, ro_cur, rn_data, ro_data;
+    annk::DevBuf<uint32_t> gnew, gold, gncnt, gocnt;  // unioned lists, sorted (n x 2S, n x (P+S))
+    annk::DevBuf<uint64_t> thr;                       // start-of-round pool tail per point
+    annk::DevBuf<uint32_t> ocnt;                      // join offer counts
+    annk::DevBuf<uint64_t> obuf;                      // n x offer_cap offer keys
+    int stage = 0;  // 0 none, 1 after rebuild_sample_lists, 2 after union_reverse_lists
+    uint64_t join_rows = 0;
+    uint32_t offer_cap = 0;
+};
+
+struct annk_searcher {
+    const annk_dataset* base = nullptr;
+    const annk_forest* forest = nullptr;
+    uint32_t gn = 0, gk = 0;
+    annk::DevBuf<uint32_t> graph;  // gn x gk
+};
+
+namespace annk {
+void set_error(const std::string& m);
+
+// Runs f at the C-ABI boundary: exceptions become status codes + message.
+template <class F>
+int abi(F&& f) {
+    try {
+        f();
+        return kOk;
+    } catch (const Error& e) {
+        set_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return kOutOfMemory;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return kInternal;
+    }
+}
+
+void forest_ensure_links(annk_forest* f);
+void forest_upload_views(annk_forest* f);
+// exact top-k helper used by brute force and accuracy scoring
+void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
+                        const uint32_t* self_rows, uint32_t k, uint64_t* out_keys);
+}  // namespace annk

@@ -1,0 +1,198 @@
+// runtime.cu — library state, error plumbing, dataset handles, host-side
+// input generators.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/annkit_b200.h"
+#include "internal.cuh"
+
+namespace annk {
+
+namespace {
+thread_local std::string g_err;
+int g_device = 0;
+cudaStream_t g_stream = nullptr;
+unsigned long long g_launches = 0;
+int g_sms = 0, g_smem_optin = 0;
+
+void init_runtime() {
+    if (g_stream) return;
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (count == 0) throw Error(kCudaError, "no CUDA device");
+    CK(cudaSetDevice(g_device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, g_device));
+    if (prop.major < 10)
+        throw Error(kCudaError, std::string("annkit_b200 needs an sm_100 device, found ") + prop.name);
+    g_sms = prop.multiProcessorCount;
+    g_smem_optin = int(prop.sharedMemPerBlockOptin);
+    CK(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, g_device));
+    uint64_t thresh = ~0ull;  // keep freed blocks cached across calls
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+}
+}  // namespace
+
+cudaStream_t stream() {
+    init_runtime();
+    return g_stream;
+}
+void note_launch() { ++g_launches; }
+int num_sms() {
+    init_runtime();
+    return g_sms;
+}
+int max_smem_optin() {
+    init_runtime();
+    return g_smem_optin;
+}
+
+void set_error(const std::string& m) { g_err = m; }
+
+}  // namespace annk
+
+using namespace annk;
+
+// Upload with zero padding to the ld stride.
+static void upload_rows(annk_dataset* ds, const float* host) {
+    const size_t n = ds->n, dim = ds->dim, ld = ds->ld;
+    ds->data.alloc(std::max<size_t>(n * ld, 1));
+    if (n == 0) return;
+    if (ld == dim) {
+        ds->data.upload(host, n * dim);
+    } else {
+        CK(cudaMemsetAsync(ds->data.p, 0, n * ld * sizeof(float), stream()));
+        CK(cudaMemcpy2DAsync(ds->data.p, ld * sizeof(float), host, dim * sizeof(float),
+                             dim * sizeof(float), n, cudaMemcpyHostToDevice, stream()));
+    }
+}
+
+extern "C" {
+
+const char* annk_last_error(void) { return g_err.c_str(); }
+const char* annk_version(void) { return "annkit_b200 0.1 (sm_100a)"; }
+
+int annk_set_device(int device) {
+    return abi([&] {
+        if (g_stream) {
+            if (device != g_device) throw_invalid("annk_set_device: device already initialised");
+            return;
+        }
+        g_device = device;
+        init_runtime();
+    });
+}
+uint64_t annk_stream(void) {
+    uint64_t s = 0;
+    abi([&] { s = reinterpret_cast<uint64_t>(stream()); });
+    return s;
+}
+uint64_t annk_launch_count(void) { return g_launches; }
+int annk_synchronize(void) {
+    return abi([&] { ssync(); });
+}
+
+int annk_dataset_create(const float* host, uint32_t n, uint32_t dim, annk_dataset** out) {
+    return abi([&] {
+        if (!out) throw_invalid("dataset_create: null out");
+        if (dim < 1) throw_invalid("dataset_create: dim must be >= 1");
+        if (n > 0 && !host) throw_invalid("dataset_create: null data");
+        for (size_t i = 0; i < size_t(n) * dim; ++i)
+            if (!std::isfinite(host[i])) throw_invalid("dataset_create: non-finite value");
+        auto* ds = new annk_dataset;
+        ds->n = n;
+        ds->dim = dim;
+        ds->ld = (dim + 3) & ~3u;
+        try {
+            upload_rows(ds, host);
+            ssync();
+        } catch (...) {
+            delete ds;
+            throw;
+        }
+        *out = ds;
+    });
+}
+int annk_dataset_destroy(annk_dataset* ds) {
+    return abi([&] { delete ds; });
+}
+int annk_dataset_shape(const annk_dataset* ds, uint32_t* n, uint32_t* dim) {
+    return abi([&] {
+        *n = ds->n;
+        *dim = ds->dim;
+    });
+}
+
+// dataset.cpp:201-214: std::mt19937_64(seed), top 24 bits * 2^-24.
+int annk_gen_synthetic(uint32_t n, uint32_t dim, uint64_t seed, float* out) {
+    return abi([&] {
+        if (dim < 1) throw_invalid("gen_synthetic: dim must be >= 1");
+        uint64_t mt[312];
+        mt[0] = seed;
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
+        int idx = 312;
+        for (size_t i = 0; i < size_t(n) * dim; ++i) {
+            if (idx == 312) {
+                for (int j = 0; j < 312; ++j) mt[j] = mt_twist(mt[j], mt[(j + 1) % 312], mt[(j + 156) % 312]);
+                idx = 0;
+            }
+            out[i] = float(uint32_t(mt_temper(mt[idx++]) >> 40)) * 0x1p-24f;
+        }
+    });
+}
+
+// Seeded Gaussian mixture.  Counter-based so
+// any thread split produces the same bytes:
+//   u(s, j)   = (mix64(s + j) >> 11) * 2^-53
+//   center[c][j] = lo + (hi - lo) * u(substream(seed, 0), c*dim + j)
+//   point i of stream sid: ps = substream(substream(seed, sid), i),
+//     c = mix64(ps) % n_centers, z_j = sqrt(-2 ln(1-u(ps,1+2j))) cos(2 pi u(ps,2+2j)),
+//     v = clip(center[c][j] + sd * z_j), optionally nearbyint.
+int annk_gen_mixture(uint32_t n, uint32_t dim, uint32_t n_centers, float center_lo,
+                     float center_hi, float sd, float clip_lo, float clip_hi, int round_to_int,
+                     uint64_t seed, uint32_t stream_id, float* out) {
+    return abi([&] {
+        if (dim < 1 || n_centers < 1) throw_invalid("gen_mixture: dim and n_centers must be >= 1");
+        auto u = [](uint64_t s, uint64_t j) { return double(mix64(s + j) >> 11) * 0x1p-53; };
+        std::vector<double> centers(size_t(n_centers) * dim);
+        const uint64_t s0 = substream(seed, 0);
+        for (size_t i = 0; i < centers.size(); ++i)
+            centers[i] = double(center_lo) + (double(center_hi) - double(center_lo)) * u(s0, i);
+        const uint64_t ss = substream(seed, stream_id);
+        unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const uint32_t workers = std::min<uint32_t>(hw, std::max<uint32_t>(1, n / 4096));
+        auto work = [&](uint32_t b, uint32_t e) {
+            const double two_pi = 6.283185307179586476925286766559;
+            for (uint32_t i = b; i < e; ++i) {
+                const uint64_t ps = substream(ss, i);
+                const uint32_t c = uint32_t(mix64(ps) % n_centers);
+                for (uint32_t j = 0; j < dim; ++j) {
+                    const double u1 = u(ps, 1 + 2ull * j), u2 = u(ps, 2 + 2ull * j);
+                    const double z = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(two_pi * u2);
+                    double v = centers[size_t(c) * dim + j] + double(sd) * z;
+                    v = std::min(std::max(v, double(clip_lo)), double(clip_hi));
+                    if (round_to_int) v = std::nearbyint(v);
+                    out[size_t(i) * dim + j] = float(v);
+                }
+            }
+        };
+        if (workers <= 1) {
+            work(0, n);
+        } else {
+            std::vector<std::thread> th;
+            const uint32_t chunk = (n + workers - 1) / workers;
+            for (uint32_t w = 0; w < workers; ++w) {
+                const uint32_t b = w * chunk, e = std::min(n, b + chunk);
+                if (b < e) th.emplace_back(work, b, e);
+            }
+            for (auto& t : th) t.join();
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,549 @@
+// search.cu — batched tree-seeded graph search (reference: proj/src/search.cpp).
+//
+// One CTA per query (persistent over the batch).  Per query:
+//   1. seeding (search.cpp:121-151): each of the first n_trees threads runs
+//      best-bin-first on its tree (kd_forest.cpp:276-305, heap in global
+//      scratch); the leaves' points are visited in parallel.  A per-slot
+//      visited bitmap (HBM) plays the reference's epoch-stamped visit table;
+//      every fresh id costs one exact distance, so dist_comps matches the
+//      reference exactly.  Seeds are sorted by (dist, id); the first E form the
+//      pool, the rest are kept as the "reserve" (they may re-enter later with
+//      their cached distance, search.cpp:56-63,79-82).
+//   2. expansion rounds (search.cpp:65-93): the unchecked pool members are
+//      snapshotted and marked checked; their graph rows are visited in
+//      parallel; every candidate that beats the pool's start-of-round tail is
+//      buffered in shared memory and merged (sort, unique, keep P).  The result
+//      is top-P of (pool U buffer), i.e. the reference's sort+unique+truncate.
+//   3. fallback scan (search.cpp:95-106) when fewer than k_return remain.
+#include <algorithm>
+
+#include "../../include/annkit_b200.h"
+#include "internal.cuh"
+
+namespace annk {
+namespace {
+
+constexpr uint32_t kThreads = 256;
+constexpr uint32_t kBuf = 2048;
+
+struct HeapEnt {
+    double cost;
+    uint32_t node;
+    uint32_t pad;
+};
+__device__ __forceinline__ bool hless(const HeapEnt& x, const HeapEnt& y) {
+    return x.cost != y.cost ? x.cost < y.cost : x.node < y.node;
+}
+
+struct SearchArgs {
+    const float* x;
+    uint32_t n, ld;
+    const float* q;
+    uint32_t nq;
+    const TreeView* trees;
+    uint32_t nt, n_node, leaf_cap;
+    const uint32_t* graph;
+    uint32_t gk;
+    uint32_t k_return, P, E, iters;
+    int random_init;
+    uint32_t rcount;
+    uint64_t seed;
+    uint32_t seed_cap;   // pow2 >= max seed points
+    // per-slot scratch
+    uint32_t* bitmap;    // slots x words
+    uint32_t words;
+    uint32_t* vlist;     // slots x vcap
+    uint32_t vcap;
+    HeapEnt* heaps;      // slots x nt x hcap
+    uint32_t hcap;
+    uint32_t* leaves;    // slots x nt x n_node
+    uint64_t* mtstate;   // slots x 312 (random init)
+    uint64_t* out_keys;  // nq x k_return
+    uint64_t* stats;     // nq x 4
+};
+
+struct Smem {
+    uint64_t* pool;     // P
+    uint8_t* checked;   // P
+    uint64_t* seeds;    // seed_cap (later: reserve, swapped keys)
+    uint64_t* buf;      // kBuf
+    uint64_t* tmp;      // P
+    uint8_t* tmpc;      // P
+    uint32_t* expand;   // P
+    uint32_t* scan;     // kThreads/32 + 1
+    float* q;           // ld
+    uint32_t* ctr;      // [0] pool size, [1] buf count, [2] visited count, [3] seeds, [4] reserve size,
+                        // [5] expand count, [6] leaves visited, [7] hops
+};
+
+__device__ __forceinline__ uint32_t lower_bound64(const uint64_t* a, uint32_t n, uint64_t v) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Visit id: returns true if fresh (this thread owns its distance).
+__device__ __forceinline__ bool mark_visited(const SearchArgs& a, uint32_t slot, Smem& s, uint32_t id) {
+    uint32_t* bm = a.bitmap + size_t(slot) * a.words;
+    DCHK(id < a.n);
+    const uint32_t bit = 1u << (id & 31);
+    const uint32_t old = atomicOr(&bm[id >> 5], bit);
+    if (old & bit) return false;
+    const uint32_t v = atomicAdd(&s.ctr[2], 1u);
+    if (v < a.vcap) a.vlist[size_t(slot) * a.vcap + v] = id;
+    return true;
+}
+
+__device__ __forceinline__ float qdist(const SearchArgs& a, const Smem& s, uint32_t id) {
+    DCHK(id < a.n);
+    return l2_exact_ldg(s.q, a.x + size_t(id) * a.ld, a.ld);
+}
+
+// Block exclusive scan of one flag per thread; returns prefix, total in *tot.
+__device__ __forceinline__ uint32_t block_scan(Smem& s, bool f, uint32_t* tot) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t b = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s.scan[warp] = __popc(b);
+    __syncthreads();
+    uint32_t pre = 0, all = 0;
+    for (uint32_t w = 0; w < kThreads / 32; ++w) {
+        const uint32_t c = s.scan[w];
+        if (w < warp) pre += c;
+        all += c;
+    }
+    __syncthreads();
+    *tot = all;
+    return pre + __popc(b & ((1u << lane) - 1u));
+}
+
+// pool := top-P(pool U buf), dedup by key (pool entry wins; buffer entries unchecked).
+__device__ void merge_buffer(const SearchArgs& a, Smem& s) {
+    __syncthreads();
+    const uint32_t c = s.ctr[1];
+    if (c == 0) return;
+    const uint32_t m = next_pow2(c);
+    DCHK(m <= kBuf);
+    for (uint32_t j = c + threadIdx.x; j < m; j += kThreads) s.buf[j] = kEmptyKey;
+    __syncthreads();
+    block_bitonic_sort(s.buf, m);
+    const uint32_t ps = s.ctr[0];
+    // unique and not already pooled, compacted in order
+    uint32_t nu = 0;
+    for (uint32_t base = 0; base < c; base += kThreads) {
+        const uint32_t j = base + threadIdx.x;
+        uint64_t v = kEmptyKey;
+        bool keep = false;
+        if (j < c) {
+            v = s.buf[j];
+            keep = j == 0 || s.buf[j - 1] != v;
+            if (keep) {
+                const uint32_t p = lower_bound64(s.pool, ps, v);
+                keep = !(p < ps && s.pool[p] == v);
+            }
+        }
+        uint32_t tot;
+        const uint32_t pos = block_scan(s, keep, &tot);
+        __syncthreads();
+        if (keep) s.buf[nu + pos] = v;  // nu + pos <= j: in-place compaction is safe after the barrier
+        nu += tot;
+        __syncthreads();
+    }
+    for (uint32_t j = threadIdx.x; j < ps; j += kThreads) {
+        const uint32_t r = j + lower_bound64(s.buf, nu, s.pool[j]);
+        if (r < a.P) { s.tmp[r] = s.pool[j]; s.tmpc[r] = s.checked[j]; }
+    }
+    for (uint32_t j = threadIdx.x; j < nu; j += kThreads) {
+        const uint32_t r = j + lower_bound64(s.pool, ps, s.buf[j]);
+        if (r < a.P) { s.tmp[r] = s.buf[j]; s.tmpc[r] = 0; }
+    }
+    __syncthreads();
+    const uint32_t nps = min(a.P, ps + nu);
+    for (uint32_t j = threadIdx.x; j < nps; j += kThreads) {
+        s.pool[j] = s.tmp[j];
+        s.checked[j] = s.tmpc[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s.ctr[0] = nps;
+        s.ctr[1] = 0;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t tail_key(const SearchArgs& a, const Smem& s) {
+    return s.ctr[0] == a.P ? s.pool[a.P - 1] : kEmptyKey;
+}
+
+__device__ __forceinline__ void push_buf(Smem& s, uint64_t key) {
+    const uint32_t slot = atomicAdd(&s.ctr[1], 1u);
+    DCHK(slot < kBuf);
+    s.buf[slot] = key;
+}
+
+__global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
+    extern __shared__ __align__(16) unsigned char raw[];
+    Smem s;
+    {
+        unsigned char* p = raw;
+        s.q = reinterpret_cast<float*>(p); p += size_t(a.ld) * 4;  // first: float4 loads need 16 B alignment
+        s.pool = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
+        s.tmp = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
+        s.seeds = reinterpret_cast<uint64_t*>(p); p += size_t(a.seed_cap) * 8;
+        s.buf = reinterpret_cast<uint64_t*>(p); p += size_t(kBuf) * 8;
+        s.expand = reinterpret_cast<uint32_t*>(p); p += size_t(a.P) * 4;
+        s.scan = reinterpret_cast<uint32_t*>(p); p += 64;
+        s.ctr = reinterpret_cast<uint32_t*>(p); p += 64;
+        s.checked = p; p += a.P;
+        s.tmpc = p;
+    }
+    const uint32_t slot = blockIdx.x, tid = threadIdx.x;
+    for (uint32_t qi = blockIdx.x; qi < a.nq; qi += gridDim.x) {
+        for (uint32_t j = tid; j < a.ld; j += kThreads) s.q[j] = a.q[size_t(qi) * a.ld + j];
+        if (tid < 16) s.ctr[tid] = 0;
+        __syncthreads();
+        // ------------------------------------------------ seeding
+        if (!a.random_init) {
+            if (tid < a.nt) {
+                const TreeView tv = a.trees[tid];
+                HeapEnt* h = a.heaps + (size_t(slot) * a.nt + tid) * a.hcap;
+                uint32_t* out = a.leaves + (size_t(slot) * a.nt + tid) * a.n_node;
+                const uint32_t want = min(a.n_node, tv.leaf_count);
+                uint32_t hn = 0, cnt = 0;
+                uint32_t nd = tv.root;
+                double cost = 0.0;
+                if (want > 0) {
+                    for (;;) {
+                        for (KdNodeDev x = tv.nodes[nd]; x.split_dim != kLeaf; x = tv.nodes[nd]) {
+                            const double diff = double(s.q[x.split_dim]) - double(x.split_val);
+                            const HeapEnt v{cost + fabs(diff), diff <= 0.0 ? x.right : x.left, 0};
+                            uint32_t i = hn++;
+                            while (i > 0) {
+                                const uint32_t p = (i - 1) / 2;
+                                if (!hless(v, h[p])) break;
+                                h[i] = h[p];
+                                i = p;
+                            }
+                            DCHK(i < a.hcap);
+                            h[i] = v;
+                            nd = diff <= 0.0 ? x.left : x.right;
+                        }
+                        DCHK(cnt < a.n_node);
+                        out[cnt++] = nd;
+                        if (cnt >= want || hn == 0) break;
+                        const HeapEnt top = h[0];
+                        const HeapEnt last = h[--hn];
+                        uint32_t i = 0;
+                        for (;;) {
+                            uint32_t c = 2 * i + 1;
+                            if (c >= hn) break;
+                            if (c + 1 < hn && hless(h[c + 1], h[c])) ++c;
+                            if (!hless(h[c], last)) break;
+                            h[i] = h[c];
+                            i = c;
+                        }
+                        if (hn) h[i] = last;
+                        nd = top.node;
+                        cost = top.cost;
+                    }
+                }
+                for (uint32_t j = cnt; j < a.n_node; ++j) out[j] = kInvalidId;
+                atomicAdd(&s.ctr[6], cnt);
+            }
+            __syncthreads();
+            // visit every point of every emitted leaf
+            const uint32_t total_leaves = a.nt * a.n_node;
+            for (uint32_t L = tid; L < total_leaves; L += kThreads) {
+                const uint32_t t = L / a.n_node;
+                const uint32_t leaf = a.leaves[size_t(slot) * a.nt * a.n_node + L];
+                if (leaf == kInvalidId) continue;
+                const TreeView tv = a.trees[t];
+                const KdNodeDev ln = tv.nodes[leaf];
+                for (uint32_t p = ln.left; p < ln.right; ++p) {
+                    const uint32_t id = tv.pidx[p];
+                    if (mark_visited(a, slot, s, id)) {
+                        const uint32_t k = atomicAdd(&s.ctr[3], 1u);
+                        DCHK(k < a.seed_cap); DCHK(id < a.n);
+                        s.seeds[k] = make_key(qdist(a, s, id), id);
+                    }
+                }
+            }
+        } else {
+            // search.cpp:156-173: mt19937_64(seed) draws id % n until `want` distinct
+            if (tid == 0) {
+                uint64_t* mt = a.mtstate + size_t(slot) * 312;
+                const uint64_t sd = substream(a.seed, qi);
+                mt[0] = sd;
+                for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
+                int idx = 312;
+                const uint32_t want = min(a.rcount == 0 ? a.E : a.rcount, a.n);
+                uint32_t have = 0;
+                while (have < want) {
+                    if (idx == 312) {
+                        for (int j = 0; j < 312; ++j) mt[j] = mt_twist(mt[j], mt[(j + 1) % 312], mt[(j + 156) % 312]);
+                        idx = 0;
+                    }
+                    const uint32_t id = uint32_t(mt_temper(mt[idx++]) % a.n);
+                    if (!mark_visited(a, slot, s, id)) continue;
+                    s.seeds[have++] = id;  // ids first; distances below
+                }
+                s.ctr[3] = have;
+            }
+            __syncthreads();
+            for (uint32_t j = tid; j < s.ctr[3]; j += kThreads) {
+                const uint32_t id = uint32_t(s.seeds[j]);
+                s.seeds[j] = make_key(qdist(a, s, id), id);
+            }
+        }
+        __syncthreads();
+        const uint32_t ns = s.ctr[3];
+        const uint32_t m = next_pow2(max(ns, 1u));
+        for (uint32_t j = ns + tid; j < m; j += kThreads) s.seeds[j] = kEmptyKey;
+        __syncthreads();
+        block_bitonic_sort(s.seeds, m);
+        const uint32_t ps = min(ns, a.E);
+        for (uint32_t j = tid; j < ps; j += kThreads) {
+            s.pool[j] = s.seeds[j];
+            s.checked[j] = 0;
+        }
+        // reserve: seeds ranked past E, re-keyed by id for lookup
+        const uint32_t nr = ns - ps;
+        for (uint32_t base = 0; base < m; base += kThreads) {  // uniform trip count: barriers inside
+            const uint32_t j = base + tid;
+            uint64_t v = kEmptyKey;
+            if (j < nr) {
+                const uint64_t k = s.seeds[ps + j];
+                v = (uint64_t(key_id(k)) << 32) | uint32_t(k >> 32);
+            }
+            __syncthreads();
+            if (j < m) s.seeds[j] = v;
+            __syncthreads();
+        }
+        if (tid == 0) {
+            s.ctr[0] = ps;
+            s.ctr[4] = nr;
+        }
+        __syncthreads();
+        if (nr > 1) block_bitonic_sort(s.seeds, next_pow2(nr));
+        // ------------------------------------------------ expansion rounds
+        for (uint32_t it = 0; it < a.iters; ++it) {
+            const uint32_t pss = s.ctr[0];
+            uint32_t ne = 0;
+            for (uint32_t base = 0; base < pss; base += kThreads) {
+                const uint32_t j = base + tid;
+                const bool f = j < pss && !s.checked[j];
+                uint32_t tot;
+                const uint32_t pos = block_scan(s, f, &tot);
+                if (f) {
+                    DCHK(ne + pos < a.P);
+                    s.expand[ne + pos] = key_id(s.pool[j]);
+                    s.checked[j] = 1;
+                }
+                ne += tot;
+            }
+            __syncthreads();
+            if (ne == 0) break;
+            if (tid == 0) s.ctr[7] += ne;
+            uint64_t thr = tail_key(a, s);
+            const uint32_t slots = ne * a.gk;
+            for (uint32_t base = 0; base < slots; base += kThreads) {
+                const uint32_t j = base + tid;
+                if (j < slots) {
+                    const uint32_t e = s.expand[j / a.gk];
+                    DCHK(e < a.n);
+                    const uint32_t nb = a.graph[size_t(e) * a.gk + (j % a.gk)];
+                    if (mark_visited(a, slot, s, nb)) {
+                        const uint64_t key = make_key(qdist(a, s, nb), nb);
+                        if (key < thr) push_buf(s, key);
+                    } else if (s.ctr[4]) {
+                        const uint32_t nrr = s.ctr[4];
+                        const uint32_t p = lower_bound64(s.seeds, nrr, uint64_t(nb) << 32);
+                        if (p < nrr && uint32_t(s.seeds[p] >> 32) == nb) {
+                            const uint64_t key = (uint64_t(uint32_t(s.seeds[p])) << 32) | nb;
+                            if (key < thr) push_buf(s, key);
+                        }
+                    }
+                }
+                __syncthreads();
+                if (s.ctr[1] + kThreads > kBuf) {
+                    merge_buffer(a, s);
+                    thr = tail_key(a, s);
+                }
+            }
+            merge_buffer(a, s);
+        }
+        // ------------------------------------------------ fallback scan
+        __syncthreads();
+        if (s.ctr[0] < a.k_return) {
+            uint64_t thr = tail_key(a, s);
+            for (uint32_t base = 0; base < a.n; base += kThreads) {
+                const uint32_t id = base + tid;
+                if (id < a.n) {
+                    mark_visited(a, slot, s, id);
+                    const uint64_t key = make_key(qdist(a, s, id), id);
+                    if (key < thr) push_buf(s, key);
+                }
+                __syncthreads();
+                if (s.ctr[1] + kThreads > kBuf) {
+                    merge_buffer(a, s);
+                    thr = tail_key(a, s);
+                }
+            }
+            merge_buffer(a, s);
+        }
+        __syncthreads();
+        // ------------------------------------------------ output + cleanup
+        const uint32_t fin = s.ctr[0];
+        for (uint32_t j = tid; j < a.k_return; j += kThreads)
+            a.out_keys[size_t(qi) * a.k_return + j] = j < fin ? s.pool[j] : kEmptyKey;
+        const uint32_t nv = s.ctr[2];
+        if (tid == 0) {
+            uint64_t* st = a.stats + size_t(qi) * 4;
+            st[0] = nv;
+            st[1] = s.ctr[6];
+            st[2] = s.ctr[7];
+            st[3] = ns;
+        }
+        uint32_t* bm = a.bitmap + size_t(slot) * a.words;
+        if (nv <= a.vcap) {
+            for (uint32_t j = tid; j < nv; j += kThreads) {
+                const uint32_t id = a.vlist[size_t(slot) * a.vcap + j];
+                bm[id >> 5] = 0;
+            }
+        } else {
+            for (uint32_t j = tid; j < a.words; j += kThreads) bm[j] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void keys_split_kernel(const uint64_t* __restrict__ keys, size_t cnt, uint32_t* ids, float* dists) {
+    for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < cnt; t += size_t(gridDim.x) * blockDim.x) {
+        const uint64_t k = keys[t];
+        ids[t] = k == kEmptyKey ? kInvalidId : key_id(k);
+        dists[t] = k == kEmptyKey ? 0.0f : key_dist(k);
+    }
+}
+
+void run_search(annk_searcher* sr, const float* dq, uint32_t nq, const annk_search_params* p, uint32_t* out_ids,
+                float* out_dists, uint64_t* stats_out) {
+    const annk_dataset* base = sr->base;
+    const annk_forest* f = sr->forest;
+    // search.cpp:37-45 begin_query validation
+    if (p->k_return < 1 || p->k_return > p->pool_size) throw_invalid("search: need 1 <= k_return <= pool_size");
+    if (p->expansion > p->pool_size) throw_invalid("search: need expansion <= pool_size");
+    if (p->k_return > base->n) throw_invalid("search: k_return exceeds n");
+    if (!p->random_init && !f) throw_invalid("search: tree-seeded search needs a forest");
+    if (nq == 0) return;
+    uint32_t nt = 0, n_node = 0, leaf_cap = 1, max_depth = 0;
+    if (!p->random_init) {
+        nt = p->n_trees_used == 0 ? f->n_trees : std::min(p->n_trees_used, f->n_trees);
+        // search.cpp:131-133: truncating division, clamped per tree
+        n_node = p->pool_size / std::max(1u, f->leaf_cap) / std::max(1u, nt) + 1;
+        leaf_cap = f->leaf_cap;
+        for (uint32_t t = 0; t < nt; ++t) max_depth = std::max(max_depth, f->trees[t].max_depth);
+        if (nt > kThreads) throw_invalid("search: more than 256 trees in use is not supported");
+    }
+    const uint64_t seed_bound =
+        p->random_init ? std::min<uint64_t>(p->random_seed_count ? p->random_seed_count : p->expansion, base->n)
+                       : std::min<uint64_t>(uint64_t(nt) * n_node * leaf_cap, base->n);
+    const uint32_t seed_cap = next_pow2(uint32_t(std::max<uint64_t>(seed_bound, 1)));
+    const uint32_t P = p->pool_size;
+    const size_t smem = size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kBuf) * 8 + size_t(base->ld) * 4 +
+                        size_t(P) * 4 + 128 + size_t(P) * 2 + 16;
+    if (smem > size_t(max_smem_optin()))
+        throw_invalid("search: pool_size/seed budget exceeds on-chip capacity");
+    CK(cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_kernel, kThreads, smem));
+    const uint32_t slots = std::min<uint32_t>(nq, uint32_t(num_sms()) * std::max(per_sm, 1));
+    const uint32_t words = (base->n + 31) / 32;
+    const uint64_t vbound = seed_bound + uint64_t(p->iters) * P * sr->gk;
+    const uint32_t vcap = uint32_t(std::min<uint64_t>(vbound, base->n));
+    const uint32_t hcap = (n_node + 1) * (max_depth + 1) + 1;
+    DevBuf<uint32_t> bitmap(size_t(slots) * words), vlist(size_t(slots) * std::max(vcap, 1u));
+    bitmap.zero();
+    DevBuf<HeapEnt> heaps(std::max<size_t>(size_t(slots) * nt * hcap, 1));
+    DevBuf<uint32_t> leaves(std::max<size_t>(size_t(slots) * nt * n_node, 1));
+    DevBuf<uint64_t> mt(p->random_init ? size_t(slots) * 312 : 1);
+    DevBuf<uint64_t> keys(size_t(nq) * p->k_return), st(size_t(nq) * 4);
+    SearchArgs a{base->data.p, base->n, base->ld, dq, nq, f ? f->views.p : nullptr, nt, n_node, leaf_cap,
+                 sr->graph.p, sr->gk, p->k_return, P, p->expansion, p->iters, p->random_init,
+                 p->random_seed_count, p->seed, seed_cap, bitmap.p, words, vlist.p, vcap, heaps.p, hcap,
+                 leaves.p, mt.p, keys.p, st.p};
+    LAUNCH(search_kernel, slots, kThreads, smem, a);
+    const size_t cnt = size_t(nq) * p->k_return;
+    DevBuf<uint32_t> di(cnt);
+    DevBuf<float> dd(cnt);
+    LAUNCH(keys_split_kernel, uint32_t(std::min<size_t>((cnt + 255) / 256, 65535)), 256, 0, keys.p, cnt, di.p, dd.p);
+    di.download(out_ids, cnt);
+    dd.download(out_dists, cnt);
+    if (stats_out) st.download(stats_out, size_t(nq) * 4);
+    ssync();
+}
+
+}  // namespace
+}  // namespace annk
+
+using namespace annk;
+
+extern "C" {
+
+int annk_searcher_create(const annk_dataset* base, const annk_forest* f, const uint32_t* graph_ids,
+                         uint32_t graph_n, uint32_t graph_k, annk_searcher** out) {
+    return abi([&] {
+        if (!base || !out) throw_invalid("searcher: null argument");
+        // search.cpp:23-35
+        if (graph_n != base->n) throw_invalid("searcher: graph does not match base set");
+        for (size_t i = 0; i < size_t(graph_n) * graph_k; ++i)
+            if (graph_ids[i] >= base->n) throw_invalid("searcher: graph id out of range");
+        if (f && (f->n != base->n || f->dim != base->dim)) throw_invalid("searcher: forest does not match base set");
+        auto sr = std::make_unique<annk_searcher>();
+        sr->base = base;
+        sr->forest = f;
+        sr->gn = graph_n;
+        sr->gk = graph_k;
+        sr->graph.alloc(std::max<size_t>(size_t(graph_n) * graph_k, 1));
+        sr->graph.upload(graph_ids, size_t(graph_n) * graph_k);
+        if (f) forest_ensure_links(const_cast<annk_forest*>(f));
+        ssync();
+        *out = sr.release();
+    });
+}
+
+int annk_searcher_destroy(annk_searcher* s) {
+    return abi([&] { delete s; });
+}
+
+int annk_search(annk_searcher* s, const float* queries, uint32_t nq, uint32_t dim, const annk_search_params* p,
+                uint32_t* out_ids, float* out_dists, uint64_t* stats) {
+    return abi([&] {
+        if (!s || !p) throw_invalid("search: null argument");
+        if (dim != s->base->dim) throw_invalid("search: query length mismatch");
+        const uint32_t ld = s->base->ld;
+        DevBuf<float> dq(std::max<size_t>(size_t(nq) * ld, 1));
+        if (nq) {
+            if (ld == dim) {
+                dq.upload(queries, size_t(nq) * dim);
+            } else {
+                dq.zero();
+                CK(cudaMemcpy2DAsync(dq.p, ld * 4, queries, dim * 4, dim * 4, nq, cudaMemcpyHostToDevice, stream()));
+            }
+        }
+        run_search(s, dq.p, nq, p, out_ids, out_dists, stats);
+    });
+}
+
+int annk_search_dataset(annk_searcher* s, const annk_dataset* queries, const annk_search_params* p,
+                        uint32_t* out_ids, float* out_dists, uint64_t* stats) {
+    return abi([&] {
+        if (!s || !p || !queries) throw_invalid("search: null argument");
+        if (queries->dim != s->base->dim) throw_invalid("search: query length mismatch");
+        run_search(s, queries->data.p, queries->n, p, out_ids, out_dists, stats);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,290 @@
+"""GPU parity: every hot-path entry point through the C-ABI vs the CPU oracle
+(our C restatement, itself pinned to the reference in test_oracle_pin.py) on
+identical seeded inputs.  Integer/index results must be bit-exact; distances
+are compared bit-for-bit too, because the device computes the reference's
+sequential fp32 l2_sq (tolerance 0)."""
+import numpy as np
+import pytest
+
+import paper_1609_07228_b200 as A
+from tests.helpers import assert_pools_equal, assert_trees_equal, mixture, ora
+
+pytestmark = pytest.mark.gpu
+
+
+# ------------------------------------------------------------ brute force
+
+@pytest.mark.parametrize("n,dim,k,seed", [(2000, 8, 10, 12), (3000, 32, 100, 3), (700, 960, 20, 5)])
+def test_brute_force_self_and_query(n, dim, k, seed):
+    o = ora()
+    x = A.gen_synthetic(n, dim, seed)
+    q = A.gen_synthetic(57, dim, seed + 1)
+    vo, qo = o.vs(x), o.vs(q)
+    ids_o, d_o, c_o = o.brute_force(vo, None, k, workers=8, with_dists=True)
+    comps = []
+    ids, d = A.brute_force_knn(x, None, k, dist_comps=comps, with_dists=True)
+    np.testing.assert_array_equal(ids, ids_o)
+    np.testing.assert_array_equal(d.view(np.uint32), d_o.view(np.uint32))
+    assert comps[0] == c_o == n * (n - 1)
+    ids_q = A.brute_force_knn(x, q, k)
+    np.testing.assert_array_equal(ids_q, o.brute_force(vo, qo, k, workers=8))
+
+
+def test_brute_force_integer_mixture_ties():
+    # integer-valued clustered data has many exact distance ties: order by id
+    o = ora()
+    x = mixture(4000, 128, 20, 7)
+    ids = A.brute_force_knn(x, None, 50)
+    np.testing.assert_array_equal(ids, o.brute_force(o.vs(x), None, 50, workers=8))
+
+
+def test_brute_force_edge_cases():
+    vs = np.array([[0.0], [1.0], [3.0]], np.float32)  # test_eval.cpp:10-21
+    np.testing.assert_array_equal(A.brute_force_knn(vs, None, 1)[:, 0], [1, 0, 1])
+    base = A.gen_synthetic(40, 6, 4)  # test_eval.cpp:23-33
+    ids, d = A.brute_force_knn(base, base[17:18], 3, with_dists=True)
+    assert ids[0, 0] == 17 and d[0, 0] == 0.0
+    small = A.gen_synthetic(5, 2, 1)  # test_eval.cpp:51-58
+    with pytest.raises(A.InvalidArgument):
+        A.brute_force_knn(small, None, 5)
+    A.brute_force_knn(small, None, 4)
+    q = A.gen_synthetic(2, 2, 2)
+    A.brute_force_knn(small, q, 5)
+    with pytest.raises(A.InvalidArgument):
+        A.brute_force_knn(small, q, 6)
+    # k beyond the tiled path (large-k route) still exact
+    x = A.gen_synthetic(900, 5, 9)
+    o = ora()
+    np.testing.assert_array_equal(A.brute_force_knn(x, None, 899), o.brute_force(o.vs(x), None, 899, workers=8))
+
+
+def test_brute_force_rows_sample():
+    x = mixture(5000, 128, 30, 11)
+    rows = np.array([0, 17, 4999, 2500, 33], np.uint32)
+    full = A.brute_force_knn(x, None, 20)
+    np.testing.assert_array_equal(A.brute_force_rows(x, rows, 20), full[rows])
+
+
+# ----------------------------------------------------------------- forest
+
+@pytest.mark.parametrize("n,dim,trees,leaf,seed", [
+    (10000, 128, 8, 10, 1),    # test_kd_forest.cpp:71-76 shape
+    (500, 12, 4, 10, 1234),    # test_kd_forest.cpp:78-96
+    (2000, 8, 2, 10, 55),
+    (1, 4, 3, 10, 5), (7, 4, 2, 10, 5), (300, 6, 2, 5, 4),
+    (20000, 32, 4, 8, 3),
+])
+def test_forest_bit_identical(n, dim, trees, leaf, seed):
+    o = ora()
+    x = A.gen_synthetic(n, dim, seed)
+    fo = o.build_forest(o.vs(x), trees, leaf, seed)
+    fd = A.build_forest(x, trees, leaf, seed)
+    for t in range(trees):
+        assert_trees_equal(fd.tree(t), fo.tree(t))
+
+
+def test_forest_integer_mixture_with_duplicates():
+    # clipped integer data: many equal values -> degenerate splits (even_split fallback)
+    o = ora()
+    x = mixture(30000, 128, 50, 2)
+    x[:2000] = x[0]  # a block of exact duplicates
+    fo = o.build_forest(o.vs(x), 4, 8, 9)
+    fd = A.build_forest(x, 4, 8, 9)
+    evens = 0
+    for t in range(4):
+        td = fd.tree(t)
+        assert_trees_equal(td, fo.tree(t))
+        evens += int(td.even_split.sum())
+    assert evens > 0
+
+
+def test_forest_float_mixture_inexact_sums():
+    # [0,1] clipped Gaussian floats (cfg3-like) exercise the serial-sum fallback
+    o = ora()
+    x = mixture(6000, 96, 20, 4, lo=0.05, hi=0.35, sd=0.05, clip=(0.0, 1.0), rnd=False)
+    x[::7, 3] = np.float32(1e-12)  # tiny magnitudes force inexact partial sums
+    fo = o.build_forest(o.vs(x), 3, 10, 1)
+    fd = A.build_forest(x, 3, 10, 1)
+    for t in range(3):
+        assert_trees_equal(fd.tree(t), fo.tree(t))
+
+
+def test_search_leaves_and_descend():
+    o = ora()
+    x = A.gen_synthetic(1000, 8, 17)
+    q = A.gen_synthetic(20, 8, 18)
+    fo = o.build_forest(o.vs(x), 2, 10, 99)
+    fd = A.build_forest(x, 2, 10, 99)
+    for t in range(2):
+        for nl in (1, 4, 17, 10000):
+            got = fd.search_leaves(t, q, nl)
+            for i in range(len(q)):
+                np.testing.assert_array_equal(got[i], fo.search_leaves(t, q[i], nl))
+        tr = fd.tree(t)
+        rng = np.random.default_rng(5)
+        starts = rng.integers(0, tr.n_nodes, size=len(q)).astype(np.uint32)
+        out = fd.descend_from(t, q, starts)
+        for i in range(len(q)):
+            assert out[i] == fo.descend_from(t, q[i], int(starts[i]))
+
+
+# --------------------------------------------------------- init + refine
+
+def _pair(x, trees, leaf, seed, k, dep, P, S):
+    o = ora()
+    vo = o.vs(x)
+    fo = o.build_forest(vo, trees, leaf, seed)
+    so = o.init_graph(vo, fo, k, dep, P, S, seed)
+    fd = A.build_forest(x, trees, leaf, seed)
+    sd = A.init_graph(x, fd, k, dep, P, S, seed)
+    return o, vo, so, sd
+
+
+@pytest.mark.parametrize("n,dim,trees,leaf,k,dep,P,S,seed,iters", [
+    (2000, 32, 4, 10, 10, 4, 30, 20, 1, 8),     # test_graph_build.cpp:152-192
+    (500, 8, 4, 10, 10, 2, 30, 20, 23, 3),      # :194-212
+    (3000, 128, 8, 8, 20, 4, 40, 10, 7, 4),
+    (150, 4, 2, 4, 5, 0, 20, 20, 3, 6),         # small sets / Dep 0
+])
+def test_init_and_nn_descent_bit_exact(n, dim, trees, leaf, k, dep, P, S, seed, iters):
+    x = A.gen_synthetic(n, dim, seed)
+    o, vo, so, sd = _pair(x, trees, leaf, seed, k, dep, P, S)
+    e = assert_pools_equal(sd, so)
+    assert sd.meta()["dist_comps"] == e["dist_comps"]
+    for it in range(iters):
+        so.nn_descent_iteration(vo)
+        A.detail.nn_descent_iteration(sd, x)
+        e = assert_pools_equal(sd, so)
+        m = sd.meta()
+        assert m["dist_comps"] == e["dist_comps"], f"iteration {it}"
+        assert m["iteration"] == e["iteration"]
+        for which in range(4):
+            dl, ol = sd.lists(which), so.lists(which)
+            for i in range(n):
+                np.testing.assert_array_equal(dl[i], ol[i], err_msg=f"list {which} row {i} iter {it}")
+
+
+def test_integer_mixture_refine_and_finalize():
+    x = mixture(20000, 128, 40, 3)
+    o, vo, so, sd = _pair(x, 4, 10, 3, 10, 4, 30, 10)
+    for _ in range(3):
+        so.nn_descent_iteration(vo)
+        A.detail.nn_descent_iteration(sd, x)
+    assert_pools_equal(sd, so)
+    ids_o, d_o = so.finalize(vo, 10)
+    g = A.finalize(sd, x, 10)
+    np.testing.assert_array_equal(g.ids, ids_o)
+    np.testing.assert_array_equal(g.dists.view(np.uint32), d_o.view(np.uint32))
+    gt = A.brute_force_knn(x, None, 10)
+    assert abs(A.detail.pool_topk_accuracy(sd, gt) - so.pool_topk_accuracy(gt)) == 0.0
+
+
+def test_rebuild_and_union_separately():
+    x = A.gen_synthetic(500, 8, 23)
+    o, vo, so, sd = _pair(x, 4, 10, 23, 10, 2, 30, 20)
+    for _ in range(2):
+        so.nn_descent_iteration(vo)
+        A.detail.nn_descent_iteration(sd, x)
+    so.rebuild_sample_lists()
+    A.detail.rebuild_sample_lists(sd)
+    for which in range(4):
+        dl, ol = sd.lists(which), so.lists(which)
+        for i in range(500):
+            np.testing.assert_array_equal(dl[i], ol[i])
+    m = sd.meta()
+    for i, (a, b) in enumerate(zip(sd.g_new, sd.g_old)):
+        assert len(a) <= m["sample_cap"] and len(a) + len(b) <= m["pool_cap"]
+    so.union_reverse_lists()
+    A.detail.union_reverse_lists(sd)
+    for which in (0, 1):
+        dl, ol = sd.lists(which), so.lists(which)
+        for i in range(500):
+            np.testing.assert_array_equal(dl[i], ol[i])
+    assert_pools_equal(sd, so)
+
+
+def test_exact_old_state_is_fixed_point():
+    # test_graph_build.cpp:121-137
+    x = A.gen_synthetic(120, 6, 19)
+    gt, d = A.brute_force_knn(x, None, 10, with_dists=True)
+    sd = A.RefineState.from_pools(120, 10, 10, 10, 1, np.full(120, 10, np.uint32), gt, d,
+                                  np.zeros((120, 10), np.uint8))
+    before = sd.pools()[1].copy()
+    assert A.detail.nn_descent_iteration(sd, x) == 0
+    assert sd.meta()["dist_comps"] == 0
+    np.testing.assert_array_equal(sd.pools()[1], before)
+
+
+def test_two_point_fixed_point_and_errors():
+    x = A.gen_synthetic(2, 3, 2)  # test_graph_build.cpp:139-150
+    f = A.build_forest(x, 1, 4, 2)
+    s = A.init_graph(x, f, 1, 0, 1, 5, 2)
+    _, ids, _, _ = s.pools()
+    assert ids[0, 0] == 1 and ids[1, 0] == 0
+    assert A.detail.nn_descent_iteration(s, x) == 0
+    y = A.gen_synthetic(300, 8, 51)
+    fy = A.build_forest(y, 4, 10, 51)
+    sy = A.init_graph(y, fy, 10, 4, 10, 10, 51)
+    with pytest.raises(A.InvalidArgument):
+        A.finalize(sy, y, 11)
+    with pytest.raises(A.InvalidArgument):
+        A.init_graph(y, fy, 10, 4, 5, 10, 51)  # pool_cap < k
+
+
+# ----------------------------------------------------------------- search
+
+@pytest.mark.parametrize("P,E,I,ntu", [(100, 50, 4, 0), (60, 30, 0, 0), (200, 200, 4, 2), (20, 20, 64, 0),
+                                       (300, 10, 8, 0)])
+def test_search_bit_exact(P, E, I, ntu):
+    o = ora()
+    x = A.gen_synthetic(2000, 16, 21)
+    q = A.gen_synthetic(50, 16, 22)
+    vo = o.vs(x)
+    fo = o.build_forest(vo, 8, 10, 21)
+    fd = A.build_forest(x, 8, 10, 21)
+    g = A.brute_force_graph(x, 10)
+    ids_o, d_o, st_o = o.search(vo, fo, g.ids, o.vs(q), 10, P, E, I, ntu)
+    r = A.GraphSearcher(x, fd, g).search_batch(q, A.SearchParams(10, P, E, I, ntu))
+    np.testing.assert_array_equal(r.ids, ids_o)
+    np.testing.assert_array_equal(r.dists.view(np.uint32), d_o.view(np.uint32))
+    np.testing.assert_array_equal(r.stats, st_o)
+
+
+def test_search_random_init_and_fallback():
+    o = ora()
+    x = A.gen_synthetic(600, 8, 33)
+    q = A.gen_synthetic(8, 8, 34)
+    vo = o.vs(x)
+    g = A.brute_force_graph(x, 10)
+    for P, E, I in [(600, 600, 4), (12, 12, 0), (100, 50, 4)]:
+        ids_o, d_o, st_o = o.search(vo, None, g.ids, o.vs(q), 10 if P >= 10 else P, P, E, I, random_init=True,
+                                    seed=4242)
+        r = A.GraphSearcher(x, None, g).search_batch(q, A.SearchParams(10 if P >= 10 else P, P, E, I, seed=4242),
+                                                     random_init=True)
+        np.testing.assert_array_equal(r.ids, ids_o)
+        np.testing.assert_array_equal(r.stats, st_o)
+    # disconnected graph -> fallback scan (search.cpp:95-106)
+    gbad = np.zeros((600, 2), np.uint32)
+    f = A.build_forest(x, 1, 600, 3)
+    fo = o.build_forest(vo, 1, 600, 3)
+    ids_o, d_o, st_o = o.search(vo, fo, gbad, o.vs(q), 5, 5, 0, 2)
+    r = A.GraphSearcher(x, f, gbad).search_batch(q, A.SearchParams(5, 5, 0, 2))
+    np.testing.assert_array_equal(r.ids, ids_o)
+    np.testing.assert_array_equal(r.stats, st_o)
+
+
+def test_search_validation():
+    x = A.gen_synthetic(50, 4, 66)
+    f = A.build_forest(x, 8, 10, 66)
+    g = A.brute_force_graph(x, 5)
+    s = A.GraphSearcher(x, f, g)
+    q = A.gen_synthetic(2, 4, 67)
+    for p in (A.SearchParams(k_return=0), A.SearchParams(k_return=20, pool_size=10),
+              A.SearchParams(k_return=5, pool_size=10, expansion=11)):
+        with pytest.raises(A.InvalidArgument):
+            s.search_batch(q, p)
+    s.search_batch(q, A.SearchParams(k_return=5, pool_size=10, expansion=10))
+    with pytest.raises(A.InvalidArgument):
+        s.search(np.zeros(3, np.float32), A.SearchParams(5, 10, 10))
+    with pytest.raises(A.InvalidArgument):
+        A.GraphSearcher(A.gen_synthetic(10, 4, 1), None, g)
