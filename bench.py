@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""bench.py — EFANNA hot paths on B200 vs the reference CPU library.
+
+Headline metric (BASELINE.json): "kNN-graph build s at graph acc 0.9; search
+queries/s at recall@100 0.9", on configs[1] (cfg2): 1M x 128 integer-valued
+Gaussian mixture (1000 centers), 8 trees leaf 8, K=100, P(L)=100, S=20,
+10k queries, search top-100.
+
+  value      = seconds for one kNN-graph build up to the first NN-descent
+               iteration whose graph accuracy >= 0.9 (init + refine, the
+               reference's own StopWatch boundary, graph_build.cpp:421-450; the
+               forest is built once beforehand, as `annkit build-trees` does).
+               Inputs resident in HBM; dataset 512 MB > L2 (126 MB).
+  e2e        = the same build through the C-ABI from pinned host memory:
+               H2D of the dataset + forest + init + refine + finalize + D2H of
+               the graph (ids + dists), every step.
+  search_qps = queries/s of the batched search at the smallest swept pool
+               size reaching recall@100 >= 0.9 (secondary line item).
+
+Accuracy is scored on a seeded 10,000-point sample against exact top-100 rows
+(untimed, as the reference's accuracy hook is not charged to build time).
+
+--impl reference runs the unmodified reference library (oracle/_ref, built
+from /root/reference by oracle/Makefile) on all host cores on a bounded sample:
+the same build (init + the same number of NN-descent iterations) on the first
+`ref_points` points of the same dataset, scaled linearly to the full N.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # configs[1] of BASELINE.json: the headline workload
+    "cfg2": dict(n=1_000_000, dim=128, n_queries=10_000, centers=1000, trees=8, leaf=8, k=100, P=100, S=20,
+                 max_iters=10, dep=4, k_return=100, sweep=[100, 200, 300, 400, 500, 600, 800, 1000],
+                 acc_sample=10_000, ref_points=65_536, ref_queries=500),
+    # configs[0]: the reference's own CPU-runnable case (R=50 is not expressible: reverse cap = S)
+    "cfg1": dict(n=100_000, dim=128, n_queries=1000, centers=100, trees=4, leaf=10, k=10, P=30, S=10,
+                 max_iters=8, dep=4, k_return=10, sweep=[50, 100, 200], acc_sample=10_000, ref_points=100_000,
+                 ref_queries=1000),
+    # a small smoke-sized case for quick checks
+    "tiny": dict(n=50_000, dim=128, n_queries=1000, centers=100, trees=4, leaf=8, k=20, P=40, S=10,
+                 max_iters=6, dep=4, k_return=20, sweep=[40, 80, 160], acc_sample=2000, ref_points=50_000,
+                 ref_queries=200),
+}
+SEED = 1
+
+
+def gen_data(cfg, n=None):
+    import paper_1609_07228_b200 as A
+    n = cfg["n"] if n is None else n
+    base = A.gen_mixture(n, cfg["dim"], cfg["centers"], 0.0, 128.0, 16.0, 0.0, 255.0, True, SEED, 1)
+    queries = A.gen_mixture(cfg["n_queries"], cfg["dim"], cfg["centers"], 0.0, 128.0, 16.0, 0.0, 255.0, True,
+                            SEED, 2)
+    return base, queries
+
+
+def sample_rows(n, m, seed=SEED):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n, size=min(m, n), replace=False)).astype(np.uint32)
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        util = [float(r[6]) for r in self.rows if r[6].replace(".", "").isdigit()]
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- distributed
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if args.impl != "reference" and torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, v: float) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------- reference arm
+
+def cpu_reference_build(cfg, iters, base=None):
+    """Reference library (oracle/_ref) build on the first ref_points points:
+    init_graph + `iters` NN-descent iterations, all host cores.  Returns
+    (measured seconds, points, cores, init_s, refine_s)."""
+    from oracle import oracle as O
+    ref = O.load("reference")
+    m = cfg["ref_points"]
+    if base is None:
+        base, _ = gen_data(cfg, n=m)
+    x = np.ascontiguousarray(base[:m])
+    cores = os.cpu_count() or 1
+    vs = ref.vs(x)
+    forest = ref.build_forest(vs, cfg["trees"], cfg["leaf"], SEED, workers=cores)
+    _, _, log, summ = ref.build_graph(vs, forest, k=cfg["k"], conquer_depth=cfg["dep"], pool_cap=cfg["P"],
+                                      sample_cap=cfg["S"], max_iters=iters, strategy=0, seed=SEED,
+                                      workers=cores, min_change_rate=0.0)
+    return float(summ[0] + summ[1]), m, cores, float(summ[0]), float(summ[1])
+
+
+def run_reference(args, cfg, ws, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    if not O.reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libannkit_ref.so not built"}))
+        return
+    iters = cfg["ref_iters"]
+    base, _ = gen_data(cfg, n=cfg["ref_points"])
+    for _ in range(args.warmup):
+        cpu_reference_build(cfg, iters, base)
+    times = []
+    for _ in range(args.steps):
+        t, m, cores, _, _ = cpu_reference_build(cfg, iters, base)
+        times.append(t * cfg["n"] / m)
+    v = statistics.mean(times)
+    sample = (f"reference build_graph (init + {iters} NN-descent iterations, {cfg['trees']} trees leaf "
+              f"{cfg['leaf']}) on the first {cfg['ref_points']} of {cfg['n']} points, {os.cpu_count()} workers, "
+              f"seconds scaled x{cfg['n'] / cfg['ref_points']:.2f} to N")
+    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.config, "n": cfg["n"], "dim": cfg["dim"], "trees": cfg["trees"],
+                       "leaf_cap": cfg["leaf"], "k": cfg["k"], "pool_cap": cfg["P"], "sample_cap": cfg["S"],
+                       "iterations_to_acc_0.9": iters},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": os.cpu_count(), "kind": "reference", "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+METRIC = "kNN-graph build s at graph acc 0.9; search queries/s at recall@100 0.9"
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def run_gpu(args, cfg, ws, rank, local):
+    import torch
+
+    import paper_1609_07228_b200 as A
+    A.lib.annk_set_device(local)
+    ext = torch.cuda.ExternalStream(A.stream_handle(), device=torch.device("cuda", local))
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(ext)
+        return e
+
+    t0 = time.perf_counter()
+    base, queries = gen_data(cfg)
+    gen_s = time.perf_counter() - t0
+    vs = A.VectorSet(base)
+    qs = A.VectorSet(queries)
+    n, dim, k = cfg["n"], cfg["dim"], cfg["k"]
+
+    # forest (once, like `annkit build-trees`)
+    e0 = ev()
+    forest = A.build_forest(vs, cfg["trees"], cfg["leaf"], SEED)
+    e1 = ev()
+    torch.cuda.synchronize()
+    forest_s = e0.elapsed_time(e1) / 1e3
+
+    # exact ground truth (untimed): sampled self-mode rows + query rows
+    rows = sample_rows(n, cfg["acc_sample"])
+    e0 = ev()
+    gt_rows = A.brute_force_rows(vs, rows, k)
+    e1 = ev()
+    torch.cuda.synchronize()
+    gt_rows_s = e0.elapsed_time(e1) / 1e3
+    e0 = ev()
+    gt_q = A.brute_force_knn(vs, qs, cfg["k_return"])
+    e1 = ev()
+    torch.cuda.synchronize()
+    gt_q_s = e0.elapsed_time(e1) / 1e3
+    bf_pairs = float(len(rows)) * (n - 1) + float(cfg["n_queries"]) * n
+
+    # calibration build: accuracy per iteration -> crossing iteration
+    st = A.init_graph(vs, forest, k, cfg["dep"], cfg["P"], cfg["S"], SEED)
+    accs = [A.detail.pool_topk_accuracy(st, gt_rows, rows)]
+    crossing = None
+    comps = [st.meta()["dist_comps"]]
+    join_rows = []
+    for it in range(cfg["max_iters"]):
+        A.detail.nn_descent_iteration(st, vs)
+        accs.append(A.detail.pool_topk_accuracy(st, gt_rows, rows))
+        comps.append(st.meta()["dist_comps"])
+        jr = np.zeros(1, np.uint64)
+        import ctypes
+        v = ctypes.c_uint64(0)
+        A.lib.annk_state_join_rows(st.handle, ctypes.byref(v))
+        join_rows.append(int(v.value))
+        if crossing is None and accs[-1] >= 0.9:
+            crossing = it + 1
+            if not args.full_log:
+                break
+    if crossing is None:
+        crossing = cfg["max_iters"]
+    del st
+
+    def build_once():
+        s = A.init_graph(vs, forest, k, cfg["dep"], cfg["P"], cfg["S"], SEED)
+        for _ in range(crossing):
+            A.detail.nn_descent_iteration(s, vs)
+        return s
+
+    for _ in range(args.warmup):
+        s = build_once()
+        del s
+    torch.cuda.synchronize()
+    A.profile_reset()
+    A.profile_enable(True)
+    launches0 = A.launch_count()
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0 = ev()
+        for _ in range(args.steps):
+            s = build_once()
+        e1 = ev()
+        torch.cuda.synchronize()
+    barrier(ws)
+    launches = A.launch_count() - launches0
+    A.profile_enable(False)
+    prof = A.profile_report()
+    step_s = e0.elapsed_time(e1) / 1e3 / args.steps
+    step_s = max_over_ranks(ws, step_s)
+    final_acc = A.detail.pool_topk_accuracy(s, gt_rows, rows)
+    graph = A.finalize(s, vs, k)
+    del s
+
+    # search sweep (secondary metric): smallest pool reaching recall@k_return >= 0.9
+    searcher = A.GraphSearcher(vs, forest, graph)
+    sweep = []
+    chosen = None
+    kr = cfg["k_return"]
+    for P in cfg["sweep"]:
+        p = A.SearchParams(k_return=kr, pool_size=P, expansion=P, iters=4)
+        searcher.search_batch(qs, p)  # warm
+        e0 = ev()
+        r = searcher.search_batch(qs, p)
+        e1 = ev()
+        torch.cuda.synchronize()
+        dt = e0.elapsed_time(e1) / 1e3
+        rec = float(np.mean([len(np.intersect1d(r.ids[i], gt_q[i])) / kr for i in range(len(gt_q))]))
+        row = {"pool": P, "expansion": P, "recall": round(rec, 4), "qps": round(cfg["n_queries"] / dt, 1),
+               "dist_comps_per_query": float(r.stats[:, 0].mean())}
+        sweep.append(row)
+        if chosen is None and rec >= 0.9:
+            chosen = row
+            if not args.full_log:
+                break
+
+    # e2e through the C-ABI from pinned host memory
+    pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = base
+    host = pinned.numpy()
+    e2e_times = []
+    for i in range(max(1, args.e2e_steps) + 1):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        v2 = A.VectorSet(host)
+        f2 = A.build_forest(v2, cfg["trees"], cfg["leaf"], SEED)
+        s2 = A.init_graph(v2, f2, k, cfg["dep"], cfg["P"], cfg["S"], SEED)
+        for _ in range(crossing):
+            A.detail.nn_descent_iteration(s2, v2)
+        g2 = A.finalize(s2, v2, k)
+        t2 = time.perf_counter()
+        if i > 0:  # first is warm-up
+            e2e_times.append(t2 - t1)
+        del v2, f2, s2
+    assert np.array_equal(g2.ids, graph.ids), "e2e graph differs from the device-resident build"
+    e2e_s = max_over_ranks(ws, statistics.mean(e2e_times))
+
+    # roofline: the dominant kernel's algorithmic bytes per launch / measured duration
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    row_bytes = dim * 4
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    dom_name, (dom_cnt, dom_ms) = dom
+    if dom_name == "join_kernel":
+        rows_per_launch = sum(join_rows[:crossing]) / crossing
+        alg_bytes = rows_per_launch * (row_bytes + 4) + n * 8
+        unit_desc = "sum_i(|new_i|+|old_i|) rows of 4d bytes + 4-byte ids, + N*8 thresholds"
+    elif dom_name == "init_kernel":
+        alg_bytes = comps[0] * (row_bytes + 4) + n * cfg["P"] * 9
+        unit_desc = "init dist_comps rows of 4d bytes + ids, + N*P*9 pool bytes"
+    else:
+        alg_bytes = None
+        unit_desc = "n/a"
+    per_launch_s = dom_ms / dom_cnt / 1e3
+    achieved = alg_bytes / per_launch_s / 1e9 if alg_bytes else None
+    roofline = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes, "per_launch_ms": per_launch_s * 1e3,
+                "share_of_step": dom_ms / sum(v[1] for v in prof.values()), "units": unit_desc}
+
+    # CPU baseline: the reference library on a bounded sample (rank 0, N=1)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.skip_cpu:
+        from oracle import oracle as O
+        if O.reference_available():
+            cfg_ref = dict(cfg)
+            t, m, cores, _, _ = cpu_reference_build(cfg_ref, crossing, base)
+            cpu = {"value": t * n / m, "unit": "s", "cores": cores, "kind": "reference",
+                   "sample": f"reference build_graph (init + {crossing} iterations) on the first {m} of {n} points, "
+                             f"{cores} workers, {t:.2f} s measured, scaled x{n / m:.2f} to N"}
+
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config, "n": n, "dim": dim, "trees": cfg["trees"], "leaf_cap": cfg["leaf"],
+                   "k": k, "pool_cap": cfg["P"], "sample_cap": cfg["S"], "conquer_depth": cfg["dep"],
+                   "iterations_to_acc_0.9": crossing, "accuracy_sample_rows": int(len(rows)),
+                   "l2": "inputs larger than L2 (512 MB dataset)", "parallelism": f"replicas x{ws}"},
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * dim * 4),
+                "d2h_bytes_per_step": int(n * k * 8),
+                "includes": "H2D dataset, forest build, init, refine, finalize, D2H graph ids+dists"},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "search_qps_at_recall_0.9": chosen["qps"] if chosen else None,
+        "search": {"k_return": kr, "n_queries": cfg["n_queries"], "chosen": chosen, "sweep": sweep},
+        "accuracy": {"per_iteration": [round(a, 4) for a in accs], "final_sample": round(final_acc, 4),
+                     "dist_comps": comps},
+        "aux_seconds": {"forest": forest_s, "gt_rows": gt_rows_s, "gt_queries": gt_q_s, "data_gen_host": gen_s,
+                        "brute_force_pairs_per_s": bf_pairs / (gt_rows_s + gt_q_s)},
+        "kernels_ms": {k2: round(v2[1], 3) for k2, v2 in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+    }
+    if rank == 0:
+        print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--full-log", action="store_true", help="run all iterations / sweep points")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    cfg.setdefault("ref_iters", {"cfg2": 2, "cfg1": 3, "tiny": 3}[args.config])
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, cfg, ws, rank)
+    else:
+        run_gpu(args, cfg, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

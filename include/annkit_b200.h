@@ -54,6 +54,12 @@ uint64_t annk_stream(void);
 /* Number of kernels this library has launched since load. */
 uint64_t annk_launch_count(void);
 int annk_synchronize(void);
+/* Per-kernel CUDA-event timing on the library stream (no reference
+ * counterpart; the reference only has StopWatch wall time, util.hpp:21-31).
+ * report writes "kernel_name launches total_ms" lines. */
+int annk_profile_enable(int on);
+int annk_profile_reset(void);
+int annk_profile_report(char* buf, uint64_t cap);
 
 /* ---------------------------------------------------------------- dataset */
 /* Uploads an n x dim row-major fp32 matrix (VectorSet::data).  Values must be

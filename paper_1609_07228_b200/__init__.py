@@ -23,3 +23,28 @@ def launch_count() -> int:
 def stream_handle() -> int:
     """The library's cudaStream_t (for CUDA-event timing on the launching stream)."""
     return int(lib.annk_stream())
+
+
+def profile_enable(on: bool = True) -> None:
+    """Per-kernel CUDA-event timing on the library stream."""
+    from ._lib import check
+    check(lib.annk_profile_enable(int(on)))
+
+
+def profile_reset() -> None:
+    from ._lib import check
+    check(lib.annk_profile_reset())
+
+
+def profile_report() -> dict:
+    """{kernel_name: (launches, total_ms)} accumulated since the last reset."""
+    import ctypes
+
+    from ._lib import check
+    buf = ctypes.create_string_buffer(1 << 16)
+    check(lib.annk_profile_report(buf, len(buf)))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.rsplit(" ", 2)
+        out[name] = (int(cnt), float(ms))
+    return out

@@ -60,6 +60,9 @@ _u64 = C.c_uint64
 _SIGS = {
     "annk_set_device": [C.c_int],
     "annk_synchronize": [],
+    "annk_profile_enable": [C.c_int],
+    "annk_profile_reset": [],
+    "annk_profile_report": [C.c_char_p, _u64],
     "annk_dataset_create": [_f32p, _u32, _u32, _pp],
     "annk_dataset_destroy": [_vp],
     "annk_dataset_shape": [_vp, C.POINTER(_u32), C.POINTER(_u32)],

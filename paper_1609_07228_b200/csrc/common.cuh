@@ -52,10 +52,15 @@ cudaStream_t stream();
 void note_launch();
 int num_sms();
 int max_smem_optin();
+// Optional per-kernel CUDA-event timing on the library stream (annk_profile_*).
+void prof_begin(const char* name);
+void prof_end();
 
 #define LAUNCH(kernel, grid, block, smem, ...)                                   \
     do {                                                                         \
+        ::annk::prof_begin(#kernel);                                             \
         kernel<<<(grid), (block), (smem), ::annk::stream()>>>(__VA_ARGS__);      \
+        ::annk::prof_end();                                                      \
         ::annk::note_launch();                                                   \
         CK(cudaGetLastError());                                                  \
     } while (0)

@@ -377,13 +377,26 @@ struct JoinArgs {
     uint32_t* ocnt;
     uint64_t* obuf;
     unsigned long long* comps;
+    // spill list for targets whose fixed slots are full (hub points)
+    uint32_t* ov_cnt;
+    uint32_t* ov_tgt;
+    uint64_t* ov_key;
+    uint32_t ov_cap;
 };
 
 __device__ __forceinline__ void offer(const JoinArgs& a, uint32_t owner, uint32_t cand, float d) {
     const uint64_t key = make_key(d, cand);
     if (key < a.thr[owner]) {
         const uint32_t slot = atomicAdd(&a.ocnt[owner], 1u);
-        if (slot < a.cap) a.obuf[size_t(owner) * a.cap + slot] = key;
+        if (slot < a.cap) {
+            a.obuf[size_t(owner) * a.cap + slot] = key;
+        } else {
+            const uint32_t o = atomicAdd(a.ov_cnt, 1u);
+            if (o < a.ov_cap) {
+                a.ov_tgt[o] = owner;
+                a.ov_key[o] = key;
+            }
+        }
     }
 }
 
@@ -430,6 +443,8 @@ struct MergeArgs {
     uint32_t* sizes;
     const uint32_t* ocnt;
     const uint64_t* obuf;
+    const uint32_t* ov_off;  // per-target start in the target-sorted spill list
+    const uint64_t* ov_key;
     unsigned long long* changes;
 };
 
@@ -443,21 +458,79 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t 
     return lo;
 }
 
+// Warp: R (sorted, unique, r <= P entries) := top-P unique of (R U chunk).
+// chunk (c entries, any order, capacity m = pow2 >= c) is clobbered; tmp >= P.
+__device__ uint32_t warp_topk_merge(uint64_t* R, uint32_t r, uint64_t* chunk, uint32_t c, uint32_t m,
+                                    uint32_t P, uint64_t* tmp) {
+    const uint32_t lane = lane_id();
+    for (uint32_t j = c + lane; j < m; j += 32) chunk[j] = kEmptyKey;
+    __syncwarp();
+    warp_bitonic_sort(chunk, m);
+    uint32_t nu = 0;  // unique, not already in R
+    for (uint32_t base = 0; base < c; base += 32) {
+        const uint32_t j = base + lane;
+        const uint64_t v = j < c ? chunk[j] : kEmptyKey;
+        bool keep = j < c && (j == 0 || chunk[j - 1] != v);
+        if (keep) {
+            const uint32_t p = lower_bound_u64(R, r, v);
+            keep = !(p < r && R[p] == v);
+        }
+        const uint32_t b = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) chunk[nu + __popc(b & ((1u << lane) - 1u))] = v;
+        nu += __popc(b);
+        __syncwarp();
+    }
+    for (uint32_t j = lane; j < r; j += 32) {
+        const uint32_t k = j + lower_bound_u64(chunk, nu, R[j]);
+        if (k < P) tmp[k] = R[j];
+    }
+    for (uint32_t j = lane; j < nu; j += 32) {
+        const uint32_t k = j + lower_bound_u64(R, r, chunk[j]);
+        if (k < P) tmp[k] = chunk[j];
+    }
+    __syncwarp();
+    const uint32_t nr = min(P, r + nu);
+    for (uint32_t j = lane; j < nr; j += 32) R[j] = tmp[j];
+    __syncwarp();
+    return nr;
+}
+
+constexpr uint32_t kMergeChunk = 256;
+
 // New pool = top-P of (pool U offers); duplicates keep the pool's entry.
-__global__ void merge_kernel(MergeArgs a, uint32_t m) {
+// Offers are first reduced to their top-P unique keys in chunks (an offer
+// beaten by P distinct offers cannot survive), then merged with the pool.
+__global__ void merge_kernel(MergeArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t warp = threadIdx.x / 32, lane = lane_id();
     const uint32_t wpb = blockDim.x / 32;
-    uint64_t* so = reinterpret_cast<uint64_t*>(smem) + size_t(warp) * (m + 2 * a.P);
-    uint64_t* sp = so + m;        // pool keys (P)
-    uint64_t* sout = sp + a.P;    // result (P)
-    uint8_t* sflag = reinterpret_cast<uint8_t*>(reinterpret_cast<uint64_t*>(smem) + size_t(wpb) * (m + 2 * a.P)) +
+    const size_t per_warp_u64 = kMergeChunk + 3 * size_t(a.P);
+    uint64_t* chunk = reinterpret_cast<uint64_t*>(smem) + size_t(warp) * per_warp_u64;
+    uint64_t* R = chunk + kMergeChunk;   // top-P offers
+    uint64_t* sp = R + a.P;              // pool keys
+    uint64_t* sout = sp + a.P;           // scratch / result
+    uint8_t* sflag = reinterpret_cast<uint8_t*>(reinterpret_cast<uint64_t*>(smem) + size_t(wpb) * per_warp_u64) +
                      size_t(warp) * 2 * a.P;
     uint8_t* soutf = sflag + a.P;
     const uint32_t i = blockIdx.x * wpb + warp;
     if (i >= a.n) return;
-    const uint32_t c = min(a.ocnt[i], a.cap);
-    if (c == 0) return;
+    const uint32_t total = a.ocnt[i];
+    if (total == 0) return;
+    const uint32_t c_fix = min(total, a.cap);
+    const uint32_t c_ov = total - c_fix;
+    const uint64_t* ob = a.obuf + size_t(i) * a.cap;
+    const uint64_t* ov = a.ov_key + (c_ov ? a.ov_off[i] : 0);
+    uint32_t r = 0;
+    for (uint32_t base = 0; base < total; base += kMergeChunk) {
+        const uint32_t c = min(kMergeChunk, total - base);
+        for (uint32_t j = lane; j < c; j += 32) {
+            const uint32_t t = base + j;
+            chunk[j] = t < c_fix ? ob[t] : ov[t - c_fix];
+        }
+        __syncwarp();
+        r = warp_topk_merge(R, r, chunk, c, next_pow2(c), a.P, sout);
+    }
     const uint32_t sz = a.sizes[i];
     uint64_t* pk = a.keys + size_t(i) * a.P;
     uint8_t* pf = a.flags + size_t(i) * a.P;
@@ -465,35 +538,31 @@ __global__ void merge_kernel(MergeArgs a, uint32_t m) {
         sp[j] = j < sz ? pk[j] : kEmptyKey;
         sflag[j] = j < sz ? pf[j] : 0;
     }
-    const uint64_t* ob = a.obuf + size_t(i) * a.cap;
-    for (uint32_t j = lane; j < m; j += 32) so[j] = j < c ? ob[j] : kEmptyKey;
     __syncwarp();
-    warp_bitonic_sort(so, m);
-    // unique offers not already in the pool
+    // offers already present in the pool keep the pool's entry (and flag)
     uint32_t nu = 0;
-    for (uint32_t base = 0; base < c; base += 32) {
+    for (uint32_t base = 0; base < r; base += 32) {
         const uint32_t j = base + lane;
-        const uint64_t v = j < c ? so[j] : kEmptyKey;
-        bool keep = j < c && (j == 0 || so[j - 1] != v);
+        const uint64_t v = j < r ? R[j] : kEmptyKey;
+        bool keep = j < r;
         if (keep) {
             const uint32_t p = lower_bound_u64(sp, sz, v);
             keep = !(p < sz && sp[p] == v);
         }
         const uint32_t b = __ballot_sync(0xffffffffu, keep);
         __syncwarp();
-        if (keep) so[nu + __popc(b & ((1u << lane) - 1u))] = v;
+        if (keep) R[nu + __popc(b & ((1u << lane) - 1u))] = v;
         nu += __popc(b);
         __syncwarp();
     }
-    // merge by ranks (no equal keys remain between the two sorted runs)
     uint32_t added = 0;
     for (uint32_t j = lane; j < sz; j += 32) {
-        const uint32_t r = j + lower_bound_u64(so, nu, sp[j]);
-        if (r < a.P) { sout[r] = sp[j]; soutf[r] = sflag[j]; }
+        const uint32_t k = j + lower_bound_u64(R, nu, sp[j]);
+        if (k < a.P) { sout[k] = sp[j]; soutf[k] = sflag[j]; }
     }
     for (uint32_t j = lane; j < nu; j += 32) {
-        const uint32_t r = j + lower_bound_u64(sp, sz, so[j]);
-        if (r < a.P) { sout[r] = so[j]; soutf[r] = 1; ++added; }
+        const uint32_t k = j + lower_bound_u64(sp, sz, R[j]);
+        if (k < a.P) { sout[k] = R[j]; soutf[k] = 1; ++added; }
     }
     __syncwarp();
     const uint32_t nsz = min(a.P, sz + nu);
@@ -506,6 +575,13 @@ __global__ void merge_kernel(MergeArgs a, uint32_t m) {
         a.sizes[i] = nsz;
         if (added) atomicAdd(a.changes, (unsigned long long)added);
     }
+}
+
+__global__ void spill_counts_kernel(const uint32_t* __restrict__ ocnt, uint32_t n, uint32_t cap,
+                                    uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = ocnt[i] > cap ? ocnt[i] - cap : 0;
+    if (i == n) out[n] = 0;
 }
 
 // --------------------------------------------------------------- finalize
@@ -601,7 +677,9 @@ void exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t n) {
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n + 1, stream()));
     DevBuf<unsigned char> t(tmp);
+    prof_begin("cub_exclusive_scan");
     CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n + 1, stream()));
+    prof_end();
     note_launch();
 }
 
@@ -611,7 +689,9 @@ void segmented_sort(uint32_t* data, uint32_t total, const uint32_t* off, uint32_
     size_t tmp = 0;
     CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, data, out.p, total, n, off, off + 1, stream()));
     DevBuf<unsigned char> t(tmp);
+    prof_begin("cub_segmented_sort");
     CK(cub::DeviceSegmentedSort::SortKeys(t.p, tmp, data, out.p, total, n, off, off + 1, stream()));
+    prof_end();
     note_launch();
     CK(cudaMemcpyAsync(data, out.p, size_t(total) * 4, cudaMemcpyDeviceToDevice, stream()));
 }
@@ -718,38 +798,62 @@ void do_union(annk_state* s) {
 
 uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
     const uint32_t n = s->n;
-    if (s->offer_cap == 0) s->offer_cap = next_pow2(std::max(2 * s->P, 64u));
+    // fixed per-point offer slots; overflow (hub points) spills to a global list
+    if (s->offer_cap == 0) s->offer_cap = std::max(2 * s->P, 64u);
+    if (s->ov_cap == 0) s->ov_cap = std::max<uint32_t>(1u << 20, n * 8u);
     DevBuf<unsigned long long> counters(2);
-    size_t red_tmp = 0;
-    DevBuf<uint32_t> dmax(1);
-    CK(cub::DeviceReduce::Max(nullptr, red_tmp, s->ocnt.p, dmax.p, n, stream()));
-    DevBuf<unsigned char> red(red_tmp);
+    DevBuf<uint32_t> ov_cnt(1);
+    uint32_t spilled = 0;
     for (;;) {
         if (s->obuf.n != size_t(n) * s->offer_cap) s->obuf.alloc(size_t(n) * s->offer_cap);
+        if (s->ov_tgt.n != s->ov_cap) {
+            s->ov_tgt.alloc(s->ov_cap);
+            s->ov_key.alloc(s->ov_cap);
+        }
         s->ocnt.zero();
         counters.zero();
+        ov_cnt.zero();
         JoinArgs ja{ds->data.p, n, ds->ld, s->P, s->S, s->offer_cap, s->gnew.p, s->gold.p, s->gncnt.p,
-                    s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p};
+                    s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p,
+                    ov_cnt.p, s->ov_tgt.p, s->ov_key.p, s->ov_cap};
         const uint32_t wpb = 8;
         LAUNCH(join_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
-        CK(cub::DeviceReduce::Max(red.p, red_tmp, s->ocnt.p, dmax.p, n, stream()));
-        note_launch();
-        uint32_t mx = 0;
-        dmax.download(&mx, 1);
+        ov_cnt.download(&spilled, 1);
         ssync();
-        if (mx <= s->offer_cap) break;
-        s->offer_cap = next_pow2(mx);  // buffers too small: grow and redo (pools untouched so far)
+        if (spilled <= s->ov_cap) break;
+        s->ov_cap = next_pow2(spilled);  // spill list too small: grow and redo (pools untouched so far)
     }
     unsigned long long comps = 0;
     counters.download(&comps, 1);
-    const uint32_t m = next_pow2(s->offer_cap);
-    const size_t per_warp = size_t(m + 2 * s->P) * 8 + 2 * s->P;
-    uint32_t wpb = uint32_t(std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per_warp)));
+    // group the spill list by target: offsets from per-target spill counts
+    DevBuf<uint32_t> ov_off(size_t(n) + 1);
+    DevBuf<uint64_t> ov_sorted_key;
+    if (spilled) {
+        DevBuf<uint32_t> counts(size_t(n) + 1);
+        LAUNCH(spill_counts_kernel, (n + 256) / 256, 256, 0, s->ocnt.p, n, s->offer_cap, counts.p);
+        exclusive_scan(counts.p, ov_off.p, n);
+        DevBuf<uint32_t> tgt_sorted(spilled);
+        ov_sorted_key.alloc(spilled);
+        int bits = 1;
+        while ((uint64_t(1) << bits) < n) ++bits;
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, ov_sorted_key.p,
+                                           spilled, 0, bits, stream()));
+        DevBuf<unsigned char> t(tmp);
+        prof_begin("cub_radix_sort_spill");
+        CK(cub::DeviceRadixSort::SortPairs(t.p, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, ov_sorted_key.p,
+                                           spilled, 0, bits, stream()));
+        prof_end();
+        note_launch();
+    }
+    const size_t per_warp = (kMergeChunk + 3 * size_t(s->P)) * 8 + 2 * s->P;
+    const uint32_t wpb = uint32_t(std::max<size_t>(1, std::min<size_t>(8, (64 * 1024) / per_warp)));
     const size_t smem = wpb * per_warp;
     if (smem > 48 * 1024)
         CK(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    MergeArgs ma{n, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p, counters.p + 1};
-    LAUNCH(merge_kernel, (n + wpb - 1) / wpb, wpb * 32, smem, ma, m);
+    MergeArgs ma{n, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p,
+                 ov_off.p, spilled ? ov_sorted_key.p : s->ov_key.p, counters.p + 1};
+    LAUNCH(merge_kernel, (n + wpb - 1) / wpb, wpb * 32, smem, ma);
     unsigned long long changes = 0;
     CK(cudaMemcpyAsync(&changes, counters.p + 1, 8, cudaMemcpyDeviceToHost, stream()));
     ssync();

@@ -66,6 +66,9 @@ struct annk_state {
     annk::DevBuf<uint64_t> thr;                       // start-of-round pool tail per point
     annk::DevBuf<uint32_t> ocnt;                      // join offer counts
     annk::DevBuf<uint64_t> obuf;                      // n x offer_cap offer keys
+    annk::DevBuf<uint32_t> ov_tgt;                    // spill list: target ids
+    annk::DevBuf<uint64_t> ov_key;                    // spill list: offer keys
+    uint32_t ov_cap = 0;
     int stage = 0;  // 0 none, 1 after rebuild_sample_lists, 2 after union_reverse_lists
     uint64_t join_rows = 0;
     uint32_t offer_cap = 0;

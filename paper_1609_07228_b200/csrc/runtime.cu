@@ -43,6 +43,71 @@ cudaStream_t stream() {
     return g_stream;
 }
 void note_launch() { ++g_launches; }
+
+// ---- per-kernel CUDA-event profiler (annk_profile_*): events are recorded on
+// the library stream around each launch; durations are resolved lazily.
+namespace {
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+bool g_prof = false;
+std::vector<ProfRec> g_prof_pending;
+std::vector<cudaEvent_t> g_prof_free;
+struct ProfAgg {
+    std::string name;
+    uint64_t count = 0;
+    double ms = 0.0;
+};
+std::vector<ProfAgg> g_prof_agg;
+cudaEvent_t prof_event() {
+    if (!g_prof_free.empty()) {
+        cudaEvent_t e = g_prof_free.back();
+        g_prof_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+}
+void prof_resolve() {
+    if (g_prof_pending.empty()) return;
+    CK(cudaStreamSynchronize(g_stream));
+    for (const ProfRec& r : g_prof_pending) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.a, r.b));
+        ProfAgg* agg = nullptr;
+        for (auto& x : g_prof_agg)
+            if (x.name == r.name) agg = &x;
+        if (!agg) {
+            g_prof_agg.push_back(ProfAgg{r.name});
+            agg = &g_prof_agg.back();
+        }
+        agg->count += 1;
+        agg->ms += ms;
+        g_prof_free.push_back(r.a);
+        g_prof_free.push_back(r.b);
+    }
+    g_prof_pending.clear();
+}
+}  // namespace
+
+void prof_begin(const char* name) {
+    if (!g_prof) return;
+    ProfRec r{name, prof_event(), prof_event()};
+    CK(cudaEventRecord(r.a, stream()));
+    g_prof_pending.push_back(r);
+    if (g_prof_pending.size() > 4096) {  // bound the number of live events
+        ProfRec last = g_prof_pending.back();
+        g_prof_pending.pop_back();
+        prof_resolve();
+        g_prof_pending.push_back(last);
+    }
+}
+void prof_end() {
+    if (!g_prof || g_prof_pending.empty()) return;
+    CK(cudaEventRecord(g_prof_pending.back().b, stream()));
+}
 int num_sms() {
     init_runtime();
     return g_sms;
@@ -93,6 +158,33 @@ uint64_t annk_stream(void) {
     return s;
 }
 uint64_t annk_launch_count(void) { return g_launches; }
+
+int annk_profile_enable(int on) {
+    return abi([&] {
+        stream();
+        prof_resolve();
+        g_prof = on != 0;
+    });
+}
+int annk_profile_reset(void) {
+    return abi([&] {
+        prof_resolve();
+        g_prof_agg.clear();
+    });
+}
+// Writes "name count total_ms\n" lines into buf (NUL-terminated).
+int annk_profile_report(char* buf, uint64_t cap) {
+    return abi([&] {
+        prof_resolve();
+        std::string out;
+        for (const auto& x : g_prof_agg)
+            out += x.name + " " + std::to_string(x.count) + " " + std::to_string(x.ms) + "\n";
+        if (cap == 0) return;
+        const size_t m = std::min<size_t>(out.size(), cap - 1);
+        memcpy(buf, out.data(), m);
+        buf[m] = 0;
+    });
+}
 int annk_synchronize(void) {
     return abi([&] { ssync(); });
 }
