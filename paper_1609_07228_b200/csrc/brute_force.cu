@@ -142,6 +142,136 @@ bf_tile_kernel(const float* __restrict__ base, uint32_t nb, uint32_t ld, const f
     }
 }
 
+// Exact u8 datapath (see annk_dataset::u8): whole rows staged as 32-bit words
+// (stride W+4 keeps 16-byte loads conflict-free), each thread accumulates a
+// 2 x 4 block of dp4a dot products; dist = |q|^2 + |b|^2 - 2 q.b exactly.
+__global__ void __launch_bounds__(kThreads)
+bf_tile_u8_kernel(const uint8_t* __restrict__ base8, const int32_t* __restrict__ bnorm, uint32_t nb,
+                  uint32_t ld8, const uint8_t* __restrict__ q8, const int32_t* __restrict__ qnorm, uint32_t nq,
+                  const uint32_t* __restrict__ self_ids, uint32_t k, uint32_t cb, uint32_t splits,
+                  uint32_t tiles_per_split, uint64_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t W = ld8 / 4, WS = W + 4;
+    uint64_t* buf = reinterpret_cast<uint64_t*>(smem);                   // QT x cb
+    uint64_t* thr = buf + size_t(QT) * cb;                               // QT
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(thr + QT);              // QT
+    uint32_t* selfq = cnt + QT;                                          // QT
+    int32_t* qn = reinterpret_cast<int32_t*>(selfq + QT);                // QT
+    int32_t* bn = qn + QT;                                               // BT
+    uint32_t* sq = reinterpret_cast<uint32_t*>(bn + BT);                 // QT x WS (16 B aligned)
+    uint32_t* sb = sq + QT * WS;                                         // BT x WS
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t q0 = blockIdx.x * QT;
+    const uint32_t split = blockIdx.y;
+    const uint32_t n_tiles = (nb + BT - 1) / BT;
+    const uint32_t t_begin = split * tiles_per_split;
+    const uint32_t t_end = min(n_tiles, t_begin + tiles_per_split);
+    if (tid < QT) {
+        cnt[tid] = 0;
+        thr[tid] = kEmptyKey;
+        const uint32_t qi = q0 + tid;
+        selfq[tid] = (self_ids && qi < nq) ? self_ids[qi] : kInvalidId;
+        qn[tid] = qi < nq ? qnorm[qi] : 0;
+    }
+    const uint32_t w4 = W / 4;  // uint4 per row
+    for (uint32_t j = tid; j < QT * w4; j += kThreads) {
+        const uint32_t r = j / w4, c = (j % w4) * 4;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (q0 + r < nq) v = __ldg(reinterpret_cast<const uint4*>(q8 + size_t(q0 + r) * ld8) + j % w4);
+        *reinterpret_cast<uint4*>(sq + r * WS + c) = v;
+    }
+    const uint32_t tq = tid >> 4, tb = tid & 15;
+    __syncthreads();
+    for (uint32_t t = t_begin; t < t_end; ++t) {
+        const uint32_t b0 = t * BT;
+        for (uint32_t j = tid; j < BT * w4; j += kThreads) {
+            const uint32_t r = j / w4, c = (j % w4) * 4;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (b0 + r < nb) v = __ldg(reinterpret_cast<const uint4*>(base8 + size_t(b0 + r) * ld8) + j % w4);
+            *reinterpret_cast<uint4*>(sb + r * WS + c) = v;
+        }
+        if (tid < BT) bn[tid] = b0 + tid < nb ? bnorm[b0 + tid] : 0;
+        __syncthreads();
+        uint32_t dot[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        const uint32_t* qa = sq + tq * WS;
+        const uint32_t* qb = sq + (tq + 16) * WS;
+#pragma unroll 2
+        for (uint32_t w = 0; w < W; w += 4) {
+            const uint4 x0 = *reinterpret_cast<const uint4*>(qa + w);
+            const uint4 x1 = *reinterpret_cast<const uint4*>(qb + w);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const uint4 y = *reinterpret_cast<const uint4*>(sb + (tb + 16 * m) * WS + w);
+                dot[0][m] = __dp4a(x0.x, y.x, dot[0][m]);
+                dot[0][m] = __dp4a(x0.y, y.y, dot[0][m]);
+                dot[0][m] = __dp4a(x0.z, y.z, dot[0][m]);
+                dot[0][m] = __dp4a(x0.w, y.w, dot[0][m]);
+                dot[1][m] = __dp4a(x1.x, y.x, dot[1][m]);
+                dot[1][m] = __dp4a(x1.y, y.y, dot[1][m]);
+                dot[1][m] = __dp4a(x1.z, y.z, dot[1][m]);
+                dot[1][m] = __dp4a(x1.w, y.w, dot[1][m]);
+            }
+        }
+#pragma unroll
+        for (int a2 = 0; a2 < 2; ++a2) {
+            const uint32_t ql = tq + 16 * a2;
+            if (q0 + ql >= nq) continue;
+            const uint64_t th = thr[ql];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const uint32_t bj = b0 + tb + 16 * m;
+                if (bj >= nb || bj == selfq[ql]) continue;
+                const float d = float(qn[ql] + bn[tb + 16 * m] - 2 * int32_t(dot[a2][m]));
+                const uint64_t key = make_key(d, bj);
+                if (key < th) {
+                    const uint32_t slot = atomicAdd(&cnt[ql], 1u);
+                    buf[size_t(ql) * cb + slot] = key;
+                }
+            }
+        }
+        __syncthreads();
+        for (uint32_t ql = warp; ql < QT; ql += kThreads / 32) {
+            const uint32_t c = cnt[ql];
+            if (c + BT <= cb) continue;
+            uint64_t* bq = buf + size_t(ql) * cb;
+            for (uint32_t j = c + lane; j < cb; j += 32) bq[j] = kEmptyKey;
+            __syncwarp();
+            warp_bitonic_sort(bq, cb);
+            if (lane == 0) {
+                const uint32_t keep = min(c, k);
+                cnt[ql] = keep;
+                if (keep == k) thr[ql] = bq[k - 1];
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    for (uint32_t ql = warp; ql < QT; ql += kThreads / 32) {
+        const uint32_t qi = q0 + ql;
+        if (qi >= nq) continue;
+        const uint32_t c = cnt[ql];
+        uint64_t* bq = buf + size_t(ql) * cb;
+        for (uint32_t j = c + lane; j < cb; j += 32) bq[j] = kEmptyKey;
+        __syncwarp();
+        warp_bitonic_sort(bq, cb);
+        uint64_t* o = out + (size_t(qi) * splits + split) * k;
+        for (uint32_t j = lane; j < k; j += 32) o[j] = bq[j];
+        __syncwarp();
+    }
+}
+
+__global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int32_t* __restrict__ norms,
+                                      uint32_t ld8, const uint32_t* __restrict__ rows, uint32_t nr,
+                                      uint8_t* __restrict__ dst, int32_t* __restrict__ dnorms) {
+    const uint32_t r = blockIdx.x;
+    if (r >= nr) return;
+    const uint8_t* s = src + size_t(rows[r]) * ld8;
+    uint8_t* d = dst + size_t(r) * ld8;
+    for (uint32_t j = threadIdx.x; j < ld8; j += blockDim.x) d[j] = s[j];
+    if (threadIdx.x == 0) dnorms[r] = norms[rows[r]];
+}
+
 // Merge `splits` sorted k-lists per query into the final k.
 __global__ void bf_merge_kernel(const uint64_t* __restrict__ part, uint32_t nq, uint32_t splits,
                                 uint32_t k, uint32_t m, uint64_t* __restrict__ out) {
@@ -198,7 +328,8 @@ __global__ void keys_to_ids_kernel(const uint64_t* __restrict__ keys, size_t n, 
 }  // namespace
 
 void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
-                        const uint32_t* self_ids, uint32_t k, uint64_t* out_keys) {
+                        const uint32_t* self_ids, uint32_t k, uint64_t* out_keys, const uint8_t* q8,
+                        const int32_t* qnorm) {
     if (nq == 0) return;
     const uint32_t nb = base->n, ld = base->ld;
     if (q_ld != ld) throw_invalid("brute_force: query stride mismatch");
@@ -212,10 +343,18 @@ void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q
         return;
     }
     const uint32_t cb = next_pow2(k + BT);
-    const size_t smem = size_t(QT) * cb * 8 + QT * 8 + QT * 4 * 2 + size_t(QT + BT) * (DC + 1) * 4;
-    CK(cudaFuncSetAttribute(bf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const bool u8 = base->u8 && q8 != nullptr;
+    const size_t smem =
+        u8 ? size_t(QT) * cb * 8 + QT * 8 + QT * 4 * 3 + BT * 4 + size_t(QT + BT) * (base->ld8 / 4 + 4) * 4
+           : size_t(QT) * cb * 8 + QT * 8 + QT * 4 * 2 + size_t(QT + BT) * (DC + 1) * 4;
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_tile_kernel, kThreads, smem));
+    if (u8) {
+        CK(cudaFuncSetAttribute(bf_tile_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_tile_u8_kernel, kThreads, smem));
+    } else {
+        CK(cudaFuncSetAttribute(bf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_tile_kernel, kThreads, smem));
+    }
     const uint32_t qtiles = (nq + QT - 1) / QT;
     const uint32_t n_tiles = (nb + BT - 1) / BT;
     const uint32_t want = uint32_t(num_sms()) * std::max(per_sm, 1) * 2;
@@ -223,13 +362,16 @@ void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q
     splits = std::min(splits, std::max(1u, 4096u / k));  // merge list fits 32 KB per warp
     const uint32_t tps = (n_tiles + splits - 1) / splits;
     splits = (n_tiles + tps - 1) / tps;
-    if (splits == 1) {
-        LAUNCH(bf_tile_kernel, dim3(qtiles, 1), kThreads, smem, base->data.p, nb, ld, qdata, nq, self_ids, k,
-               cb, 1u, tps, out_keys);
+    DevBuf<uint64_t> part(splits == 1 ? 0 : size_t(nq) * splits * k);
+    uint64_t* dst = splits == 1 ? out_keys : part.p;
+    if (u8) {
+        LAUNCH(bf_tile_u8_kernel, dim3(qtiles, splits), kThreads, smem, base->data8.p, base->norms8.p, nb,
+               base->ld8, q8, qnorm, nq, self_ids, k, cb, splits, tps, dst);
     } else {
-        DevBuf<uint64_t> part(size_t(nq) * splits * k);
         LAUNCH(bf_tile_kernel, dim3(qtiles, splits), kThreads, smem, base->data.p, nb, ld, qdata, nq, self_ids,
-               k, cb, splits, tps, part.p);
+               k, cb, splits, tps, dst);
+    }
+    if (splits > 1) {
         const uint32_t m = next_pow2(splits * k);
         const uint32_t wpb = std::max(1u, std::min(8u, uint32_t(64 * 1024 / (m * 8))));
         CK(cudaFuncSetAttribute(bf_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wpb * m * 8)));
@@ -275,8 +417,10 @@ int annk_brute_force_knn(const annk_dataset* base, const annk_dataset* queries, 
             selfids.alloc(nq);
             selfids.upload(iota.data(), nq);
         }
-        brute_force_device(base, self ? base->data.p : queries->data.p, base->ld, nq,
-                           self ? selfids.p : nullptr, k, keys.p);
+        const annk_dataset* qs = self ? base : queries;
+        const bool u8 = base->u8 && qs->u8 && qs->ld8 == base->ld8;
+        brute_force_device(base, qs->data.p, base->ld, nq, self ? selfids.p : nullptr, k, keys.p,
+                           u8 ? qs->data8.p : nullptr, u8 ? qs->norms8.p : nullptr);
         finish_keys(keys, size_t(nq) * k, out_ids, out_dists);
         if (dist_comps) *dist_comps += uint64_t(nq) * (self ? base->n - 1 : base->n);
     });
@@ -294,8 +438,14 @@ int annk_brute_force_rows(const annk_dataset* base, const uint32_t* rows, uint32
         drows.upload(rows, n_rows);
         DevBuf<float> q(size_t(n_rows) * base->ld);
         LAUNCH(gather_rows_kernel, n_rows, 128, 0, base->data.p, base->ld, drows.p, n_rows, q.p);
+        DevBuf<uint8_t> q8(base->u8 ? size_t(n_rows) * base->ld8 : 0);
+        DevBuf<int32_t> qn(base->u8 ? n_rows : 0);
+        if (base->u8)
+            LAUNCH(gather_rows_u8_kernel, n_rows, 128, 0, base->data8.p, base->norms8.p, base->ld8, drows.p, n_rows,
+                   q8.p, qn.p);
         DevBuf<uint64_t> keys(size_t(n_rows) * k);
-        brute_force_device(base, q.p, base->ld, n_rows, drows.p, k, keys.p);
+        brute_force_device(base, q.p, base->ld, n_rows, drows.p, k, keys.p, base->u8 ? q8.p : nullptr,
+                           base->u8 ? qn.p : nullptr);
         finish_keys(keys, size_t(n_rows) * k, out_ids, out_dists);
     });
 }

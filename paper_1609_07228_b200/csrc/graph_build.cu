@@ -119,6 +119,9 @@ struct InitArgs {
     uint32_t* sizes;
     unsigned long long* comps;
     uint32_t* overflow;  // [count, ids...]
+    const uint8_t* x8;   // exact u8 rows (nullptr: fp32 path)
+    uint32_t ld8;
+    const int32_t* norms8;
 };
 
 // Collects point i's candidate set (graph_build.cpp:266-280) into cand;
@@ -182,8 +185,12 @@ __device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, uint3
         const uint32_t id = j < u ? cand[j] : kInvalidId;
         const bool keep = j < u && id != i;
         const uint32_t b = __ballot_sync(0xffffffffu, keep);
-        if (keep) keys[nk + __popc(b & ((1u << lane) - 1u))] =
-            make_key(l2_exact_ldg(q, a.x + size_t(id) * a.ld, a.ld), id);
+        if (keep) {
+            const float d = a.x8 ? l2_u8(a.x8 + size_t(i) * a.ld8, a.x8 + size_t(id) * a.ld8, a.ld8,
+                                         a.norms8[i], a.norms8[id])
+                                 : l2_exact_ldg(q, a.x + size_t(id) * a.ld, a.ld);
+            keys[nk + __popc(b & ((1u << lane) - 1u))] = make_key(d, id);
+        }
         nk += __popc(b);
     }
     const uint32_t mk = next_pow2(max(nk, 1u));
@@ -204,7 +211,8 @@ __device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, uint3
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint32_t sib_cap) {
+__global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint32_t sib_cap,
+                                                               const uint32_t* __restrict__ order) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t warp = threadIdx.x / 32, lane = lane_id();
     const size_t per_warp = (size_t(kInitCap) * 4 + size_t(kInitCap) * 8 + size_t(a.ld) * 4 +
@@ -215,7 +223,10 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
     float* q = reinterpret_cast<float*>(base + size_t(kInitCap) * 12);
     uint32_t* sib = reinterpret_cast<uint32_t*>(base + size_t(kInitCap) * 12 + size_t(a.ld) * 4);
     uint32_t* s_cnt = sib + 2 * sib_cap;
-    for (uint32_t i = blockIdx.x * kInitWarps + warp; i < a.n; i += gridDim.x * kInitWarps) {
+    for (uint32_t ord = blockIdx.x * kInitWarps + warp; ord < a.n; ord += gridDim.x * kInitWarps) {
+        // visit points in tree-0 leaf order: concurrently processed points share
+        // most candidate rows, so the gathers hit L2
+        const uint32_t i = order ? order[ord] : ord;
         for (uint32_t j = lane; j < a.ld; j += 32) q[j] = a.x[size_t(i) * a.ld + j];
         __syncwarp();
         const uint32_t c = init_collect(a, i, q, cand, kInitCap, sib, sib_cap, s_cnt);
@@ -429,6 +440,233 @@ __global__ void join_kernel(JoinArgs a) {
             offer(a, j, k2, d);
             offer(a, k2, j, d);
         }
+    }
+    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
+    if (lane == 0 && comps) atomicAdd(a.comps, comps);
+}
+
+// Staged join: one CTA per point.  The point's list rows (new first, then
+// old) are copied into shared memory with a padded stride (ld+4 floats keeps
+// float4 alignment and makes 8 consecutive rows hit distinct 16-byte bank
+// groups).  Needed pairs are {(x, y): x < A, x < y < R}: new x new upper
+// triangle plus new x old.  Work item = (group of 4 new rows, 32 partner
+// columns starting right after the group's first row); each lane owns one
+// partner column and accumulates 4 exact distances (the 4 new rows are
+// broadcast float4 loads), so the kernel is FP32-pipe bound instead of
+// L2-gather bound.  Owners of every offer are list members, so their
+// start-of-round thresholds are staged too.
+constexpr uint32_t kJoinThreads = 256;
+constexpr uint32_t kJoinXR = 4;
+
+__global__ void __launch_bounds__(kJoinThreads)
+join_staged_kernel(JoinArgs a, const uint32_t* __restrict__ order, uint32_t rmax) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t rs = a.ld + 4;  // padded row stride (floats)
+    float* rows = reinterpret_cast<float*>(smem);
+    uint64_t* thr_s = reinterpret_cast<uint64_t*>(rows + size_t(rmax) * rs);
+    uint32_t* ids = reinterpret_cast<uint32_t*>(thr_s + rmax);
+    uint32_t* gstart = ids + rmax;  // item prefix per row group (<= rmax/4 + 2)
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr uint32_t kWarps = kJoinThreads / 32;
+    unsigned long long comps = 0;
+    for (uint32_t ord = blockIdx.x; ord < a.n; ord += gridDim.x) {
+        const uint32_t i = order ? order[ord] : ord;
+        const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
+        if (A == 0) continue;  // uniform across the CTA
+        const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
+        const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
+        for (uint32_t r = tid; r < R; r += kJoinThreads) {
+            const uint32_t id = r < A ? nw[r] : od[r - A];
+            ids[r] = id;
+            thr_s[r] = a.thr[id];
+        }
+        // item table: group g covers new rows [4g, 4g+4), partners from 4g+1 up to R
+        if (tid == 0) {
+            uint32_t acc = 0;
+            const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
+            for (uint32_t g = 0; g < ng; ++g) {
+                gstart[g] = acc;
+                const uint32_t y0 = g * kJoinXR + 1;
+                acc += R > y0 ? (R - y0 + 31) / 32 : 0;
+            }
+            gstart[ng] = acc;
+        }
+        __syncthreads();
+        const uint32_t v4 = a.ld / 4;
+        for (uint32_t j = tid; j < R * v4; j += kJoinThreads) {
+            const uint32_t r = j / v4, c = (j % v4) * 4;
+            const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + size_t(ids[r]) * a.ld + c));
+            *reinterpret_cast<float4*>(rows + size_t(r) * rs + c) = v;
+        }
+        __syncthreads();
+        const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
+        const uint32_t n_items = gstart[ng];
+        for (uint32_t item = warp; item < n_items; item += kWarps) {
+            uint32_t g = 0;
+            while (gstart[g + 1] <= item) ++g;
+            const uint32_t x0 = g * kJoinXR;
+            const uint32_t y = x0 + 1 + (item - gstart[g]) * 32 + lane;
+            const bool yv = y < R;
+            const float* yr = rows + size_t(yv ? y : 0) * rs;
+            const float* xr = rows + size_t(x0) * rs;
+            float acc[kJoinXR];
+#pragma unroll
+            for (uint32_t k = 0; k < kJoinXR; ++k) acc[k] = 0.0f;
+            for (uint32_t c = 0; c < a.ld; c += 4) {
+                const float4 b = *reinterpret_cast<const float4*>(yr + c);
+#pragma unroll
+                for (uint32_t k = 0; k < kJoinXR; ++k) {
+                    // rows x0+k beyond A read (unused) staged rows or padding; results are discarded
+                    const float4 x = *reinterpret_cast<const float4*>(xr + size_t(min(x0 + k, R - 1) - x0) * rs + c);
+                    float d;
+                    d = __fsub_rn(x.x, b.x); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
+                    d = __fsub_rn(x.y, b.y); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
+                    d = __fsub_rn(x.z, b.z); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
+                    d = __fsub_rn(x.w, b.w); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
+                }
+            }
+            if (yv) {
+                const uint32_t idy = ids[y];
+                const uint64_t thy = thr_s[y];
+#pragma unroll
+                for (uint32_t k = 0; k < kJoinXR; ++k) {
+                    const uint32_t x = x0 + k;
+                    if (x >= A || y <= x) continue;
+                    const uint32_t idx = ids[x];
+                    if (idx == idy) continue;  // graph_build.cpp:146 (l == j)
+                    ++comps;
+                    const float d = acc[k];
+                    const uint64_t kx = make_key(d, idy);  // offer y to x's pool
+                    if (kx < thr_s[x]) {
+                        const uint32_t slot = atomicAdd(&a.ocnt[idx], 1u);
+                        if (slot < a.cap) a.obuf[size_t(idx) * a.cap + slot] = kx;
+                        else {
+                            const uint32_t o = atomicAdd(a.ov_cnt, 1u);
+                            if (o < a.ov_cap) { a.ov_tgt[o] = idx; a.ov_key[o] = kx; }
+                        }
+                    }
+                    const uint64_t ky = make_key(d, idx);  // offer x to y's pool
+                    if (ky < thy) {
+                        const uint32_t slot = atomicAdd(&a.ocnt[idy], 1u);
+                        if (slot < a.cap) a.obuf[size_t(idy) * a.cap + slot] = ky;
+                        else {
+                            const uint32_t o = atomicAdd(a.ov_cnt, 1u);
+                            if (o < a.ov_cap) { a.ov_tgt[o] = idy; a.ov_key[o] = ky; }
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
+    if (lane == 0 && comps) atomicAdd(a.comps, comps);
+}
+
+__device__ __forceinline__ void push_offer(const JoinArgs& a, uint32_t owner, uint64_t key) {
+    const uint32_t slot = atomicAdd(&a.ocnt[owner], 1u);
+    if (slot < a.cap) {
+        a.obuf[size_t(owner) * a.cap + slot] = key;
+    } else {
+        const uint32_t o = atomicAdd(a.ov_cnt, 1u);
+        if (o < a.ov_cap) {
+            a.ov_tgt[o] = owner;
+            a.ov_key[o] = key;
+        }
+    }
+}
+
+// Same schedule as join_staged_kernel on the exact u8 datapath: rows staged as
+// bytes (ld8 + 16 stride), 4 dp4a per 16 bytes, dist = |x|^2 + |y|^2 - 2 x.y.
+__global__ void __launch_bounds__(kJoinThreads)
+join_u8_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const int32_t* __restrict__ norms,
+               const uint32_t* __restrict__ order, uint32_t rmax) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t rs = ld8 + 16;  // padded row stride (bytes): conflict-free 16-byte loads
+    uint8_t* rows = smem;
+    uint64_t* thr_s = reinterpret_cast<uint64_t*>(rows + size_t(rmax) * rs);
+    uint32_t* ids = reinterpret_cast<uint32_t*>(thr_s + rmax);
+    int32_t* nrm = reinterpret_cast<int32_t*>(ids + rmax);
+    uint32_t* gstart = reinterpret_cast<uint32_t*>(nrm + rmax);
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr uint32_t kWarps = kJoinThreads / 32;
+    unsigned long long comps = 0;
+    for (uint32_t ord = blockIdx.x; ord < a.n; ord += gridDim.x) {
+        const uint32_t i = order ? order[ord] : ord;
+        const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
+        if (A == 0) continue;
+        const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
+        const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
+        for (uint32_t r = tid; r < R; r += kJoinThreads) {
+            const uint32_t id = r < A ? nw[r] : od[r - A];
+            ids[r] = id;
+            thr_s[r] = a.thr[id];
+            nrm[r] = norms[id];
+        }
+        if (tid == 0) {
+            uint32_t acc = 0;
+            const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
+            for (uint32_t g = 0; g < ng; ++g) {
+                gstart[g] = acc;
+                const uint32_t y0 = g * kJoinXR + 1;
+                acc += R > y0 ? (R - y0 + 31) / 32 : 0;
+            }
+            gstart[ng] = acc;
+        }
+        __syncthreads();
+        const uint32_t v16 = ld8 / 16;
+        for (uint32_t j = tid; j < R * v16; j += kJoinThreads) {
+            const uint32_t r = j / v16, c = (j % v16) * 16;
+            *reinterpret_cast<uint4*>(rows + size_t(r) * rs + c) =
+                __ldg(reinterpret_cast<const uint4*>(x8 + size_t(ids[r]) * ld8 + c));
+        }
+        __syncthreads();
+        const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
+        const uint32_t n_items = gstart[ng];
+        for (uint32_t item = warp; item < n_items; item += kWarps) {
+            uint32_t g = 0;
+            while (gstart[g + 1] <= item) ++g;
+            const uint32_t x0 = g * kJoinXR;
+            const uint32_t y = x0 + 1 + (item - gstart[g]) * 32 + lane;
+            const bool yv = y < R;
+            const uint8_t* yr = rows + size_t(yv ? y : 0) * rs;
+            const uint8_t* xr[kJoinXR];
+#pragma unroll
+            for (uint32_t k = 0; k < kJoinXR; ++k) xr[k] = rows + size_t(min(x0 + k, R - 1)) * rs;
+            uint32_t dot[kJoinXR];
+#pragma unroll
+            for (uint32_t k = 0; k < kJoinXR; ++k) dot[k] = 0;
+            for (uint32_t c = 0; c < ld8; c += 16) {
+                const uint4 b = *reinterpret_cast<const uint4*>(yr + c);
+#pragma unroll
+                for (uint32_t k = 0; k < kJoinXR; ++k) {
+                    const uint4 x = *reinterpret_cast<const uint4*>(xr[k] + c);
+                    dot[k] = __dp4a(x.x, b.x, dot[k]);
+                    dot[k] = __dp4a(x.y, b.y, dot[k]);
+                    dot[k] = __dp4a(x.z, b.z, dot[k]);
+                    dot[k] = __dp4a(x.w, b.w, dot[k]);
+                }
+            }
+            if (yv) {
+                const uint32_t idy = ids[y];
+                const uint64_t thy = thr_s[y];
+                const int32_t ny = nrm[y];
+#pragma unroll
+                for (uint32_t k = 0; k < kJoinXR; ++k) {
+                    const uint32_t x = x0 + k;
+                    if (x >= A || y <= x) continue;
+                    const uint32_t idx = ids[x];
+                    if (idx == idy) continue;  // graph_build.cpp:146 (l == j)
+                    ++comps;
+                    const float d = float(nrm[x] + ny - 2 * int32_t(dot[k]));
+                    const uint64_t kx = make_key(d, idy);
+                    if (kx < thr_s[x]) push_offer(a, idx, kx);
+                    const uint64_t ky = make_key(d, idx);
+                    if (ky < thy) push_offer(a, idy, ky);
+                }
+            }
+        }
+        __syncthreads();
     }
     for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
     if (lane == 0 && comps) atomicAdd(a.comps, comps);
@@ -799,8 +1037,11 @@ void do_union(annk_state* s) {
 uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
     const uint32_t n = s->n;
     // fixed per-point offer slots; overflow (hub points) spills to a global list
+    // capacities learned by earlier rounds (any state) avoid a redo of the join
+    static uint64_t spill_per_point_hint = 8;
     if (s->offer_cap == 0) s->offer_cap = std::max(2 * s->P, 64u);
-    if (s->ov_cap == 0) s->ov_cap = std::max<uint32_t>(1u << 20, n * 8u);
+    if (s->ov_cap == 0)
+        s->ov_cap = uint32_t(std::min<uint64_t>(std::max<uint64_t>(1u << 20, n * spill_per_point_hint), 1u << 31));
     DevBuf<unsigned long long> counters(2);
     DevBuf<uint32_t> ov_cnt(1);
     uint32_t spilled = 0;
@@ -816,12 +1057,34 @@ uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
         JoinArgs ja{ds->data.p, n, ds->ld, s->P, s->S, s->offer_cap, s->gnew.p, s->gold.p, s->gncnt.p,
                     s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p,
                     ov_cnt.p, s->ov_tgt.p, s->ov_key.p, s->ov_cap};
-        const uint32_t wpb = 8;
-        LAUNCH(join_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
+        const uint32_t rmax = 3 * s->S + s->P;  // |new| <= 2S, |old| <= P + S
+        const size_t staged_smem = size_t(rmax) * (ds->ld + 4) * 4 + size_t(rmax) * 12 + (rmax / 4 + 2) * 4;
+        const size_t u8_smem = size_t(rmax) * (ds->ld8 + 16) + size_t(rmax) * 16 + (rmax / 4 + 2) * 4;
+        if (ds->u8 && u8_smem <= 110 * 1024) {
+            CK(cudaFuncSetAttribute(join_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(u8_smem)));
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_u8_kernel, kJoinThreads, u8_smem));
+            const uint32_t grid = std::min<uint32_t>(n, uint32_t(num_sms()) * std::max(per_sm, 1));
+            LAUNCH(join_u8_kernel, grid, kJoinThreads, u8_smem, ja, ds->data8.p, ds->ld8, ds->norms8.p,
+                   s->order.n ? s->order.p : nullptr, rmax);
+        } else if (staged_smem <= 110 * 1024) {
+            CK(cudaFuncSetAttribute(join_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(staged_smem)));
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_staged_kernel, kJoinThreads,
+                                                             staged_smem));
+            const uint32_t grid = std::min<uint32_t>(n, uint32_t(num_sms()) * std::max(per_sm, 1));
+            LAUNCH(join_staged_kernel, grid, kJoinThreads, staged_smem, ja, s->order.n ? s->order.p : nullptr,
+                   rmax);
+        } else {
+            const uint32_t wpb = 8;
+            LAUNCH(join_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
+        }
         ov_cnt.download(&spilled, 1);
         ssync();
         if (spilled <= s->ov_cap) break;
         s->ov_cap = next_pow2(spilled);  // spill list too small: grow and redo (pools untouched so far)
+        spill_per_point_hint = std::max<uint64_t>(spill_per_point_hint, (uint64_t(s->ov_cap) + n - 1) / n);
     }
     unsigned long long comps = 0;
     counters.download(&comps, 1);
@@ -903,7 +1166,8 @@ int annk_init_graph(const annk_dataset* ds, const annk_forest* fc, uint32_t k, u
         DevBuf<uint32_t> overflow(size_t(n) + 1);
         CK(cudaMemsetAsync(overflow.p, 0, 4, stream()));
         InitArgs a{ds->data.p, n, ds->ld, f->n_trees, conquer_depth, pool_cap, f->views.p,
-                   s->keys.p, s->flags.p, s->sizes.p, comps.p, overflow.p};
+                   s->keys.p, s->flags.p, s->sizes.p, comps.p, overflow.p,
+                   ds->u8 ? ds->data8.p : nullptr, ds->ld8, ds->u8 ? ds->norms8.p : nullptr};
         const uint32_t sib_full = f->n_trees * (max_depth + 1);
         const uint32_t sib_cap = std::min<uint32_t>(sib_full, 512);
         const size_t per_warp = (size_t(kInitCap) * 12 + size_t(ds->ld) * 4 + size_t(sib_cap) * 8 + 16 + 15) &
@@ -911,7 +1175,9 @@ int annk_init_graph(const annk_dataset* ds, const annk_forest* fc, uint32_t k, u
         const size_t smem = per_warp * kInitWarps;
         CK(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         const uint32_t grid = std::min<uint32_t>((n + kInitWarps - 1) / kInitWarps, uint32_t(num_sms()) * 16);
-        LAUNCH(init_kernel, grid, kInitWarps * 32, smem, a, sib_cap);
+        s->order.alloc(n);
+        CK(cudaMemcpyAsync(s->order.p, f->trees[0].pidx.p, size_t(n) * 4, cudaMemcpyDeviceToDevice, stream()));
+        LAUNCH(init_kernel, grid, kInitWarps * 32, smem, a, sib_cap, s->order.p);
         uint32_t n_over = 0;
         overflow.download(&n_over, 1);
         ssync();

@@ -21,7 +21,32 @@ struct KdNodeDev {
 struct annk_dataset {
     uint32_t n = 0, dim = 0, ld = 0;  // ld = padded row stride (floats), multiple of 4
     annk::DevBuf<float> data;         // n x ld, zero padded
+    // Exact u8 datapath: when every value is an integer in [0,255] and
+    // dim * 255^2 < 2^24, the reference's sequential fp32 l2_sq never rounds,
+    // so ||a||^2 + ||b||^2 - 2 a.b in int32 (dp4a) is bit-identical to it.
+    bool u8 = false;
+    uint32_t ld8 = 0;                 // bytes per u8 row, multiple of 16
+    annk::DevBuf<uint8_t> data8;      // n x ld8, zero padded
+    annk::DevBuf<int32_t> norms8;     // n squared norms
 };
+
+void make_u8(annk_dataset* ds);  // runtime.cu: enables the u8 path when exact
+
+// Integer-exact squared distance of two u8 rows (ld8 bytes, 16-byte aligned):
+// na + nb - 2 * dot, dot by dp4a on 4-byte lanes.
+__device__ __forceinline__ float l2_u8(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
+                                       uint32_t ld8, int32_t na, int32_t nb) {
+    uint32_t dot = 0;  // unsigned overload: bytes are 0..255
+    for (uint32_t i = 0; i < ld8; i += 16) {
+        const uint4 x = *reinterpret_cast<const uint4*>(a + i);
+        const uint4 y = *reinterpret_cast<const uint4*>(b + i);
+        dot = __dp4a(x.x, y.x, dot);
+        dot = __dp4a(x.y, y.y, dot);
+        dot = __dp4a(x.z, y.z, dot);
+        dot = __dp4a(x.w, y.w, dot);
+    }
+    return float(na + nb - 2 * int32_t(dot));
+}
 
 struct TreeDev {
     annk::DevBuf<KdNodeDev> nodes;
@@ -68,6 +93,7 @@ struct annk_state {
     annk::DevBuf<uint64_t> obuf;                      // n x offer_cap offer keys
     annk::DevBuf<uint32_t> ov_tgt;                    // spill list: target ids
     annk::DevBuf<uint64_t> ov_key;                    // spill list: offer keys
+    annk::DevBuf<uint32_t> order;                     // point visit order (tree-0 leaf order) for L2 locality
     uint32_t ov_cap = 0;
     int stage = 0;  // 0 none, 1 after rebuild_sample_lists, 2 after union_reverse_lists
     uint64_t join_rows = 0;

@@ -123,6 +123,50 @@ void set_error(const std::string& m) { g_err = m; }
 
 using namespace annk;
 
+// Builds the u8 copy + norms; flags any value that is not an integer in [0,255].
+__global__ void to_u8_kernel(const float* __restrict__ x, uint32_t n, uint32_t dim, uint32_t ld,
+                             uint8_t* __restrict__ x8, uint32_t ld8, int32_t* __restrict__ norms,
+                             uint32_t* __restrict__ bad) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const float* r = x + size_t(warp) * ld;
+    uint8_t* o = x8 + size_t(warp) * ld8;
+    int32_t nrm = 0;
+    bool ok = true;
+    for (uint32_t j = lane; j < ld8; j += 32) {
+        const float v = j < dim ? r[j] : 0.0f;
+        const bool good = v >= 0.0f && v <= 255.0f && v == floorf(v);
+        ok &= good;
+        const uint32_t b = good ? uint32_t(v) : 0u;
+        o[j] = uint8_t(b);
+        nrm += int32_t(b * b);
+    }
+    for (int s = 16; s > 0; s >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, s);
+    if (lane == 0) norms[warp] = nrm;
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(bad, 1u);
+}
+
+void make_u8(annk_dataset* ds) {
+    ds->u8 = false;
+    if (ds->n == 0 || uint64_t(ds->dim) * 255ull * 255ull >= (1ull << 24)) return;
+    ds->ld8 = (ds->dim + 15) & ~15u;
+    ds->data8.alloc(size_t(ds->n) * ds->ld8);
+    ds->norms8.alloc(ds->n);
+    DevBuf<uint32_t> bad(1);
+    bad.zero();
+    LAUNCH(to_u8_kernel, (ds->n + 7) / 8, 256, 0, ds->data.p, ds->n, ds->dim, ds->ld, ds->data8.p, ds->ld8,
+           ds->norms8.p, bad.p);
+    uint32_t h = 0;
+    bad.download(&h, 1);
+    ssync();
+    if (h) {
+        ds->data8.release();
+        ds->norms8.release();
+        return;
+    }
+    ds->u8 = true;
+}
+
 // Upload with zero padding to the ld stride.
 static void upload_rows(annk_dataset* ds, const float* host) {
     const size_t n = ds->n, dim = ds->dim, ld = ds->ld;
@@ -202,6 +246,8 @@ int annk_dataset_create(const float* host, uint32_t n, uint32_t dim, annk_datase
         ds->ld = (dim + 3) & ~3u;
         try {
             upload_rows(ds, host);
+            const char* off = getenv("ANNK_DISABLE_U8");
+            if (!(off && off[0] == '1')) make_u8(ds);
             ssync();
         } catch (...) {
             delete ds;

@@ -60,6 +60,12 @@ struct SearchArgs {
     uint64_t* mtstate;   // slots x 312 (random init)
     uint64_t* out_keys;  // nq x k_return
     uint64_t* stats;     // nq x 4
+    // exact u8 datapath (nullptr: fp32 path)
+    const uint8_t* x8;
+    const int32_t* norms8;
+    uint32_t ld8;
+    const uint8_t* q8;
+    const int32_t* qnorms8;
 };
 
 struct Smem {
@@ -72,6 +78,8 @@ struct Smem {
     uint32_t* expand;   // P
     uint32_t* scan;     // kThreads/32 + 1
     float* q;           // ld
+    uint8_t* q8;        // ld8
+    int32_t qnorm;
     uint32_t* ctr;      // [0] pool size, [1] buf count, [2] visited count, [3] seeds, [4] reserve size,
                         // [5] expand count, [6] leaves visited, [7] hops
 };
@@ -100,6 +108,7 @@ __device__ __forceinline__ bool mark_visited(const SearchArgs& a, uint32_t slot,
 
 __device__ __forceinline__ float qdist(const SearchArgs& a, const Smem& s, uint32_t id) {
     DCHK(id < a.n);
+    if (a.x8) return l2_u8(s.q8, a.x8 + size_t(id) * a.ld8, a.ld8, s.qnorm, a.norms8[id]);
     return l2_exact_ldg(s.q, a.x + size_t(id) * a.ld, a.ld);
 }
 
@@ -190,6 +199,7 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
     {
         unsigned char* p = raw;
         s.q = reinterpret_cast<float*>(p); p += size_t(a.ld) * 4;  // first: float4 loads need 16 B alignment
+        s.q8 = p; p += a.x8 ? a.ld8 : 0;
         s.pool = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
         s.tmp = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
         s.seeds = reinterpret_cast<uint64_t*>(p); p += size_t(a.seed_cap) * 8;
@@ -203,6 +213,10 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
     const uint32_t slot = blockIdx.x, tid = threadIdx.x;
     for (uint32_t qi = blockIdx.x; qi < a.nq; qi += gridDim.x) {
         for (uint32_t j = tid; j < a.ld; j += kThreads) s.q[j] = a.q[size_t(qi) * a.ld + j];
+        if (a.x8) {
+            for (uint32_t j = tid; j < a.ld8; j += kThreads) s.q8[j] = a.q8[size_t(qi) * a.ld8 + j];
+            s.qnorm = a.qnorms8[qi];
+        }
         if (tid < 16) s.ctr[tid] = 0;
         __syncthreads();
         // ------------------------------------------------ seeding
@@ -428,7 +442,11 @@ __global__ void keys_split_kernel(const uint64_t* __restrict__ keys, size_t cnt,
     }
 }
 
-void run_search(annk_searcher* sr, const float* dq, uint32_t nq, const annk_search_params* p, uint32_t* out_ids,
+void check_status(int st) {
+    if (st != 0) throw Error(st, annk_last_error());
+}
+
+void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_params* p, uint32_t* out_ids,
                 float* out_dists, uint64_t* stats_out) {
     const annk_dataset* base = sr->base;
     const annk_forest* f = sr->forest;
@@ -437,6 +455,7 @@ void run_search(annk_searcher* sr, const float* dq, uint32_t nq, const annk_sear
     if (p->expansion > p->pool_size) throw_invalid("search: need expansion <= pool_size");
     if (p->k_return > base->n) throw_invalid("search: k_return exceeds n");
     if (!p->random_init && !f) throw_invalid("search: tree-seeded search needs a forest");
+    const uint32_t nq = qds->n;
     if (nq == 0) return;
     uint32_t nt = 0, n_node = 0, leaf_cap = 1, max_depth = 0;
     if (!p->random_init) {
@@ -453,7 +472,7 @@ void run_search(annk_searcher* sr, const float* dq, uint32_t nq, const annk_sear
     const uint32_t seed_cap = next_pow2(uint32_t(std::max<uint64_t>(seed_bound, 1)));
     const uint32_t P = p->pool_size;
     const size_t smem = size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kBuf) * 8 + size_t(base->ld) * 4 +
-                        size_t(P) * 4 + 128 + size_t(P) * 2 + 16;
+                        size_t(P) * 4 + 128 + size_t(P) * 2 + 16 + base->ld8;
     if (smem > size_t(max_smem_optin()))
         throw_invalid("search: pool_size/seed budget exceeds on-chip capacity");
     CK(cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -470,10 +489,12 @@ void run_search(annk_searcher* sr, const float* dq, uint32_t nq, const annk_sear
     DevBuf<uint32_t> leaves(std::max<size_t>(size_t(slots) * nt * n_node, 1));
     DevBuf<uint64_t> mt(p->random_init ? size_t(slots) * 312 : 1);
     DevBuf<uint64_t> keys(size_t(nq) * p->k_return), st(size_t(nq) * 4);
-    SearchArgs a{base->data.p, base->n, base->ld, dq, nq, f ? f->views.p : nullptr, nt, n_node, leaf_cap,
+    const bool u8 = base->u8 && qds->u8 && base->ld8 == qds->ld8;
+    SearchArgs a{base->data.p, base->n, base->ld, qds->data.p, nq, f ? f->views.p : nullptr, nt, n_node, leaf_cap,
                  sr->graph.p, sr->gk, p->k_return, P, p->expansion, p->iters, p->random_init,
                  p->random_seed_count, p->seed, seed_cap, bitmap.p, words, vlist.p, vcap, heaps.p, hcap,
-                 leaves.p, mt.p, keys.p, st.p};
+                 leaves.p, mt.p, keys.p, st.p, u8 ? base->data8.p : nullptr, u8 ? base->norms8.p : nullptr,
+                 base->ld8, u8 ? qds->data8.p : nullptr, u8 ? qds->norms8.p : nullptr};
     LAUNCH(search_kernel, slots, kThreads, smem, a);
     const size_t cnt = size_t(nq) * p->k_return;
     DevBuf<uint32_t> di(cnt);
@@ -523,17 +544,11 @@ int annk_search(annk_searcher* s, const float* queries, uint32_t nq, uint32_t di
     return abi([&] {
         if (!s || !p) throw_invalid("search: null argument");
         if (dim != s->base->dim) throw_invalid("search: query length mismatch");
-        const uint32_t ld = s->base->ld;
-        DevBuf<float> dq(std::max<size_t>(size_t(nq) * ld, 1));
-        if (nq) {
-            if (ld == dim) {
-                dq.upload(queries, size_t(nq) * dim);
-            } else {
-                dq.zero();
-                CK(cudaMemcpy2DAsync(dq.p, ld * 4, queries, dim * 4, dim * 4, nq, cudaMemcpyHostToDevice, stream()));
-            }
-        }
-        run_search(s, dq.p, nq, p, out_ids, out_dists, stats);
+        // a transient query set (uploads and gets the same exactness check as a dataset)
+        annk_dataset* qds = nullptr;
+        check_status(annk_dataset_create(queries, nq, dim, &qds));
+        std::unique_ptr<annk_dataset> hold(qds);
+        run_search(s, qds, p, out_ids, out_dists, stats);
     });
 }
 
@@ -542,7 +557,7 @@ int annk_search_dataset(annk_searcher* s, const annk_dataset* queries, const ann
     return abi([&] {
         if (!s || !p || !queries) throw_invalid("search: null argument");
         if (queries->dim != s->base->dim) throw_invalid("search: query length mismatch");
-        run_search(s, queries->data.p, queries->n, p, out_ids, out_dists, stats);
+        run_search(s, queries, p, out_ids, out_dists, stats);
     });
 }
 

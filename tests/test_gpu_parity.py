@@ -288,3 +288,39 @@ def test_search_validation():
         s.search(np.zeros(3, np.float32), A.SearchParams(5, 10, 10))
     with pytest.raises(A.InvalidArgument):
         A.GraphSearcher(A.gen_synthetic(10, 4, 1), None, g)
+
+
+# ------------------------------------------------------ exact u8 datapath
+
+@pytest.mark.parametrize("u8", [True, False])
+def test_integer_data_both_datapaths_bit_exact(u8, monkeypatch):
+    """Integer-valued data runs the exact u8/dp4a datapath by default; forcing
+    the fp32 path (ANNK_DISABLE_U8=1) must give the very same bits, and both must
+    equal the oracle (pools, lists, dist_comps, brute force, search)."""
+    if not u8:
+        monkeypatch.setenv("ANNK_DISABLE_U8", "1")
+    o = ora()
+    x = mixture(6000, 128, 30, 5)
+    q = mixture(80, 128, 30, 5, stream=2)
+    vo = o.vs(x)
+    ids_o, d_o, _ = o.brute_force(vo, None, 30, workers=8, with_dists=True)
+    ids, d = A.brute_force_knn(x, None, 30, with_dists=True)
+    np.testing.assert_array_equal(ids, ids_o)
+    np.testing.assert_array_equal(d.view(np.uint32), d_o.view(np.uint32))
+    np.testing.assert_array_equal(A.brute_force_knn(x, q, 30), o.brute_force(vo, o.vs(q), 30, workers=8))
+    rows = np.array([5, 77, 5999], np.uint32)
+    np.testing.assert_array_equal(A.brute_force_rows(x, rows, 30), ids_o[rows])
+    o2, vo2, so, sd = _pair(x, 4, 8, 5, 20, 4, 40, 10)
+    for _ in range(3):
+        so.nn_descent_iteration(vo2)
+        A.detail.nn_descent_iteration(sd, x)
+        e = assert_pools_equal(sd, so)
+        assert sd.meta()["dist_comps"] == e["dist_comps"]
+    g = A.finalize(sd, x, 20)
+    f = A.build_forest(x, 4, 8, 5)
+    fo = o.build_forest(vo, 4, 8, 5)
+    r = A.GraphSearcher(x, f, g).search_batch(q, A.SearchParams(20, 60, 40, 4))
+    ids_s, d_s, st_s = o.search(vo, fo, g.ids, o.vs(q), 20, 60, 40, 4)
+    np.testing.assert_array_equal(r.ids, ids_s)
+    np.testing.assert_array_equal(r.dists.view(np.uint32), d_s.view(np.uint32))
+    np.testing.assert_array_equal(r.stats, st_s)
