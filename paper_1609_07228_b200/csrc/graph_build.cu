@@ -124,113 +124,204 @@ struct InitArgs {
     const int32_t* norms8;
 };
 
-// Collects point i's candidate set (graph_build.cpp:266-280) into cand;
-// returns the count (may exceed cap: caller retries with a bigger buffer).
-__device__ uint32_t init_collect(const InitArgs& a, uint32_t i, const float* q, uint32_t* cand,
-                                 uint32_t cap, uint32_t* sib, uint32_t sib_cap, uint32_t* s_cnt) {
+// Warp-level scratch for one point's candidate set.
+//   table : open-addressing hash set of ids (2*cap u32 slots, EMPTY = ~0u),
+//           later reused as the u64 key array (cap keys)
+//   uniq  : unique candidate ids in insertion order (cap)
+struct InitScratch {
+    uint32_t* table;
+    uint32_t* uniq;
+    uint32_t cap;  // pow2
+    uint32_t* sib;
+    uint32_t sib_cap;
+    uint32_t* cnt;  // [0] unique count, [1] sibling count, [2] overflow flag
+};
+
+__device__ __forceinline__ void hs_insert(const InitScratch& w, uint32_t id) {
+    const uint32_t mask = 2 * w.cap - 1;
+    uint32_t h = (id * 2654435761u) & mask;
+    for (uint32_t probe = 0; probe <= mask; ++probe) {
+        const uint32_t old = atomicCAS(&w.table[h], 0xffffffffu, id);
+        if (old == 0xffffffffu) {
+            const uint32_t u = atomicAdd(&w.cnt[0], 1u);
+            if (u < w.cap) w.uniq[u] = id;
+            else w.cnt[2] = 1;
+            return;
+        }
+        if (old == id) return;
+        h = (h + 1) & mask;
+    }
+    w.cnt[2] = 1;
+}
+
+// Point i's candidate set (graph_build.cpp:266-281): own leaf per tree plus one
+// descended leaf per ancestor level >= conquer_depth, deduplicated in a shared
+// hash set (self excluded, as the reference skips c == i at :283).
+__device__ void init_collect(const InitArgs& a, uint32_t i, const float* q, const InitScratch& w) {
     const uint32_t lane = lane_id();
-    if (lane == 0) { s_cnt[0] = 0; s_cnt[1] = 0; }
+    // table <- EMPTY (vectorised)
+    uint4* t4 = reinterpret_cast<uint4*>(w.table);
+    for (uint32_t j = lane; j < (2 * w.cap) / 4; j += 32) t4[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (lane == 0) { w.cnt[0] = 0; w.cnt[1] = 0; w.cnt[2] = 0; }
     __syncwarp();
-    // own leaves + ancestor walk, one lane per tree
     for (uint32_t t = lane; t < a.n_trees; t += 32) {
         const TreeView tv = a.trees[t];
         const uint32_t leaf = tv.owner[i];
         const KdNodeDev ln = tv.nodes[leaf];
-        const uint32_t len = ln.right - ln.left;
-        const uint32_t slot = atomicAdd(&s_cnt[0], len);
-        for (uint32_t j = 0; j < len; ++j)
-            if (slot + j < cap) cand[slot + j] = tv.pidx[ln.left + j];
+        for (uint32_t p = ln.left; p < ln.right; ++p) {
+            const uint32_t id = tv.pidx[p];
+            if (id != i) hs_insert(w, id);
+        }
         uint32_t node = leaf;
         for (;;) {
             const uint32_t par = tv.parent[node];
             if (par == kInvalidId || tv.depth[par] < a.conquer_depth) break;
             const KdNodeDev pn = tv.nodes[par];
-            const uint32_t sb = pn.left == node ? pn.right : pn.left;
-            const uint32_t k = atomicAdd(&s_cnt[1], 1u);
-            if (k < sib_cap) {
-                sib[k] = sb;
-                sib[sib_cap + k] = t;
+            const uint32_t k = atomicAdd(&w.cnt[1], 1u);
+            if (k < w.sib_cap) {
+                w.sib[k] = pn.left == node ? pn.right : pn.left;
+                w.sib[w.sib_cap + k] = t;
+            } else {
+                w.cnt[2] = 1;
             }
             node = par;
         }
     }
     __syncwarp();
-    const uint32_t nsib = min(s_cnt[1], sib_cap);
-    // descend every off-path sibling with the point itself (descend_from)
-    for (uint32_t k = lane; k < nsib; k += 32) {
-        const TreeView tv = a.trees[sib[sib_cap + k]];
-        uint32_t nd = sib[k];
+    const uint32_t nsib = min(w.cnt[1], w.sib_cap);
+    for (uint32_t k = lane; k < nsib; k += 32) {  // descend_from(sibling, x_i) per level
+        const TreeView tv = a.trees[w.sib[w.sib_cap + k]];
+        uint32_t nd = w.sib[k];
         for (KdNodeDev x = tv.nodes[nd]; x.split_dim != kLeaf; x = tv.nodes[nd])
             nd = q[x.split_dim] <= x.split_val ? x.left : x.right;
         const KdNodeDev ln = tv.nodes[nd];
-        const uint32_t len = ln.right - ln.left;
-        const uint32_t slot = atomicAdd(&s_cnt[0], len);
-        for (uint32_t j = 0; j < len; ++j)
-            if (slot + j < cap) cand[slot + j] = tv.pidx[ln.left + j];
+        for (uint32_t p = ln.left; p < ln.right; ++p) {
+            const uint32_t id = tv.pidx[p];
+            if (id != i) hs_insert(w, id);
+        }
     }
     __syncwarp();
-    const uint32_t c = s_cnt[0];
-    __syncwarp();
-    return s_cnt[1] > sib_cap ? UINT32_MAX : c;
 }
 
-__device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, uint32_t* cand, uint32_t c,
-                            uint32_t m, uint64_t* keys) {
+// P-th smallest distance (as fp32 bits) among keys[0..nk), nk >= P, by a
+// 4-pass MSB radix select over 256-bin warp histograms.
+__device__ uint32_t warp_select_dist(const uint64_t* keys, uint32_t nk, uint32_t P, uint32_t* hist) {
     const uint32_t lane = lane_id();
-    const uint32_t u = warp_sort_unique_u32(cand, c, m);
-    // drop self, compute exact distances
-    uint32_t nk = 0;
-    for (uint32_t base = 0; base < u; base += 32) {
-        const uint32_t j = base + lane;
-        const uint32_t id = j < u ? cand[j] : kInvalidId;
-        const bool keep = j < u && id != i;
-        const uint32_t b = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-            const float d = a.x8 ? l2_u8(a.x8 + size_t(i) * a.ld8, a.x8 + size_t(id) * a.ld8, a.ld8,
-                                         a.norms8[i], a.norms8[id])
-                                 : l2_exact_ldg(q, a.x + size_t(id) * a.ld, a.ld);
-            keys[nk + __popc(b & ((1u << lane) - 1u))] = make_key(d, id);
+    uint32_t prefix = 0, pmask = 0, r = P;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (uint32_t b = lane; b < 256; b += 32) hist[b] = 0;
+        __syncwarp();
+        for (uint32_t j = lane; j < nk; j += 32) {
+            const uint32_t d = uint32_t(keys[j] >> 32);
+            if ((d & pmask) == prefix) atomicAdd(&hist[(d >> shift) & 255u], 1u);
         }
-        nk += __popc(b);
+        __syncwarp();
+        uint32_t local = 0;
+        for (uint32_t b = 0; b < 8; ++b) local += hist[lane * 8 + b];
+        uint32_t incl = local;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += v;
+        }
+        const uint32_t excl = incl - local;
+        const uint32_t owner = __ffs(__ballot_sync(0xffffffffu, incl >= r)) - 1;
+        uint32_t bin = 0, before = 0;
+        if (lane == owner) {
+            uint32_t acc = excl;
+            for (uint32_t b = 0; b < 8; ++b) {
+                const uint32_t h = hist[lane * 8 + b];
+                if (acc + h >= r) { bin = lane * 8 + b; before = acc; break; }
+                acc += h;
+            }
+        }
+        bin = __shfl_sync(0xffffffffu, bin, owner);
+        before = __shfl_sync(0xffffffffu, before, owner);
+        prefix |= bin << shift;
+        pmask |= 255u << shift;
+        r -= before;
+        __syncwarp();
     }
-    const uint32_t mk = next_pow2(max(nk, 1u));
-    for (uint32_t j = nk + lane; j < mk; j += 32) keys[j] = kEmptyKey;
+    return prefix;
+}
+
+// Distances, then the pool: exact top-P by (dist, id) of the unique candidates.
+__device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, const InitScratch& w, uint32_t* hist) {
+    const uint32_t lane = lane_id();
+    const uint32_t u = w.cnt[0];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(w.table);  // table no longer needed
     __syncwarp();
-    warp_bitonic_sort(keys, mk);
-    const uint32_t take = min(nk, a.P);
+    for (uint32_t j = lane; j < u; j += 32) {
+        const uint32_t id = w.uniq[j];
+        const float d = a.x8 ? l2_u8(a.x8 + size_t(i) * a.ld8, a.x8 + size_t(id) * a.ld8, a.ld8, a.norms8[i],
+                                     a.norms8[id])
+                             : l2_exact_ldg(q, a.x + size_t(id) * a.ld, a.ld);
+        keys[j] = make_key(d, id);
+    }
+    __syncwarp();
+    uint32_t take = min(u, a.P);
+    uint32_t* surv_ids = w.uniq;  // reuse: survivors compacted in place as keys below
+    uint64_t* surv = keys;
+    uint32_t ns = u;
+    if (u > a.P) {
+        // keep keys whose distance <= the P-th smallest distance (ties included)
+        const uint32_t T = warp_select_dist(keys, u, a.P, hist);
+        ns = 0;
+        for (uint32_t base = 0; base < u; base += 32) {
+            const uint32_t j = base + lane;
+            const uint64_t v = j < u ? keys[j] : kEmptyKey;
+            const bool keep = j < u && uint32_t(v >> 32) <= T;
+            const uint32_t b = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (keep) surv[ns + __popc(b & ((1u << lane) - 1u))] = v;  // in place: target <= j
+            ns += __popc(b);
+            __syncwarp();
+        }
+    }
+    (void)surv_ids;
+    const uint32_t m = next_pow2(max(ns, 1u));
+    for (uint32_t j = ns + lane; j < m; j += 32) surv[j] = kEmptyKey;
+    __syncwarp();
+    warp_bitonic_sort(surv, m);
     uint64_t* pk = a.keys + size_t(i) * a.P;
     uint8_t* pf = a.flags + size_t(i) * a.P;
     for (uint32_t j = lane; j < a.P; j += 32) {
-        pk[j] = j < take ? keys[j] : kEmptyKey;
+        pk[j] = j < take ? surv[j] : kEmptyKey;
         pf[j] = j < take ? 1 : 0;
     }
     if (lane == 0) {
         a.sizes[i] = take;
-        atomicAdd(a.comps, (unsigned long long)nk);
+        atomicAdd(a.comps, (unsigned long long)u);
     }
     __syncwarp();
+}
+
+__host__ __device__ __forceinline__ size_t init_warp_bytes(uint32_t cap, uint32_t ld, uint32_t sib_cap) {
+    // table (2*cap u32 == cap u64 keys) + uniq (cap u32) + q row + sib (2*sib_cap) + hist (256) + cnt (4)
+    return (size_t(cap) * 12 + size_t(ld) * 4 + size_t(sib_cap) * 8 + 256 * 4 + 16 + 15) & ~size_t(15);
 }
 
 __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint32_t sib_cap,
                                                                const uint32_t* __restrict__ order) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t warp = threadIdx.x / 32, lane = lane_id();
-    const size_t per_warp = (size_t(kInitCap) * 4 + size_t(kInitCap) * 8 + size_t(a.ld) * 4 +
-                             size_t(sib_cap) * 8 + 16 + 15) & ~size_t(15);  // float4 rows stay aligned
-    unsigned char* base = smem + warp * per_warp;
-    uint64_t* keys = reinterpret_cast<uint64_t*>(base);
-    uint32_t* cand = reinterpret_cast<uint32_t*>(base + size_t(kInitCap) * 8);
-    float* q = reinterpret_cast<float*>(base + size_t(kInitCap) * 12);
-    uint32_t* sib = reinterpret_cast<uint32_t*>(base + size_t(kInitCap) * 12 + size_t(a.ld) * 4);
-    uint32_t* s_cnt = sib + 2 * sib_cap;
+    unsigned char* base = smem + warp * init_warp_bytes(kInitCap, a.ld, sib_cap);
+    InitScratch w;
+    w.table = reinterpret_cast<uint32_t*>(base);
+    w.uniq = w.table + 2 * kInitCap;
+    w.cap = kInitCap;
+    float* q = reinterpret_cast<float*>(w.uniq + kInitCap);
+    w.sib = reinterpret_cast<uint32_t*>(q + a.ld);
+    w.sib_cap = sib_cap;
+    uint32_t* hist = w.sib + 2 * sib_cap;
+    w.cnt = hist + 256;
     for (uint32_t ord = blockIdx.x * kInitWarps + warp; ord < a.n; ord += gridDim.x * kInitWarps) {
         // visit points in tree-0 leaf order: concurrently processed points share
         // most candidate rows, so the gathers hit L2
         const uint32_t i = order ? order[ord] : ord;
         for (uint32_t j = lane; j < a.ld; j += 32) q[j] = a.x[size_t(i) * a.ld + j];
         __syncwarp();
-        const uint32_t c = init_collect(a, i, q, cand, kInitCap, sib, sib_cap, s_cnt);
-        if (c > kInitCap) {
+        init_collect(a, i, q, w);
+        if (w.cnt[2]) {  // more unique candidates than the fast path holds
             if (lane == 0) {
                 const uint32_t o = atomicAdd(&a.overflow[0], 1u);
                 a.overflow[1 + o] = i;
@@ -238,26 +329,30 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
             __syncwarp();
             continue;
         }
-        init_finish(a, i, q, cand, c, next_pow2(max(c, 1u)), keys);
+        init_finish(a, i, q, w, hist);
     }
 }
 
-// Overflow path: one warp per point with global scratch of capacity cap.
+// Overflow path: one warp per point, scratch in global memory sized for the
+// forest's worst case (trees * (max_depth+1) * leaf_cap candidates).
 __global__ void init_overflow_kernel(InitArgs a, const uint32_t* list, uint32_t count, uint32_t cap,
-                                     uint32_t sib_cap, uint32_t* gcand, uint64_t* gkeys, float* gq,
-                                     uint32_t* gsib) {
-    __shared__ uint32_t s_cnt[2];
+                                     uint32_t sib_cap, uint32_t* gscratch, float* gq) {
+    __shared__ uint32_t s_misc[256 + 4];
     const uint32_t lane = lane_id();
     for (uint32_t r = blockIdx.x; r < count; r += gridDim.x) {
         const uint32_t i = list[r];
-        uint32_t* cand = gcand + size_t(blockIdx.x) * cap;
-        uint64_t* keys = gkeys + size_t(blockIdx.x) * cap;
+        InitScratch w;
+        w.table = gscratch + size_t(blockIdx.x) * (3 * size_t(cap) + 2 * sib_cap);
+        w.uniq = w.table + 2 * cap;
+        w.cap = cap;
+        w.sib = w.uniq + cap;
+        w.sib_cap = sib_cap;
+        w.cnt = s_misc + 256;
         float* q = gq + size_t(blockIdx.x) * a.ld;
-        uint32_t* sib = gsib + size_t(blockIdx.x) * 2 * sib_cap;
         for (uint32_t j = lane; j < a.ld; j += 32) q[j] = a.x[size_t(i) * a.ld + j];
         __syncwarp();
-        const uint32_t c = init_collect(a, i, q, cand, cap, sib, sib_cap, s_cnt);
-        init_finish(a, i, q, cand, min(c, cap), next_pow2(max(min(c, cap), 1u)), keys);
+        init_collect(a, i, q, w);
+        init_finish(a, i, q, w, s_misc);
     }
 }
 
@@ -1170,11 +1265,13 @@ int annk_init_graph(const annk_dataset* ds, const annk_forest* fc, uint32_t k, u
                    ds->u8 ? ds->data8.p : nullptr, ds->ld8, ds->u8 ? ds->norms8.p : nullptr};
         const uint32_t sib_full = f->n_trees * (max_depth + 1);
         const uint32_t sib_cap = std::min<uint32_t>(sib_full, 512);
-        const size_t per_warp = (size_t(kInitCap) * 12 + size_t(ds->ld) * 4 + size_t(sib_cap) * 8 + 16 + 15) &
-                                ~size_t(15);
+        const size_t per_warp = init_warp_bytes(kInitCap, ds->ld, sib_cap);
         const size_t smem = per_warp * kInitWarps;
         CK(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        const uint32_t grid = std::min<uint32_t>((n + kInitWarps - 1) / kInitWarps, uint32_t(num_sms()) * 16);
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, init_kernel, kInitWarps * 32, smem));
+        const uint32_t grid = std::min<uint32_t>((n + kInitWarps - 1) / kInitWarps,
+                                                 uint32_t(num_sms()) * std::max(per_sm, 1));
         s->order.alloc(n);
         CK(cudaMemcpyAsync(s->order.p, f->trees[0].pidx.p, size_t(n) * 4, cudaMemcpyDeviceToDevice, stream()));
         LAUNCH(init_kernel, grid, kInitWarps * 32, smem, a, sib_cap, s->order.p);
@@ -1184,11 +1281,9 @@ int annk_init_graph(const annk_dataset* ds, const annk_forest* fc, uint32_t k, u
         if (n_over) {
             const uint32_t cap = next_pow2(f->n_trees * (max_depth + 1) * f->leaf_cap);
             const uint32_t blocks = std::min<uint32_t>(n_over, 1024);
-            DevBuf<uint32_t> gcand(size_t(blocks) * cap), gsib(size_t(blocks) * 2 * sib_full);
-            DevBuf<uint64_t> gkeys(size_t(blocks) * cap);
+            DevBuf<uint32_t> gscratch(size_t(blocks) * (3 * size_t(cap) + 2 * sib_full));
             DevBuf<float> gq(size_t(blocks) * ds->ld);
-            LAUNCH(init_overflow_kernel, blocks, 32, 0, a, overflow.p + 1, n_over, cap, sib_full, gcand.p,
-                   gkeys.p, gq.p, gsib.p);
+            LAUNCH(init_overflow_kernel, blocks, 32, 0, a, overflow.p + 1, n_over, cap, sib_full, gscratch.p, gq.p);
         }
         unsigned long long c = 0;
         comps.download(&c, 1);
