@@ -157,6 +157,9 @@ int annk_pool_topk_accuracy(const annk_state* s, const uint32_t* gt_ids, uint32_
 /* Sum over points of |g_new|+|g_old| for the last sampling step (the join's
  * row-gather count; used for the roofline). */
 int annk_state_join_rows(const annk_state* s, uint64_t* rows);
+/* Last round's device counters: [join_rows, accepted offers, spilled offers,
+ * per-point offer slots]. */
+int annk_state_stats(const annk_state* s, uint64_t* out4);
 
 /* --------------------------------------------------------------- search */
 /* search.cpp:23-35 GraphSearcher(base, forest, graph): validates the graph

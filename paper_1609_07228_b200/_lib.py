@@ -93,6 +93,7 @@ _SIGS = {
     "annk_finalize": [_vp, _vp, _u32, _u32p, _f32p],
     "annk_pool_topk_accuracy": [_vp, _u32p, _u32, _u32, _vp, C.POINTER(C.c_double)],
     "annk_state_join_rows": [_vp, C.POINTER(_u64)],
+    "annk_state_stats": [_vp, _u64p],
     "annk_searcher_create": [_vp, _vp, _u32p, _u32, _u32, _pp],
     "annk_searcher_destroy": [_vp],
     "annk_search": [_vp, _f32p, _u32, _u32, C.POINTER(SearchParamsC), _u32p, _f32p, _vp],

@@ -645,3 +645,10 @@ def recall_curve(base, forest, graph, queries, gt: np.ndarray, sweep: Sequence[S
                               float(r.stats[:, 0].astype(np.float64).mean()),
                               float(r.stats[:, 3].astype(np.float64).mean())))
     return table
+
+
+def state_stats(state: RefineState) -> dict:
+    """Device counters of the last NN-descent round (join rows, offers, spills)."""
+    out = np.zeros(4, np.uint64)
+    check(lib.annk_state_stats(state.handle, out))
+    return dict(join_rows=int(out[0]), offers=int(out[1]), spilled=int(out[2]), offer_slots=int(out[3]))

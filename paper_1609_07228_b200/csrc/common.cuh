@@ -233,6 +233,44 @@ __device__ inline void warp_bitonic_sort_u32(uint32_t* s, uint32_t n) {
     }
 }
 
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, uint32_t m) {
+    const uint32_t lo = __shfl_xor_sync(0xffffffffu, uint32_t(v), m);
+    const uint32_t hi = __shfl_xor_sync(0xffffffffu, uint32_t(v >> 32), m);
+    return (uint64_t(hi) << 32) | lo;
+}
+
+// Register-resident ascending bitonic sort of 32*V keys held V per lane in
+// element order e = r*32 + lane (no shared memory; cross-lane steps shuffle).
+template <int V>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[V]) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (uint32_t k = 2; k <= 32u * V; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int r = 0; r < V; ++r) {
+                    const int rp = r ^ int(j / 32);
+                    if (rp > r) {
+                        const bool up = ((uint32_t(r) * 32 + lane) & k) == 0;
+                        const uint64_t a = v[r], b = v[rp];
+                        if ((a > b) == up) { v[r] = b; v[rp] = a; }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < V; ++r) {
+                    const uint64_t o = shfl_xor_u64(v[r], j);
+                    const bool up = ((uint32_t(r) * 32 + lane) & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    v[r] = (lower == up) ? (v[r] < o ? v[r] : o) : (v[r] < o ? o : v[r]);
+                }
+            }
+        }
+    }
+}
+
 __host__ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
     uint32_t p = 1;
     while (p < x) p <<= 1;

@@ -384,7 +384,7 @@ __global__ void sample_kernel(SampleArgs a) {
     for (uint32_t base = 0; base < sz && taken < a.S; base += 32) {
         const uint32_t j = base + lane;
         const bool valid = j < sz;
-        const bool isnew = valid && pf[j];
+        const bool isnew = valid && (pf[j] & 1);
         const uint32_t bn = __ballot_sync(0xffffffffu, isnew);
         // entries are scanned while fewer than S news have been taken
         const uint32_t lt = (1u << lane) - 1u;
@@ -434,7 +434,64 @@ struct UnionArgs {
     uint32_t* gncnt;
     uint32_t* gocnt;
     unsigned long long* join_rows;
+    const uint32_t* samp;  // n x 2 x S sampled reverse lists (rev_sample_kernel), used when longer than S
 };
+
+// graph_build.cpp:38-48 sample_down for every reverse list longer than S, one
+// thread per (point, new/old): the sorted unique list gets a partial
+// Fisher-Yates over its first S slots driven by
+// std::mt19937_64(substream(round_seed, 2i + kind)).  Output k of a freshly
+// seeded mt19937_64 (k < 156) only needs seed words k, k+1 and k+156, so the
+// seed expansion is streamed and only words 0..S are kept; swapped positions
+// live in a small per-thread overlay in shared memory.
+__global__ void rev_sample_kernel(uint32_t n, uint32_t S, uint64_t round_seed, const uint32_t* __restrict__ rn_off,
+                                  const uint32_t* __restrict__ rn_data, const uint32_t* __restrict__ ro_off,
+                                  const uint32_t* __restrict__ ro_data, uint32_t* __restrict__ samp) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t per = size_t(S + 1) * 8 + size_t(4 * S) * 4;
+    uint64_t* xs = reinterpret_cast<uint64_t*>(smem + threadIdx.x * per);
+    uint32_t* pos = reinterpret_cast<uint32_t*>(xs + S + 1);
+    uint32_t* val = pos + 2 * S;
+    if (t >= 2 * n) return;
+    const uint32_t i = t >> 1, kind = t & 1;
+    const uint32_t* off = kind ? ro_off : rn_off;
+    const uint32_t* data = kind ? ro_data : rn_data;
+    const uint32_t b = off[i], m = off[i + 1] - b;
+    if (m <= S) return;
+    const uint32_t* a = data + b;
+    uint32_t* out = samp + (size_t(i) * 2 + kind) * S;
+    uint64_t x = substream(round_seed, 2 * uint64_t(i) + kind);
+    xs[0] = x;
+    for (uint32_t k = 1; k <= S; ++k) {
+        x = 6364136223846793005ULL * (x ^ (x >> 62)) + uint64_t(k);
+        xs[k] = x;
+    }
+    for (uint32_t k = S + 1; k < 156; ++k) x = 6364136223846793005ULL * (x ^ (x >> 62)) + uint64_t(k);
+    uint32_t no = 0;
+    for (uint32_t k = 0; k < S; ++k) {
+        x = 6364136223846793005ULL * (x ^ (x >> 62)) + uint64_t(156 + k);
+        const uint64_t r = mt_temper(mt_twist(xs[k], xs[k + 1], x));
+        const uint32_t j = k + uint32_t(r % uint64_t(m - k));
+        uint32_t vk = a[k], vj = a[j];
+        int pk = -1, pj = -1;
+        for (uint32_t q = 0; q < no; ++q) {
+            if (pos[q] == k) { vk = val[q]; pk = int(q); }
+            if (pos[q] == j) { vj = val[q]; pj = int(q); }
+        }
+        if (j == k) continue;  // swap with itself
+        if (pk < 0) { pos[no] = k; pk = int(no++); }
+        if (pj < 0) { pos[no] = j; pj = int(no++); }
+        val[pk] = vj;
+        val[pj] = vk;
+    }
+    for (uint32_t k = 0; k < S; ++k) {
+        uint32_t v = a[k];
+        for (uint32_t q = 0; q < no; ++q)
+            if (pos[q] == k) v = val[q];
+        out[k] = v;
+    }
+}
 
 // graph_build.cpp:88-103 per point: sample reverse lists, union, sort-dedup.
 __global__ void union_kernel(UnionArgs a, uint32_t m_new, uint32_t m_old) {
@@ -457,10 +514,10 @@ __global__ void union_kernel(UnionArgs a, uint32_t m_new, uint32_t m_old) {
     if (rom <= a.S) {
         for (uint32_t j = lane; j < rom; j += 32) so[co + j] = a.ro_data[rob + j];
     }
-    if (lane == 0 && rnm > a.S)
-        sample_down_sorted(a.rn_data + rnb, rnm, a.S, substream(a.round_seed, 2 * uint64_t(i)), sn + cn);
-    if (lane == 1 && rom > a.S)
-        sample_down_sorted(a.ro_data + rob, rom, a.S, substream(a.round_seed, 2 * uint64_t(i) + 1), so + co);
+    if (rnm > a.S)
+        for (uint32_t j = lane; j < a.S; j += 32) sn[cn + j] = a.samp[(size_t(i) * 2) * a.S + j];
+    if (rom > a.S)
+        for (uint32_t j = lane; j < a.S; j += 32) so[co + j] = a.samp[(size_t(i) * 2 + 1) * a.S + j];
     __syncwarp();
     const uint32_t un = warp_sort_unique_u32(sn, cn + addn, m_new);
     const uint32_t uo = warp_sort_unique_u32(so, co + addo, m_old);
@@ -488,6 +545,8 @@ struct JoinArgs {
     uint32_t* ov_tgt;
     uint64_t* ov_key;
     uint32_t ov_cap;
+    unsigned long long* offers;  // total accepted offers (stats)
+    uint32_t sub, nsub;          // this sub-round joins points with ord % nsub == sub
 };
 
 __device__ __forceinline__ void offer(const JoinArgs& a, uint32_t owner, uint32_t cand, float d) {
@@ -671,22 +730,38 @@ __device__ __forceinline__ void push_offer(const JoinArgs& a, uint32_t owner, ui
     }
 }
 
-// Same schedule as join_staged_kernel on the exact u8 datapath: rows staged as
-// bytes (ld8 + 16 stride), 4 dp4a per 16 bytes, dist = |x|^2 + |y|^2 - 2 x.y.
+// Aggregated join (both datapaths).  Same pair schedule as join_staged_kernel;
+// accepted offers are first collected in shared memory tagged with the list
+// member they go to (every offer of point i's join targets one of i's list
+// members), then flushed with ONE global atomic per member to reserve a
+// contiguous range in that member's offer slots (or the spill list).  This
+// cuts global atomics from one per offer to one per (point, member).
+constexpr uint32_t kJoinPerRound = (kJoinThreads / 32) * 32 * kJoinXR * 2;  // max offers per round
+
+template <bool U8>
 __global__ void __launch_bounds__(kJoinThreads)
-join_u8_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const int32_t* __restrict__ norms,
-               const uint32_t* __restrict__ order, uint32_t rmax) {
+join_agg_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const int32_t* __restrict__ norms,
+                const uint32_t* __restrict__ order, uint32_t rmax, uint32_t ol) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t rs = ld8 + 16;  // padded row stride (bytes): conflict-free 16-byte loads
-    uint8_t* rows = smem;
-    uint64_t* thr_s = reinterpret_cast<uint64_t*>(rows + size_t(rmax) * rs);
-    uint32_t* ids = reinterpret_cast<uint32_t*>(thr_s + rmax);
+    __shared__ uint32_t ocount;
+    const uint32_t rsb = U8 ? (ld8 + 16) : (a.ld + 4) * 4;  // padded row stride in bytes
+    unsigned char* rows = smem;
+    uint64_t* thr_s = reinterpret_cast<uint64_t*>(rows + size_t(rmax) * rsb);
+    uint64_t* okey = thr_s + rmax;
+    uint32_t* ids = reinterpret_cast<uint32_t*>(okey + ol);
     int32_t* nrm = reinterpret_cast<int32_t*>(ids + rmax);
-    uint32_t* gstart = reinterpret_cast<uint32_t*>(nrm + rmax);
+    uint32_t* mcnt = reinterpret_cast<uint32_t*>(nrm + rmax);
+    uint32_t* mbase = mcnt + rmax;
+    uint32_t* mfix = mbase + rmax;
+    uint32_t* msp = mfix + rmax;
+    uint32_t* gstart = msp + rmax;
+    uint16_t* omem = reinterpret_cast<uint16_t*>(gstart + rmax / 4 + 2);
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr uint32_t kWarps = kJoinThreads / 32;
     unsigned long long comps = 0;
-    for (uint32_t ord = blockIdx.x; ord < a.n; ord += gridDim.x) {
+    for (uint32_t t = blockIdx.x;; t += gridDim.x) {
+        const uint32_t ord = t * a.nsub + a.sub;
+        if (ord >= a.n) break;
         const uint32_t i = order ? order[ord] : ord;
         const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
         if (A == 0) continue;
@@ -696,7 +771,7 @@ join_u8_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const i
             const uint32_t id = r < A ? nw[r] : od[r - A];
             ids[r] = id;
             thr_s[r] = a.thr[id];
-            nrm[r] = norms[id];
+            if (U8) nrm[r] = norms[id];
         }
         if (tid == 0) {
             uint32_t acc = 0;
@@ -707,61 +782,141 @@ join_u8_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const i
                 acc += R > y0 ? (R - y0 + 31) / 32 : 0;
             }
             gstart[ng] = acc;
+            ocount = 0;
         }
         __syncthreads();
-        const uint32_t v16 = ld8 / 16;
-        for (uint32_t j = tid; j < R * v16; j += kJoinThreads) {
-            const uint32_t r = j / v16, c = (j % v16) * 16;
-            *reinterpret_cast<uint4*>(rows + size_t(r) * rs + c) =
-                __ldg(reinterpret_cast<const uint4*>(x8 + size_t(ids[r]) * ld8 + c));
+        if (U8) {
+            const uint32_t v16 = ld8 / 16;
+            for (uint32_t j = tid; j < R * v16; j += kJoinThreads) {
+                const uint32_t r = j / v16, c = (j % v16) * 16;
+                *reinterpret_cast<uint4*>(rows + size_t(r) * rsb + c) =
+                    __ldg(reinterpret_cast<const uint4*>(x8 + size_t(ids[r]) * ld8 + c));
+            }
+        } else {
+            const uint32_t v4 = a.ld / 4;
+            for (uint32_t j = tid; j < R * v4; j += kJoinThreads) {
+                const uint32_t r = j / v4, c = (j % v4) * 4;
+                *reinterpret_cast<float4*>(rows + size_t(r) * rsb + size_t(c) * 4) =
+                    __ldg(reinterpret_cast<const float4*>(a.x + size_t(ids[r]) * a.ld + c));
+            }
         }
         __syncthreads();
         const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
         const uint32_t n_items = gstart[ng];
-        for (uint32_t item = warp; item < n_items; item += kWarps) {
-            uint32_t g = 0;
-            while (gstart[g + 1] <= item) ++g;
-            const uint32_t x0 = g * kJoinXR;
-            const uint32_t y = x0 + 1 + (item - gstart[g]) * 32 + lane;
-            const bool yv = y < R;
-            const uint8_t* yr = rows + size_t(yv ? y : 0) * rs;
-            const uint8_t* xr[kJoinXR];
+        for (uint32_t rb = 0; rb < n_items; rb += kWarps) {
+            const uint32_t item = rb + warp;
+            if (item < n_items) {
+                uint32_t g = 0;
+                while (gstart[g + 1] <= item) ++g;
+                const uint32_t x0 = g * kJoinXR;
+                const uint32_t y = x0 + 1 + (item - gstart[g]) * 32 + lane;
+                const bool yv = y < R;
+                const unsigned char* yr = rows + size_t(yv ? y : 0) * rsb;
+                const unsigned char* xr[kJoinXR];
 #pragma unroll
-            for (uint32_t k = 0; k < kJoinXR; ++k) xr[k] = rows + size_t(min(x0 + k, R - 1)) * rs;
-            uint32_t dot[kJoinXR];
+                for (uint32_t k = 0; k < kJoinXR; ++k) xr[k] = rows + size_t(min(x0 + k, R - 1)) * rsb;
+                float dist[kJoinXR];
+                if (U8) {
+                    uint32_t dot[kJoinXR];
 #pragma unroll
-            for (uint32_t k = 0; k < kJoinXR; ++k) dot[k] = 0;
-            for (uint32_t c = 0; c < ld8; c += 16) {
-                const uint4 b = *reinterpret_cast<const uint4*>(yr + c);
+                    for (uint32_t k = 0; k < kJoinXR; ++k) dot[k] = 0;
+                    for (uint32_t c = 0; c < ld8; c += 16) {
+                        const uint4 b = *reinterpret_cast<const uint4*>(yr + c);
 #pragma unroll
-                for (uint32_t k = 0; k < kJoinXR; ++k) {
-                    const uint4 x = *reinterpret_cast<const uint4*>(xr[k] + c);
-                    dot[k] = __dp4a(x.x, b.x, dot[k]);
-                    dot[k] = __dp4a(x.y, b.y, dot[k]);
-                    dot[k] = __dp4a(x.z, b.z, dot[k]);
-                    dot[k] = __dp4a(x.w, b.w, dot[k]);
+                        for (uint32_t k = 0; k < kJoinXR; ++k) {
+                            const uint4 x = *reinterpret_cast<const uint4*>(xr[k] + c);
+                            dot[k] = __dp4a(x.x, b.x, dot[k]);
+                            dot[k] = __dp4a(x.y, b.y, dot[k]);
+                            dot[k] = __dp4a(x.z, b.z, dot[k]);
+                            dot[k] = __dp4a(x.w, b.w, dot[k]);
+                        }
+                    }
+                    const int32_t ny = nrm[yv ? y : 0];
+#pragma unroll
+                    for (uint32_t k = 0; k < kJoinXR; ++k)
+                        dist[k] = float(nrm[min(x0 + k, R - 1)] + ny - 2 * int32_t(dot[k]));
+                } else {
+#pragma unroll
+                    for (uint32_t k = 0; k < kJoinXR; ++k) dist[k] = 0.0f;
+                    for (uint32_t c = 0; c < a.ld; c += 4) {
+                        const float4 b = *reinterpret_cast<const float4*>(yr + size_t(c) * 4);
+#pragma unroll
+                        for (uint32_t k = 0; k < kJoinXR; ++k) {
+                            const float4 x = *reinterpret_cast<const float4*>(xr[k] + size_t(c) * 4);
+                            float d;
+                            d = __fsub_rn(x.x, b.x); dist[k] = __fadd_rn(dist[k], __fmul_rn(d, d));
+                            d = __fsub_rn(x.y, b.y); dist[k] = __fadd_rn(dist[k], __fmul_rn(d, d));
+                            d = __fsub_rn(x.z, b.z); dist[k] = __fadd_rn(dist[k], __fmul_rn(d, d));
+                            d = __fsub_rn(x.w, b.w); dist[k] = __fadd_rn(dist[k], __fmul_rn(d, d));
+                        }
+                    }
+                }
+                if (yv) {
+                    const uint32_t idy = ids[y];
+                    const uint64_t thy = thr_s[y];
+#pragma unroll
+                    for (uint32_t k = 0; k < kJoinXR; ++k) {
+                        const uint32_t x = x0 + k;
+                        if (x >= A || y <= x) continue;
+                        const uint32_t idx = ids[x];
+                        if (idx == idy) continue;  // graph_build.cpp:146 (l == j)
+                        ++comps;
+                        const uint64_t kx = make_key(dist[k], idy);  // offer y to x's pool
+                        if (kx < thr_s[x]) {
+                            const uint32_t s = atomicAdd(&ocount, 1u);
+                            okey[s] = kx;
+                            omem[s] = uint16_t(x);
+                        }
+                        const uint64_t ky = make_key(dist[k], idx);  // offer x to y's pool
+                        if (ky < thy) {
+                            const uint32_t s = atomicAdd(&ocount, 1u);
+                            okey[s] = ky;
+                            omem[s] = uint16_t(y);
+                        }
+                    }
                 }
             }
-            if (yv) {
-                const uint32_t idy = ids[y];
-                const uint64_t thy = thr_s[y];
-                const int32_t ny = nrm[y];
-#pragma unroll
-                for (uint32_t k = 0; k < kJoinXR; ++k) {
-                    const uint32_t x = x0 + k;
-                    if (x >= A || y <= x) continue;
-                    const uint32_t idx = ids[x];
-                    if (idx == idy) continue;  // graph_build.cpp:146 (l == j)
-                    ++comps;
-                    const float d = float(nrm[x] + ny - 2 * int32_t(dot[k]));
-                    const uint64_t kx = make_key(d, idy);
-                    if (kx < thr_s[x]) push_offer(a, idx, kx);
-                    const uint64_t ky = make_key(d, idx);
-                    if (ky < thy) push_offer(a, idy, ky);
+            __syncthreads();
+            const uint32_t c = ocount;
+            if (c > ol - kJoinPerRound || rb + kWarps >= n_items) {  // uniform
+                for (uint32_t m = tid; m < R; m += kJoinThreads) mcnt[m] = 0;
+                __syncthreads();
+                for (uint32_t e = tid; e < c; e += kJoinThreads) atomicAdd(&mcnt[omem[e]], 1u);
+                __syncthreads();
+                for (uint32_t m = tid; m < R; m += kJoinThreads) {
+                    const uint32_t cnt = mcnt[m];
+                    if (cnt) {
+                        const uint32_t base = atomicAdd(&a.ocnt[ids[m]], cnt);
+                        const uint32_t fix = base < a.cap ? min(cnt, a.cap - base) : 0;
+                        mbase[m] = base;
+                        mfix[m] = fix;
+                        msp[m] = cnt > fix ? atomicAdd(a.ov_cnt, cnt - fix) : 0;
+                    }
+                    mcnt[m] = 0;
                 }
+                __syncthreads();
+                for (uint32_t e = tid; e < c; e += kJoinThreads) {
+                    const uint32_t m = omem[e];
+                    const uint32_t r = atomicAdd(&mcnt[m], 1u);
+                    const uint32_t owner = ids[m];
+                    if (r < mfix[m]) {
+                        a.obuf[size_t(owner) * a.cap + mbase[m] + r] = okey[e];
+                    } else {
+                        const uint32_t o = msp[m] + (r - mfix[m]);
+                        if (o < a.ov_cap) {
+                            a.ov_tgt[o] = owner;
+                            a.ov_key[o] = okey[e];
+                        }
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    atomicAdd(a.offers, (unsigned long long)c);
+                    ocount = 0;
+                }
+                __syncthreads();
             }
         }
-        __syncthreads();
     }
     for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
     if (lane == 0 && comps) atomicAdd(a.comps, comps);
@@ -779,6 +934,7 @@ struct MergeArgs {
     const uint32_t* ov_off;  // per-target start in the target-sorted spill list
     const uint64_t* ov_key;
     unsigned long long* changes;
+    uint64_t* thr;  // refreshed tails for the next sub-round (nullable)
 };
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t n, uint64_t v) {
@@ -831,10 +987,160 @@ __device__ uint32_t warp_topk_merge(uint64_t* R, uint32_t r, uint64_t* chunk, ui
 
 constexpr uint32_t kMergeChunk = 256;
 
+// Sorts the first c (<= 32*V) entries of buf in registers and writes them back
+// sorted (padding with kEmptyKey).
+template <int V>
+__device__ __forceinline__ void warp_sort_buf(uint64_t* buf, uint32_t c) {
+    const uint32_t lane = lane_id();
+    uint64_t v[V];
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+        const uint32_t e = uint32_t(r) * 32 + lane;
+        v[r] = e < c ? buf[e] : kEmptyKey;
+    }
+    warp_sort_regs<V>(v);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < V; ++r) buf[uint32_t(r) * 32 + lane] = v[r];
+    __syncwarp();
+}
+
+// As warp_topk_merge, for a chunk that is already sorted ascending.
+__device__ uint32_t warp_topk_merge_sorted(uint64_t* R, uint32_t r, uint64_t* chunk, uint32_t c, uint32_t P,
+                                           uint64_t* tmp) {
+    const uint32_t lane = lane_id();
+    uint32_t nu = 0;
+    for (uint32_t base = 0; base < c; base += 32) {
+        const uint32_t j = base + lane;
+        const uint64_t v = j < c ? chunk[j] : kEmptyKey;
+        bool keep = j < c && (j == 0 || chunk[j - 1] != v);
+        if (keep) {
+            const uint32_t p = lower_bound_u64(R, r, v);
+            keep = !(p < r && R[p] == v);
+        }
+        const uint32_t b = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) chunk[nu + __popc(b & ((1u << lane) - 1u))] = v;
+        nu += __popc(b);
+        __syncwarp();
+    }
+    for (uint32_t j = lane; j < r; j += 32) {
+        const uint32_t k = j + lower_bound_u64(chunk, nu, R[j]);
+        if (k < P) tmp[k] = R[j];
+    }
+    for (uint32_t j = lane; j < nu; j += 32) {
+        const uint32_t k = j + lower_bound_u64(R, r, chunk[j]);
+        if (k < P) tmp[k] = chunk[j];
+    }
+    __syncwarp();
+    const uint32_t nr = min(P, r + nu);
+    for (uint32_t j = lane; j < nr; j += 32) R[j] = tmp[j];
+    __syncwarp();
+    return nr;
+}
+
+// Streaming merge (common path).  R starts as the pool (top-P unique so far);
+// offers are streamed warp-wide and only those strictly below R's current P-th
+// key are kept (an equal key is the same id, i.e. a duplicate).  Kept offers
+// collect in a small pending buffer that is sorted and merged into R when it
+// fills, which tightens the filter for the rest of the stream.  Keys found in
+// the original pool keep the pool's flag; the others are new.
+constexpr uint32_t kPend = 128;
+
+__global__ void merge_stream_kernel(MergeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
+    const uint32_t wpb = blockDim.x / 32;
+    const size_t per_warp = ((size_t(kPend) + 3 * size_t(a.P)) * 8 + a.P + 15) & ~size_t(15);
+    unsigned char* base = smem + warp * per_warp;
+    uint64_t* pend = reinterpret_cast<uint64_t*>(base);
+    uint64_t* R = pend + kPend;
+    uint64_t* sp = R + a.P;
+    uint64_t* tmp = sp + a.P;
+    uint8_t* sflag = reinterpret_cast<uint8_t*>(tmp + a.P);
+    const uint32_t i = blockIdx.x * wpb + warp;
+    if (i >= a.n) return;
+    const uint32_t total = a.ocnt[i];
+    if (total == 0) return;
+    const uint32_t sz = a.sizes[i];
+    uint64_t* pk = a.keys + size_t(i) * a.P;
+    uint8_t* pf = a.flags + size_t(i) * a.P;
+    for (uint32_t j = lane; j < sz; j += 32) {
+        const uint64_t k = pk[j];
+        sp[j] = k;
+        R[j] = k;
+        sflag[j] = pf[j];
+    }
+    __syncwarp();
+    uint32_t r = sz;
+    uint64_t tail = r == a.P ? R[a.P - 1] : kEmptyKey;
+    uint32_t pc = 0;
+    const uint32_t c_fix = min(total, a.cap);
+    const uint32_t c_ov = total - c_fix;
+    const uint64_t* seg[2] = {a.obuf + size_t(i) * a.cap, a.ov_key + (c_ov ? a.ov_off[i] : 0)};
+    const uint32_t segn[2] = {c_fix, c_ov};
+    for (int sgi = 0; sgi < 2; ++sgi) {
+        const uint64_t* src = seg[sgi];
+        const uint32_t cnt = segn[sgi];
+        for (uint32_t b0 = 0; b0 < cnt; b0 += 32) {
+            const uint32_t j = b0 + lane;
+            const uint64_t key = j < cnt ? src[j] : kEmptyKey;
+            const bool keep = key < tail;
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) pend[pc + __popc(bal & ((1u << lane) - 1u))] = key;
+            pc += __popc(bal);
+            __syncwarp();
+            if (pc > kPend - 32) {
+                warp_sort_buf<kPend / 32>(pend, pc);
+                r = warp_topk_merge_sorted(R, r, pend, pc, a.P, tmp);
+                tail = r == a.P ? R[a.P - 1] : kEmptyKey;
+                pc = 0;
+            }
+        }
+    }
+    if (pc) {
+        warp_sort_buf<kPend / 32>(pend, pc);
+        r = warp_topk_merge_sorted(R, r, pend, pc, a.P, tmp);
+    }
+    uint32_t added = 0;
+    for (uint32_t j = lane; j < a.P; j += 32) {
+        if (j < r) {
+            const uint64_t key = R[j];
+            const uint32_t p = lower_bound_u64(sp, sz, key);
+            const bool in_pool = p < sz && sp[p] == key;
+            pk[j] = key;
+            pf[j] = in_pool ? sflag[p] : 3;  // bit0 flag_new, bit1 inserted this round
+            added += in_pool ? 0 : 1;
+        } else {
+            pk[j] = kEmptyKey;
+            pf[j] = 0;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) added += __shfl_xor_sync(0xffffffffu, added, o);
+    if (lane == 0) {
+        a.sizes[i] = r;
+        if (a.thr) a.thr[i] = r == a.P ? R[a.P - 1] : kEmptyKey;
+        if (added) atomicAdd(a.changes, (unsigned long long)added);
+    }
+}
+
+// End of a round: entries inserted this round (flag bit 1) survive = changes.
+__global__ void count_inserted_kernel(uint8_t* __restrict__ flags, size_t cnt, unsigned long long* out) {
+    unsigned long long c = 0;
+    for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < cnt; t += size_t(gridDim.x) * blockDim.x) {
+        const uint8_t f = flags[t];
+        if (f & 2) {
+            ++c;
+            flags[t] = f & 1;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
 // New pool = top-P of (pool U offers); duplicates keep the pool's entry.
 // Offers are first reduced to their top-P unique keys in chunks (an offer
 // beaten by P distinct offers cannot survive), then merged with the pool.
-__global__ void merge_kernel(MergeArgs a) {
+__global__ void merge_kernel(MergeArgs a, const uint32_t* __restrict__ list) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t warp = threadIdx.x / 32, lane = lane_id();
     const uint32_t wpb = blockDim.x / 32;
@@ -846,8 +1152,9 @@ __global__ void merge_kernel(MergeArgs a) {
     uint8_t* sflag = reinterpret_cast<uint8_t*>(reinterpret_cast<uint64_t*>(smem) + size_t(wpb) * per_warp_u64) +
                      size_t(warp) * 2 * a.P;
     uint8_t* soutf = sflag + a.P;
-    const uint32_t i = blockIdx.x * wpb + warp;
-    if (i >= a.n) return;
+    const uint32_t li = blockIdx.x * wpb + warp;
+    if (list ? li >= list[0] : li >= a.n) return;
+    const uint32_t i = list ? list[1 + li] : li;
     const uint32_t total = a.ocnt[i];
     if (total == 0) return;
     const uint32_t c_fix = min(total, a.cap);
@@ -895,7 +1202,7 @@ __global__ void merge_kernel(MergeArgs a) {
     }
     for (uint32_t j = lane; j < nu; j += 32) {
         const uint32_t k = j + lower_bound_u64(sp, sz, R[j]);
-        if (k < a.P) { sout[k] = R[j]; soutf[k] = 1; ++added; }
+        if (k < a.P) { sout[k] = R[j]; soutf[k] = 3; ++added; }
     }
     __syncwarp();
     const uint32_t nsz = min(a.P, sz + nu);
@@ -1117,9 +1424,17 @@ void do_union(annk_state* s) {
     const uint32_t m_new = next_pow2(2 * s->S), m_old = next_pow2(s->P + s->S);
     DevBuf<unsigned long long> rows(1);
     rows.zero();
-    UnionArgs a{n, s->P, s->S, substream(s->seed, s->iteration), s->fnew.p, s->fold.p, s->cnew.p, s->cold.p,
+    const uint64_t round_seed = substream(s->seed, s->iteration);
+    DevBuf<uint32_t> samp(size_t(n) * 2 * s->S);
+    {
+        const uint32_t tpb = 64;
+        const size_t per = size_t(s->S + 1) * 8 + size_t(4 * s->S) * 4;
+        LAUNCH(rev_sample_kernel, (2 * n + tpb - 1) / tpb, tpb, tpb * per, n, s->S, round_seed, s->rn_off.p,
+               s->rn_data.p, s->ro_off.p, s->ro_data.p, samp.p);
+    }
+    UnionArgs a{n, s->P, s->S, round_seed, s->fnew.p, s->fold.p, s->cnew.p, s->cold.p,
                 s->rn_off.p, s->rn_data.p, s->ro_off.p, s->ro_data.p, s->gnew.p, s->gold.p,
-                s->gncnt.p, s->gocnt.p, rows.p};
+                s->gncnt.p, s->gocnt.p, rows.p, samp.p};
     const uint32_t wpb = 4;
     LAUNCH(union_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * (m_new + m_old) * 4, a, m_new, m_old);
     unsigned long long h = 0;
@@ -1129,92 +1444,145 @@ void do_union(annk_state* s) {
     s->stage = 2;
 }
 
+// One NN-descent join + merge round, split into `nsub` interleaved sub-rounds:
+// sub-round j joins the points whose visit order is j mod nsub, then merges
+// the offers into the pools and refreshes the thresholds.  Exact: merging is
+// associative (top-P(top-P(pool U A) U B) = top-P(pool U A U B), same flags),
+// and later sub-rounds filter offers against tighter tails, which cuts the
+// offer volume the merge has to process.
 uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
     const uint32_t n = s->n;
-    // fixed per-point offer slots; overflow (hub points) spills to a global list
-    // capacities learned by earlier rounds (any state) avoid a redo of the join
+    // capacities learned by earlier rounds (any state) avoid redoing a join
     static uint64_t spill_per_point_hint = 8;
-    if (s->offer_cap == 0) s->offer_cap = std::max(2 * s->P, 64u);
+    static uint32_t offer_cap_hint = 0;
+    // per-point offer slots: sized from the offer volume seen so far, within a
+    // 12 GB budget (offers past the slots spill to a target-sorted global list)
+    const uint32_t cap_floor = std::max(2 * s->P, 64u);
+    uint32_t cap_max = cap_floor;
+    while (uint64_t(cap_max) * 2 * n * 8 <= 12ull << 30 && cap_max < 4096) cap_max *= 2;
+    if (s->offer_cap == 0) s->offer_cap = std::min(cap_max, std::max(cap_floor, offer_cap_hint));
     if (s->ov_cap == 0)
         s->ov_cap = uint32_t(std::min<uint64_t>(std::max<uint64_t>(1u << 20, n * spill_per_point_hint), 1u << 31));
-    DevBuf<unsigned long long> counters(2);
+
+    const uint32_t rmax = 3 * s->S + s->P;  // |new| <= 2S, |old| <= P + S
+    const size_t staged_smem = size_t(rmax) * (ds->ld + 4) * 4 + size_t(rmax) * 12 + (rmax / 4 + 2) * 4;
+    const auto agg_smem = [&](bool u8, uint32_t ol) {
+        const size_t rsb = u8 ? ds->ld8 + 16 : size_t(ds->ld + 4) * 4;
+        return size_t(rmax) * rsb + size_t(rmax) * 8 + size_t(ol) * 8 + size_t(rmax) * 24 + (rmax / 4 + 2) * 4 +
+               size_t(ol) * 2 + 16;
+    };
+    const uint32_t ol_u8 = 4096, ol_f32 = 2048;
+    const bool agg_u8 = ds->u8 && agg_smem(true, ol_u8) <= 120 * 1024;
+    const bool agg_f32 = !agg_u8 && agg_smem(false, ol_f32) <= 160 * 1024;
+    uint32_t nsub = 1;  // measured: sub-rounds cut offers <5% at cfg2, merge launches cost more
+    if (const char* e = getenv("ANNK_SUBROUNDS")) nsub = std::max(1, atoi(e));
+    if (!agg_u8 && !agg_f32) nsub = 1;
+
+    DevBuf<unsigned long long> counters(3);  // [comps, unused, offers] per attempt
     DevBuf<uint32_t> ov_cnt(1);
-    uint32_t spilled = 0;
-    for (;;) {
-        if (s->obuf.n != size_t(n) * s->offer_cap) s->obuf.alloc(size_t(n) * s->offer_cap);
-        if (s->ov_tgt.n != s->ov_cap) {
-            s->ov_tgt.alloc(s->ov_cap);
-            s->ov_key.alloc(s->ov_cap);
+    unsigned long long comps = 0, offers = 0, spilled_total = 0;
+    for (uint32_t sub = 0; sub < nsub; ++sub) {
+        uint32_t spilled = 0;
+        for (;;) {
+            if (s->obuf.n != size_t(n) * s->offer_cap) s->obuf.alloc(size_t(n) * s->offer_cap);
+            if (s->ov_tgt.n != s->ov_cap) {
+                s->ov_tgt.alloc(s->ov_cap);
+                s->ov_key.alloc(s->ov_cap);
+            }
+            s->ocnt.zero();
+            counters.zero();
+            ov_cnt.zero();
+            JoinArgs ja{ds->data.p, n, ds->ld, s->P, s->S, s->offer_cap, s->gnew.p, s->gold.p, s->gncnt.p,
+                        s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p,
+                        ov_cnt.p, s->ov_tgt.p, s->ov_key.p, s->ov_cap, counters.p + 2, sub, nsub};
+            const uint32_t* order = s->order.n ? s->order.p : nullptr;
+            if (agg_u8 || agg_f32) {
+                const size_t sm = agg_smem(agg_u8, agg_u8 ? ol_u8 : ol_f32);
+                const void* fn = agg_u8 ? reinterpret_cast<const void*>(join_agg_kernel<true>)
+                                        : reinterpret_cast<const void*>(join_agg_kernel<false>);
+                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+                int per_sm = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinThreads, sm));
+                const uint32_t grid =
+                    std::min<uint32_t>((n + nsub - 1) / nsub, uint32_t(num_sms()) * std::max(per_sm, 1));
+                if (agg_u8)
+                    LAUNCH(join_agg_kernel<true>, grid, kJoinThreads, sm, ja, ds->data8.p, ds->ld8, ds->norms8.p,
+                           order, rmax, ol_u8);
+                else
+                    LAUNCH(join_agg_kernel<false>, grid, kJoinThreads, sm, ja, nullptr, 0u, nullptr, order, rmax,
+                           ol_f32);
+            } else if (staged_smem <= 110 * 1024) {
+                CK(cudaFuncSetAttribute(join_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(staged_smem)));
+                int per_sm = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_staged_kernel, kJoinThreads,
+                                                                 staged_smem));
+                const uint32_t grid = std::min<uint32_t>(n, uint32_t(num_sms()) * std::max(per_sm, 1));
+                LAUNCH(join_staged_kernel, grid, kJoinThreads, staged_smem, ja, order, rmax);
+            } else {
+                const uint32_t wpb = 8;
+                LAUNCH(join_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
+            }
+            ov_cnt.download(&spilled, 1);
+            ssync();
+            if (spilled <= s->ov_cap) break;
+            s->ov_cap = next_pow2(spilled);  // spill list too small: grow and redo (pools untouched so far)
+            spill_per_point_hint = std::max<uint64_t>(spill_per_point_hint, (uint64_t(s->ov_cap) + n - 1) / n);
         }
-        s->ocnt.zero();
-        counters.zero();
-        ov_cnt.zero();
-        JoinArgs ja{ds->data.p, n, ds->ld, s->P, s->S, s->offer_cap, s->gnew.p, s->gold.p, s->gncnt.p,
-                    s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p,
-                    ov_cnt.p, s->ov_tgt.p, s->ov_key.p, s->ov_cap};
-        const uint32_t rmax = 3 * s->S + s->P;  // |new| <= 2S, |old| <= P + S
-        const size_t staged_smem = size_t(rmax) * (ds->ld + 4) * 4 + size_t(rmax) * 12 + (rmax / 4 + 2) * 4;
-        const size_t u8_smem = size_t(rmax) * (ds->ld8 + 16) + size_t(rmax) * 16 + (rmax / 4 + 2) * 4;
-        if (ds->u8 && u8_smem <= 110 * 1024) {
-            CK(cudaFuncSetAttribute(join_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(u8_smem)));
-            int per_sm = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_u8_kernel, kJoinThreads, u8_smem));
-            const uint32_t grid = std::min<uint32_t>(n, uint32_t(num_sms()) * std::max(per_sm, 1));
-            LAUNCH(join_u8_kernel, grid, kJoinThreads, u8_smem, ja, ds->data8.p, ds->ld8, ds->norms8.p,
-                   s->order.n ? s->order.p : nullptr, rmax);
-        } else if (staged_smem <= 110 * 1024) {
-            CK(cudaFuncSetAttribute(join_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(staged_smem)));
-            int per_sm = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_staged_kernel, kJoinThreads,
-                                                             staged_smem));
-            const uint32_t grid = std::min<uint32_t>(n, uint32_t(num_sms()) * std::max(per_sm, 1));
-            LAUNCH(join_staged_kernel, grid, kJoinThreads, staged_smem, ja, s->order.n ? s->order.p : nullptr,
-                   rmax);
-        } else {
-            const uint32_t wpb = 8;
-            LAUNCH(join_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
+        unsigned long long cnt3[3] = {0, 0, 0};
+        CK(cudaMemcpyAsync(cnt3, counters.p, 24, cudaMemcpyDeviceToHost, stream()));
+        // group the spill list by target: offsets from per-target spill counts
+        DevBuf<uint32_t> ov_off(size_t(n) + 1);
+        DevBuf<uint64_t> ov_sorted_key;
+        if (spilled) {
+            DevBuf<uint32_t> counts(size_t(n) + 1);
+            LAUNCH(spill_counts_kernel, (n + 256) / 256, 256, 0, s->ocnt.p, n, s->offer_cap, counts.p);
+            exclusive_scan(counts.p, ov_off.p, n);
+            DevBuf<uint32_t> tgt_sorted(spilled);
+            ov_sorted_key.alloc(spilled);
+            int bits = 1;
+            while ((uint64_t(1) << bits) < n) ++bits;
+            size_t tmp = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p,
+                                               ov_sorted_key.p, spilled, 0, bits, stream()));
+            DevBuf<unsigned char> t(tmp);
+            prof_begin("cub_radix_sort_spill");
+            CK(cub::DeviceRadixSort::SortPairs(t.p, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, ov_sorted_key.p,
+                                               spilled, 0, bits, stream()));
+            prof_end();
+            note_launch();
         }
-        ov_cnt.download(&spilled, 1);
+        MergeArgs ma{n, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p,
+                     ov_off.p, spilled ? ov_sorted_key.p : s->ov_key.p, counters.p + 1,
+                     sub + 1 < nsub ? s->thr.p : nullptr};
+        const size_t pw = ((size_t(kPend) + 3 * size_t(s->P)) * 8 + s->P + 15) & ~size_t(15);
+        const uint32_t wps = 8;
+        if (pw * wps > 48 * 1024)
+            CK(cudaFuncSetAttribute(merge_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(pw * wps)));
+        LAUNCH(merge_stream_kernel, (n + wps - 1) / wps, wps * 32, pw * wps, ma);
         ssync();
-        if (spilled <= s->ov_cap) break;
-        s->ov_cap = next_pow2(spilled);  // spill list too small: grow and redo (pools untouched so far)
-        spill_per_point_hint = std::max<uint64_t>(spill_per_point_hint, (uint64_t(s->ov_cap) + n - 1) / n);
+        comps += cnt3[0];
+        offers += cnt3[2];
+        spilled_total += spilled;
     }
-    unsigned long long comps = 0;
-    counters.download(&comps, 1);
-    // group the spill list by target: offsets from per-target spill counts
-    DevBuf<uint32_t> ov_off(size_t(n) + 1);
-    DevBuf<uint64_t> ov_sorted_key;
-    if (spilled) {
-        DevBuf<uint32_t> counts(size_t(n) + 1);
-        LAUNCH(spill_counts_kernel, (n + 256) / 256, 256, 0, s->ocnt.p, n, s->offer_cap, counts.p);
-        exclusive_scan(counts.p, ov_off.p, n);
-        DevBuf<uint32_t> tgt_sorted(spilled);
-        ov_sorted_key.alloc(spilled);
-        int bits = 1;
-        while ((uint64_t(1) << bits) < n) ++bits;
-        size_t tmp = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, ov_sorted_key.p,
-                                           spilled, 0, bits, stream()));
-        DevBuf<unsigned char> t(tmp);
-        prof_begin("cub_radix_sort_spill");
-        CK(cub::DeviceRadixSort::SortPairs(t.p, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, ov_sorted_key.p,
-                                           spilled, 0, bits, stream()));
-        prof_end();
-        note_launch();
-    }
-    const size_t per_warp = (kMergeChunk + 3 * size_t(s->P)) * 8 + 2 * s->P;
-    const uint32_t wpb = uint32_t(std::max<size_t>(1, std::min<size_t>(8, (64 * 1024) / per_warp)));
-    const size_t smem = wpb * per_warp;
-    if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    MergeArgs ma{n, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p,
-                 ov_off.p, spilled ? ov_sorted_key.p : s->ov_key.p, counters.p + 1};
-    LAUNCH(merge_kernel, (n + wpb - 1) / wpb, wpb * 32, smem, ma);
+    // changes: entries inserted this round that survive (flag bit 1), bit cleared
+    DevBuf<unsigned long long> ch(1);
+    ch.zero();
+    const size_t cells = size_t(n) * s->P;
+    LAUNCH(count_inserted_kernel, uint32_t(std::min<size_t>((cells + 255) / 256, 16384)), 256, 0, s->flags.p,
+           cells, ch.p);
     unsigned long long changes = 0;
-    CK(cudaMemcpyAsync(&changes, counters.p + 1, 8, cudaMemcpyDeviceToHost, stream()));
+    ch.download(&changes, 1);
     ssync();
+    s->last_offers = offers;
+    {
+        const uint64_t want = std::max<uint64_t>(cap_floor, (offers / nsub / std::max(n, 1u)) * 5 / 4);
+        const uint32_t next = std::min<uint32_t>(cap_max, next_pow2(uint32_t(std::min<uint64_t>(want, 1u << 20))));
+        offer_cap_hint = std::max(offer_cap_hint, next);
+        s->offer_cap = std::max(s->offer_cap, next);  // takes effect next round (buffers reallocated)
+    }
+    s->last_spilled = spilled_total;
     s->dist_comps += comps;
     s->iteration += 1;
     s->last_changes = changes;
@@ -1465,6 +1833,15 @@ int annk_pool_topk_accuracy(const annk_state* s, const uint32_t* gt_ids, uint32_
         double sum = 0.0;  // graph_build.cpp:213-225 summation order
         for (uint32_t r = 0; r < gt_rows; ++r) sum += double(h[r]) / double(gt_k);
         *acc = sum / gt_rows;
+    });
+}
+
+int annk_state_stats(const annk_state* s, uint64_t* out) {
+    return abi([&] {
+        out[0] = s->join_rows;
+        out[1] = s->last_offers;
+        out[2] = s->last_spilled;
+        out[3] = s->offer_cap;
     });
 }
 

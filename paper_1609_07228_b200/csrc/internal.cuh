@@ -98,6 +98,7 @@ struct annk_state {
     int stage = 0;  // 0 none, 1 after rebuild_sample_lists, 2 after union_reverse_lists
     uint64_t join_rows = 0;
     uint32_t offer_cap = 0;
+    uint64_t last_offers = 0, last_spilled = 0;
 };
 
 struct annk_searcher {

@@ -106,7 +106,10 @@ void prof_begin(const char* name) {
 }
 void prof_end() {
     if (!g_prof || g_prof_pending.empty()) return;
-    CK(cudaEventRecord(g_prof_pending.back().b, stream()));
+    const cudaError_t e = cudaEventRecord(g_prof_pending.back().b, stream());
+    if (e != cudaSuccess)
+        throw Error(kCudaError, std::string("after kernel ") + g_prof_pending.back().name + ": " +
+                                    cudaGetErrorString(e));
 }
 int num_sms() {
     init_runtime();

@@ -40,3 +40,18 @@ for mode in ["plain", "plain", "prof", "sampler", "prof+sampler", "plain"]:
     print(mode, f"total {t1 - t0:.3f}s init {ts[0] - t0:.3f} it1 {ts[1] - ts[0]:.3f} it2 {ts[2] - ts[1]:.3f}",
           f"kernels {sum(v[1] for v in rep.values()) / 1e3:.3f}s", flush=True)
     del s
+
+# per-kernel breakdown of one step, per phase
+for phase in ("init", "it1", "it2", "it3"):
+    pass
+A.profile_reset()
+A.profile_enable(True)
+s = A.init_graph(vs, f, cfg["k"], cfg["dep"], cfg["P"], cfg["S"], bench.SEED)
+rep0 = A.profile_report()
+print("init:", {k: round(v[1], 2) for k, v in rep0.items()})
+for it in range(3):
+    A.profile_reset()
+    A.detail.nn_descent_iteration(s, vs)
+    rep = A.profile_report()
+    print(f"it{it + 1}:", {k: round(v[1], 2) for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])}, A.state_stats(s), s.meta()["dist_comps"])
+A.profile_enable(False)
