@@ -54,9 +54,13 @@ struct BuildArgs {
     uint32_t* rtmp;
     uint64_t* sortbuf;  // next_pow2(n) keys, for fallback sorts larger than kSortSmem
     uint32_t* meta;     // [num_nodes, root, leaf_count, max_depth, error]
+    const uint8_t* x8;  // exact u8 copy (nullptr: fp32 gathers)
+    uint32_t ld8;
 };
 
 struct Smem {
+    uint32_t sub[kWarpSubtree];   // warp path: subtree slice of point_index
+    uint32_t sub2[kWarpSubtree];  // warp path: right half during a partition
     uint64_t mt[312];
     uint64_t sortk[kSortSmem];
     StackEntry bstack[kStack];
@@ -157,38 +161,59 @@ __device__ uint32_t warp_draw(Smem& s, uint32_t dim) {
 
 // -------------------------------------------------------------- warp path
 
-__device__ void warp_sort_node(const BuildArgs& a, Smem& s, uint32_t start, uint32_t size,
-                               uint32_t d) {
+// Sorts sub[st, st+size) (subtree-local point ids) by (value, id) on dim d.
+__device__ void warp_sort_local(const BuildArgs& a, Smem& s, uint32_t* sub, uint32_t st, uint32_t size,
+                                uint32_t d) {
     const uint32_t lane = lane_id();
     const uint32_t m = next_pow2(size);
     uint64_t* k = m <= kSortSmem ? s.sortk : a.sortbuf;
     for (uint32_t j = lane; j < m; j += 32) {
         uint64_t key = kEmptyKey;
         if (j < size) {
-            const uint32_t id = a.pidx[start + j];
+            const uint32_t id = sub[st + j];
             key = val_id_key(ldx(a, id, d), id);
         }
         k[j] = key;
     }
     __syncwarp();
     warp_bitonic_sort(k, m);
-    for (uint32_t j = lane; j < size; j += 32) a.pidx[start + j] = uint32_t(k[j]);
+    for (uint32_t j = lane; j < size; j += 32) sub[st + j] = uint32_t(k[j]);
     __syncwarp();
 }
 
-// Builds the subtree rooted at `root` (its pre-order id is assigned here) with
-// warp 0 only.
+__device__ __forceinline__ float ldv(const BuildArgs& a, uint32_t p, uint32_t d) {
+    return a.x8 ? float(__ldg(a.x8 + size_t(p) * a.ld8 + d)) : __ldg(a.x + size_t(p) * a.ld + d);
+}
+
+// Builds the subtree rooted at `root` (<= kWarpSubtree points) with warp 0,
+// in pre-order (the root's id is assigned here).  The subtree's slice of
+// point_index lives in shared memory; each node gathers its column once (into
+// registers for nodes of <= 256 points), sums it exactly, and partitions by
+// ballots in shared memory.
 __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root) {
     const uint32_t lane = lane_id();
-    uint32_t wsp = 0;
-    if (lane == 0) s.wstack[0] = root;
-    wsp = 1;
-    bool prefetched = false;
+    const uint32_t base = root.start, total = root.end - root.start;
+    uint32_t* sub = s.sub;
+    uint32_t* rtmp = s.sub2;
+    for (uint32_t j = lane; j < total; j += 32) sub[j] = a.pidx[base + j];
+    __syncwarp();
+    // stage the subtree's rows in L2: every node below gathers from them
+    if (a.x8) {
+        for (uint32_t j = lane; j < total; j += 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.x8 + size_t(sub[j]) * a.ld8));
+    } else if (size_t(total) * a.ld * 4 <= kPrefetchBytes) {
+        const uint32_t lines = (a.ld * 4 + 127) / 128;
+        for (uint32_t j = lane; j < total * lines; j += 32) {
+            const char* ptr = reinterpret_cast<const char*>(a.x + size_t(sub[j / lines]) * a.ld) + (j % lines) * 128;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+        }
+    }
+    uint32_t wsp = 1;
+    if (lane == 0) s.wstack[0] = StackEntry{0, total, root.depth, root.parent, root.side};
     __syncwarp();
     while (wsp > 0) {
         --wsp;
         const StackEntry e = s.wstack[wsp];
-        __syncwarp();
         const uint32_t size = e.end - e.start;
         const uint32_t id = s.node_count;
         __syncwarp();
@@ -203,70 +228,126 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
         }
         if (size <= a.leaf_cap) {
             if (lane == 0) {
-                a.nodes[id] = KdNodeDev{kLeaf, 0.0f, e.start, e.end};
+                a.nodes[id] = KdNodeDev{kLeaf, 0.0f, base + e.start, base + e.end};
                 a.even[id] = 0;
                 s.leaf_count++;
             }
             __syncwarp();
             continue;
         }
-        if (!prefetched && size_t(size) * a.ld * 4 <= kPrefetchBytes) {
-            // Stage this subtree's rows in L2: every deeper node gathers from them.
-            prefetched = true;
-            const uint32_t lines = (a.ld * 4 + 127) / 128;
-            for (uint32_t j = lane; j < size * lines; j += 32) {
-                const uint32_t p = a.pidx[e.start + j / lines];
-                const char* ptr = reinterpret_cast<const char*>(a.x + size_t(p) * a.ld) + (j % lines) * 128;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
-            }
-        }
         const uint32_t d = warp_draw(s, a.dim);
-        // mean (kd_forest.cpp:55-59)
-        double sum = 0.0;
-        int top = INT_MIN, lsb = INT_MAX;
-        for (uint32_t p = e.start + lane; p < e.end; p += 32) {
-            const float v = ldx(a, a.pidx[p], d);
-            sum += double(v);
-            val_stats(v, top, lsb);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            top = max(top, __shfl_xor_sync(0xffffffffu, top, o));
-            lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
-        }
-        if (!sum_is_exact(top, lsb, size)) {
-            if (lane == 0) {
-                sum = 0.0;
-                for (uint32_t p = e.start; p < e.end; ++p) sum += double(ldx(a, a.pidx[p], d));
-            }
-            sum = __shfl_sync(0xffffffffu, sum, 0);
-        }
-        float split = __double2float_rn(__ddiv_rn(sum, double(size)));
-        // stable partition by value <= split (kd_forest.cpp:61-65)
+        const uint32_t chunks = (size + 31) / 32;
+        float split;
         uint32_t nl = 0, nr = 0;
-        for (uint32_t base = e.start; base < e.end; base += 32) {
-            const uint32_t p = base + lane;
-            const bool valid = p < e.end;
-            const uint32_t pid = valid ? a.pidx[p] : 0;
-            const bool left = valid && ldx(a, pid, d) <= split;
-            const uint32_t bl = __ballot_sync(0xffffffffu, left);
-            const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
+        if (chunks <= 8) {
+            // ---- register path: one gather per point
+            float v[8];
+            uint32_t pid[8];
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t j = e.start + u * 32 + lane;
+                const bool ok = u < chunks && j < e.end;
+                pid[u] = ok ? sub[j] : 0;
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t j = e.start + u * 32 + lane;
+                v[u] = (u < chunks && j < e.end) ? ldv(a, pid[u], d) : 0.0f;
+            }
+            double sum;
+            if (a.x8) {
+                uint32_t is = 0;
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) is += uint32_t(v[u]);
+                sum = double(__reduce_add_sync(0xffffffffu, is));  // exact: integers
+            } else {
+                sum = 0.0;
+                int top = INT_MIN, lsb = INT_MAX;
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) {
+                    sum += double(v[u]);
+                    val_stats(v[u], top, lsb);
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                    top = max(top, __shfl_xor_sync(0xffffffffu, top, o));
+                    lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+                }
+                if (!sum_is_exact(top, lsb, size)) {  // reference order: sequential over point_index
+                    double ser = 0.0;
+                    if (lane == 0)
+                        for (uint32_t p = e.start; p < e.end; ++p) ser += double(ldv(a, sub[p], d));
+                    sum = __shfl_sync(0xffffffffu, ser, 0);
+                }
+            }
+            split = __double2float_rn(__ddiv_rn(sum, double(size)));
             const uint32_t lt = (1u << lane) - 1u;
-            if (left) a.pidx[e.start + nl + __popc(bl & lt)] = pid;
-            else if (valid) a.rtmp[e.start + nr + __popc(br & lt)] = pid;
-            nl += __popc(bl);
-            nr += __popc(br);
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                if (u >= chunks) break;
+                const uint32_t j = e.start + u * 32 + lane;
+                const bool valid = j < e.end;
+                const bool left = valid && v[u] <= split;
+                const uint32_t bl = __ballot_sync(0xffffffffu, left);
+                const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
+                if (left) sub[e.start + nl + __popc(bl & lt)] = pid[u];
+                else if (valid) rtmp[nr + __popc(br & lt)] = pid[u];
+                nl += __popc(bl);
+                nr += __popc(br);
+            }
+        } else {
+            // ---- streaming path (large subtree roots): gather twice
+            double sum = 0.0;
+            int top = INT_MIN, lsb = INT_MAX;
+            uint32_t is = 0;
+            for (uint32_t p = e.start + lane; p < e.end; p += 32) {
+                const float x = ldv(a, sub[p], d);
+                if (a.x8) is += uint32_t(x);
+                else {
+                    sum += double(x);
+                    val_stats(x, top, lsb);
+                }
+            }
+            if (a.x8) {
+                sum = double(__reduce_add_sync(0xffffffffu, is));
+            } else {
+                for (int o = 16; o > 0; o >>= 1) {
+                    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                    top = max(top, __shfl_xor_sync(0xffffffffu, top, o));
+                    lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+                }
+                if (!sum_is_exact(top, lsb, size)) {
+                    double ser = 0.0;
+                    if (lane == 0)
+                        for (uint32_t p = e.start; p < e.end; ++p) ser += double(ldv(a, sub[p], d));
+                    sum = __shfl_sync(0xffffffffu, ser, 0);
+                }
+            }
+            split = __double2float_rn(__ddiv_rn(sum, double(size)));
+            const uint32_t lt = (1u << lane) - 1u;
+            for (uint32_t b0 = e.start; b0 < e.end; b0 += 32) {
+                const uint32_t p = b0 + lane;
+                const bool valid = p < e.end;
+                const uint32_t pid = valid ? sub[p] : 0;
+                const bool left = valid && ldv(a, pid, d) <= split;
+                const uint32_t bl = __ballot_sync(0xffffffffu, left);
+                const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
+                if (left) sub[e.start + nl + __popc(bl & lt)] = pid;
+                else if (valid) rtmp[nr + __popc(br & lt)] = pid;
+                nl += __popc(bl);
+                nr += __popc(br);
+            }
         }
         __syncwarp();
-        for (uint32_t j = lane; j < nr; j += 32) a.pidx[e.start + nl + j] = a.rtmp[e.start + j];
+        for (uint32_t j = lane; j < nr; j += 32) sub[e.start + nl + j] = rtmp[j];
         __syncwarp();
         uint32_t mid = e.start + nl;
         uint8_t even = 0;
         if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
             // kd_forest.cpp:70-83 degenerate split: sort by (value, id), split at the median
-            warp_sort_node(a, s, e.start, size, d);
+            warp_sort_local(a, s, sub, e.start, size, d);
             mid = e.start + size / 2;
-            split = midpoint_f(ldx(a, a.pidx[mid - 1], d), ldx(a, a.pidx[mid], d));
+            split = midpoint_f(ldx(a, sub[mid - 1], d), ldx(a, sub[mid], d));
             even = 1;
         }
         if (lane == 0) {
@@ -274,15 +355,14 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
             a.even[id] = even;
             s.wstack[wsp] = StackEntry{mid, e.end, e.depth + 1, id, 1};
             s.wstack[wsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, 0};
+            if (wsp + 2 > kStack - 2) s.error = 1;
         }
-        wsp += 2;
-        if (wsp > kStack - 2 && lane == 0) s.error = 1;
-        if (wsp > kStack - 2) break;
+        wsp = min(wsp + 2, kStack - 2);
         __syncwarp();
     }
+    for (uint32_t j = lane; j < total; j += 32) a.pidx[base + j] = sub[j];
     __syncwarp();
 }
-
 // ------------------------------------------------------------- block path
 
 __device__ void block_reduce_stats(Smem& s, double& sum, int& top, int& lsb) {
@@ -629,7 +709,7 @@ int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_ca
             args[t] = BuildArgs{ds->data.p, n, ds->dim, ds->ld, leaf_cap, substream(seed, t),
                                 tr.nodes.p, tr.depth.p, tr.even.p, tr.pidx.p,
                                 rtmp.p + size_t(t) * n, sortbuf.p + size_t(t) * next_pow2(n),
-                                meta.p + 5 * t};
+                                meta.p + 5 * t, ds->u8 ? ds->data8.p : nullptr, ds->ld8};
         }
         DevBuf<BuildArgs> dargs(n_trees);
         dargs.upload(args.data(), n_trees);
