@@ -276,10 +276,16 @@ def run_gpu(args, cfg, ws, rank, local):
         crossing = cfg["max_iters"]
     del st
 
+    phase_ms = {"init": [], **{f"iter{j + 1}": [] for j in range(crossing)}}
+
     def build_once():
+        t0 = time.perf_counter()
         s = A.init_graph(vs, forest, k, cfg["dep"], cfg["P"], cfg["S"], SEED)
-        for _ in range(crossing):
+        phase_ms["init"].append((time.perf_counter() - t0) * 1e3)
+        for j in range(crossing):
+            t0 = time.perf_counter()
             A.detail.nn_descent_iteration(s, vs)
+            phase_ms[f"iter{j + 1}"].append((time.perf_counter() - t0) * 1e3)
         return s
 
     for _ in range(args.warmup):
@@ -419,6 +425,7 @@ def run_gpu(args, cfg, ws, rank, local):
         "aux_seconds": {"forest": forest_s, "gt_rows": gt_rows_s, "gt_queries": gt_q_s, "data_gen_host": gen_s,
                         "brute_force_pairs_per_s": bf_pairs / (gt_rows_s + gt_q_s)},
         "host_wall_s_per_step": wall_s,
+        "phase_wall_ms_median": {p: round(statistics.median(v), 2) for p, v in phase_ms.items() if v},
         "kernels_ms": {k2: round(v2[1], 3) for k2, v2 in sorted(prof.items(), key=lambda kv: -kv[1][1])},
     }
     if rank == 0:

@@ -65,7 +65,13 @@ void prof_end();
         CK(cudaGetLastError());                                                  \
     } while (0)
 
-// Stream-ordered device buffer (cudaMallocAsync on the library stream).
+// Device memory through a size-keyed block cache on top of the stream-ordered
+// pool: repeated builds reuse the previous state's scratch (GBs at 1M points)
+// instead of re-mapping it.  All work runs on one stream, so reuse is ordered.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes) noexcept;
+
+// Stream-ordered device buffer.
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -83,10 +89,10 @@ struct DevBuf {
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream()));
+        if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
     }
     void release() noexcept {
-        if (p) cudaFreeAsync(p, stream());
+        if (p) dev_free(p, n * sizeof(T));
         p = nullptr;
         n = 0;
     }

@@ -44,6 +44,54 @@ cudaStream_t stream() {
 }
 void note_launch() { ++g_launches; }
 
+// ---- size-keyed device block cache (see common.cuh)
+namespace {
+struct Cached {
+    size_t bytes;
+    void* p;
+};
+std::vector<Cached> g_cache;
+size_t g_cache_bytes = 0;
+constexpr size_t kCacheCap = size_t(48) << 30;
+}  // namespace
+
+void* dev_alloc(size_t bytes) {
+    for (size_t i = g_cache.size(); i-- > 0;) {
+        if (g_cache[i].bytes == bytes) {
+            void* p = g_cache[i].p;
+            g_cache_bytes -= bytes;
+            g_cache.erase(g_cache.begin() + long(i));
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, stream());
+    if (e == cudaErrorMemoryAllocation && !g_cache.empty()) {  // give cached blocks back and retry
+        cudaGetLastError();
+        for (auto& c : g_cache) cudaFreeAsync(c.p, stream());
+        g_cache.clear();
+        g_cache_bytes = 0;
+        e = cudaMallocAsync(&p, bytes, stream());
+    }
+    CK(e);
+    return p;
+}
+
+void dev_free(void* p, size_t bytes) noexcept {
+    if (!p) return;
+    if (bytes < (size_t(1) << 20)) {  // small blocks: the pool handles them well
+        cudaFreeAsync(p, g_stream);
+        return;
+    }
+    g_cache.push_back(Cached{bytes, p});
+    g_cache_bytes += bytes;
+    while (g_cache_bytes > kCacheCap && !g_cache.empty()) {
+        cudaFreeAsync(g_cache.front().p, g_stream);
+        g_cache_bytes -= g_cache.front().bytes;
+        g_cache.erase(g_cache.begin());
+    }
+}
+
 // ---- per-kernel CUDA-event profiler (annk_profile_*): events are recorded on
 // the library stream around each launch; durations are resolved lazily.
 namespace {
@@ -149,6 +197,25 @@ __global__ void to_u8_kernel(const float* __restrict__ x, uint32_t n, uint32_t d
     if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(bad, 1u);
 }
 
+__global__ void finite_kernel(const float* __restrict__ x, size_t count, uint32_t* __restrict__ bad) {
+    bool ok = true;
+    for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < count; t += size_t(gridDim.x) * blockDim.x)
+        ok &= isfinite(x[t]);
+    if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+void check_finite(annk_dataset* ds) {
+    const size_t count = size_t(ds->n) * ds->ld;
+    if (count == 0) return;
+    DevBuf<uint32_t> bad(1);
+    bad.zero();
+    LAUNCH(finite_kernel, uint32_t(std::min<size_t>((count + 255) / 256, 8192)), 256, 0, ds->data.p, count, bad.p);
+    uint32_t h = 0;
+    bad.download(&h, 1);
+    ssync();
+    if (h) throw_invalid("dataset_create: non-finite value");
+}
+
 void make_u8(annk_dataset* ds) {
     ds->u8 = false;
     if (ds->n == 0 || uint64_t(ds->dim) * 255ull * 255ull >= (1ull << 24)) return;
@@ -241,14 +308,13 @@ int annk_dataset_create(const float* host, uint32_t n, uint32_t dim, annk_datase
         if (!out) throw_invalid("dataset_create: null out");
         if (dim < 1) throw_invalid("dataset_create: dim must be >= 1");
         if (n > 0 && !host) throw_invalid("dataset_create: null data");
-        for (size_t i = 0; i < size_t(n) * dim; ++i)
-            if (!std::isfinite(host[i])) throw_invalid("dataset_create: non-finite value");
         auto* ds = new annk_dataset;
         ds->n = n;
         ds->dim = dim;
         ds->ld = (dim + 3) & ~3u;
         try {
             upload_rows(ds, host);
+            check_finite(ds);  // load_fvecs rejects non-finite values (dataset.cpp:123-126)
             const char* off = getenv("ANNK_DISABLE_U8");
             if (!(off && off[0] == '1')) make_u8(ds);
             ssync();

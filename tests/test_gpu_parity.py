@@ -324,3 +324,13 @@ def test_integer_data_both_datapaths_bit_exact(u8, monkeypatch):
     np.testing.assert_array_equal(r.ids, ids_s)
     np.testing.assert_array_equal(r.dists.view(np.uint32), d_s.view(np.uint32))
     np.testing.assert_array_equal(r.stats, st_s)
+
+
+def test_dataset_rejects_non_finite():
+    x = A.gen_synthetic(100, 5, 1)
+    x[37, 2] = np.nan
+    with pytest.raises(A.InvalidArgument):
+        A.VectorSet(x)
+    x[37, 2] = np.inf
+    with pytest.raises(A.InvalidArgument):
+        A.VectorSet(x)
