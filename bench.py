@@ -371,25 +371,37 @@ def run_gpu(args, cfg, ws, rank, local):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    row_bytes = dim * 4
+    dsinfo = vs.info()
+    row_bytes = dsinfo["row_bytes"]  # bytes per row actually gathered (u8 rows on the exact u8 path)
     dom = max(prof.items(), key=lambda kv: kv[1][1])
     dom_name, (dom_cnt, dom_ms) = dom
-    if dom_name == "join_kernel":
+    if dom_name.startswith("join"):
         rows_per_launch = sum(join_rows[:crossing]) / crossing
         alg_bytes = rows_per_launch * (row_bytes + 4) + n * 8
-        unit_desc = "sum_i(|new_i|+|old_i|) rows of 4d bytes + 4-byte ids, + N*8 thresholds"
+        unit_desc = (f"per launch: sum_i(|new_i|+|old_i|) list rows x ({row_bytes} B row + 4 B id) + N x 8 B "
+                     "thresholds (each list member's row gathered once per point)")
     elif dom_name == "init_kernel":
         alg_bytes = comps[0] * (row_bytes + 4) + n * cfg["P"] * 9
-        unit_desc = "init dist_comps rows of 4d bytes + ids, + N*P*9 pool bytes"
+        unit_desc = (f"per launch: init dist_comps x ({row_bytes} B candidate row + 4 B id) + N x P x 9 B "
+                     "pool writes")
     else:
         alg_bytes = None
         unit_desc = "n/a"
     per_launch_s = dom_ms / dom_cnt / 1e3
     achieved = alg_bytes / per_launch_s / 1e9 if alg_bytes else None
+    traffic = None
+    try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh).get(args.config, {}).get(dom_name)
+            traffic = tr["dram_bytes_per_launch"] if tr else None
+    except Exception:
+        pass
     roofline = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
-                "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes, "per_launch_ms": per_launch_s * 1e3,
-                "share_of_step": dom_ms / sum(v[1] for v in prof.values()), "units": unit_desc}
+                "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
+                "per_launch_ms": per_launch_s * 1e3,
+                "share_of_step": dom_ms / sum(v[1] for v in prof.values()), "units": unit_desc,
+                "exact_u8_path": dsinfo["u8"]}
 
     # CPU baseline: the reference library on a bounded sample (rank 0, N=1)
     cpu = None
@@ -406,7 +418,7 @@ def run_gpu(args, cfg, ws, rank, local):
     line = {
         "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic",
+        "dtype": "u8" if dsinfo["u8"] else "f32", "data": "synthetic",
         "config": {"workload": args.config, "n": n, "dim": dim, "trees": cfg["trees"], "leaf_cap": cfg["leaf"],
                    "k": k, "pool_cap": cfg["P"], "sample_cap": cfg["S"], "conquer_depth": cfg["dep"],
                    "iterations_to_acc_0.9": crossing, "accuracy_sample_rows": int(len(rows)),

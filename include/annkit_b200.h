@@ -67,6 +67,10 @@ int annk_profile_report(char* buf, uint64_t cap);
 int annk_dataset_create(const float* host, uint32_t n, uint32_t dim, annk_dataset** out);
 int annk_dataset_destroy(annk_dataset* ds);
 int annk_dataset_shape(const annk_dataset* ds, uint32_t* n, uint32_t* dim);
+/* [n, dim, exact_u8_path (0/1), bytes per row the kernels gather].  The u8
+ * path is taken when every value is an integer in [0,255] and dim*255^2 < 2^24:
+ * then the reference's fp32 l2_sq is exact and |a|^2+|b|^2-2a.b in int32 equals it. */
+int annk_dataset_info(const annk_dataset* ds, uint32_t* out4);
 
 /* dataset.cpp:201-214 gen_synthetic — host helper, same bytes as the reference. */
 int annk_gen_synthetic(uint32_t n, uint32_t dim, uint64_t seed, float* out);

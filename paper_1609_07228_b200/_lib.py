@@ -66,6 +66,7 @@ _SIGS = {
     "annk_dataset_create": [_f32p, _u32, _u32, _pp],
     "annk_dataset_destroy": [_vp],
     "annk_dataset_shape": [_vp, C.POINTER(_u32), C.POINTER(_u32)],
+    "annk_dataset_info": [_vp, _u32p],
     "annk_gen_synthetic": [_u32, _u32, _u64, _f32p],
     "annk_gen_mixture": [_u32, _u32, _u32, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int,
                          _u64, _u32, _f32p],

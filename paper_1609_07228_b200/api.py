@@ -62,6 +62,12 @@ class VectorSet:
     def handle(self):
         return self._h
 
+    def info(self) -> dict:
+        """n, dim, whether the exact u8 datapath is active, bytes per gathered row."""
+        out = np.zeros(4, np.uint32)
+        check(lib.annk_dataset_info(self._h, out))
+        return dict(n=int(out[0]), dim=int(out[1]), u8=bool(out[2]), row_bytes=int(out[3]))
+
     def row(self, i: int) -> np.ndarray:
         return self.data[i]
 

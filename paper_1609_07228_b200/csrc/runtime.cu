@@ -328,6 +328,15 @@ int annk_dataset_create(const float* host, uint32_t n, uint32_t dim, annk_datase
 int annk_dataset_destroy(annk_dataset* ds) {
     return abi([&] { delete ds; });
 }
+int annk_dataset_info(const annk_dataset* ds, uint32_t* out4) {
+    return abi([&] {
+        out4[0] = ds->n;
+        out4[1] = ds->dim;
+        out4[2] = ds->u8 ? 1u : 0u;
+        out4[3] = ds->u8 ? ds->ld8 : ds->ld * 4;  // bytes per gathered row
+    });
+}
+
 int annk_dataset_shape(const annk_dataset* ds, uint32_t* n, uint32_t* dim) {
     return abi([&] {
         *n = ds->n;
