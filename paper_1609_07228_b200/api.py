@@ -377,11 +377,15 @@ def refine_nn_descent(state: RefineState, vs, max_iters: int, workers: int = 1,
     return int(it.value)
 
 
-def finalize(state: RefineState, vs, k: int) -> KnnGraph:
-    """graph_build.cpp:346-373."""
+def finalize(state: RefineState, vs, k: int, out_ids: Optional[np.ndarray] = None,
+             out_dists: Optional[np.ndarray] = None) -> KnnGraph:
+    """graph_build.cpp:346-373.  out_ids/out_dists (n x k, C-contiguous) may be
+    caller buffers, e.g. pinned host memory for fast device-to-host copies."""
     n = state.meta()["n"]
-    ids = np.empty((n, k), np.uint32)
-    d = np.empty((n, k), np.float32)
+    ids = np.empty((n, k), np.uint32) if out_ids is None else out_ids
+    d = np.empty((n, k), np.float32) if out_dists is None else out_dists
+    if ids.shape != (n, k) or d.shape != (n, k) or ids.dtype != np.uint32 or d.dtype != np.float32:
+        raise InvalidArgument("finalize: output buffers must be n x k uint32 / float32")
     v = _as_vs(vs)
     check(lib.annk_finalize(state.handle, v.handle, k, ids, d))
     return KnnGraph(ids, d)

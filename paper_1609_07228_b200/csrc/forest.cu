@@ -25,6 +25,8 @@
 // node (always true for integer-valued data and for gen_synthetic data); when
 // it fails the node's sum is done serially in point_index order.
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../include/annkit_b200.h"
 #include "internal.cuh"
@@ -38,6 +40,11 @@ constexpr uint32_t kWarpSubtree = 4096;
 constexpr uint32_t kSortSmem = 4096;
 constexpr uint32_t kStack = 160;
 constexpr size_t kPrefetchBytes = 4u << 20;
+constexpr uint32_t kDrawWin = 256;
+#ifndef ANNK_PREFETCH_NEXT
+#define ANNK_PREFETCH_NEXT 0
+#endif
+constexpr bool kPrefetchNext = ANNK_PREFETCH_NEXT != 0;  // measured: no gain
 
 struct StackEntry {
     uint32_t start, end, depth, parent, side;  // side 0 = left child, 1 = right
@@ -56,19 +63,24 @@ struct BuildArgs {
     uint32_t* meta;     // [num_nodes, root, leaf_count, max_depth, error]
     const uint8_t* x8;  // exact u8 copy (nullptr: fp32 gathers)
     uint32_t ld8;
+    const uint32_t* draws;  // split dimension of the k-th internal node in pre-order
+    uint32_t n_draws;
 };
 
 struct Smem {
+    float vals[2][kWarpSubtree];  // warp path: left child's values on its split dim, by depth parity
     uint32_t sub[kWarpSubtree];   // warp path: subtree slice of point_index
     uint32_t sub2[kWarpSubtree];  // warp path: right half during a partition
-    uint64_t mt[312];
     uint64_t sortk[kSortSmem];
     StackEntry bstack[kStack];
     StackEntry wstack[kStack];
     double red_sum[kWarps];
     int red_top[kWarps], red_lsb[kWarps];
     uint32_t cnt_l[kWarps], cnt_r[kWarps];
-    uint32_t mt_idx, node_count, leaf_count, max_depth, error;
+    uint32_t dwin[kDrawWin];
+    uint32_t dwin_base, draw_idx, node_count, leaf_count, max_depth, error;
+    long long cyc_block, cyc_warp;
+    long long ft[8], ft_last;
     uint32_t bsp;
     // broadcast slots for the block path
     uint32_t b_d, b_nl, b_nr, b_mid, b_even;
@@ -121,45 +133,48 @@ __device__ __forceinline__ float midpoint_f(float a, float b) {
     return __fadd_rn(__fdiv_rn(a, 2.0f), __fdiv_rn(b, 2.0f));
 }
 
-// In-place std::mt19937_64 regeneration of 312 words by one warp.
-__device__ void warp_twist(uint64_t* mt) {
-    const uint32_t lane = lane_id();
-    for (uint32_t b = 0; b < 156; b += 32) {  // phase 1: i in [0,156)
-        const uint32_t i = b + lane;
-        uint64_t v = 0;
-        if (i < 156) v = mt_twist(mt[i], mt[i + 1], mt[i + 156]);
-        __syncwarp();
-        if (i < 156) mt[i] = v;
-        __syncwarp();
-    }
-    for (uint32_t b = 156; b < 311; b += 32) {  // phase 2: i in [156,311)
-        const uint32_t i = b + lane;
-        uint64_t v = 0;
-        if (i < 311) v = mt_twist(mt[i], mt[i + 1], mt[i - 156]);
-        __syncwarp();
-        if (i < 311) mt[i] = v;
-        __syncwarp();
-    }
-    if (lane == 0) mt[311] = mt_twist(mt[311], mt[0], mt[155]);
+// Split dimension of internal node k in pre-order (kd_forest.cpp:53:
+// rng_() % dim), read through a shared-memory window over the tree's
+// precomputed draw stream (draws_kernel).  Warp-collective.
+__device__ uint32_t warp_draw_at(const BuildArgs& a, Smem& s, uint32_t k) {
     __syncwarp();
+    if (k < s.dwin_base || k >= s.dwin_base + kDrawWin) {
+        const uint32_t base = k & ~(kDrawWin - 1);
+        for (uint32_t j = lane_id(); j < kDrawWin; j += 32)
+            s.dwin[j] = base + j < a.n_draws ? a.draws[base + j] : 0u;
+        __syncwarp();
+        if (lane_id() == 0) s.dwin_base = base;
+        __syncwarp();
+    }
+    const uint32_t d = s.dwin[k - s.dwin_base];
+    __syncwarp();
+    return d;
 }
-
-// Next split dimension (kd_forest.cpp:53: rng_() % dim). Warp-collective.
-__device__ uint32_t warp_draw(Smem& s, uint32_t dim) {
+__device__ uint32_t warp_draw(const BuildArgs& a, Smem& s) {
+    const uint32_t k = s.draw_idx;
+    const uint32_t d = warp_draw_at(a, s, k);
+    if (lane_id() == 0) s.draw_idx = k + 1;
     __syncwarp();
-    if (s.mt_idx >= 312) {
-        warp_twist(s.mt);
-        if (lane_id() == 0) s.mt_idx = 0;
-        __syncwarp();
-    }
-    const uint64_t v = mt_temper(s.mt[s.mt_idx]);
-    __syncwarp();
-    if (lane_id() == 0) s.mt_idx++;
-    __syncwarp();
-    return uint32_t(v % uint64_t(dim));
+    return d;
 }
 
 // -------------------------------------------------------------- warp path
+
+#ifdef ANNK_FOREST_TIMING
+// phase probes: cycles between consecutive marks accumulate in s.ft[mark]
+#define FT_MARK(m)                                                   \
+    do {                                                             \
+        const long long _t = clock64();                              \
+        if (lane_id() == 0) {                                        \
+            if ((m) > 0) s.ft[(m)] += _t - s.ft_last;                \
+            s.ft_last = _t;                                          \
+        }                                                            \
+    } while (0)
+#else
+#define FT_MARK(m) \
+    do {           \
+    } while (0)
+#endif
 
 // Sorts sub[st, st+size) (subtree-local point ids) by (value, id) on dim d.
 __device__ void warp_sort_local(const BuildArgs& a, Smem& s, uint32_t* sub, uint32_t st, uint32_t size,
@@ -208,8 +223,10 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
         }
     }
+    // side bit 0: right child; bit 1: this node's split-dim values are staged in
+    // vals[depth & 1] (gathered by the parent, whose next draw is ours)
     uint32_t wsp = 1;
-    if (lane == 0) s.wstack[0] = StackEntry{0, total, root.depth, root.parent, root.side};
+    if (lane == 0) s.wstack[0] = StackEntry{0, total, root.depth, root.parent, root.side & 1u};
     __syncwarp();
     while (wsp > 0) {
         --wsp;
@@ -220,7 +237,7 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
         if (lane == 0) {
             s.node_count = id + 1;
             if (e.parent != kInvalidId) {
-                if (e.side == 0) a.nodes[e.parent].left = id;
+                if ((e.side & 1u) == 0) a.nodes[e.parent].left = id;
                 else a.nodes[e.parent].right = id;
             }
             a.depth[id] = e.depth;
@@ -235,13 +252,22 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
             __syncwarp();
             continue;
         }
-        const uint32_t d = warp_draw(s, a.dim);
+        FT_MARK(0);
+        const uint32_t k = s.draw_idx;
+        const uint32_t d = warp_draw(a, s);
+        // the left child, if internal, is the next internal node in pre-order: draw k+1
+        const bool want_next = kPrefetchNext && size > a.leaf_cap + 1;
+        const uint32_t dn = want_next ? warp_draw_at(a, s, k + 1) : 0u;
+        FT_MARK(1);
+        const bool staged = (e.side & 2u) != 0;
+        const float* vin = s.vals[e.depth & 1u];
+        float* vout = s.vals[(e.depth + 1) & 1u];
         const uint32_t chunks = (size + 31) / 32;
         float split;
         uint32_t nl = 0, nr = 0;
         if (chunks <= 8) {
-            // ---- register path: one gather per point
-            float v[8];
+            // ---- register path: at most one gather round for this node and its left child
+            float v[8], w[8];
             uint32_t pid[8];
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
@@ -252,8 +278,11 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
                 const uint32_t j = e.start + u * 32 + lane;
-                v[u] = (u < chunks && j < e.end) ? ldv(a, pid[u], d) : 0.0f;
+                const bool ok = u < chunks && j < e.end;
+                v[u] = ok ? (staged ? vin[j] : ldv(a, pid[u], d)) : 0.0f;
+                w[u] = (ok && want_next) ? ldv(a, pid[u], dn) : 0.0f;
             }
+            FT_MARK(2);
             double sum;
             if (a.x8) {
                 uint32_t is = 0;
@@ -281,6 +310,7 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
                 }
             }
             split = __double2float_rn(__ddiv_rn(sum, double(size)));
+            FT_MARK(3);
             const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
@@ -290,18 +320,23 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
                 const bool left = valid && v[u] <= split;
                 const uint32_t bl = __ballot_sync(0xffffffffu, left);
                 const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
-                if (left) sub[e.start + nl + __popc(bl & lt)] = pid[u];
-                else if (valid) rtmp[nr + __popc(br & lt)] = pid[u];
+                if (left) {
+                    const uint32_t pos = e.start + nl + __popc(bl & lt);
+                    sub[pos] = pid[u];
+                    vout[pos] = w[u];
+                } else if (valid) {
+                    rtmp[nr + __popc(br & lt)] = pid[u];
+                }
                 nl += __popc(bl);
                 nr += __popc(br);
             }
         } else {
-            // ---- streaming path (large subtree roots): gather twice
+            // ---- streaming path (subtree roots > 256 points): two passes
             double sum = 0.0;
             int top = INT_MIN, lsb = INT_MAX;
             uint32_t is = 0;
             for (uint32_t p = e.start + lane; p < e.end; p += 32) {
-                const float x = ldv(a, sub[p], d);
+                const float x = staged ? vin[p] : ldv(a, sub[p], d);
                 if (a.x8) is += uint32_t(x);
                 else {
                     sum += double(x);
@@ -329,20 +364,29 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
                 const uint32_t p = b0 + lane;
                 const bool valid = p < e.end;
                 const uint32_t pid = valid ? sub[p] : 0;
-                const bool left = valid && ldv(a, pid, d) <= split;
+                const float x = valid ? (staged ? vin[p] : ldv(a, pid, d)) : 0.0f;
+                const float wn = (valid && want_next) ? ldv(a, pid, dn) : 0.0f;
+                const bool left = valid && x <= split;
                 const uint32_t bl = __ballot_sync(0xffffffffu, left);
                 const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
-                if (left) sub[e.start + nl + __popc(bl & lt)] = pid;
-                else if (valid) rtmp[nr + __popc(br & lt)] = pid;
+                if (left) {
+                    const uint32_t pos = e.start + nl + __popc(bl & lt);
+                    sub[pos] = pid;
+                    vout[pos] = wn;
+                } else if (valid) {
+                    rtmp[nr + __popc(br & lt)] = pid;
+                }
                 nl += __popc(bl);
                 nr += __popc(br);
             }
         }
+        FT_MARK(4);
         __syncwarp();
         for (uint32_t j = lane; j < nr; j += 32) sub[e.start + nl + j] = rtmp[j];
         __syncwarp();
         uint32_t mid = e.start + nl;
         uint8_t even = 0;
+        FT_MARK(5);
         if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
             // kd_forest.cpp:70-83 degenerate split: sort by (value, id), split at the median
             warp_sort_local(a, s, sub, e.start, size, d);
@@ -353,16 +397,19 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
         if (lane == 0) {
             a.nodes[id] = KdNodeDev{d, split, 0u, 0u};
             a.even[id] = even;
-            s.wstack[wsp] = StackEntry{mid, e.end, e.depth + 1, id, 1};
-            s.wstack[wsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, 0};
+            const uint32_t left_staged = (want_next && !even) ? 2u : 0u;
+            s.wstack[wsp] = StackEntry{mid, e.end, e.depth + 1, id, 1u};
+            s.wstack[wsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, left_staged};
             if (wsp + 2 > kStack - 2) s.error = 1;
         }
         wsp = min(wsp + 2, kStack - 2);
         __syncwarp();
+        FT_MARK(6);
     }
     for (uint32_t j = lane; j < total; j += 32) a.pidx[base + j] = sub[j];
     __syncwarp();
 }
+
 // ------------------------------------------------------------- block path
 
 __device__ void block_reduce_stats(Smem& s, double& sum, int& top, int& lsb) {
@@ -422,7 +469,7 @@ __device__ void block_split_node(const BuildArgs& a, Smem& s, const StackEntry& 
     const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid / 32;
     const uint32_t size = e.end - e.start;
     if (warp == 0) {
-        const uint32_t d = warp_draw(s, a.dim);
+        const uint32_t d = warp_draw(a, s);
         if (lane == 0) s.b_d = d;
     }
     __syncthreads();
@@ -509,14 +556,15 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
     const uint32_t tid = threadIdx.x;
     for (uint32_t i = tid; i < a.n; i += kBlock) a.pidx[i] = i;
     if (tid == 0) {
-        s.mt[0] = a.seed;
-        for (int i = 1; i < 312; ++i)
-            s.mt[i] = 6364136223846793005ULL * (s.mt[i - 1] ^ (s.mt[i - 1] >> 62)) + uint64_t(i);
-        s.mt_idx = 312;
+        s.dwin_base = 0xffffffffu - kDrawWin;  // empty window
+        s.draw_idx = 0;
         s.node_count = 0;
         s.leaf_count = 0;
         s.max_depth = 0;
         s.error = 0;
+        s.cyc_block = 0;
+        s.cyc_warp = 0;
+        for (int q = 0; q < 8; ++q) s.ft[q] = 0;
         s.bstack[0] = StackEntry{0, a.n, 0, kInvalidId, 0};
         s.bsp = 1;
     }
@@ -528,7 +576,9 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
         if (size <= kWarpSubtree) {
             if (tid == 0) s.bsp -= 1;
             __syncthreads();
+            const long long c0 = clock64();
             if (tid < 32) warp_build_subtree(a, s, e);
+            if (tid == 0) s.cyc_warp += clock64() - c0;
             __syncthreads();
             continue;
         }
@@ -545,7 +595,9 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
             s.max_depth = max(s.max_depth, e.depth);
         }
         __syncthreads();
+        const long long c1 = clock64();
         block_split_node(a, s, e, id);
+        if (tid == 0) s.cyc_block += clock64() - c1;
     }
     __syncthreads();
     if (tid == 0) {
@@ -554,6 +606,43 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
         a.meta[2] = s.leaf_count;
         a.meta[3] = s.max_depth;
         a.meta[4] = s.error;
+        a.meta[5] = uint32_t(s.cyc_block >> 10);  // phase timing (kcycles), debug/profiling
+        a.meta[6] = uint32_t(s.cyc_warp >> 10);
+#ifdef ANNK_FOREST_TIMING
+        printf("tree %u phases (Mcycles): draw %.1f gather %.1f sum %.1f part %.1f copy %.1f tail %.1f\n",
+               blockIdx.x, s.ft[1] / 1e6, s.ft[2] / 1e6, s.ft[3] / 1e6, s.ft[4] / 1e6, s.ft[5] / 1e6, s.ft[6] / 1e6);
+#endif
+    }
+}
+
+// The per-tree split-dimension stream: out[t][k] = mt19937_64(substream(seed,t))
+// output k mod dim (kd_forest.cpp:53,259).  One CTA per tree; each 312-word
+// regeneration is a 3-phase parallel twist, tempering and the modulo are
+// per-word parallel.  n draws cover every internal node (<= n-1).
+__global__ void draws_kernel(uint64_t seed, uint32_t dim, uint32_t count, uint32_t* __restrict__ out) {
+    __shared__ uint64_t mt[312];
+    const uint32_t t = blockIdx.x, tid = threadIdx.x;
+    uint32_t* o = out + size_t(t) * count;
+    if (tid == 0) {
+        mt[0] = substream(seed, t);
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
+    }
+    __syncthreads();
+    for (uint32_t g = 0; g * 312 < count; ++g) {
+        uint64_t v = 0;
+        if (tid < 156) v = mt_twist(mt[tid], mt[tid + 1], mt[tid + 156]);
+        __syncthreads();
+        if (tid < 156) mt[tid] = v;
+        __syncthreads();
+        if (tid >= 156 && tid < 311) v = mt_twist(mt[tid], mt[tid + 1], mt[tid - 156]);
+        __syncthreads();
+        if (tid >= 156 && tid < 311) mt[tid] = v;
+        __syncthreads();
+        if (tid == 0) mt[311] = mt_twist(mt[311], mt[0], mt[155]);
+        __syncthreads();
+        const uint32_t k = g * 312 + tid;
+        if (tid < 312 && k < count) o[k] = uint32_t(mt_temper(mt[tid]) % uint64_t(dim));
+        __syncthreads();
     }
 }
 
@@ -698,7 +787,9 @@ int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_ca
         const size_t cap_nodes = 2 * size_t(n);
         DevBuf<uint32_t> rtmp(size_t(n) * n_trees);
         DevBuf<uint64_t> sortbuf(size_t(next_pow2(n)) * n_trees);
-        DevBuf<uint32_t> meta(5 * n_trees);
+        DevBuf<uint32_t> meta(8 * n_trees);
+        DevBuf<uint32_t> draws(size_t(n) * n_trees);
+        LAUNCH(draws_kernel, n_trees, 320, 0, seed, ds->dim, n, draws.p);
         std::vector<BuildArgs> args(n_trees);
         for (uint32_t t = 0; t < n_trees; ++t) {
             TreeDev& tr = f->trees[t];
@@ -709,23 +800,27 @@ int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_ca
             args[t] = BuildArgs{ds->data.p, n, ds->dim, ds->ld, leaf_cap, substream(seed, t),
                                 tr.nodes.p, tr.depth.p, tr.even.p, tr.pidx.p,
                                 rtmp.p + size_t(t) * n, sortbuf.p + size_t(t) * next_pow2(n),
-                                meta.p + 5 * t, ds->u8 ? ds->data8.p : nullptr, ds->ld8};
+                                meta.p + 8 * t, ds->u8 ? ds->data8.p : nullptr, ds->ld8,
+                                draws.p + size_t(t) * n, n};
         }
         DevBuf<BuildArgs> dargs(n_trees);
         dargs.upload(args.data(), n_trees);
         const size_t smem = sizeof(Smem);
         CK(cudaFuncSetAttribute(forest_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         LAUNCH(forest_build_kernel, n_trees, kBlock, smem, dargs.p);
-        std::vector<uint32_t> hm(5 * n_trees);
+        std::vector<uint32_t> hm(8 * n_trees);
         meta.download(hm.data(), hm.size());
         ssync();
         for (uint32_t t = 0; t < n_trees; ++t) {
-            if (hm[5 * t + 4]) throw Error(kInternal, "build_forest: traversal stack overflow");
+            if (hm[8 * t + 4]) throw Error(kInternal, "build_forest: traversal stack overflow");
             TreeDev& tr = f->trees[t];
-            tr.num_nodes = hm[5 * t + 0];
-            tr.root = hm[5 * t + 1];
-            tr.leaf_count = hm[5 * t + 2];
-            tr.max_depth = hm[5 * t + 3];
+            tr.num_nodes = hm[8 * t + 0];
+            tr.root = hm[8 * t + 1];
+            tr.leaf_count = hm[8 * t + 2];
+            tr.max_depth = hm[8 * t + 3];
+            if (getenv("ANNK_DEBUG_FOREST"))
+                fprintf(stderr, "tree %u: nodes %u, block-path %u kcycles, warp-path %u kcycles\n", t,
+                        tr.num_nodes, hm[8 * t + 5], hm[8 * t + 6]);
         }
         forest_upload_views(f.get());
         *out = f.release();
