@@ -34,17 +34,15 @@
 namespace annk {
 namespace {
 
-constexpr uint32_t kBlock = 512;
+constexpr uint32_t kBlock = 256;
 constexpr uint32_t kWarps = kBlock / 32;
 constexpr uint32_t kWarpSubtree = 4096;
-constexpr uint32_t kSortSmem = 4096;
+constexpr uint32_t kSortSmem = 2048;
+constexpr uint32_t kTileMax = 1024;      // staged-tile path: points per tile
+constexpr uint32_t kStageBytes = 147456;  // staged rows (u8 path), row stride ld8 + 4
 constexpr uint32_t kStack = 160;
 constexpr size_t kPrefetchBytes = 4u << 20;
 constexpr uint32_t kDrawWin = 256;
-#ifndef ANNK_PREFETCH_NEXT
-#define ANNK_PREFETCH_NEXT 0
-#endif
-constexpr bool kPrefetchNext = ANNK_PREFETCH_NEXT != 0;  // measured: no gain
 
 struct StackEntry {
     uint32_t start, end, depth, parent, side;  // side 0 = left child, 1 = right
@@ -68,10 +66,12 @@ struct BuildArgs {
 };
 
 struct Smem {
-    float vals[2][kWarpSubtree];  // warp path: left child's values on its split dim, by depth parity
+    float col[kWarpSubtree];      // warp path: the node's column on its split dim
     uint32_t sub[kWarpSubtree];   // warp path: subtree slice of point_index
     uint32_t sub2[kWarpSubtree];  // warp path: right half during a partition
     uint64_t sortk[kSortSmem];
+    uint16_t lidx[kTileMax];  // staged tile: local row index per slot
+    uint16_t ltmp[kTileMax];
     StackEntry bstack[kStack];
     StackEntry wstack[kStack];
     double red_sum[kWarps];
@@ -79,15 +79,18 @@ struct Smem {
     uint32_t cnt_l[kWarps], cnt_r[kWarps];
     uint32_t dwin[kDrawWin];
     uint32_t dwin_base, draw_idx, node_count, leaf_count, max_depth, error;
+    uint32_t t_start, t_size, t_sb;  // staged-tile request to the helper warps (t_size 0: done)
     long long cyc_block, cyc_warp;
-    long long ft[8], ft_last;
+    long long ft[16], ft_last;
     uint32_t bsp;
     // broadcast slots for the block path
     uint32_t b_d, b_nl, b_nr, b_mid, b_even;
     float b_split;
     double b_sum;
     int b_exact;
+    alignas(16) unsigned char stage[kStageBytes];  // staged tile rows
 };
+static_assert(sizeof(Smem) <= 232448, "forest shared memory exceeds 227 KB");
 
 __device__ __forceinline__ float ldx(const BuildArgs& a, uint32_t p, uint32_t d) {
     return __ldg(a.x + size_t(p) * a.ld + d);
@@ -166,7 +169,7 @@ __device__ uint32_t warp_draw(const BuildArgs& a, Smem& s) {
     do {                                                             \
         const long long _t = clock64();                              \
         if (lane_id() == 0) {                                        \
-            if ((m) > 0) s.ft[(m)] += _t - s.ft_last;                \
+            s.ft[(m)] += _t - s.ft_last;                              \
             s.ft_last = _t;                                          \
         }                                                            \
     } while (0)
@@ -200,16 +203,311 @@ __device__ __forceinline__ float ldv(const BuildArgs& a, uint32_t p, uint32_t d)
     return a.x8 ? float(__ldg(a.x8 + size_t(p) * a.ld8 + d)) : __ldg(a.x + size_t(p) * a.ld + d);
 }
 
+// Points per staged tile (0: staged tiles off — fp32 rows, or rows too wide).
+__device__ __forceinline__ uint32_t tile_capacity(const BuildArgs& a) {
+    if (!a.x8) return 0u;
+    const uint32_t t = min(kTileMax, kStageBytes / (a.ld8 + 4));
+    return t >= 64 ? t : 0u;
+}
+
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Copies the rows of s.sub[ts, ts+tsz) (u8, ld8 bytes each) into s.stage with
+// row stride sb.  Called by all kBlock threads (warp 0 + the helper warps).
+__device__ __forceinline__ void stage_rows(const BuildArgs& a, Smem& s, uint32_t ts, uint32_t tsz, uint32_t sb) {
+    const uint32_t parts = a.ld8 / 16;
+    const uint32_t total = tsz * parts;
+    for (uint32_t j0 = 0; j0 < total; j0 += kBlock * 8) {
+        uint4 r[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+            const uint32_t j = j0 + u * kBlock + threadIdx.x;
+            if (j < total) {
+                const uint32_t row = j / parts, part = j - row * parts;
+                r[u] = __ldg(reinterpret_cast<const uint4*>(a.x8 + size_t(s.sub[ts + row]) * a.ld8) + part);
+            }
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+            const uint32_t j = j0 + u * kBlock + threadIdx.x;
+            if (j < total) {
+                const uint32_t row = j / parts, part = j - row * parts;
+                uint32_t* dst = reinterpret_cast<uint32_t*>(s.stage + row * sb + part * 16);
+                dst[0] = r[u].x;
+                dst[1] = r[u].y;
+                dst[2] = r[u].z;
+                dst[3] = r[u].w;
+            }
+        }
+    }
+}
+
+// Helper warps (1..kWarps-1) while warp 0 builds a warp subtree: stage the
+// rows of each tile warp 0 requests (named barrier 1 = request, 2 = done).
+__device__ void stage_helper(const BuildArgs& a, Smem& s) {
+    for (;;) {
+        named_bar(1, kBlock);
+        const uint32_t ts = s.t_start, tsz = s.t_size;
+        if (tsz == 0) break;
+        stage_rows(a, s, ts, tsz, s.t_sb);
+        named_bar(2, kBlock);
+    }
+}
+
+// One tile node of <= 32*C points, all in registers: gather the column,
+// integer sum, ballot the sides, then either scatter both sides of li in place
+// (balanced split) or sort the rows by (value, global id) (kd_forest.cpp:70-83).
+// Returns the split position; writes split / even.
+template <int C>
+__device__ __forceinline__ uint32_t tile_node_reg(const unsigned char* __restrict__ st, uint16_t* li,
+                                                  const uint32_t* gid, uint32_t sb, uint32_t d,
+                                                  uint32_t start, uint32_t end, float& split, uint8_t& even) {
+    const uint32_t lane = lane_id(), ltm = (1u << lane) - 1u;
+    const uint32_t size = end - start;
+    uint32_t loc[C], v[C];
+#pragma unroll
+    for (int u = 0; u < C; ++u) {
+        const uint32_t p = start + u * 32 + lane;
+        loc[u] = p < end ? li[p] : 0u;
+    }
+    uint32_t is = 0;
+#pragma unroll
+    for (int u = 0; u < C; ++u) {
+        const uint32_t p = start + u * 32 + lane;
+        v[u] = p < end ? st[loc[u] * sb + d] : 0u;
+        is += v[u];
+    }
+    const uint32_t isum = __reduce_add_sync(0xffffffffu, is);
+    uint32_t bl[C], nl = 0;
+#pragma unroll
+    for (int u = 0; u < C; ++u) {
+        const uint32_t p = start + u * 32 + lane;
+        bl[u] = __ballot_sync(0xffffffffu, p < end && v[u] * size <= isum);
+        nl += __popc(bl[u]);
+    }
+    const uint32_t nr = size - nl;
+    if (nl != 0 && nr != 0 && max(nl, nr) <= 4u * min(nl, nr)) {
+        uint32_t cl = 0, cr = 0;
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            const uint32_t p = start + u * 32 + lane;
+            const uint32_t pl = __popc(bl[u] & ltm);
+            if (p < end) {
+                if ((bl[u] >> lane) & 1u) li[start + cl + pl] = uint16_t(loc[u]);
+                else li[start + nl + cr + (lane - pl)] = uint16_t(loc[u]);
+            }
+            const uint32_t c = __popc(bl[u]);
+            cl += c;
+            cr += min(32u, end - min(end, start + u * 32)) - c;
+        }
+        split = __fdiv_rn(float(isum), float(size));
+        even = 0;
+        __syncwarp();
+        return start + nl;
+    }
+    uint64_t k[C];
+#pragma unroll
+    for (int u = 0; u < C; ++u) {
+        const uint32_t p = start + u * 32 + lane;
+        k[u] = p < end ? (uint64_t(v[u]) << 53) | (uint64_t(gid[loc[u]]) << 11) | loc[u] : kEmptyKey;
+    }
+    warp_sort_regs<C>(k);
+#pragma unroll
+    for (int u = 0; u < C; ++u) {
+        const uint32_t p = start + u * 32 + lane;
+        if (p < end) li[p] = uint16_t(k[u] & 0x7ffu);
+    }
+    // values at sorted positions size/2 - 1 and size/2
+    const uint32_t q0 = size / 2 - 1, q1 = size / 2;
+    uint32_t a0 = 0, a1 = 0;
+#pragma unroll
+    for (int u = 0; u < C; ++u) {
+        const uint32_t x = __shfl_sync(0xffffffffu, uint32_t(k[u] >> 53), q0 & 31);
+        const uint32_t y = __shfl_sync(0xffffffffu, uint32_t(k[u] >> 53), q1 & 31);
+        if (q0 / 32 == uint32_t(u)) a0 = x;
+        if (q1 / 32 == uint32_t(u)) a1 = y;
+    }
+    split = midpoint_f(float(a0), float(a1));
+    even = 1;
+    __syncwarp();
+    return start + size / 2;
+}
+
+// Builds the whole subtree under `root` (<= tile_max points, u8 datapath)
+// from rows staged in shared memory by the whole CTA: every node's column
+// gather is then a shared-memory byte read and the partition moves 16-bit
+// local row indices; point_index is permuted once at the end.  Same
+// pre-order, draws and splits as the warp path.  For a node of `size` points
+// with integer sum `isum` (size <= 1024): split = fl32(fl64(isum/size)) ==
+// __fdiv_rn(isum, size) (isum, size < 2^24 exact in float, and no double
+// rounding since size < 2^28), and for an integer value v,
+// v <= split  <=>  v*size <= isum  (the quotient is >= 1/size away from any
+// integer it does not equal, far more than half a float ulp below 256).
+// `sb` = row stride in bytes (odd word count: consecutive rows in different
+// banks).  Node/draw/leaf counters live in registers for the whole tile.
+__device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& root, uint32_t base,
+                                uint32_t sp0, uint32_t sb) {
+    const uint32_t lane = lane_id();
+    const uint32_t ts = root.start, tsz = root.end - root.start;
+    FT_MARK(0);
+    if (lane == 0) {
+        s.t_start = ts;
+        s.t_size = tsz;
+        s.t_sb = sb;
+    }
+    __syncwarp();
+    named_bar(1, kBlock);
+    stage_rows(a, s, ts, tsz, sb);
+    for (uint32_t j = lane; j < tsz; j += 32) s.lidx[j] = uint16_t(j);
+    named_bar(2, kBlock);
+    FT_MARK(13);
+    const unsigned char* st = s.stage;
+    uint16_t* li = s.lidx - ts;  // indexed by subtree-local slot
+    uint16_t* lt = s.ltmp;
+    const uint32_t ltm = (1u << lane) - 1u;
+    uint32_t nid = s.node_count, kd = s.draw_idx, wb = s.dwin_base, nleaf = s.leaf_count, maxd = s.max_depth;
+    uint32_t wsp = sp0 + 1;
+    if (lane == 0) s.wstack[sp0] = root;
+    __syncwarp();
+    while (wsp > sp0) {
+        --wsp;
+        const StackEntry e = s.wstack[wsp];
+        const uint32_t size = e.end - e.start;
+        const uint32_t id = nid++;
+        maxd = max(maxd, e.depth);
+        if (lane == 0) {
+            if (e.side == 0) a.nodes[e.parent].left = id;
+            else a.nodes[e.parent].right = id;
+            a.depth[id] = e.depth;
+        }
+        if (size <= a.leaf_cap) {
+            if (lane == 0) {
+                a.nodes[id] = KdNodeDev{kLeaf, 0.0f, base + e.start, base + e.end};
+                a.even[id] = 0;
+            }
+            ++nleaf;
+            __syncwarp();
+            FT_MARK(15);
+            continue;
+        }
+        FT_MARK(0);
+        if (kd - wb >= kDrawWin) {  // refill the draw window (uniform)
+            wb = kd & ~(kDrawWin - 1);
+            __syncwarp();
+            for (uint32_t j = lane; j < kDrawWin; j += 32) s.dwin[j] = wb + j < a.n_draws ? a.draws[wb + j] : 0u;
+            __syncwarp();
+        }
+        const uint32_t d = s.dwin[kd - wb];
+        ++kd;
+        FT_MARK(8);
+        float split;
+        uint8_t even;
+        uint32_t mid;
+        const uint32_t* gid = s.sub + ts;
+        if (size <= 32) {
+            mid = tile_node_reg<1>(st, li, gid, sb, d, e.start, e.end, split, even);
+        } else if (size <= 64) {
+            mid = tile_node_reg<2>(st, li, gid, sb, d, e.start, e.end, split, even);
+        } else if (size <= 128) {
+            mid = tile_node_reg<4>(st, li, gid, sb, d, e.start, e.end, split, even);
+        } else if (size <= 256) {
+            mid = tile_node_reg<8>(st, li, gid, sb, d, e.start, e.end, split, even);
+        } else {
+            // ---- shared-memory path (257..tile points): two passes
+            uint32_t is = 0;
+            for (uint32_t p0 = e.start; p0 < e.end; p0 += 256) {
+                uint32_t x[8];
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) {
+                    const uint32_t p = p0 + u * 32 + lane;
+                    x[u] = p < e.end ? st[uint32_t(li[p]) * sb + d] : 0u;
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) is += x[u];
+            }
+            const uint32_t isum = __reduce_add_sync(0xffffffffu, is);
+            uint32_t nl = 0, nr = 0;
+            for (uint32_t b0 = e.start; b0 < e.end; b0 += 32) {
+                const uint32_t p = b0 + lane;
+                const bool valid = p < e.end;
+                const uint16_t lc = valid ? li[p] : uint16_t(0);
+                const bool left = valid && uint32_t(st[uint32_t(lc) * sb + d]) * size <= isum;
+                const uint32_t bl = __ballot_sync(0xffffffffu, left);
+                const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
+                if (left) li[e.start + nl + __popc(bl & ltm)] = lc;
+                else if (valid) lt[nr + __popc(br & ltm)] = lc;
+                nl += __popc(bl);
+                nr += __popc(br);
+            }
+            __syncwarp();
+            for (uint32_t j = lane; j < nr; j += 32) li[e.start + nl + j] = lt[j];
+            __syncwarp();
+            split = __fdiv_rn(float(isum), float(size));
+            mid = e.start + nl;
+            even = 0;
+            if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
+                // kd_forest.cpp:70-83: sort by (value, id); key = value | global id | local row
+                const uint32_t m = next_pow2(size);
+                uint64_t* k = s.sortk;
+                for (uint32_t j = lane; j < m; j += 32) {
+                    uint64_t key = kEmptyKey;
+                    if (j < size) {
+                        const uint32_t lc = li[e.start + j];
+                        key = (uint64_t(st[lc * sb + d]) << 53) | (uint64_t(gid[lc]) << 11) | lc;
+                    }
+                    k[j] = key;
+                }
+                __syncwarp();
+                warp_bitonic_sort(k, m);
+                for (uint32_t j = lane; j < size; j += 32) li[e.start + j] = uint16_t(k[j] & 0x7ffu);
+                __syncwarp();
+                mid = e.start + size / 2;
+                split = midpoint_f(float(st[uint32_t(li[mid - 1]) * sb + d]), float(st[uint32_t(li[mid]) * sb + d]));
+                even = 1;
+            }
+        }
+        FT_MARK(10);
+        if (lane == 0) {
+            a.nodes[id] = KdNodeDev{d, split, 0u, 0u};
+            a.even[id] = even;
+            s.wstack[wsp] = StackEntry{mid, e.end, e.depth + 1, id, 1u};
+            s.wstack[wsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, 0u};
+        }
+        if (wsp + 2 > kStack - 2) s.error = 1;
+        wsp = min(wsp + 2, kStack - 2);
+        __syncwarp();
+        FT_MARK(12);
+    }
+    if (lane == 0) {
+        s.node_count = nid;
+        s.draw_idx = kd;
+        s.dwin_base = wb;
+        s.leaf_count = nleaf;
+        s.max_depth = maxd;
+    }
+    // point_index of the tile in leaf order
+    for (uint32_t j = lane; j < tsz; j += 32) s.sub2[j] = s.sub[ts + s.lidx[j]];
+    __syncwarp();
+    for (uint32_t j = lane; j < tsz; j += 32) s.sub[ts + j] = s.sub2[j];
+    __syncwarp();
+    FT_MARK(14);
+}
+
 // Builds the subtree rooted at `root` (<= kWarpSubtree points) with warp 0,
 // in pre-order (the root's id is assigned here).  The subtree's slice of
-// point_index lives in shared memory; each node gathers its column once (into
-// registers for nodes of <= 256 points), sums it exactly, and partitions by
+// point_index lives in shared memory.  Nodes of <= 256 points gather their
+// column into registers (8 independent loads per lane); larger nodes gather
+// it into shared memory (s.col) in batches of 8 loads per lane, so neither
+// pass waits on one L2 round trip per chunk.  Sum exactly, partition by
 // ballots in shared memory.
 __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root) {
     const uint32_t lane = lane_id();
     const uint32_t base = root.start, total = root.end - root.start;
     uint32_t* sub = s.sub;
     uint32_t* rtmp = s.sub2;
+    float* col = s.col;
     for (uint32_t j = lane; j < total; j += 32) sub[j] = a.pidx[base + j];
     __syncwarp();
     // stage the subtree's rows in L2: every node below gathers from them
@@ -223,21 +521,28 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
         }
     }
-    // side bit 0: right child; bit 1: this node's split-dim values are staged in
-    // vals[depth & 1] (gathered by the parent, whose next draw is ours)
     uint32_t wsp = 1;
-    if (lane == 0) s.wstack[0] = StackEntry{0, total, root.depth, root.parent, root.side & 1u};
+    if (lane == 0) s.wstack[0] = StackEntry{0, total, root.depth, root.parent, root.side};
     __syncwarp();
+    const uint32_t lt = (1u << lane) - 1u;
+    // staged-tile path (u8 rows fit shared memory)
+    const uint32_t sb = a.ld8 + 4;
+    const uint32_t tile_max = tile_capacity(a);
     while (wsp > 0) {
         --wsp;
         const StackEntry e = s.wstack[wsp];
         const uint32_t size = e.end - e.start;
+        if (size <= tile_max && size > a.leaf_cap && size >= 64 && e.parent != kInvalidId) {
+            __syncwarp();
+            warp_build_tile(a, s, e, base, wsp, sb);
+            continue;
+        }
         const uint32_t id = s.node_count;
         __syncwarp();
         if (lane == 0) {
             s.node_count = id + 1;
             if (e.parent != kInvalidId) {
-                if ((e.side & 1u) == 0) a.nodes[e.parent].left = id;
+                if (e.side == 0) a.nodes[e.parent].left = id;
                 else a.nodes[e.parent].right = id;
             }
             a.depth[id] = e.depth;
@@ -253,34 +558,24 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
             continue;
         }
         FT_MARK(0);
-        const uint32_t k = s.draw_idx;
         const uint32_t d = warp_draw(a, s);
-        // the left child, if internal, is the next internal node in pre-order: draw k+1
-        const bool want_next = kPrefetchNext && size > a.leaf_cap + 1;
-        const uint32_t dn = want_next ? warp_draw_at(a, s, k + 1) : 0u;
         FT_MARK(1);
-        const bool staged = (e.side & 2u) != 0;
-        const float* vin = s.vals[e.depth & 1u];
-        float* vout = s.vals[(e.depth + 1) & 1u];
         const uint32_t chunks = (size + 31) / 32;
         float split;
         uint32_t nl = 0, nr = 0;
         if (chunks <= 8) {
-            // ---- register path: at most one gather round for this node and its left child
-            float v[8], w[8];
+            // ---- register path: one gather round
+            float v[8];
             uint32_t pid[8];
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
                 const uint32_t j = e.start + u * 32 + lane;
-                const bool ok = u < chunks && j < e.end;
-                pid[u] = ok ? sub[j] : 0;
+                pid[u] = (u < chunks && j < e.end) ? sub[j] : 0;
             }
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
                 const uint32_t j = e.start + u * 32 + lane;
-                const bool ok = u < chunks && j < e.end;
-                v[u] = ok ? (staged ? vin[j] : ldv(a, pid[u], d)) : 0.0f;
-                w[u] = (ok && want_next) ? ldv(a, pid[u], dn) : 0.0f;
+                v[u] = (u < chunks && j < e.end) ? ldv(a, pid[u], d) : 0.0f;
             }
             FT_MARK(2);
             double sum;
@@ -311,7 +606,6 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
             }
             split = __double2float_rn(__ddiv_rn(sum, double(size)));
             FT_MARK(3);
-            const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
                 if (u >= chunks) break;
@@ -320,29 +614,35 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
                 const bool left = valid && v[u] <= split;
                 const uint32_t bl = __ballot_sync(0xffffffffu, left);
                 const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
-                if (left) {
-                    const uint32_t pos = e.start + nl + __popc(bl & lt);
-                    sub[pos] = pid[u];
-                    vout[pos] = w[u];
-                } else if (valid) {
-                    rtmp[nr + __popc(br & lt)] = pid[u];
-                }
+                if (left) sub[e.start + nl + __popc(bl & lt)] = pid[u];
+                else if (valid) rtmp[nr + __popc(br & lt)] = pid[u];
                 nl += __popc(bl);
                 nr += __popc(br);
             }
         } else {
-            // ---- streaming path (subtree roots > 256 points): two passes
+            // ---- shared-memory path (257..4096 points): gather the column once
             double sum = 0.0;
             int top = INT_MIN, lsb = INT_MAX;
             uint32_t is = 0;
-            for (uint32_t p = e.start + lane; p < e.end; p += 32) {
-                const float x = staged ? vin[p] : ldv(a, sub[p], d);
-                if (a.x8) is += uint32_t(x);
-                else {
-                    sum += double(x);
-                    val_stats(x, top, lsb);
+            for (uint32_t p0 = e.start; p0 < e.end; p0 += 256) {
+                float x[8];
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) {
+                    const uint32_t p = p0 + u * 32 + lane;
+                    x[u] = p < e.end ? ldv(a, sub[p], d) : 0.0f;
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) {
+                    const uint32_t p = p0 + u * 32 + lane;
+                    if (p < e.end) col[p] = x[u];
+                    if (a.x8) is += uint32_t(x[u]);
+                    else {
+                        sum += double(x[u]);
+                        val_stats(x[u], top, lsb);
+                    }
                 }
             }
+            FT_MARK(2);
             if (a.x8) {
                 sum = double(__reduce_add_sync(0xffffffffu, is));
             } else {
@@ -352,30 +652,25 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
                     lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
                 }
                 if (!sum_is_exact(top, lsb, size)) {
+                    __syncwarp();
                     double ser = 0.0;
                     if (lane == 0)
-                        for (uint32_t p = e.start; p < e.end; ++p) ser += double(ldv(a, sub[p], d));
+                        for (uint32_t p = e.start; p < e.end; ++p) ser += double(col[p]);
                     sum = __shfl_sync(0xffffffffu, ser, 0);
                 }
             }
             split = __double2float_rn(__ddiv_rn(sum, double(size)));
-            const uint32_t lt = (1u << lane) - 1u;
+            __syncwarp();
+            FT_MARK(3);
             for (uint32_t b0 = e.start; b0 < e.end; b0 += 32) {
                 const uint32_t p = b0 + lane;
                 const bool valid = p < e.end;
                 const uint32_t pid = valid ? sub[p] : 0;
-                const float x = valid ? (staged ? vin[p] : ldv(a, pid, d)) : 0.0f;
-                const float wn = (valid && want_next) ? ldv(a, pid, dn) : 0.0f;
-                const bool left = valid && x <= split;
+                const bool left = valid && col[p] <= split;
                 const uint32_t bl = __ballot_sync(0xffffffffu, left);
                 const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
-                if (left) {
-                    const uint32_t pos = e.start + nl + __popc(bl & lt);
-                    sub[pos] = pid;
-                    vout[pos] = wn;
-                } else if (valid) {
-                    rtmp[nr + __popc(br & lt)] = pid;
-                }
+                if (left) sub[e.start + nl + __popc(bl & lt)] = pid;
+                else if (valid) rtmp[nr + __popc(br & lt)] = pid;
                 nl += __popc(bl);
                 nr += __popc(br);
             }
@@ -397,9 +692,8 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
         if (lane == 0) {
             a.nodes[id] = KdNodeDev{d, split, 0u, 0u};
             a.even[id] = even;
-            const uint32_t left_staged = (want_next && !even) ? 2u : 0u;
             s.wstack[wsp] = StackEntry{mid, e.end, e.depth + 1, id, 1u};
-            s.wstack[wsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, left_staged};
+            s.wstack[wsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, 0u};
             if (wsp + 2 > kStack - 2) s.error = 1;
         }
         wsp = min(wsp + 2, kStack - 2);
@@ -407,6 +701,11 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
         FT_MARK(6);
     }
     for (uint32_t j = lane; j < total; j += 32) a.pidx[base + j] = sub[j];
+    if (tile_max) {  // release the helper warps
+        if (lane == 0) s.t_size = 0;
+        __syncwarp();
+        named_bar(1, kBlock);
+    }
     __syncwarp();
 }
 
@@ -465,7 +764,21 @@ __device__ void block_sort_node(const BuildArgs& a, Smem& s, uint32_t start, uin
     __syncthreads();
 }
 
+// Column value of point p on dim d: u8 copy when present (exact), else fp32.
+template <bool U8>
+__device__ __forceinline__ float colv(const BuildArgs& a, uint32_t p, uint32_t d) {
+    if constexpr (U8) return float(__ldg(a.x8 + size_t(p) * a.ld8 + d));
+    else return __ldg(a.x + size_t(p) * a.ld + d);
+}
+
+// One node of > kWarpSubtree points with the whole CTA.  Pass 1 gathers the
+// column with 8 loads in flight per thread and sums it (u8: integer sum, exact;
+// fp32: double sum + exactness test, serial fallback).  Pass 2 is a stable
+// partition over chunks of kBlock*8 points, 8 consecutive points per thread,
+// with one block-wide scan of packed (left, right) counts per chunk.
+template <bool U8>
 __device__ void block_split_node(const BuildArgs& a, Smem& s, const StackEntry& e, uint32_t id) {
+    constexpr uint32_t kPer = 8, kChunk = kBlock * kPer;
     const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid / 32;
     const uint32_t size = e.end - e.start;
     if (warp == 0) {
@@ -476,56 +789,94 @@ __device__ void block_split_node(const BuildArgs& a, Smem& s, const StackEntry& 
     const uint32_t d = s.b_d;
     double sum = 0.0;
     int top = INT_MIN, lsb = INT_MAX;
-    for (uint32_t p = e.start + tid; p < e.end; p += 4 * kBlock) {
-        float v[4];
+    uint64_t isum = 0;
+    for (uint32_t p0 = e.start; p0 < e.end; p0 += kChunk) {
+        uint32_t pid[kPer];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t q = p + u * kBlock;
-            v[u] = q < e.end ? ldx(a, a.pidx[q], d) : 0.0f;
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t q = p0 + u * kBlock + tid;
+            pid[u] = q < e.end ? a.pidx[q] : 0u;
+        }
+        float v[kPer];
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t q = p0 + u * kBlock + tid;
+            v[u] = q < e.end ? colv<U8>(a, pid[u], d) : 0.0f;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            sum += double(v[u]);
-            val_stats(v[u], top, lsb);
+        for (uint32_t u = 0; u < kPer; ++u) {
+            if constexpr (U8) {
+                isum += uint32_t(v[u]);
+            } else {
+                sum += double(v[u]);
+                val_stats(v[u], top, lsb);
+            }
         }
     }
-    block_reduce_stats(s, sum, top, lsb);
-    if (!sum_is_exact(top, lsb, size)) {
+    if constexpr (U8) {
+        for (int o = 16; o > 0; o >>= 1) isum += __shfl_xor_sync(0xffffffffu, isum, o);
+        if (lane == 0) s.red_sum[warp] = double(isum);  // < 2^53: exact
+        __syncthreads();
         if (tid == 0) {
-            sum = 0.0;
-            for (uint32_t p = e.start; p < e.end; ++p) sum += double(ldx(a, a.pidx[p], d));
-            s.b_sum = sum;
+            double t = 0.0;
+            for (uint32_t w = 0; w < kWarps; ++w) t += s.red_sum[w];
+            s.b_sum = t;
         }
         __syncthreads();
         sum = s.b_sum;
+    } else {
+        block_reduce_stats(s, sum, top, lsb);
+        if (!sum_is_exact(top, lsb, size)) {
+            if (tid == 0) {
+                sum = 0.0;
+                for (uint32_t p = e.start; p < e.end; ++p) sum += double(ldx(a, a.pidx[p], d));
+                s.b_sum = sum;
+            }
+            __syncthreads();
+            sum = s.b_sum;
+        }
     }
     float split = __double2float_rn(__ddiv_rn(sum, double(size)));
-    // block-wide stable partition
     uint32_t nl = 0, nr = 0;
-    for (uint32_t base = e.start; base < e.end; base += kBlock) {
-        const uint32_t p = base + tid;
-        const bool valid = p < e.end;
-        const uint32_t pid = valid ? a.pidx[p] : 0;
-        const bool left = valid && ldx(a, pid, d) <= split;
-        const uint32_t bl = __ballot_sync(0xffffffffu, left);
-        const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
-        if (lane == 0) {
-            s.cnt_l[warp] = __popc(bl);
-            s.cnt_r[warp] = __popc(br);
+    for (uint32_t b0 = e.start; b0 < e.end; b0 += kChunk) {
+        const uint32_t q0 = b0 + tid * kPer;
+        uint32_t pid[kPer];
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) pid[i] = q0 + i < e.end ? a.pidx[q0 + i] : 0u;
+        uint32_t lm = 0, vm = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) {
+            if (q0 + i < e.end) {
+                vm |= 1u << i;
+                if (colv<U8>(a, pid[i], d) <= split) lm |= 1u << i;
+            }
         }
+        // block exclusive scan of (lefts | rights << 16)
+        const uint32_t x = __popc(lm) | (__popc(vm & ~lm) << 16);
+        uint32_t incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += y;
+        }
+        if (lane == 31) s.cnt_l[warp] = incl;
         __syncthreads();
-        uint32_t pl = 0, pr = 0, tl = 0, tr = 0;
+        uint32_t wp = 0, tot = 0;
+#pragma unroll
         for (uint32_t w = 0; w < kWarps; ++w) {
-            const uint32_t cl = s.cnt_l[w], cr = s.cnt_r[w];
-            if (w < warp) { pl += cl; pr += cr; }
-            tl += cl;
-            tr += cr;
+            const uint32_t c = s.cnt_l[w];
+            wp += w < warp ? c : 0u;
+            tot += c;
         }
-        const uint32_t lt = (1u << lane) - 1u;
-        if (left) a.pidx[e.start + nl + pl + __popc(bl & lt)] = pid;
-        else if (valid) a.rtmp[e.start + nr + pr + __popc(br & lt)] = pid;
-        nl += tl;
-        nr += tr;
+        const uint32_t ex = wp + incl - x;
+        uint32_t ol = e.start + nl + (ex & 0xffffu), orr = e.start + nr + (ex >> 16);
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) {
+            if ((lm >> i) & 1u) a.pidx[ol++] = pid[i];
+            else if ((vm >> i) & 1u) a.rtmp[orr++] = pid[i];
+        }
+        nl += tot & 0xffffu;
+        nr += tot >> 16;
         __syncthreads();
     }
     for (uint32_t j = tid; j < nr; j += kBlock) a.pidx[e.start + nl + j] = a.rtmp[e.start + j];
@@ -564,7 +915,7 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
         s.error = 0;
         s.cyc_block = 0;
         s.cyc_warp = 0;
-        for (int q = 0; q < 8; ++q) s.ft[q] = 0;
+        for (int q = 0; q < 16; ++q) s.ft[q] = 0;
         s.bstack[0] = StackEntry{0, a.n, 0, kInvalidId, 0};
         s.bsp = 1;
     }
@@ -578,6 +929,7 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
             __syncthreads();
             const long long c0 = clock64();
             if (tid < 32) warp_build_subtree(a, s, e);
+            else if (tile_capacity(a)) stage_helper(a, s);
             if (tid == 0) s.cyc_warp += clock64() - c0;
             __syncthreads();
             continue;
@@ -596,7 +948,8 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
         }
         __syncthreads();
         const long long c1 = clock64();
-        block_split_node(a, s, e, id);
+        if (a.x8) block_split_node<true>(a, s, e, id);
+        else block_split_node<false>(a, s, e, id);
         if (tid == 0) s.cyc_block += clock64() - c1;
     }
     __syncthreads();
@@ -611,6 +964,9 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
 #ifdef ANNK_FOREST_TIMING
         printf("tree %u phases (Mcycles): draw %.1f gather %.1f sum %.1f part %.1f copy %.1f tail %.1f\n",
                blockIdx.x, s.ft[1] / 1e6, s.ft[2] / 1e6, s.ft[3] / 1e6, s.ft[4] / 1e6, s.ft[5] / 1e6, s.ft[6] / 1e6);
+        printf("tree %u tile (Mcycles): gap %.1f leaf %.1f stage %.1f draw %.1f sum %.1f part %.1f copy %.1f tail %.1f perm %.1f\n",
+               blockIdx.x, s.ft[0] / 1e6, s.ft[15] / 1e6, s.ft[13] / 1e6, s.ft[8] / 1e6, s.ft[9] / 1e6, s.ft[10] / 1e6, s.ft[11] / 1e6,
+               s.ft[12] / 1e6, s.ft[14] / 1e6);
 #endif
     }
 }

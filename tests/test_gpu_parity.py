@@ -98,6 +98,23 @@ def test_forest_integer_mixture_with_duplicates():
     assert evens > 0
 
 
+@pytest.mark.parametrize("n,dim,trees,leaf,dups", [
+    (12000, 960, 2, 8, 0),    # wide rows: staged tiles of 152 points
+    (5000, 2500, 1, 8, 0),    # rows too wide to stage: warp path gathers
+    (20000, 64, 2, 100, 0),   # leaf_cap above the tile floor
+    (24000, 32, 2, 8, 9000),  # duplicate block > kWarpSubtree: block-path even split
+])
+def test_forest_integer_mixture_shapes(n, dim, trees, leaf, dups):
+    o = ora()
+    x = mixture(n, dim, 30, 6)
+    if dups:
+        x[:dups] = x[1]
+    fo = o.build_forest(o.vs(x), trees, leaf, 21)
+    fd = A.build_forest(x, trees, leaf, 21)
+    for t in range(trees):
+        assert_trees_equal(fd.tree(t), fo.tree(t))
+
+
 def test_forest_float_mixture_inexact_sums():
     # [0,1] clipped Gaussian floats (cfg3-like) exercise the serial-sum fallback
     o = ora()

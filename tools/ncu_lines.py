@@ -1,0 +1,35 @@
+"""Aggregate ncu per-SASS warp-stall samples by CUDA source line.
+
+usage: ncu_lines.py <sass.csv from `ncu -i X --page source --csv --print-source sass`>
+                    <nvdisasm --print-line-info listing of the same kernel> [top]
+"""
+import csv
+import re
+import sys
+from collections import defaultdict
+
+rows = list(csv.reader(open(sys.argv[1])))
+hdr, data = rows[1], rows[2:]
+base = int(data[0][0], 16)
+line_of = {}
+cur = None
+for l in open(sys.argv[2]):
+    m = re.search(r'line (\d+)', l)
+    if m and '//##' in l:
+        cur = int(m.group(1))
+        continue
+    m = re.search(r'/\*([0-9a-f]{4,})\*/', l)
+    if m and cur is not None:
+        line_of[int(m.group(1), 16)] = cur
+col = hdr.index('Warp Stall Sampling (All Samples)')
+ex = hdr.index('Instructions Executed')
+agg = defaultdict(lambda: [0, 0])
+for r in data:
+    off = int(r[0], 16) - base
+    ln = line_of.get(off, -1)
+    agg[ln][0] += int(r[col] or 0)
+    agg[ln][1] += int(r[ex] or 0)
+tot = sum(v[0] for v in agg.values())
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+for ln, (smp, n) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    print(f"line {ln:5d}  samples {smp:8d} ({100 * smp / tot:5.1f}%)  inst {n}")
