@@ -245,6 +245,12 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, uint32_t m) {
     return (uint64_t(hi) << 32) | lo;
 }
 
+__device__ __forceinline__ uint64_t shfl_idx_u64(uint64_t v, uint32_t src) {
+    const uint32_t lo = __shfl_sync(0xffffffffu, uint32_t(v), src);
+    const uint32_t hi = __shfl_sync(0xffffffffu, uint32_t(v >> 32), src);
+    return (uint64_t(hi) << 32) | lo;
+}
+
 // Register-resident ascending bitonic sort of 32*V keys held V per lane in
 // element order e = r*32 + lane (no shared memory; cross-lane steps shuffle).
 template <int V>

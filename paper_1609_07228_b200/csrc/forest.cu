@@ -41,6 +41,7 @@ constexpr uint32_t kSortSmem = 2048;
 constexpr uint32_t kTileMax = 1024;      // staged-tile path: points per tile
 constexpr uint32_t kStageBytes = 147456;  // staged rows (u8 path), row stride ld8 + 4
 constexpr uint32_t kStack = 160;
+constexpr uint32_t kTileStack = 128;
 constexpr size_t kPrefetchBytes = 4u << 20;
 constexpr uint32_t kDrawWin = 256;
 
@@ -74,6 +75,7 @@ struct Smem {
     uint16_t ltmp[kTileMax];
     StackEntry bstack[kStack];
     StackEntry wstack[kStack];
+    uint64_t tstack[kTileStack];
     double red_sum[kWarps];
     int red_top[kWarps], red_lsb[kWarps];
     uint32_t cnt_l[kWarps], cnt_r[kWarps];
@@ -313,21 +315,49 @@ __device__ __forceinline__ uint32_t tile_node_reg(const unsigned char* __restric
         const uint32_t p = start + u * 32 + lane;
         k[u] = p < end ? (uint64_t(v[u]) << 53) | (uint64_t(gid[loc[u]]) << 11) | loc[u] : kEmptyKey;
     }
-    warp_sort_regs<C>(k);
-#pragma unroll
-    for (int u = 0; u < C; ++u) {
-        const uint32_t p = start + u * 32 + lane;
-        if (p < end) li[p] = uint16_t(k[u] & 0x7ffu);
-    }
-    // values at sorted positions size/2 - 1 and size/2
     const uint32_t q0 = size / 2 - 1, q1 = size / 2;
     uint32_t a0 = 0, a1 = 0;
+    if constexpr (C <= 2) {
+        // rank sort: keys are unique, rank = number of smaller keys (independent
+        // broadcasts instead of a dependent bitonic network)
+        uint32_t rk[C];
 #pragma unroll
-    for (int u = 0; u < C; ++u) {
-        const uint32_t x = __shfl_sync(0xffffffffu, uint32_t(k[u] >> 53), q0 & 31);
-        const uint32_t y = __shfl_sync(0xffffffffu, uint32_t(k[u] >> 53), q1 & 31);
-        if (q0 / 32 == uint32_t(u)) a0 = x;
-        if (q1 / 32 == uint32_t(u)) a1 = y;
+        for (int u = 0; u < C; ++u) rk[u] = 0;
+#pragma unroll
+        for (int r = 0; r < C; ++r) {
+            const uint32_t cnt = min(32u, size - min(size, uint32_t(r) * 32));
+            for (uint32_t j = 0; j < cnt; ++j) {
+                const uint64_t kj = shfl_idx_u64(k[r], j);
+#pragma unroll
+                for (int u = 0; u < C; ++u) rk[u] += kj < k[u] ? 1u : 0u;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            const uint32_t p = start + u * 32 + lane;
+            if (p < end) li[start + rk[u]] = uint16_t(loc[u]);
+            const uint32_t b0 = __ballot_sync(0xffffffffu, p < end && rk[u] == q0);
+            const uint32_t b1 = __ballot_sync(0xffffffffu, p < end && rk[u] == q1);
+            const uint32_t x = __shfl_sync(0xffffffffu, v[u], (__ffs(b0) - 1) & 31);
+            const uint32_t y = __shfl_sync(0xffffffffu, v[u], (__ffs(b1) - 1) & 31);
+            if (b0) a0 = x;
+            if (b1) a1 = y;
+        }
+    } else {
+        warp_sort_regs<C>(k);
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            const uint32_t p = start + u * 32 + lane;
+            if (p < end) li[p] = uint16_t(k[u] & 0x7ffu);
+        }
+        // values at sorted positions size/2 - 1 and size/2
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            const uint32_t x = __shfl_sync(0xffffffffu, uint32_t(k[u] >> 53), q0 & 31);
+            const uint32_t y = __shfl_sync(0xffffffffu, uint32_t(k[u] >> 53), q1 & 31);
+            if (q0 / 32 == uint32_t(u)) a0 = x;
+            if (q1 / 32 == uint32_t(u)) a1 = y;
+        }
     }
     split = midpoint_f(float(a0), float(a1));
     even = 1;
@@ -347,8 +377,15 @@ __device__ __forceinline__ uint32_t tile_node_reg(const unsigned char* __restric
 // integer it does not equal, far more than half a float ulp below 256).
 // `sb` = row stride in bytes (odd word count: consecutive rows in different
 // banks).  Node/draw/leaf counters live in registers for the whole tile.
+// Tile stack entry packed in 64 bits: parent id | start(11) | end(11) |
+// depth below the tile root(8) | link(2: bit0 = set the parent's child link,
+// bit1 = right child).  start/end are relative to the tile.
+__device__ __forceinline__ uint64_t tpack(uint32_t parent, uint32_t st, uint32_t en, uint32_t dep, uint32_t link) {
+    return (uint64_t(parent) << 32) | (st << 21) | (en << 10) | (dep << 2) | link;
+}
+
 __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& root, uint32_t base,
-                                uint32_t sp0, uint32_t sb) {
+                                uint32_t sb) {
     const uint32_t lane = lane_id();
     const uint32_t ts = root.start, tsz = root.end - root.start;
     FT_MARK(0);
@@ -364,32 +401,36 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
     named_bar(2, kBlock);
     FT_MARK(13);
     const unsigned char* st = s.stage;
-    uint16_t* li = s.lidx - ts;  // indexed by subtree-local slot
+    uint16_t* li = s.lidx;  // indexed by tile-relative slot
     uint16_t* lt = s.ltmp;
+    const uint32_t* gid = s.sub + ts;
     const uint32_t ltm = (1u << lane) - 1u;
+    const uint32_t lcap = a.leaf_cap, pbase = base + ts, dep0 = root.depth;
     uint32_t nid = s.node_count, kd = s.draw_idx, wb = s.dwin_base, nleaf = s.leaf_count, maxd = s.max_depth;
-    uint32_t wsp = sp0 + 1;
-    if (lane == 0) s.wstack[sp0] = root;
+    uint32_t wsp = 1;
+    if (lane == 0) s.tstack[0] = tpack(root.parent, 0, tsz, 0, 1u | (root.side ? 2u : 0u));
     __syncwarp();
-    while (wsp > sp0) {
+    while (wsp > 0) {
         --wsp;
-        const StackEntry e = s.wstack[wsp];
-        const uint32_t size = e.end - e.start;
+        const uint64_t pe = s.tstack[wsp];
+        const uint32_t parent = uint32_t(pe >> 32), lo = uint32_t(pe);
+        const uint32_t e_start = (lo >> 21) & 0x7ffu, e_end = (lo >> 10) & 0x7ffu;
+        const uint32_t dep = dep0 + ((lo >> 2) & 0xffu), link = lo & 3u;
+        const uint32_t size = e_end - e_start;
         const uint32_t id = nid++;
-        maxd = max(maxd, e.depth);
-        if (lane == 0) {
-            if (e.side == 0) a.nodes[e.parent].left = id;
-            else a.nodes[e.parent].right = id;
-            a.depth[id] = e.depth;
+        maxd = max(maxd, dep);
+        if (lane == 0 && (link & 1u)) {
+            if (link & 2u) a.nodes[parent].right = id;
+            else a.nodes[parent].left = id;
         }
-        if (size <= a.leaf_cap) {
+        if (size <= lcap) {  // a right child whose left sibling was internal
             if (lane == 0) {
-                a.nodes[id] = KdNodeDev{kLeaf, 0.0f, base + e.start, base + e.end};
+                a.nodes[id] = KdNodeDev{kLeaf, 0.0f, pbase + e_start, pbase + e_end};
+                a.depth[id] = dep;
                 a.even[id] = 0;
             }
             ++nleaf;
             __syncwarp();
-            FT_MARK(15);
             continue;
         }
         FT_MARK(0);
@@ -405,47 +446,46 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
         float split;
         uint8_t even;
         uint32_t mid;
-        const uint32_t* gid = s.sub + ts;
         if (size <= 32) {
-            mid = tile_node_reg<1>(st, li, gid, sb, d, e.start, e.end, split, even);
+            mid = tile_node_reg<1>(st, li, gid, sb, d, e_start, e_end, split, even);
         } else if (size <= 64) {
-            mid = tile_node_reg<2>(st, li, gid, sb, d, e.start, e.end, split, even);
+            mid = tile_node_reg<2>(st, li, gid, sb, d, e_start, e_end, split, even);
         } else if (size <= 128) {
-            mid = tile_node_reg<4>(st, li, gid, sb, d, e.start, e.end, split, even);
+            mid = tile_node_reg<4>(st, li, gid, sb, d, e_start, e_end, split, even);
         } else if (size <= 256) {
-            mid = tile_node_reg<8>(st, li, gid, sb, d, e.start, e.end, split, even);
+            mid = tile_node_reg<8>(st, li, gid, sb, d, e_start, e_end, split, even);
         } else {
             // ---- shared-memory path (257..tile points): two passes
             uint32_t is = 0;
-            for (uint32_t p0 = e.start; p0 < e.end; p0 += 256) {
+            for (uint32_t p0 = e_start; p0 < e_end; p0 += 256) {
                 uint32_t x[8];
 #pragma unroll
                 for (uint32_t u = 0; u < 8; ++u) {
                     const uint32_t p = p0 + u * 32 + lane;
-                    x[u] = p < e.end ? st[uint32_t(li[p]) * sb + d] : 0u;
+                    x[u] = p < e_end ? st[uint32_t(li[p]) * sb + d] : 0u;
                 }
 #pragma unroll
                 for (uint32_t u = 0; u < 8; ++u) is += x[u];
             }
             const uint32_t isum = __reduce_add_sync(0xffffffffu, is);
             uint32_t nl = 0, nr = 0;
-            for (uint32_t b0 = e.start; b0 < e.end; b0 += 32) {
+            for (uint32_t b0 = e_start; b0 < e_end; b0 += 32) {
                 const uint32_t p = b0 + lane;
-                const bool valid = p < e.end;
+                const bool valid = p < e_end;
                 const uint16_t lc = valid ? li[p] : uint16_t(0);
                 const bool left = valid && uint32_t(st[uint32_t(lc) * sb + d]) * size <= isum;
                 const uint32_t bl = __ballot_sync(0xffffffffu, left);
                 const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
-                if (left) li[e.start + nl + __popc(bl & ltm)] = lc;
+                if (left) li[e_start + nl + __popc(bl & ltm)] = lc;
                 else if (valid) lt[nr + __popc(br & ltm)] = lc;
                 nl += __popc(bl);
                 nr += __popc(br);
             }
             __syncwarp();
-            for (uint32_t j = lane; j < nr; j += 32) li[e.start + nl + j] = lt[j];
+            for (uint32_t j = lane; j < nr; j += 32) li[e_start + nl + j] = lt[j];
             __syncwarp();
             split = __fdiv_rn(float(isum), float(size));
-            mid = e.start + nl;
+            mid = e_start + nl;
             even = 0;
             if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
                 // kd_forest.cpp:70-83: sort by (value, id); key = value | global id | local row
@@ -454,29 +494,69 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
                 for (uint32_t j = lane; j < m; j += 32) {
                     uint64_t key = kEmptyKey;
                     if (j < size) {
-                        const uint32_t lc = li[e.start + j];
+                        const uint32_t lc = li[e_start + j];
                         key = (uint64_t(st[lc * sb + d]) << 53) | (uint64_t(gid[lc]) << 11) | lc;
                     }
                     k[j] = key;
                 }
                 __syncwarp();
                 warp_bitonic_sort(k, m);
-                for (uint32_t j = lane; j < size; j += 32) li[e.start + j] = uint16_t(k[j] & 0x7ffu);
+                for (uint32_t j = lane; j < size; j += 32) li[e_start + j] = uint16_t(k[j] & 0x7ffu);
                 __syncwarp();
-                mid = e.start + size / 2;
+                mid = e_start + size / 2;
                 split = midpoint_f(float(st[uint32_t(li[mid - 1]) * sb + d]), float(st[uint32_t(li[mid]) * sb + d]));
                 even = 1;
             }
         }
         FT_MARK(10);
-        if (lane == 0) {
-            a.nodes[id] = KdNodeDev{d, split, 0u, 0u};
-            a.even[id] = even;
-            s.wstack[wsp] = StackEntry{mid, e.end, e.depth + 1, id, 1u};
-            s.wstack[wsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, 0u};
+        // this node's record (left child = id + 1 in pre-order) and its leaf
+        // children, one lane each: lane 0 node, lane 1 left leaf, lane 2 right leaf
+        const bool lleaf = mid - e_start <= lcap, rleaf = e_end - mid <= lcap;
+        const bool both = lleaf && rleaf;
+        if (lane < 3) {
+            KdNodeDev rec;
+            uint32_t rid = id, rdep = dep + 1;
+            uint8_t rev = 0;
+            bool w = true;
+            if (lane == 0) {
+                rec = KdNodeDev{d, split, id + 1, lleaf ? id + 2 : 0u};
+                rdep = dep;
+                rev = even;
+            } else if (lane == 1) {
+                rec = KdNodeDev{kLeaf, 0.0f, pbase + e_start, pbase + mid};
+                rid = id + 1;
+                w = lleaf;
+            } else {
+                rec = KdNodeDev{kLeaf, 0.0f, pbase + mid, pbase + e_end};
+                rid = id + 2;
+                w = both;
+            }
+            if (w) {
+                reinterpret_cast<uint4*>(a.nodes)[rid] =
+                    make_uint4(rec.split_dim, __float_as_uint(rec.split_val), rec.left, rec.right);
+                a.depth[rid] = rdep;
+                a.even[rid] = rev;
+            }
         }
-        if (wsp + 2 > kStack - 2) s.error = 1;
-        wsp = min(wsp + 2, kStack - 2);
+        if (lleaf) {
+            nid += both ? 2u : 1u;
+            nleaf += both ? 2u : 1u;
+            maxd = max(maxd, dep + 1);
+            if (!rleaf) {
+                if (lane == 0) s.tstack[wsp] = tpack(id, mid, e_end, dep + 1 - dep0, 0u);
+                ++wsp;
+            }
+        } else {
+            if (lane == 0) {
+                s.tstack[wsp] = tpack(id, mid, e_end, dep + 1 - dep0, 3u);
+                s.tstack[wsp + 1] = tpack(id, e_start, mid, dep + 1 - dep0, 0u);
+            }
+            wsp += 2;
+        }
+        if (wsp > kTileStack - 2 || dep + 1 - dep0 > 255) {
+            if (lane == 0) s.error = 1;
+            wsp = kTileStack - 2;
+        }
         __syncwarp();
         FT_MARK(12);
     }
@@ -488,7 +568,7 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
         s.max_depth = maxd;
     }
     // point_index of the tile in leaf order
-    for (uint32_t j = lane; j < tsz; j += 32) s.sub2[j] = s.sub[ts + s.lidx[j]];
+    for (uint32_t j = lane; j < tsz; j += 32) s.sub2[j] = gid[s.lidx[j]];
     __syncwarp();
     for (uint32_t j = lane; j < tsz; j += 32) s.sub[ts + j] = s.sub2[j];
     __syncwarp();
@@ -534,7 +614,7 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
         const uint32_t size = e.end - e.start;
         if (size <= tile_max && size > a.leaf_cap && size >= 64 && e.parent != kInvalidId) {
             __syncwarp();
-            warp_build_tile(a, s, e, base, wsp, sb);
+            warp_build_tile(a, s, e, base, sb);
             continue;
         }
         const uint32_t id = s.node_count;
@@ -920,11 +1000,14 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
         s.bsp = 1;
     }
     __syncthreads();
+    // staged tiles on: the block path runs down to tile size (its chunked
+    // partition beats warp 0's streaming path on 1k-4k point nodes)
+    const uint32_t warp_limit = tile_capacity(a) ? tile_capacity(a) : kWarpSubtree;
     while (s.bsp > 0 && !s.error) {
         const StackEntry e = s.bstack[s.bsp - 1];
         __syncthreads();
         const uint32_t size = e.end - e.start;
-        if (size <= kWarpSubtree) {
+        if (size <= warp_limit) {
             if (tid == 0) s.bsp -= 1;
             __syncthreads();
             const long long c0 = clock64();
