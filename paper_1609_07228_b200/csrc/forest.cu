@@ -31,6 +31,8 @@
 #include "../../include/annkit_b200.h"
 #include "internal.cuh"
 
+#include <cub/cub.cuh>
+
 namespace annk {
 namespace {
 
@@ -1100,6 +1102,26 @@ __global__ void forest_links_kernel(const KdNodeDev* __restrict__ nodes, uint32_
     }
 }
 
+// Per-leaf sibling lists (CSR over node ids): for a leaf at depth D, entry j
+// (0 <= j < D) is the sibling of its ancestor chain at parent depth D-1-j —
+// the subtrees graph_build.cpp:266-281 descends into, nearest level first.
+__global__ void sib_count_kernel(const KdNodeDev* __restrict__ nodes, const uint32_t* __restrict__ depth,
+                                 uint32_t num_nodes, uint32_t* __restrict__ cnt) {
+    for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id <= num_nodes; id += gridDim.x * blockDim.x)
+        cnt[id] = (id < num_nodes && nodes[id].split_dim == kLeaf) ? depth[id] : 0u;
+}
+__global__ void sib_fill_kernel(const KdNodeDev* __restrict__ nodes, const uint32_t* __restrict__ parent,
+                                uint32_t num_nodes, const uint32_t* __restrict__ off, uint32_t* __restrict__ list) {
+    for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id < num_nodes; id += gridDim.x * blockDim.x) {
+        if (nodes[id].split_dim != kLeaf) continue;
+        uint32_t o = off[id], node = id;
+        for (uint32_t par = parent[node]; par != kInvalidId; node = par, par = parent[node]) {
+            const KdNodeDev pn = nodes[par];
+            list[o++] = pn.left == node ? pn.right : pn.left;
+        }
+    }
+}
+
 // Batched best-bin-first (kd_forest.cpp:276-305).  One thread per query with
 // a binary min-heap over (double cost, node) in global scratch.
 struct HeapEnt {
@@ -1185,6 +1207,19 @@ void forest_ensure_links(annk_forest* f) {
         const uint32_t grid = std::min<uint32_t>((t.num_nodes + 255) / 256, 4096);
         LAUNCH(forest_links_kernel, std::max(grid, 1u), 256, 0, t.nodes.p, t.num_nodes, t.pidx.p,
                t.parent.p, t.owner.p);
+        // sibling lists
+        t.sib_off.alloc(size_t(t.num_nodes) + 1);
+        LAUNCH(sib_count_kernel, std::max(grid, 1u), 256, 0, t.nodes.p, t.depth.p, t.num_nodes, t.sib_off.p);
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, t.sib_off.p, t.sib_off.p, t.num_nodes + 1, stream()));
+        DevBuf<unsigned char> scratch(std::max<size_t>(tmp, 1));
+        CK(cub::DeviceScan::ExclusiveSum(scratch.p, tmp, t.sib_off.p, t.sib_off.p, t.num_nodes + 1, stream()));
+        uint32_t total = 0;
+        CK(cudaMemcpyAsync(&total, t.sib_off.p + t.num_nodes, 4, cudaMemcpyDeviceToHost, stream()));
+        ssync();
+        t.sib_list.alloc(std::max<size_t>(total, 1));
+        LAUNCH(sib_fill_kernel, std::max(grid, 1u), 256, 0, t.nodes.p, t.parent.p, t.num_nodes, t.sib_off.p,
+               t.sib_list.p);
     }
     f->links_ready = true;
     forest_upload_views(f);
@@ -1194,7 +1229,7 @@ void forest_upload_views(annk_forest* f) {
     std::vector<TreeView> v(f->n_trees);
     for (uint32_t i = 0; i < f->n_trees; ++i) {
         const TreeDev& t = f->trees[i];
-        v[i] = TreeView{t.nodes.p, t.depth.p, t.pidx.p, t.parent.p, t.owner.p,
+        v[i] = TreeView{t.nodes.p, t.depth.p, t.pidx.p, t.parent.p, t.owner.p, t.sib_off.p, t.sib_list.p,
                         t.root, t.num_nodes, t.leaf_count, t.max_depth};
     }
     f->views.alloc(f->n_trees);

@@ -131,14 +131,15 @@ struct InitArgs {
 struct InitScratch {
     uint32_t* table;
     uint32_t* uniq;
-    uint32_t cap;  // pow2
+    uint32_t cap;     // unique-candidate capacity (pow2)
+    uint32_t tslots;  // hash slots (pow2, >= cap)
     uint32_t* sib;
     uint32_t sib_cap;
     uint32_t* cnt;  // [0] unique count, [1] sibling count, [2] overflow flag
 };
 
 __device__ __forceinline__ void hs_insert(const InitScratch& w, uint32_t id) {
-    const uint32_t mask = 2 * w.cap - 1;
+    const uint32_t mask = w.tslots - 1;
     uint32_t h = (id * 2654435761u) & mask;
     for (uint32_t probe = 0; probe <= mask; ++probe) {
         const uint32_t old = atomicCAS(&w.table[h], 0xffffffffu, id);
@@ -156,48 +157,97 @@ __device__ __forceinline__ void hs_insert(const InitScratch& w, uint32_t id) {
 
 // Point i's candidate set (graph_build.cpp:266-281): own leaf per tree plus one
 // descended leaf per ancestor level >= conquer_depth, deduplicated in a shared
-// hash set (self excluded, as the reference skips c == i at :283).
+// hash set (self excluded, as the reference skips c == i at :283).  The
+// ancestor siblings come from the forest's per-leaf sibling lists, flattened
+// over the trees of a 32-tree group so every lane takes independent
+// (tree, level) entries; each lane walks kDesc descents interleaved so their
+// dependent node loads overlap.
+constexpr uint32_t kDesc = 4;
 __device__ void init_collect(const InitArgs& a, uint32_t i, const float* q, const InitScratch& w) {
     const uint32_t lane = lane_id();
     // table <- EMPTY (vectorised)
     uint4* t4 = reinterpret_cast<uint4*>(w.table);
-    for (uint32_t j = lane; j < (2 * w.cap) / 4; j += 32) t4[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (uint32_t j = lane; j < w.tslots / 4; j += 32) t4[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
     if (lane == 0) { w.cnt[0] = 0; w.cnt[1] = 0; w.cnt[2] = 0; }
     __syncwarp();
-    for (uint32_t t = lane; t < a.n_trees; t += 32) {
-        const TreeView tv = a.trees[t];
-        const uint32_t leaf = tv.owner[i];
-        const KdNodeDev ln = tv.nodes[leaf];
-        for (uint32_t p = ln.left; p < ln.right; ++p) {
-            const uint32_t id = tv.pidx[p];
-            if (id != i) hs_insert(w, id);
-        }
-        uint32_t node = leaf;
-        for (;;) {
-            const uint32_t par = tv.parent[node];
-            if (par == kInvalidId || tv.depth[par] < a.conquer_depth) break;
-            const KdNodeDev pn = tv.nodes[par];
-            const uint32_t k = atomicAdd(&w.cnt[1], 1u);
-            if (k < w.sib_cap) {
-                w.sib[k] = pn.left == node ? pn.right : pn.left;
-                w.sib[w.sib_cap + k] = t;
-            } else {
-                w.cnt[2] = 1;
+    for (uint32_t g = 0; g < a.n_trees; g += 32) {
+        const uint32_t t = g + lane;
+        uint32_t nsib = 0, soff = 0;
+        if (t < a.n_trees) {
+            const TreeView& tv = a.trees[t];
+            const uint32_t leaf = tv.owner[i];
+            const KdNodeDev ln = tv.nodes[leaf];
+            const uint32_t dl = tv.depth[leaf];
+            nsib = dl > a.conquer_depth ? dl - a.conquer_depth : 0u;
+            soff = tv.sib_off[leaf];
+            for (uint32_t p = ln.left; p < ln.right; ++p) {
+                const uint32_t id = tv.pidx[p];
+                if (id != i) hs_insert(w, id);
             }
-            node = par;
         }
-    }
-    __syncwarp();
-    const uint32_t nsib = min(w.cnt[1], w.sib_cap);
-    for (uint32_t k = lane; k < nsib; k += 32) {  // descend_from(sibling, x_i) per level
-        const TreeView tv = a.trees[w.sib[w.sib_cap + k]];
-        uint32_t nd = w.sib[k];
-        for (KdNodeDev x = tv.nodes[nd]; x.split_dim != kLeaf; x = tv.nodes[nd])
-            nd = q[x.split_dim] <= x.split_val ? x.left : x.right;
-        const KdNodeDev ln = tv.nodes[nd];
-        for (uint32_t p = ln.left; p < ln.right; ++p) {
-            const uint32_t id = tv.pidx[p];
-            if (id != i) hs_insert(w, id);
+        uint32_t incl = nsib;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += y;
+        }
+        const uint32_t excl = incl - nsib;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t k0 = 0; k0 < total; k0 += 32 * kDesc) {
+            uint32_t nd[kDesc];
+            const KdNodeDev* nodes[kDesc];
+            const uint32_t* pidx[kDesc];
+            bool act[kDesc];
+#pragma unroll
+            for (uint32_t r = 0; r < kDesc; ++r) {
+                const uint32_t k = k0 + r * 32 + lane;
+                // owner lane of entry k: the last lane whose exclusive prefix is <= k
+                uint32_t lo = 0;
+#pragma unroll
+                for (uint32_t st = 16; st > 0; st >>= 1) {
+                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, lo + st);
+                    if (ex <= k) lo += st;
+                }
+                const uint32_t ex_lo = __shfl_sync(0xffffffffu, excl, lo);
+                const uint32_t off_lo = __shfl_sync(0xffffffffu, soff, lo);
+                act[r] = k < total;
+                nd[r] = 0;
+                nodes[r] = nullptr;
+                pidx[r] = nullptr;
+                if (act[r]) {
+                    const TreeView& tv = a.trees[g + lo];
+                    nodes[r] = tv.nodes;
+                    pidx[r] = tv.pidx;
+                    nd[r] = tv.sib_list[off_lo + (k - ex_lo)];
+                }
+            }
+            // descend_from(sibling, x_i), kDesc walks interleaved
+            KdNodeDev cur[kDesc];
+#pragma unroll
+            for (uint32_t r = 0; r < kDesc; ++r)
+                if (act[r]) cur[r] = nodes[r][nd[r]];
+            for (;;) {
+                bool more = false;
+#pragma unroll
+                for (uint32_t r = 0; r < kDesc; ++r) {
+                    if (act[r] && cur[r].split_dim != kLeaf) {
+                        nd[r] = q[cur[r].split_dim] <= cur[r].split_val ? cur[r].left : cur[r].right;
+                        more = true;
+                    }
+                }
+                if (!more) break;
+#pragma unroll
+                for (uint32_t r = 0; r < kDesc; ++r)
+                    if (act[r] && cur[r].split_dim != kLeaf) cur[r] = nodes[r][nd[r]];
+            }
+#pragma unroll
+            for (uint32_t r = 0; r < kDesc; ++r) {
+                if (!act[r]) continue;
+                for (uint32_t p = cur[r].left; p < cur[r].right; ++p) {
+                    const uint32_t id = pidx[r][p];
+                    if (id != i) hs_insert(w, id);
+                }
+            }
         }
     }
     __syncwarp();
@@ -250,12 +300,57 @@ __device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, const
     const uint32_t u = w.cnt[0];
     uint64_t* keys = reinterpret_cast<uint64_t*>(w.table);  // table no longer needed
     __syncwarp();
-    for (uint32_t j = lane; j < u; j += 32) {
-        const uint32_t id = w.uniq[j];
-        const float d = a.x8 ? l2_u8(a.x8 + size_t(i) * a.ld8, a.x8 + size_t(id) * a.ld8, a.ld8, a.norms8[i],
-                                     a.norms8[id])
-                             : l2_exact_ldg(q, a.x + size_t(id) * a.ld, a.ld);
-        keys[j] = make_key(d, id);
+    if (a.x8) {
+        // 8 lanes per candidate row (one coalesced 128-byte segment per step),
+        // 4 rows per warp step, kRows steps in flight; dot reduced by shuffles
+        constexpr uint32_t kRows = 8;
+        const uint32_t sub = lane & 7, grp = lane >> 3;
+        const uint8_t* xi = a.x8 + size_t(i) * a.ld8;
+        const int32_t ni = a.norms8[i];
+        const uint32_t nch = (a.ld8 + 127) / 128;
+        uint4 qv0 = make_uint4(0, 0, 0, 0);
+        if (sub * 16 < a.ld8) qv0 = *reinterpret_cast<const uint4*>(xi + sub * 16);
+        for (uint32_t j0 = 0; j0 < u; j0 += 4 * kRows) {
+            uint32_t id[kRows], dot[kRows];
+            int32_t nb[kRows];
+#pragma unroll
+            for (uint32_t r = 0; r < kRows; ++r) {
+                const uint32_t j = j0 + r * 4 + grp;
+                id[r] = j < u ? w.uniq[j] : i;
+                dot[r] = 0;
+                nb[r] = sub == 0 ? a.norms8[id[r]] : 0;
+            }
+            for (uint32_t c = 0; c < nch; ++c) {
+                const uint32_t off = (c * 8 + sub) * 16;
+                if (off < a.ld8) {
+                    const uint4 qv = c == 0 ? qv0 : *reinterpret_cast<const uint4*>(xi + off);
+                    uint4 rv[kRows];
+#pragma unroll
+                    for (uint32_t r = 0; r < kRows; ++r)
+                        rv[r] = *reinterpret_cast<const uint4*>(a.x8 + size_t(id[r]) * a.ld8 + off);
+#pragma unroll
+                    for (uint32_t r = 0; r < kRows; ++r) {
+                        dot[r] = __dp4a(qv.x, rv[r].x, dot[r]);
+                        dot[r] = __dp4a(qv.y, rv[r].y, dot[r]);
+                        dot[r] = __dp4a(qv.z, rv[r].z, dot[r]);
+                        dot[r] = __dp4a(qv.w, rv[r].w, dot[r]);
+                    }
+                }
+            }
+#pragma unroll
+            for (uint32_t r = 0; r < kRows; ++r) {
+                dot[r] += __shfl_xor_sync(0xffffffffu, dot[r], 1);
+                dot[r] += __shfl_xor_sync(0xffffffffu, dot[r], 2);
+                dot[r] += __shfl_xor_sync(0xffffffffu, dot[r], 4);
+                const uint32_t j = j0 + r * 4 + grp;
+                if (sub == 0 && j < u) keys[j] = make_key(float(ni + nb[r] - 2 * int32_t(dot[r])), id[r]);
+            }
+        }
+    } else {
+        for (uint32_t j = lane; j < u; j += 32) {
+            const uint32_t id = w.uniq[j];
+            keys[j] = make_key(l2_exact_ldg(q, a.x + size_t(id) * a.ld, a.ld), id);
+        }
     }
     __syncwarp();
     uint32_t take = min(u, a.P);
@@ -296,8 +391,8 @@ __device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, const
 }
 
 __host__ __device__ __forceinline__ size_t init_warp_bytes(uint32_t cap, uint32_t ld, uint32_t sib_cap) {
-    // table (2*cap u32 == cap u64 keys) + uniq (cap u32) + q row + sib (2*sib_cap) + hist (256) + cnt (4)
-    return (size_t(cap) * 12 + size_t(ld) * 4 + size_t(sib_cap) * 8 + 256 * 4 + 16 + 15) & ~size_t(15);
+    // table (cap u32) + uniq (cap u32) == cap u64 keys, q row, sib (2*sib_cap), hist (256), cnt (4)
+    return (size_t(cap) * 8 + size_t(ld) * 4 + size_t(sib_cap) * 8 + 256 * 4 + 16 + 15) & ~size_t(15);
 }
 
 __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint32_t sib_cap,
@@ -307,7 +402,11 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
     unsigned char* base = smem + warp * init_warp_bytes(kInitCap, a.ld, sib_cap);
     InitScratch w;
     w.table = reinterpret_cast<uint32_t*>(base);
-    w.uniq = w.table + 2 * kInitCap;
+    // one 8 KB region: hash slots [0, 4 KB) + unique list [4 KB, 8 KB); the
+    // u64 keys then overwrite it in place (key j covers unique entries
+    // 2j-1024 and 2j-1023, already consumed when keys are written in order)
+    w.tslots = kInitCap;
+    w.uniq = w.table + kInitCap;
     w.cap = kInitCap;
     float* q = reinterpret_cast<float*>(w.uniq + kInitCap);
     w.sib = reinterpret_cast<uint32_t*>(q + a.ld);
@@ -345,6 +444,7 @@ __global__ void init_overflow_kernel(InitArgs a, const uint32_t* list, uint32_t 
         w.table = gscratch + size_t(blockIdx.x) * (3 * size_t(cap) + 2 * sib_cap);
         w.uniq = w.table + 2 * cap;
         w.cap = cap;
+        w.tslots = 2 * cap;
         w.sib = w.uniq + cap;
         w.sib_cap = sib_cap;
         w.cnt = s_misc + 256;
@@ -1632,7 +1732,7 @@ int annk_init_graph(const annk_dataset* ds, const annk_forest* fc, uint32_t k, u
                    s->keys.p, s->flags.p, s->sizes.p, comps.p, overflow.p,
                    ds->u8 ? ds->data8.p : nullptr, ds->ld8, ds->u8 ? ds->norms8.p : nullptr};
         const uint32_t sib_full = f->n_trees * (max_depth + 1);
-        const uint32_t sib_cap = std::min<uint32_t>(sib_full, 512);
+        const uint32_t sib_cap = 0;  // sibling lists come from the forest (sib_list)
         const size_t per_warp = init_warp_bytes(kInitCap, ds->ld, sib_cap);
         const size_t smem = per_warp * kInitWarps;
         CK(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

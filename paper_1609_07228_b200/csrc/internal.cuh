@@ -55,6 +55,8 @@ struct TreeDev {
     annk::DevBuf<uint32_t> pidx;    // point_index permutation (n)
     annk::DevBuf<uint32_t> parent;  // lazily built (init_graph)
     annk::DevBuf<uint32_t> owner;   // lazily built: leaf owning each point
+    annk::DevBuf<uint32_t> sib_off;   // lazily built: per-leaf sibling lists (CSR)
+    annk::DevBuf<uint32_t> sib_list;
     uint32_t num_nodes = 0, root = 0, leaf_count = 0, max_depth = 0;
 };
 
@@ -65,6 +67,8 @@ struct TreeView {
     const uint32_t* pidx;
     const uint32_t* parent;
     const uint32_t* owner;
+    const uint32_t* sib_off;   // per node: start of its sibling list (leaves only)
+    const uint32_t* sib_list;  // leaf ancestors' siblings, nearest level first
     uint32_t root, num_nodes, leaf_count, max_depth;
 };
 
