@@ -165,6 +165,46 @@ int annk_state_join_rows(const annk_state* s, uint64_t* rows);
  * per-point offer slots]. */
 int annk_state_stats(const annk_state* s, uint64_t* out4);
 
+/* ----------------------------------------------------- shard mode (multi-GPU)
+ * one process per GPU, pools sharded by point.  A state owns the
+ * points [lo, hi): init, sampling, the join (as the visiting point i), the
+ * merge (as the target) and finalize touch only those.  One NN-descent round
+ * over G ranks (the driver is paper_1609_07228_b200/sharded.py):
+ *   annk_shard_sample        forward lists + tails of the owned points
+ *   all-gather               annk_state_rows(FNEW, CNEW, FOLD, COLD, THR) rows
+ *   annk_shard_union         reverse lists from all forward lists, union
+ *                            (graph_build.cpp:88-103; same RNG streams on every rank)
+ *   annk_shard_join          local join of owned points; offers to any target
+ *   all-to-all               annk_shard_offers_count/pack per destination range,
+ *                            annk_shard_offers_add on the receiver
+ *   annk_shard_merge         top-P(start U offers) of the owned pools
+ * The pools equal the single-GPU ones: the merge is order-independent
+ * (graph_build.cpp:105-162 reads only the snapshot lists).  Buffers passed to
+ * the row / offer calls may be host or device pointers (UVA copies). */
+#define ANNK_ROWS_FNEW 0 /* n x sample_cap u32: sampled new ids (pool order) */
+#define ANNK_ROWS_CNEW 1 /* n u32 */
+#define ANNK_ROWS_FOLD 2 /* n x pool_cap u32: sampled old ids */
+#define ANNK_ROWS_COLD 3 /* n u32 */
+#define ANNK_ROWS_THR 4  /* n u64: start-of-round pool tail keys */
+/* init_graph for the points [lo, hi) only (the rest stay empty). */
+int annk_init_graph_shard(const annk_dataset* ds, const annk_forest* f, uint32_t k,
+                          uint32_t conquer_depth, uint32_t pool_cap, uint32_t sample_cap, uint64_t seed,
+                          uint32_t lo, uint32_t hi, annk_state** out);
+int annk_state_set_shard(annk_state* s, uint32_t lo, uint32_t hi);
+/* Copies rows [lo, hi) of a per-point buffer out of (put = 0) or into (put = 1) the state. */
+int annk_state_rows(annk_state* s, int which, int put, uint32_t lo, uint32_t hi, void* buf);
+int annk_shard_sample(annk_state* s);
+int annk_shard_union(annk_state* s);
+int annk_shard_join(annk_state* s, const annk_dataset* ds, uint64_t* comps);
+/* Offers held for targets [lo, hi): total count; then pack them target-major
+ * (counts: hi - lo u32, keys: total u64). */
+int annk_shard_offers_count(annk_state* s, uint32_t lo, uint32_t hi, uint64_t* total);
+int annk_shard_offers_pack(annk_state* s, uint32_t lo, uint32_t hi, uint32_t* counts, uint64_t* keys);
+/* Adds received offers for owned targets [lo, hi) (same packed layout). */
+int annk_shard_offers_add(annk_state* s, uint32_t lo, uint32_t hi, const uint32_t* counts,
+                          const uint64_t* keys);
+int annk_shard_merge(annk_state* s, uint64_t* changes);
+
 /* --------------------------------------------------------------- search */
 /* search.cpp:23-35 GraphSearcher(base, forest, graph): validates the graph
  * and uploads it (n x graph_k ids). forest may be NULL (random init only). */

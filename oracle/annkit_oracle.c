@@ -183,7 +183,7 @@ static void parallel_for(uint32_t n, uint32_t workers, range_fn fn, void* ctx) {
 typedef struct {
     uint32_t id;
     float dist;
-    uint8_t flag_new, checked;
+    uint8_t flag_new, checked, fresh; /* fresh: inserted during the current shard merge */
 } entry;
 typedef struct {
     uint32_t cap, size;
@@ -199,7 +199,7 @@ static void pool_init(pool* p, uint32_t cap) {
     p->e = xmalloc(sizeof(entry) * (cap + 1));
 }
 static int pool_insert(pool* p, uint32_t id, float dist, int flag_new) {
-    const entry x = {id, dist, (uint8_t)(flag_new ? 1 : 0), 0};
+    const entry x = {id, dist, (uint8_t)(flag_new ? 1 : 0), 0, 1};
     uint32_t lo = 0, hi = p->size;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) / 2;
@@ -878,6 +878,153 @@ void ora_union_reverse_lists(void* p) {
     }
     free(rn.a);
     free(ro.a);
+}
+
+/* ------------------------------------------------------------ shard mode --
+ * Test-only restatement of the multi-GPU protocol (include/annkit_b200.h,
+ * "shard mode"): the same five steps over a per-rank copy of the state, with
+ * the forward rows / thresholds / offers exchanged by the Python driver.  The
+ * pools it yields equal ora_nn_descent_iteration's (graph_build.cpp:105-162
+ * reads only the snapshot lists, so the join's inserts commute). */
+static uint64_t pool_key(const entry* e) {
+    uint32_t b;
+    memcpy(&b, &e->dist, 4);
+    return ((uint64_t)b << 32) | e->id;
+}
+
+/* graph_build.cpp:71-85 for i in [lo, hi): forward rows + start tails. */
+void ora_shard_sample(void* p, uint32_t lo, uint32_t hi, uint32_t* fnew, uint32_t* cnew, uint32_t* fold,
+                      uint32_t* cold, uint64_t* thr) {
+    rstate* s = p;
+    const uint32_t S = s->sample_cap, P = s->pool_cap;
+    for (uint32_t i = lo; i < hi; ++i) {
+        uint32_t taken = 0, nold = 0;
+        pool* pl = &s->pools[i];
+        for (uint32_t j = 0; j < pl->size; ++j) {
+            if (taken >= S) break;
+            entry* e = &pl->e[j];
+            if (e->flag_new) {
+                fnew[(size_t)i * S + taken++] = e->id;
+                e->flag_new = 0;
+            } else {
+                fold[(size_t)i * P + nold++] = e->id;
+            }
+        }
+        cnew[i] = taken;
+        cold[i] = nold;
+        thr[i] = pl->size == P ? pool_key(&pl->e[P - 1]) : ~0ull;
+    }
+}
+
+/* graph_build.cpp:59-103 from the forward rows of all points: reverse lists in
+ * ascending owner order, sample_down, union (every rank computes all points). */
+void ora_shard_union(void* p, const uint32_t* fnew, const uint32_t* cnew, const uint32_t* fold,
+                     const uint32_t* cold) {
+    rstate* s = p;
+    const uint32_t S = s->sample_cap, P = s->pool_cap;
+    for (uint32_t i = 0; i < s->n; ++i) s->g_new[i].n = s->g_old[i].n = s->g_rnew[i].n = s->g_rold[i].n = 0;
+    for (uint32_t i = 0; i < s->n; ++i) {
+        for (uint32_t j = 0; j < cnew[i]; ++j) {
+            const uint32_t id = fnew[(size_t)i * S + j];
+            ul_push(&s->g_new[i], id);
+            ul_push(&s->g_rnew[id], i);
+        }
+        for (uint32_t j = 0; j < cold[i]; ++j) {
+            const uint32_t id = fold[(size_t)i * P + j];
+            ul_push(&s->g_old[i], id);
+            ul_push(&s->g_rold[id], i);
+        }
+    }
+    ora_union_reverse_lists(s);
+}
+
+/* Offers produced by the join of the owned points (target, key). */
+typedef struct {
+    uint32_t* tgt;
+    uint64_t* key;
+    size_t n, cap;
+} offer_list;
+static __thread offer_list g_offers;
+static void offer_push(uint32_t tgt, uint64_t key) {
+    if (g_offers.n == g_offers.cap) {
+        g_offers.cap = g_offers.cap ? g_offers.cap * 2 : 1024;
+        g_offers.tgt = realloc(g_offers.tgt, sizeof(uint32_t) * g_offers.cap);
+        g_offers.key = realloc(g_offers.key, sizeof(uint64_t) * g_offers.cap);
+        if (!g_offers.tgt || !g_offers.key) abort();
+    }
+    g_offers.tgt[g_offers.n] = tgt;
+    g_offers.key[g_offers.n] = key;
+    ++g_offers.n;
+}
+static uint64_t make_key_f(float d, uint32_t id) {
+    uint32_t b;
+    memcpy(&b, &d, 4);
+    return ((uint64_t)b << 32) | id;
+}
+
+/* graph_build.cpp:105-162 join for i in [lo, hi); offers that beat the
+ * target's start tail thr[target] are kept (the rest cannot enter its pool).
+ * Returns the distance count; the offers stay in a thread-local list. */
+uint64_t ora_shard_join(void* p, void* vsp, uint32_t lo, uint32_t hi, const uint64_t* thr, uint64_t* n_offers) {
+    rstate* s = p;
+    const vset* vs = vsp;
+    g_offers.n = 0;
+    uint64_t comps = 0;
+    for (uint32_t i = lo; i < hi; ++i) {
+        const ulist* nw = &s->g_new[i];
+        const ulist* od = &s->g_old[i];
+        for (uint32_t a = 0; a < nw->n; ++a) {
+            const uint32_t j = nw->a[a];
+            const float* jr = row(vs, j);
+            for (uint32_t b = a + 1; b < nw->n; ++b) {
+                const uint32_t k2 = nw->a[b];
+                const float d = l2(jr, row(vs, k2), vs->dim);
+                ++comps;
+                if (j != k2) {
+                    if (make_key_f(d, k2) < thr[j]) offer_push(j, make_key_f(d, k2));
+                    if (make_key_f(d, j) < thr[k2]) offer_push(k2, make_key_f(d, j));
+                }
+            }
+            for (uint32_t b = 0; b < od->n; ++b) {
+                const uint32_t l = od->a[b];
+                if (l == j) continue;
+                const float d = l2(jr, row(vs, l), vs->dim);
+                ++comps;
+                if (make_key_f(d, l) < thr[j]) offer_push(j, make_key_f(d, l));
+                if (make_key_f(d, j) < thr[l]) offer_push(l, make_key_f(d, j));
+            }
+        }
+    }
+    s->dist_comps += comps;
+    *n_offers = g_offers.n;
+    return comps;
+}
+void ora_shard_offers_get(uint32_t* tgt, uint64_t* key) {
+    memcpy(tgt, g_offers.tgt, sizeof(uint32_t) * g_offers.n);
+    memcpy(key, g_offers.key, sizeof(uint64_t) * g_offers.n);
+}
+
+/* Inserts offers (all for owned targets) into their pools with flag new; the
+ * return value counts inserted entries that survive (the device's `changes`). */
+uint64_t ora_shard_merge(void* p, uint32_t lo, uint32_t hi, const uint32_t* tgt, const uint64_t* key, size_t m) {
+    rstate* s = p;
+    for (uint32_t i = lo; i < hi; ++i)
+        for (uint32_t j = 0; j < s->pools[i].size; ++j) s->pools[i].e[j].fresh = 0;
+    for (size_t r = 0; r < m; ++r) {
+        float d;
+        const uint32_t b = (uint32_t)(key[r] >> 32);
+        memcpy(&d, &b, 4);
+        pool_insert(&s->pools[tgt[r]], (uint32_t)key[r], d, 1);
+    }
+    uint64_t changes = 0;
+    for (uint32_t i = lo; i < hi; ++i)
+        for (uint32_t j = 0; j < s->pools[i].size; ++j) {
+            changes += s->pools[i].e[j].fresh;
+            s->pools[i].e[j].fresh = 0;
+        }
+    ++s->iteration;
+    s->last_changes = changes;
+    return changes;
 }
 
 /* graph_build.cpp:105-162 nn_descent_iteration, single-worker order. */

@@ -107,6 +107,14 @@ class OracleLib:
         L.ora_nn_expansion_iteration.restype = _u64
         L.ora_nn_expansion_iteration.argtypes = [_vp, _vp, _u32]
         L.ora_rebuild_sample_lists.argtypes = [_vp]
+        if hasattr(L, "ora_shard_sample"):  # restatement only: shard-mode protocol
+            L.ora_shard_sample.argtypes = [_vp, _u32, _u32, _u32p, _u32p, _u32p, _u32p, _u64p]
+            L.ora_shard_union.argtypes = [_vp, _u32p, _u32p, _u32p, _u32p]
+            L.ora_shard_join.restype = _u64
+            L.ora_shard_join.argtypes = [_vp, _vp, _u32, _u32, _u64p, C.POINTER(_u64)]
+            L.ora_shard_offers_get.argtypes = [_u32p, _u64p]
+            L.ora_shard_merge.restype = _u64
+            L.ora_shard_merge.argtypes = [_vp, _u32, _u32, _u32p, _u64p, C.c_size_t]
         L.ora_union_reverse_lists.argtypes = [_vp]
         L.ora_refine_nn_descent.argtypes = [_vp, _vp, _u32, _u32, C.c_double]
         L.ora_finalize.argtypes = [_vp, _vp, _u32, _u32p, _f32p]
@@ -312,6 +320,26 @@ class State:
 
     def rebuild_sample_lists(self):
         self.lib.L.ora_rebuild_sample_lists(self.h)
+
+    # shard-mode protocol (see annkit_oracle.c); row buffers are full-n arrays
+    def shard_sample(self, lo, hi, fnew, cnew, fold, cold, thr):
+        self.lib.L.ora_shard_sample(self.h, lo, hi, fnew, cnew, fold, cold, thr)
+
+    def shard_union(self, fnew, cnew, fold, cold):
+        self.lib.L.ora_shard_union(self.h, fnew, cnew, fold, cold)
+
+    def shard_join(self, vs, lo, hi, thr):
+        m = C.c_uint64(0)
+        comps = int(self.lib.L.ora_shard_join(self.h, vs.h, lo, hi, thr, C.byref(m)))
+        tgt = np.empty(max(m.value, 1), np.uint32)
+        key = np.empty(max(m.value, 1), np.uint64)
+        self.lib.L.ora_shard_offers_get(tgt, key)
+        return comps, tgt[:m.value], key[:m.value]
+
+    def shard_merge(self, lo, hi, tgt, key):
+        tgt = np.ascontiguousarray(tgt, np.uint32)
+        key = np.ascontiguousarray(key, np.uint64)
+        return int(self.lib.L.ora_shard_merge(self.h, lo, hi, tgt, key, tgt.size))
 
     def union_reverse_lists(self):
         self.lib.L.ora_union_reverse_lists(self.h)

@@ -85,6 +85,14 @@ void ora_state_lists(void* s, int which, uint32_t* offsets, uint32_t* data);
 uint64_t ora_nn_descent_iteration(void* s, void* vs, uint32_t workers);
 uint64_t ora_nn_expansion_iteration(void* s, void* vs, uint32_t workers);
 void ora_rebuild_sample_lists(void* s);
+/* shard-mode protocol (test-only; see annkit_oracle.c) */
+void ora_shard_sample(void* s, uint32_t lo, uint32_t hi, uint32_t* fnew, uint32_t* cnew, uint32_t* fold,
+                      uint32_t* cold, uint64_t* thr);
+void ora_shard_union(void* s, const uint32_t* fnew, const uint32_t* cnew, const uint32_t* fold,
+                     const uint32_t* cold);
+uint64_t ora_shard_join(void* s, void* vs, uint32_t lo, uint32_t hi, const uint64_t* thr, uint64_t* n_offers);
+void ora_shard_offers_get(uint32_t* tgt, uint64_t* key);
+uint64_t ora_shard_merge(void* s, uint32_t lo, uint32_t hi, const uint32_t* tgt, const uint64_t* key, size_t m);
 void ora_union_reverse_lists(void* s);
 int ora_refine_nn_descent(void* s, void* vs, uint32_t max_iters, uint32_t workers,
                           double min_change_rate);

@@ -21,6 +21,9 @@ ANNK_CUDA_ERROR = 3
 ANNK_OUT_OF_MEMORY = 4
 ANNK_INTERNAL = 5
 
+# annk_state_rows buffers (include/annkit_b200.h)
+ANNK_ROWS_FNEW, ANNK_ROWS_CNEW, ANNK_ROWS_FOLD, ANNK_ROWS_COLD, ANNK_ROWS_THR = range(5)
+
 
 class AnnkError(RuntimeError):
     """CUDA / internal failure."""
@@ -95,6 +98,16 @@ _SIGS = {
     "annk_pool_topk_accuracy": [_vp, _u32p, _u32, _u32, _vp, C.POINTER(C.c_double)],
     "annk_state_join_rows": [_vp, C.POINTER(_u64)],
     "annk_state_stats": [_vp, _u64p],
+    "annk_init_graph_shard": [_vp, _vp, _u32, _u32, _u32, _u32, _u64, _u32, _u32, _pp],
+    "annk_state_set_shard": [_vp, _u32, _u32],
+    "annk_state_rows": [_vp, C.c_int, C.c_int, _u32, _u32, _vp],
+    "annk_shard_sample": [_vp],
+    "annk_shard_union": [_vp],
+    "annk_shard_join": [_vp, _vp, C.POINTER(_u64)],
+    "annk_shard_offers_count": [_vp, _u32, _u32, C.POINTER(_u64)],
+    "annk_shard_offers_pack": [_vp, _u32, _u32, _vp, _vp],
+    "annk_shard_offers_add": [_vp, _u32, _u32, _vp, _vp],
+    "annk_shard_merge": [_vp, C.POINTER(_u64)],
     "annk_searcher_create": [_vp, _vp, _u32p, _u32, _u32, _pp],
     "annk_searcher_destroy": [_vp],
     "annk_search": [_vp, _f32p, _u32, _u32, C.POINTER(SearchParamsC), _u32p, _f32p, _vp],

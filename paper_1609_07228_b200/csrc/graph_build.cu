@@ -396,7 +396,8 @@ __host__ __device__ __forceinline__ size_t init_warp_bytes(uint32_t cap, uint32_
 }
 
 __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint32_t sib_cap,
-                                                               const uint32_t* __restrict__ order) {
+                                                               const uint32_t* __restrict__ order,
+                                                               uint32_t n_visit) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t warp = threadIdx.x / 32, lane = lane_id();
     unsigned char* base = smem + warp * init_warp_bytes(kInitCap, a.ld, sib_cap);
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
     w.sib_cap = sib_cap;
     uint32_t* hist = w.sib + 2 * sib_cap;
     w.cnt = hist + 256;
-    for (uint32_t ord = blockIdx.x * kInitWarps + warp; ord < a.n; ord += gridDim.x * kInitWarps) {
+    for (uint32_t ord = blockIdx.x * kInitWarps + warp; ord < n_visit; ord += gridDim.x * kInitWarps) {
         // visit points in tree-0 leaf order: concurrently processed points share
         // most candidate rows, so the gathers hit L2
         const uint32_t i = order ? order[ord] : ord;
@@ -467,15 +468,14 @@ struct SampleArgs {
     uint32_t* fold;  // n x P
     uint32_t* cnew;
     uint32_t* cold;
-    uint32_t* rn_cnt;
-    uint32_t* ro_cnt;
     uint64_t* thr;
+    uint32_t lo;  // points [lo, n) are sampled
 };
 
 // graph_build.cpp:71-85: ascending scan until S new entries are taken.
 __global__ void sample_kernel(SampleArgs a) {
     const uint32_t lane = lane_id();
-    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const uint32_t i = a.lo + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (i >= a.n) return;
     const uint32_t sz = a.sizes[i];
     const uint64_t* pk = a.keys + size_t(i) * a.P;
@@ -495,10 +495,8 @@ __global__ void sample_kernel(SampleArgs a) {
         if (in_scan && isnew) {
             a.fnew[size_t(i) * a.S + rank_new] = id;
             pf[j] = 0;
-            atomicAdd(&a.rn_cnt[id], 1u);
         } else if (in_scan) {
             a.fold[size_t(i) * a.P + nold + __popc(bo & lt)] = id;
-            atomicAdd(&a.ro_cnt[id], 1u);
         }
         taken = min(a.S, taken + __popc(bn));
         nold += __popc(bo);
@@ -508,6 +506,16 @@ __global__ void sample_kernel(SampleArgs a) {
         a.cold[i] = nold;
         a.thr[i] = sz == a.P ? pk[a.P - 1] : kEmptyKey;
     }
+}
+
+// Reverse-list sizes from the forward lists of all points.
+__global__ void rev_count_kernel(uint32_t n, uint32_t width, const uint32_t* __restrict__ fwd,
+                                 const uint32_t* __restrict__ cnt, uint32_t* __restrict__ out) {
+    const uint32_t lane = lane_id();
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= n) return;
+    const uint32_t c = cnt[i];
+    for (uint32_t j = lane; j < c; j += 32) atomicAdd(&out[fwd[size_t(i) * width + j]], 1u);
 }
 
 __global__ void reverse_scatter_kernel(uint32_t n, uint32_t width, const uint32_t* __restrict__ fwd,
@@ -646,7 +654,7 @@ struct JoinArgs {
     uint64_t* ov_key;
     uint32_t ov_cap;
     unsigned long long* offers;  // total accepted offers (stats)
-    uint32_t sub, nsub;          // this sub-round joins points with ord % nsub == sub
+    const uint32_t* order;       // visit list of n points (nullptr: 0..n-1)
 };
 
 __device__ __forceinline__ void offer(const JoinArgs& a, uint32_t owner, uint32_t cand, float d) {
@@ -673,8 +681,9 @@ __global__ void join_kernel(JoinArgs a) {
     const uint32_t warp = threadIdx.x / 32, lane = lane_id();
     const uint32_t wpb = blockDim.x / 32;
     float* row = reinterpret_cast<float*>(smem) + size_t(warp) * a.ld;
-    const uint32_t i = blockIdx.x * wpb + warp;
-    if (i >= a.n) return;
+    const uint32_t w = blockIdx.x * wpb + warp;
+    if (w >= a.n) return;
+    const uint32_t i = a.order ? a.order[w] : w;
     const uint32_t A = a.gncnt[i], B = a.gocnt[i];
     const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
     const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
@@ -859,8 +868,7 @@ join_agg_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr uint32_t kWarps = kJoinThreads / 32;
     unsigned long long comps = 0;
-    for (uint32_t t = blockIdx.x;; t += gridDim.x) {
-        const uint32_t ord = t * a.nsub + a.sub;
+    for (uint32_t ord = blockIdx.x;; ord += gridDim.x) {
         if (ord >= a.n) break;
         const uint32_t i = order ? order[ord] : ord;
         const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
@@ -1034,7 +1042,7 @@ struct MergeArgs {
     const uint32_t* ov_off;  // per-target start in the target-sorted spill list
     const uint64_t* ov_key;
     unsigned long long* changes;
-    uint64_t* thr;  // refreshed tails for the next sub-round (nullable)
+    uint32_t lo;    // targets [lo, n) are merged
 };
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t n, uint64_t v) {
@@ -1158,7 +1166,7 @@ __global__ void merge_stream_kernel(MergeArgs a) {
     uint64_t* sp = R + a.P;
     uint64_t* tmp = sp + a.P;
     uint8_t* sflag = reinterpret_cast<uint8_t*>(tmp + a.P);
-    const uint32_t i = blockIdx.x * wpb + warp;
+    const uint32_t i = a.lo + blockIdx.x * wpb + warp;
     if (i >= a.n) return;
     const uint32_t total = a.ocnt[i];
     if (total == 0) return;
@@ -1219,7 +1227,6 @@ __global__ void merge_stream_kernel(MergeArgs a) {
     for (int o = 16; o > 0; o >>= 1) added += __shfl_xor_sync(0xffffffffu, added, o);
     if (lane == 0) {
         a.sizes[i] = r;
-        if (a.thr) a.thr[i] = r == a.P ? R[a.P - 1] : kEmptyKey;
         if (added) atomicAdd(a.changes, (unsigned long long)added);
     }
 }
@@ -1330,10 +1337,10 @@ __global__ void spill_counts_kernel(const uint32_t* __restrict__ ocnt, uint32_t 
 // in ascending order (tiny inputs only).  One warp per deficient point.
 __global__ void fill_sparse_kernel(const float* __restrict__ x, uint32_t n, uint32_t ld, uint32_t P,
                                    uint32_t k, uint64_t* keys, uint8_t* flags, uint32_t* sizes,
-                                   unsigned long long* comps) {
+                                   unsigned long long* comps, uint32_t lo, uint32_t hi) {
     const uint32_t lane = lane_id();
-    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-    if (i >= n) return;
+    const uint32_t i = lo + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= hi) return;
     uint32_t sz = sizes[i];
     if (sz >= k) return;
     uint64_t* pk = keys + size_t(i) * P;
@@ -1404,6 +1411,74 @@ __global__ void split_keys_kernel(const uint64_t* __restrict__ keys, size_t cnt,
         const uint64_t k = keys[t];
         ids[t] = key_id(k);
         dists[t] = key_dist(k);
+    }
+}
+
+// ------------------------------------------------------------ shard mode
+
+__global__ void iota_kernel(uint32_t* __restrict__ out, uint32_t first, uint32_t count) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < count) out[t] = first + t;
+}
+struct InRange {
+    uint32_t lo, hi;
+    __host__ __device__ bool operator()(uint32_t v) const { return v >= lo && v < hi; }
+};
+
+// Offers held for targets [lo, lo+m): per-target counts (+ a trailing 0 for the scan).
+__global__ void offer_counts_kernel(const uint32_t* __restrict__ ocnt, uint32_t lo, uint32_t m,
+                                    uint32_t* __restrict__ out) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < m) out[t] = ocnt[lo + t];
+    if (t == m) out[m] = 0;
+}
+// Packs the offers of targets [lo, lo+m) target-major: fixed slots, then the
+// target's segment of the target-sorted spill list.  One warp per target.
+__global__ void offer_pack_kernel(const uint32_t* __restrict__ ocnt, const uint64_t* __restrict__ obuf,
+                                  uint32_t cap, const uint32_t* __restrict__ ov_off,
+                                  const uint64_t* __restrict__ ov_key, uint32_t lo, uint32_t m,
+                                  const uint32_t* __restrict__ off, uint64_t* __restrict__ out) {
+    const uint32_t lane = lane_id();
+    const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (t >= m) return;
+    const uint32_t tgt = lo + t, c = ocnt[tgt], fix = min(c, cap);
+    uint64_t* o = out + off[t];
+    for (uint32_t j = lane; j < fix; j += 32) o[j] = obuf[size_t(tgt) * cap + j];
+    if (c > fix) {
+        const uint64_t* sp = ov_key + ov_off[tgt];
+        for (uint32_t j = lane; j < c - fix; j += 32) o[fix + j] = sp[j];
+    }
+}
+// Appends received offers for targets [lo, lo+m) to their slots / the spill
+// list (merge order does not matter: the merge forms top-P of the union).
+__global__ void offer_add_kernel(uint32_t lo, uint32_t m, const uint32_t* __restrict__ cnt,
+                                 const uint32_t* __restrict__ off, const uint64_t* __restrict__ keys,
+                                 uint32_t* __restrict__ ocnt, uint64_t* __restrict__ obuf, uint32_t cap,
+                                 uint32_t* __restrict__ ov_cnt, uint32_t* __restrict__ ov_tgt,
+                                 uint64_t* __restrict__ ov_key) {
+    const uint32_t lane = lane_id();
+    const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (t >= m) return;
+    const uint32_t c = cnt[t];
+    if (c == 0) return;
+    const uint32_t tgt = lo + t;
+    uint32_t base = 0, o0 = 0;
+    if (lane == 0) {
+        base = atomicAdd(&ocnt[tgt], c);
+        const uint32_t nfix = base < cap ? min(c, cap - base) : 0u;
+        if (c > nfix) o0 = atomicAdd(ov_cnt, c - nfix);
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    o0 = __shfl_sync(0xffffffffu, o0, 0);
+    const uint32_t nfix = base < cap ? min(c, cap - base) : 0u;
+    const uint64_t* k = keys + off[t];
+    for (uint32_t j = lane; j < c; j += 32) {
+        if (j < nfix) {
+            obuf[size_t(tgt) * cap + base + j] = k[j];
+        } else {
+            ov_tgt[o0 + j - nfix] = tgt;
+            ov_key[o0 + j - nfix] = k[j];
+        }
     }
 }
 
@@ -1491,14 +1566,29 @@ void ensure_scratch(annk_state* s) {
     s->ocnt.alloc(n);
 }
 
-void do_rebuild(annk_state* s) {
+uint32_t own_lo(const annk_state* s) { return s->sharded ? s->lo : 0u; }
+uint32_t own_hi(const annk_state* s) { return s->sharded ? s->hi : s->n; }
+
+// graph_build.cpp:59-86 forward half: the owned points' pools are scanned and
+// their forward lists + start-of-round tails written.
+void do_sample(annk_state* s) {
+    ensure_scratch(s);
+    const uint32_t lo = own_lo(s), hi = own_hi(s);
+    SampleArgs a{hi, s->P, s->S, s->keys.p, s->flags.p, s->sizes.p, s->fnew.p, s->fold.p,
+                 s->cnew.p, s->cold.p, s->thr.p, lo};
+    if (hi > lo) LAUNCH(sample_kernel, grid_for(size_t(hi - lo) * 32, 256), 256, 0, a);
+    s->stage = 0;
+}
+
+// graph_build.cpp:59-86 reverse half, from the forward lists of ALL points
+// (in shard mode the other ranks' rows arrive through annk_state_rows first).
+void do_reverse(annk_state* s) {
     ensure_scratch(s);
     const uint32_t n = s->n;
     s->rn_cnt.zero();
     s->ro_cnt.zero();
-    SampleArgs a{n, s->P, s->S, s->keys.p, s->flags.p, s->sizes.p, s->fnew.p, s->fold.p,
-                 s->cnew.p, s->cold.p, s->rn_cnt.p, s->ro_cnt.p, s->thr.p};
-    LAUNCH(sample_kernel, grid_for(size_t(n) * 32, 256), 256, 0, a);
+    LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->S, s->fnew.p, s->cnew.p, s->rn_cnt.p);
+    LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->P, s->fold.p, s->cold.p, s->ro_cnt.p);
     exclusive_scan(s->rn_cnt.p, s->rn_off.p, n);
     exclusive_scan(s->ro_cnt.p, s->ro_off.p, n);
     s->rn_cur.zero();
@@ -1516,6 +1606,11 @@ void do_rebuild(annk_state* s) {
     segmented_sort(s->rn_data.p, tot[0], s->rn_off.p, n);
     segmented_sort(s->ro_data.p, tot[1], s->ro_off.p, n);
     s->stage = 1;
+}
+
+void do_rebuild(annk_state* s) {
+    do_sample(s);
+    do_reverse(s);
 }
 
 void do_union(annk_state* s) {
@@ -1544,26 +1639,27 @@ void do_union(annk_state* s) {
     s->stage = 2;
 }
 
-// One NN-descent join + merge round, split into `nsub` interleaved sub-rounds:
-// sub-round j joins the points whose visit order is j mod nsub, then merges
-// the offers into the pools and refreshes the thresholds.  Exact: merging is
-// associative (top-P(top-P(pool U A) U B) = top-P(pool U A U B), same flags),
-// and later sub-rounds filter offers against tighter tails, which cuts the
-// offer volume the merge has to process.
-uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
-    const uint32_t n = s->n;
-    // capacities learned by earlier rounds (any state) avoid redoing a join
-    static uint64_t spill_per_point_hint = 8;
-    static uint32_t offer_cap_hint = 0;
-    // per-point offer slots: sized from the offer volume seen so far, within a
-    // 12 GB budget (offers past the slots spill to a target-sorted global list)
+// per-point offer slots: sized from the offer volume seen so far, within a
+// 12 GB budget (offers past the slots spill to a target-sorted global list)
+uint32_t offer_cap_max(const annk_state* s) {
     const uint32_t cap_floor = std::max(2 * s->P, 64u);
     uint32_t cap_max = cap_floor;
-    while (uint64_t(cap_max) * 2 * n * 8 <= 12ull << 30 && cap_max < 4096) cap_max *= 2;
-    if (s->offer_cap == 0) s->offer_cap = std::min(cap_max, std::max(cap_floor, offer_cap_hint));
-    if (s->ov_cap == 0)
-        s->ov_cap = uint32_t(std::min<uint64_t>(std::max<uint64_t>(1u << 20, n * spill_per_point_hint), 1u << 31));
+    while (uint64_t(cap_max) * 2 * s->n * 8 <= 12ull << 30 && cap_max < 4096) cap_max *= 2;
+    return cap_max;
+}
+uint32_t g_offer_cap_hint = 0;          // capacities learned by earlier rounds (any state)
+uint64_t g_spill_per_point_hint = 8;
 
+// Join of the owned points (graph_build.cpp:105-162): every offer that beats its
+// target's start-of-round tail lands in the target's slots or the spill list;
+// pools are not touched.  Offers may target any point.
+void join_phase(annk_state* s, const annk_dataset* ds) {
+    if (s->stage != 2) throw_invalid("join: call union_reverse_lists first");
+    const uint32_t n = s->n;
+    const uint32_t cap_floor = std::max(2 * s->P, 64u), cap_max = offer_cap_max(s);
+    if (s->offer_cap == 0) s->offer_cap = std::min(cap_max, std::max(cap_floor, g_offer_cap_hint));
+    if (s->ov_cap == 0)
+        s->ov_cap = uint32_t(std::min<uint64_t>(std::max<uint64_t>(1u << 20, n * g_spill_per_point_hint), 1u << 31));
     const uint32_t rmax = 3 * s->S + s->P;  // |new| <= 2S, |old| <= P + S
     const size_t staged_smem = size_t(rmax) * (ds->ld + 4) * 4 + size_t(rmax) * 12 + (rmax / 4 + 2) * 4;
     const auto agg_smem = [&](bool u8, uint32_t ol) {
@@ -1574,119 +1670,163 @@ uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
     const uint32_t ol_u8 = 4096, ol_f32 = 2048;
     const bool agg_u8 = ds->u8 && agg_smem(true, ol_u8) <= 120 * 1024;
     const bool agg_f32 = !agg_u8 && agg_smem(false, ol_f32) <= 160 * 1024;
-    uint32_t nsub = 1;  // measured: sub-rounds cut offers <5% at cfg2, merge launches cost more
-    if (const char* e = getenv("ANNK_SUBROUNDS")) nsub = std::max(1, atoi(e));
-    if (!agg_u8 && !agg_f32) nsub = 1;
-
-    DevBuf<unsigned long long> counters(3);  // [comps, unused, offers] per attempt
-    DevBuf<uint32_t> ov_cnt(1);
-    unsigned long long comps = 0, offers = 0, spilled_total = 0;
-    for (uint32_t sub = 0; sub < nsub; ++sub) {
-        uint32_t spilled = 0;
-        for (;;) {
-            if (s->obuf.n != size_t(n) * s->offer_cap) s->obuf.alloc(size_t(n) * s->offer_cap);
-            if (s->ov_tgt.n != s->ov_cap) {
-                s->ov_tgt.alloc(s->ov_cap);
-                s->ov_key.alloc(s->ov_cap);
-            }
-            s->ocnt.zero();
-            counters.zero();
-            ov_cnt.zero();
-            JoinArgs ja{ds->data.p, n, ds->ld, s->P, s->S, s->offer_cap, s->gnew.p, s->gold.p, s->gncnt.p,
-                        s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p,
-                        ov_cnt.p, s->ov_tgt.p, s->ov_key.p, s->ov_cap, counters.p + 2, sub, nsub};
-            const uint32_t* order = s->order.n ? s->order.p : nullptr;
-            if (agg_u8 || agg_f32) {
-                const size_t sm = agg_smem(agg_u8, agg_u8 ? ol_u8 : ol_f32);
-                const void* fn = agg_u8 ? reinterpret_cast<const void*>(join_agg_kernel<true>)
-                                        : reinterpret_cast<const void*>(join_agg_kernel<false>);
-                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-                int per_sm = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinThreads, sm));
-                const uint32_t grid =
-                    std::min<uint32_t>((n + nsub - 1) / nsub, uint32_t(num_sms()) * std::max(per_sm, 1));
-                if (agg_u8)
-                    LAUNCH(join_agg_kernel<true>, grid, kJoinThreads, sm, ja, ds->data8.p, ds->ld8, ds->norms8.p,
-                           order, rmax, ol_u8);
-                else
-                    LAUNCH(join_agg_kernel<false>, grid, kJoinThreads, sm, ja, nullptr, 0u, nullptr, order, rmax,
-                           ol_f32);
-            } else if (staged_smem <= 110 * 1024) {
-                CK(cudaFuncSetAttribute(join_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(staged_smem)));
-                int per_sm = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_staged_kernel, kJoinThreads,
-                                                                 staged_smem));
-                const uint32_t grid = std::min<uint32_t>(n, uint32_t(num_sms()) * std::max(per_sm, 1));
-                LAUNCH(join_staged_kernel, grid, kJoinThreads, staged_smem, ja, order, rmax);
-            } else {
-                const uint32_t wpb = 8;
-                LAUNCH(join_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
-            }
-            ov_cnt.download(&spilled, 1);
-            ssync();
-            if (spilled <= s->ov_cap) break;
-            s->ov_cap = next_pow2(spilled);  // spill list too small: grow and redo (pools untouched so far)
-            spill_per_point_hint = std::max<uint64_t>(spill_per_point_hint, (uint64_t(s->ov_cap) + n - 1) / n);
+    // visit list: tree-0 leaf order (L2 locality), restricted to owned points
+    const uint32_t* order = s->sharded ? s->order_own.p : (s->order.n ? s->order.p : nullptr);
+    const uint32_t n_visit = own_hi(s) - own_lo(s);
+    DevBuf<unsigned long long> counters(3);  // [comps, unused, offers]
+    if (s->ov_count.n != 1) s->ov_count.alloc(1);
+    uint32_t spilled = 0;
+    for (;;) {
+        if (s->obuf.n != size_t(n) * s->offer_cap) s->obuf.alloc(size_t(n) * s->offer_cap);
+        if (s->ov_tgt.n != s->ov_cap) {
+            s->ov_tgt.alloc(s->ov_cap);
+            s->ov_key.alloc(s->ov_cap);
         }
-        unsigned long long cnt3[3] = {0, 0, 0};
-        CK(cudaMemcpyAsync(cnt3, counters.p, 24, cudaMemcpyDeviceToHost, stream()));
-        // group the spill list by target: offsets from per-target spill counts
-        DevBuf<uint32_t> ov_off(size_t(n) + 1);
-        DevBuf<uint64_t> ov_sorted_key;
-        if (spilled) {
-            DevBuf<uint32_t> counts(size_t(n) + 1);
-            LAUNCH(spill_counts_kernel, (n + 256) / 256, 256, 0, s->ocnt.p, n, s->offer_cap, counts.p);
-            exclusive_scan(counts.p, ov_off.p, n);
-            DevBuf<uint32_t> tgt_sorted(spilled);
-            ov_sorted_key.alloc(spilled);
-            int bits = 1;
-            while ((uint64_t(1) << bits) < n) ++bits;
-            size_t tmp = 0;
-            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p,
-                                               ov_sorted_key.p, spilled, 0, bits, stream()));
-            DevBuf<unsigned char> t(tmp);
-            prof_begin("cub_radix_sort_spill");
-            CK(cub::DeviceRadixSort::SortPairs(t.p, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, ov_sorted_key.p,
-                                               spilled, 0, bits, stream()));
-            prof_end();
-            note_launch();
+        s->ocnt.zero();
+        counters.zero();
+        s->ov_count.zero();
+        JoinArgs ja{ds->data.p, n_visit, ds->ld, s->P, s->S, s->offer_cap, s->gnew.p, s->gold.p, s->gncnt.p,
+                    s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p,
+                    s->ov_count.p, s->ov_tgt.p, s->ov_key.p, s->ov_cap, counters.p + 2, order};
+        if (n_visit == 0) {
+        } else if (agg_u8 || agg_f32) {
+            const size_t sm = agg_smem(agg_u8, agg_u8 ? ol_u8 : ol_f32);
+            const void* fn = agg_u8 ? reinterpret_cast<const void*>(join_agg_kernel<true>)
+                                    : reinterpret_cast<const void*>(join_agg_kernel<false>);
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinThreads, sm));
+            const uint32_t grid = std::min<uint32_t>(n_visit, uint32_t(num_sms()) * std::max(per_sm, 1));
+            if (agg_u8)
+                LAUNCH(join_agg_kernel<true>, grid, kJoinThreads, sm, ja, ds->data8.p, ds->ld8, ds->norms8.p,
+                       order, rmax, ol_u8);
+            else
+                LAUNCH(join_agg_kernel<false>, grid, kJoinThreads, sm, ja, nullptr, 0u, nullptr, order, rmax,
+                       ol_f32);
+        } else if (staged_smem <= 110 * 1024) {
+            CK(cudaFuncSetAttribute(join_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(staged_smem)));
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_staged_kernel, kJoinThreads,
+                                                             staged_smem));
+            const uint32_t grid = std::min<uint32_t>(n_visit, uint32_t(num_sms()) * std::max(per_sm, 1));
+            LAUNCH(join_staged_kernel, grid, kJoinThreads, staged_smem, ja, order, rmax);
+        } else {
+            const uint32_t wpb = 8;
+            LAUNCH(join_kernel, (n_visit + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
         }
-        MergeArgs ma{n, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p,
-                     ov_off.p, spilled ? ov_sorted_key.p : s->ov_key.p, counters.p + 1,
-                     sub + 1 < nsub ? s->thr.p : nullptr};
-        const size_t pw = ((size_t(kPend) + 3 * size_t(s->P)) * 8 + s->P + 15) & ~size_t(15);
-        const uint32_t wps = 8;
-        if (pw * wps > 48 * 1024)
-            CK(cudaFuncSetAttribute(merge_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(pw * wps)));
-        LAUNCH(merge_stream_kernel, (n + wps - 1) / wps, wps * 32, pw * wps, ma);
+        s->ov_count.download(&spilled, 1);
         ssync();
-        comps += cnt3[0];
-        offers += cnt3[2];
-        spilled_total += spilled;
+        if (spilled <= s->ov_cap) break;
+        s->ov_cap = next_pow2(spilled);  // spill list too small: grow and redo (pools untouched so far)
+        g_spill_per_point_hint = std::max<uint64_t>(g_spill_per_point_hint, (uint64_t(s->ov_cap) + n - 1) / n);
     }
-    // changes: entries inserted this round that survive (flag bit 1), bit cleared
-    DevBuf<unsigned long long> ch(1);
+    unsigned long long cnt3[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(cnt3, counters.p, 24, cudaMemcpyDeviceToHost, stream()));
+    ssync();
+    s->spilled = spilled;
+    s->spill_sorted = false;
+    s->pending_comps = cnt3[0];
+    s->last_offers = cnt3[2];
+    s->last_spilled = spilled;
+    s->pack_hi = s->pack_lo = 0;
+    s->stage = 3;
+}
+
+// Groups the spill list by target (stable radix sort) and derives per-target
+// offsets from the slot overflow counts.
+void group_spills(annk_state* s) {
+    const uint32_t n = s->n;
+    if (s->ov_off.n != size_t(n) + 1) s->ov_off.alloc(size_t(n) + 1);
+    if (s->spill_sorted) return;
+    if (s->spilled) {
+        DevBuf<uint32_t> counts(size_t(n) + 1);
+        LAUNCH(spill_counts_kernel, (n + 256) / 256, 256, 0, s->ocnt.p, n, s->offer_cap, counts.p);
+        exclusive_scan(counts.p, s->ov_off.p, n);
+        DevBuf<uint32_t> tgt_sorted(s->ov_cap);
+        DevBuf<uint64_t> key_sorted(s->ov_cap);
+        int bits = 1;
+        while ((uint64_t(1) << bits) < n) ++bits;
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, key_sorted.p,
+                                           s->spilled, 0, bits, stream()));
+        DevBuf<unsigned char> t(tmp);
+        prof_begin("cub_radix_sort_spill");
+        CK(cub::DeviceRadixSort::SortPairs(t.p, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, key_sorted.p,
+                                           s->spilled, 0, bits, stream()));
+        prof_end();
+        note_launch();
+        std::swap(s->ov_tgt, tgt_sorted);
+        std::swap(s->ov_key, key_sorted);
+    }
+    s->spill_sorted = true;
+}
+
+// Merge of the owned targets' offers into their pools, then `changes`.
+uint64_t merge_phase(annk_state* s) {
+    if (s->stage != 3) throw_invalid("merge: call join first");
+    const uint32_t n = s->n, lo = own_lo(s), hi = own_hi(s);
+    group_spills(s);
+    DevBuf<unsigned long long> ch(2);
     ch.zero();
-    const size_t cells = size_t(n) * s->P;
-    LAUNCH(count_inserted_kernel, uint32_t(std::min<size_t>((cells + 255) / 256, 16384)), 256, 0, s->flags.p,
-           cells, ch.p);
+    MergeArgs ma{hi, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p,
+                 s->ov_off.p, s->ov_key.p, ch.p + 1, lo};
+    const size_t pw = ((size_t(kPend) + 3 * size_t(s->P)) * 8 + s->P + 15) & ~size_t(15);
+    const uint32_t wps = 8;
+    if (pw * wps > 48 * 1024)
+        CK(cudaFuncSetAttribute(merge_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pw * wps)));
+    if (hi > lo) LAUNCH(merge_stream_kernel, (hi - lo + wps - 1) / wps, wps * 32, pw * wps, ma);
+    // changes: entries inserted this round that survive (flag bit 1), bit cleared
+    const size_t cells = size_t(hi - lo) * s->P;
+    if (cells)
+        LAUNCH(count_inserted_kernel, uint32_t(std::min<size_t>((cells + 255) / 256, 16384)), 256, 0,
+               s->flags.p + size_t(lo) * s->P, cells, ch.p);
     unsigned long long changes = 0;
     ch.download(&changes, 1);
     ssync();
-    s->last_offers = offers;
     {
-        const uint64_t want = std::max<uint64_t>(cap_floor, (offers / nsub / std::max(n, 1u)) * 5 / 4);
+        const uint32_t cap_floor = std::max(2 * s->P, 64u), cap_max = offer_cap_max(s);
+        const uint64_t want = std::max<uint64_t>(cap_floor, (s->last_offers / std::max(n, 1u)) * 5 / 4);
         const uint32_t next = std::min<uint32_t>(cap_max, next_pow2(uint32_t(std::min<uint64_t>(want, 1u << 20))));
-        offer_cap_hint = std::max(offer_cap_hint, next);
+        g_offer_cap_hint = std::max(g_offer_cap_hint, next);
         s->offer_cap = std::max(s->offer_cap, next);  // takes effect next round (buffers reallocated)
     }
-    s->last_spilled = spilled_total;
-    s->dist_comps += comps;
+    s->dist_comps += s->pending_comps;
+    s->pending_comps = 0;
     s->iteration += 1;
     s->last_changes = changes;
+    s->stage = 2;  // the round's lists stay inspectable (the reference keeps them)
     return changes;
+}
+
+uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
+    join_phase(s, ds);
+    return merge_phase(s);
+}
+
+// Owned visit order: tree-0 leaf order restricted to [lo, hi) (or lo..hi-1).
+void set_shard(annk_state* s, uint32_t lo, uint32_t hi) {
+    if (lo > hi || hi > s->n) throw_range("shard: range out of bounds");
+    s->lo = lo;
+    s->hi = hi;
+    s->sharded = !(lo == 0 && hi == s->n);
+    if (!s->sharded) {
+        s->order_own.release();
+        return;
+    }
+    s->order_own.alloc(std::max<size_t>(hi - lo, 1));
+    if (s->order.n == s->n) {
+        DevBuf<uint32_t> nsel(1);
+        size_t tmp = 0;
+        CK(cub::DeviceSelect::If(nullptr, tmp, s->order.p, s->order_own.p, nsel.p, s->n, InRange{lo, hi},
+                                 stream()));
+        DevBuf<unsigned char> t(std::max<size_t>(tmp, 1));
+        CK(cub::DeviceSelect::If(t.p, tmp, s->order.p, s->order_own.p, nsel.p, s->n, InRange{lo, hi}, stream()));
+        note_launch();
+    } else if (hi > lo) {
+        LAUNCH(iota_kernel, (hi - lo + 255) / 256, 256, 0, s->order_own.p, lo, hi - lo);
+    }
+    ssync();
 }
 
 annk_state* new_state(uint32_t n, uint32_t k, uint32_t P, uint32_t S, uint64_t seed) {
@@ -1712,52 +1852,217 @@ annk_state* new_state(uint32_t n, uint32_t k, uint32_t P, uint32_t S, uint64_t s
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+annk_state* init_graph_impl(const annk_dataset* ds, const annk_forest* fc, uint32_t k, uint32_t conquer_depth,
+                            uint32_t pool_cap, uint32_t sample_cap, uint64_t seed, uint32_t lo, uint32_t hi) {
+    if (!ds || !fc) throw_invalid("init_graph: null argument");
+    if (fc->n != ds->n || fc->dim != ds->dim) throw_invalid("init_graph: forest was built over different data");
+    annk_forest* f = const_cast<annk_forest*>(fc);
+    std::unique_ptr<annk_state> s(new_state(ds->n, k, pool_cap, sample_cap, seed));
+    forest_ensure_links(f);
+    uint32_t max_depth = 0;
+    for (const auto& t : f->trees) max_depth = std::max(max_depth, t.max_depth);
+    const uint32_t n = ds->n;
+    s->order.alloc(n);
+    CK(cudaMemcpyAsync(s->order.p, f->trees[0].pidx.p, size_t(n) * 4, cudaMemcpyDeviceToDevice, stream()));
+    set_shard(s.get(), lo, hi);
+    const uint32_t* visit = s->sharded ? s->order_own.p : s->order.p;
+    const uint32_t n_visit = hi - lo;
+    DevBuf<unsigned long long> comps(1);
+    comps.zero();
+    DevBuf<uint32_t> overflow(size_t(n) + 1);
+    CK(cudaMemsetAsync(overflow.p, 0, 4, stream()));
+    InitArgs a{ds->data.p, n, ds->ld, f->n_trees, conquer_depth, pool_cap, f->views.p,
+               s->keys.p, s->flags.p, s->sizes.p, comps.p, overflow.p,
+               ds->u8 ? ds->data8.p : nullptr, ds->ld8, ds->u8 ? ds->norms8.p : nullptr};
+    const uint32_t sib_full = f->n_trees * (max_depth + 1);
+    const uint32_t sib_cap = 0;  // sibling lists come from the forest (sib_list)
+    const size_t per_warp = init_warp_bytes(kInitCap, ds->ld, sib_cap);
+    const size_t smem = per_warp * kInitWarps;
+    CK(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, init_kernel, kInitWarps * 32, smem));
+    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((n_visit + kInitWarps - 1) / kInitWarps,
+                                                                    uint32_t(num_sms()) * std::max(per_sm, 1)));
+    s->sizes.zero();  // points outside the shard keep empty pools
+    if (n_visit) LAUNCH(init_kernel, grid, kInitWarps * 32, smem, a, sib_cap, visit, n_visit);
+    uint32_t n_over = 0;
+    overflow.download(&n_over, 1);
+    ssync();
+    if (n_over) {
+        const uint32_t cap = next_pow2(f->n_trees * (max_depth + 1) * f->leaf_cap);
+        const uint32_t blocks = std::min<uint32_t>(n_over, 1024);
+        DevBuf<uint32_t> gscratch(size_t(blocks) * (3 * size_t(cap) + 2 * sib_full));
+        DevBuf<float> gq(size_t(blocks) * ds->ld);
+        LAUNCH(init_overflow_kernel, blocks, 32, 0, a, overflow.p + 1, n_over, cap, sib_full, gscratch.p, gq.p);
+    }
+    unsigned long long c = 0;
+    comps.download(&c, 1);
+    ssync();
+    s->dist_comps = c;
+    return s.release();
+}
+}  // namespace
+
+extern "C" {
+
 int annk_init_graph(const annk_dataset* ds, const annk_forest* fc, uint32_t k, uint32_t conquer_depth,
                     uint32_t pool_cap, uint32_t sample_cap, uint64_t seed, annk_state** out) {
     return abi([&] {
-        if (!ds || !fc || !out) throw_invalid("init_graph: null argument");
-        if (fc->n != ds->n || fc->dim != ds->dim)
-            throw_invalid("init_graph: forest was built over different data");
-        annk_forest* f = const_cast<annk_forest*>(fc);
-        std::unique_ptr<annk_state> s(new_state(ds->n, k, pool_cap, sample_cap, seed));
-        forest_ensure_links(f);
-        uint32_t max_depth = 0;
-        for (const auto& t : f->trees) max_depth = std::max(max_depth, t.max_depth);
-        const uint32_t n = ds->n;
-        DevBuf<unsigned long long> comps(1);
-        comps.zero();
-        DevBuf<uint32_t> overflow(size_t(n) + 1);
-        CK(cudaMemsetAsync(overflow.p, 0, 4, stream()));
-        InitArgs a{ds->data.p, n, ds->ld, f->n_trees, conquer_depth, pool_cap, f->views.p,
-                   s->keys.p, s->flags.p, s->sizes.p, comps.p, overflow.p,
-                   ds->u8 ? ds->data8.p : nullptr, ds->ld8, ds->u8 ? ds->norms8.p : nullptr};
-        const uint32_t sib_full = f->n_trees * (max_depth + 1);
-        const uint32_t sib_cap = 0;  // sibling lists come from the forest (sib_list)
-        const size_t per_warp = init_warp_bytes(kInitCap, ds->ld, sib_cap);
-        const size_t smem = per_warp * kInitWarps;
-        CK(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, init_kernel, kInitWarps * 32, smem));
-        const uint32_t grid = std::min<uint32_t>((n + kInitWarps - 1) / kInitWarps,
-                                                 uint32_t(num_sms()) * std::max(per_sm, 1));
-        s->order.alloc(n);
-        CK(cudaMemcpyAsync(s->order.p, f->trees[0].pidx.p, size_t(n) * 4, cudaMemcpyDeviceToDevice, stream()));
-        LAUNCH(init_kernel, grid, kInitWarps * 32, smem, a, sib_cap, s->order.p);
-        uint32_t n_over = 0;
-        overflow.download(&n_over, 1);
-        ssync();
-        if (n_over) {
-            const uint32_t cap = next_pow2(f->n_trees * (max_depth + 1) * f->leaf_cap);
-            const uint32_t blocks = std::min<uint32_t>(n_over, 1024);
-            DevBuf<uint32_t> gscratch(size_t(blocks) * (3 * size_t(cap) + 2 * sib_full));
-            DevBuf<float> gq(size_t(blocks) * ds->ld);
-            LAUNCH(init_overflow_kernel, blocks, 32, 0, a, overflow.p + 1, n_over, cap, sib_full, gscratch.p, gq.p);
+        if (!ds || !out) throw_invalid("init_graph: null argument");
+        *out = init_graph_impl(ds, fc, k, conquer_depth, pool_cap, sample_cap, seed, 0, ds->n);
+    });
+}
+
+int annk_init_graph_shard(const annk_dataset* ds, const annk_forest* fc, uint32_t k, uint32_t conquer_depth,
+                          uint32_t pool_cap, uint32_t sample_cap, uint64_t seed, uint32_t lo, uint32_t hi,
+                          annk_state** out) {
+    return abi([&] {
+        if (!ds || !out) throw_invalid("init_graph: null argument");
+        if (lo > hi || hi > ds->n) throw_range("init_graph: shard range out of bounds");
+        *out = init_graph_impl(ds, fc, k, conquer_depth, pool_cap, sample_cap, seed, lo, hi);
+    });
+}
+
+int annk_state_set_shard(annk_state* s, uint32_t lo, uint32_t hi) {
+    return abi([&] {
+        if (!s) throw_invalid("set_shard: null state");
+        set_shard(s, lo, hi);
+    });
+}
+
+int annk_state_rows(annk_state* s, int which, int put, uint32_t lo, uint32_t hi, void* buf) {
+    return abi([&] {
+        if (!s || (!buf && hi > lo)) throw_invalid("state_rows: null argument");
+        if (lo > hi || hi > s->n) throw_range("state_rows: row range out of bounds");
+        ensure_scratch(s);
+        char* dev;
+        size_t row_bytes;
+        switch (which) {
+            case ANNK_ROWS_FNEW: dev = reinterpret_cast<char*>(s->fnew.p); row_bytes = size_t(s->S) * 4; break;
+            case ANNK_ROWS_CNEW: dev = reinterpret_cast<char*>(s->cnew.p); row_bytes = 4; break;
+            case ANNK_ROWS_FOLD: dev = reinterpret_cast<char*>(s->fold.p); row_bytes = size_t(s->P) * 4; break;
+            case ANNK_ROWS_COLD: dev = reinterpret_cast<char*>(s->cold.p); row_bytes = 4; break;
+            case ANNK_ROWS_THR: dev = reinterpret_cast<char*>(s->thr.p); row_bytes = 8; break;
+            default: throw_invalid("state_rows: unknown row buffer");
         }
-        unsigned long long c = 0;
-        comps.download(&c, 1);
+        const size_t bytes = size_t(hi - lo) * row_bytes;
+        char* d = dev + size_t(lo) * row_bytes;
+        if (bytes) CK(cudaMemcpyAsync(put ? d : buf, put ? buf : d, bytes, cudaMemcpyDefault, stream()));
         ssync();
-        s->dist_comps = c;
-        *out = s.release();
+    });
+}
+
+int annk_shard_sample(annk_state* s) {
+    return abi([&] { do_sample(s); });
+}
+
+int annk_shard_union(annk_state* s) {
+    return abi([&] {
+        do_reverse(s);
+        do_union(s);
+    });
+}
+
+int annk_shard_join(annk_state* s, const annk_dataset* ds, uint64_t* comps) {
+    return abi([&] {
+        if (!s || !ds || ds->n != s->n) throw_invalid("join: state/dataset mismatch");
+        join_phase(s, ds);
+        if (comps) *comps = s->pending_comps;
+    });
+}
+
+int annk_shard_offers_count(annk_state* s, uint32_t lo, uint32_t hi, uint64_t* total) {
+    return abi([&] {
+        if (!s || !total) throw_invalid("offers_count: null argument");
+        if (s->stage != 3) throw_invalid("offers_count: call join first");
+        if (lo > hi || hi > s->n) throw_range("offers_count: target range out of bounds");
+        group_spills(s);
+        const uint32_t m = hi - lo;
+        s->pack_cnt.alloc(size_t(m) + 1);
+        s->pack_off.alloc(size_t(m) + 1);
+        LAUNCH(offer_counts_kernel, (m + 1 + 255) / 256, 256, 0, s->ocnt.p, lo, m, s->pack_cnt.p);
+        exclusive_scan(s->pack_cnt.p, s->pack_off.p, m);
+        uint32_t t = 0;
+        CK(cudaMemcpyAsync(&t, s->pack_off.p + m, 4, cudaMemcpyDeviceToHost, stream()));
+        ssync();
+        s->pack_lo = lo;
+        s->pack_hi = hi;
+        *total = t;
+    });
+}
+
+int annk_shard_offers_pack(annk_state* s, uint32_t lo, uint32_t hi, uint32_t* counts, uint64_t* keys) {
+    return abi([&] {
+        if (!s) throw_invalid("offers_pack: null state");
+        if (s->stage != 3 || s->pack_lo != lo || s->pack_hi != hi || s->pack_cnt.n != size_t(hi - lo) + 1)
+            throw_invalid("offers_pack: call offers_count for the same range first");
+        const uint32_t m = hi - lo;
+        uint32_t total = 0;
+        CK(cudaMemcpyAsync(&total, s->pack_off.p + m, 4, cudaMemcpyDeviceToHost, stream()));
+        ssync();
+        DevBuf<uint64_t> out(std::max<uint32_t>(total, 1));
+        if (m)
+            LAUNCH(offer_pack_kernel, grid_for(size_t(m) * 32, 256), 256, 0, s->ocnt.p, s->obuf.p, s->offer_cap,
+                   s->ov_off.p, s->ov_key.p, lo, m, s->pack_off.p, out.p);
+        if (counts && m) CK(cudaMemcpyAsync(counts, s->pack_cnt.p, size_t(m) * 4, cudaMemcpyDefault, stream()));
+        if (keys && total) CK(cudaMemcpyAsync(keys, out.p, size_t(total) * 8, cudaMemcpyDefault, stream()));
+        ssync();
+    });
+}
+
+int annk_shard_offers_add(annk_state* s, uint32_t lo, uint32_t hi, const uint32_t* counts, const uint64_t* keys) {
+    return abi([&] {
+        if (!s || (!counts && hi > lo)) throw_invalid("offers_add: null argument");
+        if (s->stage != 3) throw_invalid("offers_add: call join first");
+        if (lo < own_lo(s) || hi > own_hi(s) || lo > hi) throw_range("offers_add: targets outside the shard");
+        const uint32_t m = hi - lo;
+        if (m == 0) return;
+        DevBuf<uint32_t> cnt(size_t(m) + 1), off(size_t(m) + 1);
+        CK(cudaMemcpyAsync(cnt.p, counts, size_t(m) * 4, cudaMemcpyDefault, stream()));
+        CK(cudaMemsetAsync(cnt.p + m, 0, 4, stream()));
+        exclusive_scan(cnt.p, off.p, m);
+        uint32_t total = 0;
+        CK(cudaMemcpyAsync(&total, off.p + m, 4, cudaMemcpyDeviceToHost, stream()));
+        ssync();
+        if (total == 0) return;
+        if (!keys) throw_invalid("offers_add: null keys");
+        DevBuf<uint64_t> k(total);
+        CK(cudaMemcpyAsync(k.p, keys, size_t(total) * 8, cudaMemcpyDefault, stream()));
+        // room for the worst case (every received offer spills); keep what is there
+        const uint64_t need = uint64_t(s->spilled) + total;
+        if (need > s->ov_cap) {
+            const uint32_t cap = uint32_t(std::min<uint64_t>(next_pow2(uint32_t(std::min<uint64_t>(need, 1u << 31))),
+                                                             1u << 31));
+            DevBuf<uint32_t> t2(cap);
+            DevBuf<uint64_t> k2(cap);
+            if (s->spilled) {
+                CK(cudaMemcpyAsync(t2.p, s->ov_tgt.p, size_t(s->spilled) * 4, cudaMemcpyDeviceToDevice, stream()));
+                CK(cudaMemcpyAsync(k2.p, s->ov_key.p, size_t(s->spilled) * 8, cudaMemcpyDeviceToDevice, stream()));
+            }
+            std::swap(s->ov_tgt, t2);
+            std::swap(s->ov_key, k2);
+            s->ov_cap = cap;
+        }
+        CK(cudaMemcpyAsync(s->ov_count.p, &s->spilled, 4, cudaMemcpyHostToDevice, stream()));
+        LAUNCH(offer_add_kernel, grid_for(size_t(m) * 32, 256), 256, 0, lo, m, cnt.p, off.p, k.p, s->ocnt.p,
+               s->obuf.p, s->offer_cap, s->ov_count.p, s->ov_tgt.p, s->ov_key.p);
+        uint32_t sp = 0;
+        s->ov_count.download(&sp, 1);
+        ssync();
+        s->spilled = sp;
+        s->last_spilled = sp;
+        s->spill_sorted = false;
+        s->pack_lo = s->pack_hi = 0;
+    });
+}
+
+int annk_shard_merge(annk_state* s, uint64_t* changes) {
+    return abi([&] {
+        const uint64_t c = merge_phase(s);
+        if (changes) *changes = c;
     });
 }
 
@@ -1840,10 +2145,10 @@ int annk_state_lists(const annk_state* s, int which, uint32_t* offsets, uint32_t
             return;
         }
         if (which == 0) {
-            if (s->stage == 2) csr_from_rows(s->gnew, 2 * s->S, s->gncnt, n, offsets, data);
+            if (s->stage >= 2) csr_from_rows(s->gnew, 2 * s->S, s->gncnt, n, offsets, data);
             else csr_from_rows(s->fnew, s->S, s->cnew, n, offsets, data);
         } else if (which == 1) {
-            if (s->stage == 2) csr_from_rows(s->gold, s->P + s->S, s->gocnt, n, offsets, data);
+            if (s->stage >= 2) csr_from_rows(s->gold, s->P + s->S, s->gocnt, n, offsets, data);
             else csr_from_rows(s->fold, s->P, s->cold, n, offsets, data);
         } else {
             const DevBuf<uint32_t>& off = which == 2 ? s->rn_off : s->ro_off;
@@ -1897,17 +2202,21 @@ int annk_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* i
         if (n < 2 || n - 1 < k) throw_invalid("finalize: need n-1 >= k");
         if (k > s->P) throw_invalid("finalize: k exceeds pool capacity");
         if (!ds || ds->n != n) throw_invalid("finalize: dataset mismatch");
+        // shard mode: rows [lo, hi) only, written as (hi - lo) x k
+        const uint32_t lo = own_lo(s), m = own_hi(s) - lo;
         DevBuf<unsigned long long> comps(1);
         comps.zero();
-        LAUNCH(fill_sparse_kernel, grid_for(size_t(n) * 32, 256), 256, 0, ds->data.p, n, ds->ld, s->P, k,
-               s->keys.p, s->flags.p, s->sizes.p, comps.p);
-        DevBuf<uint32_t> di(size_t(n) * k);
-        DevBuf<float> dd(size_t(n) * k);
-        LAUNCH(finalize_kernel, grid_for(size_t(n) * k, 256), 256, 0, s->keys.p, n, s->P, k, di.p, dd.p);
+        const size_t pk = size_t(lo) * s->P;
+        if (m)
+            LAUNCH(fill_sparse_kernel, grid_for(size_t(m) * 32, 256), 256, 0, ds->data.p, n, ds->ld, s->P, k,
+                   s->keys.p, s->flags.p, s->sizes.p, comps.p, lo, lo + m);
+        DevBuf<uint32_t> di(size_t(m) * k);
+        DevBuf<float> dd(size_t(m) * k);
+        if (m) LAUNCH(finalize_kernel, grid_for(size_t(m) * k, 256), 256, 0, s->keys.p + pk, m, s->P, k, di.p, dd.p);
         unsigned long long c = 0;
         comps.download(&c, 1);
-        if (ids) di.download(ids, size_t(n) * k);
-        if (dists) dd.download(dists, size_t(n) * k);
+        if (ids) CK(cudaMemcpyAsync(ids, di.p, size_t(m) * k * 4, cudaMemcpyDefault, stream()));
+        if (dists) CK(cudaMemcpyAsync(dists, dd.p, size_t(m) * k * 4, cudaMemcpyDefault, stream()));
         ssync();
         s->dist_comps += c;
     });

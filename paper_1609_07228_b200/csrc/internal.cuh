@@ -103,6 +103,20 @@ struct annk_state {
     uint64_t join_rows = 0;
     uint32_t offer_cap = 0;
     uint64_t last_offers = 0, last_spilled = 0;
+    // join -> merge hand-off (offers stay on device between the phases)
+    annk::DevBuf<uint32_t> ov_count;   // spill list fill (1)
+    annk::DevBuf<uint32_t> ov_off;     // per-target start in the target-sorted spill list (n + 1)
+    uint32_t spilled = 0;
+    bool spill_sorted = false;
+    uint64_t pending_comps = 0;
+    // shard mode (multi-GPU): this state owns points [lo, hi); init / sample /
+    // join / merge / finalize touch only those, lists and thresholds of the
+    // other points arrive through annk_state_rows
+    uint32_t lo = 0, hi = 0;
+    bool sharded = false;
+    annk::DevBuf<uint32_t> order_own;  // visit order restricted to [lo, hi)
+    annk::DevBuf<uint32_t> pack_cnt, pack_off;
+    uint32_t pack_lo = 0, pack_hi = 0;
 };
 
 struct annk_searcher {
