@@ -133,8 +133,9 @@ def dist_setup(args):
     if ws > 1:
         import torch
         import torch.distributed as dist
-        backend = "nccl" if args.impl != "reference" and torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
+        backend = "nccl" if args.impl != "reference" and torch.cuda.is_available() and args.comm == "nccl" else "gloo"
+        if torch.cuda.is_available() and args.impl != "reference":
+            local = local % torch.cuda.device_count()  # --comm gloo may stack ranks on one GPU (functional runs)
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return ws, rank, local
@@ -446,6 +447,171 @@ def run_gpu(args, cfg, ws, rank, local):
         print(json.dumps(line))
 
 
+# ------------------------------------------------------- multi-GPU arm
+
+def run_gpu_sharded(args, cfg, ws, rank, local):
+    """N > 1: point-sharded build (paper_1609_07228_b200/sharded.py).
+    Strong scaling: the cfg's N points are split across the ranks; init, sampling,
+    the join (as visiting point) and the merge (as target) run on the owning rank,
+    forward lists / thresholds are all-gathered and offers routed all-to-all over
+    NCCL each round.  Forest and dataset are replicated.  Search and ground truth
+    are sharded by query rows.  Times are CUDA events, max over ranks."""
+    import torch
+
+    import paper_1609_07228_b200 as A
+    from paper_1609_07228_b200 import sharded as SH
+    A.lib.annk_set_device(local)
+    bufdev = "cuda" if args.comm == "nccl" else "cpu"
+    comm = SH.TorchComm(bufdev)
+    ext = torch.cuda.ExternalStream(A.stream_handle(), device=torch.device("cuda", local))
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(ext)
+        return e
+
+    base, queries = gen_data(cfg)
+    vs, qs_all = A.VectorSet(base), queries
+    n, dim, k, kr = cfg["n"], cfg["dim"], cfg["k"], cfg["k_return"]
+    lo, hi = SH.shard_ranges(n, ws)[rank]
+    qlo, qhi = SH.shard_ranges(cfg["n_queries"], ws)[rank]
+    qs = A.VectorSet(np.ascontiguousarray(qs_all[qlo:qhi]))
+
+    e0 = ev()
+    forest = A.build_forest(vs, cfg["trees"], cfg["leaf"], SEED)
+    e1 = ev()
+    torch.cuda.synchronize()
+    forest_s = max_over_ranks(ws, e0.elapsed_time(e1) / 1e3)
+
+    rows = sample_rows(n, cfg["acc_sample"])
+    rows = rows[(rows >= lo) & (rows < hi)]
+    gt_rows = A.brute_force_rows(vs, rows, k)
+    gt_q = A.brute_force_knn(vs, qs, kr)
+
+    def shard():
+        return SH.DeviceShard(vs, forest, k, cfg["dep"], cfg["P"], cfg["S"], SEED, lo, hi, buffer_device=bufdev)
+
+    # calibration: accuracy per round -> crossing round
+    e = shard()
+    accs = [SH.sharded_accuracy(e, comm, gt_rows, rows)]
+    comps = [comm.allreduce_sum(e.dist_comps())]
+    crossing = None
+    for it in range(cfg["max_iters"]):
+        _, c = SH.nn_descent_round(e, comm)
+        comps.append(comps[-1] + c)
+        accs.append(SH.sharded_accuracy(e, comm, gt_rows, rows))
+        if crossing is None and accs[-1] >= 0.9:
+            crossing = it + 1
+            if not args.full_log:
+                break
+    crossing = crossing or cfg["max_iters"]
+    del e
+
+    def build_once():
+        e = shard()
+        for _ in range(crossing):
+            SH.nn_descent_round(e, comm)
+        return e
+
+    for _ in range(args.warmup):
+        build_once()
+    torch.cuda.synchronize()
+    A.profile_reset()
+    A.profile_enable(True)
+    launches0 = A.launch_count()
+    barrier(ws)
+    e = None
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0 = ev()
+        for _ in range(args.steps):
+            e = None
+            e = build_once()
+        e1 = ev()
+        torch.cuda.synchronize()
+    barrier(ws)
+    launches = A.launch_count() - launches0
+    A.profile_enable(False)
+    prof = A.profile_report()
+    step_s = max_over_ranks(ws, e0.elapsed_time(e1) / 1e3 / args.steps)
+    final_acc = SH.sharded_accuracy(e, comm, gt_rows, rows)
+    graph = SH.allgather_graph(e.finalize(), comm)
+    del e
+
+    # search: every rank holds the full index and answers its query shard
+    searcher = A.GraphSearcher(vs, forest, graph)
+    sweep, chosen = [], None
+    for P in cfg["sweep"]:
+        p = A.SearchParams(k_return=kr, pool_size=P, expansion=P, iters=4)
+        searcher.search_batch(qs, p)
+        barrier(ws)
+        e0 = ev()
+        r = searcher.search_batch(qs, p)
+        e1 = ev()
+        torch.cuda.synchronize()
+        dt = max_over_ranks(ws, e0.elapsed_time(e1) / 1e3)
+        hits = sum(len(np.intersect1d(r.ids[i], gt_q[i])) for i in range(len(gt_q)))
+        rec = comm.allreduce_sum(hits) / (cfg["n_queries"] * kr)
+        row = {"pool": P, "expansion": P, "recall": round(rec, 4), "qps": round(cfg["n_queries"] / dt, 1)}
+        sweep.append(row)
+        if chosen is None and rec >= 0.9:
+            chosen = row
+            if not args.full_log:
+                break
+
+    # e2e: host dataset in, own graph rows out, per rank
+    pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = base
+    host = pinned.numpy()
+    e2e_times = []
+    for i in range(max(1, args.e2e_steps) + 1):
+        torch.cuda.synchronize()
+        barrier(ws)
+        t1 = time.perf_counter()
+        v2 = A.VectorSet(host)
+        f2 = A.build_forest(v2, cfg["trees"], cfg["leaf"], SEED)
+        e2 = SH.DeviceShard(v2, f2, k, cfg["dep"], cfg["P"], cfg["S"], SEED, lo, hi, buffer_device=bufdev)
+        for _ in range(crossing):
+            SH.nn_descent_round(e2, comm)
+        g2 = e2.finalize()
+        t2 = time.perf_counter()
+        if i > 0:
+            e2e_times.append(t2 - t1)
+        del v2, f2, e2
+    assert np.array_equal(g2.ids, graph.ids[lo:hi]), "e2e graph differs from the device-resident build"
+    e2e_s = max_over_ranks(ws, statistics.mean(e2e_times))
+
+    dsinfo = vs.info()
+    line = {
+        "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u8" if dsinfo["u8"] else "f32", "data": "synthetic",
+        "config": {"workload": args.config, "n": n, "dim": dim, "trees": cfg["trees"], "leaf_cap": cfg["leaf"],
+                   "k": k, "pool_cap": cfg["P"], "sample_cap": cfg["S"], "conquer_depth": cfg["dep"],
+                   "iterations_to_acc_0.9": crossing, "accuracy_sample_rows": cfg["acc_sample"],
+                   "l2": "inputs larger than L2 (512 MB dataset)",
+                   "parallelism": f"point-sharded build x{ws} (NCCL all-gather + all-to-all per round), "
+                                  f"query-sharded search"},
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(ws * n * dim * 4),
+                "d2h_bytes_per_step": int(n * k * 8),
+                "includes": "per rank: H2D dataset, forest build, sharded init + rounds, finalize, D2H own rows"},
+        "gpu_launches": int(launches),
+        "roofline": None,
+        "cpu_baseline": None,
+        "clocks": clk.summary(),
+        "search_qps_at_recall_0.9": chosen["qps"] if chosen else None,
+        "search": {"k_return": kr, "n_queries": cfg["n_queries"], "chosen": chosen, "sweep": sweep},
+        "accuracy": {"per_iteration": [round(a, 4) for a in accs], "final_sample": round(final_acc, 4),
+                     "dist_comps": comps},
+        "aux_seconds": {"forest": forest_s},
+        "kernels_ms_rank0": {k2: round(v2[1], 3) for k2, v2 in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+    }
+    if rank == 0:
+        print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -456,12 +622,16 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--full-log", action="store_true", help="run all iterations / sweep points")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 collectives; gloo keeps buffers on the host (functional runs on one GPU)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     cfg.setdefault("ref_iters", {"cfg2": 2, "cfg1": 3, "tiny": 3}[args.config])
     ws, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, cfg, ws, rank)
+    elif ws > 1:
+        run_gpu_sharded(args, cfg, ws, rank, local)
     else:
         run_gpu(args, cfg, ws, rank, local)
     if ws > 1:

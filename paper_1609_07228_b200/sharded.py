@@ -125,6 +125,12 @@ class TorchComm:
         self.dist.all_reduce(t)
         return int(t.item())
 
+    def allreduce_sumf(self, v: float) -> float:
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64, device=self.device)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
     def barrier(self):
         self.dist.barrier()
 
@@ -158,6 +164,9 @@ class ThreadComm:
 
     def allreduce_sum(self, v: int) -> int:
         return int(sum(self._exchange(int(v))))
+
+    def allreduce_sumf(self, v: float) -> float:
+        return float(sum(self._exchange(float(v))))
 
     def barrier(self):
         self._exchange(None)
@@ -279,6 +288,33 @@ class DeviceShard:
         with _LIB_LOCK:
             p = self.state.pools()
         return tuple(v[self.lo:self.hi] for v in p)
+
+    def accuracy_sum(self, gt_rows: np.ndarray, rows: np.ndarray) -> tuple:
+        """graph_build.cpp:209-226 over the owned sample rows: (sum of per-row
+        scores, row count); the driver all-reduces both."""
+        sel = (rows >= self.lo) & (rows < self.hi)
+        m = int(sel.sum())
+        if m == 0:
+            return 0.0, 0
+        with _LIB_LOCK:
+            acc = api.detail.pool_topk_accuracy(self.state, gt_rows[sel], rows[sel])
+        return acc * m, m
+
+
+def sharded_accuracy(e, comm, gt_rows, rows) -> float:
+    s, m = e.accuracy_sum(gt_rows, rows)
+    return comm.allreduce_sumf(s) / max(comm.allreduce_sum(m), 1)
+
+
+def allgather_graph(g: api.KnnGraph, comm) -> api.KnnGraph:
+    """Full graph on every rank from the ranks' finalized rows."""
+    import torch
+    ids = torch.from_numpy(g.ids.view(np.int32)).to(comm.device)
+    d = torch.from_numpy(g.dists).to(comm.device)
+    all_ids = comm.allgather(ids)
+    all_d = comm.allgather(d)
+    return api.KnnGraph(np.ascontiguousarray(torch.cat(all_ids).cpu().numpy().view(np.uint32)),
+                        np.ascontiguousarray(torch.cat(all_d).cpu().numpy()))
 
 
 # --------------------------------------------------------------- protocol
