@@ -509,24 +509,31 @@ __global__ void sample_kernel(SampleArgs a) {
 }
 
 // Reverse-list sizes from the forward lists of all points.
+// Only targets in [tlo, thi) are counted (shard mode: the owned points).
 __global__ void rev_count_kernel(uint32_t n, uint32_t width, const uint32_t* __restrict__ fwd,
-                                 const uint32_t* __restrict__ cnt, uint32_t* __restrict__ out) {
-    const uint32_t lane = lane_id();
-    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-    if (i >= n) return;
-    const uint32_t c = cnt[i];
-    for (uint32_t j = lane; j < c; j += 32) atomicAdd(&out[fwd[size_t(i) * width + j]], 1u);
-}
-
-__global__ void reverse_scatter_kernel(uint32_t n, uint32_t width, const uint32_t* __restrict__ fwd,
-                                       const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
-                                       uint32_t* __restrict__ cursor, uint32_t* __restrict__ data) {
+                                 const uint32_t* __restrict__ cnt, uint32_t* __restrict__ out, uint32_t tlo,
+                                 uint32_t thi) {
     const uint32_t lane = lane_id();
     const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (i >= n) return;
     const uint32_t c = cnt[i];
     for (uint32_t j = lane; j < c; j += 32) {
         const uint32_t id = fwd[size_t(i) * width + j];
+        if (id >= tlo && id < thi) atomicAdd(&out[id], 1u);
+    }
+}
+
+__global__ void reverse_scatter_kernel(uint32_t n, uint32_t width, const uint32_t* __restrict__ fwd,
+                                       const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                                       uint32_t* __restrict__ cursor, uint32_t* __restrict__ data, uint32_t tlo,
+                                       uint32_t thi) {
+    const uint32_t lane = lane_id();
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= n) return;
+    const uint32_t c = cnt[i];
+    for (uint32_t j = lane; j < c; j += 32) {
+        const uint32_t id = fwd[size_t(i) * width + j];
+        if (id < tlo || id >= thi) continue;
         const uint32_t pos = atomicAdd(&cursor[id], 1u);
         data[off[id] + pos] = i;
     }
@@ -543,6 +550,7 @@ struct UnionArgs {
     uint32_t* gocnt;
     unsigned long long* join_rows;
     const uint32_t* samp;  // n x 2 x S sampled reverse lists (rev_sample_kernel), used when longer than S
+    uint32_t lo;           // points [lo, n) are unioned
 };
 
 // graph_build.cpp:38-48 sample_down for every reverse list longer than S, one
@@ -554,15 +562,15 @@ struct UnionArgs {
 // live in a small per-thread overlay in shared memory.
 __global__ void rev_sample_kernel(uint32_t n, uint32_t S, uint64_t round_seed, const uint32_t* __restrict__ rn_off,
                                   const uint32_t* __restrict__ rn_data, const uint32_t* __restrict__ ro_off,
-                                  const uint32_t* __restrict__ ro_data, uint32_t* __restrict__ samp) {
+                                  const uint32_t* __restrict__ ro_data, uint32_t* __restrict__ samp, uint32_t lo) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     const size_t per = size_t(S + 1) * 8 + size_t(4 * S) * 4;
     uint64_t* xs = reinterpret_cast<uint64_t*>(smem + threadIdx.x * per);
     uint32_t* pos = reinterpret_cast<uint32_t*>(xs + S + 1);
     uint32_t* val = pos + 2 * S;
-    if (t >= 2 * n) return;
-    const uint32_t i = t >> 1, kind = t & 1;
+    if (t >= 2 * (n - lo)) return;
+    const uint32_t i = lo + (t >> 1), kind = t & 1;
     const uint32_t* off = kind ? ro_off : rn_off;
     const uint32_t* data = kind ? ro_data : rn_data;
     const uint32_t b = off[i], m = off[i + 1] - b;
@@ -608,7 +616,7 @@ __global__ void union_kernel(UnionArgs a, uint32_t m_new, uint32_t m_old) {
     const uint32_t wpb = blockDim.x / 32;
     uint32_t* sn = reinterpret_cast<uint32_t*>(smem) + warp * (m_new + m_old);
     uint32_t* so = sn + m_new;
-    const uint32_t i = blockIdx.x * wpb + warp;
+    const uint32_t i = a.lo + blockIdx.x * wpb + warp;
     if (i >= a.n) return;
     const uint32_t cn = a.cnew[i], co = a.cold[i];
     for (uint32_t j = lane; j < cn; j += 32) sn[j] = a.fnew[size_t(i) * a.S + j];
@@ -1587,16 +1595,20 @@ void do_reverse(annk_state* s) {
     const uint32_t n = s->n;
     s->rn_cnt.zero();
     s->ro_cnt.zero();
-    LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->S, s->fnew.p, s->cnew.p, s->rn_cnt.p);
-    LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->P, s->fold.p, s->cold.p, s->ro_cnt.p);
+    // reverse lists are needed for the owned points only (all of them unsharded)
+    const uint32_t tlo = own_lo(s), thi = own_hi(s);
+    LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->S, s->fnew.p, s->cnew.p, s->rn_cnt.p,
+           tlo, thi);
+    LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->P, s->fold.p, s->cold.p, s->ro_cnt.p,
+           tlo, thi);
     exclusive_scan(s->rn_cnt.p, s->rn_off.p, n);
     exclusive_scan(s->ro_cnt.p, s->ro_off.p, n);
     s->rn_cur.zero();
     s->ro_cur.zero();
     LAUNCH(reverse_scatter_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->S, s->fnew.p, s->cnew.p,
-           s->rn_off.p, s->rn_cur.p, s->rn_data.p);
+           s->rn_off.p, s->rn_cur.p, s->rn_data.p, tlo, thi);
     LAUNCH(reverse_scatter_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->P, s->fold.p, s->cold.p,
-           s->ro_off.p, s->ro_cur.p, s->ro_data.p);
+           s->ro_off.p, s->ro_cur.p, s->ro_data.p, tlo, thi);
     uint32_t tot[2];
     CK(cudaMemcpyAsync(&tot[0], s->rn_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
     CK(cudaMemcpyAsync(&tot[1], s->ro_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
@@ -1615,7 +1627,7 @@ void do_rebuild(annk_state* s) {
 
 void do_union(annk_state* s) {
     if (s->stage != 1) throw_invalid("union_reverse_lists: call rebuild_sample_lists first");
-    const uint32_t n = s->n;
+    const uint32_t n = s->n, lo = own_lo(s), hi = own_hi(s);
     const uint32_t m_new = next_pow2(2 * s->S), m_old = next_pow2(s->P + s->S);
     DevBuf<unsigned long long> rows(1);
     rows.zero();
@@ -1624,14 +1636,16 @@ void do_union(annk_state* s) {
     {
         const uint32_t tpb = 64;
         const size_t per = size_t(s->S + 1) * 8 + size_t(4 * s->S) * 4;
-        LAUNCH(rev_sample_kernel, (2 * n + tpb - 1) / tpb, tpb, tpb * per, n, s->S, round_seed, s->rn_off.p,
-               s->rn_data.p, s->ro_off.p, s->ro_data.p, samp.p);
+        if (hi > lo)
+            LAUNCH(rev_sample_kernel, (2 * (hi - lo) + tpb - 1) / tpb, tpb, tpb * per, hi, s->S, round_seed,
+                   s->rn_off.p, s->rn_data.p, s->ro_off.p, s->ro_data.p, samp.p, lo);
     }
     UnionArgs a{n, s->P, s->S, round_seed, s->fnew.p, s->fold.p, s->cnew.p, s->cold.p,
                 s->rn_off.p, s->rn_data.p, s->ro_off.p, s->ro_data.p, s->gnew.p, s->gold.p,
-                s->gncnt.p, s->gocnt.p, rows.p, samp.p};
+                s->gncnt.p, s->gocnt.p, rows.p, samp.p, lo};
+    a.n = hi;
     const uint32_t wpb = 4;
-    LAUNCH(union_kernel, (n + wpb - 1) / wpb, wpb * 32, wpb * (m_new + m_old) * 4, a, m_new, m_old);
+    if (hi > lo) LAUNCH(union_kernel, (hi - lo + wpb - 1) / wpb, wpb * 32, wpb * (m_new + m_old) * 4, a, m_new, m_old);
     unsigned long long h = 0;
     rows.download(&h, 1);
     ssync();
