@@ -66,6 +66,7 @@ struct BuildArgs {
     uint32_t ld8;
     const uint32_t* draws;  // split dimension of the k-th internal node in pre-order
     uint32_t n_draws;
+    float* col;  // block path: the node's gathered column, by point_index slot (n floats)
 };
 
 struct Smem {
@@ -379,6 +380,68 @@ __device__ __forceinline__ uint32_t tile_node_reg(const unsigned char* __restric
 // integer it does not equal, far more than half a float ulp below 256).
 // `sb` = row stride in bytes (odd word count: consecutive rows in different
 // banks).  Node/draw/leaf counters live in registers for the whole tile.
+// One tile node of 257..tile points from shared memory: two passes (sum, then
+// stable ballot partition through ltmp), degenerate fallback = bitonic sort of
+// (value, global id, local row) keys.  Returns the split position.
+__device__ __noinline__ uint32_t tile_node_smem(Smem& s, const unsigned char* __restrict__ st, uint16_t* li,
+                                                uint16_t* lt, const uint32_t* gid, uint32_t sb, uint32_t d,
+                                                uint32_t e_start, uint32_t e_end, float& split, uint8_t& even) {
+    const uint32_t lane = lane_id(), ltm = (1u << lane) - 1u;
+    const uint32_t size = e_end - e_start;
+    uint32_t is = 0;
+    for (uint32_t p0 = e_start; p0 < e_end; p0 += 256) {
+        uint32_t x[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) {
+            const uint32_t p = p0 + u * 32 + lane;
+            x[u] = p < e_end ? st[uint32_t(li[p]) * sb + d] : 0u;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 8; ++u) is += x[u];
+    }
+    const uint32_t isum = __reduce_add_sync(0xffffffffu, is);
+    uint32_t nl = 0, nr = 0;
+    for (uint32_t b0 = e_start; b0 < e_end; b0 += 32) {
+        const uint32_t p = b0 + lane;
+        const bool valid = p < e_end;
+        const uint16_t lc = valid ? li[p] : uint16_t(0);
+        const bool left = valid && uint32_t(st[uint32_t(lc) * sb + d]) * size <= isum;
+        const uint32_t bl = __ballot_sync(0xffffffffu, left);
+        const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
+        if (left) li[e_start + nl + __popc(bl & ltm)] = lc;
+        else if (valid) lt[nr + __popc(br & ltm)] = lc;
+        nl += __popc(bl);
+        nr += __popc(br);
+    }
+    __syncwarp();
+    for (uint32_t j = lane; j < nr; j += 32) li[e_start + nl + j] = lt[j];
+    __syncwarp();
+    split = __fdiv_rn(float(isum), float(size));
+    uint32_t mid = e_start + nl;
+    even = 0;
+    if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
+        // kd_forest.cpp:70-83: sort by (value, id); key = value | global id | local row
+        const uint32_t m = next_pow2(size);
+        uint64_t* k = s.sortk;
+        for (uint32_t j = lane; j < m; j += 32) {
+            uint64_t key = kEmptyKey;
+            if (j < size) {
+                const uint32_t lc = li[e_start + j];
+                key = (uint64_t(st[lc * sb + d]) << 53) | (uint64_t(gid[lc]) << 11) | lc;
+            }
+            k[j] = key;
+        }
+        __syncwarp();
+        warp_bitonic_sort(k, m);
+        for (uint32_t j = lane; j < size; j += 32) li[e_start + j] = uint16_t(k[j] & 0x7ffu);
+        __syncwarp();
+        mid = e_start + size / 2;
+        split = midpoint_f(float(st[uint32_t(li[mid - 1]) * sb + d]), float(st[uint32_t(li[mid]) * sb + d]));
+        even = 1;
+    }
+    return mid;
+}
+
 // Tile stack entry packed in 64 bits: parent id | start(11) | end(11) |
 // depth below the tile root(8) | link(2: bit0 = set the parent's child link,
 // bit1 = right child).  start/end are relative to the tile.
@@ -406,161 +469,104 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
     uint16_t* li = s.lidx;  // indexed by tile-relative slot
     uint16_t* lt = s.ltmp;
     const uint32_t* gid = s.sub + ts;
-    const uint32_t ltm = (1u << lane) - 1u;
     const uint32_t lcap = a.leaf_cap, pbase = base + ts, dep0 = root.depth;
     uint32_t nid = s.node_count, kd = s.draw_idx, wb = s.dwin_base, nleaf = s.leaf_count, maxd = s.max_depth;
-    uint32_t wsp = 1;
-    if (lane == 0) s.tstack[0] = tpack(root.parent, 0, tsz, 0, 1u | (root.side ? 2u : 0u));
-    __syncwarp();
-    while (wsp > 0) {
-        --wsp;
-        const uint64_t pe = s.tstack[wsp];
-        const uint32_t parent = uint32_t(pe >> 32), lo = uint32_t(pe);
-        const uint32_t e_start = (lo >> 21) & 0x7ffu, e_end = (lo >> 10) & 0x7ffu;
-        const uint32_t dep = dep0 + ((lo >> 2) & 0xffu), link = lo & 3u;
-        const uint32_t size = e_end - e_start;
+    // current node in registers; only right siblings go through the stack.
+    // Depth inside a tile is bounded (splits are <= 4:1 or even), so the
+    // stack cannot overflow: <= log_{5/4}(1024) + 1 entries.
+    uint32_t cs = 0, ce = tsz, cdep = root.depth, cpar = root.parent, clink = 1u | (root.side ? 2u : 0u);
+    uint32_t wsp = 0;
+    for (;;) {
+        const uint32_t size = ce - cs;
         const uint32_t id = nid++;
-        maxd = max(maxd, dep);
-        if (lane == 0 && (link & 1u)) {
-            if (link & 2u) a.nodes[parent].right = id;
-            else a.nodes[parent].left = id;
+        if (lane == 0 && (clink & 1u)) {
+            if (clink & 2u) a.nodes[cpar].right = id;
+            else a.nodes[cpar].left = id;
         }
         if (size <= lcap) {  // a right child whose left sibling was internal
             if (lane == 0) {
-                a.nodes[id] = KdNodeDev{kLeaf, 0.0f, pbase + e_start, pbase + e_end};
-                a.depth[id] = dep;
+                reinterpret_cast<uint4*>(a.nodes)[id] = make_uint4(kLeaf, 0u, pbase + cs, pbase + ce);
+                a.depth[id] = cdep;
                 a.even[id] = 0;
             }
             ++nleaf;
-            __syncwarp();
-            continue;
-        }
-        FT_MARK(0);
-        if (kd - wb >= kDrawWin) {  // refill the draw window (uniform)
-            wb = kd & ~(kDrawWin - 1);
-            __syncwarp();
-            for (uint32_t j = lane; j < kDrawWin; j += 32) s.dwin[j] = wb + j < a.n_draws ? a.draws[wb + j] : 0u;
-            __syncwarp();
-        }
-        const uint32_t d = s.dwin[kd - wb];
-        ++kd;
-        FT_MARK(8);
-        float split;
-        uint8_t even;
-        uint32_t mid;
-        if (size <= 32) {
-            mid = tile_node_reg<1>(st, li, gid, sb, d, e_start, e_end, split, even);
-        } else if (size <= 64) {
-            mid = tile_node_reg<2>(st, li, gid, sb, d, e_start, e_end, split, even);
-        } else if (size <= 128) {
-            mid = tile_node_reg<4>(st, li, gid, sb, d, e_start, e_end, split, even);
-        } else if (size <= 256) {
-            mid = tile_node_reg<8>(st, li, gid, sb, d, e_start, e_end, split, even);
+            maxd = max(maxd, cdep);
         } else {
-            // ---- shared-memory path (257..tile points): two passes
-            uint32_t is = 0;
-            for (uint32_t p0 = e_start; p0 < e_end; p0 += 256) {
-                uint32_t x[8];
-#pragma unroll
-                for (uint32_t u = 0; u < 8; ++u) {
-                    const uint32_t p = p0 + u * 32 + lane;
-                    x[u] = p < e_end ? st[uint32_t(li[p]) * sb + d] : 0u;
-                }
-#pragma unroll
-                for (uint32_t u = 0; u < 8; ++u) is += x[u];
-            }
-            const uint32_t isum = __reduce_add_sync(0xffffffffu, is);
-            uint32_t nl = 0, nr = 0;
-            for (uint32_t b0 = e_start; b0 < e_end; b0 += 32) {
-                const uint32_t p = b0 + lane;
-                const bool valid = p < e_end;
-                const uint16_t lc = valid ? li[p] : uint16_t(0);
-                const bool left = valid && uint32_t(st[uint32_t(lc) * sb + d]) * size <= isum;
-                const uint32_t bl = __ballot_sync(0xffffffffu, left);
-                const uint32_t br = __ballot_sync(0xffffffffu, valid && !left);
-                if (left) li[e_start + nl + __popc(bl & ltm)] = lc;
-                else if (valid) lt[nr + __popc(br & ltm)] = lc;
-                nl += __popc(bl);
-                nr += __popc(br);
-            }
-            __syncwarp();
-            for (uint32_t j = lane; j < nr; j += 32) li[e_start + nl + j] = lt[j];
-            __syncwarp();
-            split = __fdiv_rn(float(isum), float(size));
-            mid = e_start + nl;
-            even = 0;
-            if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
-                // kd_forest.cpp:70-83: sort by (value, id); key = value | global id | local row
-                const uint32_t m = next_pow2(size);
-                uint64_t* k = s.sortk;
-                for (uint32_t j = lane; j < m; j += 32) {
-                    uint64_t key = kEmptyKey;
-                    if (j < size) {
-                        const uint32_t lc = li[e_start + j];
-                        key = (uint64_t(st[lc * sb + d]) << 53) | (uint64_t(gid[lc]) << 11) | lc;
-                    }
-                    k[j] = key;
-                }
+            FT_MARK(0);
+            if (kd - wb >= kDrawWin) {  // refill the draw window (uniform)
+                wb = kd & ~(kDrawWin - 1);
                 __syncwarp();
-                warp_bitonic_sort(k, m);
-                for (uint32_t j = lane; j < size; j += 32) li[e_start + j] = uint16_t(k[j] & 0x7ffu);
+                for (uint32_t j = lane; j < kDrawWin; j += 32) s.dwin[j] = wb + j < a.n_draws ? a.draws[wb + j] : 0u;
                 __syncwarp();
-                mid = e_start + size / 2;
-                split = midpoint_f(float(st[uint32_t(li[mid - 1]) * sb + d]), float(st[uint32_t(li[mid]) * sb + d]));
-                even = 1;
             }
-        }
-        FT_MARK(10);
-        // this node's record (left child = id + 1 in pre-order) and its leaf
-        // children, one lane each: lane 0 node, lane 1 left leaf, lane 2 right leaf
-        const bool lleaf = mid - e_start <= lcap, rleaf = e_end - mid <= lcap;
-        const bool both = lleaf && rleaf;
-        if (lane < 3) {
-            KdNodeDev rec;
-            uint32_t rid = id, rdep = dep + 1;
-            uint8_t rev = 0;
-            bool w = true;
-            if (lane == 0) {
-                rec = KdNodeDev{d, split, id + 1, lleaf ? id + 2 : 0u};
-                rdep = dep;
-                rev = even;
-            } else if (lane == 1) {
-                rec = KdNodeDev{kLeaf, 0.0f, pbase + e_start, pbase + mid};
-                rid = id + 1;
-                w = lleaf;
+            const uint32_t d = s.dwin[kd - wb];
+            ++kd;
+            FT_MARK(8);
+            float split;
+            uint8_t even;
+            uint32_t mid;
+            if (size <= 32) {
+                mid = tile_node_reg<1>(st, li, gid, sb, d, cs, ce, split, even);
+            } else if (size <= 64) {
+                mid = tile_node_reg<2>(st, li, gid, sb, d, cs, ce, split, even);
+            } else if (size <= 128) {
+                mid = tile_node_reg<4>(st, li, gid, sb, d, cs, ce, split, even);
+            } else if (size <= 256) {
+                mid = tile_node_reg<8>(st, li, gid, sb, d, cs, ce, split, even);
             } else {
-                rec = KdNodeDev{kLeaf, 0.0f, pbase + mid, pbase + e_end};
-                rid = id + 2;
-                w = both;
+                mid = tile_node_smem(s, st, li, lt, gid, sb, d, cs, ce, split, even);
             }
-            if (w) {
-                reinterpret_cast<uint4*>(a.nodes)[rid] =
-                    make_uint4(rec.split_dim, __float_as_uint(rec.split_val), rec.left, rec.right);
-                a.depth[rid] = rdep;
-                a.even[rid] = rev;
+            FT_MARK(10);
+            // this node's record (left child = id + 1 in pre-order) and its leaf
+            // children, one lane each: lane 0 node, lane 1 left leaf, lane 2 right leaf
+            const bool lleaf = mid - cs <= lcap, rleaf = ce - mid <= lcap;
+            const bool both = lleaf && rleaf;
+            if (lane < 3) {
+                const bool l0 = lane == 0, l1 = lane == 1;
+                const uint32_t rid = id + lane;
+                const uint4 rec = l0 ? make_uint4(d, __float_as_uint(split), id + 1, lleaf ? id + 2 : 0u)
+                                     : make_uint4(kLeaf, 0u, pbase + (l1 ? cs : mid), pbase + (l1 ? mid : ce));
+                if (l0 || (l1 ? lleaf : both)) {
+                    reinterpret_cast<uint4*>(a.nodes)[rid] = rec;
+                    a.depth[rid] = l0 ? cdep : cdep + 1;
+                    a.even[rid] = l0 ? even : uint8_t(0);
+                }
             }
-        }
-        if (lleaf) {
+            maxd = max(maxd, cdep + 1);
+            if (!lleaf) {
+                // descend into the left child; the right one waits on the stack
+                if (lane == 0) s.tstack[wsp] = tpack(id, mid, ce, cdep + 1 - dep0, 3u);
+                ++wsp;
+                DCHK(wsp < kTileStack);
+                ce = mid;
+                cdep += 1;
+                cpar = id;
+                clink = 0;  // left = id + 1 is already in the record
+                FT_MARK(12);
+                continue;
+            }
             nid += both ? 2u : 1u;
             nleaf += both ? 2u : 1u;
-            maxd = max(maxd, dep + 1);
-            if (!rleaf) {
-                if (lane == 0) s.tstack[wsp] = tpack(id, mid, e_end, dep + 1 - dep0, 0u);
-                ++wsp;
+            if (!rleaf) {  // left leaf emitted; the right child (= id + 2) is next
+                cs = mid;
+                cdep += 1;
+                cpar = id;
+                clink = 0;
+                FT_MARK(12);
+                continue;
             }
-        } else {
-            if (lane == 0) {
-                s.tstack[wsp] = tpack(id, mid, e_end, dep + 1 - dep0, 3u);
-                s.tstack[wsp + 1] = tpack(id, e_start, mid, dep + 1 - dep0, 0u);
-            }
-            wsp += 2;
+            FT_MARK(12);
         }
-        if (wsp > kTileStack - 2 || dep + 1 - dep0 > 255) {
-            if (lane == 0) s.error = 1;
-            wsp = kTileStack - 2;
-        }
+        if (wsp == 0) break;
         __syncwarp();
-        FT_MARK(12);
+        --wsp;
+        const uint64_t pe = s.tstack[wsp];
+        const uint32_t lo = uint32_t(pe);
+        cpar = uint32_t(pe >> 32);
+        cs = (lo >> 21) & 0x7ffu;
+        ce = (lo >> 10) & 0x7ffu;
+        cdep = dep0 + ((lo >> 2) & 0xffu);
+        clink = lo & 3u;
     }
     if (lane == 0) {
         s.node_count = nid;
@@ -872,21 +878,24 @@ __device__ void block_split_node(const BuildArgs& a, Smem& s, const StackEntry& 
     double sum = 0.0;
     int top = INT_MIN, lsb = INT_MAX;
     uint64_t isum = 0;
-    for (uint32_t p0 = e.start; p0 < e.end; p0 += kChunk) {
-        uint32_t pid[kPer];
+    constexpr uint32_t kSumPer = 8;  // gathers in flight per thread in the sum pass (16: no gain)
+    for (uint32_t p0 = e.start; p0 < e.end; p0 += kBlock * kSumPer) {
+        uint32_t pid[kSumPer];
 #pragma unroll
-        for (uint32_t u = 0; u < kPer; ++u) {
+        for (uint32_t u = 0; u < kSumPer; ++u) {
             const uint32_t q = p0 + u * kBlock + tid;
             pid[u] = q < e.end ? a.pidx[q] : 0u;
         }
-        float v[kPer];
+        float v[kSumPer];
 #pragma unroll
-        for (uint32_t u = 0; u < kPer; ++u) {
+        for (uint32_t u = 0; u < kSumPer; ++u) {
             const uint32_t q = p0 + u * kBlock + tid;
             v[u] = q < e.end ? colv<U8>(a, pid[u], d) : 0.0f;
         }
 #pragma unroll
-        for (uint32_t u = 0; u < kPer; ++u) {
+        for (uint32_t u = 0; u < kSumPer; ++u) {
+            const uint32_t q = p0 + u * kBlock + tid;
+            if (q < e.end) a.col[q] = v[u];  // coalesced; read back by the partition pass
             if constexpr (U8) {
                 isum += uint32_t(v[u]);
             } else {
@@ -923,14 +932,18 @@ __device__ void block_split_node(const BuildArgs& a, Smem& s, const StackEntry& 
     for (uint32_t b0 = e.start; b0 < e.end; b0 += kChunk) {
         const uint32_t q0 = b0 + tid * kPer;
         uint32_t pid[kPer];
+        float cv[kPer];
 #pragma unroll
-        for (uint32_t i = 0; i < kPer; ++i) pid[i] = q0 + i < e.end ? a.pidx[q0 + i] : 0u;
+        for (uint32_t i = 0; i < kPer; ++i) {
+            pid[i] = q0 + i < e.end ? a.pidx[q0 + i] : 0u;
+            cv[i] = q0 + i < e.end ? a.col[q0 + i] : 0.0f;
+        }
         uint32_t lm = 0, vm = 0;
 #pragma unroll
         for (uint32_t i = 0; i < kPer; ++i) {
             if (q0 + i < e.end) {
                 vm |= 1u << i;
-                if (colv<U8>(a, pid[i], d) <= split) lm |= 1u << i;
+                if (cv[i] <= split) lm |= 1u << i;
             }
         }
         // block exclusive scan of (lefts | rights << 16)
@@ -1263,6 +1276,7 @@ int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_ca
         DevBuf<uint64_t> sortbuf(size_t(next_pow2(n)) * n_trees);
         DevBuf<uint32_t> meta(8 * n_trees);
         DevBuf<uint32_t> draws(size_t(n) * n_trees);
+        DevBuf<float> col(size_t(n) * n_trees);
         LAUNCH(draws_kernel, n_trees, 320, 0, seed, ds->dim, n, draws.p);
         std::vector<BuildArgs> args(n_trees);
         for (uint32_t t = 0; t < n_trees; ++t) {
@@ -1275,7 +1289,7 @@ int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_ca
                                 tr.nodes.p, tr.depth.p, tr.even.p, tr.pidx.p,
                                 rtmp.p + size_t(t) * n, sortbuf.p + size_t(t) * next_pow2(n),
                                 meta.p + 8 * t, ds->u8 ? ds->data8.p : nullptr, ds->ld8,
-                                draws.p + size_t(t) * n, n};
+                                draws.p + size_t(t) * n, n, col.p + size_t(t) * n};
         }
         DevBuf<BuildArgs> dargs(n_trees);
         dargs.upload(args.data(), n_trees);
