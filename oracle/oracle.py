@@ -107,6 +107,12 @@ class OracleLib:
         L.ora_nn_expansion_iteration.restype = _u64
         L.ora_nn_expansion_iteration.argtypes = [_vp, _vp, _u32]
         L.ora_rebuild_sample_lists.argtypes = [_vp]
+        if hasattr(L, "ora_ref_save_forest"):  # reference only: its own file writers/readers
+            L.ora_ref_save_forest.argtypes = [_vp, C.c_char_p]
+            L.ora_ref_load_forest.restype = _vp
+            L.ora_ref_load_forest.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
+            L.ora_ref_save_fvecs.argtypes = [_vp, C.c_char_p]
+            L.ora_ref_save_ivecs.argtypes = [_u32p, _u32, _u32, C.c_char_p]
         if hasattr(L, "ora_shard_sample"):  # restatement only: shard-mode protocol
             L.ora_shard_sample.argtypes = [_vp, _u32, _u32, _u32p, _u32p, _u32p, _u32p, _u64p]
             L.ora_shard_union.argtypes = [_vp, _u32p, _u32p, _u32p, _u32p]
@@ -179,6 +185,23 @@ class OracleLib:
             cat("right", np.uint32), cat("depth", np.uint32), cat("even", np.uint8),
             cat("point_index", np.uint32))
         return Forest(self, h, n, dim, leaf_cap, seed)
+
+    # reference-only file writers/readers (byte-compatibility checks)
+    def ref_save_forest(self, forest: "Forest", path: str):
+        self._check(self.L.ora_ref_save_forest(forest.h, path.encode()))
+
+    def ref_load_forest(self, path: str, n, dim, leaf_cap, seed) -> "Forest":
+        st = C.c_int(0)
+        h = self.L.ora_ref_load_forest(path.encode(), C.byref(st))
+        self._check(st.value)
+        return Forest(self, h, n, dim, leaf_cap, seed)
+
+    def ref_save_fvecs(self, vs: "VS", path: str):
+        self._check(self.L.ora_ref_save_fvecs(vs.h, path.encode()))
+
+    def ref_save_ivecs(self, ids: np.ndarray, path: str):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        self._check(self.L.ora_ref_save_ivecs(ids, ids.shape[0], ids.shape[1], path.encode()))
 
     def init_graph(self, vs, forest, k, conquer_depth, pool_cap, sample_cap, seed, workers=1) -> "State":
         st = C.c_int(0)

@@ -364,4 +364,27 @@ int ora_search(void* base, void* f, const uint32_t* graph_ids, const float* grap
     });
 }
 
+/* Reference file writers/readers (kd_forest.cpp:307-372, dataset.cpp:96-200,
+ * knn_graph.cpp:5-37): byte-compatibility checks for the framework's formats. */
+int ora_ref_save_forest(void* f, const char* path) {
+    return guard([&] { save_forest(*F(f), path); });
+}
+void* ora_ref_load_forest(const char* path, int* status) {
+    KdForest* out = nullptr;
+    *status = guard([&] { out = new KdForest(load_forest(path)); });
+    return out;
+}
+int ora_ref_save_fvecs(void* vs, const char* path) {
+    return guard([&] { save_fvecs(*V(vs), path); });
+}
+int ora_ref_save_ivecs(const uint32_t* ids, uint32_t n, uint32_t k, const char* path) {
+    return guard([&] {
+        GroundTruth gt;
+        gt.n = n;
+        gt.k = k;
+        gt.ids.assign(ids, ids + size_t(n) * k);
+        save_ivecs(gt, path);
+    });
+}
+
 }  // extern "C"
