@@ -93,6 +93,11 @@ int annk_brute_force_knn(const annk_dataset* base, const annk_dataset* queries, 
  * rows act as queries (used to score accuracy on a seeded sample). */
 int annk_brute_force_rows(const annk_dataset* base, const uint32_t* rows, uint32_t n_rows,
                           uint32_t k, uint32_t* out_ids, float* out_dists);
+/* eval.cpp:129-155 accuracy_vs_k: for each k' in k_list, the fraction of graph
+ * edges (n x k ids) whose target lies in the exact k'-NN of the source (exact
+ * self-mode truth at max k' computed on the device). out: n_k doubles. */
+int annk_accuracy_vs_k(const annk_dataset* vs, const uint32_t* graph_ids, uint32_t n, uint32_t k,
+                       const uint32_t* k_list, uint32_t n_k, double* out);
 
 /* ---------------------------------------------------------------- forest */
 /* kd_forest.cpp:245-264 build_forest — bit-identical trees (same split_dim,

@@ -113,6 +113,7 @@ class OracleLib:
             L.ora_ref_load_forest.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
             L.ora_ref_save_fvecs.argtypes = [_vp, C.c_char_p]
             L.ora_ref_save_ivecs.argtypes = [_u32p, _u32, _u32, C.c_char_p]
+            L.ora_ref_accuracy_vs_k.argtypes = [_vp, _u32p, _u32, _u32, _u32p, _u32, _f64p]
         if hasattr(L, "ora_shard_sample"):  # restatement only: shard-mode protocol
             L.ora_shard_sample.argtypes = [_vp, _u32, _u32, _u32p, _u32p, _u32p, _u32p, _u64p]
             L.ora_shard_union.argtypes = [_vp, _u32p, _u32p, _u32p, _u32p]
@@ -198,6 +199,13 @@ class OracleLib:
 
     def ref_save_fvecs(self, vs: "VS", path: str):
         self._check(self.L.ora_ref_save_fvecs(vs.h, path.encode()))
+
+    def ref_accuracy_vs_k(self, vs: "VS", ids: np.ndarray, k_list) -> list:
+        ids = np.ascontiguousarray(ids, np.uint32)
+        kl = np.ascontiguousarray(k_list, np.uint32)
+        out = np.empty(kl.size, np.float64)
+        self._check(self.L.ora_ref_accuracy_vs_k(vs.h, ids, ids.shape[0], ids.shape[1], kl, kl.size, out))
+        return out.tolist()
 
     def ref_save_ivecs(self, ids: np.ndarray, path: str):
         ids = np.ascontiguousarray(ids, np.uint32)

@@ -377,6 +377,17 @@ void* ora_ref_load_forest(const char* path, int* status) {
 int ora_ref_save_fvecs(void* vs, const char* path) {
     return guard([&] { save_fvecs(*V(vs), path); });
 }
+int ora_ref_accuracy_vs_k(void* vs, const uint32_t* ids, uint32_t n, uint32_t k, const uint32_t* kl,
+                          uint32_t nk, double* out) {
+    return guard([&] {
+        KnnGraph g;
+        g.n = n;
+        g.k = k;
+        g.ids.assign(ids, ids + size_t(n) * k);
+        const auto t = accuracy_vs_k(g, *V(vs), std::span<const uint32_t>(kl, nk), 1);
+        for (uint32_t q = 0; q < nk; ++q) out[q] = t[q].second;
+    });
+}
 int ora_ref_save_ivecs(const uint32_t* ids, uint32_t n, uint32_t k, const char* path) {
     return guard([&] {
         GroundTruth gt;

@@ -7,7 +7,8 @@ include/annkit_b200.h); this package is the reference-shaped host mirror.
 from ._lib import AnnkError, InvalidArgument, OutOfRange, lib  # noqa: F401
 from .api import (  # noqa: F401
     BatchResult, BuildParams, BuildResult, BuildStats, GraphSearcher, IterationLog, KdForest, KdTree, KnnGraph,
-    RefineState, SearchParams, SearchResult, SearchStats, SweepPoint, SweepRow, VectorSet, brute_force_graph,
+    RefineState, SearchParams, SearchResult, SearchStats, SweepPoint, SweepRow, VectorSet, accuracy_vs_k,
+    brute_force_graph,
     brute_force_knn, brute_force_rows, build_forest, build_graph, descend_from, detail, finalize, gen_mixture,
     state_stats,
     gen_synthetic, graph_accuracy, init_graph, recall, recall_curve, refine_nn_descent, search_leaves,

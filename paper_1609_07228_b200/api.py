@@ -156,6 +156,20 @@ def brute_force_rows(base, rows: np.ndarray, k: int, with_dists: bool = False):
     return (ids, d) if with_dists else ids
 
 
+def accuracy_vs_k(graph, vs, k_list, workers: int = 1) -> list:
+    """eval.cpp:129-155: [(k', fraction of graph edges inside the exact k'-NN)],
+    exact truth and membership counted on the device."""
+    g = graph.ids if isinstance(graph, KnnGraph) else np.asarray(graph)
+    g = np.ascontiguousarray(g, np.uint32)
+    v = _as_vs(vs)
+    kl = np.ascontiguousarray(np.asarray(k_list, np.uint32).ravel())
+    out = np.empty(max(kl.size, 1), np.float64)
+    if g.ndim != 2:
+        raise InvalidArgument("accuracy_vs_k: graph must be n x k")
+    check(lib.annk_accuracy_vs_k(v.handle, g, g.shape[0], g.shape[1], kl, kl.size, out))
+    return [(int(k), float(a)) for k, a in zip(kl, out)]
+
+
 # ------------------------------------------------------------------ forest
 
 @dataclass

@@ -327,6 +327,51 @@ __global__ void keys_to_ids_kernel(const uint64_t* __restrict__ keys, size_t n, 
 
 }  // namespace
 
+// eval.cpp:129-155 accuracy_vs_k, membership part: for row i, the rank of each
+// graph id in the exact row truth[i] (k_max ids, ascending (dist, id)) via a
+// shared-memory hash (id -> rank), then per k' in k_list: hits += rank < k'.
+// One CTA per row (grid-stride); per-k' hit counts are 64-bit atomics.
+__global__ void accuracy_hits_kernel(const uint32_t* __restrict__ graph, uint32_t n, uint32_t k,
+                                     const uint32_t* __restrict__ truth, uint32_t kmax,
+                                     const uint32_t* __restrict__ klist, uint32_t nk, uint32_t slots,
+                                     unsigned long long* __restrict__ hits) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* tab = reinterpret_cast<uint64_t*>(smem);  // (id << 32 | rank), empty = ~0
+    unsigned long long* local = reinterpret_cast<unsigned long long*>(tab + slots);
+    const uint32_t mask = slots - 1;
+    for (uint32_t j = threadIdx.x; j < nk; j += blockDim.x) local[j] = 0;
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        for (uint32_t j = threadIdx.x; j < slots; j += blockDim.x) tab[j] = ~0ull;
+        __syncthreads();
+        const uint32_t* tr = truth + size_t(i) * kmax;
+        for (uint32_t r = threadIdx.x; r < kmax; r += blockDim.x) {
+            const uint32_t id = tr[r];
+            uint32_t h = (id * 2654435761u) & mask;
+            const uint64_t v = (uint64_t(id) << 32) | r;
+            while (atomicCAS(reinterpret_cast<unsigned long long*>(&tab[h]), ~0ull, v) != ~0ull) h = (h + 1) & mask;
+        }
+        __syncthreads();
+        const uint32_t* gr = graph + size_t(i) * k;
+        for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
+            const uint32_t id = gr[j];
+            uint32_t h = (id * 2654435761u) & mask, rank = 0xffffffffu;
+            for (;;) {
+                const uint64_t e = tab[h];
+                if (e == ~0ull) break;
+                if (uint32_t(e >> 32) == id) { rank = uint32_t(e); break; }
+                h = (h + 1) & mask;
+            }
+            if (rank != 0xffffffffu)
+                for (uint32_t q = 0; q < nk; ++q)
+                    if (rank < klist[q]) atomicAdd(&local[q], 1ull);
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < nk; j += blockDim.x)
+        if (local[j]) atomicAdd(&hits[j], local[j]);
+}
+
 void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
                         const uint32_t* self_ids, uint32_t k, uint64_t* out_keys, const uint8_t* q8,
                         const int32_t* qnorm) {
@@ -423,6 +468,48 @@ int annk_brute_force_knn(const annk_dataset* base, const annk_dataset* queries, 
                            u8 ? qs->data8.p : nullptr, u8 ? qs->norms8.p : nullptr);
         finish_keys(keys, size_t(nq) * k, out_ids, out_dists);
         if (dist_comps) *dist_comps += uint64_t(nq) * (self ? base->n - 1 : base->n);
+    });
+}
+
+int annk_accuracy_vs_k(const annk_dataset* vs, const uint32_t* graph_ids, uint32_t n, uint32_t k,
+                       const uint32_t* k_list, uint32_t n_k, double* out) {
+    return abi([&] {
+        if (!vs || !graph_ids || !k_list || !out) throw_invalid("accuracy_vs_k: null argument");
+        if (n != vs->n) throw_invalid("accuracy_vs_k: graph does not match data");
+        if (n_k == 0) throw_invalid("accuracy_vs_k: empty k list");
+        uint32_t kmax = 0;
+        for (uint32_t q = 0; q < n_k; ++q) kmax = std::max(kmax, k_list[q]);
+        if (kmax > vs->n - 1) throw_invalid("accuracy_vs_k: k exceeds n-1");
+        if (k == 0) throw_invalid("accuracy_vs_k: empty graph rows");
+        // exact self-mode truth at k_max (eval.cpp:139 brute_force_knn)
+        DevBuf<uint64_t> keys(size_t(n) * kmax);
+        DevBuf<uint32_t> selfids(n);
+        {
+            std::vector<uint32_t> iota(n);
+            for (uint32_t i = 0; i < n; ++i) iota[i] = i;
+            selfids.upload(iota.data(), n);
+        }
+        brute_force_device(vs, vs->data.p, vs->ld, n, selfids.p, kmax, keys.p, vs->u8 ? vs->data8.p : nullptr,
+                           vs->u8 ? vs->norms8.p : nullptr);
+        DevBuf<uint32_t> truth(size_t(n) * kmax), g(size_t(n) * k), kl(n_k);
+        const uint32_t kgrid = uint32_t(std::min<size_t>((size_t(n) * kmax + 255) / 256, 65535));
+        LAUNCH(keys_to_ids_kernel, std::max(kgrid, 1u), 256, 0, keys.p, size_t(n) * kmax, truth.p, nullptr);
+        keys.release();
+        g.upload(graph_ids, size_t(n) * k);
+        kl.upload(k_list, n_k);
+        DevBuf<unsigned long long> hits(n_k);
+        hits.zero();
+        uint32_t slots = 64;
+        while (slots < 2 * kmax) slots *= 2;
+        const size_t sm = size_t(slots) * 8 + size_t(n_k) * 8;
+        if (sm > 200 * 1024) throw_invalid("accuracy_vs_k: k_max too large for the device membership kernel");
+        CK(cudaFuncSetAttribute(accuracy_hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        LAUNCH(accuracy_hits_kernel, std::min<uint32_t>(n, uint32_t(num_sms()) * 4), 256, sm, g.p, n, k, truth.p,
+               kmax, kl.p, n_k, slots, hits.p);
+        std::vector<unsigned long long> h(n_k);
+        hits.download(h.data(), n_k);
+        ssync();
+        for (uint32_t q = 0; q < n_k; ++q) out[q] = double(h[q]) / (double(n) * k);
     });
 }
 
