@@ -9,7 +9,8 @@ import sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
-hdr, data = rows[1], rows[2:]
+hdr = rows[1]
+data = [r for r in rows[2:] if r and r[0].startswith("0x")]  # one kernel's SASS rows (headers skipped)
 base = int(data[0][0], 16)
 line_of = {}
 cur = None
