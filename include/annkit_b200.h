@@ -132,6 +132,11 @@ int annk_descend_from(const annk_forest* f, uint32_t t, const float* queries, ui
 int annk_init_graph(const annk_dataset* ds, const annk_forest* f, uint32_t k,
                     uint32_t conquer_depth, uint32_t pool_cap, uint32_t sample_cap, uint64_t seed,
                     annk_state** out);
+/* graph_build.cpp:294-326 init_random (the random-descent baseline's start):
+ * per point min(pool_cap, n-1) distinct ids drawn from
+ * mt19937_64(substream(seed, i)) (all other points when pool_cap >= n-1). */
+int annk_init_random(const annk_dataset* ds, uint32_t k, uint32_t pool_cap, uint32_t sample_cap,
+                     uint64_t seed, annk_state** out);
 /* A RefineState from host pools (n rows of pool_cap slots, sizes[i] used). */
 int annk_state_import(uint32_t n, uint32_t k, uint32_t pool_cap, uint32_t sample_cap,
                       uint64_t seed, uint32_t iteration, uint64_t dist_comps,

@@ -100,6 +100,7 @@ _SIGS = {
     "annk_state_join_rows": [_vp, C.POINTER(_u64)],
     "annk_state_stats": [_vp, _u64p],
     "annk_init_graph_shard": [_vp, _vp, _u32, _u32, _u32, _u32, _u64, _u32, _u32, _pp],
+    "annk_init_random": [_vp, _u32, _u32, _u32, _u64, _pp],
     "annk_state_set_shard": [_vp, _u32, _u32],
     "annk_state_rows": [_vp, C.c_int, C.c_int, _u32, _u32, _vp],
     "annk_shard_sample": [_vp],

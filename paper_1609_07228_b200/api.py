@@ -355,6 +355,14 @@ def init_graph(vs, forest: KdForest, k: int, conquer_depth: int, pool_cap: int, 
     return RefineState(h)
 
 
+def init_random(vs, k: int, pool_cap: int, sample_cap: int, seed: int, workers: int = 1) -> RefineState:
+    """graph_build.cpp:294-326 (random-descent baseline start)."""
+    v = _as_vs(vs)
+    h = C.c_void_p()
+    check(lib.annk_init_random(v.handle, k, pool_cap, sample_cap, seed, C.byref(h)))
+    return RefineState(h)
+
+
 class detail:
     """graph_build.hpp:117-133 detail:: entry points."""
 
@@ -492,13 +500,18 @@ def build_graph(vs, forest: Optional[KdForest], params: BuildParams, gt: Optiona
         acc = graph_accuracy(g, gt) if gt is not None else -1.0
         st.iterations.append(IterationLog(0, st.init_seconds, comps[0], 0, acc))
         return BuildResult(g, st)
-    if params.strategy not in ("efanna", "init-only"):
+    if params.strategy not in ("efanna", "init-only", "random-descent"):
         raise InvalidArgument(f"build_graph: strategy {params.strategy} is a CPU baseline, not a device path")
-    if forest is None:
+    tree_init = params.strategy != "random-descent"
+    if tree_init and forest is None:
         raise InvalidArgument("build_graph: strategy needs a forest")
     lib.annk_synchronize()
     t0 = time.perf_counter()
-    state = init_graph(v, forest, params.k, params.conquer_depth, params.pool_cap, params.sample_cap, params.seed)
+    if tree_init:
+        state = init_graph(v, forest, params.k, params.conquer_depth, params.pool_cap, params.sample_cap,
+                           params.seed)
+    else:
+        state = init_random(v, params.k, params.pool_cap, params.sample_cap, params.seed)
     st.init_seconds = time.perf_counter() - t0
 
     def log_row(changes):

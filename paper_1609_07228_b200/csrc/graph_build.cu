@@ -457,6 +457,131 @@ __global__ void init_overflow_kernel(InitArgs a, const uint32_t* list, uint32_t 
     }
 }
 
+// graph_build.cpp:294-326 init_random.  One warp per point i: if P >= n-1 the
+// pool is every other point; otherwise draws j = rng() % n from
+// mt19937_64(substream(seed, i)), skipping i and repeats, until P distinct ids
+// are taken (draw order decides, as in the reference's loop).  The MT state
+// (312 words) lives in the warp's shared memory: lane 0 expands the seed, the
+// warp twists in 3 phases, lanes consume 32 outputs at a time; a repeat within
+// a batch is resolved by __match_any_sync (first lane wins).  The taken ids'
+// distances are sorted by (dist, id) into the pool, all flagged new.
+__host__ __device__ __forceinline__ size_t init_random_warp_bytes(uint32_t P) {
+    // mt[312] + keys[next_pow2(P)] + hash slots (4 * P, pow2) u32
+    uint32_t m = 1;
+    while (m < P) m <<= 1;
+    uint32_t hs = 1;
+    while (hs < 4 * P) hs <<= 1;
+    return (size_t(312) * 8 + size_t(m) * 8 + size_t(hs) * 4 + 15) & ~size_t(15);
+}
+
+__global__ void init_random_kernel(InitArgs a, uint64_t seed) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
+    const uint32_t wpb = blockDim.x / 32;
+    const uint32_t P = a.P, n = a.n;
+    uint32_t m = 1;
+    while (m < P) m <<= 1;
+    uint32_t hs = 1;
+    while (hs < 4 * P) hs <<= 1;
+    unsigned char* base = smem + size_t(warp) * init_random_warp_bytes(P);
+    uint64_t* mt = reinterpret_cast<uint64_t*>(base);
+    uint64_t* keys = mt + 312;
+    uint32_t* hset = reinterpret_cast<uint32_t*>(keys + m);
+    for (uint32_t i = blockIdx.x * wpb + warp; i < n; i += gridDim.x * wpb) {
+        const uint32_t want = min(P, n - 1);
+        const uint8_t* x8i = a.x8 ? a.x8 + size_t(i) * a.ld8 : nullptr;
+        const float* xi = a.x + size_t(i) * a.ld;
+        auto dist = [&](uint32_t j) -> float {
+            return a.x8 ? l2_u8(x8i, a.x8 + size_t(j) * a.ld8, a.ld8, a.norms8[i], a.norms8[j])
+                        : l2_exact_ldg(xi, a.x + size_t(j) * a.ld, a.ld);
+        };
+        uint32_t have = 0;
+        if (want == n - 1) {
+            for (uint32_t j = lane; j < n; j += 32)
+                if (j != i) keys[j < i ? j : j - 1] = make_key(dist(j), j);
+            have = n - 1;
+        } else {
+            for (uint32_t t = lane; t < hs; t += 32) hset[t] = 0xffffffffu;
+            if (lane == 0) {
+                uint64_t x = substream(seed, i);
+                mt[0] = x;
+                for (uint32_t t = 1; t < 312; ++t) {
+                    x = 6364136223846793005ULL * (x ^ (x >> 62)) + uint64_t(t);
+                    mt[t] = x;
+                }
+            }
+            __syncwarp();
+            while (have < want) {
+                // regenerate 312 words (3 phases: [0,156), [156,311), 311)
+                // (uniform trip counts: every lane reaches every __syncwarp)
+                for (uint32_t t0 = 0; t0 < 156; t0 += 32) {
+                    const uint32_t t = t0 + lane;
+                    const uint64_t v = t < 156 ? mt_twist(mt[t], mt[t + 1], mt[t + 156]) : 0ull;
+                    __syncwarp();
+                    if (t < 156) mt[t] = v;
+                }
+                __syncwarp();
+                for (uint32_t t0 = 156; t0 < 311; t0 += 32) {
+                    const uint32_t t = t0 + lane;
+                    const uint64_t v = t < 311 ? mt_twist(mt[t], mt[t + 1], mt[t - 156]) : 0ull;
+                    __syncwarp();
+                    if (t < 311) mt[t] = v;
+                }
+                __syncwarp();
+                if (lane == 0) mt[311] = mt_twist(mt[311], mt[0], mt[155]);
+                __syncwarp();
+                for (uint32_t b0 = 0; b0 < 312 && have < want; b0 += 32) {
+                    const uint32_t t = b0 + lane;
+                    const bool ok = t < 312;
+                    const uint32_t j = ok ? uint32_t(mt_temper(mt[t]) % uint64_t(n)) : i;
+                    // seen before this batch?
+                    bool cand = ok && j != i;
+                    if (cand) {
+                        uint32_t h = (j * 2654435761u) & (hs - 1);
+                        for (;;) {
+                            const uint32_t e = hset[h];
+                            if (e == 0xffffffffu) break;
+                            if (e == j) { cand = false; break; }
+                            h = (h + 1) & (hs - 1);
+                        }
+                    }
+                    // repeats inside the batch: the lowest lane keeps it
+                    const uint32_t same = __match_any_sync(0xffffffffu, cand ? j : 0xffffffffu);
+                    cand = cand && (__ffs(same) - 1) == int(lane);
+                    const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+                    const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
+                    cand = cand && have + rank < want;
+                    if (cand) {
+                        uint32_t h = (j * 2654435761u) & (hs - 1);
+                        while (atomicCAS(&hset[h], 0xffffffffu, j) != 0xffffffffu) h = (h + 1) & (hs - 1);
+                        keys[have + rank] = uint64_t(j);  // id for now; distance below
+                    }
+                    have = min(want, have + __popc(bal));
+                    __syncwarp();
+                }
+            }
+            for (uint32_t t = lane; t < have; t += 32) {
+                const uint32_t j = uint32_t(keys[t]);
+                keys[t] = make_key(dist(j), j);
+            }
+        }
+        for (uint32_t t = have + lane; t < m; t += 32) keys[t] = kEmptyKey;
+        __syncwarp();
+        warp_bitonic_sort(keys, m);
+        uint64_t* pk = a.keys + size_t(i) * P;
+        uint8_t* pf = a.flags + size_t(i) * P;
+        for (uint32_t t = lane; t < P; t += 32) {
+            pk[t] = t < have ? keys[t] : kEmptyKey;
+            pf[t] = t < have ? 1 : 0;
+        }
+        if (lane == 0) {
+            a.sizes[i] = have;
+            atomicAdd(a.comps, (unsigned long long)have);
+        }
+        __syncwarp();
+    }
+}
+
 // -------------------------------------------------------------- sampling
 
 struct SampleArgs {
@@ -2121,6 +2246,30 @@ int annk_init_graph(const annk_dataset* ds, const annk_forest* fc, uint32_t k, u
     return abi([&] {
         if (!ds || !out) throw_invalid("init_graph: null argument");
         *out = init_graph_impl(ds, fc, k, conquer_depth, pool_cap, sample_cap, seed, 0, ds->n);
+    });
+}
+
+int annk_init_random(const annk_dataset* ds, uint32_t k, uint32_t pool_cap, uint32_t sample_cap, uint64_t seed,
+                     annk_state** out) {
+    return abi([&] {
+        if (!ds || !out) throw_invalid("init_random: null argument");
+        std::unique_ptr<annk_state> s(new_state(ds->n, k, pool_cap, sample_cap, seed));
+        const uint32_t n = ds->n;
+        DevBuf<unsigned long long> comps(1);
+        comps.zero();
+        InitArgs a{ds->data.p, n, ds->ld, 0, 0, pool_cap, nullptr, s->keys.p, s->flags.p, s->sizes.p, comps.p,
+                   nullptr, ds->u8 ? ds->data8.p : nullptr, ds->ld8, ds->u8 ? ds->norms8.p : nullptr};
+        const uint32_t wpb = 4;
+        const size_t sm = init_random_warp_bytes(pool_cap) * wpb;
+        if (sm > 200 * 1024) throw_invalid("init_random: pool_cap too large for the device path");
+        CK(cudaFuncSetAttribute(init_random_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        LAUNCH(init_random_kernel, std::min<uint32_t>((n + wpb - 1) / wpb, uint32_t(num_sms()) * 16), wpb * 32,
+               sm, a, seed);
+        unsigned long long c = 0;
+        comps.download(&c, 1);
+        ssync();
+        s->dist_comps = c;
+        *out = s.release();
     });
 }
 

@@ -351,3 +351,26 @@ def test_dataset_rejects_non_finite():
     x[37, 2] = np.inf
     with pytest.raises(A.InvalidArgument):
         A.VectorSet(x)
+
+
+# ------------------------------------------------- init_random (random-descent)
+
+@pytest.mark.parametrize("n,dim,k,P,S,seed,integer", [
+    (2000, 16, 10, 30, 10, 5, False),
+    (60, 8, 5, 80, 10, 2, False),        # pool_cap >= n-1: every other point
+    (3000, 128, 10, 40, 10, 7, True),    # u8 datapath
+    (500, 12, 10, 30, 20, 1234, False),
+])
+def test_init_random_bit_exact(n, dim, k, P, S, seed, integer):
+    o = ora()
+    x = mixture(n, dim, 20, seed) if integer else A.gen_synthetic(n, dim, seed)
+    so = o.init_random(o.vs(x), k, P, S, seed)
+    sd = A.init_random(x, k, P, S, seed)
+    e = assert_pools_equal(sd, so)
+    assert sd.meta()["dist_comps"] == e["dist_comps"]
+    vo = o.vs(x)
+    for _ in range(2):  # random-descent = init_random + NN-descent rounds
+        so.nn_descent_iteration(vo)
+        A.detail.nn_descent_iteration(sd, x)
+        e = assert_pools_equal(sd, so)
+        assert sd.meta()["dist_comps"] == e["dist_comps"]
