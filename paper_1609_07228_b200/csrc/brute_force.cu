@@ -10,6 +10,8 @@
 // second kernel.  Keys order by (dist, id), so ties break by id exactly like
 // NeighborPool (neighbor_pool.hpp:17-20).
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 
 #include "../../include/annkit_b200.h"
 #include "internal.cuh"
@@ -261,6 +263,211 @@ bf_tile_u8_kernel(const uint8_t* __restrict__ base8, const int32_t* __restrict__
     }
 }
 
+// ---------------------------------------------------- tensor-core u8 path
+// Exact kNN on the integer tensor cores: mma.sync.m16n8k32 u8 x u8 -> s32 is
+// exact (products <= 255^2, dim <= 128), so dist = |q|^2 + |b|^2 - 2 q.b equals
+// the reference's fp32 l2_sq bit-for-bit on the u8 datapath.
+// A CTA owns 64 queries; every warp keeps all 64 queries' A fragments in
+// registers for the whole base sweep.  Base tiles of 128 rows are staged in
+// shared memory with cp.async (double buffered, 144-byte padded stride so the
+// 32-bit B-fragment loads are conflict-free); each warp takes two 8-row column
+// blocks of the tile, 4 MMAs per B fragment.  The epilogue feeds the same
+// threshold filter and per-query sorted buffers as the CUDA-core kernels.
+constexpr int MQ = 32, MB = 128, MTHREADS = 256;  // queries per CTA (2 row groups)
+constexpr uint32_t kMmaStride = 144;  // bytes per staged base row (>= 128, 16-aligned, 4 mod 32 words)
+
+__device__ __forceinline__ void mma_u8(int32_t (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+    const uint32_t d = uint32_t(__cvta_generic_to_shared(smem_dst));
+    const int n = valid ? 16 : 0;  // zero-fill rows past the base set
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(n));
+}
+
+constexpr uint32_t kMmaStages = 4;  // cp.async ring depth
+
+
+template <int KS>  // 32-byte k-steps per row (ld8 <= 32 * KS)
+__global__ void __launch_bounds__(MTHREADS, 1)
+bf_mma_u8_kernel(const uint8_t* __restrict__ base8, const int32_t* __restrict__ bnorm, uint32_t nb,
+                 uint32_t ld8, const uint8_t* __restrict__ q8, const int32_t* __restrict__ qnorm, uint32_t nq,
+                 const uint32_t* __restrict__ self_ids, uint32_t k, uint32_t cb, uint32_t splits,
+                 uint32_t tiles_per_split, uint64_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t need_flush;
+    uint64_t* buf = reinterpret_cast<uint64_t*>(smem);       // MQ x cb
+    uint64_t* thr = buf + size_t(MQ) * cb;                   // MQ
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(thr + MQ);   // MQ
+    int32_t* bn = reinterpret_cast<int32_t*>(cnt + MQ);      // stages x MB base norms
+    unsigned char* sb = reinterpret_cast<unsigned char*>(bn + kMmaStages * MB);  // stages x MB x stride
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t g = lane >> 2, t4 = lane & 3;
+    const uint32_t q0 = blockIdx.x * MQ, split = blockIdx.y;
+    const uint32_t n_tiles = (nb + MB - 1) / MB;
+    const uint32_t t_begin = split * tiles_per_split, t_end = min(n_tiles, t_begin + tiles_per_split);
+    if (tid < MQ) {
+        cnt[tid] = 0;
+        thr[tid] = kEmptyKey;
+    }
+    if (tid == 0) need_flush = 0;
+    for (uint32_t j = tid; j < kMmaStages * MB; j += MTHREADS)
+        for (uint32_t c = ld8; c < 32u * KS; c += 4) *reinterpret_cast<uint32_t*>(sb + j * kMmaStride + c) = 0;
+    constexpr int RG = MQ / 16;
+    uint32_t a[RG][KS][4];
+    int32_t qn_r[2 * RG];
+    uint32_t self_r[2 * RG];
+#pragma unroll
+    for (int rg = 0; rg < RG; ++rg) {
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+            const uint32_t qi = q0 + rg * 16 + g + 8 * hr;
+            qn_r[rg * 2 + hr] = qi < nq ? qnorm[qi] : 0;
+            self_r[rg * 2 + hr] = (self_ids && qi < nq) ? self_ids[qi] : kInvalidId;
+        }
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t qi = q0 + rg * 16 + g + ((r & 1) ? 8 : 0);
+                const uint32_t kb = ks * 32 + ((r & 2) ? 16 : 0) + t4 * 4;
+                a[rg][ks][r] = (qi < nq && kb < ld8)
+                                   ? __ldg(reinterpret_cast<const uint32_t*>(q8 + size_t(qi) * ld8 + kb))
+                                   : 0u;
+            }
+    }
+    const uint32_t chunks = ld8 / 16;  // 16-byte chunks per base row
+    const bool pow2_chunks = chunks == 2 * KS && (chunks & (chunks - 1)) == 0;
+    const uint32_t cshift = 31 - __clz(max(chunks, 1u));
+    auto stage = [&](uint32_t t) {
+        if (t < t_end) {
+            const uint32_t b0 = t * MB, st = (t - t_begin) % kMmaStages;
+            unsigned char* dst = sb + size_t(st) * MB * kMmaStride;
+            for (uint32_t j = tid; j < MB * chunks; j += MTHREADS) {
+                const uint32_t r = pow2_chunks ? (j >> cshift) : j / chunks;
+                const uint32_t c = j - r * chunks;
+                const bool ok = b0 + r < nb;
+                cp_async16(dst + r * kMmaStride + c * 16, base8 + size_t(ok ? b0 + r : 0) * ld8 + c * 16, ok);
+            }
+            if (tid < MB) {
+                const bool ok = b0 + tid < nb;
+                const uint32_t d = uint32_t(__cvta_generic_to_shared(bn + st * MB + tid));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d),
+                             "l"(bnorm + (ok ? b0 + tid : 0)), "r"(ok ? 4 : 0));
+            }
+        }
+        asm volatile("cp.async.commit_group;");  // (empty groups keep the count uniform)
+    };
+#pragma unroll
+    for (uint32_t p = 0; p < kMmaStages - 1; ++p) stage(t_begin + p);
+    // keep iff qn + bn - 2 dot <= T  <=>  2 dot >= (qn - T) + bn; lim = qn - T (T = current
+    // k-th distance, an exact integer; ties pass and are settled by the exact key test)
+    int32_t lim[2 * RG];
+    uint64_t thr_k[2 * RG];
+#pragma unroll
+    for (int j = 0; j < 2 * RG; ++j) {
+        lim[j] = INT_MIN;
+        thr_k[j] = kEmptyKey;
+    }
+    const bool self_mode = self_ids != nullptr;
+    for (uint32_t t = t_begin; t < t_end; ++t) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kMmaStages - 2));
+        __syncthreads();  // tile t visible; buffers and thresholds settled; tile t-1's stage free
+        stage(t + kMmaStages - 1);
+#pragma unroll
+        for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+            for (int hr = 0; hr < 2; ++hr) {
+                const uint64_t tk = thr[rg * 16 + g + 8 * hr];
+                thr_k[rg * 2 + hr] = tk;
+                lim[rg * 2 + hr] = tk == kEmptyKey ? INT_MIN : qn_r[rg * 2 + hr] - int32_t(key_dist(tk));
+            }
+        const uint32_t st = (t - t_begin) % kMmaStages;
+        const uint32_t b0 = t * MB;
+        const unsigned char* tile = sb + size_t(st) * MB * kMmaStride;
+        const bool full = b0 + MB <= nb;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const uint32_t cbk = warp + 8 * half;  // 8-row column block of the tile
+            const uint32_t col0 = cbk * 8 + 2 * t4, bj0 = b0 + col0;
+            const int32_t bn0 = bn[st * MB + col0], bn1 = bn[st * MB + col0 + 1];
+            int32_t acc[RG][4];
+#pragma unroll
+            for (int rg = 0; rg < RG; ++rg)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[rg][r] = 0;
+            const unsigned char* brow = tile + (cbk * 8 + g) * kMmaStride + t4 * 4;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const uint32_t b0r = *reinterpret_cast<const uint32_t*>(brow + ks * 32);
+                const uint32_t b1r = *reinterpret_cast<const uint32_t*>(brow + ks * 32 + 16);
+#pragma unroll
+                for (int rg = 0; rg < RG; ++rg) mma_u8(acc[rg], a[rg][ks], b0r, b1r);
+            }
+#pragma unroll
+            for (int rg = 0; rg < RG; ++rg) {
+#pragma unroll
+                for (int hr = 0; hr < 2; ++hr) {
+                    const int qq = rg * 2 + hr;
+#pragma unroll
+                    for (int hc = 0; hc < 2; ++hc) {
+                        const int32_t two_dot = 2 * acc[rg][hr * 2 + hc];
+                        if (two_dot < lim[qq] + (hc ? bn1 : bn0)) continue;  // cheap reject (most pairs)
+                        const uint32_t bj = bj0 + hc;
+                        const uint32_t ql = rg * 16 + g + 8 * hr;
+                        if (q0 + ql >= nq || (!full && bj >= nb) || (self_mode && bj == self_r[qq])) continue;
+                        const uint64_t key = make_key(float(qn_r[qq] + (hc ? bn1 : bn0) - two_dot), bj);
+                        if (key < thr_k[qq]) {
+                            const uint32_t slot = atomicAdd(&cnt[ql], 1u);
+                            buf[size_t(ql) * cb + slot] = key;
+                            if (slot + 1 + MB > cb) need_flush = 1;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (need_flush) {  // uniform: read after the barrier
+            for (uint32_t ql = warp; ql < MQ; ql += MTHREADS / 32) {
+                const uint32_t c = cnt[ql];
+                if (c + MB <= cb) continue;
+                uint64_t* bq = buf + size_t(ql) * cb;
+                for (uint32_t j = c + lane; j < cb; j += 32) bq[j] = kEmptyKey;
+                __syncwarp();
+                warp_bitonic_sort(bq, cb);
+                if (lane == 0) {
+                    const uint32_t keep = min(c, k);
+                    cnt[ql] = keep;
+                    if (keep == k) thr[ql] = bq[k - 1];
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+            if (tid == 0) need_flush = 0;
+        }
+    }
+    asm volatile("cp.async.wait_group 0;");
+    __syncthreads();
+    for (uint32_t ql = warp; ql < MQ; ql += MTHREADS / 32) {
+        const uint32_t qi = q0 + ql;
+        if (qi >= nq) continue;
+        const uint32_t c = cnt[ql];
+        uint64_t* bq = buf + size_t(ql) * cb;
+        for (uint32_t j = c + lane; j < cb; j += 32) bq[j] = kEmptyKey;
+        __syncwarp();
+        warp_bitonic_sort(bq, cb);
+        uint64_t* o = out + (size_t(qi) * splits + split) * k;
+        for (uint32_t j = lane; j < k; j += 32) o[j] = bq[j];
+        __syncwarp();
+    }
+}
+
 __global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int32_t* __restrict__ norms,
                                       uint32_t ld8, const uint32_t* __restrict__ rows, uint32_t nr,
                                       uint8_t* __restrict__ dst, int32_t* __restrict__ dnorms) {
@@ -387,8 +594,53 @@ void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q
         ssync();
         return;
     }
-    const uint32_t cb = next_pow2(k + BT);
     const bool u8 = base->u8 && q8 != nullptr;
+    if (u8 && base->ld8 <= 128 && k <= 128 && !getenv("ANNK_BF_DP4A")) {
+        // tensor-core path
+        // buffer room past the kept k decides how often a query's buffer is sorted
+        const uint32_t cbm = std::max(next_pow2(k + MB), 512u);
+        const size_t smem = size_t(MQ) * cbm * 8 + MQ * 8 + MQ * 4 + kMmaStages * MB * 4 +
+                            size_t(kMmaStages) * MB * kMmaStride;
+        const uint32_t ks = (base->ld8 + 31) / 32;
+        const void* fn = ks == 1 ? reinterpret_cast<const void*>(bf_mma_u8_kernel<1>)
+                         : ks == 2 ? reinterpret_cast<const void*>(bf_mma_u8_kernel<2>)
+                         : ks == 3 ? reinterpret_cast<const void*>(bf_mma_u8_kernel<3>)
+                                   : reinterpret_cast<const void*>(bf_mma_u8_kernel<4>);
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, MTHREADS, smem));
+        const uint32_t qtiles = (nq + MQ - 1) / MQ;
+        const uint32_t n_tiles = (nb + MB - 1) / MB;
+        const uint32_t want = uint32_t(num_sms()) * std::max(per_sm, 1) * 2;
+        uint32_t splits = std::max(1u, std::min(n_tiles, (want + qtiles - 1) / qtiles));
+        splits = std::min(splits, std::max(1u, 4096u / k));
+        const uint32_t tps = (n_tiles + splits - 1) / splits;
+        splits = (n_tiles + tps - 1) / tps;
+        DevBuf<uint64_t> part(splits == 1 ? 0 : size_t(nq) * splits * k);
+        uint64_t* dst = splits == 1 ? out_keys : part.p;
+        const dim3 grid(qtiles, splits);
+        if (ks == 1)
+            LAUNCH(bf_mma_u8_kernel<1>, grid, MTHREADS, smem, base->data8.p, base->norms8.p, nb, base->ld8, q8,
+                   qnorm, nq, self_ids, k, cbm, splits, tps, dst);
+        else if (ks == 2)
+            LAUNCH(bf_mma_u8_kernel<2>, grid, MTHREADS, smem, base->data8.p, base->norms8.p, nb, base->ld8, q8,
+                   qnorm, nq, self_ids, k, cbm, splits, tps, dst);
+        else if (ks == 3)
+            LAUNCH(bf_mma_u8_kernel<3>, grid, MTHREADS, smem, base->data8.p, base->norms8.p, nb, base->ld8, q8,
+                   qnorm, nq, self_ids, k, cbm, splits, tps, dst);
+        else
+            LAUNCH(bf_mma_u8_kernel<4>, grid, MTHREADS, smem, base->data8.p, base->norms8.p, nb, base->ld8, q8,
+                   qnorm, nq, self_ids, k, cbm, splits, tps, dst);
+        if (splits > 1) {
+            const uint32_t m = next_pow2(splits * k);
+            const uint32_t wpb = std::max(1u, std::min(8u, uint32_t(64 * 1024 / (m * 8))));
+            CK(cudaFuncSetAttribute(bf_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(wpb * m * 8)));
+            LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part.p, nq, splits, k, m, out_keys);
+        }
+        return;
+    }
+    const uint32_t cb = next_pow2(k + BT);
     const size_t smem =
         u8 ? size_t(QT) * cb * 8 + QT * 8 + QT * 4 * 3 + BT * 4 + size_t(QT + BT) * (base->ld8 / 4 + 4) * 4
            : size_t(QT) * cb * 8 + QT * 8 + QT * 4 * 2 + size_t(QT + BT) * (DC + 1) * 4;

@@ -136,6 +136,8 @@ struct InitScratch {
     uint32_t* sib;
     uint32_t sib_cap;
     uint32_t* cnt;  // [0] unique count, [1] sibling count, [2] overflow flag
+    const uint8_t* pf_base;  // rows to prefetch into L2 on first insert (nullptr: none)
+    uint32_t pf_ld;
 };
 
 __device__ __forceinline__ void hs_insert(const InitScratch& w, uint32_t id) {
@@ -147,6 +149,8 @@ __device__ __forceinline__ void hs_insert(const InitScratch& w, uint32_t id) {
             const uint32_t u = atomicAdd(&w.cnt[0], 1u);
             if (u < w.cap) w.uniq[u] = id;
             else w.cnt[2] = 1;
+            // the candidate's row is gathered after collection: start it on its way to L2
+            if (w.pf_base) asm volatile("prefetch.global.L2 [%0];" ::"l"(w.pf_base + size_t(id) * w.pf_ld));
             return;
         }
         if (old == id) return;
@@ -409,6 +413,8 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
     w.tslots = kInitCap;
     w.uniq = w.table + kInitCap;
     w.cap = kInitCap;
+    w.pf_base = a.x8;
+    w.pf_ld = a.ld8;
     float* q = reinterpret_cast<float*>(w.uniq + kInitCap);
     w.sib = reinterpret_cast<uint32_t*>(q + a.ld);
     w.sib_cap = sib_cap;
@@ -446,6 +452,8 @@ __global__ void init_overflow_kernel(InitArgs a, const uint32_t* list, uint32_t 
         w.uniq = w.table + 2 * cap;
         w.cap = cap;
         w.tslots = 2 * cap;
+        w.pf_base = nullptr;
+        w.pf_ld = 0;
         w.sib = w.uniq + cap;
         w.sib_cap = sib_cap;
         w.cnt = s_misc + 256;

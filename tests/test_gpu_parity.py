@@ -374,3 +374,21 @@ def test_init_random_bit_exact(n, dim, k, P, S, seed, integer):
         A.detail.nn_descent_iteration(sd, x)
         e = assert_pools_equal(sd, so)
         assert sd.meta()["dist_comps"] == e["dist_comps"]
+
+
+@pytest.mark.parametrize("n,dim,k,nq", [(5000, 128, 100, 300), (3000, 40, 10, 77), (700, 16, 128, 0), (2100, 100, 7, 0)])
+def test_brute_force_tensor_core_path_matches_dp4a_and_oracle(n, dim, k, nq):
+    import os
+    x = mixture(n, dim, 25, 8)
+    q = mixture(nq, dim, 25, 8, stream=2) if nq else None
+    ids_mma, d_mma = A.brute_force_knn(x, q, k, with_dists=True)
+    os.environ["ANNK_BF_DP4A"] = "1"
+    try:
+        ids_cc, d_cc = A.brute_force_knn(x, q, k, with_dists=True)
+    finally:
+        del os.environ["ANNK_BF_DP4A"]
+    np.testing.assert_array_equal(ids_mma, ids_cc)
+    np.testing.assert_array_equal(d_mma.view(np.uint32), d_cc.view(np.uint32))
+    o = ora()
+    ids_o = o.brute_force(o.vs(x), o.vs(q) if nq else None, k)
+    np.testing.assert_array_equal(ids_mma, ids_o)
