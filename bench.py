@@ -50,6 +50,10 @@ CONFIGS = {
     "cfg1": dict(n=100_000, dim=128, n_queries=1000, centers=100, trees=4, leaf=10, k=10, P=30, S=10,
                  max_iters=8, dep=4, k_return=10, sweep=[50, 100, 200], acc_sample=10_000, ref_points=100_000,
                  ref_queries=1000),
+    # configs[2]: 960-d float data in [0,1] (GIST-like; the exact fp32 datapath, leaf 10 assumed)
+    "cfg3": dict(n=1_000_000, dim=960, n_queries=1000, centers=500, trees=8, leaf=10, k=100, P=100, S=20,
+                 max_iters=10, dep=4, k_return=100, sweep=[100, 200, 400, 800], acc_sample=2000, ref_points=16_384,
+                 ref_queries=100, mix=(0.05, 0.35, 0.05, 0.0, 1.0, False)),
     # a small smoke-sized case for quick checks
     "tiny": dict(n=50_000, dim=128, n_queries=1000, centers=100, trees=4, leaf=8, k=20, P=40, S=10,
                  max_iters=6, dep=4, k_return=20, sweep=[40, 80, 160], acc_sample=2000, ref_points=50_000,
@@ -61,9 +65,9 @@ SEED = 1
 def gen_data(cfg, n=None):
     import paper_1609_07228_b200 as A
     n = cfg["n"] if n is None else n
-    base = A.gen_mixture(n, cfg["dim"], cfg["centers"], 0.0, 128.0, 16.0, 0.0, 255.0, True, SEED, 1)
-    queries = A.gen_mixture(cfg["n_queries"], cfg["dim"], cfg["centers"], 0.0, 128.0, 16.0, 0.0, 255.0, True,
-                            SEED, 2)
+    lo, hi, sd, clo, chi, rnd = cfg.get("mix", (0.0, 128.0, 16.0, 0.0, 255.0, True))
+    base = A.gen_mixture(n, cfg["dim"], cfg["centers"], lo, hi, sd, clo, chi, rnd, SEED, 1)
+    queries = A.gen_mixture(cfg["n_queries"], cfg["dim"], cfg["centers"], lo, hi, sd, clo, chi, rnd, SEED, 2)
     return base, queries
 
 
@@ -626,7 +630,7 @@ def main():
                     help="N>1 collectives; gloo keeps buffers on the host (functional runs on one GPU)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
-    cfg.setdefault("ref_iters", {"cfg2": 2, "cfg1": 3, "tiny": 3}[args.config])
+    cfg.setdefault("ref_iters", {"cfg2": 2, "cfg1": 3, "cfg3": 3, "tiny": 3}[args.config])
     ws, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, cfg, ws, rank)

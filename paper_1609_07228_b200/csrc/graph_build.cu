@@ -1351,6 +1351,164 @@ join_warp_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const
     }
 }
 
+// Warp-per-point join for wide fp32 rows (rows too large to stage per point,
+// e.g. d = 960).  Same pairs, distances, offers and counters as the other
+// joins.  Each lane owns a partner member y (its row streamed through L1), the
+// candidate rows x are broadcast loads, and every lane runs kXB pairs' exact
+// sequential fp32 chains interleaved (dims in ascending order, 4 at a time),
+// so the dependent-add latency is covered by independent chains.  Accepted
+// offers go to a per-warp buffer flushed with one global atomic per member.
+constexpr uint32_t kWJW = 8;    // warps per CTA
+constexpr uint32_t kWOB = 512;  // offers buffered per warp
+constexpr uint32_t kXB = 16;    // candidate rows whose chains run interleaved per lane
+
+__host__ __device__ __forceinline__ size_t join_wide_bytes(uint32_t rmax) {
+    // okey (u64) + thr (u64) + ids, mcnt, mbase, mfix, msp (u32) + omem (u16)
+    return (size_t(kWOB) * 8 + size_t(rmax) * 8 + size_t(rmax) * 20 + size_t(kWOB) * 2 + 15) & ~size_t(15);
+}
+
+__device__ __forceinline__ void join_wide_flush(const JoinArgs& a, uint32_t oc, const uint64_t* okey,
+                                                const uint16_t* omem, const uint32_t* ids, uint32_t R,
+                                                uint32_t* mcnt, uint32_t* mbase, uint32_t* mfix, uint32_t* msp) {
+    const uint32_t lane = lane_id();
+    for (uint32_t e = lane; e < oc; e += 32) atomicAdd(&mcnt[omem[e]], 1u);
+    __syncwarp();
+    for (uint32_t m = lane; m < R; m += 32) {
+        const uint32_t cnt = mcnt[m];
+        if (cnt) {
+            const uint32_t base = atomicAdd(&a.ocnt[ids[m]], cnt);
+            const uint32_t fix = base < a.cap ? min(cnt, a.cap - base) : 0u;
+            mbase[m] = base;
+            mfix[m] = fix;
+            msp[m] = cnt > fix ? atomicAdd(a.ov_cnt, cnt - fix) : 0u;
+        }
+        mcnt[m] = 0;
+    }
+    __syncwarp();
+    for (uint32_t e = lane; e < oc; e += 32) {
+        const uint32_t m = omem[e];
+        const uint32_t r = atomicAdd(&mcnt[m], 1u);
+        const uint32_t owner = ids[m];
+        if (r < mfix[m]) {
+            a.obuf[size_t(owner) * a.cap + mbase[m] + r] = okey[e];
+        } else {
+            const uint32_t o = msp[m] + (r - mfix[m]);
+            if (o < a.ov_cap) {
+                a.ov_tgt[o] = owner;
+                a.ov_key[o] = okey[e];
+            }
+        }
+    }
+    __syncwarp();
+    for (uint32_t m = lane; m < R; m += 32) mcnt[m] = 0;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWJW * 32) join_wide_kernel(JoinArgs a, uint32_t rmax) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
+    const uint32_t ltm = (1u << lane) - 1u;
+    unsigned char* base = smem + size_t(warp) * join_wide_bytes(rmax);
+    uint64_t* okey = reinterpret_cast<uint64_t*>(base);
+    uint64_t* thr_s = okey + kWOB;
+    uint32_t* ids = reinterpret_cast<uint32_t*>(thr_s + rmax);
+    uint32_t* mcnt = ids + rmax;
+    uint32_t* mbase = mcnt + rmax;
+    uint32_t* mfix = mbase + rmax;
+    uint32_t* msp = mfix + rmax;
+    uint16_t* omem = reinterpret_cast<uint16_t*>(msp + rmax);
+    unsigned long long comps = 0, offers = 0;
+    for (uint32_t m = lane; m < rmax; m += 32) mcnt[m] = 0;
+    for (uint32_t w = blockIdx.x * kWJW + warp; w < a.n; w += gridDim.x * kWJW) {
+        const uint32_t i = a.order ? a.order[w] : w;
+        const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
+        if (A == 0) continue;  // uniform across the warp
+        const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
+        const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
+        __syncwarp();
+        for (uint32_t r = lane; r < R; r += 32) {
+            const uint32_t id = r < A ? nw[r] : od[r - A];
+            ids[r] = id;
+            thr_s[r] = a.thr[id];
+        }
+        __syncwarp();
+        uint32_t oc = 0;
+        for (uint32_t y0 = 1; y0 < R; y0 += 32) {
+            const uint32_t y = y0 + lane;
+            const bool yv = y < R;
+            const uint32_t idy = yv ? ids[y] : ids[0];
+            const uint64_t thy = yv ? thr_s[y] : 0ull;
+            const float4* yrow = reinterpret_cast<const float4*>(a.x + size_t(idy) * a.ld);
+            const uint32_t xmax = min(A, y0 + 31);  // some lane has x < y
+            for (uint32_t x0 = 0; x0 < xmax; x0 += kXB) {
+                const uint32_t nx = min(kXB, xmax - x0);
+                uint32_t xid[kXB];
+#pragma unroll
+                for (uint32_t u = 0; u < kXB; ++u) xid[u] = ids[x0 + min(u, nx - 1)];
+                float acc[kXB];
+#pragma unroll
+                for (uint32_t u = 0; u < kXB; ++u) acc[u] = 0.0f;
+                for (uint32_t c = 0; c < a.ld / 4; ++c) {  // ld is a multiple of 4 (zero padded)
+                    const float4 yv4 = __ldg(yrow + c);
+#pragma unroll
+                    for (uint32_t u = 0; u < kXB; ++u) {
+                        const float4 xv = __ldg(reinterpret_cast<const float4*>(a.x + size_t(xid[u]) * a.ld) + c);
+                        float d;
+                        d = __fsub_rn(xv.x, yv4.x); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                        d = __fsub_rn(xv.y, yv4.y); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                        d = __fsub_rn(xv.z, yv4.z); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                        d = __fsub_rn(xv.w, yv4.w); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                    }
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < kXB; ++u) {
+                    if (u >= nx) break;
+                    const uint32_t x = x0 + u, idx = xid[u];
+                    const bool pair = yv && y > x && idx != idy;  // graph_build.cpp:146 (l == j)
+                    comps += pair ? 1u : 0u;
+                    const uint64_t kx = make_key(acc[u], idy);  // offer y to x's pool
+                    const uint64_t ky = make_key(acc[u], idx);  // offer x to y's pool
+                    const bool ox = pair && kx < thr_s[x];
+                    const bool oy = pair && ky < thy;
+                    const uint32_t bx = __ballot_sync(0xffffffffu, ox);
+                    const uint32_t by = __ballot_sync(0xffffffffu, oy);
+                    if (ox) {
+                        const uint32_t pos = oc + __popc(bx & ltm);
+                        okey[pos] = kx;
+                        omem[pos] = uint16_t(x);
+                    }
+                    oc += __popc(bx);
+                    if (oy) {
+                        const uint32_t pos = oc + __popc(by & ltm);
+                        okey[pos] = ky;
+                        omem[pos] = uint16_t(y);
+                    }
+                    oc += __popc(by);
+                    if (oc > kWOB - 64) {  // one pair adds at most 64 offers
+                        __syncwarp();
+                        offers += oc;
+                        join_wide_flush(a, oc, okey, omem, ids, R, mcnt, mbase, mfix, msp);
+                        oc = 0;
+                    }
+                }
+            }
+        }
+        if (oc) {
+            __syncwarp();
+            offers += oc;
+            join_wide_flush(a, oc, okey, omem, ids, R, mcnt, mbase, mfix, msp);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        comps += __shfl_xor_sync(0xffffffffu, comps, o);
+        offers += __shfl_xor_sync(0xffffffffu, offers, o);
+    }
+    if (lane == 0) {
+        if (comps) atomicAdd(a.comps, comps);
+        if (offers) atomicAdd(a.offers, offers);
+    }
+}
+
 // ----------------------------------------------------------------- merge
 
 struct MergeArgs {
@@ -2052,9 +2210,14 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
                                                              staged_smem));
             const uint32_t grid = std::min<uint32_t>(n_visit, uint32_t(num_sms()) * std::max(per_sm, 1));
             LAUNCH(join_staged_kernel, grid, kJoinThreads, staged_smem, ja, order, rmax);
-        } else {
-            const uint32_t wpb = 8;
-            LAUNCH(join_kernel, (n_visit + wpb - 1) / wpb, wpb * 32, wpb * ds->ld * 4, ja);
+        } else {  // wide fp32 rows: warp per point, rows streamed through L1
+            const size_t sm = join_wide_bytes(rmax) * kWJW;
+            CK(cudaFuncSetAttribute(join_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_wide_kernel, kWJW * 32, sm));
+            const uint32_t grid = std::min<uint32_t>((n_visit + kWJW - 1) / kWJW,
+                                                     uint32_t(num_sms()) * std::max(per_sm, 1));
+            LAUNCH(join_wide_kernel, grid, kWJW * 32, sm, ja, rmax);
         }
         s->ov_count.download(&spilled, 1);
         ssync();

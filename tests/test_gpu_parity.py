@@ -392,3 +392,20 @@ def test_brute_force_tensor_core_path_matches_dp4a_and_oracle(n, dim, k, nq):
     o = ora()
     ids_o = o.brute_force(o.vs(x), o.vs(q) if nq else None, k)
     np.testing.assert_array_equal(ids_mma, ids_o)
+
+
+def test_wide_fp32_rows_join_bit_exact():
+    # d = 960 float rows (cfg3 shape): the join streams rows through L1 (join_wide_kernel)
+    o = ora()
+    x = mixture(1500, 960, 12, 3, lo=0.05, hi=0.35, sd=0.05, clip=(0.0, 1.0), rnd=False)
+    vo = o.vs(x)
+    fo = o.build_forest(vo, 3, 10, 3)
+    so = o.init_graph(vo, fo, 10, 4, 30, 10, 3)
+    fd = A.build_forest(x, 3, 10, 3)
+    sd = A.init_graph(x, fd, 10, 4, 30, 10, 3)
+    assert_pools_equal(sd, so)
+    for _ in range(3):
+        so.nn_descent_iteration(vo)
+        A.detail.nn_descent_iteration(sd, x)
+        e = assert_pools_equal(sd, so)
+        assert sd.meta()["dist_comps"] == e["dist_comps"]
