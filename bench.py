@@ -329,8 +329,11 @@ def run_gpu(args, cfg, ws, rank, local):
     sweep = []
     chosen = None
     kr = cfg["k_return"]
-    for P in cfg["sweep"]:
-        p = A.SearchParams(k_return=kr, pool_size=P, expansion=P, iters=4)
+    # the reference's search knobs (search.hpp:13-21): pool P (>= k_return), seeds kept E <= P,
+    # expansion rounds I; the fastest point reaching recall@k_return >= 0.9 is the headline
+    grid = [(P, E, it) for P in cfg["sweep"][:2] for E in (8, 16, 32, 64, P) for it in (1, 2, 4) if E <= P]
+    for P, E, it in grid:
+        p = A.SearchParams(k_return=kr, pool_size=P, expansion=E, iters=it)
         searcher.search_batch(qs, p)  # warm
         e0 = ev()
         r = searcher.search_batch(qs, p)
@@ -338,13 +341,11 @@ def run_gpu(args, cfg, ws, rank, local):
         torch.cuda.synchronize()
         dt = e0.elapsed_time(e1) / 1e3
         rec = float(np.mean([len(np.intersect1d(r.ids[i], gt_q[i])) / kr for i in range(len(gt_q))]))
-        row = {"pool": P, "expansion": P, "recall": round(rec, 4), "qps": round(cfg["n_queries"] / dt, 1),
-               "dist_comps_per_query": float(r.stats[:, 0].mean())}
+        row = {"pool": P, "expansion": E, "iters": it, "recall": round(rec, 4),
+               "qps": round(cfg["n_queries"] / dt, 1), "dist_comps_per_query": float(r.stats[:, 0].mean())}
         sweep.append(row)
-        if chosen is None and rec >= 0.9:
+        if rec >= 0.9 and (chosen is None or row["qps"] > chosen["qps"]):
             chosen = row
-            if not args.full_log:
-                break
 
     # e2e through the C-ABI from pinned host memory
     pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
@@ -547,8 +548,9 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
     # search: every rank holds the full index and answers its query shard
     searcher = A.GraphSearcher(vs, forest, graph)
     sweep, chosen = [], None
-    for P in cfg["sweep"]:
-        p = A.SearchParams(k_return=kr, pool_size=P, expansion=P, iters=4)
+    grid = [(P, E, it) for P in cfg["sweep"][:2] for E in (8, 16, 32, 64, P) for it in (1, 2, 4) if E <= P]
+    for P, E, it in grid:
+        p = A.SearchParams(k_return=kr, pool_size=P, expansion=E, iters=it)
         searcher.search_batch(qs, p)
         barrier(ws)
         e0 = ev()
@@ -558,12 +560,11 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
         dt = max_over_ranks(ws, e0.elapsed_time(e1) / 1e3)
         hits = sum(len(np.intersect1d(r.ids[i], gt_q[i])) for i in range(len(gt_q)))
         rec = comm.allreduce_sum(hits) / (cfg["n_queries"] * kr)
-        row = {"pool": P, "expansion": P, "recall": round(rec, 4), "qps": round(cfg["n_queries"] / dt, 1)}
+        row = {"pool": P, "expansion": E, "iters": it, "recall": round(rec, 4),
+               "qps": round(cfg["n_queries"] / dt, 1)}
         sweep.append(row)
-        if chosen is None and rec >= 0.9:
+        if rec >= 0.9 and (chosen is None or row["qps"] > chosen["qps"]):
             chosen = row
-            if not args.full_log:
-                break
 
     # e2e: host dataset in, own graph rows out, per rank
     pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
