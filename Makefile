@@ -7,7 +7,10 @@ SRCS      := $(wildcard $(PKG)/csrc/*.cu)
 OBJS      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 LIB       := $(PKG)/libannkit_b200.so
 
-all: $(LIB) oracle
+FACADE    := $(PKG)/libannkit_facade.so
+FACADE_T  := tests/cpp/test_facade
+
+all: $(LIB) $(FACADE) $(FACADE_T) oracle
 
 build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/annkit_b200.h
 	@mkdir -p build
@@ -16,11 +19,19 @@ build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/annkit_b200.h
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
 
+# C++ host API (include/annkit_b200.hpp) over the C-ABI, and its test program
+$(FACADE): $(PKG)/cpp/annkit_facade.cpp include/annkit_b200.hpp include/annkit_b200.h $(LIB)
+	g++ -std=c++20 -O2 -fPIC -shared -Wall -Iinclude -o $@ $< -L$(PKG) -lannkit_b200 -Wl,-rpath,'$$ORIGIN'
+
+$(FACADE_T): tests/cpp/test_facade.cpp include/annkit_b200.hpp $(FACADE)
+	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lannkit_facade -lannkit_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(FACADE) $(FACADE_T)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

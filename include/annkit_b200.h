@@ -3,7 +3,7 @@
  * NVIDIA B200 (sm_100a).
  *
  * The reference ("annkit", /root/reference/proj) exposes its hot path as a
- * C++ library API (free functions over value types, proj/include/annkit/*.hpp);
+ * C++ library API (free functions over value types, proj/include/annkit/ headers);
  * it has no plugin registry or FFI.  This header is the thin C layer that the
  * reference-shaped host API (paper_1609_07228_b200/api.py, and any C++/ctypes
  * caller) binds: plain pointers and sizes, no torch types, opaque handles for
@@ -229,7 +229,8 @@ typedef struct {
     uint32_t n_trees_used;
     uint32_t random_seed_count;
     uint64_t seed;
-    int32_t random_init;        /* 1 = search_random_init (search.cpp:156-180) */
+    int32_t random_init;        /* 1 = search_random_init (search.cpp:156-180) with per-query seed
+                                   substream(seed, qi); 2 = the same with `seed` used as given */
 } annk_search_params;
 /* search.cpp:121-154 GraphSearcher::search for a batch of queries (host
  * nq x dim).  Per-query seed = substream(params.seed, qi) as in recall_curve

@@ -1,0 +1,286 @@
+// annkit_b200.hpp — the C++ host API of the B200 framework.
+//
+// Source-compatible with the reference library's hot-path API (namespace
+// annkit, proj/include/annkit/{dataset,kd_forest,neighbor_pool,graph_build,
+// knn_graph,search,eval}.hpp): same type names and fields, same function
+// names, signatures and exceptions, so a caller of the CPU library can switch
+// by changing the include and the link line.  Every entry point runs on the
+// device through the C-ABI in annkit_b200.h (libannkit_facade.so links
+// libannkit_b200.so); results are bit-identical to the reference at
+// workers = 1.  `workers` arguments are accepted and ignored.
+//
+// Device residency: VectorSet, KdForest and RefineState carry a shared
+// handle to their device copy (uploaded on first use; the reference declares
+// these immutable after construction, and so does this API).  RefineState's
+// host fields (pools, g_new, g_old, g_rnew, g_rold, counters) are refreshed
+// after every call that changes the device state, which is what the
+// reference's unit tests inspect; that copy costs O(n * pool_cap) per call.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace annkit {
+
+constexpr std::uint32_t kInvalidId = 0xffffffffu;
+constexpr std::uint32_t kLeafMarker = 0xffffffffu;
+
+struct DeviceDataset;  // opaque device copies (annk_dataset / annk_forest / annk_state)
+struct DeviceForest;
+struct DeviceState;
+
+// ------------------------------------------------------------ dataset.hpp
+struct VectorSet {
+    std::uint32_t n = 0;
+    std::uint32_t dim = 0;
+    std::vector<float> data;  // row-major n x dim
+    mutable std::shared_ptr<DeviceDataset> device;  // set on first device use
+
+    std::span<const float> row(std::uint32_t i) const { return {data.data() + std::size_t(i) * dim, dim}; }
+    const float* row_ptr(std::uint32_t i) const { return data.data() + std::size_t(i) * dim; }
+};
+
+struct GroundTruth {
+    std::uint32_t n = 0;
+    std::uint32_t k = 0;
+    std::vector<std::uint32_t> ids;  // n x k
+
+    std::span<const std::uint32_t> row(std::uint32_t i) const { return {ids.data() + std::size_t(i) * k, k}; }
+};
+
+// dataset.cpp:201-214 (same bytes as the reference's generator).
+VectorSet gen_synthetic(std::uint32_t n, std::uint32_t dim, std::uint64_t seed);
+
+// ---------------------------------------------------------- kd_forest.hpp
+struct KdNode {
+    std::uint32_t split_dim = kLeafMarker;
+    float split_val = 0.0f;
+    std::uint32_t left = 0;   // internal: left child; leaf: first slot of its point_index range
+    std::uint32_t right = 0;  // internal: right child; leaf: one past its last slot
+    std::uint32_t depth = 0;
+    bool even_split = false;
+
+    bool is_leaf() const { return split_dim == kLeafMarker; }
+};
+
+struct KdTree {
+    std::vector<KdNode> nodes;
+    std::uint32_t root = 0;
+    std::uint32_t leaf_cap = 0;
+    std::uint32_t n = 0;
+    std::uint32_t dim = 0;
+    std::vector<std::uint32_t> point_index;
+    std::uint32_t leaf_count = 0;
+
+    std::span<const std::uint32_t> leaf_points(std::uint32_t node) const {
+        return {point_index.data() + nodes[node].left, nodes[node].right - nodes[node].left};
+    }
+};
+
+struct KdForest {
+    std::vector<KdTree> trees;
+    std::uint64_t seed = 0;
+    std::uint32_t n = 0;
+    std::uint32_t dim = 0;
+    std::uint32_t leaf_cap = 0;
+    mutable std::shared_ptr<DeviceForest> device;  // the device forest (built or imported)
+};
+
+KdForest build_forest(const VectorSet& vs, std::uint32_t n_trees, std::uint32_t leaf_cap, std::uint64_t seed,
+                      std::uint32_t workers = 1);
+std::vector<std::uint32_t> search_leaves(const KdTree& tree, std::span<const float> q, std::uint32_t n_leaves);
+std::uint32_t descend_from(const KdTree& tree, std::span<const float> q, std::uint32_t node);
+
+// ------------------------------------------------------ neighbor_pool.hpp
+struct NeighborEntry {
+    std::uint32_t id;
+    float dist;
+    bool flag_new;
+    bool checked;
+};
+
+// Host view of one device pool (ascending (dist, id)).
+class NeighborPool {
+  public:
+    NeighborPool() = default;
+    explicit NeighborPool(std::uint32_t capacity) : capacity_(capacity) {}
+    std::span<const NeighborEntry> entries() const { return entries_; }
+    std::uint32_t size() const { return std::uint32_t(entries_.size()); }
+    std::uint32_t capacity() const { return capacity_; }
+    bool contains(std::uint32_t id) const {
+        for (const auto& e : entries_)
+            if (e.id == id) return true;
+        return false;
+    }
+    std::vector<NeighborEntry>& mutable_entries() { return entries_; }
+
+  private:
+    std::vector<NeighborEntry> entries_;
+    std::uint32_t capacity_ = 0;
+};
+
+// -------------------------------------------------------- knn_graph.hpp
+struct KnnGraph {
+    std::uint32_t n = 0;
+    std::uint32_t k = 0;
+    std::vector<std::uint32_t> ids;  // n x k, rows ascending by (dist, id)
+    std::vector<float> dists;
+
+    std::span<const std::uint32_t> row(std::uint32_t i) const { return {ids.data() + std::size_t(i) * k, k}; }
+    std::span<const float> row_dists(std::uint32_t i) const { return {dists.data() + std::size_t(i) * k, k}; }
+    bool has_dists() const { return !dists.empty(); }
+};
+
+// ------------------------------------------------------ graph_build.hpp
+struct RefineState {
+    std::uint32_t k = 0;
+    std::uint32_t pool_cap = 0;
+    std::uint32_t sample_cap = 0;
+    std::uint64_t seed = 0;
+    std::uint32_t iteration = 0;
+    std::uint64_t dist_comps = 0;
+    std::uint64_t last_changes = 0;  // see DESIGN.md "Deviations": surviving inserts of the round
+
+    std::vector<NeighborPool> pools;
+    std::vector<std::vector<std::uint32_t>> g_new, g_old, g_rnew, g_rold;
+    std::shared_ptr<DeviceState> device;
+
+    std::uint32_t n() const { return std::uint32_t(pools.size()); }
+};
+
+RefineState init_graph(const VectorSet& vs, const KdForest& forest, std::uint32_t k, std::uint32_t conquer_depth,
+                       std::uint32_t pool_cap, std::uint32_t sample_cap, std::uint64_t seed,
+                       std::uint32_t workers = 1);
+RefineState init_random(const VectorSet& vs, std::uint32_t k, std::uint32_t pool_cap, std::uint32_t sample_cap,
+                        std::uint64_t seed, std::uint32_t workers = 1);
+void refine_nn_descent(RefineState& state, const VectorSet& vs, std::uint32_t max_iters, std::uint32_t workers = 1,
+                       double min_change_rate = 0.001);
+KnnGraph finalize(RefineState& state, const VectorSet& vs, std::uint32_t k);
+
+enum class BuildStrategy { efanna, random_descent, nn_expansion, brute_force, init_only };
+
+struct BuildParams {
+    std::uint32_t k = 10;
+    std::uint32_t conquer_depth = 4;
+    std::uint32_t pool_cap = 30;
+    std::uint32_t sample_cap = 20;
+    std::uint32_t max_iters = 8;
+    BuildStrategy strategy = BuildStrategy::efanna;
+    std::uint64_t seed = 1;
+    std::uint32_t workers = 1;
+    double min_change_rate = 0.001;
+};
+
+struct IterationLog {
+    std::uint32_t iteration = 0;
+    double seconds = 0.0;
+    std::uint64_t dist_comps = 0;
+    std::uint64_t changes = 0;
+    double accuracy = -1.0;
+};
+
+struct BuildStats {
+    double init_seconds = 0.0;
+    double refine_seconds = 0.0;
+    std::uint64_t dist_comps = 0;
+    bool early_stopped = false;
+    std::vector<IterationLog> iterations;
+
+    double total_seconds() const { return init_seconds + refine_seconds; }
+};
+
+struct BuildResult {
+    KnnGraph graph;
+    BuildStats stats;
+};
+
+// Device strategies: efanna, random_descent, init_only, brute_force
+// (nn_expansion is a CPU-only baseline here: std::invalid_argument).
+BuildResult build_graph(const VectorSet& vs, const KdForest* forest, const BuildParams& params,
+                        const GroundTruth* gt = nullptr);
+
+namespace detail {
+std::uint64_t nn_descent_iteration(RefineState& state, const VectorSet& vs, std::uint32_t workers);
+void rebuild_sample_lists(RefineState& state);
+void union_reverse_lists(RefineState& state);
+double pool_topk_accuracy(const RefineState& state, const GroundTruth& gt);
+}  // namespace detail
+
+// ----------------------------------------------------------- search.hpp
+struct SearchParams {
+    std::uint32_t k_return = 10;
+    std::uint32_t pool_size = 100;
+    std::uint32_t expansion = 100;
+    std::uint32_t iters = 4;
+    std::uint32_t n_trees_used = 0;
+    std::uint32_t random_seed_count = 0;
+    std::uint64_t seed = 1;
+};
+
+struct SearchStats {
+    std::uint64_t dist_comps = 0;
+    std::uint32_t leaves_visited = 0;
+    std::uint32_t graph_hops = 0;
+    std::uint32_t seed_points = 0;
+};
+
+struct SearchResult {
+    std::vector<std::uint32_t> ids;
+    std::vector<float> dists;
+    SearchStats stats;
+};
+
+struct DeviceSearcher;
+
+// Keeps references to base / forest / graph like the reference (the caller
+// keeps them alive); the device searcher holds its own graph copy.
+class GraphSearcher {
+  public:
+    GraphSearcher(const VectorSet& base, const KdForest* forest, const KnnGraph& graph);
+    SearchResult search(std::span<const float> q, const SearchParams& params);
+    SearchResult search_random_init(std::span<const float> q, const SearchParams& params);
+    // Batch form (the device path's natural shape): nq queries, row-major.
+    std::vector<SearchResult> search_batch(const VectorSet& queries, const SearchParams& params,
+                                           bool random_init = false);
+
+  private:
+    const VectorSet& base_;
+    const KdForest* forest_;
+    const KnnGraph& graph_;
+    std::shared_ptr<DeviceSearcher> dev_;
+};
+
+struct SweepPoint {
+    std::uint32_t expansion = 0;
+    std::uint32_t pool_size = 0;
+};
+
+struct SweepRow {
+    std::uint32_t expansion = 0;
+    std::uint32_t pool_size = 0;
+    double mean_time_us = 0.0;
+    double avg_recall = 0.0;
+    double avg_dist_comps = 0.0;
+    double avg_seed_points = 0.0;
+};
+
+std::vector<SweepRow> recall_curve(const VectorSet& base, const KdForest* forest, const KnnGraph& graph,
+                                   const VectorSet& queries, const GroundTruth& gt, std::span<const SweepPoint> sweep,
+                                   const SearchParams& params, bool random_init = false, std::uint32_t workers = 1);
+
+// ------------------------------------------------------------- eval.hpp
+GroundTruth brute_force_knn(const VectorSet& base, const VectorSet* queries, std::uint32_t k,
+                            std::uint32_t workers = 1, std::uint64_t* dist_comps = nullptr);
+KnnGraph brute_force_graph(const VectorSet& base, std::uint32_t k, std::uint32_t workers = 1,
+                           std::uint64_t* dist_comps = nullptr);
+double recall(std::span<const std::uint32_t> result_ids, std::span<const std::uint32_t> gt_row);
+double graph_accuracy(const KnnGraph& graph, const GroundTruth& gt);
+std::vector<std::pair<std::uint32_t, double>> accuracy_vs_k(const KnnGraph& graph, const VectorSet& vs,
+                                                            std::span<const std::uint32_t> k_list,
+                                                            std::uint32_t workers = 1);
+
+}  // namespace annkit

@@ -289,7 +289,9 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
             // search.cpp:156-173: mt19937_64(seed) draws id % n until `want` distinct
             if (tid == 0) {
                 uint64_t* mt = a.mtstate + size_t(slot) * 312;
-                const uint64_t sd = substream(a.seed, qi);
+                // 1: per-query substream(seed, qi) (recall_curve, search.cpp:208);
+                // 2: the seed as given (a single GraphSearcher::search_random_init call)
+                const uint64_t sd = a.random_init == 2 ? a.seed : substream(a.seed, qi);
                 mt[0] = sd;
                 for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
                 int idx = 312;
