@@ -169,6 +169,7 @@ __device__ __forceinline__ void hs_insert(const InitScratch& w, uint32_t id) {
 constexpr uint32_t kDesc = 4;
 __device__ void init_collect(const InitArgs& a, uint32_t i, const float* q, const InitScratch& w) {
     const uint32_t lane = lane_id();
+    const uint8_t* q8 = a.x8 ? a.x8 + size_t(i) * a.ld8 : nullptr;  // used when q is null (u8 path)
     // table <- EMPTY (vectorised)
     uint4* t4 = reinterpret_cast<uint4*>(w.table);
     for (uint32_t j = lane; j < w.tslots / 4; j += 32) t4[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -235,7 +236,8 @@ __device__ void init_collect(const InitArgs& a, uint32_t i, const float* q, cons
 #pragma unroll
                 for (uint32_t r = 0; r < kDesc; ++r) {
                     if (act[r] && cur[r].split_dim != kLeaf) {
-                        nd[r] = q[cur[r].split_dim] <= cur[r].split_val ? cur[r].left : cur[r].right;
+                        const float qd = q ? q[cur[r].split_dim] : float(__ldg(q8 + cur[r].split_dim));
+                        nd[r] = qd <= cur[r].split_val ? cur[r].left : cur[r].right;
                         more = true;
                     }
                 }
@@ -404,7 +406,9 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
                                                                uint32_t n_visit) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t warp = threadIdx.x / 32, lane = lane_id();
-    unsigned char* base = smem + warp * init_warp_bytes(kInitCap, a.ld, sib_cap);
+    // the u8 path reads the point's exact u8 row (L1) for the descents: no fp32 copy in smem
+    const uint32_t q_ld = a.x8 ? 0u : a.ld;
+    unsigned char* base = smem + warp * init_warp_bytes(kInitCap, q_ld, sib_cap);
     InitScratch w;
     w.table = reinterpret_cast<uint32_t*>(base);
     // one 8 KB region: hash slots [0, 4 KB) + unique list [4 KB, 8 KB); the
@@ -415,8 +419,9 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
     w.cap = kInitCap;
     w.pf_base = a.x8;
     w.pf_ld = a.ld8;
-    float* q = reinterpret_cast<float*>(w.uniq + kInitCap);
-    w.sib = reinterpret_cast<uint32_t*>(q + a.ld);
+    float* qbase = reinterpret_cast<float*>(w.uniq + kInitCap);
+    float* q = q_ld ? qbase : nullptr;
+    w.sib = reinterpret_cast<uint32_t*>(qbase + q_ld);
     w.sib_cap = sib_cap;
     uint32_t* hist = w.sib + 2 * sib_cap;
     w.cnt = hist + 256;
@@ -424,7 +429,7 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
         // visit points in tree-0 leaf order: concurrently processed points share
         // most candidate rows, so the gathers hit L2
         const uint32_t i = order ? order[ord] : ord;
-        for (uint32_t j = lane; j < a.ld; j += 32) q[j] = a.x[size_t(i) * a.ld + j];
+        for (uint32_t j = lane; j < q_ld; j += 32) q[j] = a.x[size_t(i) * a.ld + j];
         __syncwarp();
         init_collect(a, i, q, w);
         if (w.cnt[2]) {  // more unique candidates than the fast path holds
@@ -2383,7 +2388,7 @@ annk_state* init_graph_impl(const annk_dataset* ds, const annk_forest* fc, uint3
                ds->u8 ? ds->data8.p : nullptr, ds->ld8, ds->u8 ? ds->norms8.p : nullptr};
     const uint32_t sib_full = f->n_trees * (max_depth + 1);
     const uint32_t sib_cap = 0;  // sibling lists come from the forest (sib_list)
-    const size_t per_warp = init_warp_bytes(kInitCap, ds->ld, sib_cap);
+    const size_t per_warp = init_warp_bytes(kInitCap, ds->u8 ? 0u : ds->ld, sib_cap);
     const size_t smem = per_warp * kInitWarps;
     CK(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
