@@ -1176,186 +1176,6 @@ join_agg_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const 
     if (lane == 0 && comps) atomicAdd(a.comps, comps);
 }
 
-// Warp-per-point join (u8 datapath).  Same pairs, distances, offers and
-// counters as join_agg_kernel, without block barriers and without an offer
-// buffer: each warp owns one point i, every lane one partner member y of i's
-// list (its u8 row in registers), and the candidate (new) rows x are staged in
-// the warp's shared memory and read as broadcasts.  Two passes over the pairs:
-//   1. count the accepted offers per member (ballot counts for x, a register
-//      per lane for its y — no atomics),
-//   2. reserve each member's slot range with ONE global atomic, recompute the
-//      distances (dp4a is cheap here) and write every offer to its slot (or
-//      the spill list) directly.
-constexpr uint32_t kJW = 8;  // warps per CTA
-
-__host__ __device__ __forceinline__ size_t join_warp_bytes(uint32_t rmax, uint32_t xrows) {
-    // staged new rows (xrows x 128 B) + thr (u64) + ids, nrm, mcnt, mbase, mfix, msp (u32)
-    return (size_t(xrows) * 128 + size_t(rmax) * 8 + size_t(rmax) * 24 + 15) & ~size_t(15);
-}
-
-template <int kPass>
-__device__ __forceinline__ void join_warp_pairs(const JoinArgs& a, const uint4* xs, const uint32_t* ids,
-                                                const int32_t* nrm, const uint64_t* thr_s, uint32_t A, uint32_t R,
-                                                uint32_t y0, const uint4 (&yr)[8], uint32_t* mcnt,
-                                                const uint32_t* mbase, const uint32_t* mfix, const uint32_t* msp,
-                                                unsigned long long& comps, unsigned long long& offers) {
-    const uint32_t lane = lane_id(), ltm = (1u << lane) - 1u;
-    const uint32_t y = y0 + lane;
-    const bool yv = y < R;
-    const uint32_t idy = yv ? ids[y] : 0u;
-    const uint64_t thy = yv ? thr_s[y] : 0ull;
-    const int32_t ny = yv ? nrm[y] : 0;
-    uint32_t cy = 0;  // pass 1: offers to this lane's y
-    const uint32_t xmax = min(A, y0 + 31);  // some lane has x < y
-    for (uint32_t x0 = 0; x0 < xmax; x0 += 2) {
-        const uint32_t nx = min(2u, xmax - x0);
-        uint32_t dot[2];
-#pragma unroll
-        for (uint32_t u = 0; u < 2; ++u) {
-            const uint4* xrow = xs + size_t(x0 + min(u, nx - 1)) * 8;
-            uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;
-#pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) {
-                const uint4 xv = xrow[c];
-                d0 = __dp4a(xv.x, yr[c].x, d0);
-                d1 = __dp4a(xv.y, yr[c].y, d1);
-                d2 = __dp4a(xv.z, yr[c].z, d2);
-                d3 = __dp4a(xv.w, yr[c].w, d3);
-            }
-            dot[u] = d0 + d1 + d2 + d3;
-        }
-#pragma unroll
-        for (uint32_t u = 0; u < 2; ++u) {
-            if (u >= nx) break;
-            const uint32_t x = x0 + u, idx = ids[x];
-            const bool pair = yv && y > x && idx != idy;  // graph_build.cpp:146 (l == j)
-            const float d = float(nrm[x] + ny - 2 * int32_t(dot[u]));
-            const uint64_t kx = make_key(d, idy);  // offer y to x's pool
-            const uint64_t ky = make_key(d, idx);  // offer x to y's pool
-            const bool ox = pair && kx < thr_s[x];
-            const bool oy = pair && ky < thy;
-            const uint32_t bx = __ballot_sync(0xffffffffu, ox);
-            if (kPass == 1) {
-                comps += pair ? 1u : 0u;
-                if (lane == 0 && bx) mcnt[x] += __popc(bx);
-                cy += oy ? 1u : 0u;
-            } else {
-                // one slot cursor per member (mcnt, reset after the reservation) serves
-                // both roles a member can take: candidate x and partner y
-                uint32_t xb = 0;
-                if (lane == 0 && bx) xb = atomicAdd(&mcnt[x], __popc(bx));
-                xb = __shfl_sync(0xffffffffu, xb, 0);
-                if (ox) {
-                    const uint32_t r = xb + __popc(bx & ltm);
-                    if (r < mfix[x]) {
-                        a.obuf[size_t(idx) * a.cap + mbase[x] + r] = kx;
-                    } else {
-                        const uint32_t o = msp[x] + (r - mfix[x]);
-                        if (o < a.ov_cap) { a.ov_tgt[o] = idx; a.ov_key[o] = kx; }
-                    }
-                }
-                if (oy) {
-                    const uint32_t r = atomicAdd(&mcnt[y], 1u);
-                    if (r < mfix[y]) {
-                        a.obuf[size_t(idy) * a.cap + mbase[y] + r] = ky;
-                    } else {
-                        const uint32_t o = msp[y] + (r - mfix[y]);
-                        if (o < a.ov_cap) { a.ov_tgt[o] = idy; a.ov_key[o] = ky; }
-                    }
-                }
-                offers += (ox ? 1u : 0u) + (oy ? 1u : 0u);
-            }
-            __syncwarp();
-        }
-    }
-    if (kPass == 1 && yv && cy) mcnt[y] += cy;  // each y belongs to exactly one lane of one group
-    __syncwarp();
-}
-
-template <bool kRowInRegs>
-__global__ void __launch_bounds__(kJW * 32)
-join_warp_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const int32_t* __restrict__ norms,
-                 uint32_t rmax) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    static_assert(kRowInRegs, "join_warp_kernel: rows <= 128 bytes only");
-    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
-    const uint32_t xrows = 2 * a.S;  // |new| <= 2S rows staged
-    unsigned char* base = smem + size_t(warp) * join_warp_bytes(rmax, xrows);
-    uint4* xs = reinterpret_cast<uint4*>(base);
-    uint64_t* thr_s = reinterpret_cast<uint64_t*>(base + size_t(xrows) * 128);
-    uint32_t* ids = reinterpret_cast<uint32_t*>(thr_s + rmax);
-    int32_t* nrm = reinterpret_cast<int32_t*>(ids + rmax);
-    uint32_t* mcnt = reinterpret_cast<uint32_t*>(nrm + rmax);
-    uint32_t* mbase = mcnt + rmax;
-    uint32_t* mfix = mbase + rmax;
-    uint32_t* msp = mfix + rmax;
-    const uint32_t nv = ld8 / 16;  // 16-byte words per row (<= 8)
-    unsigned long long comps = 0, offers = 0;
-    for (uint32_t w = blockIdx.x * kJW + warp; w < a.n; w += gridDim.x * kJW) {
-        const uint32_t i = a.order ? a.order[w] : w;
-        const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
-        if (A == 0) continue;  // uniform across the warp
-        const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
-        const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
-        __syncwarp();
-        for (uint32_t r = lane; r < R; r += 32) {
-            const uint32_t id = r < A ? nw[r] : od[r - A];
-            ids[r] = id;
-            thr_s[r] = a.thr[id];
-            nrm[r] = norms[id];
-            mcnt[r] = 0;
-        }
-        __syncwarp();
-        for (uint32_t j = lane; j < A * 8; j += 32) {  // stage the new rows (candidate side of every pair)
-            const uint32_t r = j >> 3, c = j & 7;
-            xs[j] = c < nv ? __ldg(reinterpret_cast<const uint4*>(x8 + size_t(ids[r]) * ld8) + c)
-                           : make_uint4(0, 0, 0, 0);
-        }
-        __syncwarp();
-        // pass 1: count offers per member
-        for (uint32_t y0 = 1; y0 < R; y0 += 32) {
-            const uint32_t y = y0 + lane;
-            uint4 yr[8];
-            const uint4* yrow = reinterpret_cast<const uint4*>(x8 + size_t(y < R ? ids[y] : ids[0]) * ld8);
-#pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) yr[c] = c < nv ? __ldg(yrow + c) : make_uint4(0, 0, 0, 0);
-            join_warp_pairs<1>(a, xs, ids, nrm, thr_s, A, R, y0, yr, mcnt, mbase, mfix, msp, comps, offers);
-        }
-        // reserve: one atomic per member with offers
-        for (uint32_t m = lane; m < R; m += 32) {
-            const uint32_t cnt = mcnt[m];
-            uint32_t b0 = 0, fix = 0, sp = 0;
-            if (cnt) {
-                b0 = atomicAdd(&a.ocnt[ids[m]], cnt);
-                fix = b0 < a.cap ? min(cnt, a.cap - b0) : 0u;
-                if (cnt > fix) sp = atomicAdd(a.ov_cnt, cnt - fix);
-            }
-            mbase[m] = b0;
-            mfix[m] = fix;
-            msp[m] = sp;
-            mcnt[m] = 0;
-        }
-        __syncwarp();
-        // pass 2: recompute and write the offers to their slots
-        for (uint32_t y0 = 1; y0 < R; y0 += 32) {
-            const uint32_t y = y0 + lane;
-            uint4 yr[8];
-            const uint4* yrow = reinterpret_cast<const uint4*>(x8 + size_t(y < R ? ids[y] : ids[0]) * ld8);
-#pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) yr[c] = c < nv ? __ldg(yrow + c) : make_uint4(0, 0, 0, 0);
-            join_warp_pairs<2>(a, xs, ids, nrm, thr_s, A, R, y0, yr, mcnt, mbase, mfix, msp, comps, offers);
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        comps += __shfl_xor_sync(0xffffffffu, comps, o);
-        offers += __shfl_xor_sync(0xffffffffu, offers, o);
-    }
-    if (lane == 0) {
-        if (comps) atomicAdd(a.comps, comps);
-        if (offers) atomicAdd(a.offers, offers);
-    }
-}
-
 // Warp-per-point join for wide fp32 rows (rows too large to stage per point,
 // e.g. d = 960).  Same pairs, distances, offers and counters as the other
 // joins.  Each lane owns a partner member y (its row streamed through L1), the
@@ -2157,7 +1977,7 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
         return size_t(rmax) * rsb + size_t(rmax) * 8 + size_t(ol) * 8 + size_t(rmax) * 24 + (rmax / 4 + 2) * 4 +
                size_t(ol) * 2 + 16;
     };
-    const uint32_t ol_u8 = 4096, ol_f32 = 2048;
+    const uint32_t ol_u8 = 2560, ol_f32 = 2048;  // u8: 4 CTAs per SM
     const bool agg_u8 = ds->u8 && agg_smem(true, ol_u8) <= 120 * 1024;
     const bool agg_f32 = !agg_u8 && agg_smem(false, ol_f32) <= 160 * 1024;
     // visit list: tree-0 leaf order (L2 locality), restricted to owned points
@@ -2165,11 +1985,6 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
     const uint32_t n_visit = own_hi(s) - own_lo(s);
     DevBuf<unsigned long long> counters(3);  // [comps, unused, offers]
     if (s->ov_count.n != 1) s->ov_count.alloc(1);
-    // warp-per-point join for short lists (measured faster below ~40 list rows per
-    // point at cfg2; the CTA-per-point aggregated join wins on longer lists)
-    const double rows_per_point = n_visit ? double(s->join_rows) / n_visit : 0.0;
-    bool use_warp_join = rows_per_point < 40.0;
-    if (const char* e = getenv("ANNK_JOIN")) use_warp_join = std::string(e) == "warp";
     uint32_t spilled = 0;
     for (;;) {
         if (s->obuf.n != size_t(n) * s->offer_cap) s->obuf.alloc(size_t(n) * s->offer_cap);
@@ -2184,15 +1999,6 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
                     s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p,
                     s->ov_count.p, s->ov_tgt.p, s->ov_key.p, s->ov_cap, counters.p + 2, order};
         if (n_visit == 0) {
-        } else if (ds->u8 && ds->ld8 <= 128 && use_warp_join) {
-            const size_t sm = join_warp_bytes(rmax, 2 * s->S) * kJW;
-            const void* fn = reinterpret_cast<const void*>(join_warp_kernel<true>);
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            int per_sm = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJW * 32, sm));
-            const uint32_t grid = std::min<uint32_t>((n_visit + kJW - 1) / kJW,
-                                                     uint32_t(num_sms()) * std::max(per_sm, 1));
-            LAUNCH(join_warp_kernel<true>, grid, kJW * 32, sm, ja, ds->data8.p, ds->ld8, ds->norms8.p, rmax);
         } else if (agg_u8 || agg_f32) {
             const size_t sm = agg_smem(agg_u8, agg_u8 ? ol_u8 : ol_f32);
             const void* fn = agg_u8 ? reinterpret_cast<const void*>(join_agg_kernel<true>)
