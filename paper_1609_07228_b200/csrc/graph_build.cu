@@ -36,57 +36,6 @@ constexpr uint32_t kInitCap = 1024;  // fast-path candidate capacity per point
 
 // ---------------------------------------------------------------- helpers
 
-// First `count` (<= 64) outputs of std::mt19937_64(seed), without building the
-// whole 312-word state: output k needs init words k, k+1 and k+156.
-__device__ void mt_first_outputs(uint64_t seed, uint32_t count, uint64_t* out) {
-    uint64_t lo[65], hi[64];
-    uint64_t x = seed;
-    lo[0] = x;
-    const uint32_t last = 155 + count;
-    for (uint32_t i = 1; i <= last; ++i) {
-        x = 6364136223846793005ULL * (x ^ (x >> 62)) + uint64_t(i);
-        if (i <= count) lo[i] = x;
-        if (i >= 156) hi[i - 156] = x;
-    }
-    for (uint32_t k = 0; k < count; ++k) out[k] = mt_temper(mt_twist(lo[k], lo[k + 1], hi[k]));
-}
-
-// graph_build.cpp:38-48 sample_down on an already sorted, unique list `a` of
-// length m: partial Fisher-Yates over the first cap slots.  Writes the
-// sampled prefix to out (order matters only for the subsequent sort-dedup).
-__device__ uint32_t sample_down_sorted(const uint32_t* a, uint32_t m, uint32_t cap, uint64_t seed,
-                                       uint32_t* out) {
-    if (m <= cap) {
-        for (uint32_t i = 0; i < m; ++i) out[i] = a[i];
-        return m;
-    }
-    uint64_t r[64];
-    mt_first_outputs(seed, cap, r);
-    // sparse overlay of swapped positions
-    uint32_t pos[128], val[128];
-    uint32_t no = 0;
-    auto get = [&](uint32_t p) -> uint32_t {
-        for (uint32_t j = 0; j < no; ++j)
-            if (pos[j] == p) return val[j];
-        return a[p];
-    };
-    auto set = [&](uint32_t p, uint32_t v) {
-        for (uint32_t j = 0; j < no; ++j)
-            if (pos[j] == p) { val[j] = v; return; }
-        pos[no] = p;
-        val[no] = v;
-        ++no;
-    };
-    for (uint32_t i = 0; i < cap; ++i) {
-        const uint32_t j = i + uint32_t(r[i] % uint64_t(m - i));
-        const uint32_t vi = get(i), vj = get(j);
-        set(i, vj);
-        set(j, vi);
-    }
-    for (uint32_t i = 0; i < cap; ++i) out[i] = get(i);
-    return cap;
-}
-
 // Sort + unique n u32 values in smem s (capacity m = pow2 >= n) by one warp.
 // Returns the unique count (values compacted to the front).
 __device__ uint32_t warp_sort_unique_u32(uint32_t* s, uint32_t n, uint32_t m) {
@@ -803,194 +752,19 @@ struct JoinArgs {
     const uint32_t* order;       // visit list of n points (nullptr: 0..n-1)
 };
 
-__device__ __forceinline__ void offer(const JoinArgs& a, uint32_t owner, uint32_t cand, float d) {
-    const uint64_t key = make_key(d, cand);
-    if (key < a.thr[owner]) {
-        const uint32_t slot = atomicAdd(&a.ocnt[owner], 1u);
-        if (slot < a.cap) {
-            a.obuf[size_t(owner) * a.cap + slot] = key;
-        } else {
-            const uint32_t o = atomicAdd(a.ov_cnt, 1u);
-            if (o < a.ov_cap) {
-                a.ov_tgt[o] = owner;
-                a.ov_key[o] = key;
-            }
-        }
-    }
-}
-
-// graph_build.cpp:129-156: every new x new pair (a<b) and new x old pair
-// (l != j), offered both ways.  One warp per point; the shared row of the
-// pair (new[x]) is staged in shared memory.
-__global__ void join_kernel(JoinArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
-    const uint32_t wpb = blockDim.x / 32;
-    float* row = reinterpret_cast<float*>(smem) + size_t(warp) * a.ld;
-    const uint32_t w = blockIdx.x * wpb + warp;
-    if (w >= a.n) return;
-    const uint32_t i = a.order ? a.order[w] : w;
-    const uint32_t A = a.gncnt[i], B = a.gocnt[i];
-    const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
-    const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
-    unsigned long long comps = 0;
-    for (uint32_t xi = 0; xi < A; ++xi) {
-        const uint32_t j = nw[xi];
-        __syncwarp();
-        for (uint32_t c = lane; c < a.ld; c += 32) row[c] = a.x[size_t(j) * a.ld + c];
-        __syncwarp();
-        const uint32_t tri = A - 1 - xi;
-        const uint32_t total = tri + B;
-        for (uint32_t t = lane; t < total; t += 32) {
-            const uint32_t k2 = t < tri ? nw[xi + 1 + t] : od[t - tri];
-            if (t >= tri && k2 == j) continue;
-            const float d = l2_exact_ldg(row, a.x + size_t(k2) * a.ld, a.ld);
-            ++comps;
-            offer(a, j, k2, d);
-            offer(a, k2, j, d);
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
-    if (lane == 0 && comps) atomicAdd(a.comps, comps);
-}
-
-// Staged join: one CTA per point.  The point's list rows (new first, then
-// old) are copied into shared memory with a padded stride (ld+4 floats keeps
-// float4 alignment and makes 8 consecutive rows hit distinct 16-byte bank
-// groups).  Needed pairs are {(x, y): x < A, x < y < R}: new x new upper
+// Aggregated join (both datapaths), one CTA per point.  The point's list rows
+// (new first, then old) are staged in shared memory with a padded stride; the
+// needed pairs are {(x, y): x < |new|, x < y < |list|} — new x new upper
 // triangle plus new x old.  Work item = (group of 4 new rows, 32 partner
-// columns starting right after the group's first row); each lane owns one
-// partner column and accumulates 4 exact distances (the 4 new rows are
-// broadcast float4 loads), so the kernel is FP32-pipe bound instead of
-// L2-gather bound.  Owners of every offer are list members, so their
-// start-of-round thresholds are staged too.
-constexpr uint32_t kJoinThreads = 256;
-constexpr uint32_t kJoinXR = 4;
-
-__global__ void __launch_bounds__(kJoinThreads)
-join_staged_kernel(JoinArgs a, const uint32_t* __restrict__ order, uint32_t rmax) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t rs = a.ld + 4;  // padded row stride (floats)
-    float* rows = reinterpret_cast<float*>(smem);
-    uint64_t* thr_s = reinterpret_cast<uint64_t*>(rows + size_t(rmax) * rs);
-    uint32_t* ids = reinterpret_cast<uint32_t*>(thr_s + rmax);
-    uint32_t* gstart = ids + rmax;  // item prefix per row group (<= rmax/4 + 2)
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr uint32_t kWarps = kJoinThreads / 32;
-    unsigned long long comps = 0;
-    for (uint32_t ord = blockIdx.x; ord < a.n; ord += gridDim.x) {
-        const uint32_t i = order ? order[ord] : ord;
-        const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
-        if (A == 0) continue;  // uniform across the CTA
-        const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
-        const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
-        for (uint32_t r = tid; r < R; r += kJoinThreads) {
-            const uint32_t id = r < A ? nw[r] : od[r - A];
-            ids[r] = id;
-            thr_s[r] = a.thr[id];
-        }
-        // item table: group g covers new rows [4g, 4g+4), partners from 4g+1 up to R
-        if (tid == 0) {
-            uint32_t acc = 0;
-            const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
-            for (uint32_t g = 0; g < ng; ++g) {
-                gstart[g] = acc;
-                const uint32_t y0 = g * kJoinXR + 1;
-                acc += R > y0 ? (R - y0 + 31) / 32 : 0;
-            }
-            gstart[ng] = acc;
-        }
-        __syncthreads();
-        const uint32_t v4 = a.ld / 4;
-        for (uint32_t j = tid; j < R * v4; j += kJoinThreads) {
-            const uint32_t r = j / v4, c = (j % v4) * 4;
-            const float4 v = __ldg(reinterpret_cast<const float4*>(a.x + size_t(ids[r]) * a.ld + c));
-            *reinterpret_cast<float4*>(rows + size_t(r) * rs + c) = v;
-        }
-        __syncthreads();
-        const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
-        const uint32_t n_items = gstart[ng];
-        for (uint32_t item = warp; item < n_items; item += kWarps) {
-            uint32_t g = 0;
-            while (gstart[g + 1] <= item) ++g;
-            const uint32_t x0 = g * kJoinXR;
-            const uint32_t y = x0 + 1 + (item - gstart[g]) * 32 + lane;
-            const bool yv = y < R;
-            const float* yr = rows + size_t(yv ? y : 0) * rs;
-            const float* xr = rows + size_t(x0) * rs;
-            float acc[kJoinXR];
-#pragma unroll
-            for (uint32_t k = 0; k < kJoinXR; ++k) acc[k] = 0.0f;
-            for (uint32_t c = 0; c < a.ld; c += 4) {
-                const float4 b = *reinterpret_cast<const float4*>(yr + c);
-#pragma unroll
-                for (uint32_t k = 0; k < kJoinXR; ++k) {
-                    // rows x0+k beyond A read (unused) staged rows or padding; results are discarded
-                    const float4 x = *reinterpret_cast<const float4*>(xr + size_t(min(x0 + k, R - 1) - x0) * rs + c);
-                    float d;
-                    d = __fsub_rn(x.x, b.x); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(x.y, b.y); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(x.z, b.z); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(x.w, b.w); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                }
-            }
-            if (yv) {
-                const uint32_t idy = ids[y];
-                const uint64_t thy = thr_s[y];
-#pragma unroll
-                for (uint32_t k = 0; k < kJoinXR; ++k) {
-                    const uint32_t x = x0 + k;
-                    if (x >= A || y <= x) continue;
-                    const uint32_t idx = ids[x];
-                    if (idx == idy) continue;  // graph_build.cpp:146 (l == j)
-                    ++comps;
-                    const float d = acc[k];
-                    const uint64_t kx = make_key(d, idy);  // offer y to x's pool
-                    if (kx < thr_s[x]) {
-                        const uint32_t slot = atomicAdd(&a.ocnt[idx], 1u);
-                        if (slot < a.cap) a.obuf[size_t(idx) * a.cap + slot] = kx;
-                        else {
-                            const uint32_t o = atomicAdd(a.ov_cnt, 1u);
-                            if (o < a.ov_cap) { a.ov_tgt[o] = idx; a.ov_key[o] = kx; }
-                        }
-                    }
-                    const uint64_t ky = make_key(d, idx);  // offer x to y's pool
-                    if (ky < thy) {
-                        const uint32_t slot = atomicAdd(&a.ocnt[idy], 1u);
-                        if (slot < a.cap) a.obuf[size_t(idy) * a.cap + slot] = ky;
-                        else {
-                            const uint32_t o = atomicAdd(a.ov_cnt, 1u);
-                            if (o < a.ov_cap) { a.ov_tgt[o] = idy; a.ov_key[o] = ky; }
-                        }
-                    }
-                }
-            }
-        }
-        __syncthreads();
-    }
-    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
-    if (lane == 0 && comps) atomicAdd(a.comps, comps);
-}
-
-__device__ __forceinline__ void push_offer(const JoinArgs& a, uint32_t owner, uint64_t key) {
-    const uint32_t slot = atomicAdd(&a.ocnt[owner], 1u);
-    if (slot < a.cap) {
-        a.obuf[size_t(owner) * a.cap + slot] = key;
-    } else {
-        const uint32_t o = atomicAdd(a.ov_cnt, 1u);
-        if (o < a.ov_cap) {
-            a.ov_tgt[o] = owner;
-            a.ov_key[o] = key;
-        }
-    }
-}
-
-// Aggregated join (both datapaths).  Same pair schedule as join_staged_kernel;
+// columns after the group's first row): each lane owns one partner column and
+// accumulates 4 exact distances from broadcast row reads.
 // accepted offers are first collected in shared memory tagged with the list
 // member they go to (every offer of point i's join targets one of i's list
 // members), then flushed with ONE global atomic per member to reserve a
 // contiguous range in that member's offer slots (or the spill list).  This
 // cuts global atomics from one per offer to one per (point, member).
+constexpr uint32_t kJoinThreads = 256;
+constexpr uint32_t kJoinXR = 4;  // new rows per work item
 constexpr uint32_t kJoinPerRound = (kJoinThreads / 32) * 32 * kJoinXR * 2;  // max offers per round
 
 template <bool U8>
@@ -1359,46 +1133,6 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t 
     return lo;
 }
 
-// Warp: R (sorted, unique, r <= P entries) := top-P unique of (R U chunk).
-// chunk (c entries, any order, capacity m = pow2 >= c) is clobbered; tmp >= P.
-__device__ uint32_t warp_topk_merge(uint64_t* R, uint32_t r, uint64_t* chunk, uint32_t c, uint32_t m,
-                                    uint32_t P, uint64_t* tmp) {
-    const uint32_t lane = lane_id();
-    for (uint32_t j = c + lane; j < m; j += 32) chunk[j] = kEmptyKey;
-    __syncwarp();
-    warp_bitonic_sort(chunk, m);
-    uint32_t nu = 0;  // unique, not already in R
-    for (uint32_t base = 0; base < c; base += 32) {
-        const uint32_t j = base + lane;
-        const uint64_t v = j < c ? chunk[j] : kEmptyKey;
-        bool keep = j < c && (j == 0 || chunk[j - 1] != v);
-        if (keep) {
-            const uint32_t p = lower_bound_u64(R, r, v);
-            keep = !(p < r && R[p] == v);
-        }
-        const uint32_t b = __ballot_sync(0xffffffffu, keep);
-        __syncwarp();
-        if (keep) chunk[nu + __popc(b & ((1u << lane) - 1u))] = v;
-        nu += __popc(b);
-        __syncwarp();
-    }
-    for (uint32_t j = lane; j < r; j += 32) {
-        const uint32_t k = j + lower_bound_u64(chunk, nu, R[j]);
-        if (k < P) tmp[k] = R[j];
-    }
-    for (uint32_t j = lane; j < nu; j += 32) {
-        const uint32_t k = j + lower_bound_u64(R, r, chunk[j]);
-        if (k < P) tmp[k] = chunk[j];
-    }
-    __syncwarp();
-    const uint32_t nr = min(P, r + nu);
-    for (uint32_t j = lane; j < nr; j += 32) R[j] = tmp[j];
-    __syncwarp();
-    return nr;
-}
-
-constexpr uint32_t kMergeChunk = 256;
-
 // Sorts the first c (<= 32*V) entries of buf in registers and writes them back
 // sorted (padding with kEmptyKey).
 template <int V>
@@ -1535,6 +1269,7 @@ __global__ void merge_stream_kernel(MergeArgs a) {
     }
 }
 
+
 // End of a round: entries inserted this round (flag bit 1) survive = changes.
 __global__ void count_inserted_kernel(uint8_t* __restrict__ flags, size_t cnt, unsigned long long* out) {
     unsigned long long c = 0;
@@ -1547,85 +1282,6 @@ __global__ void count_inserted_kernel(uint8_t* __restrict__ flags, size_t cnt, u
     }
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
-}
-// New pool = top-P of (pool U offers); duplicates keep the pool's entry.
-// Offers are first reduced to their top-P unique keys in chunks (an offer
-// beaten by P distinct offers cannot survive), then merged with the pool.
-__global__ void merge_kernel(MergeArgs a, const uint32_t* __restrict__ list) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
-    const uint32_t wpb = blockDim.x / 32;
-    const size_t per_warp_u64 = kMergeChunk + 3 * size_t(a.P);
-    uint64_t* chunk = reinterpret_cast<uint64_t*>(smem) + size_t(warp) * per_warp_u64;
-    uint64_t* R = chunk + kMergeChunk;   // top-P offers
-    uint64_t* sp = R + a.P;              // pool keys
-    uint64_t* sout = sp + a.P;           // scratch / result
-    uint8_t* sflag = reinterpret_cast<uint8_t*>(reinterpret_cast<uint64_t*>(smem) + size_t(wpb) * per_warp_u64) +
-                     size_t(warp) * 2 * a.P;
-    uint8_t* soutf = sflag + a.P;
-    const uint32_t li = blockIdx.x * wpb + warp;
-    if (list ? li >= list[0] : li >= a.n) return;
-    const uint32_t i = list ? list[1 + li] : li;
-    const uint32_t total = a.ocnt[i];
-    if (total == 0) return;
-    const uint32_t c_fix = min(total, a.cap);
-    const uint32_t c_ov = total - c_fix;
-    const uint64_t* ob = a.obuf + size_t(i) * a.cap;
-    const uint64_t* ov = a.ov_key + (c_ov ? a.ov_off[i] : 0);
-    uint32_t r = 0;
-    for (uint32_t base = 0; base < total; base += kMergeChunk) {
-        const uint32_t c = min(kMergeChunk, total - base);
-        for (uint32_t j = lane; j < c; j += 32) {
-            const uint32_t t = base + j;
-            chunk[j] = t < c_fix ? ob[t] : ov[t - c_fix];
-        }
-        __syncwarp();
-        r = warp_topk_merge(R, r, chunk, c, next_pow2(c), a.P, sout);
-    }
-    const uint32_t sz = a.sizes[i];
-    uint64_t* pk = a.keys + size_t(i) * a.P;
-    uint8_t* pf = a.flags + size_t(i) * a.P;
-    for (uint32_t j = lane; j < a.P; j += 32) {
-        sp[j] = j < sz ? pk[j] : kEmptyKey;
-        sflag[j] = j < sz ? pf[j] : 0;
-    }
-    __syncwarp();
-    // offers already present in the pool keep the pool's entry (and flag)
-    uint32_t nu = 0;
-    for (uint32_t base = 0; base < r; base += 32) {
-        const uint32_t j = base + lane;
-        const uint64_t v = j < r ? R[j] : kEmptyKey;
-        bool keep = j < r;
-        if (keep) {
-            const uint32_t p = lower_bound_u64(sp, sz, v);
-            keep = !(p < sz && sp[p] == v);
-        }
-        const uint32_t b = __ballot_sync(0xffffffffu, keep);
-        __syncwarp();
-        if (keep) R[nu + __popc(b & ((1u << lane) - 1u))] = v;
-        nu += __popc(b);
-        __syncwarp();
-    }
-    uint32_t added = 0;
-    for (uint32_t j = lane; j < sz; j += 32) {
-        const uint32_t k = j + lower_bound_u64(R, nu, sp[j]);
-        if (k < a.P) { sout[k] = sp[j]; soutf[k] = sflag[j]; }
-    }
-    for (uint32_t j = lane; j < nu; j += 32) {
-        const uint32_t k = j + lower_bound_u64(sp, sz, R[j]);
-        if (k < a.P) { sout[k] = R[j]; soutf[k] = 3; ++added; }
-    }
-    __syncwarp();
-    const uint32_t nsz = min(a.P, sz + nu);
-    for (uint32_t j = lane; j < a.P; j += 32) {
-        pk[j] = j < nsz ? sout[j] : kEmptyKey;
-        pf[j] = j < nsz ? soutf[j] : 0;
-    }
-    for (int o = 16; o > 0; o >>= 1) added += __shfl_xor_sync(0xffffffffu, added, o);
-    if (lane == 0) {
-        a.sizes[i] = nsz;
-        if (added) atomicAdd(a.changes, (unsigned long long)added);
-    }
 }
 
 __global__ void spill_counts_kernel(const uint32_t* __restrict__ ocnt, uint32_t n, uint32_t cap,
@@ -1971,7 +1627,6 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
     if (s->ov_cap == 0)
         s->ov_cap = uint32_t(std::min<uint64_t>(std::max<uint64_t>(1u << 20, n * g_spill_per_point_hint), 1u << 31));
     const uint32_t rmax = 3 * s->S + s->P;  // |new| <= 2S, |old| <= P + S
-    const size_t staged_smem = size_t(rmax) * (ds->ld + 4) * 4 + size_t(rmax) * 12 + (rmax / 4 + 2) * 4;
     const auto agg_smem = [&](bool u8, uint32_t ol) {
         const size_t rsb = u8 ? ds->ld8 + 16 : size_t(ds->ld + 4) * 4;
         return size_t(rmax) * rsb + size_t(rmax) * 8 + size_t(ol) * 8 + size_t(rmax) * 24 + (rmax / 4 + 2) * 4 +
@@ -2013,14 +1668,6 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
             else
                 LAUNCH(join_agg_kernel<false>, grid, kJoinThreads, sm, ja, nullptr, 0u, nullptr, order, rmax,
                        ol_f32);
-        } else if (staged_smem <= 110 * 1024) {
-            CK(cudaFuncSetAttribute(join_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(staged_smem)));
-            int per_sm = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_staged_kernel, kJoinThreads,
-                                                             staged_smem));
-            const uint32_t grid = std::min<uint32_t>(n_visit, uint32_t(num_sms()) * std::max(per_sm, 1));
-            LAUNCH(join_staged_kernel, grid, kJoinThreads, staged_smem, ja, order, rmax);
         } else {  // wide fp32 rows: warp per point, rows streamed through L1
             const size_t sm = join_wide_bytes(rmax) * kWJW;
             CK(cudaFuncSetAttribute(join_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
