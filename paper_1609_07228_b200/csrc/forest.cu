@@ -31,6 +31,7 @@
 #include "../../include/annkit_b200.h"
 #include "internal.cuh"
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 namespace annk {
@@ -44,6 +45,8 @@ constexpr uint32_t kTileMax = 1024;      // staged-tile path: points per tile
 constexpr uint32_t kStageBytes = 147456;  // staged rows (u8 path), row stride ld8 + 4
 constexpr uint32_t kStack = 160;
 constexpr uint32_t kTileStack = 128;
+constexpr uint32_t kMaxCluster = 8;      // CTAs per tree (thread-block cluster)
+constexpr uint32_t kClusterMin = 8192;  // nodes above this many points use the whole cluster
 constexpr size_t kPrefetchBytes = 4u << 20;
 constexpr uint32_t kDrawWin = 256;
 
@@ -67,6 +70,7 @@ struct BuildArgs {
     const uint32_t* draws;  // split dimension of the k-th internal node in pre-order
     uint32_t n_draws;
     float* col;  // block path: the node's gathered column, by point_index slot (n floats)
+    uint32_t* ltmp;  // cluster path: left side of a partition (n)
 };
 
 struct Smem {
@@ -93,6 +97,12 @@ struct Smem {
     float b_split;
     double b_sum;
     int b_exact;
+    // cluster coordination (read by the other CTAs of the tree's cluster through DSMEM)
+    uint32_t cmd, cmd_id, cmd_d;
+    StackEntry cmd_e;
+    double cl_sum[kMaxCluster];
+    int cl_top[kMaxCluster], cl_lsb[kMaxCluster];
+    uint32_t cl_nl[kMaxCluster], cl_nr[kMaxCluster];
     alignas(16) unsigned char stage[kStageBytes];  // staged tile rows
 };
 static_assert(sizeof(Smem) <= 232448, "forest shared memory exceeds 227 KB");
@@ -995,12 +1005,214 @@ __device__ void block_split_node(const BuildArgs& a, Smem& s, const StackEntry& 
     __syncthreads();
 }
 
+namespace cg = cooperative_groups;
+
+// One node of > kClusterMin points split by the whole cluster (C CTAs, this
+// one of rank r).  Each CTA sums its slice of the node (column gathered into
+// a.col); the partial sums go to the leader's shared memory through DSMEM and
+// every CTA forms the same total, hence the same split.  The stable
+// partition needs each slice's left/right counts first (second exchange);
+// lefts and rights are then scattered to ltmp / rtmp at their global offsets
+// (other slices may still be reading pidx), and copied back to pidx.  The
+// leader then handles the degenerate fallback and the node record.
+template <bool U8>
+__device__ void cluster_split_node(const BuildArgs& a, Smem& s, Smem* lead, const cg::cluster_group& cl,
+                                   uint32_t rank, uint32_t C, const StackEntry& e, uint32_t id, uint32_t d) {
+    constexpr uint32_t kPer = 8, kChunk = kBlock * kPer;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid / 32;
+    const uint32_t size = e.end - e.start;
+    const uint32_t len = (size + C - 1) / C;
+    const uint32_t lo = e.start + min(size, rank * len), hi = e.start + min(size, (rank + 1) * len);
+    // pass 1: gather + partial sum of this slice
+    double sum = 0.0;
+    int top = INT_MIN, lsb = INT_MAX;
+    uint64_t isum = 0;
+    for (uint32_t p0 = lo; p0 < hi; p0 += kChunk) {
+        uint32_t pid[kPer];
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t q = p0 + u * kBlock + tid;
+            pid[u] = q < hi ? a.pidx[q] : 0u;
+        }
+        float v[kPer];
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t q = p0 + u * kBlock + tid;
+            v[u] = q < hi ? colv<U8>(a, pid[u], d) : 0.0f;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t q = p0 + u * kBlock + tid;
+            if (q < hi) a.col[q] = v[u];
+            if constexpr (U8) {
+                isum += uint32_t(v[u]);
+            } else {
+                sum += double(v[u]);
+                val_stats(v[u], top, lsb);
+            }
+        }
+    }
+    if constexpr (U8) {
+        for (int o = 16; o > 0; o >>= 1) isum += __shfl_xor_sync(0xffffffffu, isum, o);
+        if (lane == 0) s.red_sum[warp] = double(isum);
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (uint32_t w = 0; w < kWarps; ++w) t += s.red_sum[w];
+            lead->cl_sum[rank] = t;
+            lead->cl_top[rank] = INT_MIN;
+            lead->cl_lsb[rank] = INT_MAX;
+        }
+    } else {
+        block_reduce_stats(s, sum, top, lsb);
+        if (tid == 0) {
+            lead->cl_sum[rank] = sum;
+            lead->cl_top[rank] = top;
+            lead->cl_lsb[rank] = lsb;
+        }
+    }
+    cl.sync();
+    if (tid == 0) {
+        double t = 0.0;
+        int tp = INT_MIN, lb = INT_MAX;
+        for (uint32_t r = 0; r < C; ++r) {
+            t += lead->cl_sum[r];  // exact: integer / exactly representable partials
+            tp = max(tp, lead->cl_top[r]);
+            lb = min(lb, lead->cl_lsb[r]);
+        }
+        s.b_sum = t;
+        s.b_exact = U8 ? 1 : int(sum_is_exact(tp, lb, size));
+    }
+    __syncthreads();
+    if (!s.b_exact) {  // uniform across the cluster: the reference's sequential order, by the leader
+        cl.sync();
+        if (rank == 0 && tid == 0) {
+            double t = 0.0;
+            for (uint32_t p = e.start; p < e.end; ++p) t += double(ldx(a, a.pidx[p], d));
+            s.b_sum = t;
+        }
+        cl.sync();
+        if (tid == 0) s.b_sum = lead->b_sum;
+        __syncthreads();
+    }
+    const float split = __double2float_rn(__ddiv_rn(s.b_sum, double(size)));
+    // pass 2a: this slice's left / right counts
+    uint32_t cl_ = 0, cr_ = 0;
+    for (uint32_t q = lo + tid; q < hi; q += kBlock) {
+        if (a.col[q] <= split) ++cl_;
+        else ++cr_;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        cl_ += __shfl_xor_sync(0xffffffffu, cl_, o);
+        cr_ += __shfl_xor_sync(0xffffffffu, cr_, o);
+    }
+    if (lane == 0) {
+        s.cnt_l[warp] = cl_;
+        s.cnt_r[warp] = cr_;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t tl = 0, tr = 0;
+        for (uint32_t w = 0; w < kWarps; ++w) {
+            tl += s.cnt_l[w];
+            tr += s.cnt_r[w];
+        }
+        lead->cl_nl[rank] = tl;
+        lead->cl_nr[rank] = tr;
+    }
+    cl.sync();
+    uint32_t lpre = 0, rpre = 0, NL = 0;
+    for (uint32_t r = 0; r < C; ++r) {
+        const uint32_t x = lead->cl_nl[r], y = lead->cl_nr[r];
+        if (r < rank) {
+            lpre += x;
+            rpre += y;
+        }
+        NL += x;
+    }
+    const uint32_t NR = size - NL;
+    // pass 2b: stable scatter of this slice (8 consecutive points per thread)
+    uint32_t nl = 0, nr = 0;
+    for (uint32_t b0 = lo; b0 < hi; b0 += kChunk) {
+        const uint32_t q0 = b0 + tid * kPer;
+        uint32_t pid[kPer];
+        float cv[kPer];
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) {
+            pid[i] = q0 + i < hi ? a.pidx[q0 + i] : 0u;
+            cv[i] = q0 + i < hi ? a.col[q0 + i] : 0.0f;
+        }
+        uint32_t lm = 0, vm = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) {
+            if (q0 + i < hi) {
+                vm |= 1u << i;
+                if (cv[i] <= split) lm |= 1u << i;
+            }
+        }
+        const uint32_t x = __popc(lm) | (__popc(vm & ~lm) << 16);
+        uint32_t incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += y;
+        }
+        if (lane == 31) s.cnt_l[warp] = incl;
+        __syncthreads();
+        uint32_t wp = 0, tot = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < kWarps; ++w) {
+            const uint32_t c = s.cnt_l[w];
+            wp += w < warp ? c : 0u;
+            tot += c;
+        }
+        const uint32_t ex = wp + incl - x;
+        uint32_t ol = e.start + lpre + nl + (ex & 0xffffu), orr = e.start + rpre + nr + (ex >> 16);
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) {
+            if ((lm >> i) & 1u) a.ltmp[ol++] = pid[i];
+            else if ((vm >> i) & 1u) a.rtmp[orr++] = pid[i];
+        }
+        nl += tot & 0xffffu;
+        nr += tot >> 16;
+        __syncthreads();
+    }
+    cl.sync();
+    // copy back: positions [e.start, e.start + size) split by rank
+    for (uint32_t g = min(size, rank * len) + tid; g < min(size, (rank + 1) * len); g += kBlock)
+        a.pidx[e.start + g] = g < NL ? a.ltmp[e.start + g] : a.rtmp[e.start + g - NL];
+    cl.sync();
+    if (rank == 0) {
+        uint32_t mid = e.start + NL;
+        uint8_t even = 0;
+        float sp = split;
+        if (NL == 0 || NR == 0 || max(NL, NR) > 4u * min(NL, NR)) {
+            block_sort_node(a, s, e.start, size, d);
+            mid = e.start + size / 2;
+            sp = midpoint_f(ldx(a, a.pidx[mid - 1], d), ldx(a, a.pidx[mid], d));
+            even = 1;
+        }
+        if (tid == 0) {
+            a.nodes[id] = KdNodeDev{d, sp, 0u, 0u};
+            a.even[id] = even;
+            s.bstack[s.bsp] = StackEntry{mid, e.end, e.depth + 1, id, 1};
+            s.bstack[s.bsp + 1] = StackEntry{e.start, mid, e.depth + 1, id, 0};
+            s.bsp += 2;
+            if (s.bsp > kStack - 2) s.error = 1;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs* __restrict__ args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
-    const BuildArgs a = args[blockIdx.x];
+    const cg::cluster_group cl = cg::this_cluster();
+    const uint32_t C = cl.num_blocks(), rank = cl.block_rank();
+    const BuildArgs a = args[blockIdx.x / C];
+    Smem* lead = cl.map_shared_rank(&s, 0);  // the tree's leader CTA (rank 0) owns the build state
     const uint32_t tid = threadIdx.x;
-    for (uint32_t i = tid; i < a.n; i += kBlock) a.pidx[i] = i;
+    for (uint32_t i = rank * kBlock + tid; i < a.n; i += C * kBlock) a.pidx[i] = i;
     if (tid == 0) {
         s.dwin_base = 0xffffffffu - kDrawWin;  // empty window
         s.draw_idx = 0;
@@ -1014,42 +1226,69 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
         s.bstack[0] = StackEntry{0, a.n, 0, kInvalidId, 0};
         s.bsp = 1;
     }
-    __syncthreads();
+    cl.sync();
     // staged tiles on: the block path runs down to tile size (its chunked
     // partition beats warp 0's streaming path on 1k-4k point nodes)
     const uint32_t warp_limit = tile_capacity(a) ? tile_capacity(a) : kWarpSubtree;
-    while (s.bsp > 0 && !s.error) {
-        const StackEntry e = s.bstack[s.bsp - 1];
-        __syncthreads();
-        const uint32_t size = e.end - e.start;
-        if (size <= warp_limit) {
-            if (tid == 0) s.bsp -= 1;
+    for (;;) {
+        // the leader picks the next pre-order node: 0 done, 1 cluster split,
+        // 2 warp subtree / staged tile, 3 block split by the leader alone
+        if (rank == 0) {
+            if (tid == 0) {
+                if (s.bsp == 0 || s.error) {
+                    s.cmd = 0;
+                } else {
+                    const StackEntry e = s.bstack[--s.bsp];
+                    const uint32_t size = e.end - e.start;
+                    s.cmd_e = e;
+                    if (size <= warp_limit) {
+                        s.cmd = 2;
+                    } else {
+                        s.cmd = (C > 1 && size > kClusterMin) ? 1u : 3u;
+                        const uint32_t id = s.node_count;
+                        s.node_count = id + 1;
+                        if (e.parent != kInvalidId) {
+                            if (e.side == 0) a.nodes[e.parent].left = id;
+                            else a.nodes[e.parent].right = id;
+                        }
+                        a.depth[id] = e.depth;
+                        s.max_depth = max(s.max_depth, e.depth);
+                        s.cmd_id = id;
+                    }
+                }
+            }
             __syncthreads();
-            const long long c0 = clock64();
-            if (tid < 32) warp_build_subtree(a, s, e);
-            else if (tile_capacity(a)) stage_helper(a, s);
-            if (tid == 0) s.cyc_warp += clock64() - c0;
-            __syncthreads();
+            if (s.cmd == 1 && tid < 32) {
+                const uint32_t d = warp_draw(a, s);
+                if (tid == 0) s.cmd_d = d;
+            }
+        }
+        cl.sync();
+        const uint32_t cmd = lead->cmd;
+        if (cmd == 0) break;
+        const StackEntry e = lead->cmd_e;
+        if (cmd == 2) {
+            if (rank == 0) {
+                const long long c0 = clock64();
+                if (tid < 32) warp_build_subtree(a, s, e);
+                else if (tile_capacity(a)) stage_helper(a, s);
+                if (tid == 0) s.cyc_warp += clock64() - c0;
+                __syncthreads();
+            }
             continue;
         }
-        const uint32_t id = s.node_count;
-        __syncthreads();
-        if (tid == 0) {
-            s.bsp -= 1;
-            s.node_count = id + 1;
-            if (e.parent != kInvalidId) {
-                if (e.side == 0) a.nodes[e.parent].left = id;
-                else a.nodes[e.parent].right = id;
-            }
-            a.depth[id] = e.depth;
-            s.max_depth = max(s.max_depth, e.depth);
-        }
-        __syncthreads();
         const long long c1 = clock64();
-        if (a.x8) block_split_node<true>(a, s, e, id);
-        else block_split_node<false>(a, s, e, id);
-        if (tid == 0) s.cyc_block += clock64() - c1;
+        if (cmd == 1) {
+            if (a.x8) cluster_split_node<true>(a, s, lead, cl, rank, C, e, lead->cmd_id, lead->cmd_d);
+            else cluster_split_node<false>(a, s, lead, cl, rank, C, e, lead->cmd_id, lead->cmd_d);
+        } else if (rank == 0) {
+            if (a.x8) block_split_node<true>(a, s, e, s.cmd_id);
+            else block_split_node<false>(a, s, e, s.cmd_id);
+        }
+        if (rank == 0 && tid == 0) s.cyc_block += clock64() - c1;
     }
+    cl.sync();  // the leader's shared memory stays mapped until every CTA is done with it
+    if (rank != 0) return;
     __syncthreads();
     if (tid == 0) {
         a.meta[0] = s.node_count;
@@ -1277,6 +1516,7 @@ int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_ca
         DevBuf<uint32_t> meta(8 * n_trees);
         DevBuf<uint32_t> draws(size_t(n) * n_trees);
         DevBuf<float> col(size_t(n) * n_trees);
+        DevBuf<uint32_t> ltmp(size_t(n) * n_trees);
         LAUNCH(draws_kernel, n_trees, 320, 0, seed, ds->dim, n, draws.p);
         std::vector<BuildArgs> args(n_trees);
         for (uint32_t t = 0; t < n_trees; ++t) {
@@ -1289,13 +1529,44 @@ int annk_forest_build(const annk_dataset* ds, uint32_t n_trees, uint32_t leaf_ca
                                 tr.nodes.p, tr.depth.p, tr.even.p, tr.pidx.p,
                                 rtmp.p + size_t(t) * n, sortbuf.p + size_t(t) * next_pow2(n),
                                 meta.p + 8 * t, ds->u8 ? ds->data8.p : nullptr, ds->ld8,
-                                draws.p + size_t(t) * n, n, col.p + size_t(t) * n};
+                                draws.p + size_t(t) * n, n, col.p + size_t(t) * n, ltmp.p + size_t(t) * n};
         }
         DevBuf<BuildArgs> dargs(n_trees);
         dargs.upload(args.data(), n_trees);
         const size_t smem = sizeof(Smem);
         CK(cudaFuncSetAttribute(forest_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        LAUNCH(forest_build_kernel, n_trees, kBlock, smem, dargs.p);
+        // one thread-block cluster per tree: the largest size (<= 8) at which all
+        // trees' clusters are co-resident (each CTA needs a whole SM's shared memory)
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.blockDim = dim3(kBlock);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream();
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        uint32_t csize = 1;
+        const char* env = getenv("ANNK_FOREST_CLUSTER");
+        for (uint32_t c = kMaxCluster; c > 1; c /= 2) {
+            if (env && uint32_t(atoi(env)) < c) continue;
+            attr[0].val.clusterDim.x = c;
+            cfg.gridDim = dim3(n_trees * c);
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, forest_build_kernel, &cfg) == cudaSuccess &&
+                ncl >= int(n_trees)) {
+                csize = c;
+                break;
+            }
+            (void)cudaGetLastError();
+        }
+        attr[0].val.clusterDim.x = csize;
+        cfg.gridDim = dim3(n_trees * csize);
+        prof_begin("forest_build_kernel");
+        CK(cudaLaunchKernelEx(&cfg, forest_build_kernel, static_cast<const BuildArgs*>(dargs.p)));
+        prof_end();
+        note_launch();
         std::vector<uint32_t> hm(8 * n_trees);
         meta.download(hm.data(), hm.size());
         ssync();

@@ -409,3 +409,19 @@ def test_wide_fp32_rows_join_bit_exact():
         A.detail.nn_descent_iteration(sd, x)
         e = assert_pools_equal(sd, so)
         assert sd.meta()["dist_comps"] == e["dist_comps"]
+
+
+@pytest.mark.parametrize("n,dim,trees,integer,dups", [
+    (100000, 8, 2, False, 0),      # fp32 path: nodes > 32k points are split by the whole CTA cluster
+    (80000, 32, 2, True, 0),       # u8 path
+    (90000, 16, 1, True, 40000),   # a 40k duplicate block: degenerate split of a cluster node
+])
+def test_forest_cluster_split_bit_identical(n, dim, trees, integer, dups):
+    o = ora()
+    x = mixture(n, dim, 40, 5) if integer else A.gen_synthetic(n, dim, 5)
+    if dups:
+        x[:dups] = x[7]
+    fo = o.build_forest(o.vs(x), trees, 8, 13)
+    fd = A.build_forest(x, trees, 8, 13)
+    for t in range(trees):
+        assert_trees_equal(fd.tree(t), fo.tree(t))
