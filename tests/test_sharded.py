@@ -172,3 +172,36 @@ def test_device_shard_integer_mixture_u8_path():
     for i in range(4000):
         m = int(sizes[i])
         np.testing.assert_array_equal(ids[i, :m], ref["ids"][i, :m])
+
+
+def _nccl_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        import paper_1609_07228_b200 as A
+        o = ora()
+        x = _data(o)
+        vs = A.VectorSet(x)
+        f = A.build_forest(vs, TREES, LEAF, SEED)
+        lo, hi = SH.shard_ranges(N, world)[rank]
+        e = SH.DeviceShard(vs, f, K, DEP, P, S, SEED, lo, hi, buffer_device="cuda")
+        comm = SH.TorchComm("cuda")
+        comps = [SH.nn_descent_round(e, comm)[1] for _ in range(ITERS)]
+        pools = e.pools()
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), sizes=pools[0], ids=pools[1], dists=pools[2],
+                 flags=pools[3], comps=np.array(comps, np.int64))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_single_rank_device_buffers():
+    # the multi-GPU bench path (NCCL collectives on CUDA tensors) with one rank
+    o = ora()
+    ref, ref_comps = _single(o, _data(o))
+    with tempfile.TemporaryDirectory() as d:
+        torch.multiprocessing.spawn(_nccl_worker, args=(1, _free_port(), d), nprocs=1, join=True)
+        z = np.load(os.path.join(d, "rank0.npz"))
+        parts = [((z["sizes"], z["ids"], z["dists"], z["flags"]), [int(c) for c in z["comps"]])]
+    _check(parts, ref, ref_comps)
