@@ -594,23 +594,34 @@ class GraphSearcher:
         return SearchParamsC(p.k_return, p.pool_size, p.expansion, p.iters, p.n_trees_used,
                              p.random_seed_count, seed_base, int(random_init))
 
-    def search_batch(self, queries, params: SearchParams, random_init: bool = False) -> BatchResult:
+    def search_batch(self, queries, params: SearchParams, random_init: bool = False,
+                     out: Optional[tuple] = None) -> BatchResult:
         """All queries at once; per-query seed = substream(params.seed, qi) as in
-        recall_curve (search.cpp:208)."""
+        recall_curve (search.cpp:208).  `out` = (ids, dists, stats) caller
+        buffers (nq x k_return uint32, nq x k_return float32, nq x 4 uint64),
+        e.g. pinned host memory for fast device-to-host copies."""
         cp = self._params(params, random_init, params.seed)
+        q = None
         if isinstance(queries, VectorSet):
             nq = queries.n
-            ids = np.empty((nq, params.k_return), np.uint32)
-            d = np.empty((nq, params.k_return), np.float32)
-            st = np.empty((nq, 4), np.uint64)
-            check(lib.annk_search_dataset(self._h, queries.handle, C.byref(cp), ids, d, ptr(st)))
         else:
             q = np.ascontiguousarray(np.atleast_2d(queries), np.float32)
-            nq, dim = q.shape
-            ids = np.empty((nq, params.k_return), np.uint32)
-            d = np.empty((nq, params.k_return), np.float32)
+            nq = q.shape[0]
+        kr = params.k_return
+        if out is None:
+            ids = np.empty((nq, kr), np.uint32)
+            d = np.empty((nq, kr), np.float32)
             st = np.empty((nq, 4), np.uint64)
-            check(lib.annk_search(self._h, q, nq, dim, C.byref(cp), ids, d, ptr(st)))
+        else:
+            ids, d, st = out
+            if (ids.shape != (nq, kr) or d.shape != (nq, kr) or st.shape != (nq, 4) or ids.dtype != np.uint32
+                    or d.dtype != np.float32 or st.dtype != np.uint64 or not all(
+                        a.flags.c_contiguous for a in (ids, d, st))):
+                raise InvalidArgument("search: output buffers must be nq x k_return uint32 / float32, nq x 4 uint64")
+        if q is None:
+            check(lib.annk_search_dataset(self._h, queries.handle, C.byref(cp), ids, d, ptr(st)))
+        else:
+            check(lib.annk_search(self._h, q, nq, q.shape[1], C.byref(cp), ids, d, ptr(st)))
         return BatchResult(ids, d, st)
 
     def _one(self, q, params, random_init):
