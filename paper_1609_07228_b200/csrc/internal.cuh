@@ -11,7 +11,7 @@
 // Tree node as the kernels see it: 16 bytes, one sector per descent hop.
 // (Reference KdNode, kd_forest.hpp:18-27; depth and even_split live in
 // side arrays because descents never read them.)
-struct KdNodeDev {
+struct __align__(16) KdNodeDev {  // one 128-bit load per descent step
     uint32_t split_dim;  // annk::kLeaf => leaf
     float split_val;
     uint32_t left;   // internal: left child; leaf: range start in point_index

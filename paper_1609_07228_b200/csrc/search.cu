@@ -24,7 +24,8 @@ namespace annk {
 namespace {
 
 constexpr uint32_t kThreads = 256;
-constexpr uint32_t kBuf = 2048;
+constexpr uint32_t kBuf = 1024;
+constexpr size_t kHeapSmem = 12288;  // BBF heaps in shared memory up to this size
 
 struct HeapEnt {
     double cost;
@@ -54,9 +55,9 @@ struct SearchArgs {
     uint32_t words;
     uint32_t* vlist;     // slots x vcap
     uint32_t vcap;
-    HeapEnt* heaps;      // slots x nt x hcap
+    HeapEnt* heaps;      // slots x nt x hcap (nullptr: heaps in shared memory)
     uint32_t hcap;
-    uint32_t* leaves;    // slots x nt x n_node
+    uint2* leaves;       // slots x nt x n_node leaf ranges [left, right) of point_index
     uint64_t* mtstate;   // slots x 312 (random init)
     uint64_t* out_keys;  // nq x k_return
     uint64_t* stats;     // nq x 4
@@ -82,7 +83,12 @@ struct Smem {
     int32_t qnorm;
     uint32_t* ctr;      // [0] pool size, [1] buf count, [2] visited count, [3] seeds, [4] reserve size,
                         // [5] expand count, [6] leaves visited, [7] hops
+    uint32_t* hist;     // kHist radix-select bins + 8 scalars
+    HeapEnt* heap;      // nt x hcap when the heaps fit kHeapSmem
 };
+
+constexpr uint32_t kHist = 256;
+constexpr uint32_t kConsumed = 0xffffffffu;  // reserve entry already offered (low word of an id-major key)
 
 __device__ __forceinline__ uint32_t lower_bound64(const uint64_t* a, uint32_t n, uint64_t v) {
     uint32_t lo = 0, hi = n;
@@ -129,18 +135,135 @@ __device__ __forceinline__ uint32_t block_scan(Smem& s, bool f, uint32_t* tot) {
     return pre + __popc(b & ((1u << lane) - 1u));
 }
 
-// pool := top-P(pool U buf), dedup by key (pool entry wins; buffer entries unchecked).
+template <int V>
+__device__ __forceinline__ void warp0_sort(uint64_t* a, uint32_t n) {
+    if (threadIdx.x < 32) {
+        uint64_t v[V];
+#pragma unroll
+        for (int r = 0; r < V; ++r) {
+            const uint32_t e = uint32_t(r) * 32 + threadIdx.x;
+            v[r] = e < n ? a[e] : kEmptyKey;
+        }
+        warp_sort_regs<V>(v);
+#pragma unroll
+        for (int r = 0; r < V; ++r) {
+            const uint32_t e = uint32_t(r) * 32 + threadIdx.x;
+            if (e < n) a[e] = v[r];
+        }
+    }
+}
+
+// Ascending sort of a[0..n); up to 256 keys in warp 0's registers (no block
+// barriers inside), larger sets by the block (a must have room for
+// next_pow2(n) keys).  Ends with a barrier.
+__device__ void block_sort_keys(uint64_t* a, uint32_t n) {
+    if (n <= 32) warp0_sort<1>(a, n);
+    else if (n <= 64) warp0_sort<2>(a, n);
+    else if (n <= 128) warp0_sort<4>(a, n);
+    else if (n <= 256) warp0_sort<8>(a, n);
+    else {
+        const uint32_t m = next_pow2(n);
+        for (uint32_t j = n + threadIdx.x; j < m; j += kThreads) a[j] = kEmptyKey;
+        __syncthreads();
+        block_bitonic_sort(a, m);
+    }
+    __syncthreads();
+}
+
+// Keep the `want` smallest of the c (> want) DISTINCT keys in buf, compacted
+// to buf[0..want) in no particular order: MSD radix select over 8-bit digits,
+// starting at the highest bit in which the keys differ.  Entry and exit at a
+// barrier.
+__device__ void block_select_smallest(Smem& s, uint32_t c, uint32_t want) {
+    uint32_t* hist = s.hist;
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    if (tid < 2) hist[kHist + tid] = 0;
+    __syncthreads();
+    const uint64_t k0 = s.buf[0];
+    uint64_t diff = 0;
+    for (uint32_t j = tid; j < c; j += kThreads) diff |= s.buf[j] ^ k0;
+    const uint32_t dlo = __reduce_or_sync(0xffffffffu, uint32_t(diff));
+    const uint32_t dhi = __reduce_or_sync(0xffffffffu, uint32_t(diff >> 32));
+    if (lane == 0) {
+        if (dlo) atomicOr(&hist[kHist], dlo);
+        if (dhi) atomicOr(&hist[kHist + 1], dhi);
+    }
+    __syncthreads();
+    const uint64_t d = (uint64_t(hist[kHist + 1]) << 32) | hist[kHist];
+    int shift = d ? ((63 - __clzll(d)) & ~7) : 0;  // byte holding the highest differing bit
+    uint64_t prefix = shift + 8 < 64 ? (k0 >> (shift + 8)) << (shift + 8) : 0;
+    uint32_t need = want;
+    for (;;) {
+        for (uint32_t j = tid; j < kHist; j += kThreads) hist[j] = 0;
+        __syncthreads();
+        const uint32_t hs = uint32_t(shift) + 8;
+        for (uint32_t j = tid; j < c; j += kThreads) {
+            const uint64_t v = s.buf[j];
+            if (hs >= 64 || (v >> hs) == (prefix >> hs)) atomicAdd(&hist[uint32_t(v >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {  // bucket b with below(b) < need <= below(b) + hist[b]
+            uint32_t h[8], sum = 0;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) { h[r] = hist[lane * 8 + r]; sum += h[r]; }
+            uint32_t inc = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= uint32_t(o)) inc += t;
+            }
+            uint32_t below = inc - sum;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                if (below < need && need <= below + h[r]) {
+                    hist[kHist + 2] = lane * 8 + r;
+                    hist[kHist + 3] = below;
+                    hist[kHist + 4] = h[r];
+                }
+                below += h[r];
+            }
+        }
+        __syncthreads();
+        const uint32_t b = hist[kHist + 2], below = hist[kHist + 3], inb = hist[kHist + 4];
+        prefix |= uint64_t(b) << shift;
+        need -= below;
+        if (need == inb || shift == 0) break;  // distinct keys: at shift 0 a bucket holds one key
+        shift -= 8;
+    }
+    // keep v iff (v >> shift) <= (prefix >> shift): exactly `want` keys
+    uint32_t nu = 0;
+    for (uint32_t base = 0; base < c; base += kThreads) {
+        const uint32_t j = base + tid;
+        uint64_t v = 0;
+        bool keep = false;
+        if (j < c) {
+            v = s.buf[j];
+            keep = (v >> shift) <= (prefix >> shift);
+        }
+        uint32_t tot;
+        const uint32_t pos = block_scan(s, keep, &tot);
+        if (keep) s.buf[nu + pos] = v;  // nu + pos <= j; block_scan's barriers order reads before writes
+        nu += tot;
+    }
+    DCHK(nu == want);
+    __syncthreads();
+}
+
+// pool := top-P(pool U buf).  Buffer keys are distinct (fresh visits, and
+// reserve entries are consumed on their first offer); a buffer key may equal
+// a pool key only in the fallback scan, so pooled keys are dropped here.
+// Only the P smallest buffer keys can enter the top-P, so larger buffers are
+// cut to those before sorting.
 __device__ void merge_buffer(const SearchArgs& a, Smem& s) {
     __syncthreads();
-    const uint32_t c = s.ctr[1];
+    uint32_t c = s.ctr[1];
     if (c == 0) return;
-    const uint32_t m = next_pow2(c);
-    DCHK(m <= kBuf);
-    for (uint32_t j = c + threadIdx.x; j < m; j += kThreads) s.buf[j] = kEmptyKey;
-    __syncthreads();
-    block_bitonic_sort(s.buf, m);
+    if (c > a.P) {
+        block_select_smallest(s, c, a.P);
+        c = a.P;
+    }
+    block_sort_keys(s.buf, c);
     const uint32_t ps = s.ctr[0];
-    // unique and not already pooled, compacted in order
     uint32_t nu = 0;
     for (uint32_t base = 0; base < c; base += kThreads) {
         const uint32_t j = base + threadIdx.x;
@@ -148,19 +271,15 @@ __device__ void merge_buffer(const SearchArgs& a, Smem& s) {
         bool keep = false;
         if (j < c) {
             v = s.buf[j];
-            keep = j == 0 || s.buf[j - 1] != v;
-            if (keep) {
-                const uint32_t p = lower_bound64(s.pool, ps, v);
-                keep = !(p < ps && s.pool[p] == v);
-            }
+            const uint32_t p = lower_bound64(s.pool, ps, v);
+            keep = !(p < ps && s.pool[p] == v);
         }
         uint32_t tot;
         const uint32_t pos = block_scan(s, keep, &tot);
-        __syncthreads();
-        if (keep) s.buf[nu + pos] = v;  // nu + pos <= j: in-place compaction is safe after the barrier
+        if (keep) s.buf[nu + pos] = v;
         nu += tot;
-        __syncthreads();
     }
+    __syncthreads();
     for (uint32_t j = threadIdx.x; j < ps; j += kThreads) {
         const uint32_t r = j + lower_bound64(s.buf, nu, s.pool[j]);
         if (r < a.P) { s.tmp[r] = s.pool[j]; s.tmpc[r] = s.checked[j]; }
@@ -198,7 +317,8 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
     Smem s;
     {
         unsigned char* p = raw;
-        s.q = reinterpret_cast<float*>(p); p += size_t(a.ld) * 4;  // first: float4 loads need 16 B alignment
+        s.heap = reinterpret_cast<HeapEnt*>(p); p += a.heaps ? 0 : size_t(a.nt) * a.hcap * sizeof(HeapEnt);
+        s.q = reinterpret_cast<float*>(p); p += size_t(a.ld) * 4;  // float4 loads need 16 B alignment
         s.q8 = p; p += a.x8 ? a.ld8 : 0;
         s.pool = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
         s.tmp = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
@@ -207,6 +327,7 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
         s.expand = reinterpret_cast<uint32_t*>(p); p += size_t(a.P) * 4;
         s.scan = reinterpret_cast<uint32_t*>(p); p += 64;
         s.ctr = reinterpret_cast<uint32_t*>(p); p += 64;
+        s.hist = reinterpret_cast<uint32_t*>(p); p += (kHist + 8) * 4;
         s.checked = p; p += a.P;
         s.tmpc = p;
     }
@@ -223,15 +344,16 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
         if (!a.random_init) {
             if (tid < a.nt) {
                 const TreeView tv = a.trees[tid];
-                HeapEnt* h = a.heaps + (size_t(slot) * a.nt + tid) * a.hcap;
-                uint32_t* out = a.leaves + (size_t(slot) * a.nt + tid) * a.n_node;
+                HeapEnt* h = a.heaps ? a.heaps + (size_t(slot) * a.nt + tid) * a.hcap : s.heap + tid * a.hcap;
+                uint2* out = a.leaves + (size_t(slot) * a.nt + tid) * a.n_node;
                 const uint32_t want = min(a.n_node, tv.leaf_count);
                 uint32_t hn = 0, cnt = 0;
                 uint32_t nd = tv.root;
                 double cost = 0.0;
                 if (want > 0) {
                     for (;;) {
-                        for (KdNodeDev x = tv.nodes[nd]; x.split_dim != kLeaf; x = tv.nodes[nd]) {
+                        KdNodeDev x = tv.nodes[nd];
+                        for (; x.split_dim != kLeaf; x = tv.nodes[nd]) {
                             const double diff = double(s.q[x.split_dim]) - double(x.split_val);
                             const HeapEnt v{cost + fabs(diff), diff <= 0.0 ? x.right : x.left, 0};
                             uint32_t i = hn++;
@@ -246,7 +368,7 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
                             nd = diff <= 0.0 ? x.left : x.right;
                         }
                         DCHK(cnt < a.n_node);
-                        out[cnt++] = nd;
+                        out[cnt++] = make_uint2(x.left, x.right);
                         if (cnt >= want || hn == 0) break;
                         const HeapEnt top = h[0];
                         const HeapEnt last = h[--hn];
@@ -264,20 +386,18 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
                         cost = top.cost;
                     }
                 }
-                for (uint32_t j = cnt; j < a.n_node; ++j) out[j] = kInvalidId;
+                for (uint32_t j = cnt; j < a.n_node; ++j) out[j] = make_uint2(0, 0);
                 atomicAdd(&s.ctr[6], cnt);
             }
             __syncthreads();
-            // visit every point of every emitted leaf
-            const uint32_t total_leaves = a.nt * a.n_node;
-            for (uint32_t L = tid; L < total_leaves; L += kThreads) {
-                const uint32_t t = L / a.n_node;
-                const uint32_t leaf = a.leaves[size_t(slot) * a.nt * a.n_node + L];
-                if (leaf == kInvalidId) continue;
-                const TreeView tv = a.trees[t];
-                const KdNodeDev ln = tv.nodes[leaf];
-                for (uint32_t p = ln.left; p < ln.right; ++p) {
-                    const uint32_t id = tv.pidx[p];
+            // visit every point of every emitted leaf: one thread per (leaf, slot)
+            const uint32_t items = a.nt * a.n_node * a.leaf_cap;
+            for (uint32_t j = tid; j < items; j += kThreads) {
+                const uint32_t L = j / a.leaf_cap;
+                const uint2 r = a.leaves[size_t(slot) * a.nt * a.n_node + L];
+                const uint32_t* pidx = a.trees[L / a.n_node].pidx;
+                for (uint32_t p = r.x + (j - L * a.leaf_cap); p < r.y; p += a.leaf_cap) {
+                    const uint32_t id = pidx[p];
                     if (mark_visited(a, slot, s, id)) {
                         const uint32_t k = atomicAdd(&s.ctr[3], 1u);
                         DCHK(k < a.seed_cap); DCHK(id < a.n);
@@ -317,9 +437,7 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
         __syncthreads();
         const uint32_t ns = s.ctr[3];
         const uint32_t m = next_pow2(max(ns, 1u));
-        for (uint32_t j = ns + tid; j < m; j += kThreads) s.seeds[j] = kEmptyKey;
-        __syncthreads();
-        block_bitonic_sort(s.seeds, m);
+        block_sort_keys(s.seeds, ns);
         const uint32_t ps = min(ns, a.E);
         for (uint32_t j = tid; j < ps; j += kThreads) {
             s.pool[j] = s.seeds[j];
@@ -343,7 +461,7 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
             s.ctr[4] = nr;
         }
         __syncthreads();
-        if (nr > 1) block_bitonic_sort(s.seeds, next_pow2(nr));
+        if (nr > 1) block_sort_keys(s.seeds, nr);
         // ------------------------------------------------ expansion rounds
         for (uint32_t it = 0; it < a.iters; ++it) {
             const uint32_t pss = s.ctr[0];
@@ -375,11 +493,19 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
                         const uint64_t key = make_key(qdist(a, s, nb), nb);
                         if (key < thr) push_buf(s, key);
                     } else if (s.ctr[4]) {
+                        // a reserve seed re-enters with its cached distance (search.cpp:79-82).
+                        // It is offered once: the pool tail never rises, so a key
+                        // the pool rejects (or evicts) can never re-enter it.
                         const uint32_t nrr = s.ctr[4];
                         const uint32_t p = lower_bound64(s.seeds, nrr, uint64_t(nb) << 32);
-                        if (p < nrr && uint32_t(s.seeds[p] >> 32) == nb) {
-                            const uint64_t key = (uint64_t(uint32_t(s.seeds[p])) << 32) | nb;
-                            if (key < thr) push_buf(s, key);
+                        const uint64_t e = p < nrr ? s.seeds[p] : 0;
+                        if (p < nrr && uint32_t(e >> 32) == nb && uint32_t(e) != kConsumed) {
+                            const uint64_t key = (uint64_t(uint32_t(e)) << 32) | nb;
+                            if (key < thr) {
+                                const unsigned long long mark = (uint64_t(nb) << 32) | kConsumed;
+                                const uint64_t old = atomicExch(reinterpret_cast<unsigned long long*>(&s.seeds[p]), mark);
+                                if (uint32_t(old) != kConsumed) push_buf(s, key);
+                            }
                         }
                     }
                 }
@@ -473,8 +599,11 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
                        : std::min<uint64_t>(uint64_t(nt) * n_node * leaf_cap, base->n);
     const uint32_t seed_cap = next_pow2(uint32_t(std::max<uint64_t>(seed_bound, 1)));
     const uint32_t P = p->pool_size;
-    const size_t smem = size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kBuf) * 8 + size_t(base->ld) * 4 +
-                        size_t(P) * 4 + 128 + size_t(P) * 2 + 16 + base->ld8;
+    const uint32_t hcap = (n_node + 1) * (max_depth + 1) + 1;
+    const size_t heap_bytes = size_t(nt) * hcap * sizeof(HeapEnt);
+    const bool heap_smem = heap_bytes <= kHeapSmem;
+    const size_t smem = (heap_smem ? heap_bytes : 0) + size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kBuf) * 8 +
+                        size_t(base->ld) * 4 + size_t(P) * 4 + 128 + (kHist + 8) * 4 + size_t(P) * 2 + 16 + base->ld8;
     if (smem > size_t(max_smem_optin()))
         throw_invalid("search: pool_size/seed budget exceeds on-chip capacity");
     CK(cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -484,11 +613,10 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
     const uint32_t words = (base->n + 31) / 32;
     const uint64_t vbound = seed_bound + uint64_t(p->iters) * P * sr->gk;
     const uint32_t vcap = uint32_t(std::min<uint64_t>(vbound, base->n));
-    const uint32_t hcap = (n_node + 1) * (max_depth + 1) + 1;
     DevBuf<uint32_t> bitmap(size_t(slots) * words), vlist(size_t(slots) * std::max(vcap, 1u));
     bitmap.zero();
-    DevBuf<HeapEnt> heaps(std::max<size_t>(size_t(slots) * nt * hcap, 1));
-    DevBuf<uint32_t> leaves(std::max<size_t>(size_t(slots) * nt * n_node, 1));
+    DevBuf<HeapEnt> heaps(heap_smem ? 0 : size_t(slots) * nt * hcap);
+    DevBuf<uint2> leaves(std::max<size_t>(size_t(slots) * nt * n_node, 1));
     DevBuf<uint64_t> mt(p->random_init ? size_t(slots) * 312 : 1);
     DevBuf<uint64_t> keys(size_t(nq) * p->k_return), st(size_t(nq) * 4);
     const bool u8 = base->u8 && qds->u8 && base->ld8 == qds->ld8;

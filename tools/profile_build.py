@@ -27,5 +27,5 @@ for _ in range(args.iters):
     A.detail.nn_descent_iteration(s, vs)
 if args.search:
     g = A.finalize(s, vs, cfg["k"])
-    r = A.GraphSearcher(vs, f, g).search_batch(queries, A.SearchParams(cfg["k_return"], cfg["P"], cfg["P"], 4))
+    r = A.GraphSearcher(vs, f, g).search_batch(queries, A.SearchParams(cfg["k_return"], cfg["P"], 16, 1))  # the bench's chosen point
 print("profile_build done", A.launch_count())
