@@ -55,9 +55,9 @@ struct SearchArgs {
     uint32_t words;
     uint32_t* vlist;     // slots x vcap
     uint32_t vcap;
-    HeapEnt* heaps;      // slots x nt x hcap (nullptr: heaps in shared memory)
+    HeapEnt* heaps;      // slots x 32 x hcap (nullptr: heaps in shared memory)
     uint32_t hcap;
-    uint2* leaves;       // slots x nt x n_node leaf ranges [left, right) of point_index
+    uint2* leaves;       // slots x 2 x nt x n_node leaf ranges [left, right) of point_index
     uint64_t* mtstate;   // slots x 312 (random init)
     uint64_t* out_keys;  // nq x k_return
     uint64_t* stats;     // nq x 4
@@ -84,7 +84,8 @@ struct Smem {
     uint32_t* ctr;      // [0] pool size, [1] buf count, [2] visited count, [3] seeds, [4] reserve size,
                         // [5] expand count, [6] leaves visited, [7] hops
     uint32_t* hist;     // kHist radix-select bins + 8 scalars
-    HeapEnt* heap;      // nt x hcap when the heaps fit kHeapSmem
+    HeapEnt* heap;      // min(nt, 32) x hcap when the heaps fit kHeapSmem
+    uint32_t* lcnt;     // leaves emitted per leaf-range buffer
 };
 
 constexpr uint32_t kHist = 256;
@@ -118,19 +119,46 @@ __device__ __forceinline__ float qdist(const SearchArgs& a, const Smem& s, uint3
     return l2_exact_ldg(s.q, a.x + size_t(id) * a.ld, a.ld);
 }
 
+// Worker barrier (named barrier 1 over the W worker threads; the BBF
+// producer warp, when present, never joins it).
+template <uint32_t W>
+__device__ __forceinline__ void wsync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(W) : "memory");
+}
+// Producer/worker hand-off barriers over all kThreads threads; id is
+// 2 + b ("ranges of buffer b ready") or 4 + b ("buffer b read").  Immediate
+// barrier ids keep the kernel at 6 hardware barriers.
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t) {
+    switch (id) {
+        case 2: asm volatile("bar.sync 2, %0;" ::"n"(kThreads) : "memory"); break;
+        case 3: asm volatile("bar.sync 3, %0;" ::"n"(kThreads) : "memory"); break;
+        case 4: asm volatile("bar.sync 4, %0;" ::"n"(kThreads) : "memory"); break;
+        default: asm volatile("bar.sync 5, %0;" ::"n"(kThreads) : "memory"); break;
+    }
+}
+__device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t) {
+    switch (id) {
+        case 2: asm volatile("bar.arrive 2, %0;" ::"n"(kThreads) : "memory"); break;
+        case 3: asm volatile("bar.arrive 3, %0;" ::"n"(kThreads) : "memory"); break;
+        case 4: asm volatile("bar.arrive 4, %0;" ::"n"(kThreads) : "memory"); break;
+        default: asm volatile("bar.arrive 5, %0;" ::"n"(kThreads) : "memory"); break;
+    }
+}
+
 // Block exclusive scan of one flag per thread; returns prefix, total in *tot.
+template <uint32_t W>
 __device__ __forceinline__ uint32_t block_scan(Smem& s, bool f, uint32_t* tot) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t b = __ballot_sync(0xffffffffu, f);
     if (lane == 0) s.scan[warp] = __popc(b);
-    __syncthreads();
+    wsync<W>();
     uint32_t pre = 0, all = 0;
-    for (uint32_t w = 0; w < kThreads / 32; ++w) {
+    for (uint32_t w = 0; w < W / 32; ++w) {
         const uint32_t c = s.scan[w];
         if (w < warp) pre += c;
         all += c;
     }
-    __syncthreads();
+    wsync<W>();
     *tot = all;
     return pre + __popc(b & ((1u << lane) - 1u));
 }
@@ -156,6 +184,7 @@ __device__ __forceinline__ void warp0_sort(uint64_t* a, uint32_t n) {
 // Ascending sort of a[0..n); up to 256 keys in warp 0's registers (no block
 // barriers inside), larger sets by the block (a must have room for
 // next_pow2(n) keys).  Ends with a barrier.
+template <uint32_t W>
 __device__ void block_sort_keys(uint64_t* a, uint32_t n) {
     if (n <= 32) warp0_sort<1>(a, n);
     else if (n <= 64) warp0_sort<2>(a, n);
@@ -163,45 +192,57 @@ __device__ void block_sort_keys(uint64_t* a, uint32_t n) {
     else if (n <= 256) warp0_sort<8>(a, n);
     else {
         const uint32_t m = next_pow2(n);
-        for (uint32_t j = n + threadIdx.x; j < m; j += kThreads) a[j] = kEmptyKey;
-        __syncthreads();
-        block_bitonic_sort(a, m);
+        for (uint32_t j = n + threadIdx.x; j < m; j += W) a[j] = kEmptyKey;
+        wsync<W>();
+        for (uint32_t k = 2; k <= m; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = threadIdx.x; i < m; i += W) {
+                    const uint32_t ixj = i ^ j;
+                    if (ixj > i) {
+                        const uint64_t x = a[i], y = a[ixj];
+                        if ((x > y) == ((i & k) == 0)) { a[i] = y; a[ixj] = x; }
+                    }
+                }
+                wsync<W>();
+            }
+        }
     }
-    __syncthreads();
+    wsync<W>();
 }
 
 // Keep the `want` smallest of the c (> want) DISTINCT keys in buf, compacted
 // to buf[0..want) in no particular order: MSD radix select over 8-bit digits,
 // starting at the highest bit in which the keys differ.  Entry and exit at a
 // barrier.
+template <uint32_t W>
 __device__ void block_select_smallest(Smem& s, uint32_t c, uint32_t want) {
     uint32_t* hist = s.hist;
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     if (tid < 2) hist[kHist + tid] = 0;
-    __syncthreads();
+    wsync<W>();
     const uint64_t k0 = s.buf[0];
     uint64_t diff = 0;
-    for (uint32_t j = tid; j < c; j += kThreads) diff |= s.buf[j] ^ k0;
+    for (uint32_t j = tid; j < c; j += W) diff |= s.buf[j] ^ k0;
     const uint32_t dlo = __reduce_or_sync(0xffffffffu, uint32_t(diff));
     const uint32_t dhi = __reduce_or_sync(0xffffffffu, uint32_t(diff >> 32));
     if (lane == 0) {
         if (dlo) atomicOr(&hist[kHist], dlo);
         if (dhi) atomicOr(&hist[kHist + 1], dhi);
     }
-    __syncthreads();
+    wsync<W>();
     const uint64_t d = (uint64_t(hist[kHist + 1]) << 32) | hist[kHist];
     int shift = d ? ((63 - __clzll(d)) & ~7) : 0;  // byte holding the highest differing bit
     uint64_t prefix = shift + 8 < 64 ? (k0 >> (shift + 8)) << (shift + 8) : 0;
     uint32_t need = want;
     for (;;) {
-        for (uint32_t j = tid; j < kHist; j += kThreads) hist[j] = 0;
-        __syncthreads();
+        for (uint32_t j = tid; j < kHist; j += W) hist[j] = 0;
+        wsync<W>();
         const uint32_t hs = uint32_t(shift) + 8;
-        for (uint32_t j = tid; j < c; j += kThreads) {
+        for (uint32_t j = tid; j < c; j += W) {
             const uint64_t v = s.buf[j];
             if (hs >= 64 || (v >> hs) == (prefix >> hs)) atomicAdd(&hist[uint32_t(v >> shift) & 255u], 1u);
         }
-        __syncthreads();
+        wsync<W>();
         if (tid < 32) {  // bucket b with below(b) < need <= below(b) + hist[b]
             uint32_t h[8], sum = 0;
 #pragma unroll
@@ -223,7 +264,7 @@ __device__ void block_select_smallest(Smem& s, uint32_t c, uint32_t want) {
                 below += h[r];
             }
         }
-        __syncthreads();
+        wsync<W>();
         const uint32_t b = hist[kHist + 2], below = hist[kHist + 3], inb = hist[kHist + 4];
         prefix |= uint64_t(b) << shift;
         need -= below;
@@ -232,7 +273,7 @@ __device__ void block_select_smallest(Smem& s, uint32_t c, uint32_t want) {
     }
     // keep v iff (v >> shift) <= (prefix >> shift): exactly `want` keys
     uint32_t nu = 0;
-    for (uint32_t base = 0; base < c; base += kThreads) {
+    for (uint32_t base = 0; base < c; base += W) {
         const uint32_t j = base + tid;
         uint64_t v = 0;
         bool keep = false;
@@ -241,12 +282,12 @@ __device__ void block_select_smallest(Smem& s, uint32_t c, uint32_t want) {
             keep = (v >> shift) <= (prefix >> shift);
         }
         uint32_t tot;
-        const uint32_t pos = block_scan(s, keep, &tot);
+        const uint32_t pos = block_scan<W>(s, keep, &tot);
         if (keep) s.buf[nu + pos] = v;  // nu + pos <= j; block_scan's barriers order reads before writes
         nu += tot;
     }
     DCHK(nu == want);
-    __syncthreads();
+    wsync<W>();
 }
 
 // pool := top-P(pool U buf).  Buffer keys are distinct (fresh visits, and
@@ -254,18 +295,19 @@ __device__ void block_select_smallest(Smem& s, uint32_t c, uint32_t want) {
 // a pool key only in the fallback scan, so pooled keys are dropped here.
 // Only the P smallest buffer keys can enter the top-P, so larger buffers are
 // cut to those before sorting.
+template <uint32_t W>
 __device__ void merge_buffer(const SearchArgs& a, Smem& s) {
-    __syncthreads();
+    wsync<W>();
     uint32_t c = s.ctr[1];
     if (c == 0) return;
     if (c > a.P) {
-        block_select_smallest(s, c, a.P);
+        block_select_smallest<W>(s, c, a.P);
         c = a.P;
     }
-    block_sort_keys(s.buf, c);
+    block_sort_keys<W>(s.buf, c);
     const uint32_t ps = s.ctr[0];
     uint32_t nu = 0;
-    for (uint32_t base = 0; base < c; base += kThreads) {
+    for (uint32_t base = 0; base < c; base += W) {
         const uint32_t j = base + threadIdx.x;
         uint64_t v = kEmptyKey;
         bool keep = false;
@@ -275,31 +317,31 @@ __device__ void merge_buffer(const SearchArgs& a, Smem& s) {
             keep = !(p < ps && s.pool[p] == v);
         }
         uint32_t tot;
-        const uint32_t pos = block_scan(s, keep, &tot);
+        const uint32_t pos = block_scan<W>(s, keep, &tot);
         if (keep) s.buf[nu + pos] = v;
         nu += tot;
     }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < ps; j += kThreads) {
+    wsync<W>();
+    for (uint32_t j = threadIdx.x; j < ps; j += W) {
         const uint32_t r = j + lower_bound64(s.buf, nu, s.pool[j]);
         if (r < a.P) { s.tmp[r] = s.pool[j]; s.tmpc[r] = s.checked[j]; }
     }
-    for (uint32_t j = threadIdx.x; j < nu; j += kThreads) {
+    for (uint32_t j = threadIdx.x; j < nu; j += W) {
         const uint32_t r = j + lower_bound64(s.pool, ps, s.buf[j]);
         if (r < a.P) { s.tmp[r] = s.buf[j]; s.tmpc[r] = 0; }
     }
-    __syncthreads();
+    wsync<W>();
     const uint32_t nps = min(a.P, ps + nu);
-    for (uint32_t j = threadIdx.x; j < nps; j += kThreads) {
+    for (uint32_t j = threadIdx.x; j < nps; j += W) {
         s.pool[j] = s.tmp[j];
         s.checked[j] = s.tmpc[j];
     }
-    __syncthreads();
+    wsync<W>();
     if (threadIdx.x == 0) {
         s.ctr[0] = nps;
         s.ctr[1] = 0;
     }
-    __syncthreads();
+    wsync<W>();
 }
 
 __device__ __forceinline__ uint64_t tail_key(const SearchArgs& a, const Smem& s) {
@@ -312,12 +354,85 @@ __device__ __forceinline__ void push_buf(Smem& s, uint64_t key) {
     s.buf[slot] = key;
 }
 
+// BBF producer (tree-seeded search): the last warp walks the trees of the
+// CTA's NEXT query (kd_forest.cpp:276-305, one lane per tree) while the
+// worker warps process the current one.  Leaf ranges go to one of two
+// buffers; named barriers 2+b ("ranges of buffer b ready", producer arrives)
+// and 4+b ("buffer b read", workers arrive) hand them over.
+__device__ void bbf_producer(const SearchArgs& a, Smem& s) {
+    const uint32_t lane = threadIdx.x & 31, slot = blockIdx.x;
+    HeapEnt* h = a.heaps ? a.heaps + (size_t(slot) * 32 + lane) * a.hcap : s.heap + lane * a.hcap;
+    uint32_t k = 0;
+    for (uint32_t qi = blockIdx.x; qi < a.nq; qi += gridDim.x, ++k) {
+        const uint32_t b = k & 1;
+        if (k >= 2) bar_sync(4 + b, kThreads);
+        const float* q = a.q + size_t(qi) * a.ld;
+        uint2* leaves = a.leaves + (size_t(slot) * 2 + b) * a.nt * a.n_node;
+        uint32_t tot = 0;
+        for (uint32_t t = lane; t < a.nt; t += 32) {
+            const TreeView tv = a.trees[t];
+            uint2* out = leaves + size_t(t) * a.n_node;
+            const uint32_t want = min(a.n_node, tv.leaf_count);
+            uint32_t hn = 0, cnt = 0;
+            uint32_t nd = tv.root;
+            double cost = 0.0;
+            if (want > 0) {
+                for (;;) {
+                    KdNodeDev x = tv.nodes[nd];
+                    for (; x.split_dim != kLeaf; x = tv.nodes[nd]) {
+                        const double diff = double(__ldg(q + x.split_dim)) - double(x.split_val);
+                        const HeapEnt v{cost + fabs(diff), diff <= 0.0 ? x.right : x.left, 0};
+                        uint32_t i = hn++;
+                        while (i > 0) {
+                            const uint32_t p = (i - 1) / 2;
+                            if (!hless(v, h[p])) break;
+                            h[i] = h[p];
+                            i = p;
+                        }
+                        DCHK(i < a.hcap);
+                        h[i] = v;
+                        nd = diff <= 0.0 ? x.left : x.right;
+                    }
+                    DCHK(cnt < a.n_node);
+                    out[cnt++] = make_uint2(x.left, x.right);
+                    if (cnt >= want || hn == 0) break;
+                    const HeapEnt top = h[0];
+                    const HeapEnt last = h[--hn];
+                    uint32_t i = 0;
+                    for (;;) {
+                        uint32_t c = 2 * i + 1;
+                        if (c >= hn) break;
+                        if (c + 1 < hn && hless(h[c + 1], h[c])) ++c;
+                        if (!hless(h[c], last)) break;
+                        h[i] = h[c];
+                        i = c;
+                    }
+                    if (hn) h[i] = last;
+                    nd = top.node;
+                    cost = top.cost;
+                }
+            }
+            for (uint32_t j = cnt; j < a.n_node; ++j) out[j] = make_uint2(0, 0);
+            tot += cnt;
+        }
+        tot = __reduce_add_sync(0xffffffffu, tot);
+        if (lane == 0) s.lcnt[b] = tot;
+        __threadfence_block();
+        __syncwarp();
+        bar_arrive(2 + b, kThreads);
+    }
+    // match the workers' last "buffer read" arrivals so every barrier generation completes
+    for (uint32_t j = k >= 2 ? k - 2 : 0; j < k; ++j) bar_sync(4 + (j & 1), kThreads);
+}
+
+template <bool kTree>
 __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
+    constexpr uint32_t W = kTree ? kThreads - 32 : kThreads;  // worker threads
     extern __shared__ __align__(16) unsigned char raw[];
     Smem s;
     {
         unsigned char* p = raw;
-        s.heap = reinterpret_cast<HeapEnt*>(p); p += a.heaps ? 0 : size_t(a.nt) * a.hcap * sizeof(HeapEnt);
+        s.heap = reinterpret_cast<HeapEnt*>(p); p += a.heaps ? 0 : size_t(min(a.nt, 32u)) * a.hcap * sizeof(HeapEnt);
         s.q = reinterpret_cast<float*>(p); p += size_t(a.ld) * 4;  // float4 loads need 16 B alignment
         s.q8 = p; p += a.x8 ? a.ld8 : 0;
         s.pool = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
@@ -328,83 +443,46 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
         s.scan = reinterpret_cast<uint32_t*>(p); p += 64;
         s.ctr = reinterpret_cast<uint32_t*>(p); p += 64;
         s.hist = reinterpret_cast<uint32_t*>(p); p += (kHist + 8) * 4;
+        s.lcnt = reinterpret_cast<uint32_t*>(p); p += 16;
         s.checked = p; p += a.P;
         s.tmpc = p;
     }
     const uint32_t slot = blockIdx.x, tid = threadIdx.x;
-    for (uint32_t qi = blockIdx.x; qi < a.nq; qi += gridDim.x) {
-        for (uint32_t j = tid; j < a.ld; j += kThreads) s.q[j] = a.q[size_t(qi) * a.ld + j];
+    if (kTree && tid >= W) {
+        bbf_producer(a, s);
+        return;
+    }
+    uint32_t k = 0;
+    for (uint32_t qi = blockIdx.x; qi < a.nq; qi += gridDim.x, ++k) {
+        for (uint32_t j = tid; j < a.ld; j += W) s.q[j] = a.q[size_t(qi) * a.ld + j];
         if (a.x8) {
-            for (uint32_t j = tid; j < a.ld8; j += kThreads) s.q8[j] = a.q8[size_t(qi) * a.ld8 + j];
+            for (uint32_t j = tid; j < a.ld8; j += W) s.q8[j] = a.q8[size_t(qi) * a.ld8 + j];
             s.qnorm = a.qnorms8[qi];
         }
         if (tid < 16) s.ctr[tid] = 0;
-        __syncthreads();
+        wsync<W>();
         // ------------------------------------------------ seeding
-        if (!a.random_init) {
-            if (tid < a.nt) {
-                const TreeView tv = a.trees[tid];
-                HeapEnt* h = a.heaps ? a.heaps + (size_t(slot) * a.nt + tid) * a.hcap : s.heap + tid * a.hcap;
-                uint2* out = a.leaves + (size_t(slot) * a.nt + tid) * a.n_node;
-                const uint32_t want = min(a.n_node, tv.leaf_count);
-                uint32_t hn = 0, cnt = 0;
-                uint32_t nd = tv.root;
-                double cost = 0.0;
-                if (want > 0) {
-                    for (;;) {
-                        KdNodeDev x = tv.nodes[nd];
-                        for (; x.split_dim != kLeaf; x = tv.nodes[nd]) {
-                            const double diff = double(s.q[x.split_dim]) - double(x.split_val);
-                            const HeapEnt v{cost + fabs(diff), diff <= 0.0 ? x.right : x.left, 0};
-                            uint32_t i = hn++;
-                            while (i > 0) {
-                                const uint32_t p = (i - 1) / 2;
-                                if (!hless(v, h[p])) break;
-                                h[i] = h[p];
-                                i = p;
-                            }
-                            DCHK(i < a.hcap);
-                            h[i] = v;
-                            nd = diff <= 0.0 ? x.left : x.right;
-                        }
-                        DCHK(cnt < a.n_node);
-                        out[cnt++] = make_uint2(x.left, x.right);
-                        if (cnt >= want || hn == 0) break;
-                        const HeapEnt top = h[0];
-                        const HeapEnt last = h[--hn];
-                        uint32_t i = 0;
-                        for (;;) {
-                            uint32_t c = 2 * i + 1;
-                            if (c >= hn) break;
-                            if (c + 1 < hn && hless(h[c + 1], h[c])) ++c;
-                            if (!hless(h[c], last)) break;
-                            h[i] = h[c];
-                            i = c;
-                        }
-                        if (hn) h[i] = last;
-                        nd = top.node;
-                        cost = top.cost;
-                    }
-                }
-                for (uint32_t j = cnt; j < a.n_node; ++j) out[j] = make_uint2(0, 0);
-                atomicAdd(&s.ctr[6], cnt);
-            }
-            __syncthreads();
+        if (kTree) {
+            const uint32_t b = k & 1;
+            bar_sync(2 + b, kThreads);  // this query's leaf ranges are ready
+            if (tid == 0) s.ctr[6] = s.lcnt[b];
             // visit every point of every emitted leaf: one thread per (leaf, slot)
+            const uint2* leaves = a.leaves + (size_t(slot) * 2 + b) * a.nt * a.n_node;
             const uint32_t items = a.nt * a.n_node * a.leaf_cap;
-            for (uint32_t j = tid; j < items; j += kThreads) {
+            for (uint32_t j = tid; j < items; j += W) {
                 const uint32_t L = j / a.leaf_cap;
-                const uint2 r = a.leaves[size_t(slot) * a.nt * a.n_node + L];
+                const uint2 r = leaves[L];
                 const uint32_t* pidx = a.trees[L / a.n_node].pidx;
                 for (uint32_t p = r.x + (j - L * a.leaf_cap); p < r.y; p += a.leaf_cap) {
                     const uint32_t id = pidx[p];
                     if (mark_visited(a, slot, s, id)) {
-                        const uint32_t k = atomicAdd(&s.ctr[3], 1u);
-                        DCHK(k < a.seed_cap); DCHK(id < a.n);
-                        s.seeds[k] = make_key(qdist(a, s, id), id);
+                        const uint32_t kk = atomicAdd(&s.ctr[3], 1u);
+                        DCHK(kk < a.seed_cap); DCHK(id < a.n);
+                        s.seeds[kk] = make_key(qdist(a, s, id), id);
                     }
                 }
             }
+            bar_arrive(4 + b, kThreads);  // buffer b may be refilled
         } else {
             // search.cpp:156-173: mt19937_64(seed) draws id % n until `want` distinct
             if (tid == 0) {
@@ -428,49 +506,49 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
                 }
                 s.ctr[3] = have;
             }
-            __syncthreads();
-            for (uint32_t j = tid; j < s.ctr[3]; j += kThreads) {
+            wsync<W>();
+            for (uint32_t j = tid; j < s.ctr[3]; j += W) {
                 const uint32_t id = uint32_t(s.seeds[j]);
                 s.seeds[j] = make_key(qdist(a, s, id), id);
             }
         }
-        __syncthreads();
+        wsync<W>();
         const uint32_t ns = s.ctr[3];
         const uint32_t m = next_pow2(max(ns, 1u));
-        block_sort_keys(s.seeds, ns);
+        block_sort_keys<W>(s.seeds, ns);
         const uint32_t ps = min(ns, a.E);
-        for (uint32_t j = tid; j < ps; j += kThreads) {
+        for (uint32_t j = tid; j < ps; j += W) {
             s.pool[j] = s.seeds[j];
             s.checked[j] = 0;
         }
         // reserve: seeds ranked past E, re-keyed by id for lookup
         const uint32_t nr = ns - ps;
-        for (uint32_t base = 0; base < m; base += kThreads) {  // uniform trip count: barriers inside
+        for (uint32_t base = 0; base < m; base += W) {  // uniform trip count: barriers inside
             const uint32_t j = base + tid;
             uint64_t v = kEmptyKey;
             if (j < nr) {
                 const uint64_t k = s.seeds[ps + j];
                 v = (uint64_t(key_id(k)) << 32) | uint32_t(k >> 32);
             }
-            __syncthreads();
+            wsync<W>();
             if (j < m) s.seeds[j] = v;
-            __syncthreads();
+            wsync<W>();
         }
         if (tid == 0) {
             s.ctr[0] = ps;
             s.ctr[4] = nr;
         }
-        __syncthreads();
-        if (nr > 1) block_sort_keys(s.seeds, nr);
+        wsync<W>();
+        if (nr > 1) block_sort_keys<W>(s.seeds, nr);
         // ------------------------------------------------ expansion rounds
         for (uint32_t it = 0; it < a.iters; ++it) {
             const uint32_t pss = s.ctr[0];
             uint32_t ne = 0;
-            for (uint32_t base = 0; base < pss; base += kThreads) {
+            for (uint32_t base = 0; base < pss; base += W) {
                 const uint32_t j = base + tid;
                 const bool f = j < pss && !s.checked[j];
                 uint32_t tot;
-                const uint32_t pos = block_scan(s, f, &tot);
+                const uint32_t pos = block_scan<W>(s, f, &tot);
                 if (f) {
                     DCHK(ne + pos < a.P);
                     s.expand[ne + pos] = key_id(s.pool[j]);
@@ -478,12 +556,12 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
                 }
                 ne += tot;
             }
-            __syncthreads();
+            wsync<W>();
             if (ne == 0) break;
             if (tid == 0) s.ctr[7] += ne;
             uint64_t thr = tail_key(a, s);
             const uint32_t slots = ne * a.gk;
-            for (uint32_t base = 0; base < slots; base += kThreads) {
+            for (uint32_t base = 0; base < slots; base += W) {
                 const uint32_t j = base + tid;
                 if (j < slots) {
                     const uint32_t e = s.expand[j / a.gk];
@@ -509,37 +587,37 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
                         }
                     }
                 }
-                __syncthreads();
-                if (s.ctr[1] + kThreads > kBuf) {
-                    merge_buffer(a, s);
+                wsync<W>();
+                if (s.ctr[1] + W > kBuf) {
+                    merge_buffer<W>(a, s);
                     thr = tail_key(a, s);
                 }
             }
-            merge_buffer(a, s);
+            merge_buffer<W>(a, s);
         }
         // ------------------------------------------------ fallback scan
-        __syncthreads();
+        wsync<W>();
         if (s.ctr[0] < a.k_return) {
             uint64_t thr = tail_key(a, s);
-            for (uint32_t base = 0; base < a.n; base += kThreads) {
+            for (uint32_t base = 0; base < a.n; base += W) {
                 const uint32_t id = base + tid;
                 if (id < a.n) {
                     mark_visited(a, slot, s, id);
                     const uint64_t key = make_key(qdist(a, s, id), id);
                     if (key < thr) push_buf(s, key);
                 }
-                __syncthreads();
-                if (s.ctr[1] + kThreads > kBuf) {
-                    merge_buffer(a, s);
+                wsync<W>();
+                if (s.ctr[1] + W > kBuf) {
+                    merge_buffer<W>(a, s);
                     thr = tail_key(a, s);
                 }
             }
-            merge_buffer(a, s);
+            merge_buffer<W>(a, s);
         }
-        __syncthreads();
+        wsync<W>();
         // ------------------------------------------------ output + cleanup
         const uint32_t fin = s.ctr[0];
-        for (uint32_t j = tid; j < a.k_return; j += kThreads)
+        for (uint32_t j = tid; j < a.k_return; j += W)
             a.out_keys[size_t(qi) * a.k_return + j] = j < fin ? s.pool[j] : kEmptyKey;
         const uint32_t nv = s.ctr[2];
         if (tid == 0) {
@@ -551,14 +629,14 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
         }
         uint32_t* bm = a.bitmap + size_t(slot) * a.words;
         if (nv <= a.vcap) {
-            for (uint32_t j = tid; j < nv; j += kThreads) {
+            for (uint32_t j = tid; j < nv; j += W) {
                 const uint32_t id = a.vlist[size_t(slot) * a.vcap + j];
                 bm[id >> 5] = 0;
             }
         } else {
-            for (uint32_t j = tid; j < a.words; j += kThreads) bm[j] = 0;
+            for (uint32_t j = tid; j < a.words; j += W) bm[j] = 0;
         }
-        __syncthreads();
+        wsync<W>();
     }
 }
 
@@ -600,23 +678,25 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
     const uint32_t seed_cap = next_pow2(uint32_t(std::max<uint64_t>(seed_bound, 1)));
     const uint32_t P = p->pool_size;
     const uint32_t hcap = (n_node + 1) * (max_depth + 1) + 1;
-    const size_t heap_bytes = size_t(nt) * hcap * sizeof(HeapEnt);
+    const size_t heap_bytes = size_t(std::min(nt, 32u)) * hcap * sizeof(HeapEnt);  // one heap per producer lane
     const bool heap_smem = heap_bytes <= kHeapSmem;
     const size_t smem = (heap_smem ? heap_bytes : 0) + size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kBuf) * 8 +
-                        size_t(base->ld) * 4 + size_t(P) * 4 + 128 + (kHist + 8) * 4 + size_t(P) * 2 + 16 + base->ld8;
+                        size_t(base->ld) * 4 + size_t(P) * 4 + 128 + (kHist + 8) * 4 + 16 + size_t(P) * 2 + 16 +
+                        base->ld8;
     if (smem > size_t(max_smem_optin()))
         throw_invalid("search: pool_size/seed budget exceeds on-chip capacity");
-    CK(cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const auto kern = p->random_init ? search_kernel<false> : search_kernel<true>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_kernel, kThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
     const uint32_t slots = std::min<uint32_t>(nq, uint32_t(num_sms()) * std::max(per_sm, 1));
     const uint32_t words = (base->n + 31) / 32;
     const uint64_t vbound = seed_bound + uint64_t(p->iters) * P * sr->gk;
     const uint32_t vcap = uint32_t(std::min<uint64_t>(vbound, base->n));
     DevBuf<uint32_t> bitmap(size_t(slots) * words), vlist(size_t(slots) * std::max(vcap, 1u));
     bitmap.zero();
-    DevBuf<HeapEnt> heaps(heap_smem ? 0 : size_t(slots) * nt * hcap);
-    DevBuf<uint2> leaves(std::max<size_t>(size_t(slots) * nt * n_node, 1));
+    DevBuf<HeapEnt> heaps(heap_smem || p->random_init ? 0 : size_t(slots) * 32 * hcap);
+    DevBuf<uint2> leaves(std::max<size_t>(size_t(slots) * 2 * nt * n_node, 1));
     DevBuf<uint64_t> mt(p->random_init ? size_t(slots) * 312 : 1);
     DevBuf<uint64_t> keys(size_t(nq) * p->k_return), st(size_t(nq) * 4);
     const bool u8 = base->u8 && qds->u8 && base->ld8 == qds->ld8;
@@ -625,7 +705,8 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
                  p->random_seed_count, p->seed, seed_cap, bitmap.p, words, vlist.p, vcap, heaps.p, hcap,
                  leaves.p, mt.p, keys.p, st.p, u8 ? base->data8.p : nullptr, u8 ? base->norms8.p : nullptr,
                  base->ld8, u8 ? qds->data8.p : nullptr, u8 ? qds->norms8.p : nullptr};
-    LAUNCH(search_kernel, slots, kThreads, smem, a);
+    if (p->random_init) LAUNCH(search_kernel<false>, slots, kThreads, smem, a);
+    else LAUNCH(search_kernel<true>, slots, kThreads, smem, a);
     const size_t cnt = size_t(nq) * p->k_return;
     DevBuf<uint32_t> di(cnt);
     DevBuf<float> dd(cnt);
