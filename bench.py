@@ -219,6 +219,15 @@ METRIC = "kNN-graph build s at graph acc 0.9; search queries/s at recall@100 0.9
 # ---------------------------------------------------------------- GPU arm
 
 _PINNED_OUT = {}
+REF_ITERS = 4  # SearchParams::iters default (search.hpp:17), fixed across recall_curve's sweep
+
+
+def measured_hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return 6650.0
 
 
 def timed_search(searcher, qs, p, ev, reps=3):
@@ -352,7 +361,7 @@ def run_gpu(args, cfg, ws, rank, local):
     # search sweep (secondary metric): smallest pool reaching recall@k_return >= 0.9
     searcher = A.GraphSearcher(vs, forest, graph)
     sweep = []
-    chosen = None
+    chosen = fastest = None
     kr = cfg["k_return"]
     # the reference's search knobs (search.hpp:13-21): pool P (>= k_return), seeds kept E <= P,
     # expansion rounds I; the fastest point reaching recall@k_return >= 0.9 is the headline
@@ -364,18 +373,31 @@ def run_gpu(args, cfg, ws, rank, local):
         row = {"pool": P, "expansion": E, "iters": it, "recall": round(rec, 4),
                "qps": round(cfg["n_queries"] / dt, 1), "dist_comps_per_query": float(r.stats[:, 0].mean())}
         sweep.append(row)
-        if rec >= 0.9 and (chosen is None or row["qps"] > chosen["qps"]):
-            chosen = row
+        if rec >= 0.9 and it == REF_ITERS and chosen is None:
+            chosen = row  # recall_curve's definition: first sweep point (P, then E ascending) at the default I
+        if rec >= 0.9 and (fastest is None or row["qps"] > fastest["qps"]):
+            fastest = row
 
     search_kernels = None
-    if chosen:  # device time of the chosen point's kernels (profiler on, outside the timed sweep)
+    search_roofline = None
+    for row in (fastest, chosen):  # kernel-only time of the reported points (profiler on, outside the sweep)
+        if not row:
+            continue
         A.profile_reset()
         A.profile_enable(True)
-        searcher.search_batch(qs, A.SearchParams(k_return=kr, pool_size=chosen["pool"],
-                                                 expansion=chosen["expansion"], iters=chosen["iters"]))
+        rr = searcher.search_batch(qs, A.SearchParams(k_return=kr, pool_size=row["pool"],
+                                                      expansion=row["expansion"], iters=row["iters"]))
         A.profile_enable(False)
         search_kernels = {k2: round(v2[1], 3) for k2, v2 in A.profile_report().items()}
-        chosen["kernel_qps"] = round(cfg["n_queries"] / (sum(search_kernels.values()) / 1e3), 1)
+        row["kernel_qps"] = round(cfg["n_queries"] / (sum(search_kernels.values()) / 1e3), 1)
+        # HBM-gather model: every distance gathers one base row + its id, every
+        # expanded point reads its graph row
+        rb = vs.info()["row_bytes"]
+        alg = float(rr.stats[:, 0].sum()) * (rb + 4) + float(rr.stats[:, 2].sum()) * graph.ids.shape[1] * 4
+        kms = max(v for k2, v in search_kernels.items() if k2.startswith("search_kernel"))
+        pk = measured_hbm_peak()
+        row["roofline"] = {"bound": "hbm", "achieved": alg / (kms / 1e3) / 1e9, "peak": pk, "unit": "GB/s",
+                           "frac": alg / (kms / 1e3) / 1e9 / pk, "algorithmic_bytes": alg, "kernel_ms": kms}
 
     # e2e through the C-ABI from pinned host memory
     pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
@@ -470,7 +492,11 @@ def run_gpu(args, cfg, ws, rank, local):
         "clocks": clocks,
         "search_qps_at_recall_0.9": chosen["qps"] if chosen else None,
         "search_kernels_ms": search_kernels,
-        "search": {"k_return": kr, "n_queries": cfg["n_queries"], "chosen": chosen, "sweep": sweep},
+        "search": {"k_return": kr, "n_queries": cfg["n_queries"],
+                   "definition": f"recall_curve sweep (P, then E ascending) at the default I={REF_ITERS}; "
+                                 "first point with recall@k_return >= 0.9; Q / device time of the batch "
+                                 "through the public API (results D2H to pinned memory included)",
+                   "chosen": chosen, "fastest_any_iters": fastest, "sweep": sweep},
         "accuracy": {"per_iteration": [round(a, 4) for a in accs], "final_sample": round(final_acc, 4),
                      "dist_comps": comps},
         "aux_seconds": {"forest": forest_s, "gt_rows": gt_rows_s, "gt_queries": gt_q_s, "data_gen_host": gen_s,
@@ -578,7 +604,7 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
 
     # search: every rank holds the full index and answers its query shard
     searcher = A.GraphSearcher(vs, forest, graph)
-    sweep, chosen = [], None
+    sweep, chosen, fastest = [], None, None
     grid = [(P, E, it) for P in cfg["sweep"][:2] for E in (8, 16, 32, 64, P) for it in (1, 2, 4) if E <= P]
     for P, E, it in grid:
         p = A.SearchParams(k_return=kr, pool_size=P, expansion=E, iters=it)
@@ -590,8 +616,10 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
         row = {"pool": P, "expansion": E, "iters": it, "recall": round(rec, 4),
                "qps": round(cfg["n_queries"] / dt, 1)}
         sweep.append(row)
-        if rec >= 0.9 and (chosen is None or row["qps"] > chosen["qps"]):
-            chosen = row
+        if rec >= 0.9 and it == REF_ITERS and chosen is None:
+            chosen = row  # recall_curve's definition: first sweep point (P, then E ascending) at the default I
+        if rec >= 0.9 and (fastest is None or row["qps"] > fastest["qps"]):
+            fastest = row
 
     # e2e: host dataset in, own graph rows out, per rank
     pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
@@ -634,7 +662,8 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
         "cpu_baseline": None,
         "clocks": clk.summary(),
         "search_qps_at_recall_0.9": chosen["qps"] if chosen else None,
-        "search": {"k_return": kr, "n_queries": cfg["n_queries"], "chosen": chosen, "sweep": sweep},
+        "search": {"k_return": kr, "n_queries": cfg["n_queries"], "chosen": chosen, "fastest_any_iters": fastest,
+                   "sweep": sweep},
         "accuracy": {"per_iteration": [round(a, 4) for a in accs], "final_sample": round(final_acc, 4),
                      "dist_comps": comps},
         "aux_seconds": {"forest": forest_s},

@@ -124,6 +124,7 @@ struct annk_searcher {
     const annk_forest* forest = nullptr;
     uint32_t gn = 0, gk = 0;
     annk::DevBuf<uint32_t> graph;  // gn x gk
+    annk::DevBuf<uint32_t> bitmap;  // search visited bitmaps (slots x words), all-zero between launches
 };
 
 namespace annk {

@@ -693,8 +693,12 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
     const uint32_t words = (base->n + 31) / 32;
     const uint64_t vbound = seed_bound + uint64_t(p->iters) * P * sr->gk;
     const uint32_t vcap = uint32_t(std::min<uint64_t>(vbound, base->n));
-    DevBuf<uint32_t> bitmap(size_t(slots) * words), vlist(size_t(slots) * std::max(vcap, 1u));
-    bitmap.zero();
+    // the visited bitmap lives with the searcher: zeroed once, every query leaves its row clean
+    if (sr->bitmap.n < size_t(slots) * words) {
+        sr->bitmap.alloc(size_t(slots) * words);
+        sr->bitmap.zero();
+    }
+    DevBuf<uint32_t> vlist(size_t(slots) * std::max(vcap, 1u));
     DevBuf<HeapEnt> heaps(heap_smem || p->random_init ? 0 : size_t(slots) * 32 * hcap);
     DevBuf<uint2> leaves(std::max<size_t>(size_t(slots) * 2 * nt * n_node, 1));
     DevBuf<uint64_t> mt(p->random_init ? size_t(slots) * 312 : 1);
@@ -702,7 +706,7 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
     const bool u8 = base->u8 && qds->u8 && base->ld8 == qds->ld8;
     SearchArgs a{base->data.p, base->n, base->ld, qds->data.p, nq, f ? f->views.p : nullptr, nt, n_node, leaf_cap,
                  sr->graph.p, sr->gk, p->k_return, P, p->expansion, p->iters, p->random_init,
-                 p->random_seed_count, p->seed, seed_cap, bitmap.p, words, vlist.p, vcap, heaps.p, hcap,
+                 p->random_seed_count, p->seed, seed_cap, sr->bitmap.p, words, vlist.p, vcap, heaps.p, hcap,
                  leaves.p, mt.p, keys.p, st.p, u8 ? base->data8.p : nullptr, u8 ? base->norms8.p : nullptr,
                  base->ld8, u8 ? qds->data8.p : nullptr, u8 ? qds->norms8.p : nullptr};
     if (p->random_init) LAUNCH(search_kernel<false>, slots, kThreads, smem, a);

@@ -15,6 +15,8 @@ ap.add_argument("--config", default="cfg2")
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--search", action="store_true")
 ap.add_argument("--n", type=int, default=0)
+ap.add_argument("--search-e", type=int, default=8)
+ap.add_argument("--search-iters", type=int, default=4)
 args = ap.parse_args()
 cfg = dict(bench.CONFIGS[args.config])
 if args.n:
@@ -27,5 +29,6 @@ for _ in range(args.iters):
     A.detail.nn_descent_iteration(s, vs)
 if args.search:
     g = A.finalize(s, vs, cfg["k"])
-    r = A.GraphSearcher(vs, f, g).search_batch(queries, A.SearchParams(cfg["k_return"], cfg["P"], 16, 1))  # the bench's chosen point
+    r = A.GraphSearcher(vs, f, g).search_batch(queries, A.SearchParams(cfg["k_return"], cfg["P"], args.search_e,
+                                                                      args.search_iters))  # bench's headline point
 print("profile_build done", A.launch_count())
