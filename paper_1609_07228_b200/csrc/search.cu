@@ -24,7 +24,8 @@ namespace annk {
 namespace {
 
 constexpr uint32_t kThreads = 256;
-constexpr uint32_t kBuf = 1024;
+constexpr uint32_t kBuf = 2048;
+constexpr uint32_t kU = 4;  // expansion slots per worker thread per batch (atomics in flight)
 constexpr size_t kHeapSmem = 12288;  // BBF heaps in shared memory up to this size
 
 struct HeapEnt {
@@ -86,7 +87,11 @@ struct Smem {
     uint32_t* hist;     // kHist radix-select bins + 8 scalars
     HeapEnt* heap;      // min(nt, 32) x hcap when the heaps fit kHeapSmem
     uint32_t* lcnt;     // leaves emitted per leaf-range buffer
+    uint32_t* rbloom;   // kBloomBits-bit filter of the reserve's ids
 };
+
+constexpr uint32_t kBloomBits = 4096;
+__device__ __forceinline__ uint32_t bloom_bit(uint32_t id) { return (id * 2654435761u) >> 20; }
 
 constexpr uint32_t kHist = 256;
 constexpr uint32_t kConsumed = 0xffffffffu;  // reserve entry already offered (low word of an id-major key)
@@ -426,7 +431,7 @@ __device__ void bbf_producer(const SearchArgs& a, Smem& s) {
 }
 
 template <bool kTree>
-__global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
+__global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
     constexpr uint32_t W = kTree ? kThreads - 32 : kThreads;  // worker threads
     extern __shared__ __align__(16) unsigned char raw[];
     Smem s;
@@ -444,6 +449,7 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
         s.ctr = reinterpret_cast<uint32_t*>(p); p += 64;
         s.hist = reinterpret_cast<uint32_t*>(p); p += (kHist + 8) * 4;
         s.lcnt = reinterpret_cast<uint32_t*>(p); p += 16;
+        s.rbloom = reinterpret_cast<uint32_t*>(p); p += kBloomBits / 8;
         s.checked = p; p += a.P;
         s.tmpc = p;
     }
@@ -540,6 +546,13 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
         }
         wsync<W>();
         if (nr > 1) block_sort_keys<W>(s.seeds, nr);
+        for (uint32_t j = tid; j < kBloomBits / 32; j += W) s.rbloom[j] = 0;
+        wsync<W>();
+        for (uint32_t j = tid; j < nr; j += W) {
+            const uint32_t h = bloom_bit(uint32_t(s.seeds[j] >> 32));
+            atomicOr(&s.rbloom[h >> 5], 1u << (h & 31));
+        }
+        wsync<W>();
         // ------------------------------------------------ expansion rounds
         for (uint32_t it = 0; it < a.iters; ++it) {
             const uint32_t pss = s.ctr[0];
@@ -561,34 +574,53 @@ __global__ void __launch_bounds__(kThreads) search_kernel(SearchArgs a) {
             if (tid == 0) s.ctr[7] += ne;
             uint64_t thr = tail_key(a, s);
             const uint32_t slots = ne * a.gk;
-            for (uint32_t base = 0; base < slots; base += W) {
-                const uint32_t j = base + tid;
-                if (j < slots) {
-                    const uint32_t e = s.expand[j / a.gk];
-                    DCHK(e < a.n);
-                    const uint32_t nb = a.graph[size_t(e) * a.gk + (j % a.gk)];
-                    if (mark_visited(a, slot, s, nb)) {
-                        const uint64_t key = make_key(qdist(a, s, nb), nb);
+            uint32_t* bm = a.bitmap + size_t(slot) * a.words;
+            for (uint32_t base = 0; base < slots; base += W * kU) {
+                // kU slots per thread: graph reads, then the visited atomics all in flight
+                uint32_t nb[kU], old[kU];
+#pragma unroll
+                for (uint32_t u = 0; u < kU; ++u) {
+                    const uint32_t j = base + u * W + tid;
+                    nb[u] = kInvalidId;
+                    if (j < slots) {
+                        const uint32_t e = s.expand[j / a.gk];
+                        DCHK(e < a.n);
+                        nb[u] = a.graph[size_t(e) * a.gk + (j % a.gk)];
+                    }
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < kU; ++u)
+                    old[u] = nb[u] != kInvalidId ? atomicOr(&bm[nb[u] >> 5], 1u << (nb[u] & 31)) : 0u;
+#pragma unroll
+                for (uint32_t u = 0; u < kU; ++u) {
+                    const uint32_t id = nb[u];
+                    if (id == kInvalidId) continue;
+                    if (!(old[u] & (1u << (id & 31)))) {
+                        const uint32_t v = atomicAdd(&s.ctr[2], 1u);
+                        if (v < a.vcap) a.vlist[size_t(slot) * a.vcap + v] = id;
+                        const uint64_t key = make_key(qdist(a, s, id), id);
                         if (key < thr) push_buf(s, key);
-                    } else if (s.ctr[4]) {
-                        // a reserve seed re-enters with its cached distance (search.cpp:79-82).
-                        // It is offered once: the pool tail never rises, so a key
-                        // the pool rejects (or evicts) can never re-enter it.
-                        const uint32_t nrr = s.ctr[4];
-                        const uint32_t p = lower_bound64(s.seeds, nrr, uint64_t(nb) << 32);
-                        const uint64_t e = p < nrr ? s.seeds[p] : 0;
-                        if (p < nrr && uint32_t(e >> 32) == nb && uint32_t(e) != kConsumed) {
-                            const uint64_t key = (uint64_t(uint32_t(e)) << 32) | nb;
-                            if (key < thr) {
-                                const unsigned long long mark = (uint64_t(nb) << 32) | kConsumed;
-                                const uint64_t old = atomicExch(reinterpret_cast<unsigned long long*>(&s.seeds[p]), mark);
-                                if (uint32_t(old) != kConsumed) push_buf(s, key);
-                            }
+                        continue;
+                    }
+                    const uint32_t h = bloom_bit(id);
+                    if (!s.ctr[4] || !((s.rbloom[h >> 5] >> (h & 31)) & 1u)) continue;
+                    // a reserve seed re-enters with its cached distance (search.cpp:79-82).
+                    // It is offered once: the pool tail never rises, so a key
+                    // the pool rejects (or evicts) can never re-enter it.
+                    const uint32_t nrr = s.ctr[4];
+                    const uint32_t p = lower_bound64(s.seeds, nrr, uint64_t(id) << 32);
+                    const uint64_t e = p < nrr ? s.seeds[p] : 0;
+                    if (p < nrr && uint32_t(e >> 32) == id && uint32_t(e) != kConsumed) {
+                        const uint64_t key = (uint64_t(uint32_t(e)) << 32) | id;
+                        if (key < thr) {
+                            const unsigned long long mark = (uint64_t(id) << 32) | kConsumed;
+                            const uint64_t prev = atomicExch(reinterpret_cast<unsigned long long*>(&s.seeds[p]), mark);
+                            if (uint32_t(prev) != kConsumed) push_buf(s, key);
                         }
                     }
                 }
                 wsync<W>();
-                if (s.ctr[1] + W > kBuf) {
+                if (s.ctr[1] + W * kU > kBuf) {
                     merge_buffer<W>(a, s);
                     thr = tail_key(a, s);
                 }
@@ -681,8 +713,8 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
     const size_t heap_bytes = size_t(std::min(nt, 32u)) * hcap * sizeof(HeapEnt);  // one heap per producer lane
     const bool heap_smem = heap_bytes <= kHeapSmem;
     const size_t smem = (heap_smem ? heap_bytes : 0) + size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kBuf) * 8 +
-                        size_t(base->ld) * 4 + size_t(P) * 4 + 128 + (kHist + 8) * 4 + 16 + size_t(P) * 2 + 16 +
-                        base->ld8;
+                        size_t(base->ld) * 4 + size_t(P) * 4 + 128 + (kHist + 8) * 4 + 16 + kBloomBits / 8 +
+                        size_t(P) * 2 + 16 + base->ld8;
     if (smem > size_t(max_smem_optin()))
         throw_invalid("search: pool_size/seed budget exceeds on-chip capacity");
     const auto kern = p->random_init ? search_kernel<false> : search_kernel<true>;
