@@ -68,12 +68,13 @@ struct SearchArgs {
     uint32_t ld8;
     const uint8_t* q8;
     const int32_t* qnorms8;
+    uint32_t gk_magic;  // floor(2^32 / gk): slot -> (expanded point, column) without a hardware divide
 };
 
 struct Smem {
     uint64_t* pool;     // P
     uint8_t* checked;   // P
-    uint64_t* seeds;    // seed_cap (later: reserve, swapped keys)
+    uint64_t* seeds;    // seed_cap
     uint64_t* buf;      // kBuf
     uint64_t* tmp;      // P
     uint8_t* tmpc;      // P
@@ -87,11 +88,12 @@ struct Smem {
     uint32_t* hist;     // kHist radix-select bins + 8 scalars
     HeapEnt* heap;      // min(nt, 32) x hcap when the heaps fit kHeapSmem
     uint32_t* lcnt;     // leaves emitted per leaf-range buffer
-    uint32_t* rbloom;   // kBloomBits-bit filter of the reserve's ids
+    uint64_t* rhash;    // 2 x seed_cap: the reserve, open addressing on id, entries (id << 32) | dist bits
 };
 
-constexpr uint32_t kBloomBits = 4096;
-__device__ __forceinline__ uint32_t bloom_bit(uint32_t id) { return (id * 2654435761u) >> 20; }
+__device__ __forceinline__ uint32_t rhash_slot(uint32_t id, uint32_t rbits) {
+    return (id * 2654435761u) >> (32 - rbits);
+}
 
 constexpr uint32_t kHist = 256;
 constexpr uint32_t kConsumed = 0xffffffffu;  // reserve entry already offered (low word of an id-major key)
@@ -444,12 +446,12 @@ __global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
         s.tmp = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
         s.seeds = reinterpret_cast<uint64_t*>(p); p += size_t(a.seed_cap) * 8;
         s.buf = reinterpret_cast<uint64_t*>(p); p += size_t(kBuf) * 8;
+        s.rhash = reinterpret_cast<uint64_t*>(p); p += size_t(a.seed_cap) * 16;  // 8-byte entries: before expand
         s.expand = reinterpret_cast<uint32_t*>(p); p += size_t(a.P) * 4;
         s.scan = reinterpret_cast<uint32_t*>(p); p += 64;
         s.ctr = reinterpret_cast<uint32_t*>(p); p += 64;
         s.hist = reinterpret_cast<uint32_t*>(p); p += (kHist + 8) * 4;
         s.lcnt = reinterpret_cast<uint32_t*>(p); p += 16;
-        s.rbloom = reinterpret_cast<uint32_t*>(p); p += kBloomBits / 8;
         s.checked = p; p += a.P;
         s.tmpc = p;
     }
@@ -520,37 +522,26 @@ __global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
         }
         wsync<W>();
         const uint32_t ns = s.ctr[3];
-        const uint32_t m = next_pow2(max(ns, 1u));
         block_sort_keys<W>(s.seeds, ns);
         const uint32_t ps = min(ns, a.E);
         for (uint32_t j = tid; j < ps; j += W) {
             s.pool[j] = s.seeds[j];
             s.checked[j] = 0;
         }
-        // reserve: seeds ranked past E, re-keyed by id for lookup
+        // reserve: seeds ranked past E, in a hash table on id (load <= 1/2)
         const uint32_t nr = ns - ps;
-        for (uint32_t base = 0; base < m; base += W) {  // uniform trip count: barriers inside
-            const uint32_t j = base + tid;
-            uint64_t v = kEmptyKey;
-            if (j < nr) {
-                const uint64_t k = s.seeds[ps + j];
-                v = (uint64_t(key_id(k)) << 32) | uint32_t(k >> 32);
-            }
-            wsync<W>();
-            if (j < m) s.seeds[j] = v;
-            wsync<W>();
-        }
-        if (tid == 0) {
-            s.ctr[0] = ps;
-            s.ctr[4] = nr;
-        }
-        wsync<W>();
-        if (nr > 1) block_sort_keys<W>(s.seeds, nr);
-        for (uint32_t j = tid; j < kBloomBits / 32; j += W) s.rbloom[j] = 0;
+        const uint32_t rbits = 32 - __clz(max(2 * nr, 2u) - 1);  // table of 2^rbits >= 2 nr slots
+        const uint32_t rmask = (1u << rbits) - 1;
+        for (uint32_t j = tid; j <= rmask; j += W) s.rhash[j] = kEmptyKey;
+        if (tid == 0) s.ctr[0] = ps;
         wsync<W>();
         for (uint32_t j = tid; j < nr; j += W) {
-            const uint32_t h = bloom_bit(uint32_t(s.seeds[j] >> 32));
-            atomicOr(&s.rbloom[h >> 5], 1u << (h & 31));
+            const uint64_t k = s.seeds[ps + j];
+            const uint32_t id = key_id(k);
+            const unsigned long long v = (uint64_t(id) << 32) | uint32_t(k >> 32);
+            uint32_t h = rhash_slot(id, rbits);
+            while (atomicCAS(reinterpret_cast<unsigned long long*>(&s.rhash[h]), kEmptyKey, v) != kEmptyKey)
+                h = (h + 1) & rmask;
         }
         wsync<W>();
         // ------------------------------------------------ expansion rounds
@@ -583,9 +574,11 @@ __global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
                     const uint32_t j = base + u * W + tid;
                     nb[u] = kInvalidId;
                     if (j < slots) {
-                        const uint32_t e = s.expand[j / a.gk];
+                        uint32_t q = __umulhi(j, a.gk_magic), c = j - q * a.gk;
+                        if (c >= a.gk) { ++q; c -= a.gk; }
+                        const uint32_t e = s.expand[q];
                         DCHK(e < a.n);
-                        nb[u] = a.graph[size_t(e) * a.gk + (j % a.gk)];
+                        nb[u] = a.graph[size_t(e) * a.gk + c];
                     }
                 }
 #pragma unroll
@@ -602,21 +595,23 @@ __global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
                         if (key < thr) push_buf(s, key);
                         continue;
                     }
-                    const uint32_t h = bloom_bit(id);
-                    if (!s.ctr[4] || !((s.rbloom[h >> 5] >> (h & 31)) & 1u)) continue;
+                    if (nr == 0) continue;
                     // a reserve seed re-enters with its cached distance (search.cpp:79-82).
                     // It is offered once: the pool tail never rises, so a key
                     // the pool rejects (or evicts) can never re-enter it.
-                    const uint32_t nrr = s.ctr[4];
-                    const uint32_t p = lower_bound64(s.seeds, nrr, uint64_t(id) << 32);
-                    const uint64_t e = p < nrr ? s.seeds[p] : 0;
-                    if (p < nrr && uint32_t(e >> 32) == id && uint32_t(e) != kConsumed) {
-                        const uint64_t key = (uint64_t(uint32_t(e)) << 32) | id;
-                        if (key < thr) {
-                            const unsigned long long mark = (uint64_t(id) << 32) | kConsumed;
-                            const uint64_t prev = atomicExch(reinterpret_cast<unsigned long long*>(&s.seeds[p]), mark);
-                            if (uint32_t(prev) != kConsumed) push_buf(s, key);
+                    for (uint32_t h = rhash_slot(id, rbits);; h = (h + 1) & rmask) {
+                        const uint64_t e = s.rhash[h];
+                        if (e == kEmptyKey) break;
+                        if (uint32_t(e >> 32) != id) continue;
+                        if (uint32_t(e) != kConsumed) {
+                            const uint64_t key = (uint64_t(uint32_t(e)) << 32) | id;
+                            if (key < thr) {
+                                const unsigned long long mark = (uint64_t(id) << 32) | kConsumed;
+                                const uint64_t prev = atomicExch(reinterpret_cast<unsigned long long*>(&s.rhash[h]), mark);
+                                if (uint32_t(prev) != kConsumed) push_buf(s, key);
+                            }
                         }
+                        break;
                     }
                 }
                 wsync<W>();
@@ -713,7 +708,7 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
     const size_t heap_bytes = size_t(std::min(nt, 32u)) * hcap * sizeof(HeapEnt);  // one heap per producer lane
     const bool heap_smem = heap_bytes <= kHeapSmem;
     const size_t smem = (heap_smem ? heap_bytes : 0) + size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kBuf) * 8 +
-                        size_t(base->ld) * 4 + size_t(P) * 4 + 128 + (kHist + 8) * 4 + 16 + kBloomBits / 8 +
+                        size_t(base->ld) * 4 + size_t(P) * 4 + 128 + (kHist + 8) * 4 + 16 + size_t(seed_cap) * 16 +
                         size_t(P) * 2 + 16 + base->ld8;
     if (smem > size_t(max_smem_optin()))
         throw_invalid("search: pool_size/seed budget exceeds on-chip capacity");
@@ -740,7 +735,8 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
                  sr->graph.p, sr->gk, p->k_return, P, p->expansion, p->iters, p->random_init,
                  p->random_seed_count, p->seed, seed_cap, sr->bitmap.p, words, vlist.p, vcap, heaps.p, hcap,
                  leaves.p, mt.p, keys.p, st.p, u8 ? base->data8.p : nullptr, u8 ? base->norms8.p : nullptr,
-                 base->ld8, u8 ? qds->data8.p : nullptr, u8 ? qds->norms8.p : nullptr};
+                 base->ld8, u8 ? qds->data8.p : nullptr, u8 ? qds->norms8.p : nullptr,
+                 sr->gk > 1 ? uint32_t((uint64_t(1) << 32) / sr->gk) : 0xffffffffu};
     if (p->random_init) LAUNCH(search_kernel<false>, slots, kThreads, smem, a);
     else LAUNCH(search_kernel<true>, slots, kThreads, smem, a);
     const size_t cnt = size_t(nq) * p->k_return;
