@@ -230,6 +230,16 @@ def measured_hbm_peak():
         return 6650.0
 
 
+def ncu_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh).get(config, {}).get(kernel)
+            return tr["dram_bytes_per_launch"] if tr else None
+    except Exception:
+        return None
+
+
 def timed_search(searcher, qs, p, ev, reps=3):
     """One warm call, then the median of `reps` timed calls of the whole batch
     through the public API (upload-free: queries are a resident VectorSet;
@@ -396,8 +406,11 @@ def run_gpu(args, cfg, ws, rank, local):
         alg = float(rr.stats[:, 0].sum()) * (rb + 4) + float(rr.stats[:, 2].sum()) * graph.ids.shape[1] * 4
         kms = max(v for k2, v in search_kernels.items() if k2.startswith("search_kernel"))
         pk = measured_hbm_peak()
+        tkey = "search_kernel<true>" + ("" if (row["expansion"], row["iters"]) == (8, 4) else
+                                        f"@E{row['expansion']}I{row['iters']}")
         row["roofline"] = {"bound": "hbm", "achieved": alg / (kms / 1e3) / 1e9, "peak": pk, "unit": "GB/s",
-                           "frac": alg / (kms / 1e3) / 1e9 / pk, "algorithmic_bytes": alg, "kernel_ms": kms}
+                           "frac": alg / (kms / 1e3) / 1e9 / pk, "algorithmic_bytes": alg, "kernel_ms": kms,
+                           "traffic": ncu_traffic(args.config, tkey)}
 
     # e2e through the C-ABI from pinned host memory
     pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
