@@ -203,7 +203,7 @@ def run_reference(args, cfg, ws, rank):
               f"{cfg['leaf']}) on the first {cfg['ref_points']} of {cfg['n']} points, {os.cpu_count()} workers, "
               f"seconds scaled x{cfg['n'] / cfg['ref_points']:.2f} to N")
     line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.config, "n": cfg["n"], "dim": cfg["dim"], "trees": cfg["trees"],
                        "leaf_cap": cfg["leaf"], "k": cfg["k"], "pool_cap": cfg["P"], "sample_cap": cfg["S"],
@@ -490,7 +490,7 @@ def run_gpu(args, cfg, ws, rank, local):
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "u8" if dsinfo["u8"] else "f32", "data": "synthetic",
         "config": {"workload": args.config, "n": n, "dim": dim, "trees": cfg["trees"], "leaf_cap": cfg["leaf"],
                    "k": k, "pool_cap": cfg["P"], "sample_cap": cfg["S"], "conquer_depth": cfg["dep"],
