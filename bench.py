@@ -11,9 +11,12 @@ Gaussian mixture (1000 centers), 8 trees leaf 8, K=100, P(L)=100, S=20,
                reference's own StopWatch boundary, graph_build.cpp:421-450; the
                forest is built once beforehand, as `annkit build-trees` does).
                Inputs resident in HBM; dataset 512 MB > L2 (126 MB).
-  e2e        = the same build through the C-ABI from pinned host memory:
-               H2D of the dataset + forest + init + refine + finalize + D2H of
-               the graph (ids + dists), every step.
+  e2e        = the same build through the C-ABI from pinned host memory, at
+               the same boundary: H2D of the dataset and of the prebuilt forest
+               (host arrays, as build_graph receives its forest) + init + refine
+               + finalize + D2H of the graph (ids + dists), every step.
+               `e2e_with_forest_build` also builds the forest on the device
+               inside the timed region.
   search_qps = queries/s of the batched search at the smallest swept pool
                size reaching recall@100 >= 0.9 (secondary line item).
 
@@ -222,6 +225,19 @@ _PINNED_OUT = {}
 REF_ITERS = 4  # SearchParams::iters default (search.hpp:17), fixed across recall_curve's sweep
 
 
+def pinned_forest(A, forest):
+    """The device forest exported once to pinned host arrays in annk_forest_import's layout."""
+    import torch
+    trees = forest.trees
+    tdt = {np.uint32: torch.int32, np.float32: torch.float32, np.uint8: torch.uint8}
+    tot = sum(len(t.split_dim) for t in trees)
+    shapes = {"split_dim": (tot, np.uint32), "split_val": (tot, np.float32), "left": (tot, np.uint32),
+              "right": (tot, np.uint32), "depth": (tot, np.uint32), "even": (tot, np.uint8),
+              "point_index": (len(trees) * forest.n, np.uint32)}
+    out = {key: torch.empty(m, dtype=tdt[dt], pin_memory=True).numpy().view(dt) for key, (m, dt) in shapes.items()}
+    return A.KdForest.pack_trees(trees, out=out)
+
+
 def measured_hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -418,22 +434,32 @@ def run_gpu(args, cfg, ws, rank, local):
     host = pinned.numpy()
     out_ids = torch.empty((n, k), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     out_d = torch.empty((n, k), dtype=torch.float32, pin_memory=True).numpy()
-    e2e_times = []
-    for i in range(max(1, args.e2e_steps) + 1):
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        v2 = A.VectorSet(host)
-        f2 = A.build_forest(v2, cfg["trees"], cfg["leaf"], SEED)
-        s2 = A.init_graph(v2, f2, k, cfg["dep"], cfg["P"], cfg["S"], SEED)
-        for _ in range(crossing):
-            A.detail.nn_descent_iteration(s2, v2)
-        g2 = A.finalize(s2, v2, k, out_ids=out_ids, out_dists=out_d)
-        t2 = time.perf_counter()
-        if i > 0:  # first is warm-up
-            e2e_times.append(t2 - t1)
-        del v2, f2, s2
-    assert np.array_equal(g2.ids, graph.ids), "e2e graph differs from the device-resident build"
-    e2e_s = max_over_ranks(ws, statistics.mean(e2e_times))
+    packed = pinned_forest(A, forest)  # the prebuilt forest as host arrays (outside the timed region)
+    f_bytes = sum(int(v.nbytes) for v in packed.values())
+
+    def e2e_run(with_forest_build):
+        times = []
+        for i in range(max(1, args.e2e_steps) + 1):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            v2 = A.VectorSet(host)
+            if with_forest_build:
+                f2 = A.build_forest(v2, cfg["trees"], cfg["leaf"], SEED)
+            else:
+                f2 = A.KdForest.import_packed(n, dim, cfg["leaf"], SEED, packed)
+            s2 = A.init_graph(v2, f2, k, cfg["dep"], cfg["P"], cfg["S"], SEED)
+            for _ in range(crossing):
+                A.detail.nn_descent_iteration(s2, v2)
+            g2 = A.finalize(s2, v2, k, out_ids=out_ids, out_dists=out_d)
+            t2 = time.perf_counter()
+            if i > 0:  # first is warm-up
+                times.append(t2 - t1)
+            del v2, f2, s2
+            assert np.array_equal(g2.ids, graph.ids), "e2e graph differs from the device-resident build"
+        return max_over_ranks(ws, statistics.mean(times))
+
+    e2e_s = e2e_run(False)
+    e2e_fb_s = e2e_run(True)
 
     # roofline: the dominant kernel's algorithmic bytes per launch / measured duration
     peaks = {}
@@ -496,9 +522,14 @@ def run_gpu(args, cfg, ws, rank, local):
                    "k": k, "pool_cap": cfg["P"], "sample_cap": cfg["S"], "conquer_depth": cfg["dep"],
                    "iterations_to_acc_0.9": crossing, "accuracy_sample_rows": int(len(rows)),
                    "l2": "inputs larger than L2 (512 MB dataset)", "parallelism": f"replicas x{ws}"},
-        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * dim * 4),
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * dim * 4) + f_bytes,
                 "d2h_bytes_per_step": int(n * k * 8),
-                "includes": "H2D dataset, forest build, init, refine, finalize, D2H graph ids+dists"},
+                "includes": "H2D dataset + H2D prebuilt forest (host arrays; the reference's build_graph is timed "
+                            "with its forest built beforehand), init, refine, finalize, D2H graph ids+dists"},
+        "e2e_with_forest_build": {"value": e2e_fb_s, "unit": "s", "h2d_bytes_per_step": int(n * dim * 4),
+                                  "d2h_bytes_per_step": int(n * k * 8),
+                                  "includes": "H2D dataset, forest build on the device, init, refine, finalize, "
+                                              "D2H graph ids+dists"},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -634,27 +665,37 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
         if rec >= 0.9 and (fastest is None or row["qps"] > fastest["qps"]):
             fastest = row
 
-    # e2e: host dataset in, own graph rows out, per rank
+    # e2e: host dataset (and prebuilt forest) in, own graph rows out, per rank
     pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
     pinned.numpy()[:] = base
     host = pinned.numpy()
-    e2e_times = []
-    for i in range(max(1, args.e2e_steps) + 1):
-        torch.cuda.synchronize()
-        barrier(ws)
-        t1 = time.perf_counter()
-        v2 = A.VectorSet(host)
-        f2 = A.build_forest(v2, cfg["trees"], cfg["leaf"], SEED)
-        e2 = SH.DeviceShard(v2, f2, k, cfg["dep"], cfg["P"], cfg["S"], SEED, lo, hi, buffer_device=bufdev)
-        for _ in range(crossing):
-            SH.nn_descent_round(e2, comm)
-        g2 = e2.finalize()
-        t2 = time.perf_counter()
-        if i > 0:
-            e2e_times.append(t2 - t1)
-        del v2, f2, e2
-    assert np.array_equal(g2.ids, graph.ids[lo:hi]), "e2e graph differs from the device-resident build"
-    e2e_s = max_over_ranks(ws, statistics.mean(e2e_times))
+    packed = pinned_forest(A, forest)
+    f_bytes = sum(int(v.nbytes) for v in packed.values())
+
+    def e2e_run(with_forest_build):
+        times = []
+        for i in range(max(1, args.e2e_steps) + 1):
+            torch.cuda.synchronize()
+            barrier(ws)
+            t1 = time.perf_counter()
+            v2 = A.VectorSet(host)
+            if with_forest_build:
+                f2 = A.build_forest(v2, cfg["trees"], cfg["leaf"], SEED)
+            else:
+                f2 = A.KdForest.import_packed(n, dim, cfg["leaf"], SEED, packed)
+            e2 = SH.DeviceShard(v2, f2, k, cfg["dep"], cfg["P"], cfg["S"], SEED, lo, hi, buffer_device=bufdev)
+            for _ in range(crossing):
+                SH.nn_descent_round(e2, comm)
+            g2 = e2.finalize()
+            t2 = time.perf_counter()
+            if i > 0:
+                times.append(t2 - t1)
+            del v2, f2, e2
+            assert np.array_equal(g2.ids, graph.ids[lo:hi]), "e2e graph differs from the device-resident build"
+        return max_over_ranks(ws, statistics.mean(times))
+
+    e2e_s = e2e_run(False)
+    e2e_fb_s = e2e_run(True)
 
     dsinfo = vs.info()
     line = {
@@ -667,9 +708,13 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
                    "l2": "inputs larger than L2 (512 MB dataset)",
                    "parallelism": f"point-sharded build x{ws} (NCCL all-gather + all-to-all per round), "
                                   f"query-sharded search"},
-        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(ws * n * dim * 4),
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(ws * (n * dim * 4 + f_bytes)),
                 "d2h_bytes_per_step": int(n * k * 8),
-                "includes": "per rank: H2D dataset, forest build, sharded init + rounds, finalize, D2H own rows"},
+                "includes": "per rank: H2D dataset + prebuilt forest, sharded init + rounds, finalize, D2H own rows"},
+        "e2e_with_forest_build": {"value": e2e_fb_s, "unit": "s", "h2d_bytes_per_step": int(ws * n * dim * 4),
+                                  "d2h_bytes_per_step": int(n * k * 8),
+                                  "includes": "per rank: H2D dataset, forest build, sharded init + rounds, "
+                                              "finalize, D2H own rows"},
         "gpu_launches": int(launches),
         "roofline": None,
         "cpu_baseline": None,

@@ -229,20 +229,38 @@ class KdForest:
             self._trees = [self.tree(t) for t in range(self.n_trees)]
         return self._trees
 
+    @staticmethod
+    def pack_trees(trees: Sequence, out=None) -> dict:
+        """Concatenated host arrays of `trees` in annk_forest_import's layout;
+        `out` (same keys) may supply preallocated (e.g. pinned) buffers."""
+        ev_attr = "even_split" if hasattr(trees[0], "even_split") else "even"
+        fields = {"split_dim": ("split_dim", np.uint32), "split_val": ("split_val", np.float32),
+                  "left": ("left", np.uint32), "right": ("right", np.uint32), "depth": ("depth", np.uint32),
+                  "even": (ev_attr, np.uint8), "point_index": ("point_index", np.uint32)}
+        packed = {"node_counts": np.array([len(t.split_dim) for t in trees], np.uint32),
+                  "roots": np.array([t.root for t in trees], np.uint32)}
+        for key, (attr, dt) in fields.items():
+            cat = np.concatenate([np.asarray(getattr(t, attr)) for t in trees]).astype(dt)
+            if out is not None:
+                out[key][...] = cat
+                cat = out[key]
+            packed[key] = np.ascontiguousarray(cat)
+        return packed
+
+    @classmethod
+    def import_packed(cls, n, dim, leaf_cap, seed, packed: dict) -> "KdForest":
+        """Device forest from pack_trees() arrays (kd_forest.cpp:332-372 load, then upload)."""
+        h = C.c_void_p()
+        check(lib.annk_forest_import(
+            n, dim, leaf_cap, seed, len(packed["roots"]), packed["node_counts"], packed["roots"],
+            packed["split_dim"], packed["split_val"], packed["left"], packed["right"], packed["depth"],
+            packed["even"], packed["point_index"], C.byref(h)))
+        return cls(h, n, dim, leaf_cap, seed, len(packed["roots"]))
+
     @classmethod
     def from_trees(cls, n, dim, leaf_cap, seed, trees: Sequence) -> "KdForest":
         """Device forest from host trees (e.g. exported by the CPU reference)."""
-        cat = lambda attr, dt: np.ascontiguousarray(
-            np.concatenate([np.asarray(getattr(t, attr)) for t in trees]).astype(dt))
-        ev_attr = "even_split" if hasattr(trees[0], "even_split") else "even"
-        h = C.c_void_p()
-        check(lib.annk_forest_import(
-            n, dim, leaf_cap, seed, len(trees),
-            np.array([len(t.split_dim) for t in trees], np.uint32), np.array([t.root for t in trees], np.uint32),
-            cat("split_dim", np.uint32), cat("split_val", np.float32), cat("left", np.uint32),
-            cat("right", np.uint32), cat("depth", np.uint32), cat(ev_attr, np.uint8),
-            cat("point_index", np.uint32), C.byref(h)))
-        return cls(h, n, dim, leaf_cap, seed, len(trees))
+        return cls.import_packed(n, dim, leaf_cap, seed, cls.pack_trees(trees))
 
     def search_leaves(self, t: int, queries: np.ndarray, n_leaves: int):
         """kd_forest.cpp:276-305 for a batch; returns a list of leaf-id arrays."""
