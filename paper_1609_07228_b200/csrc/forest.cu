@@ -1308,6 +1308,36 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
     }
 }
 
+// annk_forest_import: pack (split_dim, split_val, left, right) into
+// KdNodeDev records and validate them; stats = [leaves, max depth, error bits
+// (1 leaf range, 2 split dimension, 4 child id)].
+__global__ void import_nodes_kernel(const uint32_t* __restrict__ sd, const float* __restrict__ sv,
+                                    const uint32_t* __restrict__ lf, const uint32_t* __restrict__ rt,
+                                    const uint32_t* __restrict__ depth, uint32_t m, uint32_t n, uint32_t dim,
+                                    KdNodeDev* __restrict__ out, uint32_t* stats) {
+    uint32_t leaves = 0, maxd = 0, err = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const uint32_t d = sd[i], l = lf[i], r = rt[i];
+        out[i] = KdNodeDev{d, sv[i], l, r};
+        if (d == kLeaf) {
+            ++leaves;
+            if (l >= r || r > n) err |= 1u;
+        } else {
+            if (d >= dim) err |= 2u;
+            if (l >= m || r >= m) err |= 4u;
+        }
+        maxd = max(maxd, depth[i]);
+    }
+    leaves = __reduce_add_sync(0xffffffffu, leaves);
+    maxd = __reduce_max_sync(0xffffffffu, maxd);
+    err = __reduce_or_sync(0xffffffffu, err);
+    if ((threadIdx.x & 31) == 0) {
+        if (leaves) atomicAdd(&stats[0], leaves);
+        if (maxd) atomicMax(&stats[1], maxd);
+        if (err) atomicOr(&stats[2], err);
+    }
+}
+
 // The per-tree split-dimension stream: out[t][k] = mt19937_64(substream(seed,t))
 // output k mod dim (kd_forest.cpp:53,259).  One CTA per tree; each 312-word
 // regeneration is a 3-phase parallel twist, tempering and the modulo are
@@ -1646,40 +1676,50 @@ int annk_forest_import(uint32_t n, uint32_t dim, uint32_t leaf_cap, uint64_t see
         f->leaf_cap = leaf_cap;
         f->seed = seed;
         f->trees.resize(n_trees);
+        // node arrays go up as given (one copy each); a kernel packs KdNodeDev
+        // records and validates them (kd_forest.cpp:332-372 checks)
+        size_t total = 0;
+        for (uint32_t t = 0; t < n_trees; ++t) {
+            const uint32_t m = node_counts[t];
+            if (m == 0 || m > 2 * n) throw_invalid("forest_import: implausible node count");
+            if (roots[t] >= m) throw_invalid("forest_import: bad root");
+            total += m;
+        }
+        DevBuf<uint32_t> sd(total), lf(total), rt(total);
+        DevBuf<float> sv(total);
+        sd.upload(split_dim, total);
+        sv.upload(split_val, total);
+        lf.upload(left, total);
+        rt.upload(right, total);
+        DevBuf<uint32_t> stats(size_t(n_trees) * 4);
+        stats.zero();
         size_t off = 0;
         for (uint32_t t = 0; t < n_trees; ++t) {
             TreeDev& tr = f->trees[t];
             const uint32_t m = node_counts[t];
-            if (m == 0 || m > 2 * n) throw_invalid("forest_import: implausible node count");
-            std::vector<KdNodeDev> nodes(m);
-            uint32_t leaves = 0, maxd = 0;
-            for (uint32_t i = 0; i < m; ++i) {
-                nodes[i] = KdNodeDev{split_dim[off + i], split_val[off + i], left[off + i], right[off + i]};
-                const bool leaf = split_dim[off + i] == kLeaf;
-                leaves += leaf;
-                if (leaf) {
-                    if (left[off + i] >= right[off + i] || right[off + i] > n) throw_invalid("forest_import: bad leaf range");
-                } else {
-                    if (split_dim[off + i] >= dim) throw_invalid("forest_import: split dimension out of range");
-                    if (left[off + i] >= m || right[off + i] >= m) throw_invalid("forest_import: child id out of range");
-                }
-                maxd = std::max(maxd, depth[off + i]);
-            }
             tr.num_nodes = m;
             tr.root = roots[t];
-            if (tr.root >= m) throw_invalid("forest_import: bad root");
-            tr.leaf_count = leaves;
-            tr.max_depth = maxd;
             tr.nodes.alloc(m);
-            tr.nodes.upload(nodes.data(), m);
             tr.depth.alloc(m);
             tr.depth.upload(depth + off, m);
             tr.even.alloc(m);
             tr.even.upload(even_split + off, m);
             tr.pidx.alloc(n);
             tr.pidx.upload(point_index + size_t(t) * n, n);
-            ssync();
+            LAUNCH(import_nodes_kernel, std::min<uint32_t>((m + 255) / 256, 4096), 256, 0, sd.p + off, sv.p + off,
+                   lf.p + off, rt.p + off, tr.depth.p, m, n, dim, tr.nodes.p, stats.p + size_t(t) * 4);
             off += m;
+        }
+        std::vector<uint32_t> st(size_t(n_trees) * 4);
+        stats.download(st.data(), st.size());
+        ssync();
+        for (uint32_t t = 0; t < n_trees; ++t) {
+            const uint32_t err = st[size_t(t) * 4 + 2];
+            if (err & 1u) throw_invalid("forest_import: bad leaf range");
+            if (err & 2u) throw_invalid("forest_import: split dimension out of range");
+            if (err & 4u) throw_invalid("forest_import: child id out of range");
+            f->trees[t].leaf_count = st[size_t(t) * 4];
+            f->trees[t].max_depth = st[size_t(t) * 4 + 1];
         }
         forest_upload_views(f.get());
         *out = f.release();

@@ -425,3 +425,45 @@ def test_forest_cluster_split_bit_identical(n, dim, trees, integer, dups):
     fd = A.build_forest(x, trees, 8, 13)
     for t in range(trees):
         assert_trees_equal(fd.tree(t), fo.tree(t))
+
+
+@pytest.mark.gpu
+def test_forest_import_roundtrip_reference_trees_and_validation():
+    # annk_forest_import (the AKF1 load path, kd_forest.cpp:332-372): export -> import is the
+    # identity, a forest built by the CPU reference drives the device init bit-exactly, and
+    # malformed trees are rejected with InvalidArgument
+    o = ora()
+    n, dim, trees, leaf, seed = 3000, 32, 4, 8, 4
+    x = A.gen_synthetic(n, dim, seed)
+    fd = A.build_forest(x, trees, leaf, seed)
+    fi = A.KdForest.from_trees(n, dim, leaf, seed, fd.trees)
+    for t in range(trees):
+        a, b = fd.tree(t), fi.tree(t)
+        assert (a.root, a.leaf_count, a.max_depth) == (b.root, b.leaf_count, b.max_depth)
+        for f in ("split_dim", "left", "right", "depth", "even_split", "point_index"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+        np.testing.assert_array_equal(a.split_val.view(np.uint32), b.split_val.view(np.uint32))
+    vo = o.vs(x)
+    fo = o.build_forest(vo, trees, leaf, seed)
+    fref = A.KdForest.from_trees(n, dim, leaf, seed, [fo.tree(t) for t in range(trees)])
+    so = o.init_graph(vo, fo, 10, 4, 30, 20, seed)
+    sd = A.init_graph(x, fref, 10, 4, 30, 20, seed)
+    e = assert_pools_equal(sd, so)
+    assert sd.meta()["dist_comps"] == e["dist_comps"]
+
+    packed = A.KdForest.pack_trees(fd.trees)
+    m0 = int(packed["node_counts"][0])
+    internal = int(np.nonzero(packed["split_dim"][:m0] != 0xffffffff)[0][0])
+    leafi = int(np.nonzero(packed["split_dim"][:m0] == 0xffffffff)[0][0])
+
+    def bad(key, idx, val, match):
+        p = {k: v.copy() for k, v in packed.items()}
+        p[key][idx] = val
+        with pytest.raises(A.InvalidArgument, match=match):
+            A.KdForest.import_packed(n, dim, leaf, seed, p)
+
+    bad("split_dim", internal, dim, "split dimension")
+    bad("left", internal, m0 + 3, "child id")
+    bad("right", leafi, n + 1, "leaf range")
+    bad("roots", 0, m0, "bad root")
+    bad("node_counts", 0, 0, "node count")
