@@ -9,8 +9,10 @@ LIB       := $(PKG)/libannkit_b200.so
 
 FACADE    := $(PKG)/libannkit_facade.so
 FACADE_T  := tests/cpp/test_facade
+CLI       := $(PKG)/annkit
+FACADE_SRCS := $(PKG)/cpp/annkit_facade.cpp $(PKG)/cpp/annkit_io.cpp
 
-all: $(LIB) $(FACADE) $(FACADE_T) oracle
+all: $(LIB) $(FACADE) $(FACADE_T) $(CLI) oracle
 
 build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/annkit_b200.h
 	@mkdir -p build
@@ -20,8 +22,12 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
 
 # C++ host API (include/annkit_b200.hpp) over the C-ABI, and its test program
-$(FACADE): $(PKG)/cpp/annkit_facade.cpp include/annkit_b200.hpp include/annkit_b200.h $(LIB)
-	g++ -std=c++20 -O2 -fPIC -shared -Wall -Iinclude -o $@ $< -L$(PKG) -lannkit_b200 -Wl,-rpath,'$$ORIGIN'
+$(FACADE): $(FACADE_SRCS) include/annkit_b200.hpp include/annkit_b200.h $(LIB)
+	g++ -std=c++20 -O2 -fPIC -shared -Wall -Iinclude -o $@ $(FACADE_SRCS) -L$(PKG) -lannkit_b200 -Wl,-rpath,'$$ORIGIN'
+
+# the `annkit` command line (reference proj/tools/main.cpp subcommands) over the C++ API
+$(CLI): $(PKG)/cpp/annkit_cli.cpp include/annkit_b200.hpp $(FACADE)
+	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lannkit_facade -lannkit_b200 -Wl,-rpath,'$$ORIGIN'
 
 $(FACADE_T): tests/cpp/test_facade.cpp include/annkit_b200.hpp $(FACADE)
 	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lannkit_facade -lannkit_b200 \
@@ -31,7 +37,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB) $(FACADE) $(FACADE_T)
+	rm -rf build $(LIB) $(FACADE) $(FACADE_T) $(CLI)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

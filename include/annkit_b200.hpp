@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -50,10 +51,27 @@ struct GroundTruth {
     std::vector<std::uint32_t> ids;  // n x k
 
     std::span<const std::uint32_t> row(std::uint32_t i) const { return {ids.data() + std::size_t(i) * k, k}; }
+    // dataset.cpp:78-95: ids < base_n and no duplicate within a row (data_error otherwise)
+    void validate_against(std::uint32_t base_n) const;
+};
+
+// dataset.hpp:15-24 error classes of the file readers
+struct format_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct data_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
 };
 
 // dataset.cpp:201-214 (same bytes as the reference's generator).
 VectorSet gen_synthetic(std::uint32_t n, std::uint32_t dim, std::uint64_t seed);
+
+// dataset.cpp:96-200 fvecs / ivecs: per record an int32 dimension then that
+// many little-endian float32 / int32 values (annkit_io.cpp).
+VectorSet load_fvecs(const std::string& path);
+void save_fvecs(const VectorSet& vs, const std::string& path);
+GroundTruth load_ivecs(const std::string& path);
+void save_ivecs(const GroundTruth& gt, const std::string& path);
 
 // ---------------------------------------------------------- kd_forest.hpp
 struct KdNode {
@@ -93,6 +111,9 @@ struct KdForest {
 KdForest build_forest(const VectorSet& vs, std::uint32_t n_trees, std::uint32_t leaf_cap, std::uint64_t seed,
                       std::uint32_t workers = 1);
 std::vector<std::uint32_t> search_leaves(const KdTree& tree, std::span<const float> q, std::uint32_t n_leaves);
+// kd_forest.cpp:307-372 AKF1 persistence (load validates every tree as kd_forest.cpp:175-241)
+void save_forest(const KdForest& forest, const std::string& path);
+KdForest load_forest(const std::string& path);
 std::uint32_t descend_from(const KdTree& tree, std::span<const float> q, std::uint32_t node);
 
 // ------------------------------------------------------ neighbor_pool.hpp
@@ -135,6 +156,11 @@ struct KnnGraph {
     bool has_dists() const { return !dists.empty(); }
 };
 
+// knn_graph.cpp:5-37: ids as ivecs, distances (optional) as a companion fvecs
+void save_graph(const KnnGraph& graph, const std::string& ids_path,
+                const std::optional<std::string>& dists_path = std::nullopt);
+KnnGraph load_graph(const std::string& ids_path, const std::optional<std::string>& dists_path = std::nullopt);
+
 // ------------------------------------------------------ graph_build.hpp
 struct RefineState {
     std::uint32_t k = 0;
@@ -162,6 +188,8 @@ void refine_nn_descent(RefineState& state, const VectorSet& vs, std::uint32_t ma
 KnnGraph finalize(RefineState& state, const VectorSet& vs, std::uint32_t k);
 
 enum class BuildStrategy { efanna, random_descent, nn_expansion, brute_force, init_only };
+const char* to_string(BuildStrategy s);                  // graph_build.cpp:375-384
+BuildStrategy strategy_from_string(const std::string& s);  // :386-393
 
 struct BuildParams {
     std::uint32_t k = 10;
@@ -279,6 +307,13 @@ KnnGraph brute_force_graph(const VectorSet& base, std::uint32_t k, std::uint32_t
                            std::uint64_t* dist_comps = nullptr);
 double recall(std::span<const std::uint32_t> result_ids, std::span<const std::uint32_t> gt_row);
 double graph_accuracy(const KnnGraph& graph, const GroundTruth& gt);
+struct EvalReport {  // eval.hpp
+    std::string metric;
+    double value = 0.0;
+    double seconds = 0.0;
+    std::vector<double> breakdown;  // per row
+};
+EvalReport graph_accuracy_report(const KnnGraph& graph, const GroundTruth& gt);  // eval.cpp:106-123
 std::vector<std::pair<std::uint32_t, double>> accuracy_vs_k(const KnnGraph& graph, const VectorSet& vs,
                                                             std::span<const std::uint32_t> k_list,
                                                             std::uint32_t workers = 1);

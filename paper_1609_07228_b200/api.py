@@ -488,7 +488,7 @@ def graph_accuracy(graph, gt: np.ndarray) -> float:
         raise InvalidArgument("graph_accuracy: empty graph")
     s = 0.0
     for i in range(g.shape[0]):
-        s += len(np.intersect1d(g[i], gt[i], assume_unique=True)) / gt.shape[1]
+        s += len(np.intersect1d(g[i], gt[i])) / gt.shape[1]
     return s / g.shape[0]
 
 

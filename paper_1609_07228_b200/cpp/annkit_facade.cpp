@@ -458,10 +458,17 @@ KnnGraph brute_force_graph(const VectorSet& base, std::uint32_t k, std::uint32_t
 double recall(std::span<const std::uint32_t> result_ids, std::span<const std::uint32_t> gt_row) {
     if (result_ids.size() != gt_row.size()) throw std::invalid_argument("recall: result and truth sizes differ");
     if (gt_row.empty()) throw std::invalid_argument("recall: empty truth row");
-    std::vector<std::uint32_t> t(gt_row.begin(), gt_row.end());
+    // eval.cpp:82-104: multiset intersection of the sorted rows (a duplicated
+    // result id counts once per matching truth entry)
+    std::vector<std::uint32_t> a(result_ids.begin(), result_ids.end()), t(gt_row.begin(), gt_row.end());
+    std::sort(a.begin(), a.end());
     std::sort(t.begin(), t.end());
     std::size_t hits = 0;
-    for (const auto id : result_ids) hits += std::binary_search(t.begin(), t.end(), id) ? 1 : 0;
+    for (std::size_t i = 0, j = 0; i < a.size() && j < t.size();) {
+        if (a[i] < t[j]) ++i;
+        else if (t[j] < a[i]) ++j;
+        else { ++hits; ++i; ++j; }
+    }
     return double(hits) / double(gt_row.size());
 }
 

@@ -31,6 +31,14 @@ static bool throws(F&& f) {
     return false;
 }
 
+// eval.cpp:82-104: multiset intersection; a repeated result id counts once per truth match
+static void test_recall_duplicates() {
+    const std::uint32_t res[3] = {5, 5, 7}, gt[3] = {5, 7, 9};
+    CHECK(recall(std::span<const std::uint32_t>(res, 3), std::span<const std::uint32_t>(gt, 3)) == 2.0 / 3.0);
+    CHECK(throws<std::invalid_argument>(
+        [&] { recall(std::span<const std::uint32_t>(res, 2), std::span<const std::uint32_t>(gt, 3)); }));
+}
+
 static void test_forest_invariants() {
     const VectorSet vs = gen_synthetic(3000, 12, 7);
     const KdForest f = build_forest(vs, 3, 8, 7);
@@ -141,6 +149,7 @@ static void test_acceptance_search() {
 }
 
 int main() {
+    test_recall_duplicates();
     test_forest_invariants();
     test_refine_state_mirror();
     test_acceptance_search();
