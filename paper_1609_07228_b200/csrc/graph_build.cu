@@ -879,29 +879,41 @@ join_agg_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const 
                         }
                     }
                 }
-                if (yv) {
-                    const uint32_t idy = ids[y];
-                    const uint64_t thy = thr_s[y];
+                // accepted offers: bit 2k = y offered to x's pool, bit 2k+1 = x offered to y's
+                // pool; one shared-memory atomic per warp reserves all of them
+                uint32_t acc = 0;
+                const uint32_t idy = yv ? ids[y] : 0u;
+                const uint64_t thy = yv ? thr_s[y] : 0ull;
 #pragma unroll
-                    for (uint32_t k = 0; k < kJoinXR; ++k) {
-                        const uint32_t x = x0 + k;
-                        if (x >= A || y <= x) continue;
-                        const uint32_t idx = ids[x];
-                        if (idx == idy) continue;  // graph_build.cpp:146 (l == j)
-                        ++comps;
-                        const uint64_t kx = make_key(dist[k], idy);  // offer y to x's pool
-                        if (kx < thr_s[x]) {
-                            const uint32_t s = atomicAdd(&ocount, 1u);
-                            okey[s] = kx;
-                            omem[s] = uint16_t(x);
-                        }
-                        const uint64_t ky = make_key(dist[k], idx);  // offer x to y's pool
-                        if (ky < thy) {
-                            const uint32_t s = atomicAdd(&ocount, 1u);
-                            okey[s] = ky;
-                            omem[s] = uint16_t(y);
-                        }
-                    }
+                for (uint32_t k = 0; k < kJoinXR; ++k) {
+                    const uint32_t x = x0 + k;
+                    if (!yv || x >= A || y <= x) continue;
+                    const uint32_t idx = ids[x];
+                    if (idx == idy) continue;  // graph_build.cpp:146 (l == j)
+                    ++comps;
+                    if (make_key(dist[k], idy) < thr_s[x]) acc |= 1u << (2 * k);
+                    if (make_key(dist[k], idx) < thy) acc |= 2u << (2 * k);
+                }
+                const uint32_t mine = __popc(acc);
+                uint32_t incl = mine;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= uint32_t(o)) incl += t;
+                }
+                const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+                uint32_t wbase = 0;
+                if (lane == 31 && wtot) wbase = atomicAdd(&ocount, wtot);
+                wbase = __shfl_sync(0xffffffffu, wbase, 31);
+                uint32_t s_ = wbase + incl - mine;
+                while (acc) {
+                    const uint32_t bit = __ffs(acc) - 1;
+                    acc &= acc - 1;
+                    const uint32_t k = bit >> 1;
+                    const bool to_x = (bit & 1) == 0;
+                    okey[s_] = make_key(dist[k], to_x ? idy : ids[x0 + k]);
+                    omem[s_] = uint16_t(to_x ? x0 + k : y);
+                    ++s_;
                 }
             }
             __syncthreads();
