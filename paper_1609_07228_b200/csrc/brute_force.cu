@@ -579,6 +579,13 @@ __global__ void accuracy_hits_kernel(const uint32_t* __restrict__ graph, uint32_
         if (local[j]) atomicAdd(&hits[j], local[j]);
 }
 
+void merge_split_lists(const uint64_t* part, uint32_t nq, uint32_t splits, uint32_t k, uint64_t* out_keys) {
+    const uint32_t m = next_pow2(splits * k);
+    const uint32_t wpb = std::max(1u, std::min(8u, uint32_t(64 * 1024 / (m * 8))));
+    CK(cudaFuncSetAttribute(bf_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wpb * m * 8)));
+    LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part, nq, splits, k, m, out_keys);
+}
+
 void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
                         const uint32_t* self_ids, uint32_t k, uint64_t* out_keys, const uint8_t* q8,
                         const int32_t* qnorm) {
@@ -595,6 +602,7 @@ void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q
         return;
     }
     const bool u8 = base->u8 && q8 != nullptr;
+    if (u8 && brute_force_tc(base, nq, self_ids, k, out_keys, q8, qnorm)) return;  // tcgen05 path
     if (u8 && base->ld8 <= 128 && k <= 128 && !getenv("ANNK_BF_DP4A")) {
         // tensor-core path
         // buffer room past the kept k decides how often a query's buffer is sorted
@@ -631,13 +639,7 @@ void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q
         else
             LAUNCH(bf_mma_u8_kernel<4>, grid, MTHREADS, smem, base->data8.p, base->norms8.p, nb, base->ld8, q8,
                    qnorm, nq, self_ids, k, cbm, splits, tps, dst);
-        if (splits > 1) {
-            const uint32_t m = next_pow2(splits * k);
-            const uint32_t wpb = std::max(1u, std::min(8u, uint32_t(64 * 1024 / (m * 8))));
-            CK(cudaFuncSetAttribute(bf_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(wpb * m * 8)));
-            LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part.p, nq, splits, k, m, out_keys);
-        }
+        if (splits > 1) merge_split_lists(part.p, nq, splits, k, out_keys);
         return;
     }
     const uint32_t cb = next_pow2(k + BT);

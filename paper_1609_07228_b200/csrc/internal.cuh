@@ -153,4 +153,9 @@ void forest_upload_views(annk_forest* f);
 // exact top-k helper used by brute force and accuracy scoring
 void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
                         const uint32_t* self_rows, uint32_t k, uint64_t* out_keys);
+// merge `splits` sorted k-lists per query (nq x splits x k keys) into the final k
+void merge_split_lists(const uint64_t* part, uint32_t nq, uint32_t splits, uint32_t k, uint64_t* out_keys);
+// exact kNN on tcgen05 (brute_force_tc.cu); false when the shape is not supported
+bool brute_force_tc(const annk_dataset* base, uint32_t nq, const uint32_t* self_ids, uint32_t k,
+                    uint64_t* out_keys, const uint8_t* q8, const int32_t* qnorm);
 }  // namespace annk
