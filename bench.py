@@ -502,6 +502,35 @@ def run_gpu(args, cfg, ws, rank, local):
                 "share_of_step": dom_ms / sum(v[1] for v in prof.values()), "units": unit_desc,
                 "exact_u8_path": dsinfo["u8"]}
 
+    # cfg4: exact kNN graph (self-mode top-k over all N points) on the tcgen05 kernel
+    exact = None
+    if not args.skip_cfg4 and dsinfo["u8"]:
+        bf_runs = []
+        for rep in range(2):  # first call warms the allocator
+            A.profile_reset()
+            A.profile_enable(True)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            ids_all = A.brute_force_knn(vs, None, k)
+            t2 = time.perf_counter()
+            A.profile_enable(False)
+            bf_runs.append((t2 - t1, A.profile_report()))
+        bf_s, bf_prof = bf_runs[-1]
+        kname = next((kn for kn in bf_prof if kn.startswith("bf_tc")), max(bf_prof, key=lambda kn: bf_prof[kn][1]))
+        k_ms = bf_prof[kname][1]
+        int_ops = 2.0 * dim * n * n  # u8 multiply-adds of the N x N dot products
+        t_peak = 2.0 * float(peaks.get("bf16_tflops", 1678.2))  # B200 dense int8 rate = 2x dense bf16
+        exact = {"workload": f"cfg4: self-mode exact top-{k} over {n} x {dim} (brute_force_knn(base, nullptr, k))",
+                 "seconds_through_api": bf_s, "kernels_ms": {kn: round(v[1], 3) for kn, v in bf_prof.items()},
+                 "pairs_per_s": n * (n - 1) / (k_ms / 1e3),
+                 "roofline": {"kernel": kname, "bound": "tensor", "achieved": int_ops / (k_ms / 1e3) / 1e12,
+                              "peak": t_peak, "unit": "TOP/s", "frac": int_ops / (k_ms / 1e3) / 1e12 / t_peak,
+                              "peak_source": "2 x measured dense bf16 TFLOP/s (MEASURED_PEAKS.json); B200 dense "
+                                             "int8 tensor rate is twice bf16",
+                              "traffic": ncu_traffic(args.config, kname)},
+                 "row0_first5": [int(x) for x in ids_all[0, :5]]}
+        del ids_all
+
     # CPU baseline: the reference library on a bounded sample (rank 0, N=1)
     cpu = None
     if rank == 0 and ws == 1 and not args.skip_cpu:
@@ -543,6 +572,7 @@ def run_gpu(args, cfg, ws, rank, local):
                    "chosen": chosen, "fastest_any_iters": fastest, "sweep": sweep},
         "accuracy": {"per_iteration": [round(a, 4) for a in accs], "final_sample": round(final_acc, 4),
                      "dist_comps": comps},
+        "exact_knn": exact,
         "aux_seconds": {"forest": forest_s, "gt_rows": gt_rows_s, "gt_queries": gt_q_s, "data_gen_host": gen_s,
                         "brute_force_pairs_per_s": bf_pairs / (gt_rows_s + gt_q_s)},
         "host_wall_s_per_step": wall_s,
@@ -740,6 +770,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-cfg4", action="store_true", help="skip the exact kNN graph (cfg4) measurement")
     ap.add_argument("--full-log", action="store_true", help="run all iterations / sweep points")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 collectives; gloo keeps buffers on the host (functional runs on one GPU)")

@@ -54,7 +54,8 @@ constexpr uint32_t kCB = 256;
 constexpr uint32_t kChunks = kTB / 64;     // 32-column chunks per warp per tile (two warps per row)              // candidate buffer per query (global memory)
 constexpr uint32_t kStageStride = 36;     // words per lane in the survivor staging area (conflict-free v4)
 constexpr uint32_t kNormBytes = kStages * kTB * 8;  // per stage: the tile's norms, then -(norm >> 1)
-constexpr uint32_t kSmemTC = 1024 + kABytes + kStages * kTileBytes + kNormBytes + kEpiWarps * 32 * kStageStride * 4;
+constexpr uint32_t kStageBytes = kEpiWarps * 32 * kStageStride * 4;
+constexpr uint32_t kSmemTC = 1024 + kABytes + kStages * kTileBytes + kNormBytes + kStageBytes + kTQ * 2 * 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return uint32_t(__cvta_generic_to_shared(p));
@@ -76,6 +77,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             : "r"(a), "r"(parity), "r"(hint)
             : "memory");
     } while (!ok);
+}
+// producer / MMA lanes: back off between probes so their polling does not take
+// issue slots from the epilogue warps sharing their SM sub-partitions
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    uint32_t ok = 0;
+    for (;;) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+        if (ok) return;
+        __nanosleep(64);
+    }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
@@ -239,13 +254,13 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
             for (uint32_t item = blockIdx.x; item < a.n_items; item += gridDim.x, ++ni) {
                 const uint32_t qb = item / a.splits, split = item % a.splits;
                 const uint32_t t0 = split * a.tiles_per_split, t1 = min(n_tiles, t0 + a.tiles_per_split);
-                mbar_wait(&aempty_bar, (ni & 1) ^ 1);
+                mbar_wait_backoff(&aempty_bar, (ni & 1) ^ 1);
                 mbar_expect_tx(&afull_bar, kABytes);
                 for (uint32_t h = 0; h < kNQB; ++h)
                     tma_load_2d(sA + h * kQB * kRow, &tm_q, &afull_bar, 0, int32_t(qb * kTQ + h * kQB));
                 for (uint32_t t = t0; t < t1; ++t, ++it) {
                     const uint32_t s = it % kStages;
-                    mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
+                    mbar_wait_backoff(&empty_bar[s], ((it / kStages) & 1) ^ 1);
                     const bool full_tile = (t + 1) * kTB <= a.nb;  // partial tile: norms read from global
                     mbar_expect_tx(&full_bar[s], kTileBytes + (full_tile ? kTB * 8 : 0));
                     tma_load_2d(sB + s * kTileBytes, &tm_base, &full_bar[s], 0, int32_t(t * kTB));
@@ -263,12 +278,12 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
             for (uint32_t item = blockIdx.x; item < a.n_items; item += gridDim.x, ++ni) {
                 const uint32_t split = item % a.splits;
                 const uint32_t t0 = split * a.tiles_per_split, t1 = min(n_tiles, t0 + a.tiles_per_split);
-                mbar_wait(&afull_bar, ni & 1);
+                mbar_wait_backoff(&afull_bar, ni & 1);
                 tc_fence_after();
                 for (uint32_t t = t0; t < t1; ++t, ++it) {
                     const uint32_t s = it % kStages, b = it & 1;
-                    mbar_wait(&full_bar[s], (it / kStages) & 1);
-                    mbar_wait(&tempty_bar[b], ((it >> 1) & 1) ^ 1);
+                    mbar_wait_backoff(&full_bar[s], (it / kStages) & 1);
+                    mbar_wait_backoff(&tempty_bar[b], ((it >> 1) & 1) ^ 1);
                     tc_fence_after();
 #pragma unroll
                     for (uint32_t h = 0; h < kNQB; ++h)
@@ -293,6 +308,11 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
         const int32_t* ring = reinterpret_cast<const int32_t*>(smem_raw + (sN - smem_u32(smem_raw)));
         uint32_t* st = reinterpret_cast<uint32_t*>(smem_raw + (sN + kNormBytes - smem_u32(smem_raw))) +
                        (warp * 32 + lane) * kStageStride;
+        // each half publishes its list's k-th key; the other half filters with the smaller one
+        // (the union's k-th is at most either), which roughly halves the survivors
+        uint64_t* share = reinterpret_cast<uint64_t*>(smem_raw + (sN + kNormBytes + kStageBytes - smem_u32(smem_raw)));
+        uint64_t* my_share = share + row * 2 + half;
+        const uint64_t* other_share = share + row * 2 + (half ^ 1);
         uint32_t it = 0;
         for (uint32_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
             const uint32_t qb = item / a.splits, split = item % a.splits;
@@ -308,9 +328,19 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
             // group of 4 columns as max(dot + (-h)) with one VIADDMNMX per pair.
             int32_t lim = qvalid ? INT_MIN : INT_MAX;
             int32_t L = qvalid ? (lim + 1) >> 1 : INT_MAX;
+            *my_share = kEmptyKey;
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // shares reset for this item
             for (uint32_t t = t0; t < t1; ++t, ++it) {
                 const uint32_t b = it & 1, s = it % kStages;
                 const bool full_tile = (t + 1) * kTB <= a.nb;
+                {
+                    const uint64_t o = *reinterpret_cast<const volatile uint64_t*>(other_share);
+                    if (qvalid && o < thr) {
+                        thr = o;
+                        lim = qn - int32_t(key_dist(thr));
+                        L = (lim + 1) >> 1;
+                    }
+                }
                 mbar_wait(&tfull_bar[b], (it >> 1) & 1);
                 tc_fence_after();
                 if (full_tile) mbar_wait(&full_bar[s], (it / kStages) & 1);  // column norms landed
@@ -367,10 +397,11 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                         const uint32_t keep = flush_buffer(sb, sc, a.k, lane);
                         if (lane == src) {
                             cnt = keep;
-                            if (keep == a.k) {
+                            if (keep == a.k && sb[a.k - 1] < thr) {
                                 thr = sb[a.k - 1];
                                 lim = qn - int32_t(key_dist(thr));
                                 L = (lim + 1) >> 1;
+                                *reinterpret_cast<volatile uint64_t*>(my_share) = thr;
                             }
                         }
                     }
