@@ -43,15 +43,17 @@ namespace {
 constexpr uint32_t kQB = 128;              // queries per MMA block (M)
 constexpr uint32_t kNQB = 2;               // query blocks per work item
 constexpr uint32_t kTQ = kQB * kNQB;       // queries per work item
-constexpr uint32_t kTB = 128;              // base rows per tile (N)
+constexpr uint32_t kTB = 64;               // base rows per tile (N)
 constexpr uint32_t kRow = 128;             // bytes per row (K): ld8 == 128
-constexpr uint32_t kStages = 6;
+constexpr uint32_t kStages = 12;
+constexpr uint32_t kAcc = 512 / (kNQB * kTB);  // TMEM accumulator buffers (4 x 2 x 64 columns)
 constexpr uint32_t kEpiWarps = 16;
 constexpr uint32_t kThreadsTC = (kEpiWarps + 2) * 32;
-constexpr uint32_t kTileBytes = kTB * kRow;  // 16 KB
+constexpr uint32_t kTileBytes = kTB * kRow;  // 8 KB
 constexpr uint32_t kABytes = kTQ * kRow;     // 32 KB
-constexpr uint32_t kCB = 256;
-constexpr uint32_t kChunks = kTB / 64;     // 32-column chunks per warp per tile (two warps per row)              // candidate buffer per query (global memory)
+constexpr uint32_t kCB = 192;              // candidate list per (query, half), global memory
+constexpr int kSortV = 8;                  // keys per lane in the list sorts (next pow2 of kCB, / 32)
+constexpr uint32_t kChunks = kTB / 64;     // 32-column chunks per warp per tile (two warps per row)
 constexpr uint32_t kStageStride = 36;     // words per lane in the survivor staging area (conflict-free v4)
 constexpr uint32_t kNormBytes = kStages * kTB * 8;  // per stage: the tile's norms, then -(norm >> 1)
 constexpr uint32_t kStageBytes = kEpiWarps * 32 * kStageStride * 4;
@@ -170,20 +172,20 @@ struct TcArgs {
     uint64_t* out;   // (nq x splits) x k
 };
 
-// Sort lane `src`'s candidate buffer (cnt keys) with the whole warp and keep its
-// k best at the front; returns the kept count (valid in every lane).
-__device__ __noinline__ uint32_t flush_buffer(uint64_t* b, uint32_t cnt, uint32_t k, uint32_t lane) {
-    uint64_t v[kCB / 32];
+// Fallback cut (more than kCB - 32 keys tie at the k-th distance): sort the
+// list with the whole warp and keep exactly its k best.
+__device__ __noinline__ uint32_t flush_sort(uint64_t* b, uint32_t cnt, uint32_t k, uint32_t lane) {
+    uint64_t v[kSortV];
 #pragma unroll
-    for (int r = 0; r < int(kCB / 32); ++r) {
+    for (int r = 0; r < kSortV; ++r) {
         const uint32_t e = uint32_t(r) * 32 + lane;
         v[r] = e < cnt ? b[e] : kEmptyKey;
     }
-    warp_sort_regs<kCB / 32>(v);
+    warp_sort_regs<kSortV>(v);
     __syncwarp();
     const uint32_t keep = min(cnt, k);
 #pragma unroll
-    for (int r = 0; r < int(kCB / 32); ++r) {
+    for (int r = 0; r < kSortV; ++r) {
         const uint32_t e = uint32_t(r) * 32 + lane;
         if (e < keep) b[e] = v[r];
     }
@@ -191,17 +193,60 @@ __device__ __noinline__ uint32_t flush_buffer(uint64_t* b, uint32_t cnt, uint32_
     return keep;
 }
 
+struct Cut {
+    uint32_t n;     // keys kept (>= k)
+    uint64_t tkey;  // every key of the list that can still matter is <= tkey
+};
+
+// Cut a full candidate list (cnt > k keys) back to the keys whose distance is
+// at most T = its k-th smallest distance (ties kept, so at least k remain; the
+// list stays unsorted).  T is found by a warp-wide binary search on the integer
+// distance (< 2^24 on the u8 datapath): 24 rounds of count(d <= mid) with one
+// REDUX each — a fraction of a full sort's work.  The new filter bound is
+// (T, max id): any later key with a larger distance cannot reach the top k.
+__device__ __noinline__ Cut flush_buffer(uint64_t* b, uint32_t cnt, uint32_t k, uint32_t lane) {
+    constexpr int V = kCB / 32;
+    uint64_t v[V];
+    uint32_t dv[V];
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+        const uint32_t e = uint32_t(r) * 32 + lane;
+        v[r] = e < cnt ? b[e] : kEmptyKey;
+        dv[r] = e < cnt ? uint32_t(key_dist(v[r])) : 0xffffffffu;
+    }
+    uint32_t lo = 0, hi = (1u << 24) - 1;  // smallest T with #{d <= T} >= k lies in [lo, hi]
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        uint32_t c = 0;
+#pragma unroll
+        for (int r = 0; r < V; ++r) c += dv[r] <= mid ? 1u : 0u;
+        if (__reduce_add_sync(0xffffffffu, c) >= k) hi = mid;
+        else lo = mid + 1;
+    }
+    uint32_t n = 0;
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+        const bool keep = dv[r] <= lo;
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) b[n + __popc(bal & lt)] = v[r];
+        n += __popc(bal);
+    }
+    __syncwarp();
+    return Cut{n, (uint64_t(__float_as_uint(float(lo))) << 32) | 0xffffffffull};
+}
+
 // Sort a candidate buffer (cnt keys) with the whole warp and write its k best.
 __device__ __noinline__ void emit_topk(const uint64_t* b, uint32_t cnt, uint32_t k, uint64_t* o, uint32_t lane) {
-    uint64_t v[kCB / 32];
+    uint64_t v[kSortV];
 #pragma unroll
-    for (int r = 0; r < int(kCB / 32); ++r) {
+    for (int r = 0; r < kSortV; ++r) {
         const uint32_t e = uint32_t(r) * 32 + lane;
         v[r] = e < cnt ? b[e] : kEmptyKey;
     }
-    warp_sort_regs<kCB / 32>(v);
+    warp_sort_regs<kSortV>(v);
 #pragma unroll
-    for (int r = 0; r < int(kCB / 32); ++r) {
+    for (int r = 0; r < kSortV; ++r) {
         const uint32_t e = uint32_t(r) * 32 + lane;
         if (e < k) o[e] = v[r];
     }
@@ -211,7 +256,7 @@ __device__ __noinline__ void emit_topk(const uint64_t* b, uint32_t cnt, uint32_t
 __global__ void __launch_bounds__(kThreadsTC, 1)
 bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_constant__ CUtensorMap tm_q, TcArgs a) {
     extern __shared__ unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2];
+    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[kAcc], tempty_bar[kAcc];
     __shared__ __align__(8) uint64_t afull_bar, aempty_bar;
     __shared__ uint32_t tmem_base_s;
 
@@ -225,7 +270,7 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1 + kEpiWarps);  // MMA commit + every epilogue warp (norms)
         }
-        for (uint32_t b = 0; b < 2; ++b) {
+        for (uint32_t b = 0; b < kAcc; ++b) {
             mbar_init(&tfull_bar[b], 1);
             mbar_init(&tempty_bar[b], kEpiWarps);
         }
@@ -281,9 +326,9 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                 mbar_wait_backoff(&afull_bar, ni & 1);
                 tc_fence_after();
                 for (uint32_t t = t0; t < t1; ++t, ++it) {
-                    const uint32_t s = it % kStages, b = it & 1;
-                    mbar_wait_backoff(&full_bar[s], (it / kStages) & 1);
-                    mbar_wait_backoff(&tempty_bar[b], ((it >> 1) & 1) ^ 1);
+                    const uint32_t s = it % kStages, b = it % kAcc;
+                    mbar_wait(&full_bar[s], (it / kStages) & 1);  // the MMA lane polls without backoff
+                    mbar_wait(&tempty_bar[b], ((it / kAcc) & 1) ^ 1);
                     tc_fence_after();
 #pragma unroll
                     for (uint32_t h = 0; h < kNQB; ++h)
@@ -331,7 +376,7 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
             *my_share = kEmptyKey;
             asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // shares reset for this item
             for (uint32_t t = t0; t < t1; ++t, ++it) {
-                const uint32_t b = it & 1, s = it % kStages;
+                const uint32_t b = it % kAcc, s = it % kStages;
                 const bool full_tile = (t + 1) * kTB <= a.nb;
                 {
                     const uint64_t o = *reinterpret_cast<const volatile uint64_t*>(other_share);
@@ -341,7 +386,7 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                         L = (lim + 1) >> 1;
                     }
                 }
-                mbar_wait(&tfull_bar[b], (it >> 1) & 1);
+                mbar_wait(&tfull_bar[b], (it / kAcc) & 1);
                 tc_fence_after();
                 if (full_tile) mbar_wait(&full_bar[s], (it / kStages) & 1);  // column norms landed
                 const uint32_t taddr = tmem + ((quarter * 32) << 16) + (b * kNQB + h) * kTB;
@@ -394,11 +439,15 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                         need &= need - 1;
                         uint64_t* sb = a.cand + (cbase + row - lane + src) * kCB;
                         const uint32_t sc = __shfl_sync(0xffffffffu, cnt, src);
-                        const uint32_t keep = flush_buffer(sb, sc, a.k, lane);
+                        Cut cut = flush_buffer(sb, sc, a.k, lane);
+                        if (cut.n + 32 > kCB) {  // too many ties at the k-th distance: exact cut
+                            cut.n = flush_sort(sb, sc, a.k, lane);
+                            cut.tkey = sb[a.k - 1];
+                        }
                         if (lane == src) {
-                            cnt = keep;
-                            if (keep == a.k && sb[a.k - 1] < thr) {
-                                thr = sb[a.k - 1];
+                            cnt = cut.n;
+                            if (cut.tkey < thr) {
+                                thr = cut.tkey;
                                 lim = qn - int32_t(key_dist(thr));
                                 L = (lim + 1) >> 1;
                                 *reinterpret_cast<volatile uint64_t*>(my_share) = thr;
