@@ -185,6 +185,39 @@ __device__ __forceinline__ float l2_exact_ldg(const float* __restrict__ a, const
     return acc;
 }
 
+// The same chain with the row streamed 8 float4 (one 128-byte line) at a time:
+// the eight loads are issued before the chain consumes them, so a thread keeps a
+// whole line in flight instead of one 16-byte piece (wide rows, one row per lane).
+__device__ __forceinline__ float l2_exact_ldg8(const float* __restrict__ a, const float* __restrict__ b,
+                                               uint32_t dim_pad4) {
+    float acc = 0.0f;
+    uint32_t i = 0;
+    for (; i + 32 <= dim_pad4; i += 32) {
+        float4 y[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) y[u] = __ldg(reinterpret_cast<const float4*>(b + i) + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float4 x = *reinterpret_cast<const float4*>(a + i + 4 * u);
+            float d;
+            d = __fsub_rn(x.x, y[u].x); acc = __fadd_rn(acc, __fmul_rn(d, d));
+            d = __fsub_rn(x.y, y[u].y); acc = __fadd_rn(acc, __fmul_rn(d, d));
+            d = __fsub_rn(x.z, y[u].z); acc = __fadd_rn(acc, __fmul_rn(d, d));
+            d = __fsub_rn(x.w, y[u].w); acc = __fadd_rn(acc, __fmul_rn(d, d));
+        }
+    }
+    for (; i < dim_pad4; i += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(a + i);
+        const float4 y = __ldg(reinterpret_cast<const float4*>(b + i));
+        float d;
+        d = __fsub_rn(x.x, y.x); acc = __fadd_rn(acc, __fmul_rn(d, d));
+        d = __fsub_rn(x.y, y.y); acc = __fadd_rn(acc, __fmul_rn(d, d));
+        d = __fsub_rn(x.z, y.z); acc = __fadd_rn(acc, __fmul_rn(d, d));
+        d = __fsub_rn(x.w, y.w); acc = __fadd_rn(acc, __fmul_rn(d, d));
+    }
+    return acc;
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // In-place ascending bitonic sort of n (power of two) 64-bit keys in shared

@@ -33,6 +33,7 @@ namespace {
 
 constexpr uint32_t kInitWarps = 4;
 constexpr uint32_t kInitCap = 1024;  // fast-path candidate capacity per point
+constexpr uint32_t kStageCols = 64;  // fp32 init: floats per staged candidate-row chunk
 
 // ---------------------------------------------------------------- helpers
 
@@ -87,6 +88,7 @@ struct InitScratch {
     uint32_t* cnt;  // [0] unique count, [1] sibling count, [2] overflow flag
     const uint8_t* pf_base;  // rows to prefetch into L2 on first insert (nullptr: none)
     uint32_t pf_ld;
+    float* stage;  // fp32 path: 32 candidate rows x kStageCols (+4 pad) staging (nullptr: per-lane loads)
 };
 
 __device__ __forceinline__ void hs_insert(const InitScratch& w, uint32_t id) {
@@ -249,6 +251,45 @@ __device__ uint32_t warp_select_dist(const uint64_t* keys, uint32_t nk, uint32_t
     return prefix;
 }
 
+// The pool from point i's u unique candidate keys (warp scratch): exact top-P by
+// (dist, id), all flagged new (graph_build.cpp:282-288).
+__device__ void init_select(const InitArgs& a, uint32_t i, uint64_t* keys, uint32_t u, uint32_t* hist) {
+    const uint32_t lane = lane_id();
+    uint32_t take = min(u, a.P);
+    uint64_t* surv = keys;
+    uint32_t ns = u;
+    if (u > a.P) {
+        // keep keys whose distance <= the P-th smallest distance (ties included)
+        const uint32_t T = warp_select_dist(keys, u, a.P, hist);
+        ns = 0;
+        for (uint32_t base = 0; base < u; base += 32) {
+            const uint32_t j = base + lane;
+            const uint64_t v = j < u ? keys[j] : kEmptyKey;
+            const bool keep = j < u && uint32_t(v >> 32) <= T;
+            const uint32_t b = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (keep) surv[ns + __popc(b & ((1u << lane) - 1u))] = v;  // in place: target <= j
+            ns += __popc(b);
+            __syncwarp();
+        }
+    }
+    const uint32_t m = next_pow2(max(ns, 1u));
+    for (uint32_t j = ns + lane; j < m; j += 32) surv[j] = kEmptyKey;
+    __syncwarp();
+    warp_bitonic_sort(surv, m);
+    uint64_t* pk = a.keys + size_t(i) * a.P;
+    uint8_t* pf = a.flags + size_t(i) * a.P;
+    for (uint32_t j = lane; j < a.P; j += 32) {
+        pk[j] = j < take ? surv[j] : kEmptyKey;
+        pf[j] = j < take ? 1 : 0;
+    }
+    if (lane == 0) {
+        a.sizes[i] = take;
+        atomicAdd(a.comps, (unsigned long long)u);
+    }
+    __syncwarp();
+}
+
 // Distances, then the pool: exact top-P by (dist, id) of the unique candidates.
 __device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, const InitScratch& w, uint32_t* hist) {
     const uint32_t lane = lane_id();
@@ -302,52 +343,60 @@ __device__ void init_finish(const InitArgs& a, uint32_t i, const float* q, const
             }
         }
     } else {
-        for (uint32_t j = lane; j < u; j += 32) {
-            const uint32_t id = w.uniq[j];
-            keys[j] = make_key(l2_exact_ldg(q, a.x + size_t(id) * a.ld, a.ld), id);
+        if (w.stage) {
+            // wide fp32 rows: 32 candidates at a time; their rows pass through shared
+            // memory in kStageCols-float chunks loaded coalesced (each load instruction
+            // covers 128-byte runs of a few rows instead of 16 bytes of 32 rows), then
+            // every lane runs its own candidate's exact sequential chain from there
+            constexpr uint32_t SW = kStageCols + 4;  // padded row stride: conflict-free 16-byte reads
+            constexpr uint32_t F4 = kStageCols / 4;  // float4 per staged row chunk
+            constexpr uint32_t RPI = 32 / F4;        // rows per load instruction
+            float* stg = w.stage;
+            for (uint32_t j0 = 0; j0 < u; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const uint32_t myid = w.uniq[j < u ? j : j0];
+                float acc = 0.0f;
+                for (uint32_t c0 = 0; c0 < a.ld; c0 += kStageCols) {
+                    const uint32_t nc = min(kStageCols, a.ld - c0);  // multiple of 4
+#pragma unroll
+                    for (uint32_t r0 = 0; r0 < 32; r0 += RPI) {
+                        const uint32_t r = r0 + lane / F4, f = lane % F4;
+                        const uint32_t rid = __shfl_sync(0xffffffffu, myid, r);
+                        if (f * 4 < nc)
+                            *reinterpret_cast<float4*>(stg + r * SW + f * 4) =
+                                __ldg(reinterpret_cast<const float4*>(a.x + size_t(rid) * a.ld + c0) + f);
+                    }
+                    __syncwarp();
+                    const float* mine = stg + lane * SW;
+                    for (uint32_t e = 0; e < nc; e += 4) {
+                        const float4 xv = *reinterpret_cast<const float4*>(q + c0 + e);
+                        const float4 yv = *reinterpret_cast<const float4*>(mine + e);
+                        float d;
+                        d = __fsub_rn(xv.x, yv.x); acc = __fadd_rn(acc, __fmul_rn(d, d));
+                        d = __fsub_rn(xv.y, yv.y); acc = __fadd_rn(acc, __fmul_rn(d, d));
+                        d = __fsub_rn(xv.z, yv.z); acc = __fadd_rn(acc, __fmul_rn(d, d));
+                        d = __fsub_rn(xv.w, yv.w); acc = __fadd_rn(acc, __fmul_rn(d, d));
+                    }
+                    __syncwarp();
+                }
+                if (j < u) keys[j] = make_key(acc, myid);
+            }
+        } else {
+            for (uint32_t j = lane; j < u; j += 32) {
+                const uint32_t id = w.uniq[j];
+                keys[j] = make_key(l2_exact_ldg8(q, a.x + size_t(id) * a.ld, a.ld), id);
+            }
         }
     }
     __syncwarp();
-    uint32_t take = min(u, a.P);
-    uint32_t* surv_ids = w.uniq;  // reuse: survivors compacted in place as keys below
-    uint64_t* surv = keys;
-    uint32_t ns = u;
-    if (u > a.P) {
-        // keep keys whose distance <= the P-th smallest distance (ties included)
-        const uint32_t T = warp_select_dist(keys, u, a.P, hist);
-        ns = 0;
-        for (uint32_t base = 0; base < u; base += 32) {
-            const uint32_t j = base + lane;
-            const uint64_t v = j < u ? keys[j] : kEmptyKey;
-            const bool keep = j < u && uint32_t(v >> 32) <= T;
-            const uint32_t b = __ballot_sync(0xffffffffu, keep);
-            __syncwarp();
-            if (keep) surv[ns + __popc(b & ((1u << lane) - 1u))] = v;  // in place: target <= j
-            ns += __popc(b);
-            __syncwarp();
-        }
-    }
-    (void)surv_ids;
-    const uint32_t m = next_pow2(max(ns, 1u));
-    for (uint32_t j = ns + lane; j < m; j += 32) surv[j] = kEmptyKey;
-    __syncwarp();
-    warp_bitonic_sort(surv, m);
-    uint64_t* pk = a.keys + size_t(i) * a.P;
-    uint8_t* pf = a.flags + size_t(i) * a.P;
-    for (uint32_t j = lane; j < a.P; j += 32) {
-        pk[j] = j < take ? surv[j] : kEmptyKey;
-        pf[j] = j < take ? 1 : 0;
-    }
-    if (lane == 0) {
-        a.sizes[i] = take;
-        atomicAdd(a.comps, (unsigned long long)u);
-    }
-    __syncwarp();
+    init_select(a, i, keys, u, hist);
 }
 
 __host__ __device__ __forceinline__ size_t init_warp_bytes(uint32_t cap, uint32_t ld, uint32_t sib_cap) {
-    // table (cap u32) + uniq (cap u32) == cap u64 keys, q row, sib (2*sib_cap), hist (256), cnt (4)
-    return (size_t(cap) * 8 + size_t(ld) * 4 + size_t(sib_cap) * 8 + 256 * 4 + 16 + 15) & ~size_t(15);
+    // table (cap u32) + uniq (cap u32) == cap u64 keys, q row, sib (2*sib_cap), hist (256), cnt (4),
+    // fp32 path: candidate-row staging (32 rows x (kStageCols + 4) floats)
+    return (size_t(cap) * 8 + size_t(ld) * 4 + size_t(sib_cap) * 8 + 256 * 4 + 16 +
+            (ld ? size_t(32) * (kStageCols + 4) * 4 : 0) + 15) & ~size_t(15);
 }
 
 __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint32_t sib_cap,
@@ -374,6 +423,7 @@ __global__ void __launch_bounds__(kInitWarps * 32) init_kernel(InitArgs a, uint3
     w.sib_cap = sib_cap;
     uint32_t* hist = w.sib + 2 * sib_cap;
     w.cnt = hist + 256;
+    w.stage = q_ld ? reinterpret_cast<float*>(w.cnt + 4) : nullptr;
     for (uint32_t ord = blockIdx.x * kInitWarps + warp; ord < n_visit; ord += gridDim.x * kInitWarps) {
         // visit points in tree-0 leaf order: concurrently processed points share
         // most candidate rows, so the gathers hit L2
@@ -408,6 +458,7 @@ __global__ void init_overflow_kernel(InitArgs a, const uint32_t* list, uint32_t 
         w.tslots = 2 * cap;
         w.pf_base = nullptr;
         w.pf_ld = 0;
+        w.stage = nullptr;
         w.sib = w.uniq + cap;
         w.sib_cap = sib_cap;
         w.cnt = s_misc + 256;

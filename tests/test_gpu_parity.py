@@ -181,6 +181,17 @@ def test_init_and_nn_descent_bit_exact(n, dim, trees, leaf, k, dep, P, S, seed, 
                 np.testing.assert_array_equal(dl[i], ol[i], err_msg=f"list {which} row {i} iter {it}")
 
 
+@pytest.mark.parametrize("n,dim,trees,leaf,P,seed", [
+    (1500, 960, 8, 10, 100, 4),   # cfg3-shaped wide rows (batched row loads)
+    (1001, 50, 4, 10, 30, 8),     # dim not a multiple of 32 (load-batch tail)
+])
+def test_wide_fp32_init_bit_exact(n, dim, trees, leaf, P, seed):
+    x = A.gen_synthetic(n, dim, seed)
+    o, vo, so, sd = _pair(x, trees, leaf, seed, 10, 4, P, 10)
+    e = assert_pools_equal(sd, so)
+    assert sd.meta()["dist_comps"] == e["dist_comps"]
+
+
 def test_integer_mixture_refine_and_finalize():
     x = mixture(20000, 128, 40, 3)
     o, vo, so, sd = _pair(x, 4, 10, 3, 10, 4, 30, 10)
