@@ -405,10 +405,12 @@ def test_brute_force_tensor_core_path_matches_dp4a_and_oracle(n, dim, k, nq):
     np.testing.assert_array_equal(ids_mma, ids_o)
 
 
-def test_wide_fp32_rows_join_bit_exact():
-    # d = 960 float rows (cfg3 shape): the join streams rows through L1 (join_wide_kernel)
+@pytest.mark.parametrize("dim", [960, 1000])
+def test_wide_fp32_rows_join_bit_exact(dim):
+    # wide float rows (cfg3 shape; 1000 = a partial last 64-float chunk): the join stages
+    # the lanes' rows through shared memory (join_wide_kernel)
     o = ora()
-    x = mixture(1500, 960, 12, 3, lo=0.05, hi=0.35, sd=0.05, clip=(0.0, 1.0), rnd=False)
+    x = mixture(1500, dim, 12, 3, lo=0.05, hi=0.35, sd=0.05, clip=(0.0, 1.0), rnd=False)
     vo = o.vs(x)
     fo = o.build_forest(vo, 3, 10, 3)
     so = o.init_graph(vo, fo, 10, 4, 30, 10, 3)
