@@ -123,7 +123,7 @@ __device__ __forceinline__ bool mark_visited(const SearchArgs& a, uint32_t slot,
 __device__ __forceinline__ float qdist(const SearchArgs& a, const Smem& s, uint32_t id) {
     DCHK(id < a.n);
     if (a.x8) return l2_u8(s.q8, a.x8 + size_t(id) * a.ld8, a.ld8, s.qnorm, a.norms8[id]);
-    return l2_exact_ldg(s.q, a.x + size_t(id) * a.ld, a.ld);
+    return l2_exact_ldg8(s.q, a.x + size_t(id) * a.ld, a.ld);
 }
 
 // Worker barrier (named barrier 1 over the W worker threads; the BBF
