@@ -30,7 +30,8 @@ def _mma_sync(x, q, k):
         del os.environ["ANNK_BF_MMA_SYNC"]
 
 
-@pytest.mark.parametrize("n,k,seed", [(3000, 100, 1), (1000, 1, 2), (2049, 128, 3), (300, 10, 4), (130, 129 - 2, 5)])
+@pytest.mark.parametrize("n,k,seed", [(3000, 100, 1), (1000, 1, 2), (2049, 128, 3), (300, 10, 4), (130, 129 - 2, 5),
+                                      (50, 5, 6), (64, 63, 7), (65, 64, 8)])
 def test_tc_self_mode_matches_oracle(n, k, seed):
     o = ora()
     x = mixture(n, 128, 12, seed)
@@ -83,3 +84,11 @@ def test_tc_large_self_mode_vs_mma_sync():
     ids_o = o.brute_force(o.vs(x), o.vs(x[rows]), 101, workers=8)
     for r, i in enumerate(rows):
         np.testing.assert_array_equal(ids[i], [j for j in ids_o[r] if j != i][:100])
+
+
+def test_tc_rows_subset_shard_mode():
+    # brute_force_rows (the sharded ground truth): self exclusion by the row's own id
+    x = mixture(7000, 128, 30, 21)
+    rows = np.array([0, 1, 63, 64, 6999, 4097, 12, 5000], np.uint32)
+    full = A.brute_force_knn(x, None, 100)
+    np.testing.assert_array_equal(A.brute_force_rows(x, rows, 100), full[rows])
