@@ -581,9 +581,15 @@ __global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
                         nb[u] = a.graph[size_t(e) * a.gk + c];
                     }
                 }
+                // a plain (L1-cached) read settles most revisits without an L2 atomic: a set
+                // bit is always current (bits are only cleared by this CTA's own stores at
+                // the end of a query); a clear bit may be stale, so it is set atomically
+#pragma unroll
+                for (uint32_t u = 0; u < kU; ++u) old[u] = nb[u] != kInvalidId ? bm[nb[u] >> 5] : 0u;
 #pragma unroll
                 for (uint32_t u = 0; u < kU; ++u)
-                    old[u] = nb[u] != kInvalidId ? atomicOr(&bm[nb[u] >> 5], 1u << (nb[u] & 31)) : 0u;
+                    if (nb[u] != kInvalidId && !(old[u] & (1u << (nb[u] & 31))))
+                        old[u] = atomicOr(&bm[nb[u] >> 5], 1u << (nb[u] & 31));
 #pragma unroll
                 for (uint32_t u = 0; u < kU; ++u) {
                     const uint32_t id = nb[u];
