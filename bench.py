@@ -57,12 +57,23 @@ CONFIGS = {
     "cfg3": dict(n=1_000_000, dim=960, n_queries=1000, centers=500, trees=8, leaf=10, k=100, P=100, S=20,
                  max_iters=10, dep=4, k_return=100, sweep=[100, 200, 400, 800], acc_sample=2000, ref_points=16_384,
                  ref_queries=100, mix=(0.05, 0.35, 0.05, 0.0, 1.0, False)),
+    # configs[4]: the 8-GPU scaling case (8M points, 4000 centers, 80k queries; cfg2 build parameters
+    # assumed), runnable on one GPU too; its cfg4-style exact graph (6.4e13 pairs) is not run
+    "cfg5": dict(n=8_000_000, dim=128, n_queries=80_000, centers=4000, trees=8, leaf=8, k=100, P=100, S=20,
+                 max_iters=10, dep=4, k_return=100, sweep=[100, 200, 400, 800], acc_sample=10_000,
+                 ref_points=65_536, ref_queries=500, skip_exact=True),
     # a small smoke-sized case for quick checks
     "tiny": dict(n=50_000, dim=128, n_queries=1000, centers=100, trees=4, leaf=8, k=20, P=40, S=10,
                  max_iters=6, dep=4, k_return=20, sweep=[40, 80, 160], acc_sample=2000, ref_points=50_000,
                  ref_queries=200),
 }
 SEED = 1
+_T0 = time.time()
+
+
+def _log(msg):
+    """Progress marker on stderr (stdout carries only the JSON line)."""
+    print(f"[bench +{time.time() - _T0:.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 def gen_data(cfg, n=None):
@@ -291,6 +302,7 @@ def run_gpu(args, cfg, ws, rank, local):
         return e
 
     t0 = time.perf_counter()
+    _log("data")
     base, queries = gen_data(cfg)
     gen_s = time.perf_counter() - t0
     vs = A.VectorSet(base)
@@ -305,6 +317,7 @@ def run_gpu(args, cfg, ws, rank, local):
     forest_s = e0.elapsed_time(e1) / 1e3
 
     # exact ground truth (untimed): sampled self-mode rows + query rows
+    _log("ground truth")
     rows = sample_rows(n, cfg["acc_sample"])
     e0 = ev()
     gt_rows = A.brute_force_rows(vs, rows, k)
@@ -319,6 +332,7 @@ def run_gpu(args, cfg, ws, rank, local):
     bf_pairs = float(len(rows)) * (n - 1) + float(cfg["n_queries"]) * n
 
     # calibration build: accuracy per iteration -> crossing iteration
+    _log("calibration build")
     st = A.init_graph(vs, forest, k, cfg["dep"], cfg["P"], cfg["S"], SEED)
     accs = [A.detail.pool_topk_accuracy(st, gt_rows, rows)]
     crossing = None
@@ -333,6 +347,7 @@ def run_gpu(args, cfg, ws, rank, local):
         v = ctypes.c_uint64(0)
         A.lib.annk_state_join_rows(st.handle, ctypes.byref(v))
         join_rows.append(int(v.value))
+        _log(f"iteration {it + 1}: accuracy {accs[-1]:.4f}")
         if crossing is None and accs[-1] >= 0.9:
             crossing = it + 1
             if not args.full_log:
@@ -353,6 +368,7 @@ def run_gpu(args, cfg, ws, rank, local):
             phase_ms[f"iter{j + 1}"].append((time.perf_counter() - t0) * 1e3)
         return s
 
+    _log(f"warm-up + timed builds (crossing at iteration {crossing})")
     for _ in range(args.warmup):
         s = build_once()
         s = None
@@ -384,6 +400,7 @@ def run_gpu(args, cfg, ws, rank, local):
     graph = A.finalize(s, vs, k)
     del s
 
+    _log("search sweep")
     # search sweep (secondary metric): smallest pool reaching recall@k_return >= 0.9
     searcher = A.GraphSearcher(vs, forest, graph)
     sweep = []
@@ -428,6 +445,7 @@ def run_gpu(args, cfg, ws, rank, local):
                            "frac": alg / (kms / 1e3) / 1e9 / pk, "algorithmic_bytes": alg, "kernel_ms": kms,
                            "traffic": ncu_traffic(args.config, tkey)}
 
+    _log("e2e")
     # e2e through the C-ABI from pinned host memory
     pinned = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
     pinned.numpy()[:] = base
@@ -461,6 +479,7 @@ def run_gpu(args, cfg, ws, rank, local):
     e2e_s = e2e_run(False)
     e2e_fb_s = e2e_run(True)
 
+    _log("roofline")
     # roofline: the dominant kernel's algorithmic bytes per launch / measured duration
     peaks = {}
     try:
@@ -502,9 +521,10 @@ def run_gpu(args, cfg, ws, rank, local):
                 "share_of_step": dom_ms / sum(v[1] for v in prof.values()), "units": unit_desc,
                 "exact_u8_path": dsinfo["u8"]}
 
+    _log("exact kNN")
     # cfg4: exact kNN graph (self-mode top-k over all N points) on the tcgen05 kernel
     exact = None
-    if not args.skip_cfg4 and dsinfo["u8"]:
+    if not args.skip_cfg4 and dsinfo["u8"] and not cfg.get("skip_exact"):
         bf_runs = []
         for rep in range(2):  # first call warms the allocator
             A.profile_reset()
@@ -531,6 +551,7 @@ def run_gpu(args, cfg, ws, rank, local):
                  "row0_first5": [int(x) for x in ids_all[0, :5]]}
         del ids_all
 
+    _log("cpu baseline")
     # CPU baseline: the reference library on a bounded sample (rank 0, N=1)
     cpu = None
     if rank == 0 and ws == 1 and not args.skip_cpu:
@@ -550,7 +571,7 @@ def run_gpu(args, cfg, ws, rank, local):
         "config": {"workload": args.config, "n": n, "dim": dim, "trees": cfg["trees"], "leaf_cap": cfg["leaf"],
                    "k": k, "pool_cap": cfg["P"], "sample_cap": cfg["S"], "conquer_depth": cfg["dep"],
                    "iterations_to_acc_0.9": crossing, "accuracy_sample_rows": int(len(rows)),
-                   "l2": "inputs larger than L2 (512 MB dataset)", "parallelism": f"replicas x{ws}"},
+                   "l2": f"inputs larger than L2 ({n * dim * 4 / 1e6:.0f} MB dataset)", "parallelism": f"replicas x{ws}"},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * dim * 4) + f_bytes,
                 "d2h_bytes_per_step": int(n * k * 8),
                 "includes": "H2D dataset + H2D prebuilt forest (host arrays; the reference's build_graph is timed "
@@ -776,7 +797,7 @@ def main():
                     help="N>1 collectives; gloo keeps buffers on the host (functional runs on one GPU)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
-    cfg.setdefault("ref_iters", {"cfg2": 2, "cfg1": 3, "cfg3": 3, "tiny": 3}[args.config])
+    cfg.setdefault("ref_iters", {"cfg2": 2, "cfg1": 3, "cfg3": 3, "cfg5": 2, "tiny": 3}[args.config])
     ws, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, cfg, ws, rank)

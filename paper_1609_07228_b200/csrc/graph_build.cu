@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <numeric>
 
@@ -1682,13 +1683,20 @@ uint64_t g_spill_per_point_hint = 8;
 // Join of the owned points (graph_build.cpp:105-162): every offer that beats its
 // target's start-of-round tail lands in the target's slots or the spill list;
 // pools are not touched.  Offers may target any point.
-void join_phase(annk_state* s, const annk_dataset* ds) {
+// Offers one join launch may produce: the spill reservation counter is 32-bit
+// and the spill list is capped (kMaxSpill entries, 12 bytes each); a visit range
+// that would exceed either is refused (returns false, pools untouched) and the
+// caller joins it in smaller pieces.
+constexpr uint64_t kMaxJoinOffers = 1ull << 31;
+constexpr uint32_t kMaxSpill = 1u << 28;
+
+bool join_phase(annk_state* s, const annk_dataset* ds, uint32_t vb = 0, uint32_t ve = 0xffffffffu) {
     if (s->stage != 2) throw_invalid("join: call union_reverse_lists first");
     const uint32_t n = s->n;
     const uint32_t cap_floor = std::max(2 * s->P, 64u), cap_max = offer_cap_max(s);
     if (s->offer_cap == 0) s->offer_cap = std::min(cap_max, std::max(cap_floor, g_offer_cap_hint));
     if (s->ov_cap == 0)
-        s->ov_cap = uint32_t(std::min<uint64_t>(std::max<uint64_t>(1u << 20, n * g_spill_per_point_hint), 1u << 31));
+        s->ov_cap = uint32_t(std::min<uint64_t>(std::max<uint64_t>(1u << 20, n * g_spill_per_point_hint), kMaxSpill));
     const uint32_t rmax = 3 * s->S + s->P;  // |new| <= 2S, |old| <= P + S
     const auto agg_smem = [&](bool u8, uint32_t ol) {
         const size_t rsb = u8 ? ds->ld8 + 16 : size_t(ds->ld + 4) * 4;
@@ -1700,7 +1708,9 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
     const bool agg_f32 = !agg_u8 && agg_smem(false, ol_f32) <= 160 * 1024;
     // visit list: tree-0 leaf order (L2 locality), restricted to owned points
     const uint32_t* order = s->sharded ? s->order_own.p : (s->order.n ? s->order.p : nullptr);
-    const uint32_t n_visit = own_hi(s) - own_lo(s);
+    ve = std::min(ve, own_hi(s) - own_lo(s));
+    if (order) order += vb;
+    const uint32_t n_visit = ve > vb ? ve - vb : 0u;
     DevBuf<unsigned long long> counters(3);  // [comps, unused, offers]
     if (s->ov_count.n != 1) s->ov_count.alloc(1);
     uint32_t spilled = 0;
@@ -1740,8 +1750,14 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
                                                      uint32_t(num_sms()) * std::max(per_sm, 1));
             LAUNCH(join_wide_kernel, grid, kWJW * 32, sm, ja, rmax);
         }
+        unsigned long long offers = 0;
+        CK(cudaMemcpyAsync(&offers, counters.p + 2, 8, cudaMemcpyDeviceToHost, stream()));
         s->ov_count.download(&spilled, 1);
         ssync();
+        // (the offer total bounds the spill count: below 2^31 the 32-bit counter cannot have wrapped)
+        const char* lim_env = getenv("ANNK_JOIN_MAX_OFFERS");  // tests: force the piecewise round at small N
+        const uint64_t lim = lim_env ? std::strtoull(lim_env, nullptr, 10) : kMaxJoinOffers;
+        if (offers >= lim || spilled > kMaxSpill) return false;
         if (spilled <= s->ov_cap) break;
         s->ov_cap = next_pow2(spilled);  // spill list too small: grow and redo (pools untouched so far)
         g_spill_per_point_hint = std::max<uint64_t>(g_spill_per_point_hint, (uint64_t(s->ov_cap) + n - 1) / n);
@@ -1756,6 +1772,7 @@ void join_phase(annk_state* s, const annk_dataset* ds) {
     s->last_spilled = spilled;
     s->pack_hi = s->pack_lo = 0;
     s->stage = 3;
+    return true;
 }
 
 // Groups the spill list by target (stable radix sort) and derives per-target
@@ -1788,19 +1805,26 @@ void group_spills(annk_state* s) {
 }
 
 // Merge of the owned targets' offers into their pools, then `changes`.
-uint64_t merge_phase(annk_state* s) {
-    if (s->stage != 3) throw_invalid("merge: call join first");
-    const uint32_t n = s->n, lo = own_lo(s), hi = own_hi(s);
+// top-P(pool ∪ offers) of the owned targets; merging is associative, so a round
+// may merge the offers of several join pieces one after another.
+void merge_offers(annk_state* s, unsigned long long* scratch) {
+    const uint32_t lo = own_lo(s), hi = own_hi(s);
     group_spills(s);
-    DevBuf<unsigned long long> ch(2);
-    ch.zero();
     MergeArgs ma{hi, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p,
-                 s->ov_off.p, s->ov_key.p, ch.p + 1, lo};
+                 s->ov_off.p, s->ov_key.p, scratch, lo};
     const size_t pw = ((size_t(kPend) + 3 * size_t(s->P)) * 8 + s->P + 15) & ~size_t(15);
     const uint32_t wps = 8;
     if (pw * wps > 48 * 1024)
         CK(cudaFuncSetAttribute(merge_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pw * wps)));
     if (hi > lo) LAUNCH(merge_stream_kernel, (hi - lo + wps - 1) / wps, wps * 32, pw * wps, ma);
+}
+
+uint64_t merge_phase(annk_state* s, bool merged = false) {
+    if (s->stage != 3) throw_invalid("merge: call join first");
+    const uint32_t n = s->n, lo = own_lo(s), hi = own_hi(s);
+    DevBuf<unsigned long long> ch(2);
+    ch.zero();
+    if (!merged) merge_offers(s, ch.p + 1);
     // changes: entries inserted this round that survive (flag bit 1), bit cleared
     const size_t cells = size_t(hi - lo) * s->P;
     if (cells)
@@ -1825,8 +1849,39 @@ uint64_t merge_phase(annk_state* s) {
 }
 
 uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
-    join_phase(s, ds);
-    return merge_phase(s);
+    if (s->join_pieces <= 1 && join_phase(s, ds)) return merge_phase(s);
+    // the round's offers do not fit one launch (very large N): join the visit list
+    // in pieces, merging each piece's offers before the next (pools = top-P of
+    // the start pool and all offers, whatever the grouping)
+    const uint32_t n_visit = own_hi(s) - own_lo(s);
+    if (!s->sharded && !s->order.n) {  // visit list needed for ranges
+        s->order.alloc(s->n);
+        LAUNCH(iota_kernel, (s->n + 255) / 256, 256, 0, s->order.p, 0u, s->n);
+    }
+    uint32_t pieces = std::max(2u, s->join_pieces);
+    uint64_t comps = 0, offers = 0, spilled = 0;
+    DevBuf<unsigned long long> scratch(1);
+    uint32_t pos = 0;
+    while (pos < n_visit) {
+        const uint32_t len = std::max(1u, (n_visit + pieces - 1) / pieces);
+        const uint32_t end = std::min(n_visit, pos + len);
+        if (!join_phase(s, ds, pos, end)) {
+            pieces *= 2;
+            continue;
+        }
+        comps += s->pending_comps;
+        offers += s->last_offers;
+        spilled += s->spilled;
+        merge_offers(s, scratch.p);
+        s->stage = 2;  // next piece joins against the same lists and start-of-round tails
+        pos = end;
+    }
+    s->stage = 3;
+    s->join_pieces = pieces;  // later rounds (more offers) start from here
+    s->pending_comps = comps;
+    s->last_offers = offers;
+    s->last_spilled = spilled;
+    return merge_phase(s, true);
 }
 
 // Owned visit order: tree-0 leaf order restricted to [lo, hi) (or lo..hi-1).
@@ -2018,7 +2073,8 @@ int annk_shard_union(annk_state* s) {
 int annk_shard_join(annk_state* s, const annk_dataset* ds, uint64_t* comps) {
     return abi([&] {
         if (!s || !ds || ds->n != s->n) throw_invalid("join: state/dataset mismatch");
-        join_phase(s, ds);
+        if (!join_phase(s, ds))
+            throw_invalid("join: this shard's offers exceed one launch (2^31 offers); use more ranks");
         if (comps) *comps = s->pending_comps;
     });
 }

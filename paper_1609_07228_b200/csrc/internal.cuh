@@ -109,6 +109,7 @@ struct annk_state {
     uint32_t spilled = 0;
     bool spill_sorted = false;
     uint64_t pending_comps = 0;
+    uint32_t join_pieces = 1;  // visit-list pieces per round (> 1 once a round overflowed one join launch)
     // shard mode (multi-GPU): this state owns points [lo, hi); init / sample /
     // join / merge / finalize touch only those, lists and thresholds of the
     // other points arrive through annk_state_rows

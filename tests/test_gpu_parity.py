@@ -192,6 +192,21 @@ def test_wide_fp32_init_bit_exact(n, dim, trees, leaf, P, seed):
     assert sd.meta()["dist_comps"] == e["dist_comps"]
 
 
+@pytest.mark.parametrize("integer", [True, False])
+def test_piecewise_join_round_bit_exact(integer, monkeypatch):
+    # a round whose offers exceed one join launch (very large N) is joined in pieces
+    # of the visit list, each piece's offers merged before the next: pools, flags and
+    # dist_comps must still equal the oracle's (forced here by a tiny offer limit)
+    x = mixture(6000, 128, 30, 5) if integer else A.gen_synthetic(6000, 24, 5)
+    o, vo, so, sd = _pair(x, 4, 10, 5, 10, 4, 30, 10)
+    monkeypatch.setenv("ANNK_JOIN_MAX_OFFERS", "20000")
+    for it in range(3):
+        so.nn_descent_iteration(vo)
+        A.detail.nn_descent_iteration(sd, x)
+        e = assert_pools_equal(sd, so)
+        assert sd.meta()["dist_comps"] == e["dist_comps"], f"iteration {it}"
+
+
 def test_integer_mixture_refine_and_finalize():
     x = mixture(20000, 128, 40, 3)
     o, vo, so, sd = _pair(x, 4, 10, 3, 10, 4, 30, 10)
