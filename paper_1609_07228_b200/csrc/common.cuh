@@ -316,9 +316,9 @@ __device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[V]) {
     }
 }
 
-__host__ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
+__host__ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {  // saturates at 2^31 (no wrap to 0)
     uint32_t p = 1;
-    while (p < x) p <<= 1;
+    while (p < x && p < 0x80000000u) p <<= 1;
     return p;
 }
 
