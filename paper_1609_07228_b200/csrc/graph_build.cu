@@ -1185,6 +1185,7 @@ struct MergeArgs {
     const uint64_t* ov_key;
     unsigned long long* changes;
     uint32_t lo;    // targets [lo, n) are merged
+    uint32_t* next;  // work counter: warps take targets dynamically (offer counts vary widely)
 };
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t n, uint64_t v) {
@@ -1268,10 +1269,14 @@ __global__ void merge_stream_kernel(MergeArgs a) {
     uint64_t* sp = R + a.P;
     uint64_t* tmp = sp + a.P;
     uint8_t* sflag = reinterpret_cast<uint8_t*>(tmp + a.P);
-    const uint32_t i = a.lo + blockIdx.x * wpb + warp;
+    (void)wpb;
+    for (;;) {
+    uint32_t wi = 0;
+    if (lane == 0) wi = atomicAdd(a.next, 1u);
+    const uint32_t i = a.lo + __shfl_sync(0xffffffffu, wi, 0);
     if (i >= a.n) return;
     const uint32_t total = a.ocnt[i];
-    if (total == 0) return;
+    if (total == 0) continue;
     const uint32_t sz = a.sizes[i];
     uint64_t* pk = a.keys + size_t(i) * a.P;
     uint8_t* pf = a.flags + size_t(i) * a.P;
@@ -1330,6 +1335,8 @@ __global__ void merge_stream_kernel(MergeArgs a) {
     if (lane == 0) {
         a.sizes[i] = r;
         if (added) atomicAdd(a.changes, (unsigned long long)added);
+    }
+    __syncwarp();
     }
 }
 
@@ -1810,13 +1817,18 @@ void group_spills(annk_state* s) {
 void merge_offers(annk_state* s, unsigned long long* scratch) {
     const uint32_t lo = own_lo(s), hi = own_hi(s);
     group_spills(s);
+    DevBuf<uint32_t> next(1);
+    next.zero();
     MergeArgs ma{hi, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p,
-                 s->ov_off.p, s->ov_key.p, scratch, lo};
+                 s->ov_off.p, s->ov_key.p, scratch, lo, next.p};
     const size_t pw = ((size_t(kPend) + 3 * size_t(s->P)) * 8 + s->P + 15) & ~size_t(15);
     const uint32_t wps = 8;
     if (pw * wps > 48 * 1024)
         CK(cudaFuncSetAttribute(merge_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pw * wps)));
-    if (hi > lo) LAUNCH(merge_stream_kernel, (hi - lo + wps - 1) / wps, wps * 32, pw * wps, ma);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_stream_kernel, wps * 32, pw * wps));
+    const uint32_t grid = std::min<uint32_t>((hi - lo + wps - 1) / wps, uint32_t(num_sms()) * std::max(per_sm, 1));
+    if (hi > lo) LAUNCH(merge_stream_kernel, grid, wps * 32, pw * wps, ma);
 }
 
 uint64_t merge_phase(annk_state* s, bool merged = false) {
