@@ -69,6 +69,7 @@ struct SearchArgs {
     const uint8_t* q8;
     const int32_t* qnorms8;
     uint32_t gk_magic;  // floor(2^32 / gk): slot -> (expanded point, column) without a hardware divide
+    uint32_t* qnext;    // query work counter: CTAs take queries dynamically (query costs vary)
 };
 
 struct Smem {
@@ -370,9 +371,19 @@ __device__ void bbf_producer(const SearchArgs& a, Smem& s) {
     const uint32_t lane = threadIdx.x & 31, slot = blockIdx.x;
     HeapEnt* h = a.heaps ? a.heaps + (size_t(slot) * 32 + lane) * a.hcap : s.heap + lane * a.hcap;
     uint32_t k = 0;
-    for (uint32_t qi = blockIdx.x; qi < a.nq; qi += gridDim.x, ++k) {
+    for (;; ++k) {
         const uint32_t b = k & 1;
         if (k >= 2) bar_sync(4 + b, kThreads);
+        uint32_t qi = 0;
+        if (lane == 0) qi = atomicAdd(a.qnext, 1u);
+        qi = __shfl_sync(0xffffffffu, qi, 0);
+        if (qi >= a.nq) {  // no queries left: an end marker in buffer b
+            if (lane == 0) s.lcnt[2 + b] = 0xffffffffu;
+            __threadfence_block();
+            __syncwarp();
+            bar_arrive(2 + b, kThreads);
+            break;
+        }
         const float* q = a.q + size_t(qi) * a.ld;
         uint2* leaves = a.leaves + (size_t(slot) * 2 + b) * a.nt * a.n_node;
         uint32_t tot = 0;
@@ -423,13 +434,18 @@ __device__ void bbf_producer(const SearchArgs& a, Smem& s) {
             tot += cnt;
         }
         tot = __reduce_add_sync(0xffffffffu, tot);
-        if (lane == 0) s.lcnt[b] = tot;
+        if (lane == 0) {
+            s.lcnt[b] = tot;
+            s.lcnt[2 + b] = qi;  // the query these ranges belong to
+        }
         __threadfence_block();
         __syncwarp();
         bar_arrive(2 + b, kThreads);
     }
-    // match the workers' last "buffer read" arrivals so every barrier generation completes
-    for (uint32_t j = k >= 2 ? k - 2 : 0; j < k; ++j) bar_sync(4 + (j & 1), kThreads);
+    // k = the end marker's production; the workers read productions 0..k-1 and
+    // arrived on "buffer read" for each; the production-k step above synced on
+    // generation k-2, so generation k-1 is left to match
+    if (k >= 1) bar_sync(4 + ((k - 1) & 1), kThreads);
 }
 
 template <bool kTree>
@@ -460,8 +476,17 @@ __global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
         bbf_producer(a, s);
         return;
     }
-    uint32_t k = 0;
-    for (uint32_t qi = blockIdx.x; qi < a.nq; qi += gridDim.x, ++k) {
+    for (uint32_t k = 0;; ++k) {
+        uint32_t qi;
+        if (kTree) {
+            bar_sync(2 + (k & 1), kThreads);  // production k (this query's leaf ranges, or the end marker)
+            qi = s.lcnt[2 + (k & 1)];
+        } else {
+            if (tid == 0) s.lcnt[2] = atomicAdd(a.qnext, 1u);
+            wsync<W>();
+            qi = s.lcnt[2];
+        }
+        if (qi >= a.nq) break;
         for (uint32_t j = tid; j < a.ld; j += W) s.q[j] = a.q[size_t(qi) * a.ld + j];
         if (a.x8) {
             for (uint32_t j = tid; j < a.ld8; j += W) s.q8[j] = a.q8[size_t(qi) * a.ld8 + j];
@@ -472,7 +497,6 @@ __global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
         // ------------------------------------------------ seeding
         if (kTree) {
             const uint32_t b = k & 1;
-            bar_sync(2 + b, kThreads);  // this query's leaf ranges are ready
             if (tid == 0) s.ctr[6] = s.lcnt[b];
             // visit every point of every emitted leaf: one thread per (leaf, slot)
             const uint2* leaves = a.leaves + (size_t(slot) * 2 + b) * a.nt * a.n_node;
@@ -742,7 +766,10 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
                  p->random_seed_count, p->seed, seed_cap, sr->bitmap.p, words, vlist.p, vcap, heaps.p, hcap,
                  leaves.p, mt.p, keys.p, st.p, u8 ? base->data8.p : nullptr, u8 ? base->norms8.p : nullptr,
                  base->ld8, u8 ? qds->data8.p : nullptr, u8 ? qds->norms8.p : nullptr,
-                 sr->gk > 1 ? uint32_t((uint64_t(1) << 32) / sr->gk) : 0xffffffffu};
+                 sr->gk > 1 ? uint32_t((uint64_t(1) << 32) / sr->gk) : 0xffffffffu, nullptr};
+    DevBuf<uint32_t> qnext(1);
+    qnext.zero();
+    a.qnext = qnext.p;
     if (p->random_init) LAUNCH(search_kernel<false>, slots, kThreads, smem, a);
     else LAUNCH(search_kernel<true>, slots, kThreads, smem, a);
     const size_t cnt = size_t(nq) * p->k_return;
