@@ -274,15 +274,39 @@ __device__ void init_select(const InitArgs& a, uint32_t i, uint64_t* keys, uint3
             __syncwarp();
         }
     }
-    const uint32_t m = next_pow2(max(ns, 1u));
-    for (uint32_t j = ns + lane; j < m; j += 32) surv[j] = kEmptyKey;
-    __syncwarp();
-    warp_bitonic_sort(surv, m);
     uint64_t* pk = a.keys + size_t(i) * a.P;
     uint8_t* pf = a.flags + size_t(i) * a.P;
-    for (uint32_t j = lane; j < a.P; j += 32) {
-        pk[j] = j < take ? surv[j] : kEmptyKey;
-        pf[j] = j < take ? 1 : 0;
+    __syncwarp();
+    if (ns <= 128) {
+        // the survivors (about P) are sorted in registers and written straight to the pool
+        uint64_t v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t e = uint32_t(r) * 32 + lane;
+            v[r] = e < ns ? surv[e] : kEmptyKey;
+        }
+        warp_sort_regs<4>(v);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t e = uint32_t(r) * 32 + lane;
+            if (e < a.P) {
+                pk[e] = e < take ? v[r] : kEmptyKey;
+                pf[e] = e < take ? 1 : 0;
+            }
+        }
+        for (uint32_t j = 128 + lane; j < a.P; j += 32) {
+            pk[j] = kEmptyKey;
+            pf[j] = 0;
+        }
+    } else {
+        const uint32_t m = next_pow2(max(ns, 1u));
+        for (uint32_t j = ns + lane; j < m; j += 32) surv[j] = kEmptyKey;
+        __syncwarp();
+        warp_bitonic_sort(surv, m);
+        for (uint32_t j = lane; j < a.P; j += 32) {
+            pk[j] = j < take ? surv[j] : kEmptyKey;
+            pf[j] = j < take ? 1 : 0;
+        }
     }
     if (lane == 0) {
         a.sizes[i] = take;
