@@ -316,6 +316,37 @@ __device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[V]) {
     }
 }
 
+// The same network for 32-bit keys.
+template <int V>
+__device__ __forceinline__ void warp_sort_regs_u32(uint32_t (&v)[V]) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (uint32_t k = 2; k <= 32u * V; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int r = 0; r < V; ++r) {
+                    const int rp = r ^ int(j / 32);
+                    if (rp > r) {
+                        const bool up = ((uint32_t(r) * 32 + lane) & k) == 0;
+                        const uint32_t a = v[r], b = v[rp];
+                        if ((a > b) == up) { v[r] = b; v[rp] = a; }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < V; ++r) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+                    const bool up = ((uint32_t(r) * 32 + lane) & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    v[r] = (lower == up) ? min(v[r], o) : max(v[r], o);
+                }
+            }
+        }
+    }
+}
+
 __host__ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {  // saturates at 2^31 (no wrap to 0)
     uint32_t p = 1;
     while (p < x && p < 0x80000000u) p <<= 1;

@@ -59,6 +59,33 @@ __device__ uint32_t warp_sort_unique_u32(uint32_t* s, uint32_t n, uint32_t m) {
     return out;
 }
 
+// Sorted unique ids of s[0..n) (n <= 32 V) written to out; returns the count.
+// Register sort + one ballot compaction per register row (no shared-memory passes).
+template <int V>
+__device__ uint32_t warp_unique_regs_u32(const uint32_t* s, uint32_t n, uint32_t* __restrict__ out) {
+    const uint32_t lane = lane_id(), lt = (1u << lane) - 1u;
+    uint32_t v[V];
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+        const uint32_t e = uint32_t(r) * 32 + lane;
+        v[r] = e < n ? s[e] : 0xffffffffu;
+    }
+    warp_sort_regs_u32<V>(v);
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+        uint32_t prev = __shfl_up_sync(0xffffffffu, v[r], 1);
+        const uint32_t tail = r > 0 ? __shfl_sync(0xffffffffu, v[r > 0 ? r - 1 : 0], 31) : 0u;
+        if (lane == 0) prev = tail;
+        const uint32_t e = uint32_t(r) * 32 + lane;
+        const bool keep = e < n && (e == 0 || prev != v[r]);
+        const uint32_t b = __ballot_sync(0xffffffffu, keep);
+        if (keep) out[cnt + __popc(b & lt)] = v[r];
+        cnt += __popc(b);
+    }
+    return cnt;
+}
+
 // ----------------------------------------------------------------- init
 
 struct InitArgs {
@@ -798,10 +825,21 @@ __global__ void union_kernel(UnionArgs a, uint32_t m_new, uint32_t m_old) {
     if (rom > a.S)
         for (uint32_t j = lane; j < a.S; j += 32) so[co + j] = a.samp[(size_t(i) * 2 + 1) * a.S + j];
     __syncwarp();
-    const uint32_t un = warp_sort_unique_u32(sn, cn + addn, m_new);
-    const uint32_t uo = warp_sort_unique_u32(so, co + addo, m_old);
-    for (uint32_t j = lane; j < un; j += 32) a.gnew[size_t(i) * 2 * a.S + j] = sn[j];
-    for (uint32_t j = lane; j < uo; j += 32) a.gold[size_t(i) * (a.P + a.S) + j] = so[j];
+    uint32_t un, uo;
+    uint32_t* gn = a.gnew + size_t(i) * 2 * a.S;
+    uint32_t* go = a.gold + size_t(i) * (a.P + a.S);
+    if (m_new <= 64) {
+        un = warp_unique_regs_u32<2>(sn, cn + addn, gn);
+    } else {
+        un = warp_sort_unique_u32(sn, cn + addn, m_new);
+        for (uint32_t j = lane; j < un; j += 32) gn[j] = sn[j];
+    }
+    if (m_old <= 128) {
+        uo = warp_unique_regs_u32<4>(so, co + addo, go);
+    } else {
+        uo = warp_sort_unique_u32(so, co + addo, m_old);
+        for (uint32_t j = lane; j < uo; j += 32) go[j] = so[j];
+    }
     if (lane == 0) {
         a.gncnt[i] = un;
         a.gocnt[i] = uo;
