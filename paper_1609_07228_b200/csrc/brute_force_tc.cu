@@ -306,13 +306,11 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                 for (uint32_t t = t0; t < t1; ++t, ++it) {
                     const uint32_t s = it % kStages;
                     mbar_wait_backoff(&empty_bar[s], ((it / kStages) & 1) ^ 1);
-                    const bool full_tile = (t + 1) * kTB <= a.nb;  // partial tile: norms read from global
-                    mbar_expect_tx(&full_bar[s], kTileBytes + (full_tile ? kTB * 8 : 0));
+                    mbar_expect_tx(&full_bar[s], kTileBytes + kTB * 8);
                     tma_load_2d(sB + s * kTileBytes, &tm_base, &full_bar[s], 0, int32_t(t * kTB));
-                    if (full_tile) {
-                        bulk_load(sN + s * kTB * 8, a.bnorm + size_t(t) * kTB, kTB * 4, &full_bar[s]);
-                        bulk_load(sN + s * kTB * 8 + kTB * 4, a.nhalf + size_t(t) * kTB, kTB * 4, &full_bar[s]);
-                    }
+                    // (norm arrays are padded to whole tiles: rows past the end read as sentinels)
+                    bulk_load(sN + s * kTB * 8, a.bnorm + size_t(t) * kTB, kTB * 4, &full_bar[s]);
+                    bulk_load(sN + s * kTB * 8 + kTB * 4, a.nhalf + size_t(t) * kTB, kTB * 4, &full_bar[s]);
                 }
             }
         }
@@ -377,7 +375,6 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
             asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // shares reset for this item
             for (uint32_t t = t0; t < t1; ++t, ++it) {
                 const uint32_t b = it % kAcc, s = it % kStages;
-                const bool full_tile = (t + 1) * kTB <= a.nb;
                 {
                     const uint64_t o = *reinterpret_cast<const volatile uint64_t*>(other_share);
                     if (qvalid && o < thr) {
@@ -388,7 +385,7 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                 }
                 mbar_wait(&tfull_bar[b], (it / kAcc) & 1);
                 tc_fence_after();
-                if (full_tile) mbar_wait(&full_bar[s], (it / kStages) & 1);  // column norms landed
+                mbar_wait(&full_bar[s], (it / kStages) & 1);  // column norms landed
                 const uint32_t taddr = tmem + ((quarter * 32) << 16) + (b * kNQB + h) * kTB;
 #pragma unroll 1
                 for (uint32_t c = half * kChunks; c < (half + 1) * kChunks; ++c) {
@@ -405,16 +402,7 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                     int32_t g[8];
 #pragma unroll
                     for (int gi = 0; gi < 8; ++gi) {
-                        int4 hv;
-                        if (full_tile) {
-                            hv = *reinterpret_cast<const int4*>(rowp + kTB + 4 * gi);
-                        } else {
-                            const uint32_t j = j0 + 4 * gi;
-                            hv.x = j < a.nb ? __ldg(a.nhalf + j) : INT_MIN / 2;
-                            hv.y = j + 1 < a.nb ? __ldg(a.nhalf + j + 1) : INT_MIN / 2;
-                            hv.z = j + 2 < a.nb ? __ldg(a.nhalf + j + 2) : INT_MIN / 2;
-                            hv.w = j + 3 < a.nb ? __ldg(a.nhalf + j + 3) : INT_MIN / 2;
-                        }
+                        const int4 hv = *reinterpret_cast<const int4*>(rowp + kTB + 4 * gi);
                         g[gi] = __viaddmax_s32(int32_t(d[4 * gi]), hv.x,
                                                __viaddmax_s32(int32_t(d[4 * gi + 1]), hv.y,
                                                               __viaddmax_s32(int32_t(d[4 * gi + 2]), hv.z,
@@ -459,15 +447,7 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                         gm &= gm - 1;
                         const uint4 dv = *reinterpret_cast<const uint4*>(st + 4 * gi);
                         const uint32_t jg = j0 + 4 * gi;
-                        int4 bv;
-                        if (full_tile) {
-                            bv = *reinterpret_cast<const int4*>(rowp + 4 * gi);
-                        } else {
-                            bv.x = jg < a.nb ? __ldg(a.bnorm + jg) : INT_MAX / 2;
-                            bv.y = jg + 1 < a.nb ? __ldg(a.bnorm + jg + 1) : INT_MAX / 2;
-                            bv.z = jg + 2 < a.nb ? __ldg(a.bnorm + jg + 2) : INT_MAX / 2;
-                            bv.w = jg + 3 < a.nb ? __ldg(a.bnorm + jg + 3) : INT_MAX / 2;
-                        }
+                        const int4 bv = *reinterpret_cast<const int4*>(rowp + 4 * gi);
                         const int32_t xs[4] = {int32_t(2 * dv.x) - bv.x, int32_t(2 * dv.y) - bv.y,
                                                int32_t(2 * dv.z) - bv.z, int32_t(2 * dv.w) - bv.w};
 #pragma unroll
@@ -502,8 +482,14 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
     }
 }
 
-__global__ void neg_half_kernel(const int32_t* __restrict__ n, uint32_t cnt, int32_t* __restrict__ out) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) out[i] = -(n[i] >> 1);
+// Tile-padded copies of the base norms and of -(norm >> 1); entries past the
+// end hold sentinels (the exact test then rejects them by index).
+__global__ void pad_norms_kernel(const int32_t* __restrict__ n, uint32_t cnt, uint32_t padded,
+                                 int32_t* __restrict__ norms, int32_t* __restrict__ nhalf) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < padded; i += gridDim.x * blockDim.x) {
+        norms[i] = i < cnt ? n[i] : INT_MAX / 2;
+        nhalf[i] = i < cnt ? -(n[i] >> 1) : INT_MIN / 2;
+    }
 }
 
 using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
@@ -558,9 +544,11 @@ bool brute_force_tc(const annk_dataset* base, uint32_t nq, const uint32_t* self_
     const CUtensorMap tq = make_map(q8, nq, kQB);
     DevBuf<uint64_t> cand(size_t(grid) * 2 * kTQ * kCB);
     DevBuf<uint64_t> part(size_t(nq) * splits * 2 * k);  // per (query, split, column half)
-    DevBuf<int32_t> nhalf(nb);
-    LAUNCH(neg_half_kernel, std::min((nb + 255) / 256, 4096u), 256, 0, base->norms8.p, nb, nhalf.p);
-    TcArgs args{base->norms8.p, nhalf.p, nb, qnorm, nq, self_ids, k, splits, tps, n_items, cand.p,
+    const uint32_t padded = n_tiles * kTB;
+    DevBuf<int32_t> norms(padded), nhalf(padded);
+    LAUNCH(pad_norms_kernel, std::min((padded + 255) / 256, 4096u), 256, 0, base->norms8.p, nb, padded, norms.p,
+           nhalf.p);
+    TcArgs args{norms.p, nhalf.p, nb, qnorm, nq, self_ids, k, splits, tps, n_items, cand.p,
                 part.p};
     CK(cudaFuncSetAttribute(bf_tc_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemTC)));
     LAUNCH(bf_tc_u8_kernel, grid, kThreadsTC, kSmemTC, tb, tq, args);
