@@ -491,35 +491,42 @@ def run_gpu(args, cfg, ws, rank, local):
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     dsinfo = vs.info()
     row_bytes = dsinfo["row_bytes"]  # bytes per row actually gathered (u8 rows on the exact u8 path)
-    dom = max(prof.items(), key=lambda kv: kv[1][1])
-    dom_name, (dom_cnt, dom_ms) = dom
-    if dom_name.startswith("join"):
-        rows_per_launch = sum(join_rows[:crossing]) / crossing
-        alg_bytes = rows_per_launch * (row_bytes + 4) + n * 8
-        unit_desc = (f"per launch: sum_i(|new_i|+|old_i|) list rows x ({row_bytes} B row + 4 B id) + N x 8 B "
-                     "thresholds (each list member's row gathered once per point)")
-    elif dom_name == "init_kernel":
-        alg_bytes = comps[0] * (row_bytes + 4) + n * cfg["P"] * 9
-        unit_desc = (f"per launch: init dist_comps x ({row_bytes} B candidate row + 4 B id) + N x P x 9 B "
-                     "pool writes")
-    else:
-        alg_bytes = None
-        unit_desc = "n/a"
-    per_launch_s = dom_ms / dom_cnt / 1e3
-    achieved = alg_bytes / per_launch_s / 1e9 if alg_bytes else None
-    traffic = None
-    try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            tr = json.load(fh).get(args.config, {}).get(dom_name)
-            traffic = tr["dram_bytes_per_launch"] if tr else None
-    except Exception:
-        pass
-    roofline = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+    def kernel_roofline(name):
+        """HBM roofline of one build kernel: algorithmic bytes per launch / its mean launch time."""
+        cnt, ms = prof[name]
+        if name.startswith("join"):
+            rows_per_launch = sum(join_rows[:crossing]) / crossing
+            alg_bytes = rows_per_launch * (row_bytes + 4) + n * 8
+            unit_desc = (f"per launch: sum_i(|new_i|+|old_i|) list rows x ({row_bytes} B row + 4 B id) + N x 8 B "
+                         "thresholds (each list member's row gathered once per point)")
+        elif name == "init_kernel":
+            alg_bytes = comps[0] * (row_bytes + 4) + n * cfg["P"] * 9
+            unit_desc = (f"per launch: init dist_comps x ({row_bytes} B candidate row + 4 B id) + N x P x 9 B "
+                         "pool writes")
+        else:
+            alg_bytes = None
+            unit_desc = "n/a"
+        per_launch_s = ms / cnt / 1e3
+        achieved = alg_bytes / per_launch_s / 1e9 if alg_bytes else None
+        traffic = None
+        try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                tr = json.load(fh).get(args.config, {}).get(name)
+                traffic = tr["dram_bytes_per_launch"] if tr else None
+        except Exception:
+            pass
+        return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
                 "per_launch_ms": per_launch_s * 1e3,
-                "share_of_step": dom_ms / sum(v[1] for v in prof.values()), "units": unit_desc,
+                "share_of_step": ms / sum(v[1] for v in prof.values()), "units": unit_desc,
                 "exact_u8_path": dsinfo["u8"]}
+
+    dom_name = max(prof.items(), key=lambda kv: kv[1][1])[0]
+    roofline = kernel_roofline(dom_name)
+    # the other gather kernels of the step, same model (the dominant one can change between builds)
+    roofline_others = {nm: kernel_roofline(nm) for nm in prof
+                       if nm != dom_name and (nm == "init_kernel" or nm.startswith("join"))}
 
     _log("exact kNN")
     # cfg4: exact kNN graph (self-mode top-k over all N points) on the tcgen05 kernel
@@ -582,6 +589,7 @@ def run_gpu(args, cfg, ws, rank, local):
                                               "D2H graph ids+dists"},
         "gpu_launches": int(launches),
         "roofline": roofline,
+        "roofline_other_kernels": roofline_others,
         "cpu_baseline": cpu,
         "clocks": clocks,
         "search_qps_at_recall_0.9": chosen["qps"] if chosen else None,
