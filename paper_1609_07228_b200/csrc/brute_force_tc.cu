@@ -201,7 +201,8 @@ struct Cut {
 // Cut a full candidate list (cnt > k keys) back to the keys whose distance is
 // at most T = its k-th smallest distance (ties kept, so at least k remain; the
 // list stays unsorted).  T is found by a warp-wide binary search on the integer
-// distance (< 2^24 on the u8 datapath): 24 rounds of count(d <= mid) with one
+// distance (< 2^24 on the u8 datapath) between the list's min and max: at most
+// 24 rounds (about log2 of the span) of count(d <= mid) with one
 // REDUX each — a fraction of a full sort's work.  The new filter bound is
 // (T, max id): any later key with a larger distance cannot reach the top k.
 __device__ __noinline__ Cut flush_buffer(uint64_t* b, uint32_t cnt, uint32_t k, uint32_t lane) {
@@ -214,7 +215,18 @@ __device__ __noinline__ Cut flush_buffer(uint64_t* b, uint32_t cnt, uint32_t k, 
         v[r] = e < cnt ? b[e] : kEmptyKey;
         dv[r] = e < cnt ? uint32_t(key_dist(v[r])) : 0xffffffffu;
     }
-    uint32_t lo = 0, hi = (1u << 24) - 1;  // smallest T with #{d <= T} >= k lies in [lo, hi]
+    // smallest T with #{d <= T} >= k lies in [min d, max d] of the list (cnt > k):
+    // the list's own span is far narrower than 2^24 once it has converged
+    uint32_t mn = 0xffffffffu, mx = 0;
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+        const uint32_t e = uint32_t(r) * 32 + lane;
+        if (e < cnt) {
+            mn = min(mn, dv[r]);
+            mx = max(mx, dv[r]);
+        }
+    }
+    uint32_t lo = __reduce_min_sync(0xffffffffu, mn), hi = __reduce_max_sync(0xffffffffu, mx);
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         uint32_t c = 0;
