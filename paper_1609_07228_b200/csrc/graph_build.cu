@@ -451,10 +451,13 @@ __host__ __device__ __forceinline__ size_t init_warp_bytes(uint32_t cap, uint32_
             (ld ? size_t(32) * (kStageCols + 4) * 4 : 0) + 15) & ~size_t(15);
 }
 
-// 5 CTAs per SM: 96 registers (no spills) lift residency from 16 to 20 warps,
-// which the shared-memory scratch also allows (measured: 34.9 -> 31.8 ms at
-// cfg2; 6 CTAs force spills and run slower, 45.8 ms)
-__global__ void __launch_bounds__(kInitWarps * 32, 5) init_kernel(InitArgs a, uint32_t sib_cap,
+// u8 datapath: 5 CTAs per SM — 96 registers (no spills) lift residency from 16
+// to 20 warps, which the shared-memory scratch also allows (measured: 34.9 ->
+// 31.8 ms at cfg2; 6 CTAs force spills and run slower, 45.8 ms).  The fp32
+// path's staging scratch limits residency anyway and the cap slows it (cfg3
+// init 0.56 -> 0.70 s), so it is instantiated without one.
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kInitWarps * 32, kMinBlocks) init_kernel_t(InitArgs a, uint32_t sib_cap,
                                                                const uint32_t* __restrict__ order,
                                                                uint32_t n_visit) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -2038,9 +2041,13 @@ annk_state* init_graph_impl(const annk_dataset* ds, const annk_forest* fc, uint3
     const uint32_t sib_cap = 0;  // sibling lists come from the forest (sib_list)
     const size_t per_warp = init_warp_bytes(kInitCap, ds->u8 ? 0u : ds->ld, sib_cap);
     const size_t smem = per_warp * kInitWarps;
-    CK(cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    void (*init_kernel)(InitArgs, uint32_t, const uint32_t*, uint32_t) =
+        ds->u8 ? init_kernel_t<5> : init_kernel_t<1>;
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(init_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smem)));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, init_kernel, kInitWarps * 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(init_kernel),
+                                                      kInitWarps * 32, smem));
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((n_visit + kInitWarps - 1) / kInitWarps,
                                                                     uint32_t(num_sms()) * std::max(per_sm, 1)));
     s->sizes.zero();  // points outside the shard keep empty pools
