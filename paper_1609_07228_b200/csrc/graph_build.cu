@@ -1762,7 +1762,9 @@ uint64_t g_spill_per_point_hint = 8;
 // and the spill list is capped (kMaxSpill entries, 12 bytes each); a visit range
 // that would exceed either is refused (returns false, pools untouched) and the
 // caller joins it in smaller pieces.
-constexpr uint64_t kMaxJoinOffers = 1ull << 31;
+// (spill reservations <= offers, so below 2^32 offers the 32-bit counter cannot
+// wrap; at 2^31 the cfg3 rounds were refused and re-joined in pieces, 2.0 -> 2.5 s)
+constexpr uint64_t kMaxJoinOffers = 1ull << 32;
 constexpr uint32_t kMaxSpill = 1u << 28;
 
 bool join_phase(annk_state* s, const annk_dataset* ds, uint32_t vb = 0, uint32_t ve = 0xffffffffu) {
@@ -1829,7 +1831,7 @@ bool join_phase(annk_state* s, const annk_dataset* ds, uint32_t vb = 0, uint32_t
         CK(cudaMemcpyAsync(&offers, counters.p + 2, 8, cudaMemcpyDeviceToHost, stream()));
         s->ov_count.download(&spilled, 1);
         ssync();
-        // (the offer total bounds the spill count: below 2^31 the 32-bit counter cannot have wrapped)
+        // (the offer total bounds the spill count: below 2^32 the 32-bit counter cannot have wrapped)
         const char* lim_env = getenv("ANNK_JOIN_MAX_OFFERS");  // tests: force the piecewise round at small N
         const uint64_t lim = lim_env ? std::strtoull(lim_env, nullptr, 10) : kMaxJoinOffers;
         if (offers >= lim || spilled > kMaxSpill) return false;
