@@ -152,9 +152,9 @@ int annk_state_export(const annk_state* s, uint32_t* sizes, uint32_t* ids, float
  * 3 g_rold), CSR: offsets n+1 (always), data nullable. */
 int annk_state_lists(const annk_state* s, int which, uint32_t* offsets, uint32_t* data);
 /* graph_build.cpp:105-162 detail::nn_descent_iteration.  *changes receives
- * this library's deterministic count (entries inserted this round that
- * survive in the pools) — see DESIGN.md on why the reference's count is
- * order-dependent. */
+ * the reference's single-worker count: offers its pools accept in its
+ * sequential order (point ascending, then pair order), including entries a
+ * later offer of the same round evicts again. */
 int annk_nn_descent_iteration(annk_state* s, const annk_dataset* ds, uint64_t* changes);
 /* graph_build.cpp:59-86 and :88-103 (the two halves of the sampling step). */
 int annk_rebuild_sample_lists(annk_state* s);
@@ -184,13 +184,18 @@ int annk_state_stats(const annk_state* s, uint64_t* out4);
  *   all-gather               annk_state_rows(FNEW, CNEW, FOLD, COLD, THR) rows
  *   annk_shard_union         reverse lists from all forward lists, union
  *                            (graph_build.cpp:88-103; same RNG streams on every rank)
- *   annk_shard_join          local join of owned points; offers to any target
+ *   annk_shard_join          local join of owned points; offers to any target,
+ *                            each tagged with its source point
  *   all-to-all               annk_shard_offers_count/pack per destination range,
  *                            annk_shard_offers_add on the receiver
- *   annk_shard_merge         top-P(start U offers) of the owned pools
- * The pools equal the single-GPU ones: the merge is order-independent
- * (graph_build.cpp:105-162 reads only the snapshot lists).  Buffers passed to
- * the row / offer calls may be host or device pointers (UVA copies). */
+ *   annk_shard_merge         the owned pools replay their offers in the
+ *                            reference's order (source point ascending, then
+ *                            the source's pair order; graph_build.cpp:129-156)
+ * The pools, flags and `changes` equal the single-GPU ones and the reference's.
+ * A round too large for one join launch runs in global source ranges, in
+ * ascending order: annk_shard_join_range + exchange + annk_shard_merge_piece
+ * per range, then annk_shard_finish_round.  Buffers passed to the row / offer
+ * calls may be host or device pointers (UVA copies). */
 #define ANNK_ROWS_FNEW 0 /* n x sample_cap u32: sampled new ids (pool order) */
 #define ANNK_ROWS_CNEW 1 /* n u32 */
 #define ANNK_ROWS_FOLD 2 /* n x pool_cap u32: sampled old ids */
@@ -206,14 +211,23 @@ int annk_state_rows(annk_state* s, int which, int put, uint32_t lo, uint32_t hi,
 int annk_shard_sample(annk_state* s);
 int annk_shard_union(annk_state* s);
 int annk_shard_join(annk_state* s, const annk_dataset* ds, uint64_t* comps);
+/* Join of the owned sources in [ilo, ihi).  *ok = 0 when the range's offers
+ * exceed one launch (nothing is kept; *offers reports how many there were). */
+int annk_shard_join_range(annk_state* s, const annk_dataset* ds, uint32_t ilo, uint32_t ihi, uint64_t* comps,
+                          uint64_t* offers, uint32_t* ok);
 /* Offers held for targets [lo, hi): total count; then pack them target-major
- * (counts: hi - lo u32, keys: total u64). */
+ * (counts: hi - lo u32, keys: total u64, srcs: total u32 source points). */
 int annk_shard_offers_count(annk_state* s, uint32_t lo, uint32_t hi, uint64_t* total);
-int annk_shard_offers_pack(annk_state* s, uint32_t lo, uint32_t hi, uint32_t* counts, uint64_t* keys);
+int annk_shard_offers_pack(annk_state* s, uint32_t lo, uint32_t hi, uint32_t* counts, uint64_t* keys,
+                           uint32_t* srcs);
 /* Adds received offers for owned targets [lo, hi) (same packed layout). */
 int annk_shard_offers_add(annk_state* s, uint32_t lo, uint32_t hi, const uint32_t* counts,
-                          const uint64_t* keys);
+                          const uint64_t* keys, const uint32_t* srcs);
 int annk_shard_merge(annk_state* s, uint64_t* changes);
+/* Pieces of a round joined in source ranges: replay one piece's offers, then
+ * close the round (the changes returned by finish are the round's total). */
+int annk_shard_merge_piece(annk_state* s, uint64_t* changes);
+int annk_shard_finish_round(annk_state* s, uint64_t* changes);
 
 /* --------------------------------------------------------------- search */
 /* search.cpp:23-35 GraphSearcher(base, forest, graph): validates the graph

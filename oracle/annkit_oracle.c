@@ -183,7 +183,7 @@ static void parallel_for(uint32_t n, uint32_t workers, range_fn fn, void* ctx) {
 typedef struct {
     uint32_t id;
     float dist;
-    uint8_t flag_new, checked, fresh; /* fresh: inserted during the current shard merge */
+    uint8_t flag_new, checked;
 } entry;
 typedef struct {
     uint32_t cap, size;
@@ -199,7 +199,7 @@ static void pool_init(pool* p, uint32_t cap) {
     p->e = xmalloc(sizeof(entry) * (cap + 1));
 }
 static int pool_insert(pool* p, uint32_t id, float dist, int flag_new) {
-    const entry x = {id, dist, (uint8_t)(flag_new ? 1 : 0), 0, 1};
+    const entry x = {id, dist, (uint8_t)(flag_new ? 1 : 0), 0};
     uint32_t lo = 0, hi = p->size;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) / 2;
@@ -938,22 +938,25 @@ void ora_shard_union(void* p, const uint32_t* fnew, const uint32_t* cnew, const 
     ora_union_reverse_lists(s);
 }
 
-/* Offers produced by the join of the owned points (target, key). */
+/* Offers produced by the join of the owned points (target, key, source). */
 typedef struct {
     uint32_t* tgt;
     uint64_t* key;
+    uint32_t* src;
     size_t n, cap;
 } offer_list;
 static __thread offer_list g_offers;
-static void offer_push(uint32_t tgt, uint64_t key) {
+static void offer_push(uint32_t tgt, uint64_t key, uint32_t src) {
     if (g_offers.n == g_offers.cap) {
         g_offers.cap = g_offers.cap ? g_offers.cap * 2 : 1024;
         g_offers.tgt = realloc(g_offers.tgt, sizeof(uint32_t) * g_offers.cap);
         g_offers.key = realloc(g_offers.key, sizeof(uint64_t) * g_offers.cap);
-        if (!g_offers.tgt || !g_offers.key) abort();
+        g_offers.src = realloc(g_offers.src, sizeof(uint32_t) * g_offers.cap);
+        if (!g_offers.tgt || !g_offers.key || !g_offers.src) abort();
     }
     g_offers.tgt[g_offers.n] = tgt;
     g_offers.key[g_offers.n] = key;
+    g_offers.src[g_offers.n] = src;
     ++g_offers.n;
 }
 static uint64_t make_key_f(float d, uint32_t id) {
@@ -962,9 +965,10 @@ static uint64_t make_key_f(float d, uint32_t id) {
     return ((uint64_t)b << 32) | id;
 }
 
-/* graph_build.cpp:105-162 join for i in [lo, hi); offers that beat the
- * target's start tail thr[target] are kept (the rest cannot enter its pool).
- * Returns the distance count; the offers stay in a thread-local list. */
+/* graph_build.cpp:105-162 join for i in [lo, hi), offers in the reference's
+ * sequential order; offers that beat the target's start tail thr[target] are
+ * kept (the rest cannot enter its pool at any point of the round).  Returns
+ * the distance count; the offers stay in a thread-local list. */
 uint64_t ora_shard_join(void* p, void* vsp, uint32_t lo, uint32_t hi, const uint64_t* thr, uint64_t* n_offers) {
     rstate* s = p;
     const vset* vs = vsp;
@@ -981,8 +985,8 @@ uint64_t ora_shard_join(void* p, void* vsp, uint32_t lo, uint32_t hi, const uint
                 const float d = l2(jr, row(vs, k2), vs->dim);
                 ++comps;
                 if (j != k2) {
-                    if (make_key_f(d, k2) < thr[j]) offer_push(j, make_key_f(d, k2));
-                    if (make_key_f(d, j) < thr[k2]) offer_push(k2, make_key_f(d, j));
+                    if (make_key_f(d, k2) < thr[j]) offer_push(j, make_key_f(d, k2), i);
+                    if (make_key_f(d, j) < thr[k2]) offer_push(k2, make_key_f(d, j), i);
                 }
             }
             for (uint32_t b = 0; b < od->n; ++b) {
@@ -990,8 +994,8 @@ uint64_t ora_shard_join(void* p, void* vsp, uint32_t lo, uint32_t hi, const uint
                 if (l == j) continue;
                 const float d = l2(jr, row(vs, l), vs->dim);
                 ++comps;
-                if (make_key_f(d, l) < thr[j]) offer_push(j, make_key_f(d, l));
-                if (make_key_f(d, j) < thr[l]) offer_push(l, make_key_f(d, j));
+                if (make_key_f(d, l) < thr[j]) offer_push(j, make_key_f(d, l), i);
+                if (make_key_f(d, j) < thr[l]) offer_push(l, make_key_f(d, j), i);
             }
         }
     }
@@ -999,32 +1003,54 @@ uint64_t ora_shard_join(void* p, void* vsp, uint32_t lo, uint32_t hi, const uint
     *n_offers = g_offers.n;
     return comps;
 }
-void ora_shard_offers_get(uint32_t* tgt, uint64_t* key) {
+void ora_shard_offers_get(uint32_t* tgt, uint64_t* key, uint32_t* src) {
     memcpy(tgt, g_offers.tgt, sizeof(uint32_t) * g_offers.n);
     memcpy(key, g_offers.key, sizeof(uint64_t) * g_offers.n);
+    memcpy(src, g_offers.src, sizeof(uint32_t) * g_offers.n);
 }
 
-/* Inserts offers (all for owned targets) into their pools with flag new; the
- * return value counts inserted entries that survive (the device's `changes`). */
-uint64_t ora_shard_merge(void* p, uint32_t lo, uint32_t hi, const uint32_t* tgt, const uint64_t* key, size_t m) {
+typedef struct {
+    uint32_t tgt, src;
+    size_t idx;
+} offer_ord;
+static int offer_ord_cmp(const void* pa, const void* pb) {
+    const offer_ord* a = pa;
+    const offer_ord* b = pb;
+    if (a->tgt != b->tgt) return a->tgt < b->tgt ? -1 : 1;
+    if (a->src != b->src) return a->src < b->src ? -1 : 1;
+    return a->idx < b->idx ? -1 : (a->idx > b->idx);
+}
+
+/* Inserts offers (all for owned targets) into their pools with flag new, per
+ * target in the reference's sequential order: source point ascending, and a
+ * source's offers in the order given (its pair order).  Returns the accepted
+ * inserts — the reference's `changes` contribution. */
+uint64_t ora_shard_replay(void* p, const uint32_t* tgt, const uint64_t* key, const uint32_t* src, size_t m) {
     rstate* s = p;
-    for (uint32_t i = lo; i < hi; ++i)
-        for (uint32_t j = 0; j < s->pools[i].size; ++j) s->pools[i].e[j].fresh = 0;
+    offer_ord* ord = xmalloc(sizeof(offer_ord) * (m ? m : 1));
     for (size_t r = 0; r < m; ++r) {
+        ord[r].tgt = tgt[r];
+        ord[r].src = src[r];
+        ord[r].idx = r;
+    }
+    qsort(ord, m, sizeof(offer_ord), offer_ord_cmp);
+    uint64_t changes = 0;
+    for (size_t q = 0; q < m; ++q) {
+        const size_t r = ord[q].idx;
         float d;
         const uint32_t b = (uint32_t)(key[r] >> 32);
         memcpy(&d, &b, 4);
-        pool_insert(&s->pools[tgt[r]], (uint32_t)key[r], d, 1);
+        changes += pool_insert(&s->pools[tgt[r]], (uint32_t)key[r], d, 1);
     }
-    uint64_t changes = 0;
-    for (uint32_t i = lo; i < hi; ++i)
-        for (uint32_t j = 0; j < s->pools[i].size; ++j) {
-            changes += s->pools[i].e[j].fresh;
-            s->pools[i].e[j].fresh = 0;
-        }
+    free(ord);
+    return changes;
+}
+
+/* Ends a sharded round (the replayed pieces' changes summed by the caller). */
+void ora_shard_finish(void* p, uint64_t changes) {
+    rstate* s = p;
     ++s->iteration;
     s->last_changes = changes;
-    return changes;
 }
 
 /* graph_build.cpp:105-162 nn_descent_iteration, single-worker order. */

@@ -119,9 +119,10 @@ class OracleLib:
             L.ora_shard_union.argtypes = [_vp, _u32p, _u32p, _u32p, _u32p]
             L.ora_shard_join.restype = _u64
             L.ora_shard_join.argtypes = [_vp, _vp, _u32, _u32, _u64p, C.POINTER(_u64)]
-            L.ora_shard_offers_get.argtypes = [_u32p, _u64p]
-            L.ora_shard_merge.restype = _u64
-            L.ora_shard_merge.argtypes = [_vp, _u32, _u32, _u32p, _u64p, C.c_size_t]
+            L.ora_shard_offers_get.argtypes = [_u32p, _u64p, _u32p]
+            L.ora_shard_replay.restype = _u64
+            L.ora_shard_replay.argtypes = [_vp, _u32p, _u64p, _u32p, C.c_size_t]
+            L.ora_shard_finish.argtypes = [_vp, _u64]
         L.ora_union_reverse_lists.argtypes = [_vp]
         L.ora_refine_nn_descent.argtypes = [_vp, _vp, _u32, _u32, C.c_double]
         L.ora_finalize.argtypes = [_vp, _vp, _u32, _u32p, _f32p]
@@ -364,13 +365,20 @@ class State:
         comps = int(self.lib.L.ora_shard_join(self.h, vs.h, lo, hi, thr, C.byref(m)))
         tgt = np.empty(max(m.value, 1), np.uint32)
         key = np.empty(max(m.value, 1), np.uint64)
-        self.lib.L.ora_shard_offers_get(tgt, key)
-        return comps, tgt[:m.value], key[:m.value]
+        src = np.empty(max(m.value, 1), np.uint32)
+        self.lib.L.ora_shard_offers_get(tgt, key, src)
+        return comps, tgt[:m.value], key[:m.value], src[:m.value]
 
-    def shard_merge(self, lo, hi, tgt, key):
+    def shard_replay(self, tgt, key, src):
+        """Offers replayed into their pools in the reference's order (source
+        point ascending, a source's offers as given); returns accepted inserts."""
         tgt = np.ascontiguousarray(tgt, np.uint32)
         key = np.ascontiguousarray(key, np.uint64)
-        return int(self.lib.L.ora_shard_merge(self.h, lo, hi, tgt, key, tgt.size))
+        src = np.ascontiguousarray(src, np.uint32)
+        return int(self.lib.L.ora_shard_replay(self.h, tgt, key, src, tgt.size))
+
+    def shard_finish(self, changes):
+        self.lib.L.ora_shard_finish(self.h, int(changes))
 
     def union_reverse_lists(self):
         self.lib.L.ora_union_reverse_lists(self.h)

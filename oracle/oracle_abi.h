@@ -91,8 +91,9 @@ void ora_shard_sample(void* s, uint32_t lo, uint32_t hi, uint32_t* fnew, uint32_
 void ora_shard_union(void* s, const uint32_t* fnew, const uint32_t* cnew, const uint32_t* fold,
                      const uint32_t* cold);
 uint64_t ora_shard_join(void* s, void* vs, uint32_t lo, uint32_t hi, const uint64_t* thr, uint64_t* n_offers);
-void ora_shard_offers_get(uint32_t* tgt, uint64_t* key);
-uint64_t ora_shard_merge(void* s, uint32_t lo, uint32_t hi, const uint32_t* tgt, const uint64_t* key, size_t m);
+void ora_shard_offers_get(uint32_t* tgt, uint64_t* key, uint32_t* src);
+uint64_t ora_shard_replay(void* s, const uint32_t* tgt, const uint64_t* key, const uint32_t* src, size_t m);
+void ora_shard_finish(void* s, uint64_t changes);
 void ora_union_reverse_lists(void* s);
 int ora_refine_nn_descent(void* s, void* vs, uint32_t max_iters, uint32_t workers,
                           double min_change_rate);

@@ -107,9 +107,12 @@ _SIGS = {
     "annk_shard_union": [_vp],
     "annk_shard_join": [_vp, _vp, C.POINTER(_u64)],
     "annk_shard_offers_count": [_vp, _u32, _u32, C.POINTER(_u64)],
-    "annk_shard_offers_pack": [_vp, _u32, _u32, _vp, _vp],
-    "annk_shard_offers_add": [_vp, _u32, _u32, _vp, _vp],
+    "annk_shard_join_range": [_vp, _vp, _u32, _u32, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u32)],
+    "annk_shard_offers_pack": [_vp, _u32, _u32, _vp, _vp, _vp],
+    "annk_shard_offers_add": [_vp, _u32, _u32, _vp, _vp, _vp],
     "annk_shard_merge": [_vp, C.POINTER(_u64)],
+    "annk_shard_merge_piece": [_vp, C.POINTER(_u64)],
+    "annk_shard_finish_round": [_vp, C.POINTER(_u64)],
     "annk_searcher_create": [_vp, _vp, _u32p, _u32, _u32, _pp],
     "annk_searcher_destroy": [_vp],
     "annk_search": [_vp, _f32p, _u32, _u32, C.POINTER(SearchParamsC), _u32p, _f32p, _vp],

@@ -25,9 +25,12 @@
 #include <cstdlib>
 #include <climits>
 #include <numeric>
+#include <string>
+#include <vector>
 
 #include "../../include/annkit_b200.h"
 #include "internal.cuh"
+#include "join.cuh"
 
 namespace annk {
 namespace {
@@ -853,583 +856,6 @@ __global__ void union_kernel(UnionArgs a, uint32_t m_new, uint32_t m_old) {
     }
 }
 
-// ------------------------------------------------------------------ join
-
-struct JoinArgs {
-    const float* x;
-    uint32_t n, ld, P, S, cap;
-    const uint32_t *gnew, *gold, *gncnt, *gocnt;
-    const uint64_t* thr;
-    uint32_t* ocnt;
-    uint64_t* obuf;
-    unsigned long long* comps;
-    // spill list for targets whose fixed slots are full (hub points)
-    uint32_t* ov_cnt;
-    uint32_t* ov_tgt;
-    uint64_t* ov_key;
-    uint32_t ov_cap;
-    unsigned long long* offers;  // total accepted offers (stats)
-    const uint32_t* order;       // visit list of n points (nullptr: 0..n-1)
-};
-
-// Aggregated join (both datapaths), one CTA per point.  The point's list rows
-// (new first, then old) are staged in shared memory with a padded stride; the
-// needed pairs are {(x, y): x < |new|, x < y < |list|} — new x new upper
-// triangle plus new x old.  Work item = (group of 4 new rows, 32 partner
-// columns after the group's first row): each lane owns one partner column and
-// accumulates 4 exact distances from broadcast row reads.
-// accepted offers are first collected in shared memory tagged with the list
-// member they go to (every offer of point i's join targets one of i's list
-// members), then flushed with ONE global atomic per member to reserve a
-// contiguous range in that member's offer slots (or the spill list).  This
-// cuts global atomics from one per offer to one per (point, member).
-constexpr uint32_t kJoinThreads = 256;
-constexpr uint32_t kJoinXR = 4;  // new rows per work item
-constexpr uint32_t kJoinPerRound = (kJoinThreads / 32) * 32 * kJoinXR * 2;  // max offers per round
-
-template <bool U8>
-__global__ void __launch_bounds__(kJoinThreads)
-join_agg_kernel(JoinArgs a, const uint8_t* __restrict__ x8, uint32_t ld8, const int32_t* __restrict__ norms,
-                const uint32_t* __restrict__ order, uint32_t rmax, uint32_t ol) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t ocount;
-    const uint32_t rsb = U8 ? (ld8 + 16) : (a.ld + 4) * 4;  // padded row stride in bytes
-    unsigned char* rows = smem;
-    uint64_t* thr_s = reinterpret_cast<uint64_t*>(rows + size_t(rmax) * rsb);
-    uint64_t* okey = thr_s + rmax;
-    uint32_t* ids = reinterpret_cast<uint32_t*>(okey + ol);
-    int32_t* nrm = reinterpret_cast<int32_t*>(ids + rmax);
-    uint32_t* mcnt = reinterpret_cast<uint32_t*>(nrm + rmax);
-    uint32_t* mbase = mcnt + rmax;
-    uint32_t* mfix = mbase + rmax;
-    uint32_t* msp = mfix + rmax;
-    uint32_t* gstart = msp + rmax;
-    uint16_t* omem = reinterpret_cast<uint16_t*>(gstart + rmax / 4 + 2);
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr uint32_t kWarps = kJoinThreads / 32;
-    unsigned long long comps = 0;
-    for (uint32_t ord = blockIdx.x;; ord += gridDim.x) {
-        if (ord >= a.n) break;
-        const uint32_t i = order ? order[ord] : ord;
-        const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
-        if (A == 0) continue;
-        const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
-        const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
-        for (uint32_t r = tid; r < R; r += kJoinThreads) {
-            const uint32_t id = r < A ? nw[r] : od[r - A];
-            ids[r] = id;
-            thr_s[r] = a.thr[id];
-            if (U8) nrm[r] = norms[id];
-        }
-        if (tid == 0) {
-            uint32_t acc = 0;
-            const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
-            for (uint32_t g = 0; g < ng; ++g) {
-                gstart[g] = acc;
-                const uint32_t y0 = g * kJoinXR + 1;
-                acc += R > y0 ? (R - y0 + 31) / 32 : 0;
-            }
-            gstart[ng] = acc;
-            ocount = 0;
-        }
-        __syncthreads();
-        if (U8) {
-            const uint32_t v16 = ld8 / 16;
-            for (uint32_t j = tid; j < R * v16; j += kJoinThreads) {
-                const uint32_t r = j / v16, c = (j % v16) * 16;
-                *reinterpret_cast<uint4*>(rows + size_t(r) * rsb + c) =
-                    __ldg(reinterpret_cast<const uint4*>(x8 + size_t(ids[r]) * ld8 + c));
-            }
-        } else {
-            const uint32_t v4 = a.ld / 4;
-            for (uint32_t j = tid; j < R * v4; j += kJoinThreads) {
-                const uint32_t r = j / v4, c = (j % v4) * 4;
-                *reinterpret_cast<float4*>(rows + size_t(r) * rsb + size_t(c) * 4) =
-                    __ldg(reinterpret_cast<const float4*>(a.x + size_t(ids[r]) * a.ld + c));
-            }
-        }
-        __syncthreads();
-        const uint32_t ng = (A + kJoinXR - 1) / kJoinXR;
-        const uint32_t n_items = gstart[ng];
-        for (uint32_t rb = 0; rb < n_items; rb += kWarps) {
-            const uint32_t item = rb + warp;
-            if (item < n_items) {
-                uint32_t g = 0;
-                while (gstart[g + 1] <= item) ++g;
-                const uint32_t x0 = g * kJoinXR;
-                const uint32_t y = x0 + 1 + (item - gstart[g]) * 32 + lane;
-                const bool yv = y < R;
-                const unsigned char* yr = rows + size_t(yv ? y : 0) * rsb;
-                const unsigned char* xr[kJoinXR];
-#pragma unroll
-                for (uint32_t k = 0; k < kJoinXR; ++k) xr[k] = rows + size_t(min(x0 + k, R - 1)) * rsb;
-                float dist[kJoinXR];
-                if (U8) {
-                    uint32_t dot[kJoinXR];
-#pragma unroll
-                    for (uint32_t k = 0; k < kJoinXR; ++k) dot[k] = 0;
-                    for (uint32_t c = 0; c < ld8; c += 16) {
-                        const uint4 b = *reinterpret_cast<const uint4*>(yr + c);
-#pragma unroll
-                        for (uint32_t k = 0; k < kJoinXR; ++k) {
-                            const uint4 x = *reinterpret_cast<const uint4*>(xr[k] + c);
-                            dot[k] = __dp4a(x.x, b.x, dot[k]);
-                            dot[k] = __dp4a(x.y, b.y, dot[k]);
-                            dot[k] = __dp4a(x.z, b.z, dot[k]);
-                            dot[k] = __dp4a(x.w, b.w, dot[k]);
-                        }
-                    }
-                    const int32_t ny = nrm[yv ? y : 0];
-#pragma unroll
-                    for (uint32_t k = 0; k < kJoinXR; ++k)
-                        dist[k] = float(nrm[min(x0 + k, R - 1)] + ny - 2 * int32_t(dot[k]));
-                } else {
-#pragma unroll
-                    for (uint32_t k = 0; k < kJoinXR; ++k) dist[k] = 0.0f;
-                    for (uint32_t c = 0; c < a.ld; c += 4) {
-                        const float4 b = *reinterpret_cast<const float4*>(yr + size_t(c) * 4);
-#pragma unroll
-                        for (uint32_t k = 0; k < kJoinXR; ++k) {
-                            const float4 x = *reinterpret_cast<const float4*>(xr[k] + size_t(c) * 4);
-                            float d;
-                            d = __fsub_rn(x.x, b.x); dist[k] = __fadd_rn(dist[k], __fmul_rn(d, d));
-                            d = __fsub_rn(x.y, b.y); dist[k] = __fadd_rn(dist[k], __fmul_rn(d, d));
-                            d = __fsub_rn(x.z, b.z); dist[k] = __fadd_rn(dist[k], __fmul_rn(d, d));
-                            d = __fsub_rn(x.w, b.w); dist[k] = __fadd_rn(dist[k], __fmul_rn(d, d));
-                        }
-                    }
-                }
-                // accepted offers: bit 2k = y offered to x's pool, bit 2k+1 = x offered to y's
-                // pool; one shared-memory atomic per warp reserves all of them
-                uint32_t acc = 0;
-                const uint32_t idy = yv ? ids[y] : 0u;
-                const uint64_t thy = yv ? thr_s[y] : 0ull;
-#pragma unroll
-                for (uint32_t k = 0; k < kJoinXR; ++k) {
-                    const uint32_t x = x0 + k;
-                    if (!yv || x >= A || y <= x) continue;
-                    const uint32_t idx = ids[x];
-                    if (idx == idy) continue;  // graph_build.cpp:146 (l == j)
-                    ++comps;
-                    if (make_key(dist[k], idy) < thr_s[x]) acc |= 1u << (2 * k);
-                    if (make_key(dist[k], idx) < thy) acc |= 2u << (2 * k);
-                }
-                const uint32_t mine = __popc(acc);
-                uint32_t incl = mine;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= uint32_t(o)) incl += t;
-                }
-                const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-                uint32_t wbase = 0;
-                if (lane == 31 && wtot) wbase = atomicAdd(&ocount, wtot);
-                wbase = __shfl_sync(0xffffffffu, wbase, 31);
-                uint32_t s_ = wbase + incl - mine;
-                while (acc) {
-                    const uint32_t bit = __ffs(acc) - 1;
-                    acc &= acc - 1;
-                    const uint32_t k = bit >> 1;
-                    const bool to_x = (bit & 1) == 0;
-                    okey[s_] = make_key(dist[k], to_x ? idy : ids[x0 + k]);
-                    omem[s_] = uint16_t(to_x ? x0 + k : y);
-                    ++s_;
-                }
-            }
-            __syncthreads();
-            const uint32_t c = ocount;
-            if (c > ol - kJoinPerRound || rb + kWarps >= n_items) {  // uniform
-                for (uint32_t m = tid; m < R; m += kJoinThreads) mcnt[m] = 0;
-                __syncthreads();
-                for (uint32_t e = tid; e < c; e += kJoinThreads) atomicAdd(&mcnt[omem[e]], 1u);
-                __syncthreads();
-                for (uint32_t m = tid; m < R; m += kJoinThreads) {
-                    const uint32_t cnt = mcnt[m];
-                    if (cnt) {
-                        const uint32_t base = atomicAdd(&a.ocnt[ids[m]], cnt);
-                        const uint32_t fix = base < a.cap ? min(cnt, a.cap - base) : 0;
-                        mbase[m] = base;
-                        mfix[m] = fix;
-                        msp[m] = cnt > fix ? atomicAdd(a.ov_cnt, cnt - fix) : 0;
-                    }
-                    mcnt[m] = 0;
-                }
-                __syncthreads();
-                for (uint32_t e = tid; e < c; e += kJoinThreads) {
-                    const uint32_t m = omem[e];
-                    const uint32_t r = atomicAdd(&mcnt[m], 1u);
-                    const uint32_t owner = ids[m];
-                    if (r < mfix[m]) {
-                        a.obuf[size_t(owner) * a.cap + mbase[m] + r] = okey[e];
-                    } else {
-                        const uint32_t o = msp[m] + (r - mfix[m]);
-                        if (o < a.ov_cap) {
-                            a.ov_tgt[o] = owner;
-                            a.ov_key[o] = okey[e];
-                        }
-                    }
-                }
-                __syncthreads();
-                if (tid == 0) {
-                    atomicAdd(a.offers, (unsigned long long)c);
-                    ocount = 0;
-                }
-                __syncthreads();
-            }
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
-    if (lane == 0 && comps) atomicAdd(a.comps, comps);
-}
-
-// Warp-per-point join for wide fp32 rows (rows too large to stage per point,
-// e.g. d = 960).  Same pairs, distances, offers and counters as the other
-// joins.  Each lane owns a partner member y (its row streamed through L1), the
-// candidate rows x are broadcast loads, and every lane runs kXB pairs' exact
-// sequential fp32 chains interleaved (dims in ascending order, 4 at a time),
-// so the dependent-add latency is covered by independent chains.  Accepted
-// offers go to a per-warp buffer flushed with one global atomic per member.
-constexpr uint32_t kWJW = 8;    // warps per CTA
-constexpr uint32_t kWOB = 512;  // offers buffered per warp
-constexpr uint32_t kXB = 16;    // candidate rows whose chains run interleaved per lane
-
-__host__ __device__ __forceinline__ size_t join_wide_bytes(uint32_t rmax) {
-    // okey (u64) + thr (u64) + ids, mcnt, mbase, mfix, msp (u32) + omem (u16)
-    return (size_t(kWOB) * 8 + size_t(rmax) * 8 + size_t(rmax) * 20 + size_t(kWOB) * 2 + 15) & ~size_t(15);
-}
-
-__device__ __forceinline__ void join_wide_flush(const JoinArgs& a, uint32_t oc, const uint64_t* okey,
-                                                const uint16_t* omem, const uint32_t* ids, uint32_t R,
-                                                uint32_t* mcnt, uint32_t* mbase, uint32_t* mfix, uint32_t* msp) {
-    const uint32_t lane = lane_id();
-    for (uint32_t e = lane; e < oc; e += 32) atomicAdd(&mcnt[omem[e]], 1u);
-    __syncwarp();
-    for (uint32_t m = lane; m < R; m += 32) {
-        const uint32_t cnt = mcnt[m];
-        if (cnt) {
-            const uint32_t base = atomicAdd(&a.ocnt[ids[m]], cnt);
-            const uint32_t fix = base < a.cap ? min(cnt, a.cap - base) : 0u;
-            mbase[m] = base;
-            mfix[m] = fix;
-            msp[m] = cnt > fix ? atomicAdd(a.ov_cnt, cnt - fix) : 0u;
-        }
-        mcnt[m] = 0;
-    }
-    __syncwarp();
-    for (uint32_t e = lane; e < oc; e += 32) {
-        const uint32_t m = omem[e];
-        const uint32_t r = atomicAdd(&mcnt[m], 1u);
-        const uint32_t owner = ids[m];
-        if (r < mfix[m]) {
-            a.obuf[size_t(owner) * a.cap + mbase[m] + r] = okey[e];
-        } else {
-            const uint32_t o = msp[m] + (r - mfix[m]);
-            if (o < a.ov_cap) {
-                a.ov_tgt[o] = owner;
-                a.ov_key[o] = okey[e];
-            }
-        }
-    }
-    __syncwarp();
-    for (uint32_t m = lane; m < R; m += 32) mcnt[m] = 0;
-    __syncwarp();
-}
-
-__global__ void __launch_bounds__(kWJW * 32) join_wide_kernel(JoinArgs a, uint32_t rmax) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
-    const uint32_t ltm = (1u << lane) - 1u;
-    unsigned char* base = smem + size_t(warp) * join_wide_bytes(rmax);
-    uint64_t* okey = reinterpret_cast<uint64_t*>(base);
-    uint64_t* thr_s = okey + kWOB;
-    uint32_t* ids = reinterpret_cast<uint32_t*>(thr_s + rmax);
-    uint32_t* mcnt = ids + rmax;
-    uint32_t* mbase = mcnt + rmax;
-    uint32_t* mfix = mbase + rmax;
-    uint32_t* msp = mfix + rmax;
-    uint16_t* omem = reinterpret_cast<uint16_t*>(msp + rmax);
-    unsigned long long comps = 0, offers = 0;
-    for (uint32_t m = lane; m < rmax; m += 32) mcnt[m] = 0;
-    for (uint32_t w = blockIdx.x * kWJW + warp; w < a.n; w += gridDim.x * kWJW) {
-        const uint32_t i = a.order ? a.order[w] : w;
-        const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
-        if (A == 0) continue;  // uniform across the warp
-        const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
-        const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
-        __syncwarp();
-        for (uint32_t r = lane; r < R; r += 32) {
-            const uint32_t id = r < A ? nw[r] : od[r - A];
-            ids[r] = id;
-            thr_s[r] = a.thr[id];
-        }
-        __syncwarp();
-        uint32_t oc = 0;
-        for (uint32_t y0 = 1; y0 < R; y0 += 32) {
-            const uint32_t y = y0 + lane;
-            const bool yv = y < R;
-            const uint32_t idy = yv ? ids[y] : ids[0];
-            const uint64_t thy = yv ? thr_s[y] : 0ull;
-            const float4* yrow = reinterpret_cast<const float4*>(a.x + size_t(idy) * a.ld);
-            const uint32_t xmax = min(A, y0 + 31);  // some lane has x < y
-            for (uint32_t x0 = 0; x0 < xmax; x0 += kXB) {
-                const uint32_t nx = min(kXB, xmax - x0);
-                uint32_t xid[kXB];
-#pragma unroll
-                for (uint32_t u = 0; u < kXB; ++u) xid[u] = ids[x0 + min(u, nx - 1)];
-                float acc[kXB];
-#pragma unroll
-                for (uint32_t u = 0; u < kXB; ++u) acc[u] = 0.0f;
-                for (uint32_t c = 0; c < a.ld / 4; ++c) {  // ld is a multiple of 4 (zero padded)
-                    const float4 yv4 = __ldg(yrow + c);
-#pragma unroll
-                    for (uint32_t u = 0; u < kXB; ++u) {
-                        const float4 xv = __ldg(reinterpret_cast<const float4*>(a.x + size_t(xid[u]) * a.ld) + c);
-                        float d;
-                        d = __fsub_rn(xv.x, yv4.x); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
-                        d = __fsub_rn(xv.y, yv4.y); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
-                        d = __fsub_rn(xv.z, yv4.z); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
-                        d = __fsub_rn(xv.w, yv4.w); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
-                    }
-                }
-#pragma unroll
-                for (uint32_t u = 0; u < kXB; ++u) {
-                    if (u >= nx) break;
-                    const uint32_t x = x0 + u, idx = xid[u];
-                    const bool pair = yv && y > x && idx != idy;  // graph_build.cpp:146 (l == j)
-                    comps += pair ? 1u : 0u;
-                    const uint64_t kx = make_key(acc[u], idy);  // offer y to x's pool
-                    const uint64_t ky = make_key(acc[u], idx);  // offer x to y's pool
-                    const bool ox = pair && kx < thr_s[x];
-                    const bool oy = pair && ky < thy;
-                    const uint32_t bx = __ballot_sync(0xffffffffu, ox);
-                    const uint32_t by = __ballot_sync(0xffffffffu, oy);
-                    if (ox) {
-                        const uint32_t pos = oc + __popc(bx & ltm);
-                        okey[pos] = kx;
-                        omem[pos] = uint16_t(x);
-                    }
-                    oc += __popc(bx);
-                    if (oy) {
-                        const uint32_t pos = oc + __popc(by & ltm);
-                        okey[pos] = ky;
-                        omem[pos] = uint16_t(y);
-                    }
-                    oc += __popc(by);
-                    if (oc > kWOB - 64) {  // one pair adds at most 64 offers
-                        __syncwarp();
-                        offers += oc;
-                        join_wide_flush(a, oc, okey, omem, ids, R, mcnt, mbase, mfix, msp);
-                        oc = 0;
-                    }
-                }
-            }
-        }
-        if (oc) {
-            __syncwarp();
-            offers += oc;
-            join_wide_flush(a, oc, okey, omem, ids, R, mcnt, mbase, mfix, msp);
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        comps += __shfl_xor_sync(0xffffffffu, comps, o);
-        offers += __shfl_xor_sync(0xffffffffu, offers, o);
-    }
-    if (lane == 0) {
-        if (comps) atomicAdd(a.comps, comps);
-        if (offers) atomicAdd(a.offers, offers);
-    }
-}
-
-// ----------------------------------------------------------------- merge
-
-struct MergeArgs {
-    uint32_t n, P, cap;
-    uint64_t* keys;
-    uint8_t* flags;
-    uint32_t* sizes;
-    const uint32_t* ocnt;
-    const uint64_t* obuf;
-    const uint32_t* ov_off;  // per-target start in the target-sorted spill list
-    const uint64_t* ov_key;
-    unsigned long long* changes;
-    uint32_t lo;    // targets [lo, n) are merged
-    uint32_t* next;  // work counter: warps take targets dynamically (offer counts vary widely)
-};
-
-__device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t n, uint64_t v) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (a[mid] < v) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// Sorts the first c (<= 32*V) entries of buf in registers and writes them back
-// sorted (padding with kEmptyKey).
-template <int V>
-__device__ __forceinline__ void warp_sort_buf(uint64_t* buf, uint32_t c) {
-    const uint32_t lane = lane_id();
-    uint64_t v[V];
-#pragma unroll
-    for (int r = 0; r < V; ++r) {
-        const uint32_t e = uint32_t(r) * 32 + lane;
-        v[r] = e < c ? buf[e] : kEmptyKey;
-    }
-    warp_sort_regs<V>(v);
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < V; ++r) buf[uint32_t(r) * 32 + lane] = v[r];
-    __syncwarp();
-}
-
-// As warp_topk_merge, for a chunk that is already sorted ascending.
-__device__ uint32_t warp_topk_merge_sorted(uint64_t* R, uint32_t r, uint64_t* chunk, uint32_t c, uint32_t P,
-                                           uint64_t* tmp) {
-    const uint32_t lane = lane_id();
-    uint32_t nu = 0;
-    for (uint32_t base = 0; base < c; base += 32) {
-        const uint32_t j = base + lane;
-        const uint64_t v = j < c ? chunk[j] : kEmptyKey;
-        bool keep = j < c && (j == 0 || chunk[j - 1] != v);
-        if (keep) {
-            const uint32_t p = lower_bound_u64(R, r, v);
-            keep = !(p < r && R[p] == v);
-        }
-        const uint32_t b = __ballot_sync(0xffffffffu, keep);
-        __syncwarp();
-        if (keep) chunk[nu + __popc(b & ((1u << lane) - 1u))] = v;
-        nu += __popc(b);
-        __syncwarp();
-    }
-    for (uint32_t j = lane; j < r; j += 32) {
-        const uint32_t k = j + lower_bound_u64(chunk, nu, R[j]);
-        if (k < P) tmp[k] = R[j];
-    }
-    for (uint32_t j = lane; j < nu; j += 32) {
-        const uint32_t k = j + lower_bound_u64(R, r, chunk[j]);
-        if (k < P) tmp[k] = chunk[j];
-    }
-    __syncwarp();
-    const uint32_t nr = min(P, r + nu);
-    for (uint32_t j = lane; j < nr; j += 32) R[j] = tmp[j];
-    __syncwarp();
-    return nr;
-}
-
-// Streaming merge (common path).  R starts as the pool (top-P unique so far);
-// offers are streamed warp-wide and only those strictly below R's current P-th
-// key are kept (an equal key is the same id, i.e. a duplicate).  Kept offers
-// collect in a small pending buffer that is sorted and merged into R when it
-// fills, which tightens the filter for the rest of the stream.  Keys found in
-// the original pool keep the pool's flag; the others are new.
-constexpr uint32_t kPend = 128;
-
-__global__ void merge_stream_kernel(MergeArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t warp = threadIdx.x / 32, lane = lane_id();
-    const uint32_t wpb = blockDim.x / 32;
-    const size_t per_warp = ((size_t(kPend) + 3 * size_t(a.P)) * 8 + a.P + 15) & ~size_t(15);
-    unsigned char* base = smem + warp * per_warp;
-    uint64_t* pend = reinterpret_cast<uint64_t*>(base);
-    uint64_t* R = pend + kPend;
-    uint64_t* sp = R + a.P;
-    uint64_t* tmp = sp + a.P;
-    uint8_t* sflag = reinterpret_cast<uint8_t*>(tmp + a.P);
-    (void)wpb;
-    for (;;) {
-    uint32_t wi = 0;
-    if (lane == 0) wi = atomicAdd(a.next, 1u);
-    const uint32_t i = a.lo + __shfl_sync(0xffffffffu, wi, 0);
-    if (i >= a.n) return;
-    const uint32_t total = a.ocnt[i];
-    if (total == 0) continue;
-    const uint32_t sz = a.sizes[i];
-    uint64_t* pk = a.keys + size_t(i) * a.P;
-    uint8_t* pf = a.flags + size_t(i) * a.P;
-    for (uint32_t j = lane; j < sz; j += 32) {
-        const uint64_t k = pk[j];
-        sp[j] = k;
-        R[j] = k;
-        sflag[j] = pf[j];
-    }
-    __syncwarp();
-    uint32_t r = sz;
-    uint64_t tail = r == a.P ? R[a.P - 1] : kEmptyKey;
-    uint32_t pc = 0;
-    const uint32_t c_fix = min(total, a.cap);
-    const uint32_t c_ov = total - c_fix;
-    const uint64_t* seg[2] = {a.obuf + size_t(i) * a.cap, a.ov_key + (c_ov ? a.ov_off[i] : 0)};
-    const uint32_t segn[2] = {c_fix, c_ov};
-    for (int sgi = 0; sgi < 2; ++sgi) {
-        const uint64_t* src = seg[sgi];
-        const uint32_t cnt = segn[sgi];
-        for (uint32_t b0 = 0; b0 < cnt; b0 += 32) {
-            const uint32_t j = b0 + lane;
-            const uint64_t key = j < cnt ? src[j] : kEmptyKey;
-            const bool keep = key < tail;
-            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) pend[pc + __popc(bal & ((1u << lane) - 1u))] = key;
-            pc += __popc(bal);
-            __syncwarp();
-            if (pc > kPend - 32) {
-                warp_sort_buf<kPend / 32>(pend, pc);
-                r = warp_topk_merge_sorted(R, r, pend, pc, a.P, tmp);
-                tail = r == a.P ? R[a.P - 1] : kEmptyKey;
-                pc = 0;
-            }
-        }
-    }
-    if (pc) {
-        warp_sort_buf<kPend / 32>(pend, pc);
-        r = warp_topk_merge_sorted(R, r, pend, pc, a.P, tmp);
-    }
-    uint32_t added = 0;
-    for (uint32_t j = lane; j < a.P; j += 32) {
-        if (j < r) {
-            const uint64_t key = R[j];
-            const uint32_t p = lower_bound_u64(sp, sz, key);
-            const bool in_pool = p < sz && sp[p] == key;
-            pk[j] = key;
-            pf[j] = in_pool ? sflag[p] : 3;  // bit0 flag_new, bit1 inserted this round
-            added += in_pool ? 0 : 1;
-        } else {
-            pk[j] = kEmptyKey;
-            pf[j] = 0;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) added += __shfl_xor_sync(0xffffffffu, added, o);
-    if (lane == 0) {
-        a.sizes[i] = r;
-        if (added) atomicAdd(a.changes, (unsigned long long)added);
-    }
-    __syncwarp();
-    }
-}
-
-
-// End of a round: entries inserted this round (flag bit 1) survive = changes.
-__global__ void count_inserted_kernel(uint8_t* __restrict__ flags, size_t cnt, unsigned long long* out) {
-    unsigned long long c = 0;
-    for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < cnt; t += size_t(gridDim.x) * blockDim.x) {
-        const uint8_t f = flags[t];
-        if (f & 2) {
-            ++c;
-            flags[t] = f & 1;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
-}
-
-__global__ void spill_counts_kernel(const uint32_t* __restrict__ ocnt, uint32_t n, uint32_t cap,
-                                    uint32_t* __restrict__ out) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = ocnt[i] > cap ? ocnt[i] - cap : 0;
-    if (i == n) out[n] = 0;
-}
-
 // --------------------------------------------------------------- finalize
 
 // graph_build.cpp:357-365: pools smaller than k are topped up by scanning ids
@@ -1531,30 +957,42 @@ __global__ void offer_counts_kernel(const uint32_t* __restrict__ ocnt, uint32_t 
     if (t < m) out[t] = ocnt[lo + t];
     if (t == m) out[m] = 0;
 }
-// Packs the offers of targets [lo, lo+m) target-major: fixed slots, then the
-// target's segment of the target-sorted spill list.  One warp per target.
+// Packs the offers of targets [lo, lo+m) target-major, each target's in slot
+// order then its spill segment (the order the replay reads), with their source
+// points.  One warp per target.
 __global__ void offer_pack_kernel(const uint32_t* __restrict__ ocnt, const uint64_t* __restrict__ obuf,
-                                  uint32_t cap, const uint32_t* __restrict__ ov_off,
-                                  const uint64_t* __restrict__ ov_key, uint32_t lo, uint32_t m,
-                                  const uint32_t* __restrict__ off, uint64_t* __restrict__ out) {
+                                  const uint32_t* __restrict__ osrc, uint32_t cap, const uint32_t* __restrict__ ov_off,
+                                  const uint64_t* __restrict__ ov_key, const uint32_t* __restrict__ ov_src,
+                                  uint32_t lo, uint32_t m, const uint32_t* __restrict__ off, uint64_t* __restrict__ out,
+                                  uint32_t* __restrict__ out_src) {
     const uint32_t lane = lane_id();
     const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (t >= m) return;
     const uint32_t tgt = lo + t, c = ocnt[tgt], fix = min(c, cap);
     uint64_t* o = out + off[t];
-    for (uint32_t j = lane; j < fix; j += 32) o[j] = obuf[size_t(tgt) * cap + j];
+    uint32_t* os = out_src + off[t];
+    for (uint32_t j = lane; j < fix; j += 32) {
+        o[j] = obuf[size_t(tgt) * cap + j];
+        os[j] = osrc[size_t(tgt) * cap + j];
+    }
     if (c > fix) {
         const uint64_t* sp = ov_key + ov_off[tgt];
-        for (uint32_t j = lane; j < c - fix; j += 32) o[fix + j] = sp[j];
+        const uint32_t* ss = ov_src + ov_off[tgt];
+        for (uint32_t j = lane; j < c - fix; j += 32) {
+            o[fix + j] = sp[j];
+            os[fix + j] = ss[j];
+        }
     }
 }
 // Appends received offers for targets [lo, lo+m) to their slots / the spill
-// list (merge order does not matter: the merge forms top-P of the union).
+// list as one contiguous block per (sender, target): the replay orders blocks
+// by source point, and a sender's block keeps its sources' order.
 __global__ void offer_add_kernel(uint32_t lo, uint32_t m, const uint32_t* __restrict__ cnt,
                                  const uint32_t* __restrict__ off, const uint64_t* __restrict__ keys,
-                                 uint32_t* __restrict__ ocnt, uint64_t* __restrict__ obuf, uint32_t cap,
+                                 const uint32_t* __restrict__ srcs, uint32_t* __restrict__ ocnt,
+                                 uint64_t* __restrict__ obuf, uint32_t* __restrict__ osrc, uint32_t cap,
                                  uint32_t* __restrict__ ov_cnt, uint32_t* __restrict__ ov_tgt,
-                                 uint64_t* __restrict__ ov_key) {
+                                 uint64_t* __restrict__ ov_key, uint32_t* __restrict__ ov_src, uint32_t ov_cap) {
     const uint32_t lane = lane_id();
     const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (t >= m) return;
@@ -1571,12 +1009,18 @@ __global__ void offer_add_kernel(uint32_t lo, uint32_t m, const uint32_t* __rest
     o0 = __shfl_sync(0xffffffffu, o0, 0);
     const uint32_t nfix = base < cap ? min(c, cap - base) : 0u;
     const uint64_t* k = keys + off[t];
+    const uint32_t* sr = srcs + off[t];
     for (uint32_t j = lane; j < c; j += 32) {
         if (j < nfix) {
             obuf[size_t(tgt) * cap + base + j] = k[j];
+            osrc[size_t(tgt) * cap + base + j] = sr[j];
         } else {
-            ov_tgt[o0 + j - nfix] = tgt;
-            ov_key[o0 + j - nfix] = k[j];
+            const uint64_t o = uint64_t(o0) + (j - nfix);
+            if (o < ov_cap) {  // the host sized the list for every received offer spilling
+                ov_tgt[o] = tgt;
+                ov_key[o] = k[j];
+                ov_src[o] = sr[j];
+            }
         }
     }
 }
@@ -1745,7 +1189,8 @@ void do_union(annk_state* s) {
 }
 
 // per-point offer slots: sized from the offer volume seen so far, within a
-// 12 GB budget (offers past the slots spill to a target-sorted global list)
+// 12 GB budget for the keys (offers past the slots spill to a target-sorted
+// global list); every offer also carries its source point (4 bytes)
 uint32_t offer_cap_max(const annk_state* s) {
     const uint32_t cap_floor = std::max(2 * s->P, 64u);
     uint32_t cap_max = cap_floor;
@@ -1755,215 +1200,129 @@ uint32_t offer_cap_max(const annk_state* s) {
 uint32_t g_offer_cap_hint = 0;          // capacities learned by earlier rounds (any state)
 uint64_t g_spill_per_point_hint = 8;
 
-// Join of the owned points (graph_build.cpp:105-162): every offer that beats its
-// target's start-of-round tail lands in the target's slots or the spill list;
-// pools are not touched.  Offers may target any point.
-// Offers one join launch may produce: the spill reservation counter is 32-bit
-// and the spill list is capped (kMaxSpill entries, 12 bytes each); a visit range
-// that would exceed either is refused (returns false, pools untouched) and the
-// caller joins it in smaller pieces.
-// (spill reservations <= offers, so below 2^32 offers the 32-bit counter cannot
-// wrap; at 2^31 the cfg3 rounds were refused and re-joined in pieces, 2.0 -> 2.5 s)
+// Offers one join launch may hold: the per-target slot counters and the spill
+// reservation counter are 32-bit and the spill list is capped (kMaxSpill
+// entries, 16 bytes each); a source range that would exceed either is refused
+// (returns false, pools untouched) and the caller joins it in smaller pieces.
 constexpr uint64_t kMaxJoinOffers = 1ull << 32;
 constexpr uint32_t kMaxSpill = 1u << 28;
 
-bool join_phase(annk_state* s, const annk_dataset* ds, uint32_t vb = 0, uint32_t ve = 0xffffffffu) {
+uint64_t join_offer_limit() {
+    const char* lim_env = getenv("ANNK_JOIN_MAX_OFFERS");  // tests: force the piecewise round at small N
+    return lim_env ? std::strtoull(lim_env, nullptr, 10) : kMaxJoinOffers;
+}
+
+// Join of the owned points whose id lies in [ilo, ihi) (graph_build.cpp:105-162):
+// every offer that beats its target's start-of-round tail lands, tagged with
+// its source point, in the target's slots or the spill list; pools are not
+// touched.  Offers may target any point.
+bool join_phase(annk_state* s, const annk_dataset* ds, uint32_t ilo = 0, uint32_t ihi = 0xffffffffu) {
     if (s->stage != 2) throw_invalid("join: call union_reverse_lists first");
     const uint32_t n = s->n;
     const uint32_t cap_floor = std::max(2 * s->P, 64u), cap_max = offer_cap_max(s);
     if (s->offer_cap == 0) s->offer_cap = std::min(cap_max, std::max(cap_floor, g_offer_cap_hint));
     if (s->ov_cap == 0)
         s->ov_cap = uint32_t(std::min<uint64_t>(std::max<uint64_t>(1u << 20, n * g_spill_per_point_hint), kMaxSpill));
-    const uint32_t rmax = 3 * s->S + s->P;  // |new| <= 2S, |old| <= P + S
-    const auto agg_smem = [&](bool u8, uint32_t ol) {
-        const size_t rsb = u8 ? ds->ld8 + 16 : size_t(ds->ld + 4) * 4;
-        return size_t(rmax) * rsb + size_t(rmax) * 8 + size_t(ol) * 8 + size_t(rmax) * 24 + (rmax / 4 + 2) * 4 +
-               size_t(ol) * 2 + 16;
-    };
-    const uint32_t ol_u8 = 2560, ol_f32 = 2048;  // u8: 4 CTAs per SM
-    const bool agg_u8 = ds->u8 && agg_smem(true, ol_u8) <= 120 * 1024;
-    const bool agg_f32 = !agg_u8 && agg_smem(false, ol_f32) <= 160 * 1024;
     // visit list: tree-0 leaf order (L2 locality), restricted to owned points
     const uint32_t* order = s->sharded ? s->order_own.p : (s->order.n ? s->order.p : nullptr);
-    ve = std::min(ve, own_hi(s) - own_lo(s));
-    if (order) order += vb;
-    const uint32_t n_visit = ve > vb ? ve - vb : 0u;
-    DevBuf<unsigned long long> counters(3);  // [comps, unused, offers]
+    const uint32_t n_visit = own_hi(s) - own_lo(s);
     if (s->ov_count.n != 1) s->ov_count.alloc(1);
-    uint32_t spilled = 0;
+    JoinCounters jc;
     for (;;) {
-        if (s->obuf.n != size_t(n) * s->offer_cap) s->obuf.alloc(size_t(n) * s->offer_cap);
+        if (s->obuf.n != size_t(n) * s->offer_cap) {
+            s->obuf.alloc(size_t(n) * s->offer_cap);
+            s->osrc.alloc(size_t(n) * s->offer_cap);
+        }
         if (s->ov_tgt.n != s->ov_cap) {
             s->ov_tgt.alloc(s->ov_cap);
             s->ov_key.alloc(s->ov_cap);
+            s->ov_src.alloc(s->ov_cap);
         }
         s->ocnt.zero();
-        counters.zero();
         s->ov_count.zero();
-        JoinArgs ja{ds->data.p, n_visit, ds->ld, s->P, s->S, s->offer_cap, s->gnew.p, s->gold.p, s->gncnt.p,
-                    s->gocnt.p, s->thr.p, s->ocnt.p, s->obuf.p, counters.p,
-                    s->ov_count.p, s->ov_tgt.p, s->ov_key.p, s->ov_cap, counters.p + 2, order};
-        if (n_visit == 0) {
-        } else if (agg_u8 || agg_f32) {
-            const size_t sm = agg_smem(agg_u8, agg_u8 ? ol_u8 : ol_f32);
-            const void* fn = agg_u8 ? reinterpret_cast<const void*>(join_agg_kernel<true>)
-                                    : reinterpret_cast<const void*>(join_agg_kernel<false>);
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            int per_sm = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinThreads, sm));
-            const uint32_t grid = std::min<uint32_t>(n_visit, uint32_t(num_sms()) * std::max(per_sm, 1));
-            if (agg_u8)
-                LAUNCH(join_agg_kernel<true>, grid, kJoinThreads, sm, ja, ds->data8.p, ds->ld8, ds->norms8.p,
-                       order, rmax, ol_u8);
-            else
-                LAUNCH(join_agg_kernel<false>, grid, kJoinThreads, sm, ja, nullptr, 0u, nullptr, order, rmax,
-                       ol_f32);
-        } else {  // wide fp32 rows: warp per point, rows streamed through L1
-            const size_t sm = join_wide_bytes(rmax) * kWJW;
-            CK(cudaFuncSetAttribute(join_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            int per_sm = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, join_wide_kernel, kWJW * 32, sm));
-            const uint32_t grid = std::min<uint32_t>((n_visit + kWJW - 1) / kWJW,
-                                                     uint32_t(num_sms()) * std::max(per_sm, 1));
-            LAUNCH(join_wide_kernel, grid, kWJW * 32, sm, ja, rmax);
-        }
-        unsigned long long offers = 0;
-        CK(cudaMemcpyAsync(&offers, counters.p + 2, 8, cudaMemcpyDeviceToHost, stream()));
-        s->ov_count.download(&spilled, 1);
-        ssync();
+        join_launch(s, ds, order, n_visit, ilo, std::min(ihi, n), &jc);
         // (the offer total bounds the spill count: below 2^32 the 32-bit counter cannot have wrapped)
-        const char* lim_env = getenv("ANNK_JOIN_MAX_OFFERS");  // tests: force the piecewise round at small N
-        const uint64_t lim = lim_env ? std::strtoull(lim_env, nullptr, 10) : kMaxJoinOffers;
-        if (offers >= lim || spilled > kMaxSpill) return false;
-        if (spilled <= s->ov_cap) break;
-        s->ov_cap = next_pow2(spilled);  // spill list too small: grow and redo (pools untouched so far)
+        if (jc.offers >= join_offer_limit() || jc.spilled > kMaxSpill) {
+            s->last_offers = jc.offers;
+            return false;
+        }
+        if (jc.spilled <= s->ov_cap) break;
+        s->ov_cap = next_pow2(jc.spilled);  // spill list too small: grow and redo (pools untouched so far)
         g_spill_per_point_hint = std::max<uint64_t>(g_spill_per_point_hint, (uint64_t(s->ov_cap) + n - 1) / n);
     }
-    unsigned long long cnt3[3] = {0, 0, 0};
-    CK(cudaMemcpyAsync(cnt3, counters.p, 24, cudaMemcpyDeviceToHost, stream()));
-    ssync();
-    s->spilled = spilled;
+    s->spilled = jc.spilled;
     s->spill_sorted = false;
-    s->pending_comps = cnt3[0];
-    s->last_offers = cnt3[2];
-    s->last_spilled = spilled;
+    s->pending_comps = jc.comps;
+    s->last_offers = jc.offers;
+    s->last_spilled = jc.spilled;
     s->pack_hi = s->pack_lo = 0;
     s->stage = 3;
     return true;
 }
 
-// Groups the spill list by target (stable radix sort) and derives per-target
-// offsets from the slot overflow counts.
-void group_spills(annk_state* s) {
+// Replays the owned targets' offers into their pools in the reference's order;
+// returns the accepted inserts.  Replaying the pieces of a round one after
+// another is exact when the pieces are ascending source ranges.
+uint64_t merge_offers(annk_state* s) { return replay_offers(s, own_lo(s), own_hi(s)); }
+
+void finish_round(annk_state* s, uint64_t changes) {
     const uint32_t n = s->n;
-    if (s->ov_off.n != size_t(n) + 1) s->ov_off.alloc(size_t(n) + 1);
-    if (s->spill_sorted) return;
-    if (s->spilled) {
-        DevBuf<uint32_t> counts(size_t(n) + 1);
-        LAUNCH(spill_counts_kernel, (n + 256) / 256, 256, 0, s->ocnt.p, n, s->offer_cap, counts.p);
-        exclusive_scan(counts.p, s->ov_off.p, n);
-        DevBuf<uint32_t> tgt_sorted(s->ov_cap);
-        DevBuf<uint64_t> key_sorted(s->ov_cap);
-        int bits = 1;
-        while ((uint64_t(1) << bits) < n) ++bits;
-        size_t tmp = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, key_sorted.p,
-                                           s->spilled, 0, bits, stream()));
-        DevBuf<unsigned char> t(tmp);
-        prof_begin("cub_radix_sort_spill");
-        CK(cub::DeviceRadixSort::SortPairs(t.p, tmp, s->ov_tgt.p, tgt_sorted.p, s->ov_key.p, key_sorted.p,
-                                           s->spilled, 0, bits, stream()));
-        prof_end();
-        note_launch();
-        std::swap(s->ov_tgt, tgt_sorted);
-        std::swap(s->ov_key, key_sorted);
-    }
-    s->spill_sorted = true;
-}
-
-// Merge of the owned targets' offers into their pools, then `changes`.
-// top-P(pool ∪ offers) of the owned targets; merging is associative, so a round
-// may merge the offers of several join pieces one after another.
-void merge_offers(annk_state* s, unsigned long long* scratch) {
-    const uint32_t lo = own_lo(s), hi = own_hi(s);
-    group_spills(s);
-    DevBuf<uint32_t> next(1);
-    next.zero();
-    MergeArgs ma{hi, s->P, s->offer_cap, s->keys.p, s->flags.p, s->sizes.p, s->ocnt.p, s->obuf.p,
-                 s->ov_off.p, s->ov_key.p, scratch, lo, next.p};
-    const size_t pw = ((size_t(kPend) + 3 * size_t(s->P)) * 8 + s->P + 15) & ~size_t(15);
-    const uint32_t wps = 8;
-    if (pw * wps > 48 * 1024)
-        CK(cudaFuncSetAttribute(merge_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pw * wps)));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_stream_kernel, wps * 32, pw * wps));
-    const uint32_t grid = std::min<uint32_t>((hi - lo + wps - 1) / wps, uint32_t(num_sms()) * std::max(per_sm, 1));
-    if (hi > lo) LAUNCH(merge_stream_kernel, grid, wps * 32, pw * wps, ma);
-}
-
-uint64_t merge_phase(annk_state* s, bool merged = false) {
-    if (s->stage != 3) throw_invalid("merge: call join first");
-    const uint32_t n = s->n, lo = own_lo(s), hi = own_hi(s);
-    DevBuf<unsigned long long> ch(2);
-    ch.zero();
-    if (!merged) merge_offers(s, ch.p + 1);
-    // changes: entries inserted this round that survive (flag bit 1), bit cleared
-    const size_t cells = size_t(hi - lo) * s->P;
-    if (cells)
-        LAUNCH(count_inserted_kernel, uint32_t(std::min<size_t>((cells + 255) / 256, 16384)), 256, 0,
-               s->flags.p + size_t(lo) * s->P, cells, ch.p);
-    unsigned long long changes = 0;
-    ch.download(&changes, 1);
-    ssync();
-    {
-        const uint32_t cap_floor = std::max(2 * s->P, 64u), cap_max = offer_cap_max(s);
-        const uint64_t want = std::max<uint64_t>(cap_floor, (s->last_offers / std::max(n, 1u)) * 5 / 4);
-        const uint32_t next = std::min<uint32_t>(cap_max, next_pow2(uint32_t(std::min<uint64_t>(want, 1u << 20))));
-        g_offer_cap_hint = std::max(g_offer_cap_hint, next);
-        s->offer_cap = std::max(s->offer_cap, next);  // takes effect next round (buffers reallocated)
-    }
+    const uint32_t cap_floor = std::max(2 * s->P, 64u), cap_max = offer_cap_max(s);
+    const uint64_t want = std::max<uint64_t>(cap_floor, (s->last_offers / std::max(n, 1u)) * 5 / 4);
+    const uint32_t next = std::min<uint32_t>(cap_max, next_pow2(uint32_t(std::min<uint64_t>(want, 1u << 20))));
+    g_offer_cap_hint = std::max(g_offer_cap_hint, next);
+    s->offer_cap = std::max(s->offer_cap, next);  // takes effect next round (buffers reallocated)
     s->dist_comps += s->pending_comps;
     s->pending_comps = 0;
     s->iteration += 1;
     s->last_changes = changes;
     s->stage = 2;  // the round's lists stay inspectable (the reference keeps them)
+}
+
+uint64_t merge_phase(annk_state* s) {
+    if (s->stage != 3) throw_invalid("merge: call join first");
+    const uint64_t changes = merge_offers(s);
+    finish_round(s, changes);
     return changes;
 }
 
+// A round whose offers do not fit one join launch (very large N) is joined in
+// ascending source ranges, each replayed into the pools before the next: the
+// reference visits the points in ascending order, so this is its order too.
 uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
-    if (s->join_pieces <= 1 && join_phase(s, ds)) return merge_phase(s);
-    // the round's offers do not fit one launch (very large N): join the visit list
-    // in pieces, merging each piece's offers before the next (pools = top-P of
-    // the start pool and all offers, whatever the grouping)
-    const uint32_t n_visit = own_hi(s) - own_lo(s);
-    if (!s->sharded && !s->order.n) {  // visit list needed for ranges
-        s->order.alloc(s->n);
-        LAUNCH(iota_kernel, (s->n + 255) / 256, 256, 0, s->order.p, 0u, s->n);
+    if (s->join_pieces <= 1) {
+        if (join_phase(s, ds)) return merge_phase(s);
+        const uint64_t lim = join_offer_limit();
+        s->join_pieces = uint32_t(std::max<uint64_t>(2, (2 * s->last_offers + lim - 1) / lim));
     }
-    uint32_t pieces = std::max(2u, s->join_pieces);
-    uint64_t comps = 0, offers = 0, spilled = 0;
-    DevBuf<unsigned long long> scratch(1);
-    uint32_t pos = 0;
-    while (pos < n_visit) {
-        const uint32_t len = std::max(1u, (n_visit + pieces - 1) / pieces);
-        const uint32_t end = std::min(n_visit, pos + len);
+    const uint32_t lo = own_lo(s), hi = own_hi(s);
+    uint32_t pieces = s->join_pieces;
+    uint64_t comps = 0, offers = 0, spilled = 0, changes = 0, max_piece = 0;
+    uint32_t pos = lo;
+    while (pos < hi) {
+        const uint32_t len = std::max(1u, (hi - lo + pieces - 1) / pieces);
+        const uint32_t end = std::min(hi, pos + len);
         if (!join_phase(s, ds, pos, end)) {
+            if (end - pos <= 1) throw_invalid("join: one point's offers exceed a join launch");
             pieces *= 2;
             continue;
         }
         comps += s->pending_comps;
         offers += s->last_offers;
         spilled += s->spilled;
-        merge_offers(s, scratch.p);
+        max_piece = std::max<uint64_t>(max_piece, s->last_offers);
+        changes += merge_offers(s);
         s->stage = 2;  // next piece joins against the same lists and start-of-round tails
         pos = end;
     }
-    s->stage = 3;
-    s->join_pieces = pieces;  // later rounds (more offers) start from here
     s->pending_comps = comps;
     s->last_offers = offers;
     s->last_spilled = spilled;
-    return merge_phase(s, true);
+    // later rounds start from the piece count this round needed (offer volume
+    // usually falls as the graph converges: back to one launch when it fits)
+    s->join_pieces = 2 * max_piece * pieces < join_offer_limit() ? 1u : pieces;
+    finish_round(s, changes);
+    return changes;
 }
 
 // Owned visit order: tree-0 leaf order restricted to [lo, hi) (or lo..hi-1).
@@ -2160,8 +1519,22 @@ int annk_shard_join(annk_state* s, const annk_dataset* ds, uint64_t* comps) {
     return abi([&] {
         if (!s || !ds || ds->n != s->n) throw_invalid("join: state/dataset mismatch");
         if (!join_phase(s, ds))
-            throw_invalid("join: this shard's offers exceed one launch (2^31 offers); use more ranks");
+            throw_invalid("join: this shard's offers exceed one join launch (" +
+                          std::to_string(join_offer_limit()) + " offers); join it in source ranges "
+                          "(annk_shard_join_range)");
         if (comps) *comps = s->pending_comps;
+    });
+}
+
+int annk_shard_join_range(annk_state* s, const annk_dataset* ds, uint32_t ilo, uint32_t ihi, uint64_t* comps,
+                          uint64_t* offers, uint32_t* ok) {
+    return abi([&] {
+        if (!s || !ds || ds->n != s->n || !ok) throw_invalid("join: state/dataset mismatch");
+        if (ilo > ihi || ihi > s->n) throw_range("join: source range out of bounds");
+        if (s->stage == 3) s->stage = 2;  // a refused or earlier piece: the lists are still valid
+        *ok = join_phase(s, ds, ilo, ihi) ? 1u : 0u;
+        if (comps) *comps = *ok ? s->pending_comps : 0;
+        if (offers) *offers = s->last_offers;
     });
 }
 
@@ -2185,7 +1558,8 @@ int annk_shard_offers_count(annk_state* s, uint32_t lo, uint32_t hi, uint64_t* t
     });
 }
 
-int annk_shard_offers_pack(annk_state* s, uint32_t lo, uint32_t hi, uint32_t* counts, uint64_t* keys) {
+int annk_shard_offers_pack(annk_state* s, uint32_t lo, uint32_t hi, uint32_t* counts, uint64_t* keys,
+                           uint32_t* srcs) {
     return abi([&] {
         if (!s) throw_invalid("offers_pack: null state");
         if (s->stage != 3 || s->pack_lo != lo || s->pack_hi != hi || s->pack_cnt.n != size_t(hi - lo) + 1)
@@ -2195,16 +1569,19 @@ int annk_shard_offers_pack(annk_state* s, uint32_t lo, uint32_t hi, uint32_t* co
         CK(cudaMemcpyAsync(&total, s->pack_off.p + m, 4, cudaMemcpyDeviceToHost, stream()));
         ssync();
         DevBuf<uint64_t> out(std::max<uint32_t>(total, 1));
+        DevBuf<uint32_t> out_src(std::max<uint32_t>(total, 1));
         if (m)
-            LAUNCH(offer_pack_kernel, grid_for(size_t(m) * 32, 256), 256, 0, s->ocnt.p, s->obuf.p, s->offer_cap,
-                   s->ov_off.p, s->ov_key.p, lo, m, s->pack_off.p, out.p);
+            LAUNCH(offer_pack_kernel, grid_for(size_t(m) * 32, 256), 256, 0, s->ocnt.p, s->obuf.p, s->osrc.p,
+                   s->offer_cap, s->ov_off.p, s->ov_key.p, s->ov_src.p, lo, m, s->pack_off.p, out.p, out_src.p);
         if (counts && m) CK(cudaMemcpyAsync(counts, s->pack_cnt.p, size_t(m) * 4, cudaMemcpyDefault, stream()));
         if (keys && total) CK(cudaMemcpyAsync(keys, out.p, size_t(total) * 8, cudaMemcpyDefault, stream()));
+        if (srcs && total) CK(cudaMemcpyAsync(srcs, out_src.p, size_t(total) * 4, cudaMemcpyDefault, stream()));
         ssync();
     });
 }
 
-int annk_shard_offers_add(annk_state* s, uint32_t lo, uint32_t hi, const uint32_t* counts, const uint64_t* keys) {
+int annk_shard_offers_add(annk_state* s, uint32_t lo, uint32_t hi, const uint32_t* counts, const uint64_t* keys,
+                          const uint32_t* srcs) {
     return abi([&] {
         if (!s || (!counts && hi > lo)) throw_invalid("offers_add: null argument");
         if (s->stage != 3) throw_invalid("offers_add: call join first");
@@ -2214,32 +1591,46 @@ int annk_shard_offers_add(annk_state* s, uint32_t lo, uint32_t hi, const uint32_
         DevBuf<uint32_t> cnt(size_t(m) + 1), off(size_t(m) + 1);
         CK(cudaMemcpyAsync(cnt.p, counts, size_t(m) * 4, cudaMemcpyDefault, stream()));
         CK(cudaMemsetAsync(cnt.p + m, 0, 4, stream()));
+        {  // received total in 64 bits (the u32 scan below could wrap)
+            std::vector<uint32_t> hc(m);
+            CK(cudaMemcpyAsync(hc.data(), counts, size_t(m) * 4, cudaMemcpyDefault, stream()));
+            ssync();
+            uint64_t t = 0;
+            for (uint32_t v : hc) t += v;
+            if (t >= join_offer_limit()) throw_invalid("offers_add: more received offers than one round may hold");
+        }
         exclusive_scan(cnt.p, off.p, m);
         uint32_t total = 0;
         CK(cudaMemcpyAsync(&total, off.p + m, 4, cudaMemcpyDeviceToHost, stream()));
         ssync();
         if (total == 0) return;
-        if (!keys) throw_invalid("offers_add: null keys");
+        if (!keys || !srcs) throw_invalid("offers_add: null keys");
         DevBuf<uint64_t> k(total);
+        DevBuf<uint32_t> sr(total);
         CK(cudaMemcpyAsync(k.p, keys, size_t(total) * 8, cudaMemcpyDefault, stream()));
+        CK(cudaMemcpyAsync(sr.p, srcs, size_t(total) * 4, cudaMemcpyDefault, stream()));
         // room for the worst case (every received offer spills); keep what is there
         const uint64_t need = uint64_t(s->spilled) + total;
+        if (need > kMaxSpill) throw_invalid("offers_add: spill list would exceed its cap; join in source ranges");
         if (need > s->ov_cap) {
-            const uint32_t cap = uint32_t(std::min<uint64_t>(next_pow2(uint32_t(std::min<uint64_t>(need, 1u << 31))),
-                                                             1u << 31));
-            DevBuf<uint32_t> t2(cap);
+            const uint32_t cap = next_pow2(uint32_t(need));
+            DevBuf<uint32_t> t2(cap), s2(cap);
             DevBuf<uint64_t> k2(cap);
             if (s->spilled) {
                 CK(cudaMemcpyAsync(t2.p, s->ov_tgt.p, size_t(s->spilled) * 4, cudaMemcpyDeviceToDevice, stream()));
                 CK(cudaMemcpyAsync(k2.p, s->ov_key.p, size_t(s->spilled) * 8, cudaMemcpyDeviceToDevice, stream()));
+                CK(cudaMemcpyAsync(s2.p, s->ov_src.p, size_t(s->spilled) * 4, cudaMemcpyDeviceToDevice, stream()));
             }
             std::swap(s->ov_tgt, t2);
             std::swap(s->ov_key, k2);
+            std::swap(s->ov_src, s2);
             s->ov_cap = cap;
         }
+        // received offers append after the (target-grouped) spill list; grouping it again is a
+        // stable sort, so every target keeps slot order, then its own spills, then these
         CK(cudaMemcpyAsync(s->ov_count.p, &s->spilled, 4, cudaMemcpyHostToDevice, stream()));
-        LAUNCH(offer_add_kernel, grid_for(size_t(m) * 32, 256), 256, 0, lo, m, cnt.p, off.p, k.p, s->ocnt.p,
-               s->obuf.p, s->offer_cap, s->ov_count.p, s->ov_tgt.p, s->ov_key.p);
+        LAUNCH(offer_add_kernel, grid_for(size_t(m) * 32, 256), 256, 0, lo, m, cnt.p, off.p, k.p, sr.p, s->ocnt.p,
+               s->obuf.p, s->osrc.p, s->offer_cap, s->ov_count.p, s->ov_tgt.p, s->ov_key.p, s->ov_src.p, s->ov_cap);
         uint32_t sp = 0;
         s->ov_count.download(&sp, 1);
         ssync();
@@ -2253,6 +1644,32 @@ int annk_shard_offers_add(annk_state* s, uint32_t lo, uint32_t hi, const uint32_
 int annk_shard_merge(annk_state* s, uint64_t* changes) {
     return abi([&] {
         const uint64_t c = merge_phase(s);
+        if (changes) *changes = c;
+    });
+}
+
+// One piece of a round joined in source ranges: the owned pools take the
+// piece's offers (exact when pieces arrive in ascending source order); the
+// round ends with annk_shard_finish_round.
+int annk_shard_merge_piece(annk_state* s, uint64_t* changes) {
+    return abi([&] {
+        if (s->stage != 3) throw_invalid("merge: call join first");
+        const uint64_t c = merge_offers(s);
+        s->piece_changes += c;
+        s->piece_comps += s->pending_comps;
+        s->pending_comps = 0;
+        s->stage = 2;
+        if (changes) *changes = c;
+    });
+}
+
+int annk_shard_finish_round(annk_state* s, uint64_t* changes) {
+    return abi([&] {
+        if (s->stage != 2) throw_invalid("finish_round: call union_reverse_lists first");
+        s->pending_comps = s->piece_comps;
+        const uint64_t c = s->piece_changes;
+        s->piece_comps = s->piece_changes = 0;
+        finish_round(s, c);
         if (changes) *changes = c;
     });
 }

@@ -95,8 +95,10 @@ struct annk_state {
     annk::DevBuf<uint64_t> thr;                       // start-of-round pool tail per point
     annk::DevBuf<uint32_t> ocnt;                      // join offer counts
     annk::DevBuf<uint64_t> obuf;                      // n x offer_cap offer keys
+    annk::DevBuf<uint32_t> osrc;                      // n x offer_cap source point of each offer
     annk::DevBuf<uint32_t> ov_tgt;                    // spill list: target ids
     annk::DevBuf<uint64_t> ov_key;                    // spill list: offer keys
+    annk::DevBuf<uint32_t> ov_src;                    // spill list: source points
     annk::DevBuf<uint32_t> order;                     // point visit order (tree-0 leaf order) for L2 locality
     uint32_t ov_cap = 0;
     int stage = 0;  // 0 none, 1 after rebuild_sample_lists, 2 after union_reverse_lists
@@ -109,6 +111,7 @@ struct annk_state {
     uint32_t spilled = 0;
     bool spill_sorted = false;
     uint64_t pending_comps = 0;
+    uint64_t piece_changes = 0, piece_comps = 0;  // shard mode: a round joined in source ranges
     uint32_t join_pieces = 1;  // visit-list pieces per round (> 1 once a round overflowed one join launch)
     // shard mode (multi-GPU): this state owns points [lo, hi); init / sample /
     // join / merge / finalize touch only those, lists and thresholds of the

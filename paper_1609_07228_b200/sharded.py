@@ -10,12 +10,17 @@ One NN-descent round (graph_build.cpp:59-162) runs as:
 3. ``union``    reverse lists from all forward rows, ``sample_down``, union
                 (same RNG streams on every rank, so every rank agrees)
 4. ``join``     local join of the owned points; offers may target any point
+                and carry their source point
 5. all-to-all   offers routed to the rank owning their target
-6. ``merge``    top-P(start pool U offers) of the owned pools
+6. ``merge``    the owned pools replay their offers in the reference's order
+                (source point ascending, then the source's pair order)
 7. all-reduce   dist_comps and changes
 
-Because the join only reads the snapshot lists, the final pools are the
-single-GPU pools exactly (the merge is order-independent).
+Because the join only reads the snapshot lists and the merge replays the
+reference's insert order, pools, flags and ``changes`` equal the single-GPU
+build and the reference's single-worker build exactly.  A round too large for
+one join launch is joined in global source ranges, ascending, each exchanged
+and replayed before the next.
 
 The protocol is written once against two small interfaces:
 
@@ -26,6 +31,8 @@ The protocol is written once against two small interfaces:
 """
 from __future__ import annotations
 
+import math
+import os
 import threading
 from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence
@@ -217,6 +224,8 @@ class DeviceShard:
             check(lib.annk_init_graph_shard(self.vs.handle, forest.handle, k, conquer_depth, pool_cap, sample_cap,
                                             seed, lo, hi, C.byref(h)))
         self.state = api.RefineState(h)
+        self.join_pieces = 1
+        self.limit = int(os.environ.get("ANNK_JOIN_MAX_OFFERS", str(1 << 32)))
 
     def _tensor(self, shape, dtype):
         import torch
@@ -241,6 +250,15 @@ class DeviceShard:
         with _LIB_LOCK:
             check(lib.annk_shard_union(self.state.handle))
 
+    def join_range(self, ilo, ihi):
+        """Join of the owned sources in [ilo, ihi): (comps, offers, ok); ok is
+        False when the range's offers exceed one join launch."""
+        c, o, ok = C.c_uint64(0), C.c_uint64(0), C.c_uint32(0)
+        with _LIB_LOCK:
+            check(lib.annk_shard_join_range(self.state.handle, self.vs.handle, ilo, ihi, C.byref(c), C.byref(o),
+                                            C.byref(ok)))
+        return c.value, o.value, bool(ok.value)
+
     def join(self) -> int:
         c = C.c_uint64(0)
         with _LIB_LOCK:
@@ -254,20 +272,34 @@ class DeviceShard:
             check(lib.annk_shard_offers_count(self.state.handle, lo, hi, C.byref(tot)))
             counts = self._tensor(hi - lo, torch.int32)
             keys = self._tensor(tot.value, torch.int64)
+            srcs = self._tensor(tot.value, torch.int32)
             check(lib.annk_shard_offers_pack(self.state.handle, lo, hi, C.c_void_p(counts.data_ptr()),
-                                             C.c_void_p(keys.data_ptr())))
-        return counts, keys
+                                             C.c_void_p(keys.data_ptr()), C.c_void_p(srcs.data_ptr())))
+        return counts, keys, srcs
 
-    def add(self, counts, keys):
-        counts, keys = counts.contiguous(), keys.contiguous()
+    def add(self, counts, keys, srcs):
+        counts, keys, srcs = counts.contiguous(), keys.contiguous(), srcs.contiguous()
         with _LIB_LOCK:
             check(lib.annk_shard_offers_add(self.state.handle, self.lo, self.hi, C.c_void_p(counts.data_ptr()),
-                                            C.c_void_p(keys.data_ptr()) if keys.numel() else None))
+                                            C.c_void_p(keys.data_ptr()) if keys.numel() else None,
+                                            C.c_void_p(srcs.data_ptr()) if srcs.numel() else None))
 
     def merge(self) -> int:
         c = C.c_uint64(0)
         with _LIB_LOCK:
             check(lib.annk_shard_merge(self.state.handle, C.byref(c)))
+        return c.value
+
+    def merge_piece(self) -> int:
+        c = C.c_uint64(0)
+        with _LIB_LOCK:
+            check(lib.annk_shard_merge_piece(self.state.handle, C.byref(c)))
+        return c.value
+
+    def finish_round(self) -> int:
+        c = C.c_uint64(0)
+        with _LIB_LOCK:
+            check(lib.annk_shard_finish_round(self.state.handle, C.byref(c)))
         return c.value
 
     def dist_comps(self) -> int:
@@ -319,6 +351,17 @@ def allgather_graph(g: api.KnnGraph, comm) -> api.KnnGraph:
 
 # --------------------------------------------------------------- protocol
 
+def _exchange(e, comm, ranges, me):
+    """all-to-all of the offers by target owner (keys and their source points)."""
+    packs = [None if r == me else e.pack(*ranges[r]) for r in range(comm.size)]
+    counts = comm.alltoall([None if p is None else p[0] for p in packs])
+    keys = comm.alltoall([None if p is None else p[1] for p in packs])
+    srcs = comm.alltoall([None if p is None else p[2] for p in packs])
+    for r in range(comm.size):
+        if r != me:
+            e.add(counts[r], keys[r], srcs[r])
+
+
 def nn_descent_round(e, comm) -> tuple:
     """One sharded NN-descent round; returns (global changes, global new comps)."""
     ranges = shard_ranges(e.n, comm.size)
@@ -330,15 +373,32 @@ def nn_descent_round(e, comm) -> tuple:
             if r != me:
                 e.put_rows(kind, ranges[r][0], ranges[r][1], part)
     e.union()
-    comps = e.join()
-    packs = [None if r == me else e.pack(*ranges[r]) for r in range(comm.size)]
-    counts = comm.alltoall([None if p is None else p[0] for p in packs])
-    keys = comm.alltoall([None if p is None else p[1] for p in packs])
-    for r in range(comm.size):
-        if r != me:
-            e.add(counts[r], keys[r])
-    changes = e.merge()
-    return comm.allreduce_sum(changes), comm.allreduce_sum(comps)
+    pieces = e.join_pieces
+    if pieces <= 1:
+        comps, offers, ok = e.join_range(0, e.n)
+        if comm.allreduce_sum(0 if ok else 1) == 0:
+            _exchange(e, comm, ranges, me)
+            changes = e.merge()
+            return comm.allreduce_sum(changes), comm.allreduce_sum(comps)
+        # some rank's offers do not fit one launch: the round runs in global source ranges
+        pieces = max(2, math.ceil(2 * comm.allreduce_sum(offers) / (comm.size * e.limit)) + 1)
+    # pieces in ascending source order, each replayed before the next: the
+    # reference's order (graph_build.cpp:129 walks the points ascending)
+    comps_total, max_piece, pos = 0, 0, 0
+    while pos < e.n:
+        end = min(e.n, pos + max(1, -(-e.n // pieces)))
+        comps, offers, ok = e.join_range(pos, end)
+        if comm.allreduce_sum(0 if ok else 1):
+            pieces *= 2
+            continue
+        _exchange(e, comm, ranges, me)
+        e.merge_piece()
+        comps_total += comps
+        max_piece = max(max_piece, offers)
+        pos = end
+    changes = e.finish_round()
+    e.join_pieces = 1 if 2 * max_piece * pieces < e.limit else pieces
+    return comm.allreduce_sum(changes), comm.allreduce_sum(comps_total)
 
 
 @dataclass

@@ -25,8 +25,11 @@ class OracleShard:
             ANNK_ROWS_THR: np.zeros((n, 1), np.uint64),
         }
         self.comps = 0
-        self.local_tgt = self.local_key = None
+        self.local = None
         self.recv = []
+        self.piece_changes = 0
+        self.join_pieces = 1
+        self.limit = 1 << 62  # offers one join may hold (tests lower it to force pieces)
 
     def sample(self):
         r = self.rows
@@ -46,31 +49,60 @@ class OracleShard:
         r = self.rows
         self.st.shard_union(r[ANNK_ROWS_FNEW], r[ANNK_ROWS_CNEW], r[ANNK_ROWS_FOLD], r[ANNK_ROWS_COLD])
 
-    def join(self) -> int:
-        c, tgt, key = self.st.shard_join(self.vs, self.lo, self.hi, self.rows[ANNK_ROWS_THR].reshape(-1))
+    def join_range(self, ilo, ihi):
+        """Join of the owned sources in [ilo, ihi): (comps, offers, ok)."""
+        lo, hi = max(self.lo, ilo), min(self.hi, ihi)
+        if hi <= lo:
+            c, tgt, key, src = 0, np.empty(0, np.uint32), np.empty(0, np.uint64), np.empty(0, np.uint32)
+        else:
+            c, tgt, key, src = self.st.shard_join(self.vs, lo, hi, self.rows[ANNK_ROWS_THR].reshape(-1))
+        if tgt.size >= self.limit:  # refused, as the device join refuses an oversized launch
+            return 0, int(tgt.size), False
         self.comps += c
-        self.local_tgt, self.local_key = tgt, key
+        self.local = (tgt, key, src)
         self.recv = []
+        return c, int(tgt.size), True
+
+    def join(self) -> int:
+        c, _, ok = self.join_range(0, self.n)
+        assert ok
         return c
 
     def pack(self, lo, hi):
-        sel = (self.local_tgt >= lo) & (self.local_tgt < hi)
-        tgt, key = self.local_tgt[sel], self.local_key[sel]
+        tgt, key, src = self.local
+        sel = (tgt >= lo) & (tgt < hi)
+        tgt, key, src = tgt[sel], key[sel], src[sel]
         order = np.argsort(tgt, kind="stable")
         counts = np.bincount(tgt - lo, minlength=hi - lo).astype(np.uint32)
         return (torch.from_numpy(counts.view(np.int32).copy()),
-                torch.from_numpy(key[order].view(np.int64).copy()))
+                torch.from_numpy(key[order].view(np.int64).copy()),
+                torch.from_numpy(src[order].view(np.int32).copy()))
 
-    def add(self, counts, keys):
+    def add(self, counts, keys, srcs):
         c = counts.numpy().view(np.uint32).astype(np.int64)
         tgt = np.repeat(np.arange(self.lo, self.hi, dtype=np.uint32), c)
-        self.recv.append((tgt, keys.numpy().view(np.uint64)))
+        self.recv.append((tgt, keys.numpy().view(np.uint64), srcs.numpy().view(np.uint32)))
+
+    def _replay(self) -> int:
+        tgt, key, src = self.local
+        sel = (tgt >= self.lo) & (tgt < self.hi)
+        parts = [(tgt[sel], key[sel], src[sel])] + self.recv
+        return self.st.shard_replay(*(np.concatenate([p[j] for p in parts]) for j in range(3)))
 
     def merge(self) -> int:
-        sel = (self.local_tgt >= self.lo) & (self.local_tgt < self.hi)
-        tgts = [self.local_tgt[sel]] + [t for t, _ in self.recv]
-        keys = [self.local_key[sel]] + [k for _, k in self.recv]
-        return self.st.shard_merge(self.lo, self.hi, np.concatenate(tgts), np.concatenate(keys))
+        ch = self._replay()
+        self.st.shard_finish(ch)
+        return ch
+
+    def merge_piece(self) -> int:
+        ch = self._replay()
+        self.piece_changes += ch
+        return ch
+
+    def finish_round(self) -> int:
+        ch, self.piece_changes = self.piece_changes, 0
+        self.st.shard_finish(ch)
+        return ch
 
     def dist_comps(self) -> int:
         return self.comps

@@ -169,12 +169,14 @@ def test_init_and_nn_descent_bit_exact(n, dim, trees, leaf, k, dep, P, S, seed, 
     e = assert_pools_equal(sd, so)
     assert sd.meta()["dist_comps"] == e["dist_comps"]
     for it in range(iters):
-        so.nn_descent_iteration(vo)
-        A.detail.nn_descent_iteration(sd, x)
+        co = so.nn_descent_iteration(vo)
+        cd = A.detail.nn_descent_iteration(sd, x)
+        assert cd == co, f"changes, iteration {it}"  # the reference's sequential accepted inserts
         e = assert_pools_equal(sd, so)
         m = sd.meta()
         assert m["dist_comps"] == e["dist_comps"], f"iteration {it}"
         assert m["iteration"] == e["iteration"]
+        assert m["last_changes"] == co
         for which in range(4):
             dl, ol = sd.lists(which), so.lists(which)
             for i in range(n):
@@ -194,15 +196,16 @@ def test_wide_fp32_init_bit_exact(n, dim, trees, leaf, P, seed):
 
 @pytest.mark.parametrize("integer", [True, False])
 def test_piecewise_join_round_bit_exact(integer, monkeypatch):
-    # a round whose offers exceed one join launch (very large N) is joined in pieces
-    # of the visit list, each piece's offers merged before the next: pools, flags and
-    # dist_comps must still equal the oracle's (forced here by a tiny offer limit)
+    # a round whose offers exceed one join launch (very large N) is joined in
+    # ascending source ranges, each piece's offers replayed before the next: pools,
+    # flags, dist_comps and changes must still equal the oracle's (forced here by a
+    # tiny offer limit)
     x = mixture(6000, 128, 30, 5) if integer else A.gen_synthetic(6000, 24, 5)
     o, vo, so, sd = _pair(x, 4, 10, 5, 10, 4, 30, 10)
     monkeypatch.setenv("ANNK_JOIN_MAX_OFFERS", "20000")
     for it in range(3):
-        so.nn_descent_iteration(vo)
-        A.detail.nn_descent_iteration(sd, x)
+        co = so.nn_descent_iteration(vo)
+        assert A.detail.nn_descent_iteration(sd, x) == co, f"changes, iteration {it}"
         e = assert_pools_equal(sd, so)
         assert sd.meta()["dist_comps"] == e["dist_comps"], f"iteration {it}"
 
@@ -211,8 +214,7 @@ def test_integer_mixture_refine_and_finalize():
     x = mixture(20000, 128, 40, 3)
     o, vo, so, sd = _pair(x, 4, 10, 3, 10, 4, 30, 10)
     for _ in range(3):
-        so.nn_descent_iteration(vo)
-        A.detail.nn_descent_iteration(sd, x)
+        assert A.detail.nn_descent_iteration(sd, x) == so.nn_descent_iteration(vo)
     assert_pools_equal(sd, so)
     ids_o, d_o = so.finalize(vo, 10)
     g = A.finalize(sd, x, 10)
@@ -355,8 +357,7 @@ def test_integer_data_both_datapaths_bit_exact(u8, monkeypatch):
     np.testing.assert_array_equal(A.brute_force_rows(x, rows, 30), ids_o[rows])
     o2, vo2, so, sd = _pair(x, 4, 8, 5, 20, 4, 40, 10)
     for _ in range(3):
-        so.nn_descent_iteration(vo2)
-        A.detail.nn_descent_iteration(sd, x)
+        assert A.detail.nn_descent_iteration(sd, x) == so.nn_descent_iteration(vo2)
         e = assert_pools_equal(sd, so)
         assert sd.meta()["dist_comps"] == e["dist_comps"]
     g = A.finalize(sd, x, 20)
@@ -396,8 +397,7 @@ def test_init_random_bit_exact(n, dim, k, P, S, seed, integer):
     assert sd.meta()["dist_comps"] == e["dist_comps"]
     vo = o.vs(x)
     for _ in range(2):  # random-descent = init_random + NN-descent rounds
-        so.nn_descent_iteration(vo)
-        A.detail.nn_descent_iteration(sd, x)
+        assert A.detail.nn_descent_iteration(sd, x) == so.nn_descent_iteration(vo)
         e = assert_pools_equal(sd, so)
         assert sd.meta()["dist_comps"] == e["dist_comps"]
 
@@ -422,8 +422,8 @@ def test_brute_force_tensor_core_path_matches_dp4a_and_oracle(n, dim, k, nq):
 
 @pytest.mark.parametrize("dim", [960, 1000])
 def test_wide_fp32_rows_join_bit_exact(dim):
-    # wide float rows (cfg3 shape; 1000 = a partial last 64-float chunk): the join stages
-    # the lanes' rows through shared memory (join_wide_kernel)
+    # wide float rows (cfg3 shape; 1000 = a partial last 64-float chunk): the join streams
+    # the rows from L2 (join_kernel<kModeWide>)
     o = ora()
     x = mixture(1500, dim, 12, 3, lo=0.05, hi=0.35, sd=0.05, clip=(0.0, 1.0), rnd=False)
     vo = o.vs(x)
@@ -433,8 +433,7 @@ def test_wide_fp32_rows_join_bit_exact(dim):
     sd = A.init_graph(x, fd, 10, 4, 30, 10, 3)
     assert_pools_equal(sd, so)
     for _ in range(3):
-        so.nn_descent_iteration(vo)
-        A.detail.nn_descent_iteration(sd, x)
+        assert A.detail.nn_descent_iteration(sd, x) == so.nn_descent_iteration(vo)
         e = assert_pools_equal(sd, so)
         assert sd.meta()["dist_comps"] == e["dist_comps"]
 

@@ -3,8 +3,10 @@
 CPU: the driver in paper_1609_07228_b200/sharded.py runs over the C oracle's
 shard primitives, as virtual ranks (threads) and as a world_size-2 gloo job;
 the owned pools, concatenated in rank order, must equal the single-process
-oracle's pools bit for bit, and the all-reduced dist_comps its counts.
-GPU: the same driver over device shards (virtual ranks on one GPU).
+oracle's pools bit for bit, and the all-reduced dist_comps and `changes` its
+counts (the reference's sequential accepted-insert count).
+GPU: the same driver over device shards (virtual ranks on one GPU, and two
+processes sharing one GPU over gloo).
 """
 import os
 import socket
@@ -30,23 +32,27 @@ def _single(o, x):
     f = o.build_forest(vs, TREES, LEAF, SEED)
     st = o.init_graph(vs, f, K, DEP, P, S, SEED)
     comps = [st.export()["dist_comps"]]
+    changes = []
     for _ in range(ITERS):
-        st.nn_descent_iteration(vs)
+        changes.append(st.nn_descent_iteration(vs))
         comps.append(st.export()["dist_comps"])
-    return st.export(), [b - a for a, b in zip(comps, comps[1:])]
+    return st.export(), [b - a for a, b in zip(comps, comps[1:])] + changes
 
 
-def _oracle_rank(o, x, comm):
+def _oracle_rank(o, x, comm, limit=None):
     vs = o.vs(x)
     f = o.build_forest(vs, TREES, LEAF, SEED)
     st = o.init_graph(vs, f, K, DEP, P, S, SEED)
     lo, hi = SH.shard_ranges(N, comm.size)[comm.rank]
     e = OracleShard(o, vs, st, N, P, S, lo, hi)
-    comps = []
+    if limit:
+        e.limit = limit
+    comps, changes = [], []
     for _ in range(ITERS):
-        _, c = SH.nn_descent_round(e, comm)
+        ch, c = SH.nn_descent_round(e, comm)
         comps.append(c)
-    return e.pools(), comps
+        changes.append(ch)
+    return e.pools(), comps + changes
 
 
 def _check(parts, ref, ref_comps):
@@ -79,6 +85,16 @@ def test_thread_ranks_match_single_process(size):
     x = _data(o)
     ref, ref_comps = _single(o, x)
     parts = SH.run_threads(size, lambda comm: _oracle_rank(o, x, comm))
+    _check(parts, ref, ref_comps)
+
+
+def test_thread_ranks_piecewise_rounds_match_single_process():
+    # a join limit below a rank's offer volume: every round runs in global
+    # source ranges, exchanged and replayed one after another
+    o = ora()
+    x = _data(o)
+    ref, ref_comps = _single(o, x)
+    parts = SH.run_threads(2, lambda comm: _oracle_rank(o, x, comm, limit=3000))
     _check(parts, ref, ref_comps)
 
 
@@ -125,11 +141,12 @@ def test_device_shards_match_oracle(size):
     def rank(comm):
         lo, hi = SH.shard_ranges(N, comm.size)[comm.rank]
         e = SH.DeviceShard(vs, f, K, DEP, P, S, SEED, lo, hi)
-        comps = []
+        comps, changes = [], []
         for _ in range(ITERS):
-            _, c = SH.nn_descent_round(e, comm)
+            ch, c = SH.nn_descent_round(e, comm)
             comps.append(c)
-        return e.pools(), comps, e.finalize()
+            changes.append(ch)
+        return e.pools(), comps + changes, e.finalize()
 
     parts = SH.run_threads(size, rank)
     _check([(p[0], p[1]) for p in parts], ref, ref_comps)
@@ -187,7 +204,8 @@ def _nccl_worker(rank, world, port, outdir):
         lo, hi = SH.shard_ranges(N, world)[rank]
         e = SH.DeviceShard(vs, f, K, DEP, P, S, SEED, lo, hi, buffer_device="cuda")
         comm = SH.TorchComm("cuda")
-        comps = [SH.nn_descent_round(e, comm)[1] for _ in range(ITERS)]
+        rounds = [SH.nn_descent_round(e, comm) for _ in range(ITERS)]
+        comps = [r[1] for r in rounds] + [r[0] for r in rounds]
         pools = e.pools()
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), sizes=pools[0], ids=pools[1], dists=pools[2],
                  flags=pools[3], comps=np.array(comps, np.int64))
@@ -204,4 +222,42 @@ def test_nccl_single_rank_device_buffers():
         torch.multiprocessing.spawn(_nccl_worker, args=(1, _free_port(), d), nprocs=1, join=True)
         z = np.load(os.path.join(d, "rank0.npz"))
         parts = [((z["sizes"], z["ids"], z["dists"], z["flags"]), [int(c) for c in z["comps"]])]
+    _check(parts, ref, ref_comps)
+
+
+def _gloo_device_worker(rank, world, port, outdir, limit):
+    import torch.distributed as dist
+    if limit:
+        os.environ["ANNK_JOIN_MAX_OFFERS"] = str(limit)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        import paper_1609_07228_b200 as A
+        o = ora()
+        x = _data(o)
+        vs = A.VectorSet(x)
+        f = A.build_forest(vs, TREES, LEAF, SEED)
+        lo, hi = SH.shard_ranges(N, world)[rank]
+        e = SH.DeviceShard(vs, f, K, DEP, P, S, SEED, lo, hi)
+        comm = SH.TorchComm("cpu")
+        rounds = [SH.nn_descent_round(e, comm) for _ in range(ITERS)]
+        pools = e.pools()
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), sizes=pools[0], ids=pools[1], dists=pools[2],
+                 flags=pools[3], comps=np.array([r[1] for r in rounds] + [r[0] for r in rounds], np.int64))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("limit", [0, 3000])
+def test_gloo_world2_device_shards_two_processes(limit):
+    # two processes (one DeviceShard each) on one GPU over gloo; limit > 0
+    # forces every round through the piecewise path
+    o = ora()
+    ref, ref_comps = _single(o, _data(o))
+    with tempfile.TemporaryDirectory() as d:
+        torch.multiprocessing.spawn(_gloo_device_worker, args=(2, _free_port(), d, limit), nprocs=2, join=True)
+        parts = []
+        for r in range(2):
+            z = np.load(os.path.join(d, f"rank{r}.npz"))
+            parts.append(((z["sizes"], z["ids"], z["dists"], z["flags"]), [int(c) for c in z["comps"]]))
     _check(parts, ref, ref_comps)
