@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <climits>
 #include <numeric>
@@ -1241,6 +1242,9 @@ bool join_phase(annk_state* s, const annk_dataset* ds, uint32_t ilo = 0, uint32_
         s->ocnt.zero();
         s->ov_count.zero();
         join_launch(s, ds, order, n_visit, ilo, std::min(ihi, n), &jc);
+        if (getenv("ANNK_TRACE"))
+            fprintf(stderr, "[annk] join [%u,%u): offers %llu spilled %u (cap %u, spill cap %u)\n", ilo,
+                    std::min(ihi, n), jc.offers, jc.spilled, s->offer_cap, s->ov_cap);
         // (the offer total bounds the spill count: below 2^32 the 32-bit counter cannot have wrapped)
         if (jc.offers >= join_offer_limit() || jc.spilled > kMaxSpill) {
             s->last_offers = jc.offers;

@@ -111,6 +111,9 @@ struct annk_state {
     uint32_t spilled = 0;
     bool spill_sorted = false;
     uint64_t pending_comps = 0;
+    annk::DevBuf<uint32_t> rp_big;        // replay: targets deferred to the global-scratch pass
+    annk::DevBuf<uint64_t> rp_runkey;     // replay scratch (grow-only): runs of the deferred targets
+    annk::DevBuf<uint32_t> rp_pstart, rp_seqoff;
     uint64_t piece_changes = 0, piece_comps = 0;  // shard mode: a round joined in source ranges
     uint32_t join_pieces = 1;  // visit-list pieces per round (> 1 once a round overflowed one join launch)
     // shard mode (multi-GPU): this state owns points [lo, hi); init / sample /

@@ -30,6 +30,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "join.cuh"
@@ -37,11 +38,9 @@
 namespace annk {
 namespace {
 
-constexpr uint32_t kJT = 256;           // join threads per CTA
-constexpr uint32_t kJW = kJT / 32;      // join warps per CTA
-constexpr uint32_t kXG = 4;             // fp32 staged rows: x rows per work item
-constexpr uint32_t kWX = 8;             // wide fp32 rows: interleaved chains per lane
-enum : int { kModeU8 = 0, kModeF32 = 1, kModeWide = 2 };
+constexpr uint32_t kWX = 8;   // fp32 rows: interleaved exact chains per lane
+constexpr uint32_t kStrip = 16;  // list rows per distance strip (one IMMA m-tile)
+enum : int { kModeU8 = 0, kModeF32 = 1 };
 
 __host__ __device__ __forceinline__ size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
 __host__ __device__ __forceinline__ uint32_t rup(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
@@ -55,6 +54,7 @@ struct JArgs {
     const uint64_t* thr;
     const uint32_t* order;
     uint32_t n_visit, ilo, ihi;
+    uint32_t* next;  // visit-list work counter
     uint32_t* ocnt;
     uint64_t* obuf;
     uint32_t* osrc;
@@ -64,34 +64,29 @@ struct JArgs {
     uint32_t* ov_src;
     uint32_t ov_cap;
     unsigned long long* counters;  // [0] comps, [1] offers
-    uint32_t rmax;   // list capacity 3S + P
-    uint32_t rn;     // per-member array length (rmax rounded up to 32)
-    uint32_t rs;     // D row stride (floats)
-    uint32_t xc;     // D rows per chunk (multiple of 16)
+    uint32_t rn;     // per-member array length: list capacity 3S + P rounded up to 32
+    uint32_t rs;     // D strip row stride (floats)
     uint32_t ol;     // offer buffer capacity
-    uint32_t rsb;    // staged row stride in bytes (0: rows not staged)
 };
 
-struct JLayout {
-    size_t thr, bkey, ids, nrm, mb, mf, ms, wc, rowcnt, canon, bmem, D, rows, total;
+// Per-warp shared memory: one warp processes one point at a time.
+struct WLayout {
+    size_t thr, bkey, ids, nrm, mc, mb, mf, ms, D, canon, bmem, total;
 };
-
-__host__ __device__ inline JLayout j_layout(const JArgs& a) {
-    JLayout L;
+__host__ __device__ inline WLayout w_layout(const JArgs& a) {
+    WLayout L;
     size_t o = 0;
-    L.thr = o;    o += al16(size_t(a.rn) * 8);
-    L.bkey = o;   o += al16(size_t(a.ol) * 8);
-    L.ids = o;    o += al16(size_t(a.rn) * 4);
-    L.nrm = o;    o += al16(size_t(a.rn) * 4);
-    L.mb = o;     o += al16(size_t(a.rn) * 4);
-    L.mf = o;     o += al16(size_t(a.rn) * 4);
-    L.ms = o;     o += al16(size_t(a.rn) * 4);
-    L.wc = o;     o += al16(size_t(kJW) * a.rn * 4);
-    L.rowcnt = o; o += al16(size_t(a.xc + 2) * 4 * 3);  // rowcnt, rowbase, sub-chunk bounds
-    L.canon = o;  o += al16(size_t(a.rn) * 2);
-    L.bmem = o;   o += al16(size_t(a.ol) * 2);
-    L.D = o;      o += al16(size_t(a.xc) * a.rs * 4);
-    L.rows = o;   o += size_t(a.rsb) * a.rn;
+    L.thr = o;   o += al16(size_t(a.rn) * 8);
+    L.bkey = o;  o += al16(size_t(a.ol) * 8);
+    L.ids = o;   o += al16(size_t(a.rn) * 4);
+    L.nrm = o;   o += al16(size_t(a.rn) * 4);
+    L.mc = o;    o += al16(size_t(a.rn) * 4);
+    L.mb = o;    o += al16(size_t(a.rn) * 4);
+    L.mf = o;    o += al16(size_t(a.rn) * 4);
+    L.ms = o;    o += al16(size_t(a.rn) * 4);
+    L.D = o;     o += al16(size_t(kStrip) * a.rs * 4);
+    L.canon = o; o += al16(size_t(a.rn) * 2);
+    L.bmem = o;  o += al16(size_t(a.ol) * 2);
     L.total = o;
     return L;
 }
@@ -105,369 +100,307 @@ __device__ __forceinline__ void mma_u8(int32_t (&c)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint32_t lds32(const unsigned char* p) { return *reinterpret_cast<const uint32_t*>(p); }
+__device__ __forceinline__ uint4 ldg128(const uint8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
-// D[x - xb][y] for x in [xb, xe), y in (x, R): the squared distance of list
-// members x and y (lower-triangle cells of a tile are computed and ignored).
+// D[x - xb][y] for the strip rows x in [xb, xb + 16) and y in (x, R): the
+// squared distance of list members x and y (cells with y <= x are ignored).
 template <int MODE>
-__device__ void join_distances(const JArgs& a, const unsigned char* rows, const uint32_t* ids, const int32_t* nrm,
-                               float* D, uint32_t xb, uint32_t xe, uint32_t R) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t yb0 = (xb + 1) / 32, nyb = (R + 31) / 32 - yb0;
+__device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* ids, const int32_t* nrm, float* D,
+                                                uint32_t xb, uint32_t xe, uint32_t R) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t yb0 = (xb + 1) / 32, yb1 = (R + 31) / 32;
     if (MODE == kModeU8) {
-        // Gram of the rows by IMMA: tile = 16 x-rows x 32 y-columns, K = row bytes.
+        // IMMA m16n8k32 tiles of 16 x-rows x 32 y-columns, K = row bytes, read
+        // straight from the u8 rows (L1-resident: prefetched one point ahead).
+        // A dot product does not depend on the order of its terms, so a lane
+        // loads 16 contiguous bytes per row and feeds them to two k-steps (the
+        // same k permutation for both operands).
         const uint32_t g = lane >> 2, t = lane & 3;
-        const uint32_t nmt = (xe - xb + 15) / 16, ntiles = nmt * nyb;
-        const uint32_t kb = a.rsb - 16;  // row bytes rounded up to 32 (zero padded)
-        for (uint32_t tile = warp; tile < ntiles; tile += kJW) {
-            const uint32_t m0 = xb + (tile / nyb) * 16, n0 = (yb0 + tile % nyb) * 32;
-            if (n0 + 31 <= m0) continue;  // no y > x in this tile
+        const uint32_t kb = rup(a.ld8, 64);
+        const uint8_t* ra0 = a.x8 + size_t(ids[min(xb + g, R - 1)]) * a.ld8 + t * 16;
+        const uint8_t* ra1 = a.x8 + size_t(ids[min(xb + g + 8, R - 1)]) * a.ld8 + t * 16;
+        const int32_t n_0 = nrm[xb + g], n_1 = nrm[xb + g + 8];
+        for (uint32_t yb = yb0; yb < yb1; ++yb) {
+            const uint32_t n0 = yb * 32;
             int32_t acc[4][4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0;
-            const unsigned char* ra0 = rows + size_t(m0 + g) * a.rsb + t * 4;
-            const unsigned char* ra1 = ra0 + size_t(8) * a.rsb;
-            const unsigned char* rb = rows + size_t(n0 + g) * a.rsb + t * 4;
-            for (uint32_t k0 = 0; k0 < kb; k0 += 32) {
-                const uint32_t a0 = lds32(ra0 + k0), a1 = lds32(ra1 + k0);
-                const uint32_t a2 = lds32(ra0 + k0 + 16), a3 = lds32(ra1 + k0 + 16);
+            const uint8_t* rb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rb[q] = a.x8 + size_t(ids[min(n0 + q * 8 + g, R - 1)]) * a.ld8 + t * 16;
+            for (uint32_t k0 = 0; k0 < kb; k0 += 64) {
+                const bool in = k0 + t * 16 < a.ld8;
+                const uint4 z = make_uint4(0, 0, 0, 0);
+                const uint4 u0 = in ? ldg128(ra0 + k0) : z, u1 = in ? ldg128(ra1 + k0) : z;
+                uint4 v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = in ? ldg128(rb[q] + k0) : z;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const unsigned char* r = rb + size_t(q * 8) * a.rsb + k0;
-                    mma_u8(acc[q], a0, a1, a2, a3, lds32(r), lds32(r + 16));
+                    mma_u8(acc[q], u0.x, u1.x, u0.y, u1.y, v[q].x, v[q].y);
+                    mma_u8(acc[q], u0.z, u1.z, u0.w, u1.w, v[q].z, v[q].w);
                 }
             }
-            const uint32_t r0 = m0 + g, r1 = r0 + 8;
-            const int32_t n_0 = nrm[r0], n_1 = nrm[r1];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t c = n0 + q * 8 + 2 * t;
                 const int32_t nc0 = nrm[c], nc1 = nrm[c + 1];
-                if (r0 < xe) {
-                    float2 v = make_float2(float(n_0 + nc0 - 2 * acc[q][0]), float(n_0 + nc1 - 2 * acc[q][1]));
-                    *reinterpret_cast<float2*>(D + size_t(r0 - xb) * a.rs + c) = v;
-                }
-                if (r1 < xe) {
-                    float2 v = make_float2(float(n_1 + nc0 - 2 * acc[q][2]), float(n_1 + nc1 - 2 * acc[q][3]));
-                    *reinterpret_cast<float2*>(D + size_t(r1 - xb) * a.rs + c) = v;
-                }
-            }
-        }
-    } else if (MODE == kModeF32) {
-        // rows staged in shared memory: each lane owns a y column and runs kXG
-        // exact sequential fp32 chains (graph_build.cpp l2_sq order).
-        const uint32_t nxg = (xe - xb + kXG - 1) / kXG, items = nxg * nyb;
-        for (uint32_t it = warp; it < items; it += kJW) {
-            const uint32_t x0 = xb + (it / nyb) * kXG, y = (yb0 + it % nyb) * 32 + lane;
-            if ((yb0 + it % nyb) * 32 + 31 <= x0) continue;
-            const float* yr = reinterpret_cast<const float*>(rows + size_t(y < R ? y : 0) * a.rsb);
-            const float* xr[kXG];
-#pragma unroll
-            for (uint32_t k = 0; k < kXG; ++k)
-                xr[k] = reinterpret_cast<const float*>(rows + size_t(min(x0 + k, xe - 1)) * a.rsb);
-            float acc[kXG];
-#pragma unroll
-            for (uint32_t k = 0; k < kXG; ++k) acc[k] = 0.0f;
-            for (uint32_t c = 0; c < a.ld; c += 4) {
-                const float4 b = *reinterpret_cast<const float4*>(yr + c);
-#pragma unroll
-                for (uint32_t k = 0; k < kXG; ++k) {
-                    const float4 v = *reinterpret_cast<const float4*>(xr[k] + c);
-                    float d;
-                    d = __fsub_rn(v.x, b.x); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(v.y, b.y); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(v.z, b.z); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(v.w, b.w); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                }
-            }
-            if (y < R) {
-#pragma unroll
-                for (uint32_t k = 0; k < kXG; ++k)
-                    if (x0 + k < xe) D[size_t(x0 + k - xb) * a.rs + y] = acc[k];
+                *reinterpret_cast<float2*>(D + size_t(g) * a.rs + c) =
+                    make_float2(float(n_0 + nc0 - 2 * acc[q][0]), float(n_0 + nc1 - 2 * acc[q][1]));
+                *reinterpret_cast<float2*>(D + size_t(g + 8) * a.rs + c) =
+                    make_float2(float(n_1 + nc0 - 2 * acc[q][2]), float(n_1 + nc1 - 2 * acc[q][3]));
             }
         }
     } else {
-        // wide fp32 rows streamed from L2: the lane's y row and kWX broadcast x
-        // rows, kWX interleaved exact chains per lane.
-        const uint32_t nxg = (xe - xb + kWX - 1) / kWX, items = nxg * nyb;
-        for (uint32_t it = warp; it < items; it += kJW) {
-            const uint32_t x0 = xb + (it / nyb) * kWX, y = (yb0 + it % nyb) * 32 + lane;
-            if ((yb0 + it % nyb) * 32 + 31 <= x0) continue;
-            const float4* yrow = reinterpret_cast<const float4*>(a.x + size_t(ids[y < R ? y : 0]) * a.ld);
-            const float4* xrow[kWX];
-#pragma unroll
-            for (uint32_t k = 0; k < kWX; ++k)
-                xrow[k] = reinterpret_cast<const float4*>(a.x + size_t(ids[min(x0 + k, xe - 1)]) * a.ld);
-            float acc[kWX];
-#pragma unroll
-            for (uint32_t k = 0; k < kWX; ++k) acc[k] = 0.0f;
-            for (uint32_t c = 0; c < a.ld / 4; ++c) {
-                const float4 b = __ldg(yrow + c);
-#pragma unroll
-                for (uint32_t k = 0; k < kWX; ++k) {
-                    const float4 v = __ldg(xrow[k] + c);
-                    float d;
-                    d = __fsub_rn(v.x, b.x); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(v.y, b.y); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(v.z, b.z); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    d = __fsub_rn(v.w, b.w); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                }
-            }
-            if (y < R) {
+        // fp32 rows from L1/L2: the lane's y row against kWX broadcast x rows,
+        // kWX interleaved exact sequential chains (graph_build.cpp l2_sq order).
+        for (uint32_t x0 = xb; x0 < xe; x0 += kWX) {
+            for (uint32_t yb = max(yb0, (x0 + 1) / 32); yb < yb1; ++yb) {
+                const uint32_t y = yb * 32 + lane;
+                const float4* yrow = reinterpret_cast<const float4*>(a.x + size_t(ids[min(y, R - 1)]) * a.ld);
+                const float4* xrow[kWX];
 #pragma unroll
                 for (uint32_t k = 0; k < kWX; ++k)
-                    if (x0 + k < xe) D[size_t(x0 + k - xb) * a.rs + y] = acc[k];
+                    xrow[k] = reinterpret_cast<const float4*>(a.x + size_t(ids[min(x0 + k, xe - 1)]) * a.ld);
+                float acc[kWX];
+#pragma unroll
+                for (uint32_t k = 0; k < kWX; ++k) acc[k] = 0.0f;
+                for (uint32_t c = 0; c < a.ld / 4; ++c) {
+                    const float4 b = __ldg(yrow + c);
+#pragma unroll
+                    for (uint32_t k = 0; k < kWX; ++k) {
+                        const float4 v = __ldg(xrow[k] + c);
+                        float d;
+                        d = __fsub_rn(v.x, b.x); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
+                        d = __fsub_rn(v.y, b.y); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
+                        d = __fsub_rn(v.z, b.z); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
+                        d = __fsub_rn(v.w, b.w); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
+                    }
+                }
+#pragma unroll
+                for (uint32_t k = 0; k < kWX; ++k) D[size_t(x0 + k - xb) * a.rs + y] = acc[k];
             }
         }
     }
 }
 
-// The offers of pair (x, y) (graph_build.cpp:139-151): y to x's pool, then x
-// to y's pool, each only if it beats the target's start-of-round tail (a key
-// at or above it is rejected by every pool state of the round).
-struct PairOffers {
-    bool valid, ox, oy;
-    uint64_t kx, ky;
-};
-__device__ __forceinline__ PairOffers pair_offers(const float* Dr, const uint32_t* ids, const uint64_t* thr_s,
-                                                  uint32_t x, uint32_t idx, uint64_t tx, uint32_t y, uint32_t R) {
-    PairOffers p;
-    const bool in = y < R;
-    const uint32_t idy = in ? ids[y] : idx;
-    p.valid = in && idy != idx;  // graph_build.cpp:146 (l == j is skipped)
-    const float d = p.valid ? Dr[y] : 0.0f;
-    p.kx = make_key(d, idy);
-    p.ky = make_key(d, idx);
-    p.ox = p.valid && p.kx < tx;
-    p.oy = p.valid && p.ky < thr_s[in ? y : x];
-    return p;
+// Hands the buffered offers (in the reference's pair order) to their targets:
+// a stable counting sort by target keeps each target's offers from this point
+// contiguous and in order, reserved with ONE global atomic per target.
+__device__ __forceinline__ void join_flush(const JArgs& a, uint32_t i, uint32_t c, uint32_t R, const uint32_t* ids,
+                                           const uint64_t* bkey, const uint16_t* bmem, uint32_t* mc, uint32_t* mb,
+                                           uint32_t* mf, uint32_t* ms) {
+    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    for (uint32_t e0 = 0; e0 < c; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const bool v = e < c;
+        const uint32_t m = v ? bmem[e] : 0xffffu;
+        const uint32_t mask = __match_any_sync(0xffffffffu, m);
+        if (v && (mask & lt) == 0) mc[m] += __popc(mask);
+        __syncwarp();
+    }
+    for (uint32_t m = lane; m < R; m += 32) {
+        const uint32_t run = mc[m];
+        if (run) {
+            const uint32_t base = atomicAdd(&a.ocnt[ids[m]], run);
+            const uint32_t fix = base < a.cap ? min(run, a.cap - base) : 0u;
+            mb[m] = base;
+            mf[m] = fix;
+            ms[m] = run > fix ? atomicAdd(a.ov_cnt, run - fix) : 0u;
+            mc[m] = 0;
+        }
+    }
+    __syncwarp();
+    for (uint32_t e0 = 0; e0 < c; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const bool v = e < c;
+        const uint32_t m = v ? bmem[e] : 0xffffu;
+        const uint32_t mask = __match_any_sync(0xffffffffu, m);
+        const uint32_t r = v ? mc[m] + __popc(mask & lt) : 0u;
+        __syncwarp();
+        if (v) {
+            if ((mask & lt) == 0) mc[m] += __popc(mask);
+            const uint32_t tgt = ids[m];
+            const uint64_t key = bkey[e];
+            if (r < mf[m]) {
+                const size_t slot = size_t(tgt) * a.cap + mb[m] + r;
+                a.obuf[slot] = key;
+                a.osrc[slot] = i;
+            } else {
+                const uint32_t o = ms[m] + (r - mf[m]);
+                if (o < a.ov_cap) {
+                    a.ov_tgt[o] = tgt;
+                    a.ov_key[o] = key;
+                    a.ov_src[o] = i;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    for (uint32_t m = lane; m < R; m += 32) mc[m] = 0;
+    __syncwarp();
 }
 
+// Next visited point: the visit list is handed out one point per request.
+__device__ __forceinline__ void join_next_point(const JArgs& a, uint32_t& pi, uint32_t& pa, uint32_t& pb) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (;;) {
+        uint32_t o = 0;
+        if (lane == 0) o = atomicAdd(a.next, 1u);
+        o = __shfl_sync(0xffffffffu, o, 0);
+        if (o >= a.n_visit) {
+            pa = pb = 0;
+            pi = 0xffffffffu;
+            return;
+        }
+        pi = a.order ? __ldg(a.order + o) : o;
+        if (pi < a.ilo || pi >= a.ihi) continue;
+        pa = __ldg(a.gncnt + pi);
+        if (pa == 0) continue;
+        pb = __ldg(a.gocnt + pi);
+        return;
+    }
+}
+
+constexpr uint32_t kMemRegs = 5;  // list members held per lane for the next point (lists <= 160)
+
+// One warp per point (persistent; points handed out by a counter).  The
+// point's list members are staged, the pair distances computed a 16-row strip
+// at a time, and the offers emitted row by row in the reference's order
+// (graph_build.cpp:135-152: row x = new[a], partners y > x ascending, y -> x
+// before x -> y) into a per-warp buffer flushed at row boundaries.  The next
+// point's header and members are fetched while the current one is processed.
 template <int MODE>
-__global__ void __launch_bounds__(kJT) join_kernel(JArgs a) {
+__global__ void __launch_bounds__(32) join_kernel(JArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ uint32_t s_nsub;
-    const JLayout L = j_layout(a);
+    const WLayout L = w_layout(a);
     uint64_t* thr_s = reinterpret_cast<uint64_t*>(sm + L.thr);
     uint64_t* bkey = reinterpret_cast<uint64_t*>(sm + L.bkey);
     uint32_t* ids = reinterpret_cast<uint32_t*>(sm + L.ids);
     int32_t* nrm = reinterpret_cast<int32_t*>(sm + L.nrm);
+    uint32_t* mc = reinterpret_cast<uint32_t*>(sm + L.mc);
     uint32_t* mb = reinterpret_cast<uint32_t*>(sm + L.mb);
     uint32_t* mf = reinterpret_cast<uint32_t*>(sm + L.mf);
     uint32_t* ms = reinterpret_cast<uint32_t*>(sm + L.ms);
-    uint32_t* wc = reinterpret_cast<uint32_t*>(sm + L.wc);
-    uint32_t* rowcnt = reinterpret_cast<uint32_t*>(sm + L.rowcnt);
-    uint32_t* rowbase = rowcnt + a.xc + 2;
-    uint32_t* sub = rowbase + a.xc + 2;
+    float* D = reinterpret_cast<float*>(sm + L.D);
     uint16_t* canon = reinterpret_cast<uint16_t*>(sm + L.canon);
     uint16_t* bmem = reinterpret_cast<uint16_t*>(sm + L.bmem);
-    float* D = reinterpret_cast<float*>(sm + L.D);
-    unsigned char* rows = sm + L.rows;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lt = (1u << lane) - 1u;
-    uint32_t* wcw = wc + warp * a.rn;
+    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
     unsigned long long comps = 0, offers = 0;
-    for (uint32_t j = tid; j < kJW * a.rn; j += kJT) wc[j] = 0;
-    for (uint32_t j = tid; j < a.rn; j += kJT) nrm[j] = 0;
-    for (uint32_t ord = blockIdx.x; ord < a.n_visit; ord += gridDim.x) {
-        const uint32_t i = a.order ? a.order[ord] : ord;
-        if (i < a.ilo || i >= a.ihi) continue;
-        const uint32_t A = a.gncnt[i], B = a.gocnt[i], R = A + B;
-        if (A == 0) continue;
-        __syncthreads();  // the previous point is done with shared memory
-        const uint32_t* nw = a.gnew + size_t(i) * 2 * a.S;
-        const uint32_t* od = a.gold + size_t(i) * (a.P + a.S);
-        for (uint32_t r = tid; r < R; r += kJT) {
-            const uint32_t id = r < A ? nw[r] : od[r - A];
+    for (uint32_t m = lane; m < a.rn; m += 32) {
+        mc[m] = 0;
+        nrm[m] = 0;
+    }
+    uint32_t i, A, B;
+    join_next_point(a, i, A, B);
+    uint32_t mid[kMemRegs], mnrm[kMemRegs];
+    uint64_t mthr[kMemRegs];
+#define JOIN_FETCH(pi, pa, pb)                                                                               \
+    _Pragma("unroll") for (uint32_t k = 0; k < kMemRegs; ++k) {                                          \
+        const uint32_t r = k * 32 + lane;                                                                    \
+        if (r < (pa) + (pb)) {                                                                               \
+            mid[k] = r < (pa) ? __ldg(a.gnew + size_t(pi) * 2 * a.S + r)                                     \
+                              : __ldg(a.gold + size_t(pi) * (a.P + a.S) + (r - (pa)));                       \
+            mthr[k] = __ldg(a.thr + mid[k]);                                                                 \
+            if (MODE == kModeU8) mnrm[k] = uint32_t(__ldg(a.norms + mid[k]));                                \
+        }                                                                                                    \
+    }
+    JOIN_FETCH(i, A, B)
+    while (A) {
+        const uint32_t R = A + B;
+#pragma unroll
+        for (uint32_t k = 0; k < kMemRegs; ++k) {
+            const uint32_t r = k * 32 + lane;
+            if (r < R) {
+                ids[r] = mid[k];
+                thr_s[r] = mthr[k];
+                nrm[r] = int32_t(mnrm[k]);
+            }
+        }
+        for (uint32_t r = kMemRegs * 32 + lane; r < R; r += 32) {  // lists longer than the registers hold
+            const uint32_t id = r < A ? a.gnew[size_t(i) * 2 * a.S + r] : a.gold[size_t(i) * (a.P + a.S) + r - A];
             ids[r] = id;
             thr_s[r] = a.thr[id];
             if (MODE == kModeU8) nrm[r] = a.norms[id];
         }
-        __syncthreads();
-        // a member present in both lists (new[a] == old[l]) is one pool: its
-        // offers are counted under its new-list position
-        for (uint32_t r = tid; r < R; r += kJT) {
-            uint32_t c = r;
-            if (r >= A) {
-                const uint32_t v = ids[r];
-                uint32_t lo = 0, hi = A;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (ids[mid] < v) lo = mid + 1;
-                    else hi = mid;
+        __syncwarp();
+        // a member in both lists (new[a] == old[l]) is one pool: its offers are
+        // counted under its new-list position
+        for (uint32_t r = A + lane; r < R; r += 32) {
+            const uint32_t v = ids[r];
+            uint32_t lo = 0, hi = A;
+            while (lo < hi) {
+                const uint32_t md = (lo + hi) >> 1;
+                if (ids[md] < v) lo = md + 1;
+                else hi = md;
+            }
+            canon[r] = uint16_t(lo < A && ids[lo] == v ? lo : r);
+        }
+        for (uint32_t r = lane; r < A; r += 32) canon[r] = uint16_t(r);
+        uint32_t ni, nA, nB;
+        join_next_point(a, ni, nA, nB);
+        __syncwarp();
+        uint32_t nbuf = 0;
+        for (uint32_t xb = 0; xb < A; xb += kStrip) {
+            const uint32_t xe = min(A, xb + kStrip);
+            strip_distances<MODE>(a, ids, nrm, D, xb, xe, R);
+            if (xb == 0) {
+                JOIN_FETCH(ni, nA, nB)  // next point's members: in flight while this one is processed
+            }
+            __syncwarp();
+            for (uint32_t x = xb; x < xe; ++x) {
+                if (nbuf + 2 * (R - x - 1) > a.ol) {  // a row fits an empty buffer (ol >= 2 rn)
+                    join_flush(a, i, nbuf, R, ids, bkey, bmem, mc, mb, mf, ms);
+                    offers += nbuf;
+                    nbuf = 0;
                 }
-                if (lo < A && ids[lo] == v) c = lo;
-            }
-            canon[r] = uint16_t(c);
-        }
-        if (MODE == kModeU8) {
-            const uint32_t kb = a.rsb - 16, v16 = kb / 16, l16 = a.ld8 / 16;
-            for (uint32_t j = tid; j < R * v16; j += kJT) {
-                const uint32_t r = j / v16, c = j % v16;
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (c < l16) v = __ldg(reinterpret_cast<const uint4*>(a.x8 + size_t(ids[r]) * a.ld8) + c);
-                *reinterpret_cast<uint4*>(rows + size_t(r) * a.rsb + c * 16) = v;
-            }
-        } else if (MODE == kModeF32) {
-            const uint32_t v4 = a.ld / 4;
-            for (uint32_t j = tid; j < R * v4; j += kJT) {
-                const uint32_t r = j / v4, c = j % v4;
-                *reinterpret_cast<float4*>(rows + size_t(r) * a.rsb + c * 16) =
-                    __ldg(reinterpret_cast<const float4*>(a.x + size_t(ids[r]) * a.ld) + c);
-            }
-        }
-        __syncthreads();
-        for (uint32_t xb = 0; xb < A; xb += a.xc) {
-            const uint32_t xe = min(A, xb + a.xc), nrow = xe - xb;
-            join_distances<MODE>(a, rows, ids, nrm, D, xb, xe, R);
-            __syncthreads();
-            // offers per row x (and the pairs counted as distance computations)
-            for (uint32_t x = xb + warp; x < xe; x += kJW) {
                 const uint32_t idx = ids[x];
                 const uint64_t tx = thr_s[x];
+                const uint16_t cx = canon[x];
                 const float* Dr = D + size_t(x - xb) * a.rs;
-                uint32_t cnt = 0, pairs = 0;
-                for (uint32_t y0 = x + 1; y0 < R; y0 += 32) {
-                    const PairOffers p = pair_offers(Dr, ids, thr_s, x, idx, tx, y0 + lane, R);
-                    cnt += __popc(__ballot_sync(0xffffffffu, p.ox)) + __popc(__ballot_sync(0xffffffffu, p.oy));
-                    pairs += __popc(__ballot_sync(0xffffffffu, p.valid));
-                }
-                if (lane == 0) {
-                    rowcnt[x - xb] = cnt;
-                    comps += pairs;
+                for (uint32_t y = x + 1 + lane, y0 = x + 1; y0 < R; y0 += 32, y += 32) {
+                    const bool in = y < R;
+                    const uint32_t idy = in ? ids[y] : idx;
+                    const bool valid = in && idy != idx;  // graph_build.cpp:146 (l == j is skipped)
+                    const float d = valid ? Dr[y] : 0.0f;
+                    const uint64_t kx = make_key(d, idy), ky = make_key(d, idx);
+                    const bool ox = valid && kx < tx;
+                    const bool oy = valid && ky < thr_s[in ? y : 0];
+                    const uint32_t bx = __ballot_sync(0xffffffffu, ox), by = __ballot_sync(0xffffffffu, oy);
+                    comps += valid ? 1u : 0u;
+                    const uint32_t q = nbuf + __popc(bx & lt) + __popc(by & lt);
+                    if (ox) {
+                        bkey[q] = kx;
+                        bmem[q] = cx;
+                    }
+                    if (oy) {
+                        bkey[q + (ox ? 1 : 0)] = ky;
+                        bmem[q + (ox ? 1 : 0)] = canon[y];
+                    }
+                    nbuf += __popc(bx) + __popc(by);
                 }
             }
-            __syncthreads();
-            // row offsets and sub-chunks whose offers fit the buffer
-            if (warp == 0) {
-                uint32_t run = 0;
-                for (uint32_t r0 = 0; r0 < nrow; r0 += 32) {
-                    const uint32_t r = r0 + lane;
-                    const uint32_t c = r < nrow ? rowcnt[r] : 0u;
-                    uint32_t incl = c;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= uint32_t(o)) incl += v;
-                    }
-                    if (r < nrow) rowbase[r] = run + incl - c;
-                    run += __shfl_sync(0xffffffffu, incl, 31);
-                }
-                if (lane == 0) {
-                    rowbase[nrow] = run;
-                    uint32_t ns = 0;
-                    sub[ns++] = 0;
-                    if (run > a.ol) {  // rare: greedy split at row boundaries (a row has <= 2 rmax offers)
-                        uint32_t acc = 0;
-                        for (uint32_t r = 0; r < nrow; ++r) {
-                            if (acc + rowcnt[r] > a.ol) {
-                                sub[ns++] = r;
-                                acc = 0;
-                            }
-                            acc += rowcnt[r];
-                        }
-                    }
-                    sub[ns] = nrow;
-                    s_nsub = ns;
-                }
-            }
-            __syncthreads();
-            const uint32_t nsub = s_nsub;
-            for (uint32_t sc = 0; sc < nsub; ++sc) {
-                const uint32_t sb = sub[sc], se = sub[sc + 1];
-                const uint32_t c = rowbase[se] - rowbase[sb];
-                if (c == 0) continue;  // uniform
-                // emit in the reference's pair order: row x, y ascending, y->x before x->y
-                for (uint32_t x = xb + sb + warp; x < xb + se; x += kJW) {
-                    const uint32_t idx = ids[x];
-                    const uint64_t tx = thr_s[x];
-                    const uint16_t cx = canon[x];
-                    const float* Dr = D + size_t(x - xb) * a.rs;
-                    uint32_t pos = rowbase[x - xb] - rowbase[sb];
-                    for (uint32_t y0 = x + 1; y0 < R; y0 += 32) {
-                        const uint32_t y = y0 + lane;
-                        const PairOffers p = pair_offers(Dr, ids, thr_s, x, idx, tx, y, R);
-                        const uint32_t bx = __ballot_sync(0xffffffffu, p.ox);
-                        const uint32_t by = __ballot_sync(0xffffffffu, p.oy);
-                        const uint32_t q = pos + __popc(bx & lt) + __popc(by & lt);
-                        if (p.ox) {
-                            bkey[q] = p.kx;
-                            bmem[q] = cx;
-                        }
-                        if (p.oy) {
-                            bkey[q + (p.ox ? 1 : 0)] = p.ky;
-                            bmem[q + (p.ox ? 1 : 0)] = canon[y];
-                        }
-                        pos += __popc(bx) + __popc(by);
-                    }
-                }
-                __syncthreads();
-                // flush: stable counting sort by target; one global reservation per target
-                const uint32_t seg = (c + kJW - 1) / kJW;
-                const uint32_t s0 = min(c, warp * seg), s1 = min(c, s0 + seg);
-                for (uint32_t e0 = s0; e0 < s1; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    const bool v = e < s1;
-                    const uint32_t m = v ? bmem[e] : 0xffffu;
-                    const uint32_t mask = __match_any_sync(0xffffffffu, m);
-                    if (v && (mask & lt) == 0) wcw[m] += __popc(mask);
-                }
-                __syncthreads();
-                for (uint32_t m = tid; m < R; m += kJT) {
-                    uint32_t run = 0;
-#pragma unroll
-                    for (uint32_t w = 0; w < kJW; ++w) {
-                        const uint32_t t = wc[w * a.rn + m];
-                        wc[w * a.rn + m] = run;
-                        run += t;
-                    }
-                    if (run) {
-                        const uint32_t base = atomicAdd(&a.ocnt[ids[m]], run);
-                        const uint32_t fix = base < a.cap ? min(run, a.cap - base) : 0u;
-                        mb[m] = base;
-                        mf[m] = fix;
-                        ms[m] = run > fix ? atomicAdd(a.ov_cnt, run - fix) : 0u;
-                    }
-                }
-                __syncthreads();
-                for (uint32_t e0 = s0; e0 < s1; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    const bool v = e < s1;
-                    const uint32_t m = v ? bmem[e] : 0xffffu;
-                    const uint32_t mask = __match_any_sync(0xffffffffu, m);
-                    const uint32_t r = v ? wcw[m] + __popc(mask & lt) : 0u;
-                    __syncwarp();
-                    if (v) {
-                        if ((mask & lt) == 0) wcw[m] += __popc(mask);
-                        const uint32_t tgt = ids[m];
-                        const uint64_t key = bkey[e];
-                        if (r < mf[m]) {
-                            const size_t slot = size_t(tgt) * a.cap + mb[m] + r;
-                            a.obuf[slot] = key;
-                            a.osrc[slot] = i;
-                        } else {
-                            const uint32_t o = ms[m] + (r - mf[m]);
-                            if (o < a.ov_cap) {
-                                a.ov_tgt[o] = tgt;
-                                a.ov_key[o] = key;
-                                a.ov_src[o] = i;
-                            }
-                        }
-                    }
-                    __syncwarp();
-                }
-                __syncthreads();
-                for (uint32_t m = tid; m < R; m += kJT) {
-#pragma unroll
-                    for (uint32_t w = 0; w < kJW; ++w) wc[w * a.rn + m] = 0;
-                }
-                if (tid == 0) offers += c;
-                __syncthreads();
-            }
+            __syncwarp();
         }
+        if (MODE == kModeU8) {  // next point's rows (one 128-byte line each) into L1
+#pragma unroll
+            for (uint32_t k = 0; k < kMemRegs; ++k)
+                if (k * 32 + lane < nA + nB) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.x8 + size_t(mid[k]) * a.ld8));
+        }
+        if (nbuf) {
+            join_flush(a, i, nbuf, R, ids, bkey, bmem, mc, mb, mf, ms);
+            offers += nbuf;
+        }
+        i = ni;
+        A = nA;
+        B = nB;
     }
+#undef JOIN_FETCH
     for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
-    if (lane == 0 && comps) atomicAdd(&a.counters[0], comps);
-    if (tid == 0 && offers) atomicAdd(&a.counters[1], offers);
+    if (lane == 0) {
+        if (comps) atomicAdd(&a.counters[0], comps);
+        if (offers) atomicAdd(&a.counters[1], offers);
+    }
 }
 
 // ------------------------------------------------------------------ replay
@@ -484,20 +417,21 @@ struct RArgs {
     const uint64_t* ov_key;
     const uint32_t* ov_src;
     unsigned long long* changes;
-    uint32_t* next;       // work counter
-    uint32_t runmax;      // runs held in shared memory per warp
-    uint32_t* big;        // first pass: targets with more runs, deferred
-    uint32_t* nbig;
-    const uint32_t* big_list;  // second pass: deferred targets, runs in global scratch
-    uint32_t big_n;
-    const uint64_t* big_off;   // per deferred target: scratch start (units of entries)
+    uint32_t* next;            // work counter
+    const uint32_t* list;      // targets to replay (nullptr: the range [lo, hi))
+    uint32_t list_n;
+    uint32_t runmax;           // source runs held in shared memory per warp
+    uint32_t* def;             // targets with more runs than that, deferred to a later pass
+    uint32_t* def_nr;          // ... and their run counts
+    uint32_t* ndef;
+    const uint64_t* g_off;     // global-scratch pass: per listed target, its scratch start
     uint64_t* g_runkey;
     uint32_t* g_pstart;
     uint32_t* g_seqoff;
 };
 
 __host__ __device__ inline size_t replay_warp_bytes(uint32_t P, uint32_t runmax) {
-    return al16(size_t(P) * 8) * 2 + al16(size_t(P)) * 2 + 32 * 8 + al16(size_t(runmax) * 8) +
+    return al16(size_t(P) * 8) * 2 + al16(size_t(P)) * 2 + 64 * 8 + al16(size_t(runmax) * 8) +
            al16(size_t(runmax + 1) * 4) * 2;
 }
 
@@ -511,14 +445,14 @@ __device__ __forceinline__ uint32_t lower_bound64(const uint64_t* a, uint32_t n,
     return lo;
 }
 
-// Replays target t's offers.  Returns false (pool untouched) when the target
-// has more than `runmax` source runs and no scratch was given.
-__device__ bool replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint64_t* T, uint8_t* SF, uint8_t* TF,
-                              uint64_t* accs, uint64_t* runkey, uint32_t* pstart, uint32_t* seqoff, uint32_t runmax,
+// Replays target t's offers.  Returns 0, or (pool untouched) the target's
+// number of source runs when it exceeds `runmax`.
+__device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint64_t* T, uint8_t* SF, uint8_t* TF,
+                              uint64_t* accs, uint64_t* wk, uint64_t* runkey, uint32_t* pstart, uint32_t* seqoff, uint32_t runmax,
                               unsigned long long& changes) {
     const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
     const uint32_t m = a.ocnt[t];
-    if (m == 0) return true;
+    if (m == 0) return 0;
     const uint32_t cf = min(m, a.cap);
     const uint64_t* k0 = a.obuf + size_t(t) * a.cap;
     const uint32_t* s0 = a.osrc + size_t(t) * a.cap;
@@ -545,7 +479,7 @@ __device__ bool replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint64_t*
         nr += __popc(b);
         lastsrc = __shfl_sync(0xffffffffu, src, 31);
     }
-    if (nr > runmax) return false;
+    if (nr > runmax) return nr;
     const uint32_t np2 = next_pow2(nr);
     for (uint32_t j = nr + lane; j < np2; j += 32) runkey[j] = ~0ull;
     if (lane == 0) pstart[nr] = m;
@@ -618,35 +552,34 @@ __device__ bool replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint64_t*
         const uint32_t cm = __ballot_sync(0xffffffffu, cand);
         if (cm == 0) continue;
         uint32_t rS = 0;
-        bool dup = false;
+        bool dupS = false;
         if (cand) {
             rS = lower_bound64(S, sz, c);
-            dup = rS < sz && S[rS] == c;
+            dupS = rS < sz && S[rS] == c;
         }
-        // candidates in sequence order: a later equal key is a duplicate; an
-        // earlier distinct candidate below the key counts towards its rank
+        // a key equal to an earlier one in the window is a duplicate (the earlier
+        // copy entered the pool or was rejected with the same rank)
+        const uint32_t eq = __match_any_sync(0xffffffffu, c);
+        const bool first = cand && !dupS && (eq & lt & cm) == 0;
+        const uint32_t fm = __ballot_sync(0xffffffffu, first);
+        wk[lane] = c;
+        __syncwarp();
+        // rank at arrival: pool keys below it + earlier first occurrences below it
         uint32_t below = 0;
-        for (uint32_t bits = cm; bits; bits &= bits - 1) {
-            const uint32_t s = __ffs(bits) - 1;
-            const uint64_t cs = shfl_idx_u64(c, s);
-            const bool ds = __shfl_sync(0xffffffffu, dup, s);
-            if (lane > s) {
-                if (cs == c) dup = true;
-                else if (!ds && cs < c) ++below;
-            }
-        }
-        const bool acc = cand && !dup && rS + below < a.P;
+        for (uint32_t bits = fm & lt; bits; bits &= bits - 1) below += wk[__ffs(bits) - 1] < c ? 1u : 0u;
+        const bool acc = first && rS + below < a.P;
         const uint32_t am = __ballot_sync(0xffffffffu, acc);
-        if (am == 0) continue;
-        const uint32_t na = __popc(am);
-        // merge: accepted keys sorted by rank among themselves, then pool
-        // entries shifted by the accepted keys below them
-        uint32_t arank = 0;
-        for (uint32_t bits = am; bits; bits &= bits - 1) {
-            const uint32_t s = __ffs(bits) - 1;
-            const uint64_t cs = shfl_idx_u64(c, s);
-            if (acc && cs < c) ++arank;
+        if (am == 0) {
+            __syncwarp();
+            continue;
         }
+        const uint32_t na = __popc(am);
+        // merge: accepted keys by rank among themselves, then pool entries
+        // shifted by the accepted keys below them
+        uint32_t arank = 0;
+        if (acc)
+            for (uint32_t bits = am; bits; bits &= bits - 1) arank += wk[__ffs(bits) - 1] < c ? 1u : 0u;
+        __syncwarp();
         if (acc) accs[arank] = c;
         __syncwarp();
         for (uint32_t p = lane; p < sz; p += 32) {
@@ -682,7 +615,7 @@ __device__ bool replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint64_t*
         if (lane == 0) a.sizes[t] = sz;
         changes += accepted;
     }
-    return true;
+    return 0;
 }
 
 __global__ void replay_kernel(RArgs a) {
@@ -694,36 +627,39 @@ __global__ void replay_kernel(RArgs a) {
     uint8_t* SF = base + al16(size_t(a.P) * 8) * 2;
     uint8_t* TF = SF + al16(a.P);
     uint64_t* accs = reinterpret_cast<uint64_t*>(TF + al16(a.P));
-    uint64_t* runkey = accs + 32;
+    uint64_t* wk = accs + 32;
+    uint64_t* runkey = wk + 32;
     uint32_t* pstart = reinterpret_cast<uint32_t*>(runkey + a.runmax);
     uint32_t* seqoff = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(pstart) +
                                                    al16(size_t(a.runmax + 1) * 4));
     unsigned long long changes = 0;
-    if (a.big_list) {
-        const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-        if (b < a.big_n) {
-            const uint64_t o = a.big_off[b];
-            replay_target(a, a.big_list[b], S, T, SF, TF, accs, a.g_runkey + o, a.g_pstart + o, a.g_seqoff + o,
-                          0xffffffffu, changes);
+    const uint32_t items = a.list ? a.list_n : a.hi - a.lo;
+    for (;;) {
+        uint32_t w = 0;
+        if (lane == 0) w = atomicAdd(a.next, 1u);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= items) break;
+        const uint32_t t = a.list ? a.list[w] : a.lo + w;
+        uint32_t nr;
+        if (a.g_runkey) {
+            const uint64_t o = a.g_off[w];
+            nr = replay_target(a, t, S, T, SF, TF, accs, wk, a.g_runkey + o, a.g_pstart + o, a.g_seqoff + o,
+                               0xffffffffu, changes);
+        } else {
+            nr = replay_target(a, t, S, T, SF, TF, accs, wk, runkey, pstart, seqoff, a.runmax, changes);
         }
-    } else {
-        for (;;) {
-            uint32_t w = 0;
-            if (lane == 0) w = atomicAdd(a.next, 1u);
-            const uint32_t t = a.lo + __shfl_sync(0xffffffffu, w, 0);
-            if (t >= a.hi) break;
-            if (!replay_target(a, t, S, T, SF, TF, accs, runkey, pstart, seqoff, a.runmax, changes)) {
-                if (lane == 0) a.big[atomicAdd(a.nbig, 1u)] = t;
-            }
+        if (nr && lane == 0) {
+            const uint32_t d = atomicAdd(a.ndef, 1u);
+            a.def[d] = t;
+            a.def_nr[d] = nr;
         }
     }
     if (lane == 0 && changes) atomicAdd(a.changes, changes);
 }
 
-__global__ void big_sizes_kernel(const uint32_t* __restrict__ big, uint32_t nb, const uint32_t* __restrict__ ocnt,
-                                 uint64_t* __restrict__ out) {
+__global__ void big_sizes_kernel(const uint32_t* __restrict__ nr, uint32_t nb, uint64_t* __restrict__ out) {
     const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < nb) out[b] = uint64_t(next_pow2(ocnt[big[b]] + 1)) + 1;
+    if (b < nb) out[b] = uint64_t(next_pow2(nr[b] + 1)) + 1;
     if (b == nb) out[nb] = 0;
 }
 
@@ -793,39 +729,27 @@ void join_launch(annk_state* s, const annk_dataset* ds, const uint32_t* order, u
     a.ov_src = s->ov_src.p;
     a.ov_cap = s->ov_cap;
     DevBuf<unsigned long long> counters(2);
+    DevBuf<uint32_t> next(1);
     counters.zero();
+    next.zero();
     a.counters = counters.p;
-    a.rmax = 3 * s->S + s->P;
-    a.rn = rup(a.rmax, 32);
+    a.next = next.p;
+    const uint32_t rmax = 3 * s->S + s->P;
+    if (rmax > 0xffffu) throw_invalid("join: sample_cap/pool_cap too large for the device path");
+    a.rn = rup(rmax, 32);
     a.rs = a.rn + 8;
-    const uint32_t amax = 2 * s->S;
-    a.xc = std::max(16u, std::min(rup(amax, 16), (24576u / (a.rs * 4)) / 16 * 16));
-    a.ol = rup(std::max(1024u, 2 * a.rmax), 32);
-    int mode;
-    const size_t f32_rsb = size_t(ds->ld + 4) * 4;
-    if (ds->u8) {
-        mode = kModeU8;
-        a.rsb = rup(ds->ld8, 32) + 16;
-    } else if (f32_rsb * a.rn <= 96 * 1024) {
-        mode = kModeF32;
-        a.rsb = uint32_t(f32_rsb);
-    } else {
-        mode = kModeWide;
-        a.rsb = 0;
-    }
-    const size_t smem = j_layout(a).total;
+    a.ol = rup(std::max(768u, 2 * a.rn), 32);
+    const size_t smem = w_layout(a).total;
     if (smem > size_t(max_smem_optin())) throw_invalid("join: list capacity too large for the device path");
-    const void* fn = mode == kModeU8    ? reinterpret_cast<const void*>(join_kernel<kModeU8>)
-                     : mode == kModeF32 ? reinterpret_cast<const void*>(join_kernel<kModeF32>)
-                                        : reinterpret_cast<const void*>(join_kernel<kModeWide>);
+    const void* fn = ds->u8 ? reinterpret_cast<const void*>(join_kernel<kModeU8>)
+                            : reinterpret_cast<const void*>(join_kernel<kModeF32>);
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJT, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem));
     const uint32_t grid = std::max(1u, std::min<uint32_t>(n_visit, uint32_t(num_sms()) * std::max(per_sm, 1)));
     if (n_visit) {
-        if (mode == kModeU8) LAUNCH(join_kernel<kModeU8>, grid, kJT, smem, a);
-        else if (mode == kModeF32) LAUNCH(join_kernel<kModeF32>, grid, kJT, smem, a);
-        else LAUNCH(join_kernel<kModeWide>, grid, kJT, smem, a);
+        if (ds->u8) LAUNCH(join_kernel<kModeU8>, grid, 32, smem, a);
+        else LAUNCH(join_kernel<kModeF32>, grid, 32, smem, a);
     }
     unsigned long long c[2] = {0, 0};
     CK(cudaMemcpyAsync(c, counters.p, 16, cudaMemcpyDeviceToHost, stream()));
@@ -885,44 +809,67 @@ uint64_t replay_offers(annk_state* s, uint32_t lo, uint32_t hi) {
     a.ov_key = s->ov_key.p;
     a.ov_src = s->ov_src.p;
     DevBuf<unsigned long long> changes(1);
-    DevBuf<uint32_t> ctr(2);  // [0] work counter, [1] deferred count
-    DevBuf<uint32_t> big(size_t(hi - lo));
+    DevBuf<uint32_t> ctr(4);  // per pass: [work counter, deferred count]
     changes.zero();
-    ctr.zero();
     a.changes = changes.p;
-    a.next = ctr.p;
-    a.nbig = ctr.p + 1;
-    a.big = big.p;
-    a.runmax = 256;
-    uint32_t wpb = 8;
-    while (wpb > 1 && replay_warp_bytes(a.P, a.runmax) * wpb > 96 * 1024) wpb /= 2;
-    const size_t smem = replay_warp_bytes(a.P, a.runmax) * wpb;
-    if (smem > size_t(max_smem_optin())) throw_invalid("refine: pool_cap too large for the device path");
-    CK(cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, replay_kernel, wpb * 32, smem));
-    const uint32_t grid = std::min<uint32_t>((hi - lo + wpb - 1) / wpb, uint32_t(num_sms()) * std::max(per_sm, 1));
-    LAUNCH(replay_kernel, grid, wpb * 32, smem, a);
-    uint32_t nb = 0;
-    CK(cudaMemcpyAsync(&nb, ctr.p + 1, 4, cudaMemcpyDeviceToHost, stream()));
-    ssync();
-    if (nb) {
-        // targets with more source runs than fit shared memory: runs in global scratch
-        DevBuf<uint64_t> sizes(size_t(nb) + 1), off(size_t(nb) + 1);
-        LAUNCH(big_sizes_kernel, gridn(size_t(nb) + 1, 256), 256, 0, big.p, nb, s->ocnt.p, sizes.p);
-        ex_scan(sizes.p, off.p, nb);
-        uint64_t total = 0;
-        CK(cudaMemcpyAsync(&total, off.p + nb, 8, cudaMemcpyDeviceToHost, stream()));
+    const uint32_t n = s->n;
+    if (s->rp_big.n < 4 * size_t(n)) s->rp_big.alloc(4 * size_t(n));  // two (target, run count) lists
+    uint32_t* def[2] = {s->rp_big.p, s->rp_big.p + 2 * size_t(n)};
+    const bool trace = getenv("ANNK_TRACE") != nullptr;
+    // pass 1: every target, up to 256 source runs in shared memory (8 warps per block);
+    // pass 2: the deferred ones with up to 1024 (4 warps per block);
+    // pass 3: the rest with their runs in global scratch
+    const uint32_t runmax[2] = {256, 1024}, wpbs[2] = {8, 4};
+    uint32_t nlist = 0;
+    for (int pass = 0; pass < 3; ++pass) {
+        ctr.zero();
+        a.next = ctr.p;
+        a.ndef = ctr.p + 1;
+        a.list = pass ? def[(pass - 1) & 1] : nullptr;
+        a.list_n = nlist;
+        a.def = def[pass & 1];
+        a.def_nr = def[pass & 1] + n;
+        const uint32_t items = pass ? nlist : hi - lo;
+        if (items == 0) break;
+        DevBuf<uint64_t> sizes, off;
+        if (pass < 2) {
+            a.runmax = runmax[pass];
+            a.g_runkey = nullptr;
+        } else {
+            sizes.alloc(size_t(items) + 1);
+            off.alloc(size_t(items) + 1);
+            LAUNCH(big_sizes_kernel, gridn(size_t(items) + 1, 256), 256, 0, def[1] + n, items, sizes.p);
+            ex_scan(sizes.p, off.p, items);
+            uint64_t total = 0;
+            CK(cudaMemcpyAsync(&total, off.p + items, 8, cudaMemcpyDeviceToHost, stream()));
+            ssync();
+            if (trace) fprintf(stderr, "[annk] replay: %u targets with runs in global scratch (%llu entries)\n", items,
+                               (unsigned long long)total);
+            if (s->rp_runkey.n < total) {  // grow-only scratch kept by the state
+                const size_t cap = std::max<size_t>(total + total / 4, size_t(1) << 16);
+                s->rp_runkey.alloc(cap);
+                s->rp_pstart.alloc(cap);
+                s->rp_seqoff.alloc(cap);
+            }
+            a.runmax = 0;
+            a.g_off = off.p;
+            a.g_runkey = s->rp_runkey.p;
+            a.g_pstart = s->rp_pstart.p;
+            a.g_seqoff = s->rp_seqoff.p;
+        }
+        const uint32_t wpb = pass < 2 ? wpbs[pass] : 4;
+        const size_t smem = replay_warp_bytes(a.P, a.runmax) * wpb;
+        if (smem > size_t(max_smem_optin())) throw_invalid("refine: pool_cap too large for the device path");
+        CK(cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, replay_kernel, wpb * 32, smem));
+        const uint32_t grid = std::min<uint32_t>((items + wpb - 1) / wpb, uint32_t(num_sms()) * std::max(per_sm, 1));
+        LAUNCH(replay_kernel, grid, wpb * 32, smem, a);
+        if (pass == 2) break;
+        CK(cudaMemcpyAsync(&nlist, ctr.p + 1, 4, cudaMemcpyDeviceToHost, stream()));
         ssync();
-        DevBuf<uint64_t> rk(total);
-        DevBuf<uint32_t> ps(total), so(total);
-        a.big_list = big.p;
-        a.big_n = nb;
-        a.big_off = off.p;
-        a.g_runkey = rk.p;
-        a.g_pstart = ps.p;
-        a.g_seqoff = so.p;
-        LAUNCH(replay_kernel, gridn(size_t(nb) * 32, wpb * 32), wpb * 32, smem, a);
+        if (trace) fprintf(stderr, "[annk] replay pass %d: %u targets deferred (> %u source runs)\n", pass, nlist,
+                           a.runmax);
     }
     unsigned long long c = 0;
     changes.download(&c, 1);

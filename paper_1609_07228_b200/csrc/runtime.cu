@@ -1,3 +1,4 @@
+#include <cstdio>
 // runtime.cu — library state, error plumbing, dataset handles, host-side
 // input generators.
 #include <cmath>
@@ -121,9 +122,15 @@ cudaEvent_t prof_event() {
 void prof_resolve() {
     if (g_prof_pending.empty()) return;
     CK(cudaStreamSynchronize(g_stream));
+    const bool trace = getenv("ANNK_PROF_TRACE") != nullptr;  // per-launch timeline on stderr
     for (const ProfRec& r : g_prof_pending) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, r.a, r.b));
+        if (trace) {
+            float at = 0.f;
+            CK(cudaEventElapsedTime(&at, g_prof_pending.front().a, r.a));
+            fprintf(stderr, "[prof] %10.3f ms  %8.3f ms  %s\n", at, ms, r.name);
+        }
         ProfAgg* agg = nullptr;
         for (auto& x : g_prof_agg)
             if (x.name == r.name) agg = &x;
