@@ -39,7 +39,8 @@ namespace annk {
 namespace {
 
 constexpr uint32_t kWX = 8;   // fp32 rows: interleaved exact chains per lane
-constexpr uint32_t kStrip = 16;  // list rows per distance strip (one IMMA m-tile)
+constexpr uint32_t kStrip = 8;   // list rows per distance strip (the upper half of an IMMA m-tile)
+constexpr uint32_t kPad = 64;    // member arrays padded so a partner window may read past the list
 enum : int { kModeU8 = 0, kModeF32 = 1 };
 
 __host__ __device__ __forceinline__ size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
@@ -76,16 +77,16 @@ struct WLayout {
 __host__ __device__ inline WLayout w_layout(const JArgs& a) {
     WLayout L;
     size_t o = 0;
-    L.thr = o;   o += al16(size_t(a.rn) * 8);
+    L.thr = o;   o += al16(size_t(a.rn + kPad) * 8);
     L.bkey = o;  o += al16(size_t(a.ol) * 8);
-    L.ids = o;   o += al16(size_t(a.rn) * 4);
+    L.ids = o;   o += al16(size_t(a.rn + kPad) * 4);
     L.nrm = o;   o += al16(size_t(a.rn) * 4);
     L.mc = o;    o += al16(size_t(a.rn) * 4);
     L.mb = o;    o += al16(size_t(a.rn) * 4);
     L.mf = o;    o += al16(size_t(a.rn) * 4);
     L.ms = o;    o += al16(size_t(a.rn) * 4);
     L.D = o;     o += al16(size_t(kStrip) * a.rs * 4);
-    L.canon = o; o += al16(size_t(a.rn) * 2);
+    L.canon = o; o += al16(size_t(a.rn + kPad) * 2);
     L.bmem = o;  o += al16(size_t(a.ol) * 2);
     L.total = o;
     return L;
@@ -102,7 +103,7 @@ __device__ __forceinline__ void mma_u8(int32_t (&c)[4], uint32_t a0, uint32_t a1
 
 __device__ __forceinline__ uint4 ldg128(const uint8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
-// D[x - xb][y] for the strip rows x in [xb, xb + 16) and y in (x, R): the
+// D[x - xb][y] for the strip rows x in [xb, xb + 8) and y in (x, R): the
 // squared distance of list members x and y (cells with y <= x are ignored).
 template <int MODE>
 __device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* ids, const int32_t* nrm, float* D,
@@ -110,7 +111,7 @@ __device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* 
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t yb0 = (xb + 1) / 32, yb1 = (R + 31) / 32;
     if (MODE == kModeU8) {
-        // IMMA m16n8k32 tiles of 16 x-rows x 32 y-columns, K = row bytes, read
+        // IMMA m16n8k32 tiles (both 8-row halves hold the strip) x 32 y-columns, K = row bytes, read
         // straight from the u8 rows (L1-resident: prefetched one point ahead).
         // A dot product does not depend on the order of its terms, so a lane
         // loads 16 contiguous bytes per row and feeds them to two k-steps (the
@@ -118,8 +119,7 @@ __device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* 
         const uint32_t g = lane >> 2, t = lane & 3;
         const uint32_t kb = rup(a.ld8, 64);
         const uint8_t* ra0 = a.x8 + size_t(ids[min(xb + g, R - 1)]) * a.ld8 + t * 16;
-        const uint8_t* ra1 = a.x8 + size_t(ids[min(xb + g + 8, R - 1)]) * a.ld8 + t * 16;
-        const int32_t n_0 = nrm[xb + g], n_1 = nrm[xb + g + 8];
+        const int32_t n_0 = nrm[xb + g];
         for (uint32_t yb = yb0; yb < yb1; ++yb) {
             const uint32_t n0 = yb * 32;
             int32_t acc[4][4];
@@ -131,7 +131,7 @@ __device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* 
             for (uint32_t k0 = 0; k0 < kb; k0 += 64) {
                 const bool in = k0 + t * 16 < a.ld8;
                 const uint4 z = make_uint4(0, 0, 0, 0);
-                const uint4 u0 = in ? ldg128(ra0 + k0) : z, u1 = in ? ldg128(ra1 + k0) : z;
+                const uint4 u0 = in ? ldg128(ra0 + k0) : z, u1 = u0;
                 uint4 v[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) v[q] = in ? ldg128(rb[q] + k0) : z;
@@ -147,8 +147,6 @@ __device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* 
                 const int32_t nc0 = nrm[c], nc1 = nrm[c + 1];
                 *reinterpret_cast<float2*>(D + size_t(g) * a.rs + c) =
                     make_float2(float(n_0 + nc0 - 2 * acc[q][0]), float(n_0 + nc1 - 2 * acc[q][1]));
-                *reinterpret_cast<float2*>(D + size_t(g + 8) * a.rs + c) =
-                    make_float2(float(n_1 + nc0 - 2 * acc[q][2]), float(n_1 + nc1 - 2 * acc[q][3]));
             }
         }
     } else {
@@ -334,9 +332,14 @@ __global__ void __launch_bounds__(32) join_kernel(JArgs a) {
                 if (ids[md] < v) lo = md + 1;
                 else hi = md;
             }
-            canon[r] = uint16_t(lo < A && ids[lo] == v ? lo : r);
+            const bool dual = lo < A && ids[lo] == v;
+            canon[r] = uint16_t(dual ? lo : r);
+            comps -= dual ? 1u : 0u;
         }
         for (uint32_t r = lane; r < A; r += 32) canon[r] = uint16_t(r);
+        // distance computations (graph_build.cpp:138-150): every new x with each
+        // later member, except a member against itself (an id in both lists)
+        if (lane == 0) comps += uint64_t(A) * (R - 1) - uint64_t(A) * (A - 1) / 2;
         uint32_t ni, nA, nB;
         join_next_point(a, ni, nA, nB);
         __syncwarp();
@@ -358,26 +361,38 @@ __global__ void __launch_bounds__(32) join_kernel(JArgs a) {
                 const uint64_t tx = thr_s[x];
                 const uint16_t cx = canon[x];
                 const float* Dr = D + size_t(x - xb) * a.rs;
-                for (uint32_t y = x + 1 + lane, y0 = x + 1; y0 < R; y0 += 32, y += 32) {
-                    const bool in = y < R;
-                    const uint32_t idy = in ? ids[y] : idx;
-                    const bool valid = in && idy != idx;  // graph_build.cpp:146 (l == j is skipped)
-                    const float d = valid ? Dr[y] : 0.0f;
-                    const uint64_t kx = make_key(d, idy), ky = make_key(d, idx);
-                    const bool ox = valid && kx < tx;
-                    const bool oy = valid && ky < thr_s[in ? y : 0];
-                    const uint32_t bx = __ballot_sync(0xffffffffu, ox), by = __ballot_sync(0xffffffffu, oy);
-                    comps += valid ? 1u : 0u;
-                    const uint32_t q = nbuf + __popc(bx & lt) + __popc(by & lt);
-                    if (ox) {
-                        bkey[q] = kx;
-                        bmem[q] = cx;
+                // two 32-partner windows per step (their loads overlap), emitted in order
+                for (uint32_t y0 = x + 1; y0 < R; y0 += 64) {
+                    bool ox[2], oy[2];
+                    uint64_t kx[2], ky[2];
+                    uint32_t bx[2], by[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t y = y0 + 32 * h + lane;  // < rn + kPad: reads stay in the arrays
+                        const uint32_t idy = ids[y];
+                        const float d = Dr[y];
+                        const uint64_t thy = thr_s[y];
+                        const bool valid = y < R && idy != idx;  // graph_build.cpp:146 (l == j is skipped)
+                        kx[h] = make_key(d, idy);
+                        ky[h] = make_key(d, idx);
+                        ox[h] = valid && kx[h] < tx;
+                        oy[h] = valid && ky[h] < thy;
+                        bx[h] = __ballot_sync(0xffffffffu, ox[h]);
+                        by[h] = __ballot_sync(0xffffffffu, oy[h]);
                     }
-                    if (oy) {
-                        bkey[q + (ox ? 1 : 0)] = ky;
-                        bmem[q + (ox ? 1 : 0)] = canon[y];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t q = nbuf + __popc(bx[h] & lt) + __popc(by[h] & lt);
+                        if (ox[h]) {
+                            bkey[q] = kx[h];
+                            bmem[q] = cx;
+                        }
+                        if (oy[h]) {
+                            bkey[q + (ox[h] ? 1 : 0)] = ky[h];
+                            bmem[q + (ox[h] ? 1 : 0)] = canon[y0 + 32 * h + lane];
+                        }
+                        nbuf += __popc(bx[h]) + __popc(by[h]);
                     }
-                    nbuf += __popc(bx) + __popc(by);
                 }
             }
             __syncwarp();
@@ -431,7 +446,7 @@ struct RArgs {
 };
 
 __host__ __device__ inline size_t replay_warp_bytes(uint32_t P, uint32_t runmax) {
-    return al16(size_t(P) * 8) * 2 + al16(size_t(P)) * 2 + 64 * 8 + al16(size_t(runmax) * 8) +
+    return al16(size_t(P) * 8) + al16(size_t(P)) + 64 * 8 + al16(size_t(runmax) * 8) +
            al16(size_t(runmax + 1) * 4) * 2;
 }
 
@@ -447,8 +462,7 @@ __device__ __forceinline__ uint32_t lower_bound64(const uint64_t* a, uint32_t n,
 
 // Replays target t's offers.  Returns 0, or (pool untouched) the target's
 // number of source runs when it exceeds `runmax`.
-__device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint64_t* T, uint8_t* SF, uint8_t* TF,
-                              uint64_t* accs, uint64_t* wk, uint64_t* runkey, uint32_t* pstart, uint32_t* seqoff, uint32_t runmax,
+__device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint8_t* SF, uint64_t* accs, uint64_t* wk, uint64_t* runkey, uint32_t* pstart, uint32_t* seqoff, uint32_t runmax,
                               unsigned long long& changes) {
     const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
     const uint32_t m = a.ocnt[t];
@@ -461,23 +475,32 @@ __device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint6
     const uint32_t* s1 = a.ov_src + spill;
     // runs: maximal stretches of one source (a segment boundary always starts one)
     uint32_t nr = 0, lastsrc = 0;
-    for (uint32_t q0 = 0; q0 < m; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        const bool v = q < m;
-        const uint32_t src = v ? (q < cf ? s0[q] : s1[q - cf]) : 0u;
-        uint32_t prev = __shfl_up_sync(0xffffffffu, src, 1);
-        if (lane == 0) prev = lastsrc;
-        const bool start = v && (q == 0 || q == cf || src != prev);
-        const uint32_t b = __ballot_sync(0xffffffffu, start);
-        if (start) {
-            const uint32_t idx = nr + __popc(b & lt);
-            if (idx < runmax) {
-                runkey[idx] = (uint64_t(src) << 32) | idx;
-                pstart[idx] = q;
-            }
+    for (uint32_t q00 = 0; q00 < m; q00 += 64) {
+        uint32_t src2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // both windows' loads in flight together
+            const uint32_t q = q00 + 32 * h + lane;
+            src2[h] = q < m ? (q < cf ? s0[q] : s1[q - cf]) : 0u;
         }
-        nr += __popc(b);
-        lastsrc = __shfl_sync(0xffffffffu, src, 31);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t q = q00 + 32 * h + lane;
+            const bool v = q < m;
+            const uint32_t src = src2[h];
+            uint32_t prev = __shfl_up_sync(0xffffffffu, src, 1);
+            if (lane == 0) prev = lastsrc;
+            const bool start = v && (q == 0 || q == cf || src != prev);
+            const uint32_t b = __ballot_sync(0xffffffffu, start);
+            if (start) {
+                const uint32_t idx = nr + __popc(b & lt);
+                if (idx < runmax) {
+                    runkey[idx] = (uint64_t(src) << 32) | idx;
+                    pstart[idx] = q;
+                }
+            }
+            nr += __popc(b);
+            lastsrc = __shfl_sync(0xffffffffu, src, 31);
+        }
     }
     if (nr > runmax) return nr;
     const uint32_t np2 = next_pow2(nr);
@@ -523,6 +546,13 @@ __device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint6
             if (r < nr) seqoff[r] = run + incl - len;
             run += __shfl_sync(0xffffffffu, incl, 31);
         }
+        __syncwarp();
+        // run r covers sequence positions [seqoff[r], seqoff[r+1]); position q maps to
+        // slot q + delta[r] (delta kept in runkey's low word once the order is fixed)
+        for (uint32_t r = lane; r < nr; r += 32)
+            runkey[r] = uint32_t(pstart[uint32_t(runkey[r])] - seqoff[r]);
+        if (lane == 0) seqoff[nr] = m;
+        __syncwarp();
     }
     // start pool
     uint32_t sz = a.sizes[t];
@@ -535,19 +565,20 @@ __device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint6
     __syncwarp();
     uint64_t tail = sz == a.P ? S[a.P - 1] : kEmptyKey;
     uint32_t accepted = 0;
+    uint32_t rbase = 0;  // the run holding the window's first position
     for (uint32_t q0 = 0; q0 < m; q0 += 32) {
         const uint32_t q = q0 + lane;
+        // runs starting inside the window: bit o set if one starts at q0 + o
+        const uint32_t rj = rbase + 1 + lane;
+        const uint32_t bo = rj < nr ? seqoff[rj] - q0 : 64u;
+        const uint32_t bm = __reduce_or_sync(0xffffffffu, bo < 32 ? 1u << bo : 0u);
+        const uint32_t run = rbase + __popc(bm & ((2u << lane) - 1u));
         uint64_t c = kEmptyKey;
         if (q < m) {
-            uint32_t lo = 0, hi = nr;  // last run with seqoff <= q
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (seqoff[mid] <= q) lo = mid;
-                else hi = mid;
-            }
-            const uint32_t pos = pstart[uint32_t(runkey[lo])] + (q - seqoff[lo]);
+            const uint32_t pos = q + uint32_t(runkey[run]);
             c = pos < cf ? k0[pos] : k1[pos - cf];
         }
+        rbase += __popc(__ballot_sync(0xffffffffu, bo <= 32));
         const bool cand = c < tail;
         const uint32_t cm = __ballot_sync(0xffffffffu, cand);
         if (cm == 0) continue;
@@ -574,34 +605,39 @@ __device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint6
             continue;
         }
         const uint32_t na = __popc(am);
-        // merge: accepted keys by rank among themselves, then pool entries
-        // shifted by the accepted keys below them
+        // merge in place: accepted keys ranked among themselves; pool entries at
+        // or above the lowest insertion point move up by the accepted keys below
+        // them (top-down 32-entry chunks: a chunk is read before it is written)
         uint32_t arank = 0;
         if (acc)
             for (uint32_t bits = am; bits; bits &= bits - 1) arank += wk[__ffs(bits) - 1] < c ? 1u : 0u;
+        const uint32_t pmin = __reduce_min_sync(0xffffffffu, acc ? rS : 0xffffffffu);
         __syncwarp();
         if (acc) accs[arank] = c;
         __syncwarp();
-        for (uint32_t p = lane; p < sz; p += 32) {
-            const uint64_t v = S[p];
-            const uint32_t np = p + lower_bound64(accs, na, v);
-            if (np < a.P) {
-                T[np] = v;
-                TF[np] = SF[p];
+        for (int32_t hi = int32_t(sz); hi > int32_t(pmin); hi -= 32) {
+            const int32_t p = hi - 32 + int32_t(lane);
+            uint64_t v = 0;
+            uint8_t f = 0;
+            uint32_t np = 0xffffffffu;
+            if (p >= int32_t(pmin)) {
+                v = S[p];
+                f = SF[p];
+                np = uint32_t(p) + lower_bound64(accs, na, v);
             }
+            __syncwarp();
+            if (np < a.P) {
+                S[np] = v;
+                SF[np] = f;
+            }
+            __syncwarp();
         }
         if (acc && rS + arank < a.P) {
-            T[rS + arank] = c;
-            TF[rS + arank] = 1;  // arrived this round: flag_new
+            S[rS + arank] = c;
+            SF[rS + arank] = 1;  // arrived this round: flag_new
         }
         __syncwarp();
         sz = min(a.P, sz + na);
-        uint64_t* tk = S;
-        S = T;
-        T = tk;
-        uint8_t* tf = SF;
-        SF = TF;
-        TF = tf;
         accepted += na;
         tail = sz == a.P ? S[a.P - 1] : kEmptyKey;
     }
@@ -623,10 +659,8 @@ __global__ void replay_kernel(RArgs a) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* base = sm + size_t(warp) * replay_warp_bytes(a.P, a.runmax);
     uint64_t* S = reinterpret_cast<uint64_t*>(base);
-    uint64_t* T = reinterpret_cast<uint64_t*>(base + al16(size_t(a.P) * 8));
-    uint8_t* SF = base + al16(size_t(a.P) * 8) * 2;
-    uint8_t* TF = SF + al16(a.P);
-    uint64_t* accs = reinterpret_cast<uint64_t*>(TF + al16(a.P));
+    uint8_t* SF = base + al16(size_t(a.P) * 8);
+    uint64_t* accs = reinterpret_cast<uint64_t*>(SF + al16(a.P));
     uint64_t* wk = accs + 32;
     uint64_t* runkey = wk + 32;
     uint32_t* pstart = reinterpret_cast<uint32_t*>(runkey + a.runmax);
@@ -643,10 +677,10 @@ __global__ void replay_kernel(RArgs a) {
         uint32_t nr;
         if (a.g_runkey) {
             const uint64_t o = a.g_off[w];
-            nr = replay_target(a, t, S, T, SF, TF, accs, wk, a.g_runkey + o, a.g_pstart + o, a.g_seqoff + o,
+            nr = replay_target(a, t, S, SF, accs, wk, a.g_runkey + o, a.g_pstart + o, a.g_seqoff + o,
                                0xffffffffu, changes);
         } else {
-            nr = replay_target(a, t, S, T, SF, TF, accs, wk, runkey, pstart, seqoff, a.runmax, changes);
+            nr = replay_target(a, t, S, SF, accs, wk, runkey, pstart, seqoff, a.runmax, changes);
         }
         if (nr && lane == 0) {
             const uint32_t d = atomicAdd(a.ndef, 1u);
