@@ -26,7 +26,14 @@ Accuracy is scored on a seeded 10,000-point sample against exact top-100 rows
 --impl reference runs the unmodified reference library (oracle/_ref, built
 from /root/reference by oracle/Makefile) on all host cores on a bounded sample:
 the same build (init + the same number of NN-descent iterations) on the first
-`ref_points` points of the same dataset, scaled linearly to the full N.
+`ref_points` points of the same dataset (inputs from oracle/'s byte-identical
+generator: that process never loads the product library); ms_per_step is the
+measured sample time, `value` extrapolates it to N with the exponent fitted
+between two nested prefixes.  The GPU arm's `cpu_baseline` runs the same
+reference timing plus the reference searcher at the chosen sweep point and
+brute_force_knn on 1000 sampled rows, and checks the GPU results against them.
+
+--gpus N (N > 1) relaunches itself under torchrun, one rank per GPU.
 """
 from __future__ import annotations
 
@@ -48,7 +55,7 @@ CONFIGS = {
     # configs[1] of BASELINE.json: the headline workload
     "cfg2": dict(n=1_000_000, dim=128, n_queries=10_000, centers=1000, trees=8, leaf=8, k=100, P=100, S=20,
                  max_iters=10, dep=4, k_return=100, sweep=[100, 200, 300, 400, 500, 600, 800, 1000],
-                 acc_sample=10_000, ref_points=65_536, ref_queries=500),
+                 acc_sample=10_000, ref_points=131_072, ref_queries=500),
     # configs[0]: the reference's own CPU-runnable case (R=50 is not expressible: reverse cap = S)
     "cfg1": dict(n=100_000, dim=128, n_queries=1000, centers=100, trees=4, leaf=10, k=10, P=30, S=10,
                  max_iters=8, dep=4, k_return=10, sweep=[50, 100, 200], acc_sample=10_000, ref_points=100_000,
@@ -61,7 +68,7 @@ CONFIGS = {
     # assumed), runnable on one GPU too; its cfg4-style exact graph (6.4e13 pairs) is not run
     "cfg5": dict(n=8_000_000, dim=128, n_queries=80_000, centers=4000, trees=8, leaf=8, k=100, P=100, S=20,
                  max_iters=10, dep=4, k_return=100, sweep=[100, 200, 400, 800], acc_sample=10_000,
-                 ref_points=65_536, ref_queries=500, skip_exact=True),
+                 ref_points=131_072, ref_queries=500, skip_exact=True),
     # a small smoke-sized case for quick checks
     "tiny": dict(n=50_000, dim=128, n_queries=1000, centers=100, trees=4, leaf=8, k=20, P=40, S=10,
                  max_iters=6, dep=4, k_return=20, sweep=[40, 80, 160], acc_sample=2000, ref_points=50_000,
@@ -76,12 +83,17 @@ def _log(msg):
     print(f"[bench +{time.time() - _T0:.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
-def gen_data(cfg, n=None):
-    import paper_1609_07228_b200 as A
+def gen_data(cfg, n=None, lib=None):
+    """The config's base and query sets.  `lib` is the generator: the product's
+    annk_gen_mixture (GPU arm) or its byte-identical restatement under oracle/
+    (reference arm: that process must not load the product library)."""
+    if lib is None:
+        import paper_1609_07228_b200 as A
+        lib = A
     n = cfg["n"] if n is None else n
     lo, hi, sd, clo, chi, rnd = cfg.get("mix", (0.0, 128.0, 16.0, 0.0, 255.0, True))
-    base = A.gen_mixture(n, cfg["dim"], cfg["centers"], lo, hi, sd, clo, chi, rnd, SEED, 1)
-    queries = A.gen_mixture(cfg["n_queries"], cfg["dim"], cfg["centers"], lo, hi, sd, clo, chi, rnd, SEED, 2)
+    base = lib.gen_mixture(n, cfg["dim"], cfg["centers"], lo, hi, sd, clo, chi, rnd, SEED, 1)
+    queries = lib.gen_mixture(cfg["n_queries"], cfg["dim"], cfg["centers"], lo, hi, sd, clo, chi, rnd, SEED, 2)
     return base, queries
 
 
@@ -178,52 +190,85 @@ def max_over_ranks(ws, v: float) -> float:
 
 # --------------------------------------------------------- reference arm
 
-def cpu_reference_build(cfg, iters, base=None):
-    """Reference library (oracle/_ref) build on the first ref_points points:
-    init_graph + `iters` NN-descent iterations, all host cores.  Returns
-    (measured seconds, points, cores, init_s, refine_s)."""
-    from oracle import oracle as O
-    ref = O.load("reference")
-    m = cfg["ref_points"]
-    if base is None:
-        base, _ = gen_data(cfg, n=m)
-    x = np.ascontiguousarray(base[:m])
-    cores = os.cpu_count() or 1
+def cpu_reference_build(ref, x, cfg, iters, cores):
+    """Reference library (oracle/_ref) build on the rows x: build_forest, then
+    build_graph (init_graph + `iters` NN-descent iterations, all host cores).
+    Returns the reference's own StopWatch seconds (init + refine)."""
     vs = ref.vs(x)
     forest = ref.build_forest(vs, cfg["trees"], cfg["leaf"], SEED, workers=cores)
-    _, _, log, summ = ref.build_graph(vs, forest, k=cfg["k"], conquer_depth=cfg["dep"], pool_cap=cfg["P"],
-                                      sample_cap=cfg["S"], max_iters=iters, strategy=0, seed=SEED,
-                                      workers=cores, min_change_rate=0.0)
-    return float(summ[0] + summ[1]), m, cores, float(summ[0]), float(summ[1])
+    _, _, _, summ = ref.build_graph(vs, forest, k=cfg["k"], conquer_depth=cfg["dep"], pool_cap=cfg["P"],
+                                    sample_cap=cfg["S"], max_iters=iters, strategy=0, seed=SEED, workers=cores,
+                                    min_change_rate=0.0)
+    return float(summ[0] + summ[1])
+
+
+def ref_samples(cfg):
+    """Two nested prefixes of the config's base set for the reference timing:
+    the build time of the larger one is extrapolated to N with the exponent
+    fitted between the two (per-point work grows with N: deeper trees, larger
+    working sets), not linearly."""
+    m2 = min(cfg["n"], cfg["ref_points"])
+    return max(2048, m2 // 2), m2
+
+
+def fit_exponent(t1, m1, t2, m2):
+    import math
+    if m2 <= m1 or t1 <= 0 or t2 <= 0:
+        return 1.0
+    return max(1.0, math.log(t2 / t1) / math.log(m2 / m1))
 
 
 def run_reference(args, cfg, ws, rank):
+    """--impl reference: the unmodified reference library compiled from
+    /root/reference (oracle/_ref) on this box's host cores.  This process never
+    loads the product library (inputs come from oracle/'s generator)."""
     if rank != 0:
         return
     from oracle import oracle as O
     if not O.reference_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libannkit_ref.so not built"}))
         return
+    ref, gen = O.load("reference"), O.load("oracle")
+    cores = os.cpu_count() or 1
     iters = cfg["ref_iters"]
-    base, _ = gen_data(cfg, n=cfg["ref_points"])
-    for _ in range(args.warmup):
-        cpu_reference_build(cfg, iters, base)
+    m1, m2 = ref_samples(cfg)
+    base, _ = gen_data(cfg, n=m2, lib=gen)
+    # exponent fit (untimed, counts as warm-up)
+    t1 = cpu_reference_build(ref, base[:m1], cfg, iters, cores)
+    t2 = cpu_reference_build(ref, base, cfg, iters, cores)
+    alpha = fit_exponent(t1, m1, t2, m2)
+    for _ in range(max(0, args.warmup - 2)):
+        cpu_reference_build(ref, base, cfg, iters, cores)
     times = []
+    w0 = time.perf_counter()
     for _ in range(args.steps):
-        t, m, cores, _, _ = cpu_reference_build(cfg, iters, base)
-        times.append(t * cfg["n"] / m)
-    v = statistics.mean(times)
-    sample = (f"reference build_graph (init + {iters} NN-descent iterations, {cfg['trees']} trees leaf "
-              f"{cfg['leaf']}) on the first {cfg['ref_points']} of {cfg['n']} points, {os.cpu_count()} workers, "
-              f"seconds scaled x{cfg['n'] / cfg['ref_points']:.2f} to N")
+        times.append(cpu_reference_build(ref, base, cfg, iters, cores))
+    wall = (time.perf_counter() - w0) / max(1, args.steps)
+    t = statistics.mean(times)
+    factor = (cfg["n"] / m2) ** alpha
+    v = t * factor
+    sample = (f"reference build_graph (init + {iters} NN-descent iterations, the crossing of accuracy 0.9; "
+              f"{cfg['trees']} trees leaf {cfg['leaf']}) on the first {m2} of {cfg['n']} points, {cores} workers, "
+              f"{t:.3f} s measured per step, extrapolated x{factor:.2f} = (N/{m2})^{alpha:.3f}, the exponent "
+              f"fitted from {m1} ({t1:.3f} s) and {m2} ({t2:.3f} s) points")
     line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.config, "n": cfg["n"], "dim": cfg["dim"], "trees": cfg["trees"],
                        "leaf_cap": cfg["leaf"], "k": cfg["k"], "pool_cap": cfg["P"], "sample_cap": cfg["S"],
-                       "iterations_to_acc_0.9": iters},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": os.cpu_count(), "kind": "reference", "sample": sample},
+                       "iterations_to_acc_0.9": iters, "measured_points": m2,
+                       "extrapolation": {"exponent": alpha, "factor": factor, "fit_points": [m1, m2],
+                                         "fit_seconds": [t1, t2]}},
+            "host_wall_s_per_step": wall,
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:  # evidence: this arm ran the reference library only
+        with open("/proc/self/maps") as fh:
+            maps = fh.read()
+        line["libraries"] = sorted({ln.split()[-1].split("/")[-1] for ln in maps.splitlines()
+                                    if "annkit" in ln or "oracle" in ln})
+    except OSError:
+        pass
     print(json.dumps(line))
 
 
@@ -287,6 +332,96 @@ def timed_search(searcher, qs, p, ev, reps=3):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) / 1e3)
     return r, statistics.median(ts)
+
+
+def cpu_baseline_leg(args, cfg, A, base, queries, crossing, graph, gpu_search, chosen, exact_sample, rows):
+    """The reference library on the box's host cores (rank 0, N=1), with the
+    same inputs as the GPU arm, and the GPU results checked against it:
+      build  - build_graph on two nested prefixes of the base set, extrapolated
+               to N with the fitted exponent; the GPU pools on the smaller prefix
+               are compared with the reference's after init and every round;
+      search - the reference's batched GraphSearcher::search (search.cpp:182-236)
+               over all queries at the chosen sweep point, with the GPU-built
+               graph and the reference's own forest (bit-identical to the GPU's);
+      exact  - brute_force_knn on 1000 sampled base rows (rows are independent,
+               so the time scales exactly linearly to N rows)."""
+    from oracle import oracle as O
+    if not O.reference_available():
+        return None
+    ref = O.load("reference")
+    cores = os.cpu_count() or 1
+    n, k = cfg["n"], cfg["k"]
+    out = {"unit": "s", "cores": cores, "kind": "reference"}
+    # build: exponent fit on two prefixes
+    m1, m2 = ref_samples(cfg)
+    t1 = cpu_reference_build(ref, base[:m1], cfg, crossing, cores)
+    t2 = cpu_reference_build(ref, base[:m2], cfg, crossing, cores)
+    alpha = fit_exponent(t1, m1, t2, m2)
+    factor = (n / m2) ** alpha
+    out["value"] = t2 * factor
+    out["sample"] = (f"reference build_graph (init + {crossing} iterations) on the first {m2} of {n} points, {cores} "
+                     f"workers, {t2:.3f} s measured, extrapolated x{factor:.2f} = (N/{m2})^{alpha:.3f}, the exponent "
+                     f"fitted from {m1} ({t1:.3f} s) and {m2} points")
+    out["extrapolation"] = {"exponent": alpha, "factor": factor, "fit_points": [m1, m2], "fit_seconds": [t1, t2]}
+    # build parity on the m1 prefix: pools, flags and dist_comps after init and each round
+    _log("cpu baseline: build parity")
+    xs = np.ascontiguousarray(base[:m1])
+    vo = ref.vs(xs)
+    so = ref.init_graph(vo, ref.build_forest(vo, cfg["trees"], cfg["leaf"], SEED, workers=cores), k, cfg["dep"],
+                        cfg["P"], cfg["S"], SEED, workers=cores)
+    vd = A.VectorSet(xs)
+    sd = A.init_graph(vd, A.build_forest(vd, cfg["trees"], cfg["leaf"], SEED), k, cfg["dep"], cfg["P"], cfg["S"],
+                      SEED)
+    checks = []
+    for rnd in range(crossing + 1):
+        if rnd:
+            so.nn_descent_iteration(vo, workers=cores)
+            A.detail.nn_descent_iteration(sd, vd)
+        e = so.export()
+        sz, ids, dists, flags = sd.pools()
+        same = bool(np.array_equal(sz, e["sizes"]))
+        if same:
+            P = cfg["P"]
+            mask = np.arange(P)[None, :] < sz[:, None]
+            same = (np.array_equal(ids[mask], e["ids"][mask]) and
+                    np.array_equal(dists[mask].view(np.uint32), e["dists"][mask].view(np.uint32)) and
+                    np.array_equal(flags[mask] & 1, e["flags"][mask] & 1))
+        checks.append({"round": rnd, "pools_flags_equal": bool(same),
+                       "dist_comps_equal": sd.meta()["dist_comps"] == e["dist_comps"]})
+    out["build_parity"] = {"points": m1, "rounds": checks,
+                           "all_equal": all(c["pools_flags_equal"] and c["dist_comps_equal"] for c in checks)}
+    del so, sd, vd
+    # search at the chosen point: the reference searcher over all queries, all cores
+    if chosen is not None:
+        _log("cpu baseline: search")
+        vb = ref.vs(base)
+        fo = ref.build_forest(vb, cfg["trees"], cfg["leaf"], SEED, workers=cores)
+        qo = ref.vs(queries)
+        t0 = time.perf_counter()
+        ids_s, _, _ = ref.search(vb, fo, graph.ids, qo, cfg["k_return"], chosen["pool"], chosen["expansion"],
+                                 chosen["iters"], workers=cores)
+        ts = time.perf_counter() - t0
+        out["search"] = {"value": len(queries) / ts, "unit": "queries/s", "cores": cores,
+                         "point": {"pool": chosen["pool"], "expansion": chosen["expansion"],
+                                   "iters": chosen["iters"]},
+                         "sample": f"all {len(queries)} queries through the reference GraphSearcher "
+                                   f"(recall_curve batch, {cores} workers), GPU-built graph, reference forest",
+                         "ids_equal_gpu": bool(gpu_search is not None and np.array_equal(ids_s, gpu_search.ids))}
+        del vb, fo
+    # exact kNN rows: 1000 sampled rows (query mode, k + 1, the row itself removed)
+    if exact_sample is not None:
+        _log("cpu baseline: exact kNN rows")
+        sel = rows[:len(exact_sample)]
+        vb = ref.vs(base)
+        t0 = time.perf_counter()
+        ids_q = ref.brute_force(vb, ref.vs(np.ascontiguousarray(base[sel])), k + 1, workers=cores)
+        tq = time.perf_counter() - t0
+        self_rm = np.array([row[row != i][:k] for row, i in zip(ids_q, sel)])
+        out["exact_knn"] = {"value": tq * n / len(sel), "unit": "s", "cores": cores,
+                            "sample": f"brute_force_knn on {len(sel)} sampled base rows ({tq:.2f} s, {cores} workers), "
+                                      f"scaled x{n / len(sel):.0f} to all {n} rows (rows are independent)",
+                            "ids_equal_gpu": bool(np.array_equal(self_rm, exact_sample))}
+    return out
 
 
 def run_gpu(args, cfg, ws, rank, local):
@@ -404,7 +539,7 @@ def run_gpu(args, cfg, ws, rank, local):
     # search sweep (secondary metric): smallest pool reaching recall@k_return >= 0.9
     searcher = A.GraphSearcher(vs, forest, graph)
     sweep = []
-    chosen = fastest = None
+    chosen = fastest = searcher_result = None
     kr = cfg["k_return"]
     # the reference's search knobs (search.hpp:13-21): pool P (>= k_return), seeds kept E <= P,
     # expansion rounds I; the fastest point reaching recall@k_return >= 0.9 is the headline
@@ -418,6 +553,7 @@ def run_gpu(args, cfg, ws, rank, local):
         sweep.append(row)
         if rec >= 0.9 and it == REF_ITERS and chosen is None:
             chosen = row  # recall_curve's definition: first sweep point (P, then E ascending) at the default I
+            searcher_result = r
         if rec >= 0.9 and (fastest is None or row["qps"] > fastest["qps"]):
             fastest = row
 
@@ -530,7 +666,7 @@ def run_gpu(args, cfg, ws, rank, local):
 
     _log("exact kNN")
     # cfg4: exact kNN graph (self-mode top-k over all N points) on the tcgen05 kernel
-    exact = None
+    exact = exact_sample = None
     if not args.skip_cfg4 and dsinfo["u8"] and not cfg.get("skip_exact"):
         bf_runs = []
         for rep in range(2):  # first call warms the allocator
@@ -556,19 +692,13 @@ def run_gpu(args, cfg, ws, rank, local):
                                              "int8 tensor rate is twice bf16",
                               "traffic": ncu_traffic(args.config, kname)},
                  "row0_first5": [int(x) for x in ids_all[0, :5]]}
+        exact_sample = ids_all[rows[:1000]].copy()
         del ids_all
 
     _log("cpu baseline")
-    # CPU baseline: the reference library on a bounded sample (rank 0, N=1)
-    cpu = None
-    if rank == 0 and ws == 1 and not args.skip_cpu:
-        from oracle import oracle as O
-        if O.reference_available():
-            cfg_ref = dict(cfg)
-            t, m, cores, _, _ = cpu_reference_build(cfg_ref, crossing, base)
-            cpu = {"value": t * n / m, "unit": "s", "cores": cores, "kind": "reference",
-                   "sample": f"reference build_graph (init + {crossing} iterations) on the first {m} of {n} points, "
-                             f"{cores} workers, {t:.2f} s measured, scaled x{n / m:.2f} to N"}
+    # CPU baseline: the reference library (oracle/_ref) on this box's host cores, rank 0 at N=1
+    cpu = cpu_baseline_leg(args, cfg, A, base, queries, crossing, graph, searcher_result, chosen, exact_sample,
+                           rows) if (rank == 0 and ws == 1 and not args.skip_cpu) else None
 
     clocks = clk.summary()
     line = {
@@ -804,6 +934,20 @@ def main():
     ap.add_argument("--comm", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 collectives; gloo keeps buffers on the host (functional runs on one GPU)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torchrun (the driver may
+        # also launch it that way itself, in which case WORLD_SIZE is already set)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd, env=env))
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator setup is logged for the driver
     cfg = dict(CONFIGS[args.config])
     cfg.setdefault("ref_iters", {"cfg2": 2, "cfg1": 3, "cfg3": 3, "cfg5": 2, "tiny": 3}[args.config])
     ws, rank, local = dist_setup(args)

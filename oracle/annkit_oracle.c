@@ -177,6 +177,55 @@ static void parallel_for(uint32_t n, uint32_t workers, range_fn fn, void* ctx) {
     free(jobs);
 }
 
+/* The BASELINE configs' seeded Gaussian mixture (DESIGN.md "Synthetic
+ * inputs"; the reference has no mixture generator).  The same arithmetic as
+ * the product's annk_gen_mixture — counter-based streams, so any thread split
+ * yields the same bytes — restated here so the CPU baseline and the reference
+ * arm can build their inputs without loading the product library:
+ *   u(s, j) = (mix64(s + j) >> 11) * 2^-53
+ *   center[c][j] = lo + (hi - lo) * u(substream(seed, 0), c*dim + j)
+ *   point i of stream sid: ps = substream(substream(seed, sid), i),
+ *     c = mix64(ps) % n_centers, z_j = sqrt(-2 ln(1-u(ps,1+2j))) cos(2 pi u(ps,2+2j)),
+ *     v = clip(center[c][j] + sd * z_j), optionally nearbyint. */
+typedef struct {
+    const double* centers;
+    uint32_t dim, n_centers;
+    uint64_t ss;
+    double sd, clo, chi;
+    int rnd;
+    float* out;
+} mix_ctx;
+static double mix_u(uint64_t s, uint64_t j) { return (double)(ora_mix64(s + j) >> 11) * 0x1p-53; }
+static void mix_range(void* c, uint32_t b, uint32_t e) {
+    const mix_ctx* x = c;
+    const double two_pi = 6.283185307179586476925286766559;
+    for (uint32_t i = b; i < e; ++i) {
+        const uint64_t ps = ora_substream(x->ss, i);
+        const uint32_t cc = (uint32_t)(ora_mix64(ps) % x->n_centers);
+        for (uint32_t j = 0; j < x->dim; ++j) {
+            const double u1 = mix_u(ps, 1 + 2ull * j), u2 = mix_u(ps, 2 + 2ull * j);
+            const double z = sqrt(-2.0 * log(1.0 - u1)) * cos(two_pi * u2);
+            double v = x->centers[(size_t)cc * x->dim + j] + x->sd * z;
+            v = v < x->clo ? x->clo : v;
+            v = v > x->chi ? x->chi : v;
+            if (x->rnd) v = nearbyint(v);
+            x->out[(size_t)i * x->dim + j] = (float)v;
+        }
+    }
+}
+void ora_gen_mixture(uint32_t n, uint32_t dim, uint32_t n_centers, float center_lo, float center_hi, float sd,
+                     float clip_lo, float clip_hi, int round_to_int, uint64_t seed, uint32_t stream_id,
+                     uint32_t workers, float* out) {
+    double* centers = xmalloc(sizeof(double) * (size_t)n_centers * dim);
+    const uint64_t s0 = ora_substream(seed, 0);
+    for (size_t i = 0; i < (size_t)n_centers * dim; ++i)
+        centers[i] = (double)center_lo + ((double)center_hi - (double)center_lo) * mix_u(s0, i);
+    mix_ctx x = {centers, dim, n_centers, ora_substream(seed, stream_id), (double)sd, (double)clip_lo,
+                 (double)clip_hi, round_to_int, out};
+    parallel_for(n, workers, mix_range, &x);
+    free(centers);
+}
+
 /* --------------------------------------------------------------- pool ---- */
 /* neighbor_pool.hpp:9-69: ascending (dist, id), capacity-bounded, a duplicate
  * id (same id and dist at the insertion slot) keeps the existing entry. */

@@ -72,6 +72,9 @@ class OracleLib:
         L.ora_vs_create.argtypes = [_f32p, _u32, _u32]
         L.ora_vs_free.argtypes = [_vp]
         L.ora_gen_synthetic.argtypes = [_u32, _u32, _u64, _f32p]
+        if hasattr(L, "ora_gen_mixture"):  # restatement only (not a reference function)
+            L.ora_gen_mixture.argtypes = [_u32, _u32, _u32, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float,
+                                          C.c_int, _u64, _u32, _u32, _f32p]
         L.ora_l2_sq.restype = C.c_float
         L.ora_l2_sq.argtypes = [_f32p, _f32p, _u32]
         L.ora_mix64.restype = _u64
@@ -142,6 +145,16 @@ class OracleLib:
     def gen_synthetic(self, n: int, dim: int, seed: int) -> np.ndarray:
         out = np.empty((n, dim), np.float32)
         self.L.ora_gen_synthetic(n, dim, seed, out)
+        return out
+
+    def gen_mixture(self, n, dim, n_centers, center_lo, center_hi, sd, clip_lo, clip_hi, round_to_int, seed,
+                    stream_id, workers=None) -> np.ndarray:
+        """The BASELINE configs' seeded Gaussian mixture, byte-identical to the
+        product's annk_gen_mixture (tests/test_oracle_pin.py pins it)."""
+        out = np.empty((n, dim), np.float32)
+        w = workers or max(1, min(os.cpu_count() or 1, n // 4096))
+        self.L.ora_gen_mixture(n, dim, n_centers, center_lo, center_hi, sd, clip_lo, clip_hi, int(bool(round_to_int)),
+                               seed, stream_id, w, out)
         return out
 
     def mt19937_64(self, seed: int, count: int) -> np.ndarray:

@@ -33,6 +33,10 @@ const char* ora_impl_name(void);
 void* ora_vs_create(const float* data, uint32_t n, uint32_t dim);
 void ora_vs_free(void* vs);
 void ora_gen_synthetic(uint32_t n, uint32_t dim, uint64_t seed, float* out);
+/* the BASELINE configs' Gaussian mixture (restatement of annk_gen_mixture; not a reference function) */
+void ora_gen_mixture(uint32_t n, uint32_t dim, uint32_t n_centers, float center_lo, float center_hi, float sd,
+                     float clip_lo, float clip_hi, int round_to_int, uint64_t seed, uint32_t stream_id,
+                     uint32_t workers, float* out);
 float ora_l2_sq(const float* a, const float* b, uint32_t dim);
 uint64_t ora_mix64(uint64_t x);
 uint64_t ora_substream(uint64_t seed, uint64_t id);

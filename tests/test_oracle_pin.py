@@ -206,3 +206,21 @@ def test_golden_fixtures(ora):
     assert np.array_equal(g, z["exact_ids"])
     ids, d, st = ora.search(vs, f, g, ora.vs(z["queries"]), int(z["k"]), 40, 20, 4)
     assert np.array_equal(ids, z["search_ids"]) and np.array_equal(st, z["search_stats"])
+
+
+@pytest.mark.parametrize("args", [
+    (5000, 128, 100, 0.0, 128.0, 16.0, 0.0, 255.0, True, 1, 1),     # cfg1/2/5 mixture, base stream
+    (700, 128, 1000, 0.0, 128.0, 16.0, 0.0, 255.0, True, 1, 2),     # query stream
+    (900, 960, 500, 0.05, 0.35, 0.05, 0.0, 1.0, False, 1, 1),       # cfg3 mixture
+    (333, 13, 7, -3.0, 5.0, 2.5, -1.0, 4.0, False, 9, 3),
+])
+def test_oracle_mixture_generator_is_byte_identical(args):
+    # the reference arm and the CPU baseline build their inputs with oracle/'s
+    # restatement of annk_gen_mixture (that process never loads the product);
+    # both must produce the same bytes, for any thread split
+    import paper_1609_07228_b200 as A
+    o = O.load("oracle")
+    a = A.gen_mixture(*args)
+    for w in (1, 3, 8):
+        b = o.gen_mixture(*args, workers=w)
+        np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
