@@ -553,7 +553,7 @@ def run_gpu(args, cfg, ws, rank, local):
         sweep.append(row)
         if rec >= 0.9 and it == REF_ITERS and chosen is None:
             chosen = row  # recall_curve's definition: first sweep point (P, then E ascending) at the default I
-            searcher_result = r
+            searcher_result = A.BatchResult(r.ids.copy(), r.dists.copy(), r.stats.copy())  # out= buffers are reused
         if rec >= 0.9 and (fastest is None or row["qps"] > fastest["qps"]):
             fastest = row
 
