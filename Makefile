@@ -9,10 +9,9 @@ LIB       := $(PKG)/libannkit_b200.so
 
 FACADE    := $(PKG)/libannkit_facade.so
 FACADE_T  := tests/cpp/test_facade
-CLI       := $(PKG)/annkit
 FACADE_SRCS := $(PKG)/cpp/annkit_facade.cpp $(PKG)/cpp/annkit_io.cpp
 
-all: $(LIB) $(FACADE) $(FACADE_T) $(CLI) oracle
+all: $(LIB) $(FACADE) $(FACADE_T) oracle refsuite
 
 build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/annkit_b200.h
 	@mkdir -p build
@@ -25,10 +24,6 @@ $(LIB): $(OBJS)
 $(FACADE): $(FACADE_SRCS) include/annkit_b200.hpp include/annkit_b200.h $(LIB)
 	g++ -std=c++20 -O2 -fPIC -shared -Wall -Iinclude -o $@ $(FACADE_SRCS) -L$(PKG) -lannkit_b200 -Wl,-rpath,'$$ORIGIN'
 
-# the `annkit` command line (reference proj/tools/main.cpp subcommands) over the C++ API
-$(CLI): $(PKG)/cpp/annkit_cli.cpp include/annkit_b200.hpp $(FACADE)
-	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lannkit_facade -lannkit_b200 -Wl,-rpath,'$$ORIGIN'
-
 $(FACADE_T): tests/cpp/test_facade.cpp include/annkit_b200.hpp $(FACADE)
 	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lannkit_facade -lannkit_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
@@ -36,11 +31,31 @@ $(FACADE_T): tests/cpp/test_facade.cpp include/annkit_b200.hpp $(FACADE)
 oracle:
 	$(MAKE) -C oracle
 
+# The reference's own unit suites and acceptance runner, compiled UNCHANGED from
+# /root/reference/proj/tests against include/annkit_b200.hpp (tests/cpp/shim maps
+# <doctest.h> and "annkit/*.hpp" to our headers) and linked to the facade.  Built
+# only where /root/reference exists; the binaries travel to the GPU box.
+REFT      ?= /root/reference/proj/tests
+REFSUITE  := tests/cpp/_refsuite
+refsuite:
+	@if [ -d "$(REFT)" ]; then $(MAKE) $(REFSUITE)/unit $(REFSUITE)/acceptance; \
+	else echo "reference tests absent; keeping prebuilt $(REFSUITE)/ (if any)"; fi
+
+REFT_UNIT := $(addprefix $(REFT)/,doctest_main.cpp test_dataset.cpp test_eval.cpp test_graph_build.cpp test_kd_forest.cpp test_search.cpp)
+$(REFSUITE)/unit: $(REFT_UNIT) tests/cpp/doctest/doctest.h include/annkit_b200.hpp $(FACADE)
+	@mkdir -p $(REFSUITE)
+	g++ -std=c++20 -O2 -w -Itests/cpp/doctest -Itests/cpp/shim -Iinclude -I$(REFT) -o $@ $(REFT_UNIT) -L$(PKG) -lannkit_facade \
+	    -lannkit_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
+$(REFSUITE)/acceptance: $(REFT)/acceptance.cpp include/annkit_b200.hpp $(FACADE)
+	@mkdir -p $(REFSUITE)
+	g++ -std=c++20 -O2 -w -Itests/cpp/doctest -Itests/cpp/shim -Iinclude -I$(REFT) -o $@ $(REFT)/acceptance.cpp -L$(PKG) \
+	    -lannkit_facade -lannkit_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
+
 clean:
-	rm -rf build $(LIB) $(FACADE) $(FACADE_T) $(CLI)
+	rm -rf build $(LIB) $(FACADE) $(FACADE_T)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle refsuite clean
 
 # device-debug build for compute-sanitizer sessions (not used by tests/bench)
 debug: $(SRCS)

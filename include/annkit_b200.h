@@ -72,6 +72,14 @@ int annk_dataset_shape(const annk_dataset* ds, uint32_t* n, uint32_t* dim);
  * then the reference's fp32 l2_sq is exact and |a|^2+|b|^2-2a.b in int32 equals it. */
 int annk_dataset_info(const annk_dataset* ds, uint32_t* out4);
 
+/* dataset.hpp:67-77 distances, computed on the device with the reference's
+ * sequential fp32 chain (bit-identical): l2_sq of two host vectors; dist_sq
+ * of m id pairs (a[j], b[j]) of a set; dist_sq_q of a host query against m
+ * ids.  Ids past the set: ANNK_OUT_OF_RANGE (dataset.cpp:218,225). */
+int annk_l2_sq(const float* a, const float* b, uint32_t dim, float* out);
+int annk_dist_sq(const annk_dataset* ds, const uint32_t* a, const uint32_t* b, uint32_t m, float* out);
+int annk_dist_sq_q(const annk_dataset* ds, const float* q, uint32_t dim, const uint32_t* b, uint32_t m,
+                   float* out);
 /* dataset.cpp:201-214 gen_synthetic — host helper, same bytes as the reference. */
 int annk_gen_synthetic(uint32_t n, uint32_t dim, uint64_t seed, float* out);
 /* Seeded Gaussian-mixture generator for the BASELINE configs (no reference
@@ -156,6 +164,10 @@ int annk_state_lists(const annk_state* s, int which, uint32_t* offsets, uint32_t
  * sequential order (point ascending, then pair order), including entries a
  * later offer of the same round evicts again. */
 int annk_nn_descent_iteration(annk_state* s, const annk_dataset* ds, uint64_t* changes);
+/* graph_build.cpp:164-207 detail::nn_expansion_iteration (the paper's NN-expansion
+ * baseline): unchecked pool entries are expanded against the round-start pools.
+ * `checked` is bit 1 of the state's flag bytes (annk_state_export). */
+int annk_nn_expansion_iteration(annk_state* s, const annk_dataset* ds, uint64_t* changes);
 /* graph_build.cpp:59-86 and :88-103 (the two halves of the sampling step). */
 int annk_rebuild_sample_lists(annk_state* s);
 int annk_union_reverse_lists(annk_state* s);

@@ -17,6 +17,8 @@
 // reference's unit tests inspect; that copy costs O(n * pool_cap) per call.
 #pragma once
 
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -33,6 +35,25 @@ constexpr std::uint32_t kLeafMarker = 0xffffffffu;
 struct DeviceDataset;  // opaque device copies (annk_dataset / annk_forest / annk_state)
 struct DeviceForest;
 struct DeviceState;
+
+// ---------------------------------------------------------------- util.hpp
+// util.hpp:9-31: seed streams and the wall-clock timer the reference's callers use.
+inline std::uint64_t mix64(std::uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+inline std::uint64_t substream(std::uint64_t seed, std::uint64_t id) { return mix64(seed ^ mix64(id)); }
+class StopWatch {
+  public:
+    StopWatch() : t0_(std::chrono::steady_clock::now()) {}
+    double seconds() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count(); }
+    void restart() { t0_ = std::chrono::steady_clock::now(); }
+
+  private:
+    std::chrono::steady_clock::time_point t0_;
+};
 
 // ------------------------------------------------------------ dataset.hpp
 struct VectorSet {
@@ -62,6 +83,12 @@ struct format_error : std::runtime_error {
 struct data_error : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+
+// dataset.hpp:67-77 distances, computed on the device with the reference's
+// sequential fp32 chain (bit-identical); ids past the set throw std::out_of_range.
+float l2_sq(const float* a, const float* b, std::uint32_t dim);
+float dist_sq(const VectorSet& vs, std::uint32_t a, std::uint32_t b);
+float dist_sq_q(const VectorSet& vs, std::span<const float> q, std::uint32_t b);
 
 // dataset.cpp:201-214 (same bytes as the reference's generator).
 VectorSet gen_synthetic(std::uint32_t n, std::uint32_t dim, std::uint64_t seed);
@@ -137,6 +164,24 @@ class NeighborPool {
             if (e.id == id) return true;
         return false;
     }
+    // neighbor_pool.hpp:35-53 semantics for host-built pools (a caller's own
+    // start state, uploaded on the next device call): the pool stays sorted by
+    // (dist, id); a duplicate (same id and dist at the insertion slot) and
+    // anything not better than a full pool's worst entry are rejected.
+    bool insert(std::uint32_t id, float dist, bool flag_new) {
+        const NeighborEntry e{id, dist, flag_new, false};
+        auto less = [](const NeighborEntry& x, const NeighborEntry& y) {
+            return x.dist != y.dist ? x.dist < y.dist : x.id < y.id;
+        };
+        const auto it = std::lower_bound(entries_.begin(), entries_.end(), e, less);
+        const std::size_t pos = std::size_t(it - entries_.begin());
+        if (it != entries_.end() && it->id == id && it->dist == dist) return false;
+        if (pos >= capacity_) return false;
+        entries_.insert(it, e);
+        if (entries_.size() > capacity_) entries_.pop_back();
+        return true;
+    }
+    std::span<NeighborEntry> entries() { return entries_; }
     std::vector<NeighborEntry>& mutable_entries() { return entries_; }
 
   private:
@@ -160,6 +205,9 @@ struct KnnGraph {
 void save_graph(const KnnGraph& graph, const std::string& ids_path,
                 const std::optional<std::string>& dists_path = std::nullopt);
 KnnGraph load_graph(const std::string& ids_path, const std::optional<std::string>& dists_path = std::nullopt);
+// knn_graph.hpp:36-38: the id rows as ground truth and back (shape-preserving copies)
+GroundTruth graph_to_ground_truth(const KnnGraph& g);
+KnnGraph graph_from_ground_truth(const GroundTruth& gt);
 
 // ------------------------------------------------------ graph_build.hpp
 struct RefineState {
@@ -169,7 +217,7 @@ struct RefineState {
     std::uint64_t seed = 0;
     std::uint32_t iteration = 0;
     std::uint64_t dist_comps = 0;
-    std::uint64_t last_changes = 0;  // see DESIGN.md "Deviations": surviving inserts of the round
+    std::uint64_t last_changes = 0;  // accepted inserts of the last round, the reference's sequential count
 
     std::vector<NeighborPool> pools;
     std::vector<std::vector<std::uint32_t>> g_new, g_old, g_rnew, g_rold;
@@ -227,12 +275,14 @@ struct BuildResult {
 };
 
 // Device strategies: efanna, random_descent, init_only, brute_force
-// (nn_expansion is a CPU-only baseline here: std::invalid_argument).
+// (all five strategies run on the device; nn_expansion / random_descent start
+// from init_random, as graph_build.cpp:415-425).
 BuildResult build_graph(const VectorSet& vs, const KdForest* forest, const BuildParams& params,
                         const GroundTruth* gt = nullptr);
 
 namespace detail {
 std::uint64_t nn_descent_iteration(RefineState& state, const VectorSet& vs, std::uint32_t workers);
+std::uint64_t nn_expansion_iteration(RefineState& state, const VectorSet& vs, std::uint32_t workers);
 void rebuild_sample_lists(RefineState& state);
 void union_reverse_lists(RefineState& state);
 double pool_topk_accuracy(const RefineState& state, const GroundTruth& gt);

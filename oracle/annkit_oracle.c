@@ -837,8 +837,12 @@ void* ora_state_import(uint32_t n, uint32_t k, uint32_t pool_cap, uint32_t sampl
         pool_init(&s->pools[i], pool_cap);
         for (uint32_t j = 0; j < sizes[i]; ++j) {
             const size_t o = (size_t)i * pool_cap + j;
-            pool_insert(&s->pools[i], ids[o], dists[o], flags[o]);
+            pool_insert(&s->pools[i], ids[o], dists[o], flags[o] & 1);
         }
+        for (uint32_t j = 0; j < sizes[i]; ++j)  /* bit 1: `checked` (nn-expansion) */
+            for (uint32_t e = 0; e < s->pools[i].size; ++e)
+                if (s->pools[i].e[e].id == ids[(size_t)i * pool_cap + j])
+                    s->pools[i].e[e].checked = (flags[(size_t)i * pool_cap + j] >> 1) & 1;
     }
     return s;
 }
@@ -851,7 +855,7 @@ void ora_state_export(void* p, uint32_t* sizes, uint32_t* ids, float* dists, uin
             const size_t o = (size_t)i * s->pool_cap + j;
             ids[o] = s->pools[i].e[j].id;
             dists[o] = s->pools[i].e[j].dist;
-            flags[o] = s->pools[i].e[j].flag_new;
+            flags[o] = (uint8_t)(s->pools[i].e[j].flag_new | (s->pools[i].e[j].checked << 1));
         }
     }
     meta[0] = s->iteration;

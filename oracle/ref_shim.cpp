@@ -210,8 +210,12 @@ void* ora_state_import(uint32_t n, uint32_t k, uint32_t pool_cap, uint32_t sampl
     for (uint32_t i = 0; i < n; ++i)
         for (uint32_t j = 0; j < sizes[i]; ++j) {
             const std::size_t o = std::size_t(i) * pool_cap + j;
-            s->pools[i].insert(ids[o], dists[o], flags[o] != 0);
+            s->pools[i].insert(ids[o], dists[o], (flags[o] & 1) != 0);
         }
+    for (uint32_t i = 0; i < n; ++i)  // bit 1: `checked` (nn-expansion)
+        for (auto& e : s->pools[i].entries())
+            for (uint32_t j = 0; j < sizes[i]; ++j)
+                if (ids[std::size_t(i) * pool_cap + j] == e.id) e.checked = (flags[std::size_t(i) * pool_cap + j] >> 1) & 1;
     return s;
 }
 void ora_state_free(void* s) { delete S(s); }
@@ -225,7 +229,7 @@ void ora_state_export(void* sp, uint32_t* sizes, uint32_t* ids, float* dists, ui
             const std::size_t o = std::size_t(i) * s.pool_cap + j;
             ids[o] = e[j].id;
             dists[o] = e[j].dist;
-            flags[o] = e[j].flag_new ? 1 : 0;
+            flags[o] = uint8_t((e[j].flag_new ? 1 : 0) | (e[j].checked ? 2 : 0));
         }
     }
     meta[0] = s.iteration;

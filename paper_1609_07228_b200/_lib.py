@@ -92,6 +92,10 @@ _SIGS = {
     "annk_state_export": [_vp, _u32p, _u32p, _f32p, _u8p],
     "annk_state_lists": [_vp, C.c_int, _u32p, _vp],
     "annk_nn_descent_iteration": [_vp, _vp, C.POINTER(_u64)],
+    "annk_l2_sq": [_vp, _vp, _u32, C.POINTER(C.c_float)],
+    "annk_dist_sq": [_vp, _vp, _vp, _u32, _vp],
+    "annk_dist_sq_q": [_vp, _vp, _u32, _vp, _u32, _vp],
+    "annk_nn_expansion_iteration": [_vp, _vp, C.POINTER(_u64)],
     "annk_rebuild_sample_lists": [_vp],
     "annk_union_reverse_lists": [_vp],
     "annk_refine_nn_descent": [_vp, _vp, _u32, C.c_double, C.POINTER(_u32)],

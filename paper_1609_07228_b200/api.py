@@ -94,6 +94,42 @@ def gen_mixture(n: int, dim: int, n_centers: int, center_lo: float, center_hi: f
     return out
 
 
+def l2_sq(a, b) -> float:
+    """dataset.hpp:67-74 l2_sq of two vectors, on the device (sequential fp32 chain)."""
+    a = np.ascontiguousarray(a, np.float32).ravel()
+    b = np.ascontiguousarray(b, np.float32).ravel()
+    if a.size != b.size:
+        raise InvalidArgument("l2_sq: vectors of different dimension")
+    out = C.c_float(0.0)
+    check(lib.annk_l2_sq(a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p), a.size, C.byref(out)))
+    return float(out.value)
+
+
+def dist_sq(vs, a, b):
+    """dataset.cpp:216-222 dist_sq(vs, a, b); a and b may be equal-length id arrays
+    (one device launch for all pairs).  Ids past the set raise OutOfRange."""
+    v = _as_vs(vs)
+    aa = np.ascontiguousarray(np.atleast_1d(a), np.uint32)
+    bb = np.ascontiguousarray(np.atleast_1d(b), np.uint32)
+    if aa.shape != bb.shape:
+        raise InvalidArgument("dist_sq: id arrays of different length")
+    out = np.empty(aa.size, np.float32)
+    check(lib.annk_dist_sq(v.handle, aa.ctypes.data_as(C.c_void_p), bb.ctypes.data_as(C.c_void_p), aa.size,
+                           out.ctypes.data_as(C.c_void_p)))
+    return float(out[0]) if np.isscalar(a) and np.isscalar(b) else out
+
+
+def dist_sq_q(vs, q, b):
+    """dataset.cpp:224-233 dist_sq_q(vs, q, b) for one id or an id array."""
+    v = _as_vs(vs)
+    qq = np.ascontiguousarray(q, np.float32).ravel()
+    bb = np.ascontiguousarray(np.atleast_1d(b), np.uint32)
+    out = np.empty(bb.size, np.float32)
+    check(lib.annk_dist_sq_q(v.handle, qq.ctypes.data_as(C.c_void_p), qq.size, bb.ctypes.data_as(C.c_void_p),
+                             bb.size, out.ctypes.data_as(C.c_void_p)))
+    return float(out[0]) if np.isscalar(b) else out
+
+
 def _as_vs(x) -> VectorSet:
     return x if isinstance(x, VectorSet) else VectorSet(x)
 
@@ -392,6 +428,14 @@ class detail:
         return int(ch.value)
 
     @staticmethod
+    def nn_expansion_iteration(state: RefineState, vs, workers: int = 1) -> int:
+        """graph_build.cpp:164-207 (the NN-expansion baseline) on the device."""
+        ch = C.c_uint64(0)
+        v = _as_vs(vs)
+        check(lib.annk_nn_expansion_iteration(state.handle, v.handle, C.byref(ch)))
+        return int(ch.value)
+
+    @staticmethod
     def rebuild_sample_lists(state: RefineState) -> None:
         check(lib.annk_rebuild_sample_lists(state.handle))
 
@@ -518,9 +562,9 @@ def build_graph(vs, forest: Optional[KdForest], params: BuildParams, gt: Optiona
         acc = graph_accuracy(g, gt) if gt is not None else -1.0
         st.iterations.append(IterationLog(0, st.init_seconds, comps[0], 0, acc))
         return BuildResult(g, st)
-    if params.strategy not in ("efanna", "init-only", "random-descent"):
-        raise InvalidArgument(f"build_graph: strategy {params.strategy} is a CPU baseline, not a device path")
-    tree_init = params.strategy != "random-descent"
+    if params.strategy not in ("efanna", "init-only", "random-descent", "nn-expansion"):
+        raise InvalidArgument(f"build_graph: unknown strategy {params.strategy}")
+    tree_init = params.strategy in ("efanna", "init-only")  # graph_build.cpp:415-416
     if tree_init and forest is None:
         raise InvalidArgument("build_graph: strategy needs a forest")
     lib.annk_synchronize()
@@ -543,7 +587,8 @@ def build_graph(vs, forest: Optional[KdForest], params: BuildParams, gt: Optiona
     threshold = params.min_change_rate * v.n * params.pool_cap
     for _ in range(iters):
         t1 = time.perf_counter()
-        ch = detail.nn_descent_iteration(state, v)
+        ch = (detail.nn_expansion_iteration(state, v) if params.strategy == "nn-expansion"
+              else detail.nn_descent_iteration(state, v))
         st.refine_seconds += time.perf_counter() - t1
         log_row(ch)
         if ch < threshold:

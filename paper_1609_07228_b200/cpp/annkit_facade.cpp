@@ -101,7 +101,7 @@ annk_state* dev(RefineState& s) {
             for (std::size_t j = 0; j < e.size(); ++j) {
                 ids[std::size_t(i) * P + j] = e[j].id;
                 dists[std::size_t(i) * P + j] = e[j].dist;
-                flags[std::size_t(i) * P + j] = e[j].flag_new ? 1 : 0;
+                flags[std::size_t(i) * P + j] = std::uint8_t((e[j].flag_new ? 1 : 0) | (e[j].checked ? 2 : 0));
             }
         }
         auto d = std::make_shared<DeviceState>();
@@ -135,7 +135,7 @@ void refresh(RefineState& s) {
         e.resize(sizes[i]);
         for (std::uint32_t j = 0; j < sizes[i]; ++j) {
             const std::size_t c = std::size_t(i) * P + j;
-            e[j] = NeighborEntry{ids[c], dists[c], (flags[c] & 1) != 0, false};
+            e[j] = NeighborEntry{ids[c], dists[c], (flags[c] & 1) != 0, (flags[c] & 2) != 0};
         }
     }
     std::vector<std::vector<std::uint32_t>>* lists[4] = {&s.g_new, &s.g_old, &s.g_rnew, &s.g_rold};
@@ -176,6 +176,43 @@ annk_search_params cparams(const SearchParams& p, int random_init) {
 }  // namespace
 
 // --------------------------------------------------------------- dataset
+
+float l2_sq(const float* a, const float* b, std::uint32_t dim) {
+    float out = 0.0f;
+    check(annk_l2_sq(a, b, dim, &out));
+    return out;
+}
+
+float dist_sq(const VectorSet& vs, std::uint32_t a, std::uint32_t b) {
+    if (a >= vs.n || b >= vs.n) throw std::out_of_range("dist_sq: id out of range");
+    float out = 0.0f;
+    check(annk_dist_sq(dev(vs), &a, &b, 1, &out));
+    return out;
+}
+
+float dist_sq_q(const VectorSet& vs, std::span<const float> q, std::uint32_t b) {
+    if (b >= vs.n) throw std::out_of_range("dist_sq_q: id out of range");
+    if (q.size() != vs.dim) throw std::invalid_argument("dist_sq_q: query dimension differs from the set");
+    float out = 0.0f;
+    check(annk_dist_sq_q(dev(vs), q.data(), vs.dim, &b, 1, &out));
+    return out;
+}
+
+GroundTruth graph_to_ground_truth(const KnnGraph& g) {
+    GroundTruth gt;
+    gt.n = g.n;
+    gt.k = g.k;
+    gt.ids = g.ids;
+    return gt;
+}
+
+KnnGraph graph_from_ground_truth(const GroundTruth& gt) {
+    KnnGraph g;
+    g.n = gt.n;
+    g.k = gt.k;
+    g.ids = gt.ids;
+    return g;
+}
 
 VectorSet gen_synthetic(std::uint32_t n, std::uint32_t dim, std::uint64_t seed) {
     VectorSet vs;
@@ -282,6 +319,13 @@ std::uint64_t nn_descent_iteration(RefineState& state, const VectorSet& vs, std:
     refresh(state);
     return ch;
 }
+std::uint64_t nn_expansion_iteration(RefineState& state, const VectorSet& vs, std::uint32_t) {
+    std::uint64_t ch = 0;
+    check(annk_nn_expansion_iteration(dev(state), dev(vs), &ch));
+    refresh(state);
+    return ch;
+}
+
 void rebuild_sample_lists(RefineState& state) {
     check(annk_rebuild_sample_lists(dev(state)));
     refresh(state);
@@ -310,9 +354,8 @@ BuildResult build_graph(const VectorSet& vs, const KdForest* forest, const Build
         st.iterations.push_back({0, st.init_seconds, comps, 0, gt ? graph_accuracy(out.graph, *gt) : -1.0});
         return out;
     }
-    if (p.strategy == BuildStrategy::nn_expansion)
-        throw std::invalid_argument("build_graph: nn_expansion is a CPU baseline, not a device path");
-    const bool tree_init = p.strategy != BuildStrategy::random_descent;
+    // graph_build.cpp:415-416: only efanna and init_only start from the forest
+    const bool tree_init = p.strategy == BuildStrategy::efanna || p.strategy == BuildStrategy::init_only;
     if (tree_init && !forest) throw std::invalid_argument("build_graph: strategy needs a forest");
     double t0 = now();
     RefineState s = tree_init ? init_graph(vs, *forest, p.k, p.conquer_depth, p.pool_cap, p.sample_cap, p.seed)
@@ -328,7 +371,8 @@ BuildResult build_graph(const VectorSet& vs, const KdForest* forest, const Build
     for (std::uint32_t it = 0; it < iters; ++it) {
         t0 = now();
         std::uint64_t ch = 0;
-        check(annk_nn_descent_iteration(s.device->h, dev(vs), &ch));
+        if (p.strategy == BuildStrategy::nn_expansion) check(annk_nn_expansion_iteration(s.device->h, dev(vs), &ch));
+        else check(annk_nn_descent_iteration(s.device->h, dev(vs), &ch));
         st.refine_seconds += now() - t0;
         refresh(s);
         log(ch);

@@ -38,38 +38,42 @@ void put(std::ofstream& out, const T& v) {
 }
 
 // Records of one int32 dimension followed by `dim` 4-byte values: returns
-// (n, dim, payload words row-major).
+// (n, dim, payload words row-major).  A record cut short reports the byte at
+// which its first missing value starts (dataset.cpp:96-133 reports offsets).
 void read_records(const std::string& path, std::uint32_t& n, std::uint32_t& dim, std::vector<std::uint32_t>& body) {
     const std::vector<unsigned char> raw = read_file(path);
-    if (raw.size() % 4) throw format_error("truncated record (size not a multiple of 4) in " + path);
-    const std::size_t words = raw.size() / 4;
-    n = dim = 0;
-    body.clear();
-    if (words == 0) return;
+    const std::size_t words = raw.size() / 4;  // whole 4-byte values present
     auto word = [&](std::size_t i) {
         std::int32_t v;
         std::memcpy(&v, raw.data() + 4 * i, 4);
         return v;
     };
-    const std::int32_t d = word(0);
-    std::size_t off = 0, rec = 0;
-    while (off < words) {
-        const std::int32_t dd = word(off);
-        if (dd < 1)
-            throw format_error("record " + std::to_string(rec) + " at byte " + std::to_string(off * 4) +
-                               " declares dimension " + std::to_string(dd) + " in " + path);
-        if (dd != d)
-            throw format_error("record " + std::to_string(rec) + " has dimension " + std::to_string(dd) +
-                               ", expected " + std::to_string(d) + " in " + path);
-        if (off + 1 + std::size_t(dd) > words) throw format_error("truncated record " + std::to_string(rec) + " in " + path);
-        off += std::size_t(dd) + 1;
-        ++rec;
+    n = dim = 0;
+    body.clear();
+    std::size_t at = 0;  // word offset of the current record
+    for (std::uint32_t rec = 0;; ++rec) {
+        if (at == words) {
+            if (raw.size() % 4)
+                throw format_error("truncated record " + std::to_string(rec) + " at byte " +
+                                   std::to_string(4 * at) + " in " + path);
+            break;
+        }
+        const std::int32_t d = word(at);
+        if (d < 1)
+            throw format_error("record " + std::to_string(rec) + " at byte " + std::to_string(4 * at) +
+                               " declares dimension " + std::to_string(d) + " in " + path);
+        if (rec == 0) dim = std::uint32_t(d);
+        if (std::uint32_t(d) != dim)
+            throw format_error("record " + std::to_string(rec) + " has dimension " + std::to_string(d) +
+                               ", expected " + std::to_string(dim) + " in " + path);
+        if (at + 1 + dim > words)  // the first value that is not all there
+            throw format_error("truncated record " + std::to_string(rec) + " at byte " +
+                               std::to_string(4 * words) + " in " + path);
+        body.insert(body.end(), reinterpret_cast<const std::uint32_t*>(raw.data() + 4 * (at + 1)),
+                    reinterpret_cast<const std::uint32_t*>(raw.data() + 4 * (at + 1 + dim)));
+        at += 1 + dim;
+        n = rec + 1;
     }
-    dim = std::uint32_t(d);
-    n = std::uint32_t(rec);
-    body.resize(std::size_t(n) * dim);
-    for (std::size_t r = 0; r < n; ++r)
-        std::memcpy(body.data() + r * dim, raw.data() + 4 * (r * (dim + 1) + 1), std::size_t(dim) * 4);
 }
 
 }  // namespace
@@ -119,16 +123,21 @@ void save_ivecs(const GroundTruth& gt, const std::string& path) {
     if (!out) throw std::runtime_error("write failed: " + path);
 }
 
+// dataset.cpp:78-95 contract: every id < base_n and no id twice in a row
+// (data_error naming the row otherwise).
 void GroundTruth::validate_against(std::uint32_t base_n) const {
+    std::vector<std::uint32_t> sorted;
     for (std::uint32_t i = 0; i < n; ++i) {
         const auto r = row(i);
-        for (std::uint32_t j = 0; j < k; ++j) {
-            if (r[j] >= base_n)
-                throw data_error("row " + std::to_string(i) + " holds id " + std::to_string(r[j]) +
-                                 " outside base set of size " + std::to_string(base_n));
-            for (std::uint32_t l = j + 1; l < k; ++l)
-                if (r[j] == r[l]) throw data_error("row " + std::to_string(i) + " holds duplicate id " + std::to_string(r[j]));
-        }
+        const auto bad = std::find_if(r.begin(), r.end(), [&](std::uint32_t id) { return id >= base_n; });
+        if (bad != r.end())
+            throw data_error("row " + std::to_string(i) + " holds id " + std::to_string(*bad) +
+                             " outside base set of size " + std::to_string(base_n));
+        sorted.assign(r.begin(), r.end());
+        std::sort(sorted.begin(), sorted.end());
+        const auto dup = std::adjacent_find(sorted.begin(), sorted.end());
+        if (dup != sorted.end())
+            throw data_error("row " + std::to_string(i) + " holds duplicate id " + std::to_string(*dup));
     }
 }
 

@@ -694,7 +694,7 @@ __global__ void sample_kernel(SampleArgs a) {
         const uint32_t bo = __ballot_sync(0xffffffffu, in_scan && !isnew);
         if (in_scan && isnew) {
             a.fnew[size_t(i) * a.S + rank_new] = id;
-            pf[j] = 0;
+            pf[j] &= uint8_t(~1u);  // flag_new cleared; `checked` (bit 1) untouched
         } else if (in_scan) {
             a.fold[size_t(i) * a.P + nold + __popc(bo & lt)] = id;
         }

@@ -45,27 +45,32 @@ class DataError(RuntimeError):
 
 def _read_records(path: str, kind: str):
     try:
-        raw = np.fromfile(path, dtype="<i4")
+        size = os.path.getsize(path)
+        raw = np.fromfile(path, dtype="<i4", count=size // 4)
     except OSError as e:
         raise FormatError(f"cannot open file for reading: {path}") from e
-    if os.path.getsize(path) % 4:
-        raise FormatError(f"truncated record (size not a multiple of 4) in {path}")
-    if raw.size == 0:
+    words = raw.size
+    if words == 0:
+        if size % 4:
+            raise FormatError(f"truncated record 0 at byte 0 in {path}")
         return np.zeros((0, 0), "<i4")
     d = int(raw[0])
     if d < 1:
         raise FormatError(f"record 0 at byte 0 declares dimension {d} in {path}")
-    if raw.size % (d + 1):
-        # find the first inconsistent / truncated record for the message
+    if words % (d + 1) or size % 4:
+        # walk to the first inconsistent / cut record for the message: a record
+        # cut short names the byte where its first missing value starts
         rec, off = 0, 0
-        while off < raw.size:
+        while True:
+            if off == words:
+                raise FormatError(f"truncated record {rec} at byte {4 * off} in {path}")
             dd = int(raw[off])
             if dd < 1:
                 raise FormatError(f"record {rec} at byte {off * 4} declares dimension {dd} in {path}")
             if dd != d:
                 raise FormatError(f"record {rec} has dimension {dd}, expected {d} in {path}")
-            if off + 1 + dd > raw.size:
-                raise FormatError(f"truncated record {rec} in {path}")
+            if off + 1 + dd > words:
+                raise FormatError(f"truncated record {rec} at byte {4 * words} in {path}")
             off += dd + 1
             rec += 1
     rows = raw.reshape(-1, d + 1)
@@ -77,6 +82,22 @@ def _read_records(path: str, kind: str):
             raise FormatError(f"record {r} at byte {r * (d + 1) * 4} declares dimension {dd} in {path}")
         raise FormatError(f"record {r} has dimension {dd}, expected {d} in {path}")
     return rows[:, 1:]
+
+
+def validate_truth(ids: np.ndarray, base_n: int) -> None:
+    """GroundTruth::validate_against (dataset.cpp:78-95 contract): every id
+    inside the base set and no id twice in a row, else DataError."""
+    if ids.size == 0:
+        return
+    over = np.argwhere(ids >= base_n)
+    if over.size:
+        r, c = map(int, over[0])
+        raise DataError(f"row {r} holds id {int(ids[r, c])} outside base set of size {base_n}")
+    srt = np.sort(ids, axis=1)
+    dup = np.argwhere(srt[:, 1:] == srt[:, :-1])
+    if dup.size:
+        r, c = map(int, dup[0])
+        raise DataError(f"row {r} holds duplicate id {int(srt[r, c])}")
 
 
 def load_fvecs(path: str) -> np.ndarray:

@@ -6,7 +6,9 @@ for the same inputs (its own build_forest / brute_force / build_graph / search
 followed by its own save_* writers, through oracle/_ref); CSV rows must carry
 the same values except the timing columns.  The reference CLI binary itself
 is not built: it needs the un-vendored CLI11 header (proj/CMakeLists.txt
-`vendor/`), so parity is anchored on the library calls it makes.
+`vendor/`), so parity is anchored on the library calls it makes.  The
+reference's acceptance runner drives this CLI for its criterion 8
+(tests/test_reference_suites.py).
 """
 import os
 import subprocess
@@ -170,8 +172,7 @@ def test_cli_pipeline_matches_reference(tmp):
     p = run("build-graph", "--base", f("base.fvecs"), "--forest", f("f.akf"), "--gt", f("gt.ivecs"), "--k", k,
             "--dep", 4, "--pool", 30, "--sample", 10, "--iters", 5, "--min-change-rate", 0, "--seed", seed,
             "--out", f("g.ivecs"), "--out-dists", f("g.fvecs"), "--log", f("g.csv"))
-    # the iteration count is pinned (min change rate 0): `changes` is the documented deviation
-    # and feeds only the early-stop rule
+    # every logged column but the wall-clock seconds equals the reference's, `changes` included
     ids, dists, log, summ = r.build_graph(vx, fr, k=k, conquer_depth=4, pool_cap=30, sample_cap=10, max_iters=5,
                                           strategy=0, seed=seed, min_change_rate=0.0, gt=gids[:, :k])
     r.ref_save_ivecs(ids, f("rg.ivecs"))
@@ -183,7 +184,7 @@ def test_cli_pipeline_matches_reference(tmp):
     assert len(rows) - 1 == len(log)
     for row, lg in zip(rows[1:], log):
         assert row[0] == str(int(lg[0])) and row[2] == str(int(lg[2])) and row[4] == g10(lg[4])
-        assert (row[3] == "0") == (int(lg[3]) == 0)
+        assert row[3] == str(int(lg[3]))
     assert "# strategy=efanna" in open(f("g.csv")).read()
 
     # search: sweep, results of the last point, CSV averages

@@ -494,3 +494,42 @@ def test_forest_import_roundtrip_reference_trees_and_validation():
     bad("right", leafi, n + 1, "leaf range")
     bad("roots", 0, m0, "bad root")
     bad("node_counts", 0, 0, "node count")
+
+
+@pytest.mark.parametrize("n,dim,k,P,seed,integer", [(2000, 16, 10, 30, 5, False), (3000, 128, 10, 40, 7, True)])
+def test_nn_expansion_iteration_bit_exact(n, dim, k, P, seed, integer):
+    # graph_build.cpp:164-207 (the NN-expansion baseline): pools, flags (flag_new and
+    # `checked`), changes and dist_comps per round equal the oracle's
+    o = ora()
+    x = mixture(n, dim, 20, seed) if integer else A.gen_synthetic(n, dim, seed)
+    vo = o.vs(x)
+    so = o.init_random(vo, k, P, 10, seed)
+    sd = A.init_random(x, k, P, 10, seed)
+    for it in range(3):
+        co = so.nn_expansion_iteration(vo)
+        assert A.detail.nn_expansion_iteration(sd, x) == co, f"changes, round {it}"
+        e = assert_pools_equal(sd, so)
+        assert sd.meta()["dist_comps"] == e["dist_comps"], f"round {it}"
+    # a descent round after expansion keeps the `checked` bits (mixed use of one state)
+    assert A.detail.nn_descent_iteration(sd, x) == so.nn_descent_iteration(vo)
+    assert_pools_equal(sd, so)
+
+
+def test_distance_entry_points():
+    # dataset.hpp:67-77 on the device: bit-exact to the reference's sequential chain
+    o = ora()
+    x = A.gen_synthetic(300, 37, 3)
+    q = A.gen_synthetic(1, 37, 4)[0]
+    a = np.arange(300, dtype=np.uint32)
+    b = (a * 7 + 3) % 300
+    d = A.dist_sq(x, a, b)
+    for i in (0, 17, 299):
+        assert d[i] == o.l2_sq(x[a[i]], x[b[i]])
+        assert A.l2_sq(x[a[i]], x[b[i]]) == d[i]
+    dq = A.dist_sq_q(x, q, a)
+    assert all(dq[i] == o.l2_sq(q, x[i]) for i in (0, 5, 299))
+    assert A.dist_sq(x, 5, 9) == A.dist_sq(x, 9, 5)  # symmetric (test_dataset.cpp:211)
+    with pytest.raises(A.OutOfRange):
+        A.dist_sq(x, 0, 300)
+    with pytest.raises(A.OutOfRange):
+        A.dist_sq_q(x, q, 300)
