@@ -834,6 +834,15 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
     final_acc = SH.sharded_accuracy(e, comm, gt_rows, rows)
     graph = SH.allgather_graph(e.finalize(), comm)
     del e
+    # the sharded build must equal the one-GPU build exactly (same pools: the merge
+    # replays the reference's order on every rank)
+    st1 = A.init_graph(vs, forest, k, cfg["dep"], cfg["P"], cfg["S"], SEED)
+    for _ in range(crossing):
+        A.detail.nn_descent_iteration(st1, vs)
+    g1 = A.finalize(st1, vs, k)
+    del st1
+    single_equal = bool(comm.allreduce_sum(0 if np.array_equal(g1.ids, graph.ids) else 1) == 0)
+    del g1
 
     # search: every rank holds the full index and answers its query shard
     searcher = A.GraphSearcher(vs, forest, graph)
@@ -894,9 +903,10 @@ def run_gpu_sharded(args, cfg, ws, rank, local):
         "config": {"workload": args.config, "n": n, "dim": dim, "trees": cfg["trees"], "leaf_cap": cfg["leaf"],
                    "k": k, "pool_cap": cfg["P"], "sample_cap": cfg["S"], "conquer_depth": cfg["dep"],
                    "iterations_to_acc_0.9": crossing, "accuracy_sample_rows": cfg["acc_sample"],
-                   "l2": "inputs larger than L2 (512 MB dataset)",
-                   "parallelism": f"point-sharded build x{ws} (NCCL all-gather + all-to-all per round), "
-                                  f"query-sharded search"},
+                   "l2": f"inputs larger than L2 ({n * dim * 4 / 1e6:.0f} MB dataset)",
+                   "parallelism": f"point-sharded build x{ws} ({args.comm} all-gather + all-to-all per round), "
+                                  f"query-sharded search",
+                   "graph_equal_single_gpu": single_equal},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(ws * (n * dim * 4 + f_bytes)),
                 "d2h_bytes_per_step": int(n * k * 8),
                 "includes": "per rank: H2D dataset + prebuilt forest, sharded init + rounds, finalize, D2H own rows"},
