@@ -424,6 +424,79 @@ def cpu_baseline_leg(args, cfg, A, base, queries, crossing, graph, gpu_search, c
     return out
 
 
+def exact_knn_f32_leg(args, A, peaks, vs3=None):
+    """Exact kNN of float data on the tensor cores (brute_force_f32_tc.cu): the
+    cfg3 ground truth -- 10,000 sampled rows of the 1M x 960 float mixture,
+    self-mode top-100 through annk_brute_force_rows, as the build's accuracy
+    hook uses it.  bf16x3 tcgen05 candidates + exact fp32 re-rank; a 200-row
+    prefix is checked against the exact CUDA-core kernel (ids and distance bits)
+    and the reference library times 50 of the rows on the host cores."""
+    cfg3 = dict(CONFIGS["cfg3"])
+    if vs3 is None:
+        b3, _ = gen_data(cfg3)
+        vs3 = A.VectorSet(b3)
+        del b3
+    n3, d3, k3 = cfg3["n"], cfg3["dim"], cfg3["k"]
+    rows3 = sample_rows(n3, 10000)  # the rows tools/time_bf_f32.py profiles under ncu
+    runs = []
+    for rep in range(3):  # first call warms the allocator
+        A.profile_reset()
+        A.profile_enable(True)
+        A.lib.annk_synchronize()
+        t1 = time.perf_counter()
+        ids3, d3s = A.brute_force_rows(vs3, rows3, k3, with_dists=True)
+        t2 = time.perf_counter()
+        A.profile_enable(False)
+        runs.append((t2 - t1, A.profile_report()))
+    t_api, prof3 = min(runs[1:], key=lambda r: r[0])
+    kname = "bf_tc_f32_kernel"
+    k_ms = prof3.get(kname, (1, float("nan")))[1]
+    bf16_flops = 6.0 * len(rows3) * n3 * d3  # 3 bf16 products per fp32 multiply-add
+    t_peak = float(peaks.get("bf16_tflops", 1667.9))
+    os.environ["ANNK_BF_CUDA_CORE"] = "1"
+    try:
+        A.profile_reset()
+        A.profile_enable(True)
+        ids_c, d_c = A.brute_force_rows(vs3, rows3[:200], k3, with_dists=True)
+        A.profile_enable(False)
+        cc_ms = sum(v[1] for v in A.profile_report().values())
+    finally:
+        del os.environ["ANNK_BF_CUDA_CORE"]
+    out = {"workload": f"cfg3 ground truth: {len(rows3)} sampled rows x {n3} x {d3} float, self-mode top-{k3} "
+                       "(brute_force_rows)",
+           "seconds_through_api": t_api, "kernels_ms": {kn: round(v[1], 3) for kn, v in prof3.items()},
+           "pairs_per_s": len(rows3) * n3 / t_api,
+           "roofline": {"kernel": kname, "bound": "tensor", "achieved": bf16_flops / (k_ms / 1e3) / 1e12,
+                        "peak": t_peak, "unit": "TFLOP/s", "frac": bf16_flops / (k_ms / 1e3) / 1e12 / t_peak,
+                        "peak_source": "measured dense bf16 TFLOP/s (MEASURED_PEAKS.json)",
+                        "flops_per_launch": bf16_flops,
+                        "units": "bf16 tensor flops: 3 products (hi.hi, hi.lo, lo.hi) x 2 flops per fp32 "
+                                 "multiply-add of the rows x N x dim contraction",
+                        "traffic": ncu_traffic("cfg3", kname)},
+           "cuda_core_check": {"rows": 200, "ids_equal": bool(np.array_equal(ids_c, ids3[:200])),
+                               "dist_bits_equal": bool(np.array_equal(d_c.view(np.uint32), d3s[:200].view(np.uint32))),
+                               "cuda_core_ms_for_200_rows": round(cc_ms, 2)}}
+    if not args.skip_cpu and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libannkit_ref.so")):
+        from oracle import oracle as O
+        ref = O.load("reference")
+        cores = os.cpu_count() or 1
+        b3h = vs3.data
+        if b3h is not None:
+            sel = rows3[:50]
+            vb = ref.vs(b3h)
+            t0 = time.perf_counter()
+            ids_q = ref.brute_force(vb, ref.vs(np.ascontiguousarray(b3h[sel])), k3 + 1, workers=cores)
+            tq = time.perf_counter() - t0
+            self_rm = np.array([row[row != i][:k3] for row, i in zip(ids_q, sel)])
+            out["cpu_baseline"] = {"value": tq * len(rows3) / len(sel), "unit": "s", "cores": cores,
+                                   "kind": "reference",
+                                   "sample": f"reference brute_force_knn on {len(sel)} of the rows ({tq:.2f} s, "
+                                             f"{cores} workers), scaled x{len(rows3) / len(sel):.0f}",
+                                   "ids_equal_gpu": bool(np.array_equal(self_rm, ids3[:len(sel)]))}
+            del vb
+    return out
+
+
 def run_gpu(args, cfg, ws, rank, local):
     import torch
 
@@ -695,6 +768,11 @@ def run_gpu(args, cfg, ws, rank, local):
         exact_sample = ids_all[rows[:1000]].copy()
         del ids_all
 
+    _log("exact kNN fp32")
+    exact_f32 = None
+    if not args.skip_cfg4 and not cfg.get("skip_exact") and args.config in ("cfg2", "cfg3"):
+        exact_f32 = exact_knn_f32_leg(args, A, peaks, vs if args.config == "cfg3" else None)
+
     _log("cpu baseline")
     # CPU baseline: the reference library (oracle/_ref) on this box's host cores, rank 0 at N=1
     cpu = cpu_baseline_leg(args, cfg, A, base, queries, crossing, graph, searcher_result, chosen, exact_sample,
@@ -732,6 +810,7 @@ def run_gpu(args, cfg, ws, rank, local):
         "accuracy": {"per_iteration": [round(a, 4) for a in accs], "final_sample": round(final_acc, 4),
                      "dist_comps": comps},
         "exact_knn": exact,
+        "exact_knn_f32": exact_f32,
         "aux_seconds": {"forest": forest_s, "gt_rows": gt_rows_s, "gt_queries": gt_q_s, "data_gen_host": gen_s,
                         "brute_force_pairs_per_s": bf_pairs / (gt_rows_s + gt_q_s)},
         "host_wall_s_per_step": wall_s,

@@ -586,6 +586,9 @@ void merge_split_lists(const uint64_t* part, uint32_t nq, uint32_t splits, uint3
     LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part, nq, splits, k, m, out_keys);
 }
 
+void brute_force_tiles(const annk_dataset* base, const float* qdata, uint32_t nq, const uint32_t* self_ids,
+                       uint32_t k, uint64_t* out_keys, const uint8_t* q8, const int32_t* qnorm);
+
 void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
                         const uint32_t* self_ids, uint32_t k, uint64_t* out_keys, const uint8_t* q8,
                         const int32_t* qnorm) {
@@ -603,6 +606,7 @@ void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q
     }
     const bool u8 = base->u8 && q8 != nullptr;
     if (u8 && brute_force_tc(base, nq, self_ids, k, out_keys, q8, qnorm)) return;  // tcgen05 path
+    if (!u8 && brute_force_tc_f32(base, qdata, nq, self_ids, k, out_keys)) return;  // tcgen05 bf16x3 + exact re-rank
     if (u8 && base->ld8 <= 128 && k <= 128 && !getenv("ANNK_BF_DP4A")) {
         // tensor-core path
         // buffer room past the kept k decides how often a query's buffer is sorted
@@ -642,6 +646,15 @@ void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q
         if (splits > 1) merge_split_lists(part.p, nq, splits, k, out_keys);
         return;
     }
+    brute_force_tiles(base, qdata, nq, self_ids, k, out_keys, u8 ? q8 : nullptr, qnorm);
+}
+
+// The CUDA-core tile kernels (fp32 rows: the exact sequential chain; u8 rows:
+// dp4a) with the slice merge.
+void brute_force_tiles(const annk_dataset* base, const float* qdata, uint32_t nq, const uint32_t* self_ids,
+                       uint32_t k, uint64_t* out_keys, const uint8_t* q8, const int32_t* qnorm) {
+    const uint32_t nb = base->n, ld = base->ld;
+    const bool u8 = q8 != nullptr;
     const uint32_t cb = next_pow2(k + BT);
     const size_t smem =
         u8 ? size_t(QT) * cb * 8 + QT * 8 + QT * 4 * 3 + BT * 4 + size_t(QT + BT) * (base->ld8 / 4 + 4) * 4
@@ -676,6 +689,11 @@ void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q
         CK(cudaFuncSetAttribute(bf_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wpb * m * 8)));
         LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part.p, nq, splits, k, m, out_keys);
     }
+}
+
+void brute_force_f32_tiles(const annk_dataset* base, const float* qdata, uint32_t nq, const uint32_t* self_ids,
+                           uint32_t k, uint64_t* out_keys) {
+    brute_force_tiles(base, qdata, nq, self_ids, k, out_keys, nullptr, nullptr);
 }
 
 }  // namespace annk
