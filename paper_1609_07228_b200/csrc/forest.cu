@@ -1479,8 +1479,8 @@ __global__ void descend_kernel(const KdNodeDev* __restrict__ nodes, const float*
 
 }  // namespace
 
-void forest_ensure_links(annk_forest* f) {
-    if (f->links_ready) return;
+void forest_ensure_links(annk_forest* f, bool rebuild) {
+    if (f->links_ready && !rebuild) return;
     for (auto& t : f->trees) {
         t.parent.alloc(t.num_nodes);
         t.parent.fill_bytes(0xff);

@@ -1386,7 +1386,7 @@ annk_state* init_graph_impl(const annk_dataset* ds, const annk_forest* fc, uint3
     if (fc->n != ds->n || fc->dim != ds->dim) throw_invalid("init_graph: forest was built over different data");
     annk_forest* f = const_cast<annk_forest*>(fc);
     std::unique_ptr<annk_state> s(new_state(ds->n, k, pool_cap, sample_cap, seed));
-    forest_ensure_links(f);
+    forest_ensure_links(f, /*rebuild=*/true);  // inside the build, like the reference
     uint32_t max_depth = 0;
     for (const auto& t : f->trees) max_depth = std::max(max_depth, t.max_depth);
     const uint32_t n = ds->n;

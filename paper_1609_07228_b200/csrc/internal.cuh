@@ -155,7 +155,10 @@ int abi(F&& f) {
     }
 }
 
-void forest_ensure_links(annk_forest* f);
+// parent / owner / sibling tables of every tree (init's divide-and-conquer
+// walk); rebuilt on request, as the reference's init_graph rebuilds its
+// equivalents on every call (graph_build.cpp:238-257)
+void forest_ensure_links(annk_forest* f, bool rebuild = false);
 void forest_upload_views(annk_forest* f);
 // exact top-k helper used by brute force and accuracy scoring
 void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
