@@ -691,6 +691,112 @@ __global__ void replay_kernel(RArgs a) {
     if (lane == 0 && changes) atomicAdd(a.changes, changes);
 }
 
+// ------------------------------------------------------------ compaction
+// Most offers of a round repeat an id already in the target's pool (94% of the
+// candidates of round 2 at cfg2).  Such an offer is never accepted: either the
+// entry is still there when it arrives (NeighborPool::insert rejects the
+// duplicate) or it was evicted earlier in the round, which only happens to the
+// maximum of a full pool, and the tail stays below the evicted key ever since.
+// Before the ordered replay, every target's offers are filtered against an id
+// table of its current pool and compacted in place, storage order (hence the
+// source runs and the reference order) preserved; pools, flags and `changes`
+// are unchanged.
+struct CArgs {
+    uint32_t lo, hi, P, cap;
+    const uint64_t* keys;
+    const uint32_t* sizes;
+    uint32_t* ocnt;
+    uint64_t* obuf;
+    uint32_t* osrc;
+    const uint32_t* ov_off;
+    uint64_t* ov_key;
+    uint32_t* ov_src;
+    uint32_t* next;
+    uint32_t hbits;
+    unsigned long long* dropped;
+};
+
+__device__ __forceinline__ uint32_t ct_hash(uint32_t id, uint32_t mask) { return (id * 0x9E3779B1u >> 7) & mask; }
+
+__global__ void __launch_bounds__(256) offer_compact_kernel(CArgs a) {
+    extern __shared__ __align__(16) uint32_t csm[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
+    const uint32_t hslots = 1u << a.hbits, hmask = hslots - 1;
+    uint32_t* H = csm + size_t(warp) * hslots;
+    unsigned long long dropped = 0;
+    const uint32_t items = a.hi - a.lo;
+    for (;;) {
+        uint32_t w = 0;
+        if (lane == 0) w = atomicAdd(a.next, 1u);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= items) break;
+        const uint32_t t = a.lo + w;
+        const uint32_t m = a.ocnt[t];
+        if (m == 0) continue;
+        const uint32_t cf = min(m, a.cap);
+        uint64_t* k0 = a.obuf + size_t(t) * a.cap;
+        uint32_t* s0 = a.osrc + size_t(t) * a.cap;
+        const uint32_t spill = m > cf ? a.ov_off[t] : 0u;
+        uint64_t* k1 = a.ov_key + spill;
+        uint32_t* s1 = a.ov_src + spill;
+        for (uint32_t j = lane; j < hslots; j += 32) H[j] = 0xffffffffu;
+        __syncwarp();
+        const uint32_t sz = a.sizes[t];
+        for (uint32_t j = lane; j < sz; j += 32) {
+            const uint32_t id = key_id(a.keys[size_t(t) * a.P + j]);
+            for (uint32_t h = ct_hash(id, hmask);; h = (h + 1) & hmask)
+                if (atomicCAS(&H[h], 0xffffffffu, id) == 0xffffffffu) break;
+        }
+        __syncwarp();
+        uint32_t wpos = 0;
+        for (uint32_t q00 = 0; q00 < m; q00 += 64) {
+            uint64_t key[2];
+            uint32_t src[2];
+            bool keep[2];
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {  // both windows' loads in flight together
+                const uint32_t q = q00 + 32 * h2 + lane;
+                key[h2] = q < m ? (q < cf ? k0[q] : k1[q - cf]) : kEmptyKey;
+                src[h2] = q < m ? (q < cf ? s0[q] : s1[q - cf]) : 0u;
+            }
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                keep[h2] = q00 + 32 * h2 + lane < m;
+                if (keep[h2]) {
+                    const uint32_t id = key_id(key[h2]);
+                    for (uint32_t h = ct_hash(id, hmask);; h = (h + 1) & hmask) {
+                        const uint32_t v = H[h];
+                        if (v == id) { keep[h2] = false; break; }
+                        if (v == 0xffffffffu) break;
+                    }
+                }
+            }
+            __syncwarp();  // every read of these windows precedes the writes below (they go to lower slots)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, keep[h2]);
+                if (keep[h2]) {
+                    const uint32_t pos = wpos + __popc(bal & lt);
+                    if (pos < cf) {
+                        k0[pos] = key[h2];
+                        s0[pos] = src[h2];
+                    } else {
+                        k1[pos - cf] = key[h2];
+                        s1[pos - cf] = src[h2];
+                    }
+                }
+                wpos += __popc(bal);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            a.ocnt[t] = wpos;
+            dropped += m - wpos;
+        }
+    }
+    if (lane == 0 && dropped) atomicAdd(a.dropped, dropped);
+}
+
 __global__ void big_sizes_kernel(const uint32_t* __restrict__ nr, uint32_t nb, uint64_t* __restrict__ out) {
     const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b < nb) out[b] = uint64_t(next_pow2(nr[b] + 1)) + 1;
@@ -847,9 +953,45 @@ uint64_t replay_offers(annk_state* s, uint32_t lo, uint32_t hi) {
     changes.zero();
     a.changes = changes.p;
     const uint32_t n = s->n;
+    const bool trace = getenv("ANNK_TRACE") != nullptr;
+    {  // drop the offers of ids already in their target's pool (never accepted)
+        CArgs c{};
+        c.lo = lo;
+        c.hi = hi;
+        c.P = s->P;
+        c.cap = s->offer_cap;
+        c.keys = s->keys.p;
+        c.sizes = s->sizes.p;
+        c.ocnt = s->ocnt.p;
+        c.obuf = s->obuf.p;
+        c.osrc = s->osrc.p;
+        c.ov_off = s->ov_off.p;
+        c.ov_key = s->ov_key.p;
+        c.ov_src = s->ov_src.p;
+        c.hbits = 6;
+        while ((1u << c.hbits) < 2 * s->P) ++c.hbits;  // load factor <= 1/2
+        DevBuf<unsigned long long> dropped(1);
+        dropped.zero();
+        ctr.zero();
+        c.next = ctr.p;
+        c.dropped = dropped.p;
+        const uint32_t wpb = 8;
+        const size_t smem = size_t(wpb) << (c.hbits + 2);
+        if (smem > size_t(max_smem_optin())) throw_invalid("refine: pool_cap too large for the device path");
+        CK(cudaFuncSetAttribute(offer_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, offer_compact_kernel, wpb * 32, smem));
+        const uint32_t grid = std::min<uint32_t>((hi - lo + wpb - 1) / wpb, uint32_t(num_sms()) * std::max(per_sm, 1));
+        LAUNCH(offer_compact_kernel, grid, wpb * 32, smem, c);
+        if (trace) {
+            unsigned long long d = 0;
+            dropped.download(&d, 1);
+            ssync();
+            fprintf(stderr, "[annk] replay: %llu offers of ids already in their pool dropped\n", d);
+        }
+    }
     if (s->rp_big.n < 4 * size_t(n)) s->rp_big.alloc(4 * size_t(n));  // two (target, run count) lists
     uint32_t* def[2] = {s->rp_big.p, s->rp_big.p + 2 * size_t(n)};
-    const bool trace = getenv("ANNK_TRACE") != nullptr;
     // pass 1: every target, up to 256 source runs in shared memory (8 warps per block);
     // pass 2: the deferred ones with up to 1024 (4 warps per block);
     // pass 3: the rest with their runs in global scratch
