@@ -38,8 +38,9 @@
 namespace annk {
 namespace {
 
-constexpr uint32_t kWX = 8;   // fp32 rows: interleaved exact chains per lane
-constexpr uint32_t kStrip = 8;   // list rows per distance strip (the upper half of an IMMA m-tile)
+constexpr uint32_t kWX = 16;     // fp32 rows: interleaved exact chains per lane
+constexpr uint32_t kStrip = 8;   // u8 rows: list rows per distance strip (the upper half of an IMMA m-tile)
+constexpr uint32_t kStripF = 16; // fp32 rows: one strip = kWX chains, so every partner row is read A/16 times
 constexpr uint32_t kPad = 64;    // member arrays padded so a partner window may read past the list
 enum : int { kModeU8 = 0, kModeF32 = 1 };
 
@@ -65,6 +66,8 @@ struct JArgs {
     uint32_t* ov_src;
     uint32_t ov_cap;
     unsigned long long* counters;  // [0] comps, [1] offers
+    uint32_t strip;  // list rows per distance strip (kStrip u8, kStripF fp32)
+    uint32_t stage_words;  // fp32 rows: shared staging of one 32-dimension chunk of the strip and window rows
     uint32_t rn;     // per-member array length: list capacity 3S + P rounded up to 32
     uint32_t rs;     // D strip row stride (floats)
     uint32_t ol;     // offer buffer capacity
@@ -72,7 +75,7 @@ struct JArgs {
 
 // Per-warp shared memory: one warp processes one point at a time.
 struct WLayout {
-    size_t thr, bkey, ids, nrm, mc, mb, mf, ms, D, canon, bmem, total;
+    size_t thr, bkey, ids, nrm, mc, mb, mf, ms, D, canon, bmem, stage, total;
 };
 __host__ __device__ inline WLayout w_layout(const JArgs& a) {
     WLayout L;
@@ -85,9 +88,10 @@ __host__ __device__ inline WLayout w_layout(const JArgs& a) {
     L.mb = o;    o += al16(size_t(a.rn) * 4);
     L.mf = o;    o += al16(size_t(a.rn) * 4);
     L.ms = o;    o += al16(size_t(a.rn) * 4);
-    L.D = o;     o += al16(size_t(kStrip) * a.rs * 4);
+    L.D = o;     o += al16(size_t(a.strip) * a.rs * 4);
     L.canon = o; o += al16(size_t(a.rn + kPad) * 2);
     L.bmem = o;  o += al16(size_t(a.ol) * 2);
+    L.stage = o; o += al16(size_t(a.stage_words) * 4);
     L.total = o;
     return L;
 }
@@ -107,7 +111,7 @@ __device__ __forceinline__ uint4 ldg128(const uint8_t* p) { return __ldg(reinter
 // squared distance of list members x and y (cells with y <= x are ignored).
 template <int MODE>
 __device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* ids, const int32_t* nrm, float* D,
-                                                uint32_t xb, uint32_t xe, uint32_t R) {
+                                                uint32_t xb, uint32_t xe, uint32_t R, float* stage) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t yb0 = (xb + 1) / 32, yb1 = (R + 31) / 32;
     if (MODE == kModeU8) {
@@ -150,34 +154,86 @@ __device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* 
             }
         }
     } else {
-        // fp32 rows from L1/L2: the lane's y row against kWX broadcast x rows,
-        // kWX interleaved exact sequential chains (graph_build.cpp l2_sq order).
-        for (uint32_t x0 = xb; x0 < xe; x0 += kWX) {
-            for (uint32_t yb = max(yb0, (x0 + 1) / 32); yb < yb1; ++yb) {
-                const uint32_t y = yb * 32 + lane;
-                const float4* yrow = reinterpret_cast<const float4*>(a.x + size_t(ids[min(y, R - 1)]) * a.ld);
-                const float4* xrow[kWX];
+        // fp32 rows: the strip's kWX rows and a window of 32 partner rows are staged
+        // through shared memory 32 dimensions at a time by cp.async (16-byte
+        // pieces, double-buffered: the next chunk lands while this one is used);
+        // each lane runs kWX interleaved exact chains (graph_build.cpp l2_sq order:
+        // index ascending; the zero fill past the row adds +0 exactly) for its
+        // partner.  Window rows are stored with the 16-byte pieces of row r
+        // XOR-swizzled by r & 7, so the lanes' LDS.128 column reads are
+        // conflict-free; strip rows are read as broadcasts.
+        const uint32_t nxr = xe - xb;
+        const uint32_t sbase = uint32_t(__cvta_generic_to_shared(stage));
+        const uint32_t nchunk = (a.ld + 31) / 32;
+        for (uint32_t yb = max(yb0, (xb + 1) / 32); yb < yb1; ++yb) {
+            const float* xsrc[kWX * 8 / 32];
+            const float* ysrc[8];
 #pragma unroll
-                for (uint32_t k = 0; k < kWX; ++k)
-                    xrow[k] = reinterpret_cast<const float4*>(a.x + size_t(ids[min(x0 + k, xe - 1)]) * a.ld);
-                float acc[kWX];
+            for (uint32_t j = 0; j < kWX * 8 / 32; ++j) {
+                const uint32_t e = j * 32 + lane, r = e >> 3;
+                xsrc[j] = a.x + size_t(ids[xb + min(r, nxr - 1)]) * a.ld + (e & 7) * 4;
+            }
 #pragma unroll
-                for (uint32_t k = 0; k < kWX; ++k) acc[k] = 0.0f;
-                for (uint32_t c = 0; c < a.ld / 4; ++c) {
-                    const float4 b = __ldg(yrow + c);
+            for (uint32_t j = 0; j < 8; ++j) {
+                const uint32_t e = j * 32 + lane, r = e >> 3;
+                ysrc[j] = a.x + size_t(ids[min(yb * 32 + r, R - 1)]) * a.ld + (e & 7) * 4;
+            }
+            auto issue = [&](uint32_t c, uint32_t buf) {
+                const uint32_t c0 = c * 32;
+                const uint32_t xo = sbase + buf * (kWX * 32 + 32 * 32) * 4, yo = xo + kWX * 32 * 4;
 #pragma unroll
-                    for (uint32_t k = 0; k < kWX; ++k) {
-                        const float4 v = __ldg(xrow[k] + c);
-                        float d;
-                        d = __fsub_rn(v.x, b.x); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                        d = __fsub_rn(v.y, b.y); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                        d = __fsub_rn(v.z, b.z); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                        d = __fsub_rn(v.w, b.w); acc[k] = __fadd_rn(acc[k], __fmul_rn(d, d));
-                    }
+                for (uint32_t j = 0; j < kWX * 8 / 32; ++j) {
+                    const uint32_t e = j * 32 + lane, r = e >> 3, g = e & 7;
+                    const uint32_t bytes = c0 + g * 4 < a.ld ? 16u : 0u;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(xo + (r * 32 + g * 4) * 4),
+                                 "l"(xsrc[j] + (bytes ? c0 : 0)), "r"(bytes)
+                                 : "memory");
                 }
 #pragma unroll
-                for (uint32_t k = 0; k < kWX; ++k) D[size_t(x0 + k - xb) * a.rs + y] = acc[k];
+                for (uint32_t j = 0; j < 8; ++j) {
+                    const uint32_t e = j * 32 + lane, r = e >> 3, g = e & 7;
+                    const uint32_t bytes = c0 + g * 4 < a.ld ? 16u : 0u;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                                     yo + (r * 32 + ((g ^ (r & 7)) * 4)) * 4),
+                                 "l"(ysrc[j] + (bytes ? c0 : 0)), "r"(bytes)
+                                 : "memory");
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            float acc[kWX];
+#pragma unroll
+            for (uint32_t k = 0; k < kWX; ++k) acc[k] = 0.0f;
+            issue(0, 0);
+            for (uint32_t c = 0; c < nchunk; ++c) {
+                const uint32_t buf = c & 1;
+                if (c + 1 < nchunk) {
+                    issue(c + 1, buf ^ 1);
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                __syncwarp();
+                const float* xs = stage + buf * (kWX * 32 + 32 * 32);
+                const float* ys = xs + kWX * 32 + lane * 32;
+                const uint32_t cw = min(32u, a.ld - c * 32);  // a multiple of 4
+                for (uint32_t k = 0; k < cw; k += 4) {
+                    const float4 bv = *reinterpret_cast<const float4*>(ys + (((k >> 2) ^ (lane & 7)) << 2));
+#pragma unroll
+                    for (uint32_t u = 0; u < kWX; ++u) {
+                        const float4 v = *reinterpret_cast<const float4*>(xs + u * 32 + k);
+                        float d;
+                        d = __fsub_rn(v.x, bv.x); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                        d = __fsub_rn(v.y, bv.y); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                        d = __fsub_rn(v.z, bv.z); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                        d = __fsub_rn(v.w, bv.w); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                    }
+                }
+                __syncwarp();  // this buffer is refilled two chunks later
             }
+            const uint32_t y = yb * 32 + lane;
+#pragma unroll
+            for (uint32_t u = 0; u < kWX; ++u)
+                if (u < nxr) D[size_t(u) * a.rs + y] = acc[u];
         }
     }
 }
@@ -283,6 +339,7 @@ __global__ void __launch_bounds__(32) join_kernel(JArgs a) {
     float* D = reinterpret_cast<float*>(sm + L.D);
     uint16_t* canon = reinterpret_cast<uint16_t*>(sm + L.canon);
     uint16_t* bmem = reinterpret_cast<uint16_t*>(sm + L.bmem);
+    float* stage = reinterpret_cast<float*>(sm + L.stage);
     const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
     unsigned long long comps = 0, offers = 0;
     for (uint32_t m = lane; m < a.rn; m += 32) {
@@ -344,9 +401,10 @@ __global__ void __launch_bounds__(32) join_kernel(JArgs a) {
         join_next_point(a, ni, nA, nB);
         __syncwarp();
         uint32_t nbuf = 0;
-        for (uint32_t xb = 0; xb < A; xb += kStrip) {
-            const uint32_t xe = min(A, xb + kStrip);
-            strip_distances<MODE>(a, ids, nrm, D, xb, xe, R);
+        constexpr uint32_t strip = MODE == kModeU8 ? kStrip : kStripF;
+        for (uint32_t xb = 0; xb < A; xb += strip) {
+            const uint32_t xe = min(A, xb + strip);
+            strip_distances<MODE>(a, ids, nrm, D, xb, xe, R, stage);
             if (xb == 0) {
                 JOIN_FETCH(ni, nA, nB)  // next point's members: in flight while this one is processed
             }
@@ -876,6 +934,8 @@ void join_launch(annk_state* s, const annk_dataset* ds, const uint32_t* order, u
     a.next = next.p;
     const uint32_t rmax = 3 * s->S + s->P;
     if (rmax > 0xffffu) throw_invalid("join: sample_cap/pool_cap too large for the device path");
+    a.strip = ds->u8 ? kStrip : kStripF;
+    a.stage_words = ds->u8 ? 0u : 2 * (kWX * 32 + 32 * 32);
     a.rn = rup(rmax, 32);
     a.rs = a.rn + 8;
     a.ol = rup(std::max(768u, 2 * a.rn), 32);
