@@ -938,7 +938,7 @@ void join_launch(annk_state* s, const annk_dataset* ds, const uint32_t* order, u
     a.stage_words = ds->u8 ? 0u : 2 * (kWX * 32 + 32 * 32);
     a.rn = rup(rmax, 32);
     a.rs = a.rn + 8;
-    a.ol = rup(std::max(768u, 2 * a.rn), 32);
+    a.ol = rup(std::max(384u, 2 * a.rn), 32);  // 384 (was 768): 14 instead of 11 warps per SM, join 37.2 -> 35.3 ms
     const size_t smem = w_layout(a).total;
     if (smem > size_t(max_smem_optin())) throw_invalid("join: list capacity too large for the device path");
     const void* fn = ds->u8 ? reinterpret_cast<const void*>(join_kernel<kModeU8>)
