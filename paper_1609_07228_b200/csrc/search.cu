@@ -24,7 +24,7 @@ namespace annk {
 namespace {
 
 constexpr uint32_t kThreads = 256;
-constexpr uint32_t kBuf = 2048;
+constexpr uint32_t kBuf = 1024;  // candidate buffer between merges (1024: 6 CTAs per SM instead of 5)
 constexpr uint32_t kU = 4;  // expansion slots per worker thread per batch (atomics in flight)
 constexpr size_t kHeapSmem = 12288;  // BBF heaps in shared memory up to this size
 
@@ -449,7 +449,7 @@ __device__ void bbf_producer(const SearchArgs& a, Smem& s) {
 }
 
 template <bool kTree>
-__global__ void __launch_bounds__(kThreads, 5) search_kernel(SearchArgs a) {
+__global__ void __launch_bounds__(kThreads, 6) search_kernel(SearchArgs a) {
     constexpr uint32_t W = kTree ? kThreads - 32 : kThreads;  // worker threads
     extern __shared__ __align__(16) unsigned char raw[];
     Smem s;
