@@ -409,48 +409,71 @@ __global__ void __launch_bounds__(32) join_kernel(JArgs a) {
                 JOIN_FETCH(ni, nA, nB)  // next point's members: in flight while this one is processed
             }
             __syncwarp();
-            for (uint32_t x = xb; x < xe; ++x) {
-                if (nbuf + 2 * (R - x - 1) > a.ol) {  // a row fits an empty buffer (ol >= 2 rn)
+            // the strip's pairs (x, y > x), x = xb..xe-1, flattened in the reference's
+            // order (row-major) so every lane of a window carries a pair; per pair
+            // y -> x is offered before x -> y (graph_build.cpp:135-152)
+            uint32_t off[kStripF + 1];
+            {
+                uint32_t o = 0;
+#pragma unroll
+                for (uint32_t r = 0; r <= kStripF; ++r) {
+                    off[r] = o;
+                    if (r < strip && xb + r < xe) o += R - (xb + r) - 1;
+                    else o = 0xffffffffu;  // rows past the strip: never reached
+                }
+            }
+            uint32_t total = 0;
+#pragma unroll
+            for (uint32_t r = 1; r <= kStripF; ++r)
+                if (r <= xe - xb) total = off[r];
+            for (uint32_t p0 = 0; p0 < total; p0 += 64) {
+                if (nbuf + 128 > a.ol) {  // a step adds at most 128 offers (ol >= 2 rn >= 128)
                     join_flush(a, i, nbuf, R, ids, bkey, bmem, mc, mb, mf, ms);
                     offers += nbuf;
                     nbuf = 0;
                 }
-                const uint32_t idx = ids[x];
-                const uint64_t tx = thr_s[x];
-                const uint16_t cx = canon[x];
-                const float* Dr = D + size_t(x - xb) * a.rs;
-                // two 32-partner windows per step (their loads overlap), emitted in order
-                for (uint32_t y0 = x + 1; y0 < R; y0 += 64) {
-                    bool ox[2], oy[2];
-                    uint64_t kx[2], ky[2];
-                    uint32_t bx[2], by[2];
+                bool ox[2], oy[2];
+                uint64_t kx[2], ky[2];
+                uint32_t bx[2], by[2];
+                uint16_t mx_[2], my_[2];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t y = y0 + 32 * h + lane;  // < rn + kPad: reads stay in the arrays
-                        const uint32_t idy = ids[y];
-                        const float d = Dr[y];
-                        const uint64_t thy = thr_s[y];
-                        const bool valid = y < R && idy != idx;  // graph_build.cpp:146 (l == j is skipped)
-                        kx[h] = make_key(d, idy);
-                        ky[h] = make_key(d, idx);
-                        ox[h] = valid && kx[h] < tx;
-                        oy[h] = valid && ky[h] < thy;
-                        bx[h] = __ballot_sync(0xffffffffu, ox[h]);
-                        by[h] = __ballot_sync(0xffffffffu, oy[h]);
-                    }
+                for (int h = 0; h < 2; ++h) {  // two 32-pair windows per step (their loads overlap)
+                    const uint32_t pp = p0 + 32 * h + lane;
+                    uint32_t r = 0, offr = 0;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t q = nbuf + __popc(bx[h] & lt) + __popc(by[h] & lt);
-                        if (ox[h]) {
-                            bkey[q] = kx[h];
-                            bmem[q] = cx;
+                    for (uint32_t k = 1; k < kStripF; ++k)
+                        if (k < strip && pp >= off[k]) {
+                            r = k;
+                            offr = off[k];
                         }
-                        if (oy[h]) {
-                            bkey[q + (ox[h] ? 1 : 0)] = ky[h];
-                            bmem[q + (ox[h] ? 1 : 0)] = canon[y0 + 32 * h + lane];
-                        }
-                        nbuf += __popc(bx[h]) + __popc(by[h]);
+                    const bool in = pp < total;
+                    const uint32_t x = xb + r;
+                    const uint32_t y = in ? x + 1 + (pp - offr) : x + 1;  // < rn + kPad: reads stay in the arrays
+                    const uint32_t idx = ids[x], idy = ids[y];
+                    const float d = D[size_t(r) * a.rs + y];
+                    const uint64_t tx = thr_s[x], thy = thr_s[y];
+                    const bool valid = in && idy != idx;  // graph_build.cpp:146 (l == j is skipped)
+                    kx[h] = make_key(d, idy);
+                    ky[h] = make_key(d, idx);
+                    ox[h] = valid && kx[h] < tx;
+                    oy[h] = valid && ky[h] < thy;
+                    mx_[h] = canon[x];
+                    my_[h] = canon[y];
+                    bx[h] = __ballot_sync(0xffffffffu, ox[h]);
+                    by[h] = __ballot_sync(0xffffffffu, oy[h]);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t q = nbuf + __popc(bx[h] & lt) + __popc(by[h] & lt);
+                    if (ox[h]) {
+                        bkey[q] = kx[h];
+                        bmem[q] = mx_[h];
                     }
+                    if (oy[h]) {
+                        bkey[q + (ox[h] ? 1 : 0)] = ky[h];
+                        bmem[q + (ox[h] ? 1 : 0)] = my_[h];
+                    }
+                    nbuf += __popc(bx[h]) + __popc(by[h]);
                 }
             }
             __syncwarp();
