@@ -42,6 +42,7 @@ constexpr uint32_t kWX = 16;     // fp32 rows: interleaved exact chains per lane
 constexpr uint32_t kStrip = 8;   // u8 rows: list rows per distance strip (the upper half of an IMMA m-tile)
 constexpr uint32_t kStripF = 16; // fp32 rows: one strip = kWX chains, so every partner row is read A/16 times
 constexpr uint32_t kPad = 64;    // member arrays padded so a partner window may read past the list
+constexpr uint32_t kMemRegs = 5;  // list members held per lane (lists <= 160): next-point fetch, reservations
 enum : int { kModeU8 = 0, kModeF32 = 1 };
 
 __host__ __device__ __forceinline__ size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
@@ -253,7 +254,29 @@ __device__ __forceinline__ void join_flush(const JArgs& a, uint32_t i, uint32_t 
         if (v && (mask & lt) == 0) mc[m] += __popc(mask);
         __syncwarp();
     }
-    for (uint32_t m = lane; m < R; m += 32) {
+    // slot reservations: a lane's (up to kMemRegs) atomics are all in flight before
+    // any result is used
+    {
+        uint32_t run[kMemRegs], base[kMemRegs];
+#pragma unroll
+        for (uint32_t k = 0; k < kMemRegs; ++k) {
+            const uint32_t m = k * 32 + lane;
+            run[k] = m < R ? mc[m] : 0u;
+            base[k] = run[k] ? atomicAdd(&a.ocnt[ids[m]], run[k]) : 0u;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kMemRegs; ++k) {
+            const uint32_t m = k * 32 + lane;
+            if (run[k]) {
+                const uint32_t fix = base[k] < a.cap ? min(run[k], a.cap - base[k]) : 0u;
+                mb[m] = base[k];
+                mf[m] = fix;
+                ms[m] = run[k] > fix ? atomicAdd(a.ov_cnt, run[k] - fix) : 0u;
+                mc[m] = 0;
+            }
+        }
+    }
+    for (uint32_t m = kMemRegs * 32 + lane; m < R; m += 32) {  // lists longer than the registers cover
         const uint32_t run = mc[m];
         if (run) {
             const uint32_t base = atomicAdd(&a.ocnt[ids[m]], run);
@@ -316,7 +339,6 @@ __device__ __forceinline__ void join_next_point(const JArgs& a, uint32_t& pi, ui
     }
 }
 
-constexpr uint32_t kMemRegs = 5;  // list members held per lane for the next point (lists <= 160)
 
 // One warp per point (persistent; points handed out by a counter).  The
 // point's list members are staged, the pair distances computed a 16-row strip
