@@ -29,6 +29,8 @@
 //    Pools, flags and `changes` equal the reference's bit-for-bit.
 #include <cub/cub.cuh>
 
+#include <type_traits>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -824,7 +826,7 @@ __device__ __forceinline__ uint32_t ct_hash(uint32_t id, uint32_t mask) { return
 __global__ void __launch_bounds__(256) offer_compact_kernel(CArgs a) {
     extern __shared__ __align__(16) uint32_t csm[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
-    const uint32_t hslots = 1u << a.hbits, hmask = hslots - 1;
+    const uint32_t hslots = 1u << a.hbits;
     uint32_t* H = csm + size_t(warp) * hslots;
     unsigned long long dropped = 0;
     const uint32_t items = a.hi - a.lo;
@@ -845,52 +847,70 @@ __global__ void __launch_bounds__(256) offer_compact_kernel(CArgs a) {
         for (uint32_t j = lane; j < hslots; j += 32) H[j] = 0xffffffffu;
         __syncwarp();
         const uint32_t sz = a.sizes[t];
+        // 4-slot buckets (one LDS.128 per probe), load factor <= 1/4
+        const uint32_t bmask = (hslots >> 2) - 1;
         for (uint32_t j = lane; j < sz; j += 32) {
             const uint32_t id = key_id(a.keys[size_t(t) * a.P + j]);
-            for (uint32_t h = ct_hash(id, hmask);; h = (h + 1) & hmask)
-                if (atomicCAS(&H[h], 0xffffffffu, id) == 0xffffffffu) break;
+            for (uint32_t b = ct_hash(id, bmask);; b = (b + 1) & bmask) {
+                bool done = false;
+#pragma unroll
+                for (uint32_t e = 0; e < 4 && !done; ++e) done = atomicCAS(&H[b * 4 + e], 0xffffffffu, id) == 0xffffffffu;
+                if (done) break;
+            }
         }
         __syncwarp();
         uint32_t wpos = 0;
-        for (uint32_t q00 = 0; q00 < m; q00 += 64) {
-            uint64_t key[2];
-            uint32_t src[2];
-            bool keep[2];
+        // offers at positions < cf live in the target's slots, the rest in its spill segment;
+        // survivors move to lower positions only, so a window is read before it is written
+        auto pass = [&](auto spilled) {
+            constexpr bool kSp = decltype(spilled)::value;
+            for (uint32_t q00 = 0; q00 < m; q00 += 64) {
+                uint64_t key[2];
+                uint32_t src[2];
+                bool keep[2];
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {  // both windows' loads in flight together
-                const uint32_t q = q00 + 32 * h2 + lane;
-                key[h2] = q < m ? (q < cf ? k0[q] : k1[q - cf]) : kEmptyKey;
-                src[h2] = q < m ? (q < cf ? s0[q] : s1[q - cf]) : 0u;
-            }
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                keep[h2] = q00 + 32 * h2 + lane < m;
-                if (keep[h2]) {
-                    const uint32_t id = key_id(key[h2]);
-                    for (uint32_t h = ct_hash(id, hmask);; h = (h + 1) & hmask) {
-                        const uint32_t v = H[h];
-                        if (v == id) { keep[h2] = false; break; }
-                        if (v == 0xffffffffu) break;
-                    }
-                }
-            }
-            __syncwarp();  // every read of these windows precedes the writes below (they go to lower slots)
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                const uint32_t bal = __ballot_sync(0xffffffffu, keep[h2]);
-                if (keep[h2]) {
-                    const uint32_t pos = wpos + __popc(bal & lt);
-                    if (pos < cf) {
-                        k0[pos] = key[h2];
-                        s0[pos] = src[h2];
+                for (int h2 = 0; h2 < 2; ++h2) {  // both windows' loads in flight together
+                    const uint32_t q = q00 + 32 * h2 + lane;
+                    if (kSp) {
+                        key[h2] = q < m ? (q < cf ? k0[q] : k1[q - cf]) : kEmptyKey;
+                        src[h2] = q < m ? (q < cf ? s0[q] : s1[q - cf]) : 0u;
                     } else {
-                        k1[pos - cf] = key[h2];
-                        s1[pos - cf] = src[h2];
+                        key[h2] = q < m ? k0[q] : kEmptyKey;
+                        src[h2] = q < m ? s0[q] : 0u;
                     }
                 }
-                wpos += __popc(bal);
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    keep[h2] = q00 + 32 * h2 + lane < m;
+                    if (keep[h2]) {
+                        const uint32_t id = key_id(key[h2]);
+                        for (uint32_t b = ct_hash(id, bmask);; b = (b + 1) & bmask) {
+                            const uint4 v = *reinterpret_cast<const uint4*>(H + b * 4);
+                            if (v.x == id || v.y == id || v.z == id || v.w == id) { keep[h2] = false; break; }
+                            if ((v.x & v.y & v.z & v.w) != 0xffffffffu) break;  // a free slot: not present
+                        }
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const uint32_t bal = __ballot_sync(0xffffffffu, keep[h2]);
+                    if (keep[h2]) {
+                        const uint32_t pos = wpos + __popc(bal & lt);
+                        if (!kSp || pos < cf) {
+                            k0[pos] = key[h2];
+                            s0[pos] = src[h2];
+                        } else {
+                            k1[pos - cf] = key[h2];
+                            s1[pos - cf] = src[h2];
+                        }
+                    }
+                    wpos += __popc(bal);
+                }
             }
-        }
+        };
+        if (m > cf) pass(std::true_type{});
+        else pass(std::false_type{});
         __syncwarp();
         if (lane == 0) {
             a.ocnt[t] = wpos;
@@ -1073,8 +1093,8 @@ uint64_t replay_offers(annk_state* s, uint32_t lo, uint32_t hi) {
         c.ov_off = s->ov_off.p;
         c.ov_key = s->ov_key.p;
         c.ov_src = s->ov_src.p;
-        c.hbits = 6;
-        while ((1u << c.hbits) < 2 * s->P) ++c.hbits;  // load factor <= 1/2
+        c.hbits = 7;
+        while ((1u << c.hbits) < 4 * s->P) ++c.hbits;  // load factor <= 1/4
         DevBuf<unsigned long long> dropped(1);
         dropped.zero();
         ctr.zero();
