@@ -1195,7 +1195,12 @@ void do_union(annk_state* s) {
 uint32_t offer_cap_max(const annk_state* s) {
     const uint32_t cap_floor = std::max(2 * s->P, 64u);
     uint32_t cap_max = cap_floor;
-    while (uint64_t(cap_max) * 2 * s->n * 8 <= 12ull << 30 && cap_max < 4096) cap_max *= 2;
+    // per-target offer slots (12 B each; ~16 B counted) within 32 GB of the
+    // 180 GB: at 1M points, 2048 slots -- spilled offers (a radix sort by
+    // target per round) 84M -> 21M in round 2 at cfg2
+    const char* gb = getenv("ANNK_OFFER_GB");
+    const uint64_t budget = (gb ? std::strtoull(gb, nullptr, 10) : 32ull) << 30;
+    while (uint64_t(cap_max) * 2 * s->n * 8 <= budget && cap_max < 4096) cap_max *= 2;
     return cap_max;
 }
 uint32_t g_offer_cap_hint = 0;          // capacities learned by earlier rounds (any state)
@@ -1272,7 +1277,8 @@ uint64_t merge_offers(annk_state* s) { return replay_offers(s, own_lo(s), own_hi
 void finish_round(annk_state* s, uint64_t changes) {
     const uint32_t n = s->n;
     const uint32_t cap_floor = std::max(2 * s->P, 64u), cap_max = offer_cap_max(s);
-    const uint64_t want = std::max<uint64_t>(cap_floor, (s->last_offers / std::max(n, 1u)) * 5 / 4);
+    // slots for ~2.5x the mean offers per target (hub targets take more)
+    const uint64_t want = std::max<uint64_t>(cap_floor, (s->last_offers / std::max(n, 1u)) * 10 / 4);
     const uint32_t next = std::min<uint32_t>(cap_max, next_pow2(uint32_t(std::min<uint64_t>(want, 1u << 20))));
     g_offer_cap_hint = std::max(g_offer_cap_hint, next);
     s->offer_cap = std::max(s->offer_cap, next);  // takes effect next round (buffers reallocated)
