@@ -630,6 +630,27 @@ def run_gpu(args, cfg, ws, rank, local):
         if rec >= 0.9 and (fastest is None or row["qps"] > fastest["qps"]):
             fastest = row
 
+    # BASELINE cfg2's sweep: pool sizes 100-1000 (E = P, the default I) and tree-check
+    # counts (SearchParams::n_trees_used, search.cpp:126-133) at the chosen point
+    pool_sweep, tree_sweep = [], []
+    for P in cfg["sweep"]:
+        p = A.SearchParams(k_return=kr, pool_size=P, expansion=P, iters=REF_ITERS)
+        r, dt = timed_search(searcher, qs, p, ev, reps=1)
+        rec = float(np.mean([len(np.intersect1d(r.ids[i], gt_q[i])) / kr for i in range(len(gt_q))]))
+        pool_sweep.append({"pool": P, "expansion": P, "iters": REF_ITERS, "recall": round(rec, 4),
+                           "qps": round(cfg["n_queries"] / dt, 1),
+                           "dist_comps_per_query": float(r.stats[:, 0].mean())})
+    if chosen:
+        for T in sorted({1, 2, 4, cfg["trees"]}):
+            p = A.SearchParams(k_return=kr, pool_size=chosen["pool"], expansion=chosen["expansion"],
+                               iters=chosen["iters"], n_trees_used=T)
+            r, dt = timed_search(searcher, qs, p, ev, reps=1)
+            rec = float(np.mean([len(np.intersect1d(r.ids[i], gt_q[i])) / kr for i in range(len(gt_q))]))
+            tree_sweep.append({"trees_used": T, "pool": chosen["pool"], "expansion": chosen["expansion"],
+                               "iters": chosen["iters"], "recall": round(rec, 4),
+                               "qps": round(cfg["n_queries"] / dt, 1),
+                               "dist_comps_per_query": float(r.stats[:, 0].mean())})
+
     search_kernels = None
     search_roofline = None
     for row in (fastest, chosen):  # kernel-only time of the reported points (profiler on, outside the sweep)
@@ -806,7 +827,8 @@ def run_gpu(args, cfg, ws, rank, local):
                    "definition": f"recall_curve sweep (P, then E ascending) at the default I={REF_ITERS}; "
                                  "first point with recall@k_return >= 0.9; Q / device time of the batch "
                                  "through the public API (results D2H to pinned memory included)",
-                   "chosen": chosen, "fastest_any_iters": fastest, "sweep": sweep},
+                   "chosen": chosen, "fastest_any_iters": fastest, "sweep": sweep,
+                   "pool_sweep": pool_sweep, "trees_used_sweep": tree_sweep},
         "accuracy": {"per_iteration": [round(a, 4) for a in accs], "final_sample": round(final_acc, 4),
                      "dist_comps": comps},
         "exact_knn": exact,
