@@ -24,7 +24,10 @@ namespace annk {
 namespace {
 
 constexpr uint32_t kThreads = 256;
-constexpr uint32_t kBuf = 1024;  // candidate buffer between merges (1024: 6 CTAs per SM instead of 5)
+// candidate buffer between merges: 1024 keys at small pools (6 CTAs per SM
+// instead of 5 with 2048), 2048 once P >= 700 (below that a buffer that fills
+// past P + one batch would merge after every batch)
+constexpr uint32_t kBufMin = 1024, kBufMax = 2048;
 constexpr uint32_t kU = 4;  // expansion slots per worker thread per batch (atomics in flight)
 constexpr size_t kHeapSmem = 12288;  // BBF heaps in shared memory up to this size
 
@@ -70,6 +73,7 @@ struct SearchArgs {
     const int32_t* qnorms8;
     uint32_t gk_magic;  // floor(2^32 / gk): slot -> (expanded point, column) without a hardware divide
     uint32_t* qnext;    // query work counter: CTAs take queries dynamically (query costs vary)
+    uint32_t kbuf;      // candidate buffer capacity (kBufMin or kBufMax)
 };
 
 struct Smem {
@@ -358,7 +362,7 @@ __device__ __forceinline__ uint64_t tail_key(const SearchArgs& a, const Smem& s)
 
 __device__ __forceinline__ void push_buf(Smem& s, uint64_t key) {
     const uint32_t slot = atomicAdd(&s.ctr[1], 1u);
-    DCHK(slot < kBuf);
+    DCHK(slot < kBufMax);
     s.buf[slot] = key;
 }
 
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 6) search_kernel(SearchArgs a) {
         s.pool = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
         s.tmp = reinterpret_cast<uint64_t*>(p); p += size_t(a.P) * 8;
         s.seeds = reinterpret_cast<uint64_t*>(p); p += size_t(a.seed_cap) * 8;
-        s.buf = reinterpret_cast<uint64_t*>(p); p += size_t(kBuf) * 8;
+        s.buf = reinterpret_cast<uint64_t*>(p); p += size_t(a.kbuf) * 8;
         s.rhash = reinterpret_cast<uint64_t*>(p); p += size_t(a.seed_cap) * 16;  // 8-byte entries: before expand
         s.expand = reinterpret_cast<uint32_t*>(p); p += size_t(a.P) * 4;
         s.scan = reinterpret_cast<uint32_t*>(p); p += 64;
@@ -645,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 6) search_kernel(SearchArgs a) {
                     }
                 }
                 wsync<W>();
-                if (s.ctr[1] + W * kU > kBuf) {
+                if (s.ctr[1] + W * kU > a.kbuf) {
                     merge_buffer<W>(a, s);
                     thr = tail_key(a, s);
                 }
@@ -664,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 6) search_kernel(SearchArgs a) {
                     if (key < thr) push_buf(s, key);
                 }
                 wsync<W>();
-                if (s.ctr[1] + W > kBuf) {
+                if (s.ctr[1] + W > a.kbuf) {
                     merge_buffer<W>(a, s);
                     thr = tail_key(a, s);
                 }
@@ -737,7 +741,8 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
     const uint32_t hcap = (n_node + 1) * (max_depth + 1) + 1;
     const size_t heap_bytes = size_t(std::min(nt, 32u)) * hcap * sizeof(HeapEnt);  // one heap per producer lane
     const bool heap_smem = heap_bytes <= kHeapSmem;
-    const size_t smem = (heap_smem ? heap_bytes : 0) + size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kBuf) * 8 +
+    const uint32_t kbuf = P >= 700 ? kBufMax : kBufMin;
+    const size_t smem = (heap_smem ? heap_bytes : 0) + size_t(P) * 16 + size_t(seed_cap) * 8 + size_t(kbuf) * 8 +
                         size_t(base->ld) * 4 + size_t(P) * 4 + 128 + (kHist + 8) * 4 + 16 + size_t(seed_cap) * 16 +
                         size_t(P) * 2 + 16 + base->ld8;
     if (smem > size_t(max_smem_optin()))
@@ -770,6 +775,7 @@ void run_search(annk_searcher* sr, const annk_dataset* qds, const annk_search_pa
     DevBuf<uint32_t> qnext(1);
     qnext.zero();
     a.qnext = qnext.p;
+    a.kbuf = kbuf;
     if (p->random_init) LAUNCH(search_kernel<false>, slots, kThreads, smem, a);
     else LAUNCH(search_kernel<true>, slots, kThreads, smem, a);
     const size_t cnt = size_t(nq) * p->k_return;
