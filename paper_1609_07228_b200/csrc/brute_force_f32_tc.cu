@@ -383,7 +383,10 @@ bf_tc_f32_kernel(const __grid_constant__ CUtensorMap tm_bh, const __grid_constan
                             for (int e = 0; e < 4; ++e) {
                                 const float dd = qn + v[4 * gi + e];
                                 const uint32_t j = j0 + 4 * gi + e;
-                                if (dd <= cut && j < a.nb && j != self) buf[cnt++] = make_key(fmaxf(dd, 0.0f), j);
+                                if (dd <= cut && j < a.nb && j != self) {
+                                    DCHK(cnt < kFCB);
+                                    buf[cnt++] = make_key(fmaxf(dd, 0.0f), j);
+                                }
                             }
                         }
                     }
@@ -513,6 +516,7 @@ __global__ void __launch_bounds__(256) rerank_kernel(const uint64_t* __restrict_
         const uint32_t id = key_id(s[e]);
         s[e] = make_key(l2_exact_ldg8(qr, base + size_t(id) * ld, ld), id);
     }
+    DCHK(n <= kRR);
     const uint32_t np2 = next_pow2(max(n, k));
     for (uint32_t e = n + lane; e < np2; e += 32) s[e] = kEmptyKey;
     __syncwarp();

@@ -376,7 +376,10 @@ bf_tc_u8_kernel(const __grid_constant__ CUtensorMap tm_base, const __grid_consta
                             const uint32_t j = jg + e2;
                             if (xs[e2] >= lim && j < a.nb && j != self) {
                                 const uint64_t key = make_key(float(qn - xs[e2]), j);
-                                if (key < thr) buf[cnt++] = key;
+                                if (key < thr) {
+                                    DCHK(cnt < kCB);
+                                    buf[cnt++] = key;
+                                }
                             }
                         }
                     }

@@ -73,6 +73,7 @@ struct JArgs {
     uint32_t stage_words;  // fp32 rows: shared staging of one 32-dimension chunk of the strip and window rows
     uint32_t rn;     // per-member array length: list capacity 3S + P rounded up to 32
     uint32_t rs;     // D strip row stride (floats)
+    uint32_t dbg_n;  // points (debug bounds checks)
     uint32_t ol;     // offer buffer capacity
 };
 
@@ -303,6 +304,7 @@ __device__ __forceinline__ void join_flush(const JArgs& a, uint32_t i, uint32_t 
             const uint64_t key = bkey[e];
             if (r < mf[m]) {
                 const size_t slot = size_t(tgt) * a.cap + mb[m] + r;
+                DCHK(mb[m] + r < a.cap && tgt < a.dbg_n);
                 a.obuf[slot] = key;
                 a.osrc[slot] = i;
             } else {
@@ -489,6 +491,7 @@ __global__ void __launch_bounds__(32) join_kernel(JArgs a) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t q = nbuf + __popc(bx[h] & lt) + __popc(by[h] & lt);
+                    DCHK(!(ox[h] || oy[h]) || q + (ox[h] && oy[h] ? 1u : 0u) < a.ol);
                     if (ox[h]) {
                         bkey[q] = kx[h];
                         bmem[q] = mx_[h];
@@ -681,6 +684,7 @@ __device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint8
         uint64_t c = kEmptyKey;
         if (q < m) {
             const uint32_t pos = q + uint32_t(runkey[run]);
+            DCHK(pos < m && run < nr);
             c = pos < cf ? k0[pos] : k1[pos - cf];
         }
         rbase += __popc(__ballot_sync(0xffffffffu, bo <= 32));
@@ -737,6 +741,7 @@ __device__ uint32_t replay_target(const RArgs& a, uint32_t t, uint64_t* S, uint8
             }
             __syncwarp();
         }
+        DCHK(!acc || arank < 32);
         if (acc && rS + arank < a.P) {
             S[rS + arank] = c;
             SF[rS + arank] = 1;  // arrived this round: flag_new
@@ -897,6 +902,7 @@ __global__ void __launch_bounds__(256) offer_compact_kernel(CArgs a) {
                     const uint32_t bal = __ballot_sync(0xffffffffu, keep[h2]);
                     if (keep[h2]) {
                         const uint32_t pos = wpos + __popc(bal & lt);
+                        DCHK(pos <= q00 + 32 * h2 + lane && pos < m);
                         if (!kSp || pos < cf) {
                             k0[pos] = key[h2];
                             s0[pos] = src[h2];
@@ -1000,6 +1006,7 @@ void join_launch(annk_state* s, const annk_dataset* ds, const uint32_t* order, u
     const uint32_t rmax = 3 * s->S + s->P;
     if (rmax > 0xffffu) throw_invalid("join: sample_cap/pool_cap too large for the device path");
     a.strip = ds->u8 ? kStrip : kStripF;
+    a.dbg_n = s->n;
     a.stage_words = ds->u8 ? 0u : 2 * (kWX * 32 + 32 * 32);
     a.rn = rup(rmax, 32);
     a.rs = a.rn + 8;
