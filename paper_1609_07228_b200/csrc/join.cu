@@ -43,6 +43,11 @@ namespace {
 constexpr uint32_t kWX = 16;     // fp32 rows: interleaved exact chains per lane
 constexpr uint32_t kStrip = 8;   // u8 rows: list rows per distance strip (the upper half of an IMMA m-tile)
 constexpr uint32_t kStripF = 16; // fp32 rows: one strip = kWX chains, so every partner row is read A/16 times
+constexpr uint32_t kFC = 16;     // fp32 rows: dimensions per staged chunk (double-buffered: 2 x 3 KB per warp)
+constexpr uint32_t kFG = kFC / 4;  // 16-byte pieces per staged row chunk
+// window row r's 16-byte pieces are XOR-swizzled so 8 lanes reading the same
+// piece of 8 different rows hit 8 different bank groups
+__device__ __forceinline__ uint32_t fswz(uint32_t r) { return (r >> 1) & (kFG - 1); }
 constexpr uint32_t kPad = 64;    // member arrays padded so a partner window may read past the list
 constexpr uint32_t kMemRegs = 5;  // list members held per lane (lists <= 160): next-point fetch, reservations
 enum : int { kModeU8 = 0, kModeF32 = 1 };
@@ -168,76 +173,83 @@ __device__ __forceinline__ void strip_distances(const JArgs& a, const uint32_t* 
         // conflict-free; strip rows are read as broadcasts.
         const uint32_t nxr = xe - xb;
         const uint32_t sbase = uint32_t(__cvta_generic_to_shared(stage));
-        const uint32_t nchunk = (a.ld + 31) / 32;
+        const uint32_t nchunk = (a.ld + kFC - 1) / kFC;
         for (uint32_t yb = max(yb0, (xb + 1) / 32); yb < yb1; ++yb) {
-            const float* xsrc[kWX * 8 / 32];
-            const float* ysrc[8];
+            const float* xsrc[kWX * kFG / 32];
+            const float* ysrc[32 * kFG / 32];
 #pragma unroll
-            for (uint32_t j = 0; j < kWX * 8 / 32; ++j) {
-                const uint32_t e = j * 32 + lane, r = e >> 3;
-                xsrc[j] = a.x + size_t(ids[xb + min(r, nxr - 1)]) * a.ld + (e & 7) * 4;
+            for (uint32_t j = 0; j < kWX * kFG / 32; ++j) {
+                const uint32_t e = j * 32 + lane, r = e / kFG;
+                xsrc[j] = a.x + size_t(ids[xb + min(r, nxr - 1)]) * a.ld + (e % kFG) * 4;
             }
 #pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) {
-                const uint32_t e = j * 32 + lane, r = e >> 3;
-                ysrc[j] = a.x + size_t(ids[min(yb * 32 + r, R - 1)]) * a.ld + (e & 7) * 4;
+            for (uint32_t j = 0; j < 32 * kFG / 32; ++j) {
+                const uint32_t e = j * 32 + lane, r = e / kFG;
+                ysrc[j] = a.x + size_t(ids[min(yb * 32 + r, R - 1)]) * a.ld + (e % kFG) * 4;
             }
             auto issue = [&](uint32_t c, uint32_t buf) {
-                const uint32_t c0 = c * 32;
-                const uint32_t xo = sbase + buf * (kWX * 32 + 32 * 32) * 4, yo = xo + kWX * 32 * 4;
+                const uint32_t c0 = c * kFC;
+                const uint32_t xo = sbase + buf * (kWX * kFC + 32 * kFC) * 4, yo = xo + kWX * kFC * 4;
 #pragma unroll
-                for (uint32_t j = 0; j < kWX * 8 / 32; ++j) {
-                    const uint32_t e = j * 32 + lane, r = e >> 3, g = e & 7;
+                for (uint32_t j = 0; j < kWX * kFG / 32; ++j) {
+                    const uint32_t e = j * 32 + lane, r = e / kFG, g = e % kFG;
                     const uint32_t bytes = c0 + g * 4 < a.ld ? 16u : 0u;
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(xo + (r * 32 + g * 4) * 4),
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(xo + (r * kFC + g * 4) * 4),
                                  "l"(xsrc[j] + (bytes ? c0 : 0)), "r"(bytes)
                                  : "memory");
                 }
 #pragma unroll
-                for (uint32_t j = 0; j < 8; ++j) {
-                    const uint32_t e = j * 32 + lane, r = e >> 3, g = e & 7;
+                for (uint32_t j = 0; j < 32 * kFG / 32; ++j) {
+                    const uint32_t e = j * 32 + lane, r = e / kFG, g = e % kFG;
                     const uint32_t bytes = c0 + g * 4 < a.ld ? 16u : 0u;
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
-                                     yo + (r * 32 + ((g ^ (r & 7)) * 4)) * 4),
+                                     yo + (r * kFC + ((g ^ fswz(r)) * 4)) * 4),
                                  "l"(ysrc[j] + (bytes ? c0 : 0)), "r"(bytes)
                                  : "memory");
                 }
                 asm volatile("cp.async.commit_group;" ::: "memory");
             };
-            float acc[kWX];
+            // only as many chains as the strip has rows (the last strip of a point is often short)
+            auto chains = [&](auto ncw) {
+                constexpr uint32_t NC = decltype(ncw)::value;
+                float acc[NC];
 #pragma unroll
-            for (uint32_t k = 0; k < kWX; ++k) acc[k] = 0.0f;
-            issue(0, 0);
-            for (uint32_t c = 0; c < nchunk; ++c) {
-                const uint32_t buf = c & 1;
-                if (c + 1 < nchunk) {
-                    issue(c + 1, buf ^ 1);
-                    asm volatile("cp.async.wait_group 1;" ::: "memory");
-                } else {
-                    asm volatile("cp.async.wait_group 0;" ::: "memory");
-                }
-                __syncwarp();
-                const float* xs = stage + buf * (kWX * 32 + 32 * 32);
-                const float* ys = xs + kWX * 32 + lane * 32;
-                const uint32_t cw = min(32u, a.ld - c * 32);  // a multiple of 4
-                for (uint32_t k = 0; k < cw; k += 4) {
-                    const float4 bv = *reinterpret_cast<const float4*>(ys + (((k >> 2) ^ (lane & 7)) << 2));
-#pragma unroll
-                    for (uint32_t u = 0; u < kWX; ++u) {
-                        const float4 v = *reinterpret_cast<const float4*>(xs + u * 32 + k);
-                        float d;
-                        d = __fsub_rn(v.x, bv.x); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
-                        d = __fsub_rn(v.y, bv.y); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
-                        d = __fsub_rn(v.z, bv.z); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
-                        d = __fsub_rn(v.w, bv.w); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                for (uint32_t k = 0; k < NC; ++k) acc[k] = 0.0f;
+                issue(0, 0);
+                for (uint32_t c = 0; c < nchunk; ++c) {
+                    const uint32_t buf = c & 1;
+                    if (c + 1 < nchunk) {
+                        issue(c + 1, buf ^ 1);
+                        asm volatile("cp.async.wait_group 1;" ::: "memory");
+                    } else {
+                        asm volatile("cp.async.wait_group 0;" ::: "memory");
                     }
-                }
-                __syncwarp();  // this buffer is refilled two chunks later
-            }
-            const uint32_t y = yb * 32 + lane;
+                    __syncwarp();
+                    const float* xs = stage + buf * (kWX * kFC + 32 * kFC);
+                    const float* ys = xs + kWX * kFC + lane * kFC;
+                    const uint32_t cw = min(kFC, a.ld - c * kFC);  // a multiple of 4
+                    for (uint32_t k = 0; k < cw; k += 4) {
+                        const float4 bv = *reinterpret_cast<const float4*>(ys + (((k >> 2) ^ fswz(lane)) << 2));
 #pragma unroll
-            for (uint32_t u = 0; u < kWX; ++u)
-                if (u < nxr) D[size_t(u) * a.rs + y] = acc[u];
+                        for (uint32_t u = 0; u < NC; ++u) {
+                            const float4 v = *reinterpret_cast<const float4*>(xs + u * kFC + k);
+                            float d;
+                            d = __fsub_rn(v.x, bv.x); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                            d = __fsub_rn(v.y, bv.y); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                            d = __fsub_rn(v.z, bv.z); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                            d = __fsub_rn(v.w, bv.w); acc[u] = __fadd_rn(acc[u], __fmul_rn(d, d));
+                        }
+                    }
+                    __syncwarp();  // this buffer is refilled two chunks later
+                }
+                const uint32_t y = yb * 32 + lane;
+#pragma unroll
+                for (uint32_t u = 0; u < NC; ++u)
+                    if (u < nxr) D[size_t(u) * a.rs + y] = acc[u];
+            };
+            if (nxr <= 4) chains(std::integral_constant<uint32_t, 4>{});
+            else if (nxr <= 8) chains(std::integral_constant<uint32_t, 8>{});
+            else chains(std::integral_constant<uint32_t, kWX>{});
         }
     }
 }
@@ -1007,7 +1019,7 @@ void join_launch(annk_state* s, const annk_dataset* ds, const uint32_t* order, u
     if (rmax > 0xffffu) throw_invalid("join: sample_cap/pool_cap too large for the device path");
     a.strip = ds->u8 ? kStrip : kStripF;
     a.dbg_n = s->n;
-    a.stage_words = ds->u8 ? 0u : 2 * (kWX * 32 + 32 * 32);
+    a.stage_words = ds->u8 ? 0u : 2 * (kWX * kFC + 32 * kFC);
     a.rn = rup(rmax, 32);
     a.rs = a.rn + 8;
     a.ol = rup(std::max(384u, 2 * a.rn), 32);  // 384 (was 768): 14 instead of 11 warps per SM, join 37.2 -> 35.3 ms
