@@ -481,16 +481,27 @@ __global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int
 
 // Merge `splits` sorted k-lists per query into the final k.
 __global__ void bf_merge_kernel(const uint64_t* __restrict__ part, uint32_t nq, uint32_t splits,
-                                uint32_t k, uint32_t m, uint64_t* __restrict__ out) {
+                                uint32_t k, uint32_t m, uint64_t* __restrict__ out, uint32_t out_stride,
+                                uint32_t first_sorted) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t qi = blockIdx.x * (blockDim.x / 32) + warp;
     uint64_t* s = reinterpret_cast<uint64_t*>(smem) + size_t(warp) * m;
     if (qi >= nq) return;
+    if (first_sorted) {
+        // list 0 is sorted and the other lists hold their keys first (kEmptyKey after them):
+        // when those are all empty the result is list 0
+        bool empty = true;
+        for (uint32_t l = 1 + lane; l < splits; l += 32) empty &= part[(size_t(qi) * splits + l) * k] == kEmptyKey;
+        if (__all_sync(0xffffffffu, empty)) {
+            for (uint32_t j = lane; j < k; j += 32) out[size_t(qi) * out_stride + j] = part[size_t(qi) * splits * k + j];
+            return;
+        }
+    }
     for (uint32_t j = lane; j < m; j += 32) s[j] = j < splits * k ? part[size_t(qi) * splits * k + j] : kEmptyKey;
     __syncwarp();
     warp_bitonic_sort(s, m);
-    for (uint32_t j = lane; j < k; j += 32) out[size_t(qi) * k + j] = s[j];
+    for (uint32_t j = lane; j < k; j += 32) out[size_t(qi) * out_stride + j] = s[j];
 }
 
 // Large-k path (k > kBigK, small inputs only): all keys, then a block sort per query.
@@ -579,11 +590,13 @@ __global__ void accuracy_hits_kernel(const uint32_t* __restrict__ graph, uint32_
         if (local[j]) atomicAdd(&hits[j], local[j]);
 }
 
-void merge_split_lists(const uint64_t* part, uint32_t nq, uint32_t splits, uint32_t k, uint64_t* out_keys) {
+void merge_split_lists(const uint64_t* part, uint32_t nq, uint32_t splits, uint32_t k, uint64_t* out_keys,
+                       uint32_t out_stride, bool first_sorted) {
+    if (out_stride == 0) out_stride = k;
     const uint32_t m = next_pow2(splits * k);
     const uint32_t wpb = std::max(1u, std::min(8u, uint32_t(64 * 1024 / (m * 8))));
     CK(cudaFuncSetAttribute(bf_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wpb * m * 8)));
-    LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part, nq, splits, k, m, out_keys);
+    LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part, nq, splits, k, m, out_keys, out_stride, first_sorted ? 1u : 0u);
 }
 
 void brute_force_tiles(const annk_dataset* base, const float* qdata, uint32_t nq, const uint32_t* self_ids,
@@ -687,7 +700,7 @@ void brute_force_tiles(const annk_dataset* base, const float* qdata, uint32_t nq
         const uint32_t m = next_pow2(splits * k);
         const uint32_t wpb = std::max(1u, std::min(8u, uint32_t(64 * 1024 / (m * 8))));
         CK(cudaFuncSetAttribute(bf_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wpb * m * 8)));
-        LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part.p, nq, splits, k, m, out_keys);
+        LAUNCH(bf_merge_kernel, (nq + wpb - 1) / wpb, wpb * 32, wpb * m * 8, part.p, nq, splits, k, m, out_keys, k, 0u);
     }
 }
 

@@ -164,7 +164,11 @@ void forest_upload_views(annk_forest* f);
 void brute_force_device(const annk_dataset* base, const float* qdata, uint32_t q_ld, uint32_t nq,
                         const uint32_t* self_rows, uint32_t k, uint64_t* out_keys);
 // merge `splits` sorted k-lists per query (nq x splits x k keys) into the final k
-void merge_split_lists(const uint64_t* part, uint32_t nq, uint32_t splits, uint32_t k, uint64_t* out_keys);
+// (the lists need not be sorted; out_stride: keys between consecutive queries' output rows, 0 = k;
+// first_sorted: list 0 is sorted and the others hold their keys first, so a query whose other
+// lists are empty is copied)
+void merge_split_lists(const uint64_t* part, uint32_t nq, uint32_t splits, uint32_t k, uint64_t* out_keys,
+                       uint32_t out_stride = 0, bool first_sorted = false);
 // exact kNN on tcgen05 (brute_force_tc.cu); false when the shape is not supported
 bool brute_force_tc(const annk_dataset* base, uint32_t nq, const uint32_t* self_ids, uint32_t k,
                     uint64_t* out_keys, const uint8_t* q8, const int32_t* qnorm);

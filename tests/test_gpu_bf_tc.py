@@ -92,3 +92,81 @@ def test_tc_rows_subset_shard_mode():
     rows = np.array([0, 1, 63, 64, 6999, 4097, 12, 5000], np.uint32)
     full = A.brute_force_knn(x, None, 100)
     np.testing.assert_array_equal(A.brute_force_rows(x, rows, 100), full[rows])
+
+
+def _cells(mode):
+    class _Ctx:
+        def __enter__(self):
+            os.environ["ANNK_BF_CELLS"] = mode
+
+        def __exit__(self, *a):
+            del os.environ["ANNK_BF_CELLS"]
+    return _Ctx()
+
+
+@pytest.mark.parametrize("n,k,seed", [(3000, 100, 1), (2049, 128, 3), (1000, 10, 4), (777, 1, 5)])
+def test_tc_pruned_scan_small_matches_oracle(n, k, seed):
+    # the pruned scan (rows and queries grouped by nearest pivot, home tiles first, cells beyond
+    # every threshold of a query block dropped) forced at small sizes: same ids and distance bits
+    o = ora()
+    x = mixture(n, 128, 12, seed)
+    with _cells("1"):
+        (ids, d), names = _bf(x, None, k, with_dists=True)
+    assert any("gather_cells_kernel" in s for s in names), names
+    ids_o, d_o, _ = o.brute_force(o.vs(x), None, k, workers=8, with_dists=True)
+    np.testing.assert_array_equal(ids, ids_o)
+    np.testing.assert_array_equal(d.view(np.uint32), d_o.view(np.uint32))
+    # separate query set (its own cell order) and a row subset (self exclusion by original id)
+    q = mixture(333, 128, 12, seed, stream=2)
+    with _cells("1"):
+        idq, dq = A.brute_force_knn(x, q, k, with_dists=True)
+        rows = np.array([0, 1, 63, 64, n - 1, n // 2], np.uint32)
+        sub = A.brute_force_rows(x, rows, k)
+    idq_o, dq_o, _ = o.brute_force(o.vs(x), o.vs(q), k, workers=8, with_dists=True)
+    np.testing.assert_array_equal(idq, idq_o)
+    np.testing.assert_array_equal(dq.view(np.uint32), dq_o.view(np.uint32))
+    np.testing.assert_array_equal(sub, ids[rows])
+
+
+def test_tc_pruned_scan_duplicates():
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, 256, size=(1500, 128)).astype(np.float32)
+    x[100:400] = x[7]   # more ties at distance 0 than k: ordered by original id
+    with _cells("1"):
+        ids, d = A.brute_force_knn(x, None, 70, with_dists=True)
+    o = ora()
+    ids_o, d_o, _ = o.brute_force(o.vs(x), None, 70, workers=8, with_dists=True)
+    np.testing.assert_array_equal(ids, ids_o)
+    np.testing.assert_array_equal(d.view(np.uint32), d_o.view(np.uint32))
+
+
+def test_tc_pruned_scan_equals_plain_scan_large():
+    # 50k x 50k takes the pruned scan by default; the plain scan is the checker
+    x = mixture(50000, 128, 100, 13)
+    (ids, d), names = _bf(x, None, 100, with_dists=True)
+    assert any("gather_cells_kernel" in s for s in names), names
+    with _cells("0"):
+        (ids0, d0), names0 = _bf(x, None, 100, with_dists=True)
+    assert not any("gather_cells_kernel" in s for s in names0), names0
+    np.testing.assert_array_equal(ids, ids0)
+    np.testing.assert_array_equal(d.view(np.uint32), d0.view(np.uint32))
+    q = mixture(40000, 128, 100, 13, stream=2)
+    idq = A.brute_force_knn(x, q, 100)
+    with _cells("0"):
+        idq0 = A.brute_force_knn(x, q, 100)
+    np.testing.assert_array_equal(idq, idq0)
+
+
+def test_tc_pruned_scan_uniform_rows():
+    # no cluster structure: nothing can be pruned, every cell is visited after the home tiles
+    rng = np.random.default_rng(11)
+    x = rng.integers(0, 256, size=(4000, 128)).astype(np.float32)
+    q = rng.integers(0, 256, size=(500, 128)).astype(np.float32)
+    o = ora()
+    with _cells("1"):
+        ids, d = A.brute_force_knn(x, None, 50, with_dists=True)
+        idq = A.brute_force_knn(x, q, 50)
+    ids_o, d_o, _ = o.brute_force(o.vs(x), None, 50, workers=8, with_dists=True)
+    np.testing.assert_array_equal(ids, ids_o)
+    np.testing.assert_array_equal(d.view(np.uint32), d_o.view(np.uint32))
+    np.testing.assert_array_equal(idq, o.brute_force(o.vs(x), o.vs(q), 50, workers=8))
