@@ -101,6 +101,11 @@ int annk_brute_force_knn(const annk_dataset* base, const annk_dataset* queries, 
  * rows act as queries (used to score accuracy on a seeded sample). */
 int annk_brute_force_rows(const annk_dataset* base, const uint32_t* rows, uint32_t n_rows,
                           uint32_t k, uint32_t* out_ids, float* out_dists);
+/* Measurement only (no reference counterpart): (256-query block, 64-row base
+ * tile) pairs of the last exact-kNN run on the tcgen05 u8 kernel -- all of
+ * them, and the ones its MMA passes visited (fewer when the pruned scan dropped
+ * cells that provably hold no neighbour; the result is the same).  Synchronises. */
+int annk_bf_last_scan(uint64_t* tiles_total, uint64_t* tiles_visited, int* pruned);
 /* eval.cpp:129-155 accuracy_vs_k: for each k' in k_list, the fraction of graph
  * edges (n x k ids) whose target lies in the exact k'-NN of the source (exact
  * self-mode truth at max k' computed on the device). out: n_k doubles. */

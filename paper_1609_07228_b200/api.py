@@ -192,6 +192,15 @@ def brute_force_rows(base, rows: np.ndarray, k: int, with_dists: bool = False):
     return (ids, d) if with_dists else ids
 
 
+def bf_last_scan() -> dict:
+    """Measurement only: (query block, base tile) pairs of the last exact-kNN run on
+    the tcgen05 u8 kernel, and how many of them its MMA passes visited."""
+    import ctypes as C
+    tot, vis, pr = C.c_uint64(0), C.c_uint64(0), C.c_int(0)
+    check(lib.annk_bf_last_scan(C.byref(tot), C.byref(vis), C.byref(pr)))
+    return {"tiles_total": tot.value, "tiles_visited": vis.value, "pruned": bool(pr.value)}
+
+
 def accuracy_vs_k(graph, vs, k_list, workers: int = 1) -> list:
     """eval.cpp:129-155: [(k', fraction of graph edges inside the exact k'-NN)],
     exact truth and membership counted on the device."""

@@ -822,4 +822,11 @@ int annk_brute_force_rows(const annk_dataset* base, const uint32_t* rows, uint32
     });
 }
 
+int annk_bf_last_scan(uint64_t* tiles_total, uint64_t* tiles_visited, int* pruned) {
+    return abi([&] {
+        if (!tiles_total || !tiles_visited || !pruned) throw_invalid("bf_last_scan: null argument");
+        brute_force_tc_last_scan(tiles_total, tiles_visited, pruned);
+    });
+}
+
 }  // extern "C"

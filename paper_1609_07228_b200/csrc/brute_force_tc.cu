@@ -923,7 +923,11 @@ void assign_and_sort(const uint8_t* piv8, const int32_t* pivn, uint32_t C, const
     sort_by_cell(out.cell, out.perm, n, C);
 }
 
-uint64_t g_last_tiles_total = 0, g_last_tiles_visited = 0;  // of the last pruned run (annk_bf_last_scan)
+// Tile counts of the last tcgen05 u8 run (annk_bf_last_scan): the device counters
+// land in a pinned host triple behind the run, read after a synchronize.
+uint64_t g_last_tiles_total = 0;
+bool g_last_pruned = false;
+unsigned long long* g_last_counts = nullptr;  // pinned: [0] pivot distance sum, [1] tiles kept by the pruning, [2] home tiles
 
 // Exact top-k with most of the base pruned away:
 //  1. cells: rows (and queries) grouped by their nearest of C pivot rows;
@@ -1055,15 +1059,14 @@ void tc_run_pruned(const TcProblem& pr, uint64_t* out_keys) {
     merge_split_lists(fin.p, nq, 3, k, out_keys, 0, true);
     pt.mark("merge");
     pt.report();
+    if (!g_last_counts) CK(cudaMallocHost(&g_last_counts, 3 * sizeof(unsigned long long)));
+    CK(cudaMemcpyAsync(g_last_counts, sum.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream()));
+    g_last_tiles_total = uint64_t(qblocks) * n_tiles;
+    g_last_pruned = true;
     if (getenv("ANNK_BF_STATS")) {  // (synchronises) how much of the base the rest pass visited
-        unsigned long long h[3];
-        sum.download(h, 3);
         ssync();
-        const unsigned long long home_t = h[2];
-        g_last_tiles_total = uint64_t(qblocks) * n_tiles;
-        g_last_tiles_visited = h[1] + h[2];
         fprintf(stderr, "[annk] pruned exact kNN: %u cells, tiles visited %llu of %llu (home %llu)\n", C,
-                (unsigned long long)g_last_tiles_visited, (unsigned long long)g_last_tiles_total, home_t);
+                g_last_counts[1] + g_last_counts[2], (unsigned long long)g_last_tiles_total, g_last_counts[2]);
     }
 }
 
@@ -1075,7 +1078,11 @@ void tc_run(const TcProblem& pr, uint64_t* out_keys) {
     const bool pruned = !off && n_tiles >= 8 && pr.nb > pr.k + 2 * kTB &&
                         (force || (qblocks >= uint32_t(num_sms()) && pr.nb >= 16384));
     if (pruned) tc_run_pruned(pr, out_keys);
-    else tc_launch(pr, TcMode{}, out_keys);
+    else {
+        tc_launch(pr, TcMode{}, out_keys);
+        g_last_tiles_total = uint64_t(qblocks) * n_tiles;
+        g_last_pruned = false;
+    }
 }
 
 }  // namespace
@@ -1088,6 +1095,16 @@ bool brute_force_tc(const annk_dataset* base, uint32_t nq, const uint32_t* self_
     if (getenv("ANNK_BF_MMA_SYNC")) return false;
     tc_run(TcProblem{base->data8.p, base->norms8.p, base->n, q8, qnorm, nq, self_ids, k}, out_keys);
     return true;
+}
+
+// (query block, base tile) pairs of the last brute_force_tc run: all of them, and
+// the ones its MMA passes visited (home + rest pass of the pruned scan; the
+// blockmin pass over the pivots is not counted).  Synchronises.
+void brute_force_tc_last_scan(uint64_t* total, uint64_t* visited, int* pruned) {
+    ssync();
+    *total = g_last_tiles_total;
+    *visited = g_last_pruned && g_last_counts ? g_last_counts[1] + g_last_counts[2] : g_last_tiles_total;
+    *pruned = g_last_pruned ? 1 : 0;
 }
 
 }  // namespace annk

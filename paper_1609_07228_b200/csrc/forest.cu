@@ -49,6 +49,13 @@ constexpr uint32_t kMaxCluster = 8;      // CTAs per tree (thread-block cluster)
 constexpr uint32_t kClusterMin = 8192;  // nodes above this many points use the whole cluster
 constexpr size_t kPrefetchBytes = 4u << 20;
 constexpr uint32_t kDrawWin = 256;
+// staged tiles: warp 0 only decides the splits; it hands every node to warp kWarps-1 through
+// a ring of 32-byte events, and that warp writes the records (node, leaf children, depth,
+// even, parent links) and does the split's float division -- off the tree's dependent chain
+constexpr uint32_t kEvRing = 128;              // events (power of two)
+constexpr uint32_t kStagers = kBlock - 32;     // threads staging tile rows (warps 0..kWarps-2)
+constexpr uint32_t kEvLink = 1u << 24, kEvRight = 1u << 25, kEvLLeaf = 1u << 26, kEvRLeaf = 1u << 27,
+                   kEvSplit = 1u << 28, kEvLeaf = 1u << 29, kEvQuit = 1u << 30;
 
 struct StackEntry {
     uint32_t start, end, depth, parent, side;  // side 0 = left child, 1 = right
@@ -89,6 +96,8 @@ struct Smem {
     uint32_t dwin[kDrawWin];
     uint32_t dwin_base, draw_idx, node_count, leaf_count, max_depth, error;
     uint32_t t_start, t_size, t_sb;  // staged-tile request to the helper warps (t_size 0: done)
+    uint32_t ev_count, ev_tail;      // events emitted by warp 0 / consumed by the record warp
+    alignas(16) uint4 ring[kEvRing * 2];
     long long cyc_block, cyc_warp;
     long long ft[16], ft_last;
     uint32_t bsp;
@@ -230,15 +239,15 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t count) {
 }
 
 // Copies the rows of s.sub[ts, ts+tsz) (u8, ld8 bytes each) into s.stage with
-// row stride sb.  Called by all kBlock threads (warp 0 + the helper warps).
+// row stride sb.  Called by the kStagers threads of warps 0..kWarps-2 (warp 0 + the helper warps).
 __device__ __forceinline__ void stage_rows(const BuildArgs& a, Smem& s, uint32_t ts, uint32_t tsz, uint32_t sb) {
     const uint32_t parts = a.ld8 / 16;
     const uint32_t total = tsz * parts;
-    for (uint32_t j0 = 0; j0 < total; j0 += kBlock * 8) {
+    for (uint32_t j0 = 0; j0 < total; j0 += kStagers * 8) {
         uint4 r[8];
 #pragma unroll
         for (uint32_t u = 0; u < 8; ++u) {
-            const uint32_t j = j0 + u * kBlock + threadIdx.x;
+            const uint32_t j = j0 + u * kStagers + threadIdx.x;
             if (j < total) {
                 const uint32_t row = j / parts, part = j - row * parts;
                 r[u] = __ldg(reinterpret_cast<const uint4*>(a.x8 + size_t(s.sub[ts + row]) * a.ld8) + part);
@@ -246,7 +255,7 @@ __device__ __forceinline__ void stage_rows(const BuildArgs& a, Smem& s, uint32_t
         }
 #pragma unroll
         for (uint32_t u = 0; u < 8; ++u) {
-            const uint32_t j = j0 + u * kBlock + threadIdx.x;
+            const uint32_t j = j0 + u * kStagers + threadIdx.x;
             if (j < total) {
                 const uint32_t row = j / parts, part = j - row * parts;
                 uint32_t* dst = reinterpret_cast<uint32_t*>(s.stage + row * sb + part * 16);
@@ -263,11 +272,99 @@ __device__ __forceinline__ void stage_rows(const BuildArgs& a, Smem& s, uint32_t
 // rows of each tile warp 0 requests (named barrier 1 = request, 2 = done).
 __device__ void stage_helper(const BuildArgs& a, Smem& s) {
     for (;;) {
-        named_bar(1, kBlock);
+        named_bar(1, kStagers);
         const uint32_t ts = s.t_start, tsz = s.t_size;
         if (tsz == 0) break;
         stage_rows(a, s, ts, tsz, s.t_sb);
-        named_bar(2, kBlock);
+        named_bar(2, kStagers);
+    }
+}
+
+// ---- tile events (warp 0 -> the record warp).  An event is two 16-byte halves,
+//   A = {node id, parent id, split dim | depth << 16 | flags, seq}
+//   B = {column sum (or the split's bits with kEvSplit), point_index position of the node's
+//        first point, left size | right size << 11, seq}          (kEvLeaf: left size = size)
+// each written by one 128-bit shared-memory store and read by one 128-bit load, so a half
+// is seen whole or not at all; seq = event number + 1 marks it valid (the ring starts zeroed).
+__device__ __forceinline__ void sts_v4(uint4* p, uint4 v) {
+    asm volatile("st.volatile.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(uint32_t(__cvta_generic_to_shared(p))),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(uint32_t(__cvta_generic_to_shared(p)))
+                 : "memory");
+    return v;
+}
+// warp 0, uniform arguments; ev = events emitted so far
+__device__ __forceinline__ void emit_event(Smem& s, uint32_t& ev, uint32_t id, uint32_t par, uint32_t meta,
+                                           uint32_t val, uint32_t pos, uint32_t sizes) {
+    if ((ev & 31u) == 0) {  // room for the next 32 events
+        while (ev + 32u - *reinterpret_cast<volatile uint32_t*>(&s.ev_tail) > kEvRing) {
+        }
+    }
+    if (lane_id() == 0) {
+        uint4* slot = s.ring + (ev & (kEvRing - 1)) * 2;
+        sts_v4(slot, make_uint4(id, par, meta, ev + 1));
+        sts_v4(slot + 1, make_uint4(val, pos, sizes, ev + 1));
+    }
+    ++ev;
+}
+
+// The record warp: every lane takes one pending event; records first, parent links after
+// (a link may target a record written by another lane in the same pass).
+__device__ void record_warp(const BuildArgs& a, Smem& s) {
+    const uint32_t lane = lane_id();
+    uint32_t ct = s.ev_tail;
+    for (;;) {
+        const uint32_t e = ct + lane;
+        const uint4* slot = s.ring + (e & (kEvRing - 1)) * 2;
+        const uint4 A = lds_v4(slot), B = lds_v4(slot + 1);
+        const uint32_t okm = __ballot_sync(0xffffffffu, A.w == e + 1 && B.w == e + 1);
+        const uint32_t cnt = okm == 0xffffffffu ? 32u : uint32_t(__ffs(~okm)) - 1u;
+        if (cnt == 0) {
+            __nanosleep(32);
+            continue;
+        }
+        __threadfence_block();
+        const bool mine = lane < cnt;
+        const uint32_t id = A.x, meta = A.z;
+        const uint32_t cdep = (meta >> 16) & 0xffu;
+        if (mine && !(meta & kEvQuit)) {
+            if (meta & kEvLeaf) {
+                reinterpret_cast<uint4*>(a.nodes)[id] = make_uint4(kLeaf, 0u, B.y, B.y + (B.z & 0x7ffu));
+                a.depth[id] = cdep;
+                a.even[id] = 0;
+            } else {
+                const uint32_t nl = B.z & 0x7ffu, nr = B.z >> 11;
+                const bool lleaf = meta & kEvLLeaf, rleaf = meta & kEvRLeaf;
+                const uint32_t sp = (meta & kEvSplit) ? B.x : __float_as_uint(__fdiv_rn(float(B.x), float(nl + nr)));
+                reinterpret_cast<uint4*>(a.nodes)[id] = make_uint4(meta & 0xffffu, sp, id + 1, lleaf ? id + 2 : 0u);
+                a.depth[id] = cdep;
+                a.even[id] = (meta & kEvSplit) ? 1 : 0;
+                if (lleaf) {
+                    reinterpret_cast<uint4*>(a.nodes)[id + 1] = make_uint4(kLeaf, 0u, B.y, B.y + nl);
+                    a.depth[id + 1] = cdep + 1;
+                    a.even[id + 1] = 0;
+                    if (rleaf) {
+                        reinterpret_cast<uint4*>(a.nodes)[id + 2] = make_uint4(kLeaf, 0u, B.y + nl, B.y + nl + nr);
+                        a.depth[id + 2] = cdep + 1;
+                        a.even[id + 2] = 0;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (mine && (meta & kEvLink)) {
+            if (meta & kEvRight) a.nodes[A.y].right = id;
+            else a.nodes[A.y].left = id;
+        }
+        ct += cnt;
+        if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&s.ev_tail) = ct;
+        if (__any_sync(0xffffffffu, mine && (meta & kEvQuit))) break;
     }
 }
 
@@ -278,7 +375,7 @@ __device__ void stage_helper(const BuildArgs& a, Smem& s) {
 template <int C>
 __device__ __forceinline__ uint32_t tile_node_reg(const unsigned char* __restrict__ st, uint16_t* li,
                                                   const uint32_t* gid, uint32_t sb, uint32_t d,
-                                                  uint32_t start, uint32_t end, float& split, uint8_t& even) {
+                                                  uint32_t start, uint32_t end, uint32_t& sval, uint8_t& even) {
     const uint32_t lane = lane_id(), ltm = (1u << lane) - 1u;
     const uint32_t size = end - start;
     uint32_t loc[C], v[C];
@@ -317,7 +414,7 @@ __device__ __forceinline__ uint32_t tile_node_reg(const unsigned char* __restric
             cl += c;
             cr += min(32u, end - min(end, start + u * 32)) - c;
         }
-        split = __fdiv_rn(float(isum), float(size));
+        sval = isum;  // split = isum / size, divided by the record warp
         even = 0;
         __syncwarp();
         return start + nl;
@@ -372,7 +469,7 @@ __device__ __forceinline__ uint32_t tile_node_reg(const unsigned char* __restric
             if (q1 / 32 == uint32_t(u)) a1 = y;
         }
     }
-    split = midpoint_f(float(a0), float(a1));
+    sval = __float_as_uint(midpoint_f(float(a0), float(a1)));
     even = 1;
     __syncwarp();
     return start + size / 2;
@@ -395,7 +492,7 @@ __device__ __forceinline__ uint32_t tile_node_reg(const unsigned char* __restric
 // (value, global id, local row) keys.  Returns the split position.
 __device__ __noinline__ uint32_t tile_node_smem(Smem& s, const unsigned char* __restrict__ st, uint16_t* li,
                                                 uint16_t* lt, const uint32_t* gid, uint32_t sb, uint32_t d,
-                                                uint32_t e_start, uint32_t e_end, float& split, uint8_t& even) {
+                                                uint32_t e_start, uint32_t e_end, uint32_t& sval, uint8_t& even) {
     const uint32_t lane = lane_id(), ltm = (1u << lane) - 1u;
     const uint32_t size = e_end - e_start;
     uint32_t is = 0;
@@ -426,7 +523,7 @@ __device__ __noinline__ uint32_t tile_node_smem(Smem& s, const unsigned char* __
     __syncwarp();
     for (uint32_t j = lane; j < nr; j += 32) li[e_start + nl + j] = lt[j];
     __syncwarp();
-    split = __fdiv_rn(float(isum), float(size));
+    sval = isum;
     uint32_t mid = e_start + nl;
     even = 0;
     if (nl == 0 || nr == 0 || max(nl, nr) > 4u * min(nl, nr)) {
@@ -446,7 +543,7 @@ __device__ __noinline__ uint32_t tile_node_smem(Smem& s, const unsigned char* __
         for (uint32_t j = lane; j < size; j += 32) li[e_start + j] = uint16_t(k[j] & 0x7ffu);
         __syncwarp();
         mid = e_start + size / 2;
-        split = midpoint_f(float(st[uint32_t(li[mid - 1]) * sb + d]), float(st[uint32_t(li[mid]) * sb + d]));
+        sval = __float_as_uint(midpoint_f(float(st[uint32_t(li[mid - 1]) * sb + d]), float(st[uint32_t(li[mid]) * sb + d])));
         even = 1;
     }
     return mid;
@@ -470,10 +567,10 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
         s.t_sb = sb;
     }
     __syncwarp();
-    named_bar(1, kBlock);
+    named_bar(1, kStagers);
     stage_rows(a, s, ts, tsz, sb);
     for (uint32_t j = lane; j < tsz; j += 32) s.lidx[j] = uint16_t(j);
-    named_bar(2, kBlock);
+    named_bar(2, kStagers);
     FT_MARK(13);
     const unsigned char* st = s.stage;
     uint16_t* li = s.lidx;  // indexed by tile-relative slot
@@ -481,24 +578,21 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
     const uint32_t* gid = s.sub + ts;
     const uint32_t lcap = a.leaf_cap, pbase = base + ts, dep0 = root.depth;
     uint32_t nid = s.node_count, kd = s.draw_idx, wb = s.dwin_base, nleaf = s.leaf_count, maxd = s.max_depth;
+    uint32_t ev = s.ev_count;
+    // the parent's record (written by this warp on the warp path) must be visible before the
+    // record warp links the tile root into it
+    __threadfence_block();
     // current node in registers; only right siblings go through the stack.
     // Depth inside a tile is bounded (splits are <= 4:1 or even), so the
     // stack cannot overflow: <= log_{5/4}(1024) + 1 entries.
-    uint32_t cs = 0, ce = tsz, cdep = root.depth, cpar = root.parent, clink = 1u | (root.side ? 2u : 0u);
+    uint32_t cs = 0, ce = tsz, cdep = root.depth, cpar = root.parent;
+    uint32_t clink = kEvLink | (root.side ? kEvRight : 0u);
     uint32_t wsp = 0;
     for (;;) {
         const uint32_t size = ce - cs;
         const uint32_t id = nid++;
-        if (lane == 0 && (clink & 1u)) {
-            if (clink & 2u) a.nodes[cpar].right = id;
-            else a.nodes[cpar].left = id;
-        }
         if (size <= lcap) {  // a right child whose left sibling was internal
-            if (lane == 0) {
-                reinterpret_cast<uint4*>(a.nodes)[id] = make_uint4(kLeaf, 0u, pbase + cs, pbase + ce);
-                a.depth[id] = cdep;
-                a.even[id] = 0;
-            }
+            emit_event(s, ev, id, cpar, (cdep << 16) | clink | kEvLeaf, 0u, pbase + cs, size);
             ++nleaf;
             maxd = max(maxd, cdep);
         } else {
@@ -512,36 +606,29 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
             const uint32_t d = s.dwin[kd - wb];
             ++kd;
             FT_MARK(8);
-            float split;
+            uint32_t sval;
             uint8_t even;
             uint32_t mid;
             if (size <= 32) {
-                mid = tile_node_reg<1>(st, li, gid, sb, d, cs, ce, split, even);
+                mid = tile_node_reg<1>(st, li, gid, sb, d, cs, ce, sval, even);
             } else if (size <= 64) {
-                mid = tile_node_reg<2>(st, li, gid, sb, d, cs, ce, split, even);
+                mid = tile_node_reg<2>(st, li, gid, sb, d, cs, ce, sval, even);
             } else if (size <= 128) {
-                mid = tile_node_reg<4>(st, li, gid, sb, d, cs, ce, split, even);
+                mid = tile_node_reg<4>(st, li, gid, sb, d, cs, ce, sval, even);
             } else if (size <= 256) {
-                mid = tile_node_reg<8>(st, li, gid, sb, d, cs, ce, split, even);
+                mid = tile_node_reg<8>(st, li, gid, sb, d, cs, ce, sval, even);
             } else {
-                mid = tile_node_smem(s, st, li, lt, gid, sb, d, cs, ce, split, even);
+                mid = tile_node_smem(s, st, li, lt, gid, sb, d, cs, ce, sval, even);
             }
             FT_MARK(10);
-            // this node's record (left child = id + 1 in pre-order) and its leaf
-            // children, one lane each: lane 0 node, lane 1 left leaf, lane 2 right leaf
+            // the node and its leaf children go to the record warp (left child = id + 1 in
+            // pre-order, a leaf right child of a leaf left child = id + 2)
             const bool lleaf = mid - cs <= lcap, rleaf = ce - mid <= lcap;
             const bool both = lleaf && rleaf;
-            if (lane < 3) {
-                const bool l0 = lane == 0, l1 = lane == 1;
-                const uint32_t rid = id + lane;
-                const uint4 rec = l0 ? make_uint4(d, __float_as_uint(split), id + 1, lleaf ? id + 2 : 0u)
-                                     : make_uint4(kLeaf, 0u, pbase + (l1 ? cs : mid), pbase + (l1 ? mid : ce));
-                if (l0 || (l1 ? lleaf : both)) {
-                    reinterpret_cast<uint4*>(a.nodes)[rid] = rec;
-                    a.depth[rid] = l0 ? cdep : cdep + 1;
-                    a.even[rid] = l0 ? even : uint8_t(0);
-                }
-            }
+            emit_event(s, ev, id, cpar,
+                       d | (cdep << 16) | clink | (lleaf ? kEvLLeaf : 0u) | (rleaf ? kEvRLeaf : 0u) |
+                           (even ? kEvSplit : 0u),
+                       sval, pbase + cs, (mid - cs) | ((ce - mid) << 11));
             maxd = max(maxd, cdep + 1);
             if (!lleaf) {
                 // descend into the left child; the right one waits on the stack
@@ -576,7 +663,7 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
         cs = (lo >> 21) & 0x7ffu;
         ce = (lo >> 10) & 0x7ffu;
         cdep = dep0 + ((lo >> 2) & 0xffu);
-        clink = lo & 3u;
+        clink = ((lo & 1u) ? kEvLink : 0u) | ((lo & 2u) ? kEvRight : 0u);
     }
     if (lane == 0) {
         s.node_count = nid;
@@ -584,6 +671,7 @@ __device__ void warp_build_tile(const BuildArgs& a, Smem& s, const StackEntry& r
         s.dwin_base = wb;
         s.leaf_count = nleaf;
         s.max_depth = maxd;
+        s.ev_count = ev;
     }
     // point_index of the tile in leaf order
     for (uint32_t j = lane; j < tsz; j += 32) s.sub2[j] = gid[s.lidx[j]];
@@ -799,10 +887,14 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
         FT_MARK(6);
     }
     for (uint32_t j = lane; j < total; j += 32) a.pidx[base + j] = sub[j];
-    if (tile_max) {  // release the helper warps
+    if (tile_max) {  // release the helper warps and the record warp
         if (lane == 0) s.t_size = 0;
         __syncwarp();
-        named_bar(1, kBlock);
+        named_bar(1, kStagers);
+        uint32_t ev = s.ev_count;
+        emit_event(s, ev, 0u, 0u, kEvQuit, 0u, 0u, 0u);
+        if (lane == 0) s.ev_count = ev;
+        __syncwarp();
     }
     __syncwarp();
 }
@@ -1213,8 +1305,11 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
     Smem* lead = cl.map_shared_rank(&s, 0);  // the tree's leader CTA (rank 0) owns the build state
     const uint32_t tid = threadIdx.x;
     for (uint32_t i = rank * kBlock + tid; i < a.n; i += C * kBlock) a.pidx[i] = i;
+    for (uint32_t i = tid; i < kEvRing * 2; i += kBlock) s.ring[i] = make_uint4(0u, 0u, 0u, 0u);
     if (tid == 0) {
         s.dwin_base = 0xffffffffu - kDrawWin;  // empty window
+        s.ev_count = 0;
+        s.ev_tail = 0;
         s.draw_idx = 0;
         s.node_count = 0;
         s.leaf_count = 0;
@@ -1271,7 +1366,10 @@ __global__ void __launch_bounds__(kBlock, 1) forest_build_kernel(const BuildArgs
             if (rank == 0) {
                 const long long c0 = clock64();
                 if (tid < 32) warp_build_subtree(a, s, e);
-                else if (tile_capacity(a)) stage_helper(a, s);
+                else if (tile_capacity(a)) {
+                    if (tid >= kStagers) record_warp(a, s);
+                    else stage_helper(a, s);
+                }
                 if (tid == 0) s.cyc_warp += clock64() - c0;
                 __syncthreads();
             }

@@ -172,6 +172,7 @@ void merge_split_lists(const uint64_t* part, uint32_t nq, uint32_t splits, uint3
 // exact kNN on tcgen05 (brute_force_tc.cu); false when the shape is not supported
 bool brute_force_tc(const annk_dataset* base, uint32_t nq, const uint32_t* self_ids, uint32_t k,
                     uint64_t* out_keys, const uint8_t* q8, const int32_t* qnorm);
+void brute_force_tc_last_scan(uint64_t* total, uint64_t* visited, int* pruned);
 // exact kNN of fp32 rows: tcgen05 bf16x3 candidates + exact re-rank (brute_force_f32_tc.cu)
 bool brute_force_tc_f32(const annk_dataset* base, const float* qdata, uint32_t nq, const uint32_t* self_ids,
                         uint32_t k, uint64_t* out_keys);
