@@ -106,6 +106,10 @@ int annk_brute_force_rows(const annk_dataset* base, const uint32_t* rows, uint32
  * them, and the ones its MMA passes visited (fewer when the pruned scan dropped
  * cells that provably hold no neighbour; the result is the same).  Synchronises. */
 int annk_bf_last_scan(uint64_t* tiles_total, uint64_t* tiles_visited, int* pruned);
+/* Measurement only: the dense tcgen05 kind::i8 rate of this GPU in tera-ops/s
+ * (u8 multiply-add = 2 ops), one CTA per SM issuing `groups` M=128 x N=256 x K=128
+ * MMA groups on shared-memory operands -- the exact-kNN roofline's denominator. */
+int annk_measure_i8_peak(uint32_t groups, double* tera_ops);
 /* eval.cpp:129-155 accuracy_vs_k: for each k' in k_list, the fraction of graph
  * edges (n x k ids) whose target lies in the exact k'-NN of the source (exact
  * self-mode truth at max k' computed on the device). out: n_k doubles. */

@@ -12,7 +12,7 @@ from .api import (  # noqa: F401
     brute_force_knn, brute_force_rows, build_forest, build_graph, descend_from, detail, finalize, gen_mixture,
     state_stats,
     gen_synthetic, graph_accuracy, init_graph, init_random, recall, recall_curve, refine_nn_descent, search_leaves,
-    l2_sq, dist_sq, dist_sq_q,
+    l2_sq, dist_sq, dist_sq_q, bf_last_scan, measure_i8_peak,
 )
 
 __version__ = "0.1.0"

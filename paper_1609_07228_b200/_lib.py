@@ -75,6 +75,7 @@ _SIGS = {
                          _u64, _u32, _f32p],
     "annk_brute_force_knn": [_vp, _vp, _u32, _u32p, _vp, C.POINTER(_u64)],
     "annk_brute_force_rows": [_vp, _u32p, _u32, _u32, _u32p, _vp],
+    "annk_measure_i8_peak": [_u32, C.POINTER(C.c_double)],
     "annk_bf_last_scan": [C.POINTER(_u64), C.POINTER(_u64), C.POINTER(C.c_int)],
     "annk_accuracy_vs_k": [_vp, _u32p, _u32, _u32, _u32p, _u32, np.ctypeslib.ndpointer(np.float64, flags="C")],
     "annk_forest_build": [_vp, _u32, _u32, _u64, _pp],

@@ -192,6 +192,15 @@ def brute_force_rows(base, rows: np.ndarray, k: int, with_dists: bool = False):
     return (ids, d) if with_dists else ids
 
 
+def measure_i8_peak(groups: int = 20000) -> float:
+    """Measurement only: dense tcgen05 kind::i8 tera-ops/s of this GPU (MMA issue on
+    shared-memory operands, no loads, no epilogue)."""
+    import ctypes as C
+    out = C.c_double(0.0)
+    check(lib.annk_measure_i8_peak(groups, C.byref(out)))
+    return out.value
+
+
 def bf_last_scan() -> dict:
     """Measurement only: (query block, base tile) pairs of the last exact-kNN run on
     the tcgen05 u8 kernel, and how many of them its MMA passes visited."""
