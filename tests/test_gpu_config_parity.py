@@ -80,3 +80,56 @@ def test_search_k100_graph_large_pools(P, E):
     np.testing.assert_array_equal(r.ids, ids_o)
     np.testing.assert_array_equal(r.dists.view(np.uint32), d_o.view(np.uint32))
     np.testing.assert_array_equal(r.stats, st_o)
+
+
+def _masked_equal(a, b, sizes, what):
+    m = np.arange(a.shape[1])[None, :] < sizes[:, None]
+    bad = np.nonzero((np.where(m, a, 0) != np.where(m, b, 0)).any(axis=1))[0]
+    assert bad.size == 0, f"{what}: {bad.size} rows differ, first {bad[:5]}"
+
+
+def test_cfg2_full_size_forest_init_vs_reference_and_round_properties():
+    """BASELINE cfg2 at its full size (1M x 128 integer mixture, 8 trees leaf 8, K = P = 100,
+    S = 20): the forest and the initial graph (pools, flags, dist_comps) bit-identical to the
+    reference run on all host cores (both are independent of the worker count), then two
+    NN-descent rounds checked through size-independent properties of the finalized graph."""
+    o = O.load("reference") if O.reference_available() else ora()
+    n, dim, seed = 1_000_000, 128, 1
+    x = mixture(n, dim, 1000, seed)
+    vo = o.vs(x)
+    fo = o.build_forest(vo, 8, 8, seed, workers=CORES)
+    fd = A.build_forest(x, 8, 8, seed)
+    for t in range(8):
+        td, to = fd.tree(t), fo.tree(t)
+        assert td.n_nodes == to.n_nodes and td.leaf_count == to.leaf_count
+        np.testing.assert_array_equal(td.split_dim, to.split_dim)
+        np.testing.assert_array_equal(td.split_val.view(np.uint32), to.split_val.view(np.uint32))
+        np.testing.assert_array_equal(td.left, to.left)
+        np.testing.assert_array_equal(td.right, to.right)
+        np.testing.assert_array_equal(td.point_index, to.point_index)
+    so = o.init_graph(vo, fo, 100, 4, 100, 20, seed, workers=CORES)
+    sd = A.init_graph(x, fd, 100, 4, 100, 20, seed)
+    s, ids, d, f = sd.pools()
+    e = so.export()
+    np.testing.assert_array_equal(s, e["sizes"])
+    _masked_equal(ids, e["ids"], s, "init pool ids")
+    _masked_equal(d.view(np.uint32), e["dists"].view(np.uint32), s, "init pool dists")
+    _masked_equal(f, e["flags"], s, "init pool flags")
+    assert sd.meta()["dist_comps"] == e["dist_comps"]
+    del so, e, ids, d, f
+    for _ in range(2):
+        A.detail.nn_descent_iteration(sd, x)
+    g = A.finalize(sd, x, 100)
+    gd = g.dists
+    assert (g.ids != np.arange(n, dtype=np.uint32)[:, None]).all(), "a point is its own neighbour"
+    key = (gd.view(np.uint32).astype(np.uint64) << np.uint64(32)) | g.ids.astype(np.uint64)
+    assert (key[:, 1:] > key[:, :-1]).all(), "rows are not strictly ascending in (dist, id)"
+    srt = np.sort(g.ids, axis=1)
+    assert (srt[:, 1:] != srt[:, :-1]).all(), "duplicate neighbour ids in a row"
+    rows = np.random.default_rng(5).choice(n, 2000, replace=False)
+    diff = x[rows].astype(np.int64)[:, None, :] - x[g.ids[rows]].astype(np.int64)
+    np.testing.assert_array_equal((diff * diff).sum(axis=2).astype(np.float32).view(np.uint32),
+                                  gd[rows].view(np.uint32))
+    truth = A.brute_force_rows(x, rows.astype(np.uint32), 100)
+    hits = sum(len(np.intersect1d(g.ids[r], truth[j])) for j, r in enumerate(rows))
+    assert hits / (len(rows) * 100) >= 0.9, "cfg2 reaches graph accuracy 0.9 after two rounds"
