@@ -718,7 +718,8 @@ __device__ void warp_build_subtree(const BuildArgs& a, Smem& s, StackEntry root)
         --wsp;
         const StackEntry e = s.wstack[wsp];
         const uint32_t size = e.end - e.start;
-        if (size <= tile_max && size > a.leaf_cap && size >= 64 && e.parent != kInvalidId) {
+        // (events carry the depth in 8 bits: a tile adds < 64 levels, n < 2^32 gives < 100 above it)
+        if (size <= tile_max && size > a.leaf_cap && size >= 64 && e.parent != kInvalidId && e.depth < 160) {
             __syncwarp();
             warp_build_tile(a, s, e, base, sb);
             continue;
