@@ -739,6 +739,73 @@ __global__ void reverse_scatter_kernel(uint32_t n, uint32_t width, const uint32_
     }
 }
 
+// Reverse lists as ascending sets (the reference pushes them in ascending owner
+// order, graph_build.cpp:71-85): the scatter above leaves each list in arrival
+// order, one warp sorts it in registers (bitonic network over 1/2/4/8 ids per
+// lane) up to 256 ids.  Longer lists go on a work list: rev_sort_long_kernel
+// sorts those up to kRevSortSmem ids in shared memory; a list beyond that (a
+// hub) is counted in big[0] and the host falls back to the library segmented sort.
+constexpr uint32_t kRevSortSmem = 2048, kRevSortWarps = 8, kRevLongCap = 1u << 16;
+template <int V>
+__device__ __forceinline__ void rev_sort_regs(uint32_t* __restrict__ p, uint32_t len) {
+    const uint32_t lane = lane_id();
+    uint32_t v[V];
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+        const uint32_t j = r * 32 + lane;
+        v[r] = j < len ? p[j] : 0xffffffffu;
+    }
+    warp_sort_regs_u32<V>(v);
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+        const uint32_t j = r * 32 + lane;
+        if (j < len) p[j] = v[r];
+    }
+}
+// big: [0] lists the device cannot sort, [1] work-list length; wl: list ids (kRevLongCap)
+__global__ void __launch_bounds__(kRevSortWarps * 32) rev_sort_kernel(const uint32_t* __restrict__ off,
+                                                                      uint32_t* __restrict__ data, uint32_t lo,
+                                                                      uint32_t hi, uint32_t* __restrict__ big,
+                                                                      uint32_t* __restrict__ wl) {
+    const uint32_t lane = lane_id(), warp = threadIdx.x / 32;
+    const uint32_t i = lo + blockIdx.x * kRevSortWarps + warp;
+    if (i >= hi) return;
+    const uint32_t b = off[i], len = off[i + 1] - b;
+    if (len <= 1) return;
+    uint32_t* p = data + b;
+    if (len <= 32) rev_sort_regs<1>(p, len);
+    else if (len <= 64) rev_sort_regs<2>(p, len);
+    else if (len <= 128) rev_sort_regs<4>(p, len);
+    else if (len <= 256) rev_sort_regs<8>(p, len);
+    else if (lane == 0) {
+        if (len > kRevSortSmem) {
+            atomicAdd(big, 1u);
+        } else {
+            const uint32_t w = atomicAdd(big + 1, 1u);
+            if (w < kRevLongCap) wl[w] = i;
+            else atomicAdd(big, 1u);  // more long lists than the work list holds: library sort
+        }
+    }
+}
+__global__ void __launch_bounds__(32) rev_sort_long_kernel(const uint32_t* __restrict__ off, uint32_t* __restrict__ data,
+                                                           const uint32_t* __restrict__ big,
+                                                           const uint32_t* __restrict__ wl) {
+    __shared__ uint32_t s[kRevSortSmem];
+    const uint32_t lane = lane_id();
+    const uint32_t cnt = min(big[1], kRevLongCap);
+    for (uint32_t w = blockIdx.x; w < cnt; w += gridDim.x) {
+        const uint32_t i = wl[w];
+        const uint32_t b = off[i], len = off[i + 1] - b;
+        uint32_t* p = data + b;
+        const uint32_t m = next_pow2(len);
+        for (uint32_t j = lane; j < m; j += 32) s[j] = j < len ? p[j] : 0xffffffffu;
+        __syncwarp();
+        warp_bitonic_sort_u32(s, m);
+        for (uint32_t j = lane; j < len; j += 32) p[j] = s[j];
+        __syncwarp();
+    }
+}
+
 struct UnionArgs {
     uint32_t n, P, S;
     uint64_t round_seed;
@@ -1145,14 +1212,28 @@ void do_reverse(annk_state* s) {
            s->rn_off.p, s->rn_cur.p, s->rn_data.p, tlo, thi);
     LAUNCH(reverse_scatter_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->P, s->fold.p, s->cold.p,
            s->ro_off.p, s->ro_cur.p, s->ro_data.p, tlo, thi);
-    uint32_t tot[2];
-    CK(cudaMemcpyAsync(&tot[0], s->rn_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
-    CK(cudaMemcpyAsync(&tot[1], s->ro_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
-    ssync();
     // reverse lists as sets in ascending id order (the reference pushes them in
     // ascending owner order, graph_build.cpp:71-85)
-    segmented_sort(s->rn_data.p, tot[0], s->rn_off.p, n);
-    segmented_sort(s->ro_data.p, tot[1], s->ro_off.p, n);
+    DevBuf<uint32_t> big(4), wl(2 * size_t(kRevLongCap));
+    big.zero();
+    if (thi > tlo) {
+        const uint32_t grid = (thi - tlo + kRevSortWarps - 1) / kRevSortWarps;
+        LAUNCH(rev_sort_kernel, grid, kRevSortWarps * 32, 0, s->rn_off.p, s->rn_data.p, tlo, thi, big.p, wl.p);
+        LAUNCH(rev_sort_kernel, grid, kRevSortWarps * 32, 0, s->ro_off.p, s->ro_data.p, tlo, thi, big.p + 2,
+               wl.p + kRevLongCap);
+        const uint32_t lgrid = uint32_t(num_sms()) * 4;
+        LAUNCH(rev_sort_long_kernel, lgrid, 32, 0, s->rn_off.p, s->rn_data.p, big.p, wl.p);
+        LAUNCH(rev_sort_long_kernel, lgrid, 32, 0, s->ro_off.p, s->ro_data.p, big.p + 2, wl.p + kRevLongCap);
+    }
+    uint32_t tot[2], hb[4];
+    CK(cudaMemcpyAsync(&tot[0], s->rn_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
+    CK(cudaMemcpyAsync(&tot[1], s->ro_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
+    big.download(hb, 4);
+    ssync();
+    // a list too long for one warp (a hub with > 2048 reverse neighbours): the whole array
+    // goes through the library segmented sort (sorted lists stay sorted)
+    if (hb[0]) segmented_sort(s->rn_data.p, tot[0], s->rn_off.p, n);
+    if (hb[2]) segmented_sort(s->ro_data.p, tot[1], s->ro_off.p, n);
     s->stage = 1;
 }
 
@@ -1172,6 +1253,8 @@ void do_union(annk_state* s) {
     {
         const uint32_t tpb = 64;
         const size_t per = size_t(s->S + 1) * 8 + size_t(4 * s->S) * 4;
+        // S in 32..64 needs more than the default 48 KB of dynamic shared memory (98 KB at S = 64)
+        CK(cudaFuncSetAttribute(rev_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tpb * per)));
         if (hi > lo)
             LAUNCH(rev_sample_kernel, (2 * (hi - lo) + tpb - 1) / tpb, tpb, tpb * per, hi, s->S, round_seed,
                    s->rn_off.p, s->rn_data.p, s->ro_off.p, s->ro_data.p, samp.p, lo);

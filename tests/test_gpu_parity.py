@@ -533,3 +533,37 @@ def test_distance_entry_points():
         A.dist_sq(x, 0, 300)
     with pytest.raises(A.OutOfRange):
         A.dist_sq_q(x, q, 300)
+
+
+@pytest.mark.gpu
+def test_hub_reverse_lists_bit_exact():
+    """Two hubs (the centres of shells of 2600 and 1000 points in 64 dimensions: each is its
+    shell's nearest neighbour) give reverse lists of every size class of the device's list
+    sort: registers (<= 256 ids), shared memory (<= 2048) and the segmented-sort fallback
+    (the 2600-point hub), in the new and in the old lists."""
+    rng = np.random.default_rng(3)
+    dim = 64
+
+    def shell(c, r, m):
+        u = rng.normal(size=(m, dim))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        return c + r * u
+
+    c0, c1 = np.full(dim, 100.0), np.full(dim, -100.0)
+    x = np.vstack([c0[None], c1[None], shell(c0, 10.0, 2600), shell(c1, 10.0, 1000),
+                   rng.normal(size=(398, dim)) * 5]).astype(np.float32)
+    n = len(x)
+    o, vo, so, sd = _pair(x, 4, 10, 7, 10, 2, 40, 40)
+    longest = 0
+    for it in range(4):
+        co = so.nn_descent_iteration(vo)
+        cd = A.detail.nn_descent_iteration(sd, x)
+        assert cd == co, f"changes, iteration {it}"
+        for which in range(4):
+            dl, ol = sd.lists(which), so.lists(which)
+            for i in range(n):
+                np.testing.assert_array_equal(dl[i], ol[i], err_msg=f"list {which} row {i} iter {it}")
+            if which >= 2:
+                longest = max(longest, max(len(a) for a in ol))
+        assert_pools_equal(sd, so)
+    assert longest > 2048, "the data no longer produces a hub list beyond the shared-memory sort"
