@@ -837,7 +837,9 @@ __global__ void rev_sample_kernel(uint32_t n, uint32_t S, uint64_t round_seed, c
     uint32_t* pos = reinterpret_cast<uint32_t*>(xs + S + 1);
     uint32_t* val = pos + 2 * S;
     if (t >= 2 * (n - lo)) return;
-    const uint32_t i = lo + (t >> 1), kind = t & 1;
+    // kind-major: a warp's lanes all sample new lists or all old lists (right after init there
+    // are no old lists at all, so interleaving the kinds would idle every other lane)
+    const uint32_t kind = t >= n - lo ? 1u : 0u, i = lo + (t - kind * (n - lo));
     const uint32_t* off = kind ? ro_off : rn_off;
     const uint32_t* data = kind ? ro_data : rn_data;
     const uint32_t b = off[i], m = off[i + 1] - b;
@@ -851,29 +853,35 @@ __global__ void rev_sample_kernel(uint32_t n, uint32_t S, uint64_t round_seed, c
         xs[k] = x;
     }
     for (uint32_t k = S + 1; k < 156; ++k) x = 6364136223846793005ULL * (x ^ (x >> 62)) + uint64_t(k);
+    // the swaps of the partial Fisher-Yates: positions below S live in head[] (direct), the
+    // others in a small overlay searched linearly (at most one new entry per step)
+    uint32_t* head = val;
+    uint32_t* opos = pos;
+    uint32_t* oval = pos + S;
+    for (uint32_t k = 0; k < S; ++k) head[k] = a[k];
     uint32_t no = 0;
     for (uint32_t k = 0; k < S; ++k) {
         x = 6364136223846793005ULL * (x ^ (x >> 62)) + uint64_t(156 + k);
         const uint64_t r = mt_temper(mt_twist(xs[k], xs[k + 1], x));
         const uint32_t j = k + uint32_t(r % uint64_t(m - k));
-        uint32_t vk = a[k], vj = a[j];
-        int pk = -1, pj = -1;
-        for (uint32_t q = 0; q < no; ++q) {
-            if (pos[q] == k) { vk = val[q]; pk = int(q); }
-            if (pos[q] == j) { vj = val[q]; pj = int(q); }
-        }
         if (j == k) continue;  // swap with itself
-        if (pk < 0) { pos[no] = k; pk = int(no++); }
-        if (pj < 0) { pos[no] = j; pj = int(no++); }
-        val[pk] = vj;
-        val[pj] = vk;
+        const uint32_t vk = head[k];
+        if (j < S) {
+            head[k] = head[j];
+            head[j] = vk;
+        } else {
+            uint32_t q = 0;
+            while (q < no && opos[q] != j) ++q;
+            if (q == no) {
+                opos[no++] = j;
+                head[k] = a[j];
+            } else {
+                head[k] = oval[q];
+            }
+            oval[q] = vk;
+        }
     }
-    for (uint32_t k = 0; k < S; ++k) {
-        uint32_t v = a[k];
-        for (uint32_t q = 0; q < no; ++q)
-            if (pos[q] == k) v = val[q];
-        out[k] = v;
-    }
+    for (uint32_t k = 0; k < S; ++k) out[k] = head[k];
 }
 
 // graph_build.cpp:88-103 per point: sample reverse lists, union, sort-dedup.
