@@ -670,6 +670,8 @@ struct SampleArgs {
     uint32_t* cold;
     uint64_t* thr;
     uint32_t lo;  // points [lo, n) are sampled
+    uint32_t* rn_cnt;  // reverse-list sizes counted on the way (null: rev_count_kernel does it,
+    uint32_t* ro_cnt;  // shard mode, where the other ranks' forward rows arrive later)
 };
 
 // graph_build.cpp:71-85: ascending scan until S new entries are taken.
@@ -695,8 +697,10 @@ __global__ void sample_kernel(SampleArgs a) {
         if (in_scan && isnew) {
             a.fnew[size_t(i) * a.S + rank_new] = id;
             pf[j] &= uint8_t(~1u);  // flag_new cleared; `checked` (bit 1) untouched
+            if (a.rn_cnt) atomicAdd(&a.rn_cnt[id], 1u);
         } else if (in_scan) {
             a.fold[size_t(i) * a.P + nold + __popc(bo & lt)] = id;
+            if (a.ro_cnt) atomicAdd(&a.ro_cnt[id], 1u);
         }
         taken = min(a.S, taken + __popc(bn));
         nold += __popc(bo);
@@ -1194,7 +1198,14 @@ void do_sample(annk_state* s) {
     ensure_scratch(s);
     const uint32_t lo = own_lo(s), hi = own_hi(s);
     SampleArgs a{hi, s->P, s->S, s->keys.p, s->flags.p, s->sizes.p, s->fnew.p, s->fold.p,
-                 s->cnew.p, s->cold.p, s->thr.p, lo};
+                 s->cnew.p, s->cold.p, s->thr.p, lo, nullptr, nullptr};
+    s->counts_fused = !s->sharded;
+    if (s->counts_fused) {  // every forward row is written here: count the reverse lists on the way
+        s->rn_cnt.zero();
+        s->ro_cnt.zero();
+        a.rn_cnt = s->rn_cnt.p;
+        a.ro_cnt = s->ro_cnt.p;
+    }
     if (hi > lo) LAUNCH(sample_kernel, grid_for(size_t(hi - lo) * 32, 256), 256, 0, a);
     s->stage = 0;
 }
@@ -1204,14 +1215,17 @@ void do_sample(annk_state* s) {
 void do_reverse(annk_state* s) {
     ensure_scratch(s);
     const uint32_t n = s->n;
-    s->rn_cnt.zero();
-    s->ro_cnt.zero();
     // reverse lists are needed for the owned points only (all of them unsharded)
     const uint32_t tlo = own_lo(s), thi = own_hi(s);
-    LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->S, s->fnew.p, s->cnew.p, s->rn_cnt.p,
-           tlo, thi);
-    LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->P, s->fold.p, s->cold.p, s->ro_cnt.p,
-           tlo, thi);
+    if (!s->counts_fused) {
+        s->rn_cnt.zero();
+        s->ro_cnt.zero();
+        LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->S, s->fnew.p, s->cnew.p, s->rn_cnt.p,
+               tlo, thi);
+        LAUNCH(rev_count_kernel, grid_for(size_t(n) * 32, 256), 256, 0, n, s->P, s->fold.p, s->cold.p, s->ro_cnt.p,
+               tlo, thi);
+    }
+    s->counts_fused = false;
     exclusive_scan(s->rn_cnt.p, s->rn_off.p, n);
     exclusive_scan(s->ro_cnt.p, s->ro_off.p, n);
     s->rn_cur.zero();

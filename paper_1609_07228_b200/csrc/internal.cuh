@@ -102,6 +102,7 @@ struct annk_state {
     annk::DevBuf<uint32_t> order;                     // point visit order (tree-0 leaf order) for L2 locality
     uint32_t ov_cap = 0;
     int stage = 0;  // 0 none, 1 after rebuild_sample_lists, 2 after union_reverse_lists
+    bool counts_fused = false;  // the last do_sample also counted the reverse lists (unsharded)
     uint64_t join_rows = 0;
     uint32_t offer_cap = 0;
     uint64_t last_offers = 0, last_spilled = 0;
