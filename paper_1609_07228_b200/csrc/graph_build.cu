@@ -747,9 +747,10 @@ __global__ void reverse_scatter_kernel(uint32_t n, uint32_t width, const uint32_
 // order, graph_build.cpp:71-85): the scatter above leaves each list in arrival
 // order, one warp sorts it in registers (bitonic network over 1/2/4/8 ids per
 // lane) up to 256 ids.  Longer lists go on a work list: rev_sort_long_kernel
-// sorts those up to kRevSortSmem ids in shared memory; a list beyond that (a
-// hub) is counted in big[0] and the host falls back to the library segmented sort.
-constexpr uint32_t kRevSortSmem = 2048, kRevSortWarps = 8, kRevLongCap = 1u << 16;
+// sorts those up to kRevSortSmem ids in shared memory, one 256-thread CTA per
+// list; a list beyond that (a hub with more than 8192 reverse neighbours) is
+// counted in big[0] and the host falls back to the library segmented sort.
+constexpr uint32_t kRevSortSmem = 8192, kRevSortWarps = 8, kRevLongThreads = 256;
 template <int V>
 __device__ __forceinline__ void rev_sort_regs(uint32_t* __restrict__ p, uint32_t len) {
     const uint32_t lane = lane_id();
@@ -766,7 +767,7 @@ __device__ __forceinline__ void rev_sort_regs(uint32_t* __restrict__ p, uint32_t
         if (j < len) p[j] = v[r];
     }
 }
-// big: [0] lists the device cannot sort, [1] work-list length; wl: list ids (kRevLongCap)
+// big: [0] lists the device cannot sort, [1] work-list length; wl: list ids (one slot per list)
 __global__ void __launch_bounds__(kRevSortWarps * 32) rev_sort_kernel(const uint32_t* __restrict__ off,
                                                                       uint32_t* __restrict__ data, uint32_t lo,
                                                                       uint32_t hi, uint32_t* __restrict__ big,
@@ -785,28 +786,40 @@ __global__ void __launch_bounds__(kRevSortWarps * 32) rev_sort_kernel(const uint
         if (len > kRevSortSmem) {
             atomicAdd(big, 1u);
         } else {
-            const uint32_t w = atomicAdd(big + 1, 1u);
-            if (w < kRevLongCap) wl[w] = i;
-            else atomicAdd(big, 1u);  // more long lists than the work list holds: library sort
+            wl[atomicAdd(big + 1, 1u)] = i;
         }
     }
 }
-__global__ void __launch_bounds__(32) rev_sort_long_kernel(const uint32_t* __restrict__ off, uint32_t* __restrict__ data,
-                                                           const uint32_t* __restrict__ big,
-                                                           const uint32_t* __restrict__ wl) {
+__global__ void __launch_bounds__(kRevLongThreads) rev_sort_long_kernel(const uint32_t* __restrict__ off,
+                                                                        uint32_t* __restrict__ data,
+                                                                        const uint32_t* __restrict__ big,
+                                                                        const uint32_t* __restrict__ wl) {
     __shared__ uint32_t s[kRevSortSmem];
-    const uint32_t lane = lane_id();
-    const uint32_t cnt = min(big[1], kRevLongCap);
+    const uint32_t cnt = big[1];
     for (uint32_t w = blockIdx.x; w < cnt; w += gridDim.x) {
         const uint32_t i = wl[w];
         const uint32_t b = off[i], len = off[i + 1] - b;
         uint32_t* p = data + b;
         const uint32_t m = next_pow2(len);
-        for (uint32_t j = lane; j < m; j += 32) s[j] = j < len ? p[j] : 0xffffffffu;
-        __syncwarp();
-        warp_bitonic_sort_u32(s, m);
-        for (uint32_t j = lane; j < len; j += 32) p[j] = s[j];
-        __syncwarp();
+        for (uint32_t j = threadIdx.x; j < m; j += kRevLongThreads) s[j] = j < len ? p[j] : 0xffffffffu;
+        __syncthreads();
+        for (uint32_t k = 2; k <= m; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t e = threadIdx.x; e < m; e += kRevLongThreads) {
+                    const uint32_t x = e ^ j;
+                    if (x > e) {
+                        const uint32_t va = s[e], vb = s[x];
+                        if ((va > vb) == ((e & k) == 0)) {
+                            s[e] = vb;
+                            s[x] = va;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t j = threadIdx.x; j < len; j += kRevLongThreads) p[j] = s[j];
+        __syncthreads();
     }
 }
 
@@ -1236,23 +1249,23 @@ void do_reverse(annk_state* s) {
            s->ro_off.p, s->ro_cur.p, s->ro_data.p, tlo, thi);
     // reverse lists as sets in ascending id order (the reference pushes them in
     // ascending owner order, graph_build.cpp:71-85)
-    DevBuf<uint32_t> big(4), wl(2 * size_t(kRevLongCap));
+    DevBuf<uint32_t> big(4), wl(2 * size_t(n));
     big.zero();
     if (thi > tlo) {
         const uint32_t grid = (thi - tlo + kRevSortWarps - 1) / kRevSortWarps;
         LAUNCH(rev_sort_kernel, grid, kRevSortWarps * 32, 0, s->rn_off.p, s->rn_data.p, tlo, thi, big.p, wl.p);
         LAUNCH(rev_sort_kernel, grid, kRevSortWarps * 32, 0, s->ro_off.p, s->ro_data.p, tlo, thi, big.p + 2,
-               wl.p + kRevLongCap);
+               wl.p + n);
         const uint32_t lgrid = uint32_t(num_sms()) * 4;
-        LAUNCH(rev_sort_long_kernel, lgrid, 32, 0, s->rn_off.p, s->rn_data.p, big.p, wl.p);
-        LAUNCH(rev_sort_long_kernel, lgrid, 32, 0, s->ro_off.p, s->ro_data.p, big.p + 2, wl.p + kRevLongCap);
+        LAUNCH(rev_sort_long_kernel, lgrid, kRevLongThreads, 0, s->rn_off.p, s->rn_data.p, big.p, wl.p);
+        LAUNCH(rev_sort_long_kernel, lgrid, kRevLongThreads, 0, s->ro_off.p, s->ro_data.p, big.p + 2, wl.p + n);
     }
     uint32_t tot[2], hb[4];
     CK(cudaMemcpyAsync(&tot[0], s->rn_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
     CK(cudaMemcpyAsync(&tot[1], s->ro_off.p + n, 4, cudaMemcpyDeviceToHost, stream()));
     big.download(hb, 4);
     ssync();
-    // a list too long for one warp (a hub with > 2048 reverse neighbours): the whole array
+    // a list too long for shared memory (a hub with > 8192 reverse neighbours): the whole array
     // goes through the library segmented sort (sorted lists stay sorted)
     if (hb[0]) segmented_sort(s->rn_data.p, tot[0], s->rn_off.p, n);
     if (hb[2]) segmented_sort(s->ro_data.p, tot[1], s->ro_off.p, n);

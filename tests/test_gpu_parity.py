@@ -537,10 +537,10 @@ def test_distance_entry_points():
 
 @pytest.mark.gpu
 def test_hub_reverse_lists_bit_exact():
-    """Two hubs (the centres of shells of 2600 and 1000 points in 64 dimensions: each is its
+    """Two hubs (the centres of shells of 9000 and 1000 points in 64 dimensions: each is its
     shell's nearest neighbour) give reverse lists of every size class of the device's list
-    sort: registers (<= 256 ids), shared memory (<= 2048) and the segmented-sort fallback
-    (the 2600-point hub), in the new and in the old lists."""
+    sort: registers (<= 256 ids), one CTA in shared memory (<= 8192) and the segmented-sort
+    fallback (the 9000-point hub), in the new and in the old lists."""
     rng = np.random.default_rng(3)
     dim = 64
 
@@ -550,7 +550,7 @@ def test_hub_reverse_lists_bit_exact():
         return c + r * u
 
     c0, c1 = np.full(dim, 100.0), np.full(dim, -100.0)
-    x = np.vstack([c0[None], c1[None], shell(c0, 10.0, 2600), shell(c1, 10.0, 1000),
+    x = np.vstack([c0[None], c1[None], shell(c0, 10.0, 9000), shell(c1, 10.0, 1000),
                    rng.normal(size=(398, dim)) * 5]).astype(np.float32)
     n = len(x)
     o, vo, so, sd = _pair(x, 4, 10, 7, 10, 2, 40, 40)
@@ -566,4 +566,4 @@ def test_hub_reverse_lists_bit_exact():
             if which >= 2:
                 longest = max(longest, max(len(a) for a in ol))
         assert_pools_equal(sd, so)
-    assert longest > 2048, "the data no longer produces a hub list beyond the shared-memory sort"
+    assert longest > 8192, "the data no longer produces a hub list beyond the shared-memory sort"
