@@ -155,14 +155,24 @@ class KnnGraph:
 
 
 def brute_force_knn(base, queries=None, k: int = 10, workers: int = 1, dist_comps: Optional[list] = None,
-                    with_dists: bool = False):
+                    with_dists: bool = False, out_ids: Optional[np.ndarray] = None,
+                    out_dists: Optional[np.ndarray] = None):
     """eval.cpp:33-61.  queries=None selects self mode.  Returns ids (nq x k) as a
-    GroundTruth array (plus dists when with_dists)."""
+    GroundTruth array (plus dists when with_dists).  out_ids / out_dists: caller-owned
+    C-contiguous (nq x k) uint32 / float32 arrays to fill (e.g. pinned memory, which the
+    device-to-host copy then reaches at full PCIe rate) instead of fresh ones."""
     b = _as_vs(base)
     q = None if queries is None else _as_vs(queries)
     nq = b.n if q is None else q.n
-    ids = np.empty((nq, k), np.uint32) if k > 0 else np.empty((nq, 0), np.uint32)
-    dists = np.empty((nq, k), np.float32) if with_dists and k > 0 else None
+    for arr, dt, nm in ((out_ids, np.uint32, "out_ids"), (out_dists, np.float32, "out_dists")):
+        if arr is not None and (arr.dtype != dt or arr.shape != (nq, k) or not arr.flags["C_CONTIGUOUS"]):
+            raise InvalidArgument(f"brute_force_knn: {nm} must be a C-contiguous ({nq}, {k}) {np.dtype(dt).name} array")
+    if out_dists is not None:
+        with_dists = True
+    ids = out_ids if out_ids is not None and k > 0 else (
+        np.empty((nq, k), np.uint32) if k > 0 else np.empty((nq, 0), np.uint32))
+    dists = out_dists if out_dists is not None else (
+        np.empty((nq, k), np.float32) if with_dists and k > 0 else None)
     comps = C.c_uint64(0)
     check(lib.annk_brute_force_knn(b.handle, q.handle if q else None, k, ids if k > 0 else np.empty(1, np.uint32),
                                    ptr(dists), C.byref(comps)))

@@ -567,3 +567,18 @@ def test_hub_reverse_lists_bit_exact():
                 longest = max(longest, max(len(a) for a in ol))
         assert_pools_equal(sd, so)
     assert longest > 8192, "the data no longer produces a hub list beyond the shared-memory sort"
+
+
+@pytest.mark.gpu
+def test_brute_force_caller_owned_outputs():
+    x = A.gen_synthetic(700, 12, 9)
+    ids, d = A.brute_force_knn(x, None, 7, with_dists=True)
+    oi, od = np.full((700, 7), 0xffffffff, np.uint32), np.zeros((700, 7), np.float32)
+    ri, rd = A.brute_force_knn(x, None, 7, out_ids=oi, out_dists=od)
+    assert ri is oi and rd is od
+    np.testing.assert_array_equal(oi, ids)
+    np.testing.assert_array_equal(od.view(np.uint32), d.view(np.uint32))
+    with pytest.raises(A.InvalidArgument):
+        A.brute_force_knn(x, None, 7, out_ids=np.zeros((700, 6), np.uint32))
+    with pytest.raises(A.InvalidArgument):
+        A.brute_force_knn(x, None, 7, out_ids=np.zeros((700, 7), np.int64))
