@@ -185,6 +185,15 @@ int annk_refine_nn_descent(annk_state* s, const annk_dataset* ds, uint32_t max_i
                            double min_change_rate, uint32_t* iters_run);
 /* graph_build.cpp:346-373 finalize: ids/dists are n*k. */
 int annk_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* ids, float* dists);
+/* The last round of a build and finalize in one call (graph_build.cpp:105-162
+ * followed by :346-373): identical pools, *changes, dist_comps and rows to
+ * annk_nn_descent_iteration + annk_finalize.  The replay runs in ascending
+ * target chunks, and each chunk's finalized rows travel to ids/dists (host
+ * or device, n*k) on a second stream while the next chunk replays.
+ * *round_dist_comps (nullable) receives dist_comps after the round, before
+ * finalize's fill-up of sparse pools (the reference logs that value). */
+int annk_nn_descent_iteration_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* ids,
+                                       float* dists, uint64_t* changes, uint64_t* round_dist_comps);
 /* graph_build.cpp:209-226 detail::pool_topk_accuracy.  rows == NULL scores all
  * n rows against gt (n x gt_k); otherwise gt row r belongs to point rows[r]. */
 int annk_pool_topk_accuracy(const annk_state* s, const uint32_t* gt_ids, uint32_t gt_rows,

@@ -102,6 +102,7 @@ _SIGS = {
     "annk_union_reverse_lists": [_vp],
     "annk_refine_nn_descent": [_vp, _vp, _u32, C.c_double, C.POINTER(_u32)],
     "annk_finalize": [_vp, _vp, _u32, _u32p, _f32p],
+    "annk_nn_descent_iteration_finalize": [_vp, _vp, _u32, _u32p, _f32p, C.POINTER(_u64), C.POINTER(_u64)],
     "annk_pool_topk_accuracy": [_vp, _u32p, _u32, _u32, _vp, C.POINTER(C.c_double)],
     "annk_state_join_rows": [_vp, C.POINTER(_u64)],
     "annk_state_stats": [_vp, _u64p],

@@ -456,6 +456,24 @@ class detail:
         return int(ch.value)
 
     @staticmethod
+    def nn_descent_iteration_finalize(state: RefineState, vs, k: int, out_ids: Optional[np.ndarray] = None,
+                                      out_dists: Optional[np.ndarray] = None):
+        """The last round of a build and finalize as one call
+        (graph_build.cpp:105-162 then :346-373): the same changes, pools and
+        graph as nn_descent_iteration + finalize, with the finalized rows
+        copied out chunk by chunk while the remaining targets are replayed.
+        Returns (changes, dist_comps after the round, KnnGraph)."""
+        n = state.meta()["n"]
+        ids = np.empty((n, k), np.uint32) if out_ids is None else out_ids
+        d = np.empty((n, k), np.float32) if out_dists is None else out_dists
+        if ids.shape != (n, k) or d.shape != (n, k) or ids.dtype != np.uint32 or d.dtype != np.float32:
+            raise InvalidArgument("finalize: output buffers must be n x k uint32 / float32")
+        ch, comps = C.c_uint64(0), C.c_uint64(0)
+        v = _as_vs(vs)
+        check(lib.annk_nn_descent_iteration_finalize(state.handle, v.handle, k, ids, d, C.byref(ch), C.byref(comps)))
+        return int(ch.value), int(comps.value), KnnGraph(ids, d)
+
+    @staticmethod
     def nn_expansion_iteration(state: RefineState, vs, workers: int = 1) -> int:
         """graph_build.cpp:164-207 (the NN-expansion baseline) on the device."""
         ch = C.c_uint64(0)
@@ -613,8 +631,18 @@ def build_graph(vs, forest: Optional[KdForest], params: BuildParams, gt: Optiona
     log_row(0)
     iters = 0 if params.strategy == "init-only" else params.max_iters
     threshold = params.min_change_rate * v.n * params.pool_cap
-    for _ in range(iters):
+    g = None
+    for it in range(iters):
         t1 = time.perf_counter()
+        if it == iters - 1 and gt is None and params.strategy != "nn-expansion":
+            # the iteration cap makes this the last round whatever `changes` says:
+            # replay and finalize overlap the device-to-host copy of the rows
+            ch, comps, g = detail.nn_descent_iteration_finalize(state, v, params.k)
+            st.refine_seconds += time.perf_counter() - t1
+            st.iterations.append(IterationLog(state.meta()["iteration"], st.init_seconds + st.refine_seconds,
+                                              comps, ch, -1.0))
+            st.early_stopped = ch < threshold
+            break
         ch = (detail.nn_expansion_iteration(state, v) if params.strategy == "nn-expansion"
               else detail.nn_descent_iteration(state, v))
         st.refine_seconds += time.perf_counter() - t1
@@ -622,7 +650,8 @@ def build_graph(vs, forest: Optional[KdForest], params: BuildParams, gt: Optiona
         if ch < threshold:
             st.early_stopped = True
             break
-    g = finalize(state, v, params.k)
+    if g is None:
+        g = finalize(state, v, params.k)
     st.dist_comps = state.meta()["dist_comps"]
     return BuildResult(g, st, state if keep_state else None)
 

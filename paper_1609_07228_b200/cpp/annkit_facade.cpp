@@ -368,9 +368,28 @@ BuildResult build_graph(const VectorSet& vs, const KdForest* forest, const Build
     log(0);
     const std::uint32_t iters = p.strategy == BuildStrategy::init_only ? 0 : p.max_iters;
     const double threshold = p.min_change_rate * double(vs.n) * double(p.pool_cap);
+    bool finalized = false;
     for (std::uint32_t it = 0; it < iters; ++it) {
         t0 = now();
         std::uint64_t ch = 0;
+        if (it + 1 == iters && !gt && p.strategy != BuildStrategy::nn_expansion) {
+            // the iteration cap makes this the last round: replay and finalize in one
+            // call, the finalized rows copied out while the remaining targets replay
+            std::uint64_t round_comps = 0;
+            KnnGraph& g = out.graph;
+            g.n = s.n();
+            g.k = p.k;
+            g.ids.resize(std::size_t(g.n) * p.k);
+            g.dists.resize(std::size_t(g.n) * p.k);
+            check(annk_nn_descent_iteration_finalize(s.device->h, dev(vs), p.k, g.ids.data(), g.dists.data(), &ch,
+                                                     &round_comps));
+            st.refine_seconds += now() - t0;
+            refresh(s);
+            st.iterations.push_back({s.iteration, st.init_seconds + st.refine_seconds, round_comps, ch, -1.0});
+            st.early_stopped = double(ch) < threshold;
+            finalized = true;
+            break;
+        }
         if (p.strategy == BuildStrategy::nn_expansion) check(annk_nn_expansion_iteration(s.device->h, dev(vs), &ch));
         else check(annk_nn_descent_iteration(s.device->h, dev(vs), &ch));
         st.refine_seconds += now() - t0;
@@ -381,7 +400,7 @@ BuildResult build_graph(const VectorSet& vs, const KdForest* forest, const Build
             break;
         }
     }
-    out.graph = finalize(s, vs, p.k);
+    if (!finalized) out.graph = finalize(s, vs, p.k);
     st.dist_comps = s.dist_comps;
     return out;
 }

@@ -1932,8 +1932,9 @@ int annk_refine_nn_descent(annk_state* s, const annk_dataset* ds, uint32_t max_i
     });
 }
 
-int annk_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* ids, float* dists) {
-    return abi([&] {
+namespace {
+void finalize_impl(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* ids, float* dists) {
+    {
         const uint32_t n = s->n;
         if (n < 2 || n - 1 < k) throw_invalid("finalize: need n-1 >= k");
         if (k > s->P) throw_invalid("finalize: k exceeds pool capacity");
@@ -1955,6 +1956,88 @@ int annk_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* i
         if (dists) CK(cudaMemcpyAsync(dists, dd.p, size_t(m) * k * 4, cudaMemcpyDefault, stream()));
         ssync();
         s->dist_comps += c;
+    }
+}
+}  // namespace
+
+int annk_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* ids, float* dists) {
+    return abi([&] {
+        if (!s) throw_invalid("finalize: null state");
+        finalize_impl(s, ds, k, ids, dists);
+    });
+}
+
+// The last round of a build and finalize as one call: once the join has run,
+// every target's replay touches only that target's pool, so the targets are
+// replayed in ascending chunks and each chunk's rows are finalized and copied
+// to the host (second stream) while the next chunk replays.  Same pools,
+// flags, `changes`, dist_comps and rows as annk_nn_descent_iteration followed
+// by annk_finalize.
+static cudaStream_t copy_stream() {
+    static cudaStream_t cs = nullptr;
+    if (!cs) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    return cs;
+}
+
+int annk_nn_descent_iteration_finalize(annk_state* s, const annk_dataset* ds, uint32_t k, uint32_t* ids,
+                                       float* dists, uint64_t* changes, uint64_t* round_dist_comps) {
+    return abi([&] {
+        if (!s || !ds || ds->n != s->n) throw_invalid("nn_descent_iteration: state/dataset mismatch");
+        const uint32_t n = s->n;
+        if (n < 2 || n - 1 < k) throw_invalid("finalize: need n-1 >= k");
+        if (k > s->P) throw_invalid("finalize: k exceeds pool capacity");
+        do_rebuild(s);
+        do_union(s);
+        bool one_launch = false;
+        if (!s->sharded && s->join_pieces <= 1) {
+            one_launch = join_phase(s, ds);
+            if (!one_launch) {  // as do_join_merge: this round goes in pieces
+                const uint64_t lim = join_offer_limit();
+                s->join_pieces = uint32_t(std::max<uint64_t>(2, (2 * s->last_offers + lim - 1) / lim));
+            }
+        }
+        if (!one_launch) {  // sharded states and rounds joined in pieces: the two steps one after the other
+            const uint64_t c = do_join_merge(s, ds);
+            if (changes) *changes = c;
+            if (round_dist_comps) *round_dist_comps = s->dist_comps;
+            finalize_impl(s, ds, k, ids, dists);
+            return;
+        }
+        const char* ce = getenv("ANNK_FUSED_CHUNKS");  // experiments
+        const uint32_t chunks = std::max(1u, std::min(ce ? uint32_t(atoi(ce)) : 8u, n / 32768u));
+        DevBuf<unsigned long long> comps(1);
+        comps.zero();
+        DevBuf<uint32_t> di(size_t(n) * k);
+        DevBuf<float> dd(size_t(n) * k);
+        std::vector<cudaEvent_t> evs(chunks);
+        uint64_t total = 0;
+        for (uint32_t c = 0; c < chunks; ++c) {
+            const uint32_t lo = uint32_t(uint64_t(n) * c / chunks), hi = uint32_t(uint64_t(n) * (c + 1) / chunks);
+            total += replay_offers(s, lo, hi);
+            const uint32_t m = hi - lo;
+            LAUNCH(fill_sparse_kernel, grid_for(size_t(m) * 32, 256), 256, 0, ds->data.p, n, ds->ld, s->P, k,
+                   s->keys.p, s->flags.p, s->sizes.p, comps.p, lo, hi);
+            LAUNCH(finalize_kernel, grid_for(size_t(m) * k, 256), 256, 0, s->keys.p + size_t(lo) * s->P, m, s->P, k,
+                   di.p + size_t(lo) * k, dd.p + size_t(lo) * k);
+            CK(cudaEventCreateWithFlags(&evs[c], cudaEventDisableTiming));
+            CK(cudaEventRecord(evs[c], stream()));
+            CK(cudaStreamWaitEvent(copy_stream(), evs[c], 0));
+            if (ids)
+                CK(cudaMemcpyAsync(ids + size_t(lo) * k, di.p + size_t(lo) * k, size_t(m) * k * 4, cudaMemcpyDefault,
+                                   copy_stream()));
+            if (dists)
+                CK(cudaMemcpyAsync(dists + size_t(lo) * k, dd.p + size_t(lo) * k, size_t(m) * k * 4,
+                                   cudaMemcpyDefault, copy_stream()));
+        }
+        finish_round(s, total);
+        if (changes) *changes = total;
+        if (round_dist_comps) *round_dist_comps = s->dist_comps;
+        unsigned long long fc = 0;
+        comps.download(&fc, 1);
+        ssync();
+        CK(cudaStreamSynchronize(copy_stream()));
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+        s->dist_comps += fc;
     });
 }
 

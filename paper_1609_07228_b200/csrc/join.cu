@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "join.cuh"
 
@@ -1075,6 +1076,25 @@ void group_spills(annk_state* s) {
     s->spill_sorted = true;
 }
 
+// Small device counters are read back through mapped pinned memory (a one-thread
+// kernel stores them over PCIe) instead of a device-to-host memcpy: a memcpy
+// would queue behind the bulk row copies that annk_nn_descent_iteration_finalize
+// keeps in flight on the device-to-host copy engine while the next chunk replays.
+__global__ void peek_kernel(const uint32_t* __restrict__ src, uint32_t words, volatile uint32_t* dst) {
+    for (uint32_t i = 0; i < words; ++i) dst[i] = src[i];
+}
+void peek_words(const void* dev, uint32_t words, void* out) {
+    static uint32_t* host = nullptr;
+    static uint32_t* host_dev = nullptr;
+    if (!host) {
+        CK(cudaHostAlloc(&host, 64, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(&host_dev, host, 0));
+    }
+    LAUNCH(peek_kernel, 1, 1, 0, static_cast<const uint32_t*>(dev), words, host_dev);
+    ssync();
+    memcpy(out, host, size_t(words) * 4);
+}
+
 uint64_t replay_offers(annk_state* s, uint32_t lo, uint32_t hi) {
     if (hi <= lo) return 0;
     group_spills(s);
@@ -1161,8 +1181,7 @@ uint64_t replay_offers(annk_state* s, uint32_t lo, uint32_t hi) {
             LAUNCH(big_sizes_kernel, gridn(size_t(items) + 1, 256), 256, 0, def[1] + n, items, sizes.p);
             ex_scan(sizes.p, off.p, items);
             uint64_t total = 0;
-            CK(cudaMemcpyAsync(&total, off.p + items, 8, cudaMemcpyDeviceToHost, stream()));
-            ssync();
+            peek_words(off.p + items, 2, &total);
             if (trace) fprintf(stderr, "[annk] replay: %u targets with runs in global scratch (%llu entries)\n", items,
                                (unsigned long long)total);
             if (s->rp_runkey.n < total) {  // grow-only scratch kept by the state
@@ -1186,14 +1205,12 @@ uint64_t replay_offers(annk_state* s, uint32_t lo, uint32_t hi) {
         const uint32_t grid = std::min<uint32_t>((items + wpb - 1) / wpb, uint32_t(num_sms()) * std::max(per_sm, 1));
         LAUNCH(replay_kernel, grid, wpb * 32, smem, a);
         if (pass == 2) break;
-        CK(cudaMemcpyAsync(&nlist, ctr.p + 1, 4, cudaMemcpyDeviceToHost, stream()));
-        ssync();
+        peek_words(ctr.p + 1, 1, &nlist);
         if (trace) fprintf(stderr, "[annk] replay pass %d: %u targets deferred (> %u source runs)\n", pass, nlist,
                            a.runmax);
     }
     unsigned long long c = 0;
-    changes.download(&c, 1);
-    ssync();
+    peek_words(changes.p, 2, &c);
     return c;
 }
 

@@ -582,3 +582,32 @@ def test_brute_force_caller_owned_outputs():
         A.brute_force_knn(x, None, 7, out_ids=np.zeros((700, 6), np.uint32))
     with pytest.raises(A.InvalidArgument):
         A.brute_force_knn(x, None, 7, out_ids=np.zeros((700, 7), np.int64))
+
+
+@pytest.mark.parametrize("n,integer,pieces", [(70000, True, False), (70000, False, False), (6000, True, True)])
+def test_last_round_fused_with_finalize_bit_exact(n, integer, pieces, monkeypatch):
+    # nn_descent_iteration_finalize (chunked replay overlapped with the row copies) must
+    # leave the oracle's changes, dist_comps, pools and graph rows -- also through its
+    # piecewise-round fallback and through build_graph's last round
+    x = mixture(n, 128, 40, 11) if integer else A.gen_synthetic(n, 24, 11)
+    o, vo, so, sd = _pair(x, 4, 10, 5, 10, 4, 30, 10)
+    if pieces:
+        monkeypatch.setenv("ANNK_JOIN_MAX_OFFERS", "20000")
+    assert A.detail.nn_descent_iteration(sd, x) == so.nn_descent_iteration(vo)
+    co = so.nn_descent_iteration(vo)
+    comps_o = so.export()["dist_comps"]  # after the round, before finalize fills sparse pools
+    ch, comps, g = A.detail.nn_descent_iteration_finalize(sd, x, 10)
+    assert ch == co and comps == comps_o
+    ids_o, d_o = so.finalize(vo, 10)
+    np.testing.assert_array_equal(g.ids, ids_o)
+    np.testing.assert_array_equal(g.dists.view(np.uint32), d_o.view(np.uint32))
+    e = assert_pools_equal(sd, so)
+    assert sd.meta()["dist_comps"] == e["dist_comps"]
+    if not pieces:
+        f = A.build_forest(x, 4, 10, 5)
+        r = A.build_graph(x, f, A.BuildParams(k=10, conquer_depth=4, pool_cap=30, sample_cap=10, max_iters=2,
+                                              seed=5))
+        np.testing.assert_array_equal(r.graph.ids, ids_o)
+        np.testing.assert_array_equal(r.graph.dists.view(np.uint32), d_o.view(np.uint32))
+        assert r.stats.iterations[-1].changes == co and r.stats.iterations[-1].dist_comps == comps
+        assert r.stats.dist_comps == e["dist_comps"]
