@@ -1364,7 +1364,7 @@ bool join_phase(annk_state* s, const annk_dataset* ds, uint32_t ilo = 0, uint32_
         }
         s->ocnt.zero();
         s->ov_count.zero();
-        join_launch(s, ds, order, n_visit, ilo, std::min(ihi, n), &jc);
+        join_launch(s, ds, order, n_visit, ilo, std::min(ihi, n), kMaxSpill, &jc);
         if (getenv("ANNK_TRACE"))
             fprintf(stderr, "[annk] join [%u,%u): offers %llu spilled %u (cap %u, spill cap %u)\n", ilo,
                     std::min(ihi, n), jc.offers, jc.spilled, s->offer_cap, s->ov_cap);
@@ -1419,13 +1419,20 @@ uint64_t merge_phase(annk_state* s) {
 // reference visits the points in ascending order, so this is its order too.
 uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
     if (s->join_pieces <= 1) {
-        if (join_phase(s, ds)) return merge_phase(s);
+        if (join_phase(s, ds)) {
+            // a spill list past half its cap: the next round (usually more offers while
+            // the graph is far from converged) starts in two pieces instead of failing
+            const bool heavy = s->spilled > kMaxSpill / 2;
+            const uint64_t c = merge_phase(s);
+            if (heavy) s->join_pieces = 2;
+            return c;
+        }
         const uint64_t lim = join_offer_limit();
         s->join_pieces = uint32_t(std::max<uint64_t>(2, (2 * s->last_offers + lim - 1) / lim));
     }
     const uint32_t lo = own_lo(s), hi = own_hi(s);
     uint32_t pieces = s->join_pieces;
-    uint64_t comps = 0, offers = 0, spilled = 0, changes = 0, max_piece = 0;
+    uint64_t comps = 0, offers = 0, spilled = 0, changes = 0, max_piece = 0, max_spill = 0;
     uint32_t pos = lo;
     while (pos < hi) {
         const uint32_t len = std::max(1u, (hi - lo + pieces - 1) / pieces);
@@ -1439,6 +1446,7 @@ uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
         offers += s->last_offers;
         spilled += s->spilled;
         max_piece = std::max<uint64_t>(max_piece, s->last_offers);
+        max_spill = std::max<uint64_t>(max_spill, s->spilled);
         changes += merge_offers(s);
         s->stage = 2;  // next piece joins against the same lists and start-of-round tails
         pos = end;
@@ -1448,7 +1456,8 @@ uint64_t do_join_merge(annk_state* s, const annk_dataset* ds) {
     s->last_spilled = spilled;
     // later rounds start from the piece count this round needed (offer volume
     // usually falls as the graph converges: back to one launch when it fits)
-    s->join_pieces = 2 * max_piece * pieces < join_offer_limit() ? 1u : pieces;
+    s->join_pieces = 2 * max_piece * pieces < join_offer_limit() && 2 * max_spill * pieces < kMaxSpill ? 1u : pieces;
+    if (max_spill > kMaxSpill / 2) s->join_pieces = std::min(pieces * 2, 1u << 20);  // see the one-launch case
     finish_round(s, changes);
     return changes;
 }

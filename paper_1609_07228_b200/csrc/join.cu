@@ -33,7 +33,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
+#include <thread>
 #include <cstring>
 
 #include "join.cuh"
@@ -983,7 +985,7 @@ void ex_scan(const T* in, T* out, uint32_t n) {
 }  // namespace
 
 void join_launch(annk_state* s, const annk_dataset* ds, const uint32_t* order, uint32_t n_visit, uint32_t ilo,
-                 uint32_t ihi, JoinCounters* out) {
+                 uint32_t ihi, uint32_t ov_abort, JoinCounters* out) {
     JArgs a{};
     a.x = ds->data.p;
     a.x8 = ds->u8 ? ds->data8.p : nullptr;
@@ -1035,6 +1037,35 @@ void join_launch(annk_state* s, const annk_dataset* ds, const uint32_t* order, u
     if (n_visit) {
         if (ds->u8) LAUNCH(join_kernel<kModeU8>, grid, 32, smem, a);
         else LAUNCH(join_kernel<kModeF32>, grid, 32, smem, a);
+    }
+    // A launch whose spill list outgrows ov_abort entries is thrown away by the caller
+    // (the range is joined again in pieces).  For ranges large enough for that to happen
+    // the host watches the spill counter from a second stream while the kernel runs and,
+    // past the limit, ends the visit list (the work counter jumps beyond n_visit) so the
+    // doomed launch stops early.  The kernel itself is untouched; smaller ranges (cfg2:
+    // 1M points) are not watched.
+    if (n_visit >= (1u << 20) && ov_abort != 0xffffffffu) {
+        static cudaStream_t ps = nullptr;
+        static cudaEvent_t done = nullptr;
+        static uint32_t* hp = nullptr;
+        if (!ps) {
+            CK(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+            CK(cudaHostAlloc(&hp, 8, cudaHostAllocDefault));
+        }
+        CK(cudaEventRecord(done, stream()));
+        while (cudaEventQuery(done) == cudaErrorNotReady) {
+            CK(cudaMemcpyAsync(hp, s->ov_count.p, 4, cudaMemcpyDeviceToHost, ps));
+            CK(cudaStreamSynchronize(ps));
+            if (hp[0] > ov_abort) {
+                hp[1] = 0x7fffffffu;
+                CK(cudaMemcpyAsync(next.p, hp + 1, 4, cudaMemcpyHostToDevice, ps));
+                CK(cudaStreamSynchronize(ps));
+                break;
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(200));
+        }
+        cudaGetLastError();  // cudaErrorNotReady from the query is not an error
     }
     unsigned long long c[2] = {0, 0};
     CK(cudaMemcpyAsync(c, counters.p, 16, cudaMemcpyDeviceToHost, stream()));

@@ -15,7 +15,7 @@ struct JoinCounters {
     uint32_t spilled = 0;
 };
 void join_launch(annk_state* s, const annk_dataset* ds, const uint32_t* order, uint32_t n_visit, uint32_t ilo,
-                 uint32_t ihi, JoinCounters* out);
+                 uint32_t ihi, uint32_t ov_abort, JoinCounters* out);
 
 // Groups the spill list by target (stable) so every target's offers are
 // slots[0, min(cnt, cap)) followed by its spill segment.
